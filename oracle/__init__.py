@@ -1,0 +1,1 @@
+"""CPU parity oracle (test infrastructure only; see oracle.py)."""
