@@ -1,0 +1,134 @@
+// common.cuh -- shared device helpers for the sm_100a FastPoint kernels.
+//
+// Numerics contract: every squared distance that decides an
+// index is computed in float64 as ((dx*dx + dy*dy) + dz*dz) with explicitly
+// rounded intrinsics, so nvcc can never contract it into DFMA -- the exact
+// operation sequence of the reference numba kernels
+// (/root/reference/pkg/src/pointsample/_kernels.py:55-58, 149-152).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define PS_DEV __device__ __forceinline__
+
+namespace ps {
+
+constexpr uint32_t kFull = 0xffffffffu;
+
+// f64 squared distance, no contraction (DADD/DMUL only).
+PS_DEV double sqdist(double ax, double ay, double az, double bx, double by, double bz) {
+    const double dx = __dsub_rn(bx, ax);
+    const double dy = __dsub_rn(by, ay);
+    const double dz = __dsub_rn(bz, az);
+    double s = __dmul_rn(dx, dx);
+    s = __dadd_rn(s, __dmul_rn(dy, dy));
+    s = __dadd_rn(s, __dmul_rn(dz, dz));
+    return s;
+}
+
+PS_DEV double sqdist4(float4 a, float4 b) {
+    return sqdist((double)a.x, (double)a.y, (double)a.z, (double)b.x, (double)b.y, (double)b.z);
+}
+
+// Conservative float32 pre-filter for "d2 < r2": the f32
+// evaluation of three rounded squared differences has relative error below
+// 6 * 2^-24 when nothing underflows, and absolute error below 2^-125 when
+// something does.  thr = f32(r2) * (1 + 2^-16) + 2^-120 therefore never
+// rejects a pair whose exact float64 d2 is below r2; every accepted pair is
+// re-checked exactly in float64.  Returns +inf-ish thresholds unchanged.
+PS_DEV float prefilter_threshold(double r2) {
+    float t = __double2float_ru(r2);
+    t = __fmul_ru(t, 1.0f + 1.52587890625e-05f);  // 1 + 2^-16
+    return __fadd_ru(t, 7.52316384526264e-37f);   // + 2^-120
+}
+
+PS_DEV float sqdist_f32(float4 a, float4 b) {
+    const float dx = b.x - a.x, dy = b.y - a.y, dz = b.z - a.z;
+    return __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+}
+
+// ---- warp argmax over (float64 key >= 0, lowest index on ties) -----------
+// key = raw bits of a non-negative double (monotone as u64).
+struct ArgMax {
+    uint64_t key;
+    uint32_t idx;
+};
+
+PS_DEV ArgMax warp_argmax(uint64_t key, uint32_t idx) {
+    const uint32_t hi = (uint32_t)(key >> 32), lo = (uint32_t)key;
+    const uint32_t mhi = __reduce_max_sync(kFull, hi);
+    const uint32_t mlo = __reduce_max_sync(kFull, hi == mhi ? lo : 0u);
+    const bool win = (hi == mhi) && (lo == mlo);
+    const uint32_t midx = __reduce_min_sync(kFull, win ? idx : 0xffffffffu);
+    ArgMax r;
+    r.key = ((uint64_t)mhi << 32) | mlo;
+    r.idx = midx;
+    return r;
+}
+
+// ---- cluster / DSMEM / mbarrier PTX wrappers (sm_90+) -------------------
+
+PS_DEV uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+PS_DEV uint32_t cluster_nctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
+PS_DEV uint32_t cluster_id_x() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+    return r;
+}
+PS_DEV void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n"
+                 "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+PS_DEV uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+// map a local shared::cta address to the same variable in CTA `rank`
+PS_DEV uint32_t mapa(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+PS_DEV void st_cluster_u64(uint32_t addr, uint64_t v) {
+    asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
+}
+PS_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+PS_DEV void fence_mbar_init_cluster() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+PS_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;"
+                 ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// wait for phase `parity` of a local mbarrier; acquire at cluster scope so
+// st.async data from peer CTAs is visible afterwards.
+PS_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(a), "r"(parity) : "memory");
+}
+// 16-byte asynchronous store into a peer CTA's shared memory that signals
+// the peer's mbarrier with complete_tx(16).
+PS_DEV void st_async_v4(uint32_t remote_addr, uint32_t remote_bar, uint32_t a, uint32_t b,
+                        uint32_t c, uint32_t d) {
+    asm volatile(
+        "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%2, %3, %4, %5}, [%1];"
+        ::"r"(remote_addr), "r"(remote_bar), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
+}  // namespace ps

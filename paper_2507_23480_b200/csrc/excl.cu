@@ -1,0 +1,427 @@
+// excl.cu -- K3a/K3b: fused exclusion-list construction (B200 / sm_100a).
+//
+// Replaces excl_collect + csr_fill + csr_sort_rows + csr_level_counts
+// (/root/reference/pkg/src/pointsample/_kernels.py:111-234).
+//
+//   excl_pairs     tiled i<j triangle over 128x128 point tiles staged in
+//                  shared memory; a conservative float32 pre-filter rejects
+//                  almost every pair and survivors are decided exactly in
+//                  float64 (no FMA).  Each unordered pair is evaluated once.
+//                  Hits are staged in shared memory and flushed to a per-cloud
+//                  edge list with one global atomic per flush.
+//   excl_degree    per-row degrees from the edge list.
+//   excl_scan      per-cloud exclusive scan -> indptr (self included).
+//   excl_fill      scatter self + both directions of every edge.
+//   excl_sort      rows ordered by (d2, index): warp bitonic in shared memory
+//                  for rows <= 256, CTA bitonic for longer rows; the strict
+//                  "d2 < r2" level counts are fused into the epilogue.
+//
+// Row order after the sort is a total order, so the scatter order of the
+// fill pass (atomics) never leaks into the output: the CSR is
+// byte-identical to the reference's for any schedule.
+
+#include <cfloat>
+
+#include "common.cuh"
+#include "ps_internal.h"
+
+namespace ps {
+
+namespace {
+
+constexpr int kTile = 128;
+constexpr int kPairThreads = 256;
+constexpr int kStageCap = 2048;
+
+__device__ __forceinline__ void tile_pair_from_linear(int64_t t, int64_t nt, int64_t* I, int64_t* J) {
+    // enumerate (I, J) with I <= J row by row: row I has nt - I entries
+    // solve for I via the closed form, then fix rounding
+    double a = (double)(2 * nt + 1);
+    int64_t i = (int64_t)floor((a - sqrt(a * a - 8.0 * (double)t)) * 0.5);
+    if (i < 0) i = 0;
+    auto start = [&](int64_t r) { return r * nt - r * (r - 1) / 2; };
+    while (i > 0 && start(i) > t) --i;
+    while (i + 1 < nt && start(i + 1) <= t) ++i;
+    *I = i;
+    *J = i + (t - start(i));
+}
+
+__global__ void __launch_bounds__(kPairThreads) excl_pairs_kernel(
+    const float4* __restrict__ xyz, int64_t N, const double* __restrict__ r2_levels, int L,
+    int64_t levels_ld, ExclWork w) {
+    __shared__ float4 ti[kTile];
+    __shared__ float4 tj[kTile];
+    __shared__ uint32_t s_i[kStageCap];
+    __shared__ uint32_t s_j[kStageCap];
+    __shared__ double s_d[kStageCap];
+    __shared__ int s_n;
+    __shared__ unsigned long long s_base;
+
+    const int64_t b = blockIdx.y;
+    const int64_t nt = (N + kTile - 1) / kTile;
+    int64_t I, J;
+    tile_pair_from_linear(blockIdx.x, nt, &I, &J);
+    const float4* cx = xyz + b * N;
+    const int tid = threadIdx.x;
+
+    double r2 = 0.0;
+    for (int l = 0; l < L; ++l) r2 = fmax(r2, r2_levels[b * levels_ld + l]);
+    const float thr = prefilter_threshold(r2);
+    const bool no_filter = !(thr <= FLT_MAX);
+
+    if (tid < kTile) {
+        const int64_t i = I * kTile + tid;
+        ti[tid] = i < N ? cx[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+        const int64_t j = J * kTile + (tid - kTile);
+        tj[tid - kTile] = j < N ? cx[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (tid == 0) s_n = 0;
+    __syncthreads();
+
+    const int li = tid & (kTile - 1);
+    const int half = tid >> 7;
+    const int64_t gi = I * kTile + li;
+    const float4 pi = ti[li];
+    const int64_t jlo = J * kTile + half * (kTile / 2);
+    const int jbeg = half * (kTile / 2);
+    unsigned long long* ecount = w.edge_count + b;
+    if (gi < N) {
+#pragma unroll 8
+        for (int t = 0; t < kTile / 2; ++t) {
+            const int64_t gj = jlo + t;
+            const float4 pj = tj[jbeg + t];
+            const float df = sqdist_f32(pi, pj);
+            if ((df < thr || no_filter) && gj < N && gj > gi) {
+                const double d = sqdist4(pi, pj);
+                if (d < r2) {
+                    const int slot = atomicAdd(&s_n, 1);
+                    if (slot < kStageCap) {
+                        s_i[slot] = (uint32_t)gi;
+                        s_j[slot] = (uint32_t)gj;
+                        s_d[slot] = d;
+                    } else {  // dense pathological tile: direct global append
+                        const unsigned long long p = atomicAdd(ecount, 1ull);
+                        if (p < (unsigned long long)w.cap_edges) {
+                            w.edge_i[b * w.cap_edges + p] = (uint32_t)gi;
+                            w.edge_j[b * w.cap_edges + p] = (uint32_t)gj;
+                            w.edge_d2[b * w.cap_edges + p] = d;
+                        } else {
+                            atomicOr(&w.status[b], 1);
+                        }
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    const int n = min(s_n, kStageCap);
+    if (n == 0) return;
+    if (tid == 0) s_base = atomicAdd(ecount, (unsigned long long)n);
+    __syncthreads();
+    const unsigned long long base = s_base;
+    for (int k = tid; k < n; k += kPairThreads) {
+        const unsigned long long p = base + k;
+        if (p < (unsigned long long)w.cap_edges) {
+            w.edge_i[b * w.cap_edges + p] = s_i[k];
+            w.edge_j[b * w.cap_edges + p] = s_j[k];
+            w.edge_d2[b * w.cap_edges + p] = s_d[k];
+        } else {
+            atomicOr(&w.status[b], 1);
+        }
+    }
+}
+
+__global__ void excl_degree_kernel(int64_t N, ExclWork w) {
+    const int64_t b = blockIdx.y;
+    const int64_t m = min((int64_t)w.edge_count[b], w.cap_edges);
+    int32_t* deg = w.deg + b * N;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        atomicAdd(&deg[w.edge_i[b * w.cap_edges + e]], 1);
+        atomicAdd(&deg[w.edge_j[b * w.cap_edges + e]], 1);
+    }
+}
+
+// One CTA per cloud: indptr = exclusive scan of (deg + 1); deg <- indptr (cursor).
+__global__ void __launch_bounds__(1024) excl_scan_kernel(int64_t N, ExclWork w, CsrView csr) {
+    __shared__ int64_t warp_sums[32];
+    __shared__ int64_t carry;
+    const int64_t b = blockIdx.x;
+    int32_t* deg = w.deg + b * N;
+    int64_t* indptr = csr.indptr + b * (N + 1);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) carry = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < N; base += 1024) {
+        const int64_t i = base + tid;
+        const int64_t v = i < N ? (int64_t)deg[i] + 1 : 0;
+        int64_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t y = __shfl_up_sync(kFull, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) warp_sums[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            int64_t s = warp_sums[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int64_t y = __shfl_up_sync(kFull, s, o);
+                if (lane >= o) s += y;
+            }
+            warp_sums[lane] = s;
+        }
+        __syncthreads();
+        const int64_t excl = carry + (warp ? warp_sums[warp - 1] : 0) + x - v;
+        if (i < N) {
+            indptr[i] = excl;
+            deg[i] = (int32_t)excl;  // cursor (cap_entries < 2^31 enforced by host)
+        }
+        __syncthreads();
+        if (tid == 0) carry += warp_sums[31];
+        __syncthreads();
+    }
+    if (tid == 0) {
+        indptr[N] = carry;
+        if (carry > csr.cap_entries) atomicOr(&w.status[b], 2);
+    }
+}
+
+__global__ void excl_fill_kernel(int64_t N, ExclWork w, CsrView csr) {
+    const int64_t b = blockIdx.y;
+    const int64_t m = min((int64_t)w.edge_count[b], w.cap_edges);
+    int32_t* cur = w.deg + b * N;
+    int32_t* nbr = csr.nbr + b * csr.cap_entries;
+    double* d2 = csr.d2 + b * csr.cap_entries;
+    const int64_t cap = csr.cap_entries;
+    const int64_t total = m + N;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        if (e < N) {
+            const int32_t p = atomicAdd(&cur[e], 1);
+            if (p < cap) { nbr[p] = (int32_t)e; d2[p] = 0.0; }
+        } else {
+            const int64_t k = b * w.cap_edges + (e - N);
+            const uint32_t i = w.edge_i[k], j = w.edge_j[k];
+            const double d = w.edge_d2[k];
+            const int32_t p = atomicAdd(&cur[i], 1);
+            if (p < cap) { nbr[p] = (int32_t)j; d2[p] = d; }
+            const int32_t q = atomicAdd(&cur[j], 1);
+            if (q < cap) { nbr[q] = (int32_t)i; d2[q] = d; }
+        }
+    }
+}
+
+// ---- row sort by (d2, index) + fused level counts -----------------------
+
+__device__ __forceinline__ bool key_less(double da, int32_t ia, double db, int32_t ib) {
+    return da < db || (da == db && ia < ib);
+}
+
+// Bitonic sort of n2 (power of two) entries in shared memory by `nthr`
+// cooperating threads (thread rank t), synchronised with `sync`.
+template <typename Sync>
+__device__ __forceinline__ void bitonic_smem(double* kd, int32_t* ki, int n2, int t, int nthr, Sync sync) {
+    for (int k = 2; k <= n2; k <<= 1) {
+        for (int jj = k >> 1; jj > 0; jj >>= 1) {
+            for (int x = t; x < n2 / 2; x += nthr) {
+                // x-th compare pair of this stage
+                const int lo = (x / jj) * (2 * jj) + (x % jj);
+                const int hi = lo + jj;
+                const bool up = ((lo & k) == 0);
+                const double a = kd[lo], c = kd[hi];
+                const int32_t ia = ki[lo], ic = ki[hi];
+                const bool sw = up ? key_less(c, ic, a, ia) : key_less(a, ia, c, ic);
+                if (sw) { kd[lo] = c; kd[hi] = a; ki[lo] = ic; ki[hi] = ia; }
+            }
+            sync();
+        }
+    }
+}
+
+constexpr int kSortWarps = 8;
+constexpr int kWarpRowCap = 256;
+constexpr int kCtaRowCap = 8192;
+
+__global__ void __launch_bounds__(kSortWarps * 32) excl_sort_small_kernel(CsrView csr, int64_t B,
+                                                                       const double* __restrict__ r2_levels,
+                                                                       int64_t levels_ld, ExclWork w) {
+    __shared__ double sd[kSortWarps][kWarpRowCap];
+    __shared__ int32_t si[kSortWarps][kWarpRowCap];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t N = csr.N;
+    const int64_t rows = B * N;
+    for (int64_t gr = (int64_t)blockIdx.x * kSortWarps + warp; gr < rows;
+         gr += (int64_t)gridDim.x * kSortWarps) {
+        const int64_t b = gr / N, r = gr - b * N;
+        const int64_t lo = csr.indptr[b * (N + 1) + r];
+        const int64_t hi = csr.indptr[b * (N + 1) + r + 1];
+        if (hi > csr.cap_entries) continue;  // overflowed cloud: status already set
+        const int m = (int)(hi - lo);
+        if (m > kWarpRowCap) {
+            if (lane == 0) {
+                const unsigned k = atomicAdd(w.long_count, 1u);
+                w.long_rows[k] = (int32_t)gr;
+            }
+            continue;
+        }
+        int32_t* nbr = csr.nbr + b * csr.cap_entries + lo;
+        double* d2 = csr.d2 + b * csr.cap_entries + lo;
+        int n2 = 1;
+        while (n2 < m) n2 <<= 1;
+        for (int k = lane; k < n2; k += 32) {
+            sd[warp][k] = k < m ? d2[k] : __longlong_as_double(0x7ff0000000000000LL);
+            si[warp][k] = k < m ? nbr[k] : 0x7fffffff;
+        }
+        __syncwarp();
+        if (m > 1) bitonic_smem(sd[warp], si[warp], n2, lane, 32, [] { __syncwarp(); });
+        for (int k = lane; k < m; k += 32) {
+            d2[k] = sd[warp][k];
+            nbr[k] = si[warp][k];
+        }
+        // fused level counts: #entries with d2 < r2_l (strict, _kernels.py:233)
+        for (int l = 0; l < csr.L; ++l) {
+            const double t = r2_levels[b * levels_ld + l];
+            int c = 0;
+            for (int k = lane; k < m; k += 32) c += sd[warp][k] < t ? 1 : 0;
+            c = __reduce_add_sync(kFull, c);
+            if (lane == 0) csr.counts[(b * csr.L + l) * N + r] = c;
+        }
+        __syncwarp();
+    }
+}
+
+__global__ void __launch_bounds__(1024) excl_sort_large_kernel(CsrView csr, const double* __restrict__ r2_levels,
+                                                           int64_t levels_ld, ExclWork w) {
+    extern __shared__ __align__(16) unsigned char dyn[];
+    double* sd = reinterpret_cast<double*>(dyn);
+    int32_t* si = reinterpret_cast<int32_t*>(dyn + sizeof(double) * kCtaRowCap);
+    __shared__ int red[32];
+    const int64_t N = csr.N;
+    const unsigned nlong = *w.long_count;
+    for (unsigned t = blockIdx.x; t < nlong; t += gridDim.x) {
+        const int64_t gr = w.long_rows[t];
+        const int64_t b = gr / N, r = gr - b * N;
+        const int64_t lo = csr.indptr[b * (N + 1) + r];
+        const int64_t hi = csr.indptr[b * (N + 1) + r + 1];
+        const int64_t m = hi - lo;
+        int32_t* nbr = csr.nbr + b * csr.cap_entries + lo;
+        double* d2 = csr.d2 + b * csr.cap_entries + lo;
+        double* kd;
+        int32_t* ki;
+        int n2 = 1;
+        while (n2 < m) n2 <<= 1;
+        const bool in_smem = n2 <= kCtaRowCap;
+        if (in_smem) {
+            kd = sd; ki = si;
+            for (int k = threadIdx.x; k < n2; k += blockDim.x) {
+                kd[k] = k < m ? d2[k] : __longlong_as_double(0x7ff0000000000000LL);
+                ki[k] = k < m ? nbr[k] : 0x7fffffff;
+            }
+            __syncthreads();
+            bitonic_smem(kd, ki, n2, threadIdx.x, blockDim.x, [] { __syncthreads(); });
+            for (int k = threadIdx.x; k < m; k += blockDim.x) { d2[k] = kd[k]; nbr[k] = ki[k]; }
+            __syncthreads();
+        } else {
+            // giant row (radius near the cloud diameter): odd-even transposition
+            // in global memory -- correct, slow, only for degenerate inputs.
+            for (int64_t phase = 0; phase < m; ++phase) {
+                for (int64_t k = 2 * threadIdx.x + (phase & 1); k + 1 < m; k += 2 * blockDim.x) {
+                    const double a = d2[k], c = d2[k + 1];
+                    const int32_t ia = nbr[k], ic = nbr[k + 1];
+                    if (key_less(c, ic, a, ia)) { d2[k] = c; d2[k + 1] = a; nbr[k] = ic; nbr[k + 1] = ia; }
+                }
+                __syncthreads();
+            }
+        }
+        for (int l = 0; l < csr.L; ++l) {
+            const double th = r2_levels[b * levels_ld + l];
+            int c = 0;
+            for (int64_t k = threadIdx.x; k < m; k += blockDim.x) c += d2[k] < th ? 1 : 0;
+            c = __reduce_add_sync(kFull, c);
+            if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int s = 0;
+                for (int q = 0; q < (int)(blockDim.x >> 5); ++q) s += red[q];
+                csr.counts[(b * csr.L + l) * N + r] = s;
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// level counts for an already-sorted CSR (drop-in csr_level_counts)
+__global__ void level_counts_kernel(CsrView csr, int64_t B, const double* __restrict__ r2_levels,
+                                    int64_t levels_ld) {
+    const int64_t N = csr.N;
+    for (int64_t gr = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gr < B * N;
+         gr += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = gr / N, r = gr - b * N;
+        const int64_t lo = csr.indptr[b * (N + 1) + r];
+        const int64_t hi = csr.indptr[b * (N + 1) + r + 1];
+        const double* d2 = csr.d2 + b * csr.cap_entries;
+        for (int l = 0; l < csr.L; ++l) {
+            const double t = r2_levels[b * levels_ld + l];
+            int64_t x = lo, y = hi;
+            while (x < y) {
+                const int64_t mid = x + ((y - x) >> 1);
+                if (d2[mid] < t) x = mid + 1; else y = mid;
+            }
+            csr.counts[(b * csr.L + l) * N + r] = (int32_t)(x - lo);
+        }
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_excl_build(const float4* xyz, int64_t B, int64_t N, const double* r2_levels, int L,
+                              int64_t levels_ld, CsrView csr, ExclWork w, cudaStream_t s) {
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(w.edge_count, 0, sizeof(unsigned long long) * B, s)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(w.deg, 0, sizeof(int32_t) * B * N, s)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(w.long_count, 0, sizeof(unsigned), s)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(w.status, 0, sizeof(int32_t) * B, s)) != cudaSuccess) return e;
+    const int64_t nt = (N + kTile - 1) / kTile;
+    const int64_t npairs = nt * (nt + 1) / 2;
+    excl_pairs_kernel<<<dim3((unsigned)npairs, (unsigned)B), kPairThreads, 0, s>>>(xyz, N, r2_levels, L,
+                                                                                 levels_ld, w);
+    const unsigned g = (unsigned)std::min<int64_t>(148 * 8, (w.cap_edges + 255) / 256 + 1);
+    excl_degree_kernel<<<dim3(g, (unsigned)B), 256, 0, s>>>(N, w);
+    excl_scan_kernel<<<(unsigned)B, 1024, 0, s>>>(N, w, csr);
+    const unsigned g2 = (unsigned)std::min<int64_t>(148 * 8, (w.cap_edges + N + 255) / 256 + 1);
+    excl_fill_kernel<<<dim3(g2, (unsigned)B), 256, 0, s>>>(N, w, csr);
+    excl_sort_small_kernel<<<148 * 8, kSortWarps * 32, 0, s>>>(csr, B, r2_levels, levels_ld, w);
+    const size_t dsm = (sizeof(double) + sizeof(int32_t)) * kCtaRowCap;
+    static bool attr_set = false;
+    if (!attr_set) {
+        e = cudaFuncSetAttribute(excl_sort_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    excl_sort_large_kernel<<<148, 1024, dsm, s>>>(csr, r2_levels, levels_ld, w);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sort_rows(CsrView csr, int64_t B, ExclWork w, cudaStream_t s) {
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(w.long_count, 0, sizeof(unsigned), s)) != cudaSuccess) return e;
+    csr.L = 0;
+    excl_sort_small_kernel<<<148 * 8, kSortWarps * 32, 0, s>>>(csr, B, nullptr, 0, w);
+    const size_t dsm = (sizeof(double) + sizeof(int32_t)) * kCtaRowCap;
+    e = cudaFuncSetAttribute(excl_sort_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+    if (e != cudaSuccess) return e;
+    excl_sort_large_kernel<<<148, 1024, dsm, s>>>(csr, nullptr, 0, w);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_level_counts(CsrView csr, int64_t B, const double* r2_levels, int64_t levels_ld,
+                                cudaStream_t s) {
+    const unsigned g = (unsigned)std::min<int64_t>(148 * 8, (B * csr.N + 255) / 256 + 1);
+    level_counts_kernel<<<g, 256, 0, s>>>(csr, B, r2_levels, levels_ld);
+    return cudaGetLastError();
+}
+
+}  // namespace ps

@@ -1,0 +1,305 @@
+// group.cu -- K4 grouping (ball query / kNN, naive and redundancy-free) and
+// K6 minimum sample spacing.
+//
+// Semantics follow SPEC.md:483-521 / 563-571 as pinned in oracle/oracle.py:
+// strict "d2 < r2" radius test, neighbours ordered by (d2, index), nearest
+// first cap at k, distances reported as IEEE sqrt(d2) in float64, padding
+// index -1 / distance NaN.
+//
+//   K4a bq_rf      reads the first min(count_R[c], k) entries of the
+//                  centroid's distance-sorted exclusion row -- zero new
+//                  distance evaluations.
+//   K4b knn_rf     level-1 row entries of the query that are sampled, in row
+//                  order; exact brute-force fallback when fewer than k
+//                  (SPEC.md:513-521).
+//   K4c bq_naive   warp per centroid streams the cloud (L2-resident float4),
+//                  float32 pre-filter + exact float64 test, warp-parallel
+//                  sorted insertion into a per-warp top-k list.
+//   K4d knn_naive  thread per query, pool tiles in shared memory, top-k kept
+//                  in registers.
+//   K6 spacing     thread per sample, nearest other sample (float64).
+
+#include <cfloat>
+
+#include "common.cuh"
+#include "group.h"
+
+namespace ps {
+
+namespace {
+
+PS_DEV bool kless(double da, int32_t ia, double db, int32_t ib) {
+    return da < db || (da == db && ia < ib);
+}
+
+PS_DEV double nan_d() { return __longlong_as_double(0x7ff8000000000000LL); }
+
+// ---- K4a -----------------------------------------------------------------
+__global__ void bq_rf_kernel(BqArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t g = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); g < a.B * a.n;
+         g += nw) {
+        const int64_t b = g / a.n, t = g - b * a.n;
+        const int64_t c = a.centroids[b * a.cent_ld + t];
+        const int32_t cnt = a.counts[(b * a.L + a.level) * a.N + c];
+        const int m = cnt < a.k ? cnt : a.k;
+        const int64_t base = b * a.cap_entries + a.indptr[b * (a.N + 1) + c];
+        int32_t* oi = a.idx_out + g * a.k;
+        double* od = a.dist_out + g * a.k;
+        for (int s = lane; s < a.k; s += 32) {
+            if (s < m) {
+                oi[s] = a.nbr[base + s];
+                od[s] = sqrt(a.d2[base + s]);
+            } else {
+                oi[s] = -1;
+                od[s] = nan_d();
+            }
+        }
+        if (lane == 0) a.cnt_out[g] = m;
+    }
+}
+
+// ---- K4c -----------------------------------------------------------------
+constexpr int kBqWarps = 8;
+constexpr int kBqMaxK = 128;
+
+__global__ void __launch_bounds__(kBqWarps * 32) bq_naive_kernel(BqArgs a) {
+    __shared__ double ld[kBqWarps][kBqMaxK];
+    __shared__ int32_t li[kBqWarps][kBqMaxK];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t nw = (int64_t)gridDim.x * kBqWarps;
+    const float thr = prefilter_threshold(a.r2);
+    const bool no_filter = !(thr <= FLT_MAX);
+    const int K = a.k;
+    for (int64_t g = blockIdx.x * (int64_t)kBqWarps + warp; g < a.B * a.n; g += nw) {
+        const int64_t b = g / a.n, t = g - b * a.n;
+        const float4* xyz = a.xyz + b * a.N;
+        const int64_t c = a.centroids[b * a.cent_ld + t];
+        const float4 pc = xyz[c];
+        int len = 0;
+        for (int64_t j0 = 0; j0 < a.N; j0 += 32) {
+            const int64_t j = j0 + lane;
+            bool hit = false;
+            double d = 0.0;
+            if (j < a.N) {
+                const float4 pj = xyz[j];
+                if (no_filter || sqdist_f32(pc, pj) < thr) {
+                    d = sqdist4(pc, pj);
+                    hit = d < a.r2;
+                }
+            }
+            uint32_t hits = __ballot_sync(kFull, hit);
+            while (hits) {
+                const int src = __ffs(hits) - 1;
+                hits &= hits - 1;
+                const double dn = __shfl_sync(kFull, d, src);
+                const int32_t jn = (int32_t)(j0 + src);
+                // position = #entries with (d2, idx) < new; existing indices are smaller
+                int below = 0;
+                for (int s = lane; s < len; s += 32) below += (ld[warp][s] <= dn) ? 1 : 0;
+                const int pos = __reduce_add_sync(kFull, below);
+                if (pos >= K) continue;
+                const int newlen = len < K ? len + 1 : K;
+                // shift [pos, newlen-1) up by one
+                double carry_d[kBqMaxK / 32];
+                int32_t carry_i[kBqMaxK / 32];
+#pragma unroll
+                for (int v = 0; v < kBqMaxK / 32; ++v) {
+                    const int s = lane + 32 * v;
+                    if (s > pos && s < newlen) { carry_d[v] = ld[warp][s - 1]; carry_i[v] = li[warp][s - 1]; }
+                }
+                __syncwarp();
+#pragma unroll
+                for (int v = 0; v < kBqMaxK / 32; ++v) {
+                    const int s = lane + 32 * v;
+                    if (s > pos && s < newlen) { ld[warp][s] = carry_d[v]; li[warp][s] = carry_i[v]; }
+                }
+                if (lane == 0) { ld[warp][pos] = dn; li[warp][pos] = jn; }
+                __syncwarp();
+                len = newlen;
+            }
+        }
+        int32_t* oi = a.idx_out + g * K;
+        double* od = a.dist_out + g * K;
+        for (int s = lane; s < K; s += 32) {
+            if (s < len) { oi[s] = li[warp][s]; od[s] = sqrt(ld[warp][s]); }
+            else { oi[s] = -1; od[s] = nan_d(); }
+        }
+        if (lane == 0) a.cnt_out[g] = len;
+        __syncwarp();
+    }
+}
+
+// ---- K4d / K4b fallback: top-k in registers ---------------------------------
+constexpr int kKnnMaxK = 16;
+
+struct TopK {
+    double d[kKnnMaxK];
+    int32_t i[kKnnMaxK];
+};
+
+PS_DEV void topk_init(TopK& tk) {
+#pragma unroll
+    for (int s = 0; s < kKnnMaxK; ++s) { tk.d[s] = __longlong_as_double(0x7ff0000000000000LL); tk.i[s] = 0x7fffffff; }
+}
+
+PS_DEV void topk_insert(TopK& tk, int k, double d, int32_t j) {
+    if (!kless(d, j, tk.d[k - 1], tk.i[k - 1])) return;
+#pragma unroll
+    for (int s = kKnnMaxK - 1; s > 0; --s) {
+        if (s < k) {
+            const bool shift = kless(d, j, tk.d[s - 1], tk.i[s - 1]);
+            const bool here = !shift && kless(d, j, tk.d[s], tk.i[s]);
+            if (shift) { tk.d[s] = tk.d[s - 1]; tk.i[s] = tk.i[s - 1]; }
+            else if (here) { tk.d[s] = d; tk.i[s] = j; }
+        }
+    }
+    if (kless(d, j, tk.d[0], tk.i[0])) { tk.d[0] = d; tk.i[0] = j; }
+}
+
+constexpr int kKnnThreads = 256;
+constexpr int kKnnTile = 1024;
+
+__global__ void __launch_bounds__(kKnnThreads) knn_naive_kernel(KnnArgs a) {
+    __shared__ float4 tp[kKnnTile];
+    __shared__ int32_t ti[kKnnTile];
+    const int64_t b = blockIdx.y;
+    const float4* xyz = a.xyz + b * a.N;
+    const int64_t q = blockIdx.x * (int64_t)kKnnThreads + threadIdx.x;
+    const bool active = q < a.nq;
+    const int64_t qp = active ? (a.queries ? a.queries[b * a.q_ld + q] : q) : 0;
+    const float4 pq = xyz[qp];
+    TopK tk;
+    topk_init(tk);
+    const int k = a.k;
+    for (int64_t p0 = 0; p0 < a.npool; p0 += kKnnTile) {
+        __syncthreads();
+        for (int s = threadIdx.x; s < kKnnTile; s += kKnnThreads) {
+            const int64_t p = p0 + s;
+            if (p < a.npool) {
+                const int64_t j = a.pool[b * a.pool_ld + p];
+                ti[s] = (int32_t)j;
+                tp[s] = xyz[j];
+            }
+        }
+        __syncthreads();
+        const int m = (int)((a.npool - p0) < kKnnTile ? (a.npool - p0) : kKnnTile);
+        if (active)
+            for (int s = 0; s < m; ++s) topk_insert(tk, k, sqdist4(pq, tp[s]), ti[s]);
+    }
+    if (!active) return;
+    const int64_t g = b * a.nq + q;
+    const int take = (int)(a.npool < k ? a.npool : k);
+#pragma unroll
+    for (int s = 0; s < kKnnMaxK; ++s) {
+        if (s < k) {
+            a.idx_out[g * k + s] = s < take ? tk.i[s] : -1;
+            a.dist_out[g * k + s] = s < take ? sqrt(tk.d[s]) : nan_d();
+        }
+    }
+    a.cnt_out[g] = take;
+}
+
+__global__ void __launch_bounds__(kKnnThreads) knn_rf_kernel(KnnArgs a) {
+    const int64_t b = blockIdx.y;
+    const int64_t q = blockIdx.x * (int64_t)kKnnThreads + threadIdx.x;
+    if (q >= a.nq) return;
+    const int64_t qp = a.queries ? a.queries[b * a.q_ld + q] : q;
+    const int64_t base = b * a.cap_entries + a.indptr[b * (a.N + 1) + qp];
+    const int32_t c = a.lvl1_counts[b * a.counts_stride + qp];
+    const uint8_t* smp = a.sampled + b * a.N;
+    const int k = a.k;
+    const int64_t g = b * a.nq + q;
+    int found = 0;
+    for (int32_t u = 0; u < c && found < k; ++u) {
+        const int32_t j = a.nbr[base + u];
+        if (smp[j]) {
+            a.idx_out[g * k + found] = j;
+            a.dist_out[g * k + found] = sqrt(a.d2[base + u]);
+            ++found;
+        }
+    }
+    if (found >= k) { a.cnt_out[g] = k; return; }
+    // fallback: exact brute force over the whole pool
+    atomicAdd(a.fallback_count + b, 1);
+    const float4* xyz = a.xyz + b * a.N;
+    const float4 pq = xyz[qp];
+    TopK tk;
+    topk_init(tk);
+    for (int64_t p = 0; p < a.npool; ++p) {
+        const int64_t j = a.pool[b * a.pool_ld + p];
+        topk_insert(tk, k, sqdist4(pq, xyz[j]), (int32_t)j);
+    }
+    const int take = (int)(a.npool < k ? a.npool : k);
+#pragma unroll
+    for (int s = 0; s < kKnnMaxK; ++s) {
+        if (s < k) {
+            a.idx_out[g * k + s] = s < take ? tk.i[s] : -1;
+            a.dist_out[g * k + s] = s < take ? sqrt(tk.d[s]) : nan_d();
+        }
+    }
+    a.cnt_out[g] = take;
+}
+
+// ---- K6 ------------------------------------------------------------------
+__global__ void __launch_bounds__(kKnnThreads) min_spacing_kernel(SpacingArgs a) {
+    __shared__ float4 tp[kKnnTile];
+    const int64_t b = blockIdx.y;
+    const float4* xyz = a.xyz + b * a.N;
+    const int64_t s = blockIdx.x * (int64_t)kKnnThreads + threadIdx.x;
+    const bool active = s < a.n;
+    const float4 ps_ = xyz[active ? a.samples[b * a.ld + s] : a.samples[b * a.ld]];
+    double best = __longlong_as_double(0x7ff0000000000000LL);
+    for (int64_t p0 = 0; p0 < a.n; p0 += kKnnTile) {
+        __syncthreads();
+        for (int t = threadIdx.x; t < kKnnTile; t += kKnnThreads)
+            if (p0 + t < a.n) tp[t] = xyz[a.samples[b * a.ld + p0 + t]];
+        __syncthreads();
+        const int m = (int)((a.n - p0) < kKnnTile ? (a.n - p0) : kKnnTile);
+        if (active)
+            for (int t = 0; t < m; ++t) {
+                if (p0 + t == s) continue;
+                const double d = sqdist4(ps_, tp[t]);
+                if (d < best) best = d;
+            }
+    }
+    if (active) a.out_d2[b * a.n + s] = best;
+}
+
+}  // namespace
+
+cudaError_t launch_bq_rf(const BqArgs& a, cudaStream_t s) {
+    const unsigned g = (unsigned)std::min<int64_t>(148 * 16, (a.B * a.n + 7) / 8 + 1);
+    bq_rf_kernel<<<g, 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bq_naive(const BqArgs& a, cudaStream_t s) {
+    if (a.k > kBqMaxK) return cudaErrorInvalidValue;
+    const unsigned g = (unsigned)std::min<int64_t>(148 * 8, (a.B * a.n + kBqWarps - 1) / kBqWarps + 1);
+    bq_naive_kernel<<<g, kBqWarps * 32, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_knn_naive(const KnnArgs& a, cudaStream_t s) {
+    if (a.k > kKnnMaxK || a.k < 1) return cudaErrorInvalidValue;
+    dim3 g((unsigned)((a.nq + kKnnThreads - 1) / kKnnThreads), (unsigned)a.B);
+    knn_naive_kernel<<<g, kKnnThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_knn_rf(const KnnArgs& a, cudaStream_t s) {
+    if (a.k > kKnnMaxK || a.k < 1) return cudaErrorInvalidValue;
+    dim3 g((unsigned)((a.nq + kKnnThreads - 1) / kKnnThreads), (unsigned)a.B);
+    knn_rf_kernel<<<g, kKnnThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_min_spacing(const SpacingArgs& a, cudaStream_t s) {
+    dim3 g((unsigned)((a.n + kKnnThreads - 1) / kKnnThreads), (unsigned)a.B);
+    min_spacing_kernel<<<g, kKnnThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace ps

@@ -1,0 +1,55 @@
+// ps_internal.h -- host-side launch descriptors shared by the .cu files.
+#pragma once
+
+#include <cstdint>
+#include <cstdlib>
+#include <cuda_runtime.h>
+
+namespace ps {
+
+struct FpsArgs {
+    const float4* xyz;          // [B][N]
+    double* md;                 // [B][N]
+    uint8_t* taken;             // [B][N]
+    int64_t* out_idx;           // [B][ld_out]
+    double* curve;              // [B][ld_out]
+    const int64_t* k_start_dev; // [B] or nullptr -> k_start
+    const int64_t* seed_dev;    // [B] or nullptr -> seed
+    int64_t N, ld_out, k_start, k_stop, seed;
+    int fresh;                  // 1: md=+inf, taken={seed}, out[0]=seed, curve[0]=+inf
+    int64_t points_per_cta;     // set by the launcher
+};
+
+cudaError_t launch_fps(FpsArgs a, int64_t B, cudaStream_t s);
+int fps_choose_cluster(int64_t N, int64_t B, int* C_out, int* P_out);
+
+// Exclusion-list CSR (one cloud = rows [b][0..N); entries at b*cap_entries).
+struct CsrView {
+    int64_t* indptr;    // [B][N+1], per-cloud relative offsets
+    int32_t* nbr;       // [B][cap_entries]
+    double* d2;         // [B][cap_entries]
+    int32_t* counts;    // [B][L][N]
+    int64_t cap_entries;
+    int64_t N;
+    int L;
+};
+
+struct ExclWork {
+    uint32_t* edge_i;     // [B][cap_edges]
+    uint32_t* edge_j;     // [B][cap_edges]
+    double* edge_d2;      // [B][cap_edges]
+    int64_t cap_edges;
+    unsigned long long* edge_count;  // [B]
+    int32_t* deg;         // [B][N] (doubles as the fill cursor)
+    int32_t* long_rows;   // [B*N] rows too long for the warp sort (b*N + i)
+    unsigned int* long_count;  // [1]
+    int32_t* status;      // [B] bit0: edge overflow, bit1: entry overflow
+};
+
+cudaError_t launch_excl_build(const float4* xyz, int64_t B, int64_t N, const double* r2_levels,
+                              int L, int64_t levels_ld, CsrView csr, ExclWork w, cudaStream_t s);
+cudaError_t launch_sort_rows(CsrView csr, int64_t B, ExclWork w, cudaStream_t s);
+cudaError_t launch_level_counts(CsrView csr, int64_t B, const double* r2_levels, int64_t levels_ld,
+                                cudaStream_t s);
+
+}  // namespace ps

@@ -1,0 +1,512 @@
+// sampler.cu -- K2 (curve estimate -> thresholds), K3c (predicted-distance
+// bitmap sampler) and K3d (early-termination min-distance seeding).
+//
+// K2 restates the SPEC.md curve/segmentation stage (
+// pinned in oracle/oracle.py): a = sequential-sum mean of v_i * i**e over the
+// measured prefix, tail a / i**e with a running minimum from the last
+// measured value, radii R_s = est[min(floor(n s / nseg), n-1)] with a running
+// minimum, R <= 0 -> 5e-324, r2 = max(R*R, 5e-324).  Divisions are IEEE
+// (__ddiv_rn) and min is exact, so the parallel evaluation is bit-identical
+// to the sequential oracle.
+//
+// K3c replaces _kernels.sample_predicted (_kernels.py:241-353).  The
+// reference's random pick is a swap-remove from the segment pool with
+// position z_k mod (L - k), z_k = splitmix64(state + (k+1) * GOLDEN): the
+// candidate order of a segment does not depend on the bitmaps, and a
+// candidate is accepted iff no earlier accepted candidate of the segment lies
+// in its level-s exclusion row (rows are symmetric).  One CTA per cloud
+// therefore processes each segment in chunks of 1024 draws:
+//   * positions for the chunk in parallel (u64 splitmix + modulo);
+//   * the swap chain itself (one thread, shared memory);
+//   * greedy maximal independent set over the chunk in parallel rounds
+//     (a candidate is IN when every earlier neighbour in the chunk is OUT,
+//     OUT when an earlier neighbour is IN) -- identical to the serial greedy;
+//   * truncation at the segment boundary (draws consumed = last used
+//     accept + 1, which fixes the RNG state), parallel bitmap clears.
+// Bit-packed bitmaps, pool and rank tables live in shared memory when they
+// fit (N <= ~30k) and in an L2-resident global workspace otherwise.
+//
+// K3d replaces _kernels.earlyterm_scan (_kernels.py:356-367).
+
+#include <cmath>
+
+#include "common.cuh"
+#include "ps_internal.h"
+#include "sampler.h"
+
+namespace ps {
+
+namespace {
+
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+constexpr double kTiny = 4.9406564584124654e-324;
+
+PS_DEV uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// ---------------------------------------------------------------------------
+// K2: thresholds
+
+__global__ void __launch_bounds__(1024) thresholds_kernel(ThreshArgs a) {
+    __shared__ unsigned long long seg_min[kMaxSeg];
+    __shared__ double s_a;
+    const int64_t b = blockIdx.x;
+    const double* v = a.prefix_curve + b * a.curve_ld;  // measured prefix (k0 values)
+    const int64_t k0 = a.k0, n = a.n;
+    const int nseg = a.nseg;
+    if (threadIdx.x < kMaxSeg) seg_min[threadIdx.x] = 0x7ff0000000000000ull;  // +inf bits
+    if (a.mode == 0 && threadIdx.x == 0) {
+        double s = 0.0;
+        for (int64_t i = 1; i < k0; ++i) s = __dadd_rn(s, __dmul_rn(v[i], a.pow_tab[i]));
+        s_a = __ddiv_rn(s, (double)(k0 - 1));
+    }
+    __syncthreads();
+    double est_d[kMaxSeg];
+    if (a.mode == 0) {
+        const double amp = s_a;
+        // min over tail positions i in [k0, d_s] for every s (prefix-min by segment)
+        for (int64_t i = k0 + threadIdx.x; i < n; i += blockDim.x) {
+            const double t = __ddiv_rn(amp, a.pow_tab[i]);
+            int s = 0;
+            while (s < nseg && a.d[s] < i) ++s;
+            if (s < nseg) atomicMin(&seg_min[s], (unsigned long long)__double_as_longlong(t));
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double run = v[k0 - 1];
+            // running min over the tail in order of position; segments partition it
+            for (int s = 0; s < nseg; ++s) {
+                if (a.d[s] < k0) {
+                    est_d[s] = v[a.d[s]];
+                } else {
+                    const double m = __longlong_as_double((long long)seg_min[s]);
+                    if (m < run) run = m;
+                    est_d[s] = run;
+                }
+            }
+        }
+    } else {
+        if (threadIdx.x == 0) {
+            const double* c = a.given_curve + b * a.given_ld;
+            for (int s = 0; s < nseg; ++s) est_d[s] = a.d[s] < k0 ? v[a.d[s]] : c[a.d[s]];
+        }
+    }
+    if (threadIdx.x == 0) {
+        double run = __longlong_as_double(0x7ff0000000000000LL);
+        double* R = a.R_out + b * nseg;
+        double* lv = a.r2_levels + b * a.levels_ld;
+        for (int s = 0; s < nseg; ++s) {
+            if (est_d[s] < run) run = est_d[s];
+            R[s] = run;
+            const double rc = run > 0.0 ? run : kTiny;
+            const double r2 = __dmul_rn(rc, rc);
+            lv[s] = r2 > kTiny ? r2 : kTiny;
+        }
+        for (int e = 0; e < a.n_extra; ++e) lv[nseg + e] = a.extra_r2[e];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K3c: sampler
+
+constexpr int kSampThreads = 1024;
+constexpr int kChunk = 1024;
+constexpr uint8_t kUndecided = 0, kIn = 1, kOut = 2;
+constexpr uint16_t kNoRank = 0xffffu;
+
+struct SampCtl {
+    int64_t i;
+    int seg;
+    int entered;
+    int exhausted;
+    int done;
+    uint64_t state;
+    int64_t pool_len;
+    int undecided;
+    int accepted;
+};
+
+// block-wide exclusive scan of one int per thread; returns (exclusive, total)
+PS_DEV int block_excl_scan(int v, int* warp_tot, int* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        int s = lane < (int)(blockDim.x >> 5) ? warp_tot[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, s, o);
+            if (lane >= o) s += y;
+        }
+        warp_tot[lane] = s;
+    }
+    __syncthreads();
+    const int excl = (warp ? warp_tot[warp - 1] : 0) + x - v;
+    *total = warp_tot[31];
+    __syncthreads();
+    return excl;
+}
+
+struct SampView {
+    uint32_t* bm;      // [nseg][W]
+    int32_t* pool;     // [N]
+    uint16_t* rank;    // [N] draw rank within the current chunk
+    int32_t* cand;     // [kChunk]
+    uint8_t* st;       // [kChunk]
+    uint32_t* pos;     // [kChunk]
+};
+
+PS_DEV void build_pool(const SampView& v, int seg, int64_t W, SampCtl* ctl, int* warp_tot) {
+    const uint32_t* row = v.bm + (int64_t)seg * W;
+    int64_t carry = 0;
+    for (int64_t base = 0; base < W; base += blockDim.x) {
+        const int64_t w = base + threadIdx.x;
+        const uint32_t word = w < W ? row[w] : 0u;
+        int tot;
+        const int ex = block_excl_scan(__popc(word), warp_tot, &tot);
+        int64_t p = carry + ex;
+        uint32_t x = word;
+        while (x) {
+            const int bit = __ffs(x) - 1;
+            x &= x - 1;
+            v.pool[p++] = (int32_t)(w * 32 + bit);
+        }
+        carry += tot;
+    }
+    if (threadIdx.x == 0) ctl->pool_len = carry;
+    __syncthreads();
+}
+
+// clear the level-l row prefix of point p (plus p itself) for l in [l0, nseg)
+PS_DEV void clear_point_levels(const SampView& v, const SampArgs& a, int64_t b, int64_t W, int32_t p, int l0,
+                               int lane, int nl) {
+    const int64_t N = a.N;
+    const int64_t base = a.indptr[b * (N + 1) + p];
+    const int32_t* nbr = a.nbr + b * a.cap_entries + base;
+    for (int l = l0; l < a.nseg; ++l) {
+        const int32_t c = a.counts[(b * a.L + a.seg_level_rows[l]) * N + p];
+        uint32_t* bm = v.bm + (int64_t)l * W;
+        for (int u = lane; u < c; u += nl) {
+            const int32_t q = nbr[u];
+            atomicAnd(&bm[q >> 5], ~(1u << (q & 31)));
+        }
+        if (lane == 0) atomicAnd(&bm[p >> 5], ~(1u << (p & 31)));
+    }
+}
+
+__global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
+    extern __shared__ __align__(16) unsigned char dyn[];
+    __shared__ SampCtl ctl;
+    __shared__ int warp_tot[32];
+    const int64_t b = blockIdx.x;
+    const int64_t N = a.N;
+    const int64_t W = (N + 31) >> 5;
+    const int nseg = a.nseg;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+
+    // carve the workspace: shared memory when it fits, else this cloud's global slice
+    unsigned char* ws = a.use_smem ? dyn : (a.gws + b * a.gws_stride);
+    SampView v;
+    {
+        size_t off = 0;
+        v.bm = reinterpret_cast<uint32_t*>(ws + off); off += sizeof(uint32_t) * nseg * W;
+        off = (off + 15) & ~size_t(15);
+        v.pool = reinterpret_cast<int32_t*>(ws + off); off += sizeof(int32_t) * N;
+        v.rank = reinterpret_cast<uint16_t*>(ws + off); off += sizeof(uint16_t) * N;
+        off = (off + 15) & ~size_t(15);
+        v.cand = reinterpret_cast<int32_t*>(ws + off); off += sizeof(int32_t) * kChunk;
+        v.pos = reinterpret_cast<uint32_t*>(ws + off); off += sizeof(uint32_t) * kChunk;
+        v.st = reinterpret_cast<uint8_t*>(ws + off);
+    }
+    int64_t* out = a.out_idx + b * a.ld_out;
+    const int64_t k0 = a.k0, n_total = a.n_total;
+
+    // ---- init: all bits set (valid points), rank table empty --------------
+    for (int64_t w = tid; w < (int64_t)nseg * W; w += blockDim.x) {
+        const int64_t ww = w % W;
+        const int64_t nb = N - ww * 32;
+        v.bm[w] = nb >= 32 ? 0xffffffffu : (nb <= 0 ? 0u : ((1u << nb) - 1u));
+    }
+    for (int64_t j = tid; j < N; j += blockDim.x) v.rank[j] = kNoRank;
+    if (tid == 0) {
+        ctl.state = a.state_io[b];
+        ctl.done = 0;
+        ctl.exhausted = 0;
+        ctl.entered = 0;
+    }
+    __syncthreads();
+    // pre-clear every prefix point's rows at all levels (_kernels.py:273-276)
+    for (int64_t t = warp; t < k0; t += nwarps) clear_point_levels(v, a, b, W, (int32_t)out[t], 0, lane, 32);
+    for (int64_t t = k0 + tid; t < n_total; t += blockDim.x) out[t] = -1;
+    __syncthreads();
+
+    if (tid == 0) {
+        int seg = 0;
+        while (seg < nseg && k0 >= a.boundaries[seg]) ++seg;
+        ctl.i = k0;
+        ctl.seg = seg;
+        if (seg >= nseg) {
+            ctl.done = 1;
+            ctl.exhausted = 1;
+        } else {
+            ctl.entered = 1;
+        }
+    }
+    __syncthreads();
+    if (!ctl.done) build_pool(v, ctl.seg, W, &ctl, warp_tot);
+
+    // ---- main loop: one iteration per segment visit ----------------------
+    while (!ctl.done) {
+        if (ctl.i >= n_total) break;
+        if (ctl.i >= a.boundaries[ctl.seg]) {
+            __syncthreads();
+            if (tid == 0) {
+                int seg = ctl.seg;
+                while (ctl.i >= a.boundaries[seg]) ++seg;
+                ctl.seg = seg;
+                ctl.entered += 1;
+            }
+            __syncthreads();
+            build_pool(v, ctl.seg, W, &ctl, warp_tot);
+        }
+        const int seg = ctl.seg;
+        const int64_t L = ctl.pool_len;
+        const uint64_t state0 = ctl.state;
+        const int lvl = a.seg_level_rows[seg];
+        const int32_t* cnt_row = a.counts + (b * a.L + lvl) * N;
+        const int64_t* indptr = a.indptr + b * (N + 1);
+        const int32_t* nbr_all = a.nbr + b * a.cap_entries;
+        int64_t k = 0;  // draws consumed in this segment visit
+        bool seg_over = false;
+        while (!seg_over) {
+            if (k >= L) {
+                // pool exhausted: the picked < 0 path of _kernels.py:335-347
+                __syncthreads();
+                if (tid == 0) {
+                    if (!a.pick_lowest) ctl.state = state0 + (uint64_t)L * kGolden;
+                    ctl.seg += 1;
+                    if (ctl.seg >= nseg) {
+                        ctl.exhausted = 1;
+                        ctl.done = 1;
+                    } else {
+                        ctl.entered += 1;
+                    }
+                }
+                __syncthreads();
+                if (!ctl.done) build_pool(v, ctl.seg, W, &ctl, warp_tot);
+                seg_over = true;
+                break;
+            }
+            const int K = (int)((L - k) < kChunk ? (L - k) : kChunk);
+            // candidate order for draws k .. k+K-1
+            if (a.pick_lowest) {
+                for (int t = tid; t < K; t += blockDim.x) v.cand[t] = v.pool[k + t];
+            } else {
+                for (int t = tid; t < K; t += blockDim.x) {
+                    const uint64_t z = mix64(state0 + (uint64_t)(k + t + 1) * kGolden);
+                    v.pos[t] = (uint32_t)(z % (uint64_t)(L - (k + t)));
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    int32_t* pool = v.pool;
+                    for (int t = 0; t < K; ++t) {
+                        const int64_t last = L - 1 - (k + t);
+                        const uint32_t p = v.pos[t];
+                        const int32_t c = pool[p];
+                        pool[p] = pool[last];
+                        v.cand[t] = c;
+                    }
+                }
+            }
+            __syncthreads();
+            // availability + rank
+            const uint32_t* bms = v.bm + (int64_t)seg * W;
+            for (int t = tid; t < K; t += blockDim.x) {
+                const int32_t c = v.cand[t];
+                const bool av = (bms[c >> 5] >> (c & 31)) & 1u;
+                v.st[t] = av ? kUndecided : kOut;
+                v.rank[c] = (uint16_t)t;
+            }
+            __syncthreads();
+            // greedy MIS rounds
+            for (;;) {
+                if (tid == 0) ctl.undecided = 0;
+                __syncthreads();
+                int und = 0;
+                for (int t = tid; t < K; t += blockDim.x) {
+                    if (v.st[t] != kUndecided) continue;
+                    const int32_t c = v.cand[t];
+                    const int64_t base = indptr[c];
+                    const int32_t m = cnt_row[c];
+                    const int32_t* row = nbr_all + base;
+                    bool out_ = false, blocked = false;
+                    for (int32_t u = 0; u < m; ++u) {
+                        const int32_t q = row[u];
+                        const uint32_t rq = v.rank[q];  // 0xffff = not in chunk
+                        if (rq < (uint32_t)t) {
+                            const uint8_t s = v.st[rq];
+                            if (s == kIn) { out_ = true; break; }
+                            if (s == kUndecided) blocked = true;
+                        }
+                    }
+                    if (out_) v.st[t] = kOut;
+                    else if (!blocked) v.st[t] = kIn;
+                    else ++und;
+                }
+                und = __reduce_add_sync(kFull, und);
+                if (lane == 0 && und) atomicAdd(&ctl.undecided, und);
+                __syncthreads();
+                if (ctl.undecided == 0) break;
+            }
+            // ordered compaction of accepted candidates
+            const int64_t need = a.boundaries[seg] - ctl.i;
+            int flag = (tid < K && v.st[tid] == kIn) ? 1 : 0;
+            int tot;
+            const int ex = block_excl_scan(flag, warp_tot, &tot);
+            const int64_t take = (int64_t)tot < need ? (int64_t)tot : need;
+            const int64_t i0 = ctl.i;
+            if (flag && ex < take) {
+                out[i0 + ex] = v.cand[tid];
+                if (ex == take - 1 && take == need) ctl.accepted = tid;  // draw of the last used accept
+            }
+            __syncthreads();
+            // clears: levels seg.. when the segment continues, seg+1.. when it ends
+            const bool ends = (take == need);
+            const int l0 = ends ? seg + 1 : seg;
+            if (l0 < nseg) {
+                for (int64_t x = warp; x < take; x += nwarps)
+                    clear_point_levels(v, a, b, W, (int32_t)out[i0 + x], l0, lane, 32);
+            }
+            for (int t = tid; t < K; t += blockDim.x) v.rank[v.cand[t]] = kNoRank;
+            __syncthreads();
+            if (tid == 0) {
+                ctl.i = i0 + take;
+                if (ends && !a.pick_lowest) ctl.state = state0 + (uint64_t)(k + ctl.accepted + 1) * kGolden;
+            }
+            __syncthreads();
+            if (ends) {
+                seg_over = true;
+            } else {
+                k += K;
+            }
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        a.reached[b] = ctl.i;
+        a.exhausted[b] = ctl.exhausted;
+        a.entered[b] = ctl.entered;
+        a.state_io[b] = ctl.state;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K3d: early termination
+
+__global__ void et_prepare_kernel(EtArgs a) {
+    const int64_t total = a.B * a.N;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = g / a.N;
+        if (a.reached[b] >= a.n_total) continue;
+        a.taken[g] = 0;
+        a.md[g] = __longlong_as_double(0x7ff0000000000000LL);
+    }
+}
+
+__global__ void et_mark_kernel(EtArgs a) {
+    const int64_t total = a.B * a.n_total;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = g / a.n_total, t = g - b * a.n_total;
+        const int64_t r = a.reached[b];
+        if (r >= a.n_total || t >= r) continue;
+        a.taken[b * a.N + a.out_idx[b * a.ld_out + t]] = 1;
+    }
+}
+
+}  // namespace
+
+// md[i] = min(md[i], min over the first lvl1[i] row entries j with taken[j] of d2)
+__global__ void et_scan_kernel(EtScanArgs a) {
+    const int64_t total = a.B * (a.hi - a.lo);
+    const int64_t span = a.hi - a.lo;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = g / span;
+        if (a.reached && a.reached[b] >= a.n_total) continue;
+        const int64_t i = a.lo + (g - b * span);
+        const int64_t base = a.indptr[b * (a.N + 1) + i];
+        const int32_t c = a.lvl1_counts[b * a.counts_stride + i];
+        const int32_t* nbr = a.nbr + b * a.cap_entries + base;
+        const double* d2 = a.d2 + b * a.cap_entries + base;
+        const uint8_t* tk = a.taken + b * a.N;
+        double best = a.md[b * a.N + i];
+        for (int32_t u = 0; u < c; ++u) {
+            const int32_t j = nbr[u];
+            if (tk[j]) {
+                const double d = d2[u];
+                if (d < best) best = d;
+            }
+        }
+        a.md[b * a.N + i] = best;
+    }
+}
+
+size_t sampler_ws_bytes(int64_t N, int nseg) {
+    const int64_t W = (N + 31) >> 5;
+    size_t off = sizeof(uint32_t) * nseg * W;
+    off = (off + 15) & ~size_t(15);
+    off += sizeof(int32_t) * N + sizeof(uint16_t) * N;
+    off = (off + 15) & ~size_t(15);
+    off += sizeof(int32_t) * kChunk + sizeof(uint32_t) * kChunk + kChunk;
+    return (off + 255) & ~size_t(255);
+}
+
+cudaError_t launch_thresholds(const ThreshArgs& a, int64_t B, cudaStream_t s) {
+    thresholds_kernel<<<(unsigned)B, 1024, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sampler(SampArgs a, int64_t B, cudaStream_t s) {
+    const size_t need = sampler_ws_bytes(a.N, a.nseg);
+    size_t dsm = 0;
+    if (a.use_smem) {
+        dsm = need;
+        cudaError_t e = cudaFuncSetAttribute(sampler_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+        if (e != cudaSuccess) return e;
+    }
+    sampler_kernel<<<(unsigned)B, kSampThreads, dsm, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_et(const EtArgs& a, cudaStream_t s) {
+    const unsigned g1 = (unsigned)std::min<int64_t>(148 * 8, (a.B * a.N + 255) / 256 + 1);
+    et_prepare_kernel<<<g1, 256, 0, s>>>(a);
+    const unsigned g2 = (unsigned)std::min<int64_t>(148 * 8, (a.B * a.n_total + 255) / 256 + 1);
+    et_mark_kernel<<<g2, 256, 0, s>>>(a);
+    EtScanArgs sa;
+    sa.indptr = a.indptr; sa.nbr = a.nbr; sa.d2 = a.d2; sa.cap_entries = a.cap_entries;
+    sa.lvl1_counts = a.lvl1_counts; sa.counts_stride = a.counts_stride;
+    sa.taken = a.taken; sa.md = a.md; sa.reached = a.reached; sa.n_total = a.n_total;
+    sa.B = a.B; sa.N = a.N; sa.lo = 0; sa.hi = a.N;
+    et_scan_kernel<<<g1, 256, 0, s>>>(sa);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_et_scan(const EtScanArgs& a, cudaStream_t s) {
+    const unsigned g = (unsigned)std::min<int64_t>(148 * 8, (a.B * (a.hi - a.lo) + 255) / 256 + 1);
+    et_scan_kernel<<<g, 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace ps

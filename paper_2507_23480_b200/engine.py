@@ -1,0 +1,371 @@
+"""Batched device pipeline: exact FPS, FastPoint (MDPS) sampling and grouping
+for B clouds of N points on one B200, stream-ordered through the C ABI.
+
+This is the hot path.  PyTorch provides device memory, the stream and CUDA
+graphs; every computation is one of the sm_100a kernels in csrc/.  The
+launch sequence of ``FastPoint.sample`` mirrors call stack (B) of SURVEY.md
+section 3:
+
+  K1  ps_fps                      FPS prefix, k0 = ceil(p n) iterations
+  K2  ps_thresholds               power-law estimate -> segment radii / levels
+  K3a ps_excl_build               exclusion CSR + level counts (one pass)
+  K3c ps_sample_predicted         bitmap sampler (greedy-MIS formulation)
+  K3d ps_early_termination_prepare + K1 ps_fps_loop(k_start = reached)
+  K4a ps_ball_query_rf            grouping from the cached distances
+
+No host synchronisation happens inside ``sample``/``group``; the only host
+reads are the capacity status (``check``) and the results the caller asks
+for.  All buffers are allocated once, so the whole sequence can be captured
+in a CUDA graph (``capture``).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .curve import power_table, prefix_len, radius_sq, sampler_boundaries, threshold_positions
+
+
+def _p(t):
+    return 0 if t is None else t.data_ptr()
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def as_xyz4(coords, device=None) -> torch.Tensor:
+    """[B, N, 3] (or [N, 3]) float32 -> contiguous [B, N, 4] float32 on device."""
+    t = torch.as_tensor(coords)
+    if t.dim() == 2:
+        t = t.unsqueeze(0)
+    if t.dim() != 3 or t.shape[-1] != 3:
+        raise ValueError(f"expected (B, N, 3) coordinates, got {tuple(t.shape)}")
+    if t.dtype != torch.float32:
+        raise ValueError("coordinates must be float32 (PointCloud storage, core.py:183)")
+    dev = torch.device(device) if device is not None else (t.device if t.is_cuda else torch.device("cuda"))
+    out = torch.zeros(t.shape[0], t.shape[1], 4, dtype=torch.float32, device=dev)
+    out[..., :3].copy_(t, non_blocking=True)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# exact FPS
+
+
+def fps(xyz4: torch.Tensor, n: int, seed_index: int = 0, k_stop: int | None = None):
+    """Exact FPS on a batch.  Returns (idx int64[B,n],
+    curve float64[B,n], md float64[B,N], taken uint8[B,N])."""
+    B, N, _ = xyz4.shape
+    if not (1 <= n <= N):
+        raise ValueError(f"n must be in [1, {N}], got {n}")
+    stop = n if k_stop is None else int(k_stop)
+    dev = xyz4.device
+    md = torch.empty(B, N, dtype=torch.float64, device=dev)
+    taken = torch.empty(B, N, dtype=torch.uint8, device=dev)
+    out = torch.full((B, n), -1, dtype=torch.int64, device=dev)
+    curve = torch.full((B, n), math.inf, dtype=torch.float64, device=dev)
+    _lib.call("ps_fps", _p(xyz4), B, N, _p(md), _p(taken), _p(out), _p(curve), n, stop, int(seed_index), None,
+              _stream())
+    return out, curve, md, taken
+
+
+def fps_loop(xyz4, md, taken, out_idx, curve, k_start, n_total, k_start_dev=None):
+    B, N, _ = xyz4.shape
+    _lib.call("ps_fps_loop", _p(xyz4), B, N, _p(md), _p(taken), _p(out_idx), _p(curve), out_idx.shape[1],
+              int(k_start), _p(k_start_dev), int(n_total), _stream())
+
+
+# ---------------------------------------------------------------------------
+# exclusion lists
+
+
+@dataclass
+class DeviceCsr:
+    indptr: torch.Tensor   # int64 [B, N+1]
+    nbr: torch.Tensor      # int32 [B, cap]
+    d2: torch.Tensor       # float64 [B, cap]
+    counts: torch.Tensor   # int32 [B, L, N]
+    levels: torch.Tensor   # float64 [B, L]
+    status: torch.Tensor   # int32 [B]
+    work: torch.Tensor     # uint8 workspace
+    cap_entries: int
+    cap_edges: int
+
+    @property
+    def L(self):
+        return self.counts.shape[1]
+
+    @staticmethod
+    def allocate(B, N, L, cap_entries, cap_edges, device):
+        cap_entries = int(min(max(cap_entries, N), (1 << 31) - 1))
+        cap_edges = int(max(cap_edges, 1))
+        ws = int(_lib.raw("ps_excl_workspace_bytes", B, N, cap_edges))
+        return DeviceCsr(
+            indptr=torch.zeros(B, N + 1, dtype=torch.int64, device=device),
+            nbr=torch.empty(B, cap_entries, dtype=torch.int32, device=device),
+            d2=torch.empty(B, cap_entries, dtype=torch.float64, device=device),
+            counts=torch.empty(B, L, N, dtype=torch.int32, device=device),
+            levels=torch.empty(B, L, dtype=torch.float64, device=device),
+            status=torch.zeros(B, dtype=torch.int32, device=device),
+            work=torch.empty(ws, dtype=torch.uint8, device=device),
+            cap_entries=cap_entries, cap_edges=cap_edges)
+
+    def build(self, xyz4):
+        B, N, _ = xyz4.shape
+        _lib.call("ps_excl_build", _p(xyz4), B, N, _p(self.levels), self.L, self.levels.shape[1], _p(self.indptr),
+                  _p(self.nbr), _p(self.d2), _p(self.counts), self.cap_entries, _p(self.work), self.cap_edges,
+                  _p(self.status), _stream())
+
+    def overflowed(self) -> bool:
+        return bool(int(self.status.max().item()) != 0)
+
+    def row(self, b, i):
+        lo, hi = (int(v) for v in self.indptr[b, i:i + 2].tolist())
+        return self.nbr[b, lo:hi], self.d2[b, lo:hi]
+
+
+def default_capacity(N: int, n: int) -> tuple[int, int]:
+    """CSR entries per cloud: rows average ~14 x stride at the first segment
+    radius; start with a generous bound, grow on overflow."""
+    stride = max(1, N // max(n, 1))
+    per_point = min(N, max(96, 48 * stride))
+    cap_entries = N * per_point
+    return cap_entries, max(1, (cap_entries - N) // 2 + 1)
+
+
+# ---------------------------------------------------------------------------
+# FastPoint pipeline
+
+
+class FastPoint:
+    """FastPoint sampling (+ redundancy-free grouping) on a fixed-shape batch.
+
+    Parameters mirror SPEC.md:425-433 ``mdps(cloud, n, {p, nseg, estimator,
+    seed_index, rng})``; ``extra_radii`` are ball-query radii baked into the
+    exclusion lists."""
+
+    def __init__(self, B, N, n, *, p=0.1, nseg=6, estimator="power", exponent=None, extra_radii=(),
+                 seed_index=0, pick_lowest=False, cap_entries=None, device="cuda"):
+        if not (1 <= n <= N):
+            raise ValueError(f"n must be in [1, {N}]")
+        if nseg < 1 or nseg > 16:
+            raise ValueError("nseg must be in [1, 16]")
+        if estimator not in ("power", "curve"):
+            raise ValueError(f"unknown estimator {estimator!r}")
+        if estimator == "power" and exponent is None:
+            raise ValueError("power estimator needs an exponent (fit_power_exponent)")
+        self.B, self.N, self.n = int(B), int(N), int(n)
+        self.p, self.nseg, self.estimator = float(p), int(nseg), estimator
+        self.exponent = None if exponent is None else float(exponent)
+        self.extra_radii = tuple(float(r) for r in extra_radii)
+        for r in self.extra_radii:
+            if not r > 0:
+                raise ValueError(f"extra radius must be positive, got {r}")
+        if len(self.extra_radii) > 8:
+            raise ValueError("at most 8 extra radii")
+        self.seed_index = int(seed_index)
+        self.pick_lowest = bool(pick_lowest)
+        self.device = torch.device(device)
+        self.k0 = min(prefix_len(self.n, self.p), self.n)
+        if self.k0 < 2:
+            raise ValueError("ceil(p*n) must be >= 2 (SPEC.md:240)")
+        self.d = threshold_positions(self.n, self.nseg)
+        self.boundaries = sampler_boundaries(self.n, self.nseg)
+        self.seg_level_rows = np.arange(self.nseg, dtype=np.int32)
+        self.extra_r2 = np.array([radius_sq(r) for r in self.extra_radii], np.float64)
+        self.L = self.nseg + len(self.extra_radii)
+        dev = self.device
+        B, N = self.B, self.N
+        self.xyz4 = torch.zeros(B, N, 4, dtype=torch.float32, device=dev)
+        self.md = torch.empty(B, N, dtype=torch.float64, device=dev)
+        self.taken = torch.empty(B, N, dtype=torch.uint8, device=dev)
+        self.out = torch.full((B, n), -1, dtype=torch.int64, device=dev)
+        self.curve = torch.full((B, n), math.inf, dtype=torch.float64, device=dev)
+        self.R = torch.empty(B, self.nseg, dtype=torch.float64, device=dev)
+        self.reached = torch.zeros(B, dtype=torch.int64, device=dev)
+        self.exhausted = torch.zeros(B, dtype=torch.int32, device=dev)
+        self.entered = torch.zeros(B, dtype=torch.int32, device=dev)
+        self.state = torch.zeros(B, dtype=torch.int64, device=dev)  # uint64 bit pattern
+        self.pow_tab = (torch.as_tensor(power_table(self.n, self.exponent), device=dev)
+                        if estimator == "power" else None)
+        self.given_curve = torch.zeros(B, n, dtype=torch.float64, device=dev) if estimator == "curve" else None
+        ce, cg = (default_capacity(N, n) if cap_entries is None else (int(cap_entries), int(cap_entries) // 2 + 1))
+        self.csr = DeviceCsr.allocate(B, N, self.L, ce, cg, dev)
+        ws = int(_lib.raw("ps_sampler_workspace_bytes", B, N, self.nseg))
+        self.samp_ws = torch.empty(max(ws, 1), dtype=torch.uint8, device=dev) if ws else None
+        self._bnd_c = np.ascontiguousarray(self.boundaries, np.int64)
+        self._rows_c = np.ascontiguousarray(self.seg_level_rows, np.int32)
+        self._d_c = np.ascontiguousarray(self.d, np.int64)
+        self.graph = None
+
+    # -- inputs ---------------------------------------------------------------
+    def set_points(self, coords):
+        t = torch.as_tensor(coords)
+        if t.dim() == 2:
+            t = t.unsqueeze(0)
+        if tuple(t.shape) != (self.B, self.N, 3) or t.dtype != torch.float32:
+            raise ValueError(f"expected float32 ({self.B}, {self.N}, 3), got {t.dtype} {tuple(t.shape)}")
+        self.xyz4[..., :3].copy_(t, non_blocking=True)
+
+    def set_rng(self, seeds):
+        s = np.asarray(seeds, dtype=np.uint64).reshape(-1)
+        if s.shape[0] == 1:
+            s = np.repeat(s, self.B)
+        self.state.copy_(torch.from_numpy(s.view(np.int64).copy()), non_blocking=False)
+
+    def set_curve(self, curves):
+        if self.given_curve is None:
+            raise ValueError("estimator is not 'curve'")
+        self.given_curve.copy_(torch.as_tensor(curves, dtype=torch.float64).reshape(self.B, self.n))
+
+    # -- stages -----------------------------------------------------------------
+    def _prefix(self):
+        _lib.call("ps_fps", _p(self.xyz4), self.B, self.N, _p(self.md), _p(self.taken), _p(self.out),
+                  _p(self.curve), self.n, self.k0, self.seed_index, None, _stream())
+
+    def _thresholds(self):
+        mode = 0 if self.estimator == "power" else 1
+        extra = np.ascontiguousarray(self.extra_r2) if len(self.extra_r2) else np.zeros(1)
+        _lib.call("ps_thresholds", _p(self.curve), self.n, self.B, self.k0, self.n, self.nseg,
+                  self._d_c.ctypes.data, mode, _p(self.pow_tab), _p(self.given_curve), self.n,
+                  extra.ctypes.data, len(self.extra_r2), _p(self.R), _p(self.csr.levels), self.L, _stream())
+
+    def _exclusion(self):
+        self.csr.build(self.xyz4)
+
+    def _sampler(self):
+        c = self.csr
+        _lib.call("ps_sample_predicted", _p(c.indptr), _p(c.nbr), c.cap_entries, _p(c.counts), self.L,
+                  self._rows_c.ctypes.data, self._bnd_c.ctypes.data, self.nseg, _p(self.out), self.n, self.k0,
+                  self.n, self.B, self.N, _p(self.state), 1 if self.pick_lowest else 0, _p(self.reached),
+                  _p(self.exhausted), _p(self.entered), _p(self.samp_ws), _stream())
+
+    def _early_termination(self):
+        c = self.csr
+        lvl1 = c.counts[:, int(self.seg_level_rows[0]), :]
+        _lib.call("ps_early_termination_prepare", _p(c.indptr), _p(c.nbr), _p(c.d2), c.cap_entries, _p(lvl1),
+                  self.L * self.N, _p(self.taken), _p(self.md), _p(self.out), self.n, _p(self.reached), self.n,
+                  self.B, self.N, _stream())
+        _lib.call("ps_fps_loop", _p(self.xyz4), self.B, self.N, _p(self.md), _p(self.taken), _p(self.out),
+                  _p(self.curve), self.n, 1, _p(self.reached), self.n, _stream())
+
+    def sample(self):
+        """Launch the full sampling sequence (no host sync)."""
+        if self.graph is not None:
+            self.graph.replay()
+            return
+        self._prefix()
+        self._thresholds()
+        self._exclusion()
+        self._sampler()
+        self._early_termination()
+
+    KERNELS_PER_SAMPLE = 1 + 1 + 6 + 1 + 3 + 1
+
+    def capture(self):
+        """Capture ``sample`` into a CUDA graph (buffers are static)."""
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self.sample()  # warm-up outside capture (sets kernel attributes)
+        torch.cuda.current_stream().wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.sample()
+        self.graph = g
+        return g
+
+    def check(self):
+        """Host read of the CSR capacity status; grows buffers and re-runs on
+        overflow.  Returns True when a re-run happened."""
+        if not self.csr.overflowed():
+            return False
+        E = int(self.csr.indptr[:, -1].max().item())
+        grow = max(2 * self.csr.cap_entries, E + self.N)
+        self.csr = DeviceCsr.allocate(self.B, self.N, self.L, grow, grow // 2 + 1, self.device)
+        self.graph = None
+        self.sample()
+        return True
+
+    # -- grouping ---------------------------------------------------------------
+    def level_of_radius(self, r: float) -> int:
+        for e, rr in enumerate(self.extra_radii):
+            if rr == float(r):
+                return self.nseg + e
+        raise ValueError(f"radius {r} not baked into the exclusion lists; available {list(self.extra_radii)}")
+
+    def group_rf(self, radius, k, centroids=None, out=None):
+        """rf_ball_query around the samples (default) -> (idx, dist, cnt)."""
+        lvl = self.level_of_radius(radius)
+        cent = self.out if centroids is None else centroids
+        B, n = cent.shape
+        if out is None:
+            out = (torch.empty(B, n, k, dtype=torch.int32, device=self.device),
+                   torch.empty(B, n, k, dtype=torch.float64, device=self.device),
+                   torch.empty(B, n, dtype=torch.int32, device=self.device))
+        c = self.csr
+        _lib.call("ps_ball_query_rf", _p(c.indptr), _p(c.nbr), _p(c.d2), c.cap_entries, _p(c.counts), self.L, lvl,
+                  _p(cent), cent.stride(0), B, self.N, n, int(k), _p(out[0]), _p(out[1]), _p(out[2]), _stream())
+        return out
+
+    def knn_rf(self, k, queries=None):
+        """rf_knn from every point (default) into the sampled set."""
+        B, N = self.B, self.N
+        sampled = torch.zeros(B, N, dtype=torch.uint8, device=self.device)
+        sampled.scatter_(1, self.out, 1)
+        nq = N if queries is None else queries.shape[1]
+        idx = torch.empty(B, nq, k, dtype=torch.int32, device=self.device)
+        dist = torch.empty(B, nq, k, dtype=torch.float64, device=self.device)
+        cnt = torch.empty(B, nq, dtype=torch.int32, device=self.device)
+        fb = torch.zeros(B, dtype=torch.int32, device=self.device)
+        c = self.csr
+        lvl1 = c.counts[:, int(self.seg_level_rows[0]), :]
+        _lib.call("ps_knn_rf", _p(self.xyz4), _p(c.indptr), _p(c.nbr), _p(c.d2), c.cap_entries, _p(lvl1),
+                  self.L * N, _p(sampled), _p(queries), 0 if queries is None else queries.stride(0), nq,
+                  _p(self.out), self.n, self.n, B, N, int(k), _p(idx), _p(dist), _p(cnt), _p(fb), _stream())
+        return idx, dist, cnt, fb
+
+    # -- accounting ---------------------------------------------------------------
+    def pair_evals(self) -> list[int]:
+        """Per-cloud pair-distance evaluations (SPEC.md:438 accounting):
+        prefix N(k0-1) + exclusion N(N-1)/2 + N + early termination N(n-i)."""
+        reached = self.reached.tolist()
+        N = self.N
+        base = N * (self.k0 - 1) + N * (N - 1) // 2 + N
+        return [base + N * (self.n - int(r)) for r in reached]
+
+
+def ball_query_naive(xyz4, centroids, radius, k):
+    B, N, _ = xyz4.shape
+    n = centroids.shape[1]
+    idx = torch.empty(B, n, k, dtype=torch.int32, device=xyz4.device)
+    dist = torch.empty(B, n, k, dtype=torch.float64, device=xyz4.device)
+    cnt = torch.empty(B, n, dtype=torch.int32, device=xyz4.device)
+    _lib.call("ps_ball_query_naive", _p(xyz4), _p(centroids), centroids.stride(0), B, N, n, radius_sq(float(radius)),
+              int(k), _p(idx), _p(dist), _p(cnt), _stream())
+    return idx, dist, cnt
+
+
+def knn_naive(xyz4, pool, k, queries=None):
+    B, N, _ = xyz4.shape
+    nq = N if queries is None else queries.shape[1]
+    idx = torch.empty(B, nq, k, dtype=torch.int32, device=xyz4.device)
+    dist = torch.empty(B, nq, k, dtype=torch.float64, device=xyz4.device)
+    cnt = torch.empty(B, nq, dtype=torch.int32, device=xyz4.device)
+    _lib.call("ps_knn_naive", _p(xyz4), _p(queries), 0 if queries is None else queries.stride(0), nq, _p(pool),
+              pool.stride(0), pool.shape[1], B, N, int(k), _p(idx), _p(dist), _p(cnt), _stream())
+    return idx, dist, cnt
+
+
+def min_spacing_d2(xyz4, samples):
+    B, N, _ = xyz4.shape
+    n = samples.shape[1]
+    out = torch.empty(B, n, dtype=torch.float64, device=xyz4.device)
+    _lib.call("ps_min_spacing", _p(xyz4), _p(samples), samples.stride(0), n, B, N, _p(out), _stream())
+    return out

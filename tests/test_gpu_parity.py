@@ -1,0 +1,336 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle
+and the golden vectors of the real reference.  Indices, counts and RNG state
+are compared bit-exactly; float64 distances / curves bit-exactly too (same
+operation sequence, IEEE sqrt/div)."""
+
+import numpy as np
+import pytest
+
+from golden_util import cases, digest, mdps_kwargs
+from oracle import oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2507_23480_b200 import _kernels as GK  # noqa: E402
+from paper_2507_23480_b200 import engine  # noqa: E402
+from paper_2507_23480_b200.harness import generate_cloud  # noqa: E402
+
+
+def gpu_fps(cloud, n, seed=0):
+    xyz4 = engine.as_xyz4(cloud)
+    idx, curve, md, taken = engine.fps(xyz4, n, seed)
+    return idx[0].cpu().numpy(), curve[0].cpu().numpy(), md[0].cpu().numpy(), taken[0].cpu().numpy()
+
+
+def gpu_mdps(cloud, n, **kw):
+    kw = dict(kw)
+    est = kw.pop("estimator", "power")
+    curve = kw.pop("curve", None)
+    rng_seed = kw.pop("rng_seed", 0)
+    fp = engine.FastPoint(1, cloud.shape[0], n, estimator=est, **kw)
+    fp.set_points(torch.from_numpy(np.ascontiguousarray(cloud)).cuda())
+    fp.set_rng([rng_seed])
+    if est == "curve":
+        fp.set_curve(np.asarray(curve).reshape(1, n))
+    fp.sample()
+    fp.check()
+    return fp
+
+
+# ---- K1 exact FPS ---------------------------------------------------------------
+
+def test_fps_golden(golden):
+    for k in golden.files:
+        if not (k.startswith("fps/") and k.endswith("/idx")):
+            continue
+        _, name, s, _ = k.split("/")
+        seed = int(s[1:])
+        c = golden[f"cloud/{name}"]
+        n = int(golden[f"fps/{name}/n"])
+        idx, curve, md, _ = gpu_fps(c, n, seed)
+        np.testing.assert_array_equal(idx, golden[k], err_msg=k)
+        np.testing.assert_array_equal(curve, golden[f"fps/{name}/s{seed}/curve"], err_msg=k)
+        np.testing.assert_array_equal(digest(md), golden[f"fps/{name}/s{seed}/md"], err_msg=k)
+
+
+@pytest.mark.parametrize("N,n,family", [
+    (1, 1, "uniform-box"), (2, 2, "uniform-box"), (37, 37, "lattice"), (300, 75, "unit-sphere"),
+    (1024, 512, "unit-sphere"), (4096, 1024, "uniform-box"), (5000, 1250, "lattice"),
+    (24000, 6000, "room-surfaces"), (65536, 2048, "uniform-box"), (70001, 600, "gaussian-clusters"),
+])
+def test_fps_matches_oracle_across_cluster_shapes(N, n, family):
+    c = generate_cloud(family, N, N + n)
+    idx, curve, md, taken = gpu_fps(c, n, seed=N // 3)
+    ri, rc, rmd, rtk, _ = O.fps(c, n, N // 3)
+    np.testing.assert_array_equal(idx, ri)
+    np.testing.assert_array_equal(curve, rc)
+    np.testing.assert_array_equal(md, rmd)
+    np.testing.assert_array_equal(taken, rtk)
+
+
+def test_fps_batched_and_duplicates():
+    B, N = 5, 900
+    base = generate_cloud("uniform-box", 300, 5)
+    clouds = np.stack([np.repeat(base, 3, axis=0)[np.random.default_rng(b).permutation(N)] for b in range(B)])
+    xyz4 = engine.as_xyz4(torch.from_numpy(clouds).cuda())
+    idx, curve, _, _ = engine.fps(xyz4, N, 4)  # n = N forces the duplicate fallback
+    for b in range(B):
+        ri, rc, *_ = O.fps(clouds[b], N, 4)
+        np.testing.assert_array_equal(idx[b].cpu().numpy(), ri)
+        np.testing.assert_array_equal(curve[b].cpu().numpy(), rc)
+
+
+def test_fps_loop_resume_dropin():
+    c = generate_cloud("room-surfaces", 3000, 9)
+    x, y, z = O.columns_f64(c)
+    n = 700
+    st = {}
+    for nm, K in (("gpu", GK), ("ora", O.CKernels)):
+        md = np.full(3000, np.inf)
+        tk = np.zeros(3000, np.uint8)
+        out = np.full(n, -1, np.int64)
+        cv = np.full(n, np.inf)
+        out[0] = 17
+        tk[17] = 1
+        e1 = K.fps_loop(x, y, z, md, tk, out, cv, 1, 333)
+        e2 = K.fps_loop(x, y, z, md, tk, out, cv, 333, n)
+        st[nm] = (md, tk, out, cv, e1 + e2)
+    for a, b in zip(st["gpu"], st["ora"]):
+        np.testing.assert_array_equal(a, b)
+
+
+def test_dropin_chunk_and_first_untaken():
+    c = generate_cloud("lattice", 2000, 3)
+    x, y, z = O.columns_f64(c)
+    md_g = np.full(2000, np.inf)
+    md_o = md_g.copy()
+    for (lo, hi, p) in ((0, 2000, 5), (100, 777, 42), (1500, 2000, 1999), (10, 10, 3)):
+        rg = GK.fps_update_chunk(x, y, z, x[p], y[p], z[p], md_g, lo, hi)
+        ro = O.CKernels.fps_update_chunk(x, y, z, x[p], y[p], z[p], md_o, lo, hi)
+        assert rg == ro
+        np.testing.assert_array_equal(md_g, md_o)
+    tk = np.ones(2000, np.uint8)
+    assert GK.first_untaken(tk) == -1
+    tk[1234] = 0
+    tk[1999] = 0
+    assert GK.first_untaken(tk) == 1234
+
+
+# ---- K3a/K3b exclusion lists --------------------------------------------------------
+
+def test_excl_golden(golden):
+    for t in cases(golden, "excl"):
+        k = f"excl/{t}"
+        c = golden[f"cloud/{golden[k + '/cloud']}"]
+        R = list(golden[f"{k}/R"])
+        extra = tuple(golden[f"{k}/extra"])
+        levels = golden[f"{k}/levels"]  # oracle layout: sorted unique r2 levels
+        x, y, z = O.columns_f64(c)
+        indptr, nbr, d2, counts, evals = GK.build_csr(x, y, z, levels)
+        assert indptr[-1] == int(golden[f"{k}/E"])
+        assert evals + len(c) == int(golden[f"{k}/evals"])
+        np.testing.assert_array_equal(digest(indptr, nbr, d2, counts), golden[f"{k}/digest"], err_msg=k)
+
+
+@pytest.mark.parametrize("family,N,R", [("uniform-box", 6000, 0.05), ("room-surfaces", 8000, 0.2),
+                                        ("lattice", 4096, 0.1000001), ("gaussian-clusters", 3000, 0.02)])
+def test_excl_matches_oracle(family, N, R):
+    c = generate_cloud(family, N, 77)
+    e = O.build_exclusion_lists(c, [R, R * 0.8, R * 0.5], (R * 0.6,))
+    x, y, z = O.columns_f64(c)
+    indptr, nbr, d2, counts, _ = GK.build_csr(x, y, z, e.r2_levels)
+    np.testing.assert_array_equal(indptr, e.indptr)
+    np.testing.assert_array_equal(nbr, e.nbr)
+    np.testing.assert_array_equal(d2, e.d2)
+    np.testing.assert_array_equal(counts, e.counts)
+
+
+def test_excl_prefilter_adversarial():
+    # pairs placed at float64 distances straddling r exactly: the float32
+    # pre-filter must never drop a pair whose exact d2 is below r2.
+    rng = np.random.default_rng(1)
+    base = rng.random((400, 3)).astype(np.float32) * 10
+    r = np.float64(0.3)
+    pts = [base]
+    for s in (1 - 1e-7, 1 - 3e-8, 1.0, 1 + 3e-8):
+        off = (rng.normal(size=(400, 3)))
+        off /= np.linalg.norm(off, axis=1, keepdims=True)
+        pts.append((base + (off * r * s)).astype(np.float32))
+    c = np.concatenate(pts)
+    x, y, z = O.columns_f64(c)
+    r2 = [float(r * r)]
+    e_ip, e_nb, e_d2, _ = O.CKernels.excl_build(x, y, z, r2[0])
+    indptr, nbr, d2, counts, _ = GK.build_csr(x, y, z, r2)
+    np.testing.assert_array_equal(indptr, e_ip)
+    np.testing.assert_array_equal(nbr, e_nb)
+    np.testing.assert_array_equal(d2, e_d2)
+
+
+def test_dropin_collect_fill_sort_counts():
+    c = generate_cloud("uniform-box", 1500, 8)
+    x, y, z = O.columns_f64(c)
+    r2 = 0.09 ** 2
+    N = 1500
+    T = (N + 1) // 2
+    ei, ej, ed, ev = GK.excl_collect(x, y, z, 0, T, r2, 1024)
+    # reference order/semantics restated: rows (k, N-1-k), j ascending
+    e = O.build_exclusion_lists(c, [0.09])
+    deg = np.ones(N, np.int64)
+    np.add.at(deg, ei, 1)
+    np.add.at(deg, ej, 1)
+    indptr = np.zeros(N + 1, np.int64)
+    np.cumsum(deg, out=indptr[1:])
+    nbr = np.empty(indptr[-1], np.int64)
+    d2 = np.empty(indptr[-1], np.float64)
+    GK.csr_fill(ei, ej, ed, indptr, nbr, d2)
+    GK.csr_sort_rows(indptr, d2, nbr)
+    np.testing.assert_array_equal(indptr, e.indptr)
+    np.testing.assert_array_equal(nbr, e.nbr)
+    np.testing.assert_array_equal(d2, e.d2)
+    assert ev == N * (N - 1) // 2
+    np.testing.assert_array_equal(GK.csr_level_counts(indptr, d2, e.r2_levels), e.counts)
+
+
+# ---- K2/K3c/K3d full FastPoint pipeline --------------------------------------------
+
+def test_mdps_golden(golden):
+    for t in cases(golden, "mdps"):
+        k = f"mdps/{t}"
+        c = golden[f"cloud/{golden[k + '/cloud']}"]
+        n = int(golden[f"{k}/n"])
+        kw = mdps_kwargs(golden, t)
+        fp = gpu_mdps(c, n, **kw)
+        np.testing.assert_array_equal(fp.out[0].cpu().numpy(), golden[f"{k}/idx"], err_msg=k)
+        assert int(fp.reached.item()) == int(golden[f"{k}/reached"]), k
+        assert bool(fp.exhausted.item()) == bool(golden[f"{k}/exhausted"]), k
+        assert int(fp.entered.item()) == int(golden[f"{k}/entered"]), k
+        st = int(np.int64(fp.state.item()).view(np.uint64))
+        assert st == int(golden[f"{k}/state"]), k
+        np.testing.assert_array_equal(fp.R[0].cpu().numpy(), golden[f"{k}/R"], err_msg=k)
+        assert fp.pair_evals()[0] == int(golden[f"{k}/evals"]), k
+
+
+@pytest.mark.parametrize("B,N,n,family,nseg,pick", [
+    (4, 4096, 1024, "uniform-box", 6, False), (3, 3000, 750, "room-surfaces", 6, True),
+    (2, 24000, 6000, "room-surfaces", 6, False), (2, 5000, 1250, "lattice", 4, False),
+    (1, 40000, 10000, "uniform-box", 6, False),  # global-memory sampler workspace
+])
+def test_mdps_batched_matches_oracle(B, N, n, family, nseg, pick):
+    clouds = np.stack([generate_cloud(family, N, 1000 + b) for b in range(B)])
+    e = 0.42
+    fp = engine.FastPoint(B, N, n, nseg=nseg, exponent=e, extra_radii=(0.1,), pick_lowest=pick)
+    fp.set_points(torch.from_numpy(clouds).cuda())
+    fp.set_rng([7 + b for b in range(B)])
+    fp.sample()
+    fp.check()
+    gi, gd, gc = fp.group_rf(0.1, 32)
+    for b in range(B):
+        ref = O.mdps(clouds[b], n, nseg=nseg, exponent=e, rng_seed=7 + b, extra_radii=(0.1,), pick_lowest=pick)
+        np.testing.assert_array_equal(fp.out[b].cpu().numpy(), ref.indices, err_msg=f"cloud {b}")
+        assert int(fp.reached[b].item()) == ref.reached
+        assert int(np.int64(fp.state[b].item()).view(np.uint64)) == ref.rng_state
+        oi, od, oc = O.rf_ball_query(ref.excl, 0.1, ref.indices, 32)
+        np.testing.assert_array_equal(gi[b].cpu().numpy().astype(np.int64), oi)
+        np.testing.assert_array_equal(gd[b].cpu().numpy(), od)
+        np.testing.assert_array_equal(gc[b].cpu().numpy().astype(np.int64), oc)
+
+
+def test_dropin_sampler_and_earlyterm():
+    c = generate_cloud("uniform-box", 2500, 4)
+    e = O.build_exclusion_lists(c, [0.09, 0.07, 0.06], ())
+    prefix = O.fps(c, 60)[0]
+    bnd = O.sampler_boundaries(600, 3)
+    for pick in (False, True):
+        for seed in (0, 123456789):
+            g = GK.sample_predicted(e.indptr, e.nbr, e.counts, e.seg_level_rows, bnd, prefix, 600, 2500,
+                                    np.uint64(seed), pick)
+            o = O.CKernels.sample_predicted(e.indptr, e.nbr, e.counts, e.seg_level_rows, bnd, prefix, 600, 2500,
+                                            np.uint64(seed), pick)
+            np.testing.assert_array_equal(g[0], o[0])
+            assert g[1:] == o[1:]
+    taken = np.zeros(2500, np.uint8)
+    taken[::5] = 1
+    md_g = np.full(2500, np.inf)
+    md_o = md_g.copy()
+    lv = np.ascontiguousarray(e.counts[e.seg_level_rows[0]])
+    GK.earlyterm_scan(e.indptr, e.nbr, e.d2, lv, taken, md_g, 0, 2500)
+    O.CKernels.earlyterm_scan(e.indptr, e.nbr, e.d2, lv, taken, md_o, 0, 2500)
+    np.testing.assert_array_equal(md_g, md_o)
+
+
+def test_mdps_cuda_graph_replay_identical():
+    B, N, n = 2, 4096, 1024
+    clouds = np.stack([generate_cloud("uniform-box", N, 50 + b) for b in range(B)])
+    fp = engine.FastPoint(B, N, n, exponent=0.4, extra_radii=(0.05,))
+    fp.set_points(torch.from_numpy(clouds).cuda())
+    fp.set_rng([1, 2])
+    fp.sample()
+    first = fp.out.clone()
+    fp.capture()
+    for _ in range(3):
+        fp.set_rng([1, 2])
+        fp.out.fill_(-7)
+        fp.sample()
+        torch.cuda.synchronize()
+        assert torch.equal(fp.out, first)
+
+
+# ---- K4 grouping and K6 quality ------------------------------------------------------
+
+def test_ball_query_naive_and_rf_equal_oracle():
+    c = generate_cloud("room-surfaces", 6000, 21)
+    cent = O.fps(c, 1500)[0]
+    for r, k in ((0.1, 32), (0.25, 64), (0.05, 1)):
+        oi, od, oc = O.ball_query_naive(c, cent, r, k)
+        xyz4 = engine.as_xyz4(c)
+        gi, gd, gc = engine.ball_query_naive(xyz4, torch.from_numpy(cent).cuda().reshape(1, -1), r, k)
+        np.testing.assert_array_equal(gi[0].cpu().numpy().astype(np.int64), oi)
+        np.testing.assert_array_equal(gd[0].cpu().numpy(), od)
+        np.testing.assert_array_equal(gc[0].cpu().numpy().astype(np.int64), oc)
+        e = O.build_exclusion_lists(c, [r * 0.5], (r,))
+        ri, rd, rc = O.rf_ball_query(e, r, cent, k)
+        np.testing.assert_array_equal(ri, oi)  # RF == naive (A2)
+
+
+def test_knn_naive_and_rf():
+    c = generate_cloud("uniform-box", 4000, 31)
+    n = 1000
+    fp = gpu_mdps(c, n, exponent=0.4)
+    pool = fp.out[0].cpu().numpy()
+    queries = np.arange(4000)
+    for k in (1, 3, 16):
+        oi, od, oc = O.knn_naive(c, queries, pool, k)
+        xyz4 = engine.as_xyz4(c)
+        gi, gd, gc = engine.knn_naive(xyz4, fp.out, k)
+        np.testing.assert_array_equal(gi[0].cpu().numpy().astype(np.int64), oi)
+        np.testing.assert_array_equal(gd[0].cpu().numpy(), od)
+        ri, rd, rc, fb = fp.knn_rf(k)
+        np.testing.assert_array_equal(ri[0].cpu().numpy().astype(np.int64), oi)
+        np.testing.assert_array_equal(rd[0].cpu().numpy(), od)
+    assert int(fb[0].item()) > 0  # k = 16 forces fallbacks
+
+
+def test_min_spacing_tolerance():
+    c = generate_cloud("uniform-box", 5000, 41)
+    s = O.fps(c, 1200)[0]
+    ref_d2 = O.min_spacing_d2(c, s)
+    xyz4 = engine.as_xyz4(c)
+    got = engine.min_spacing_d2(xyz4, torch.from_numpy(s).cuda().reshape(1, -1))[0].cpu().numpy()
+    np.testing.assert_array_equal(got, ref_d2)  # per-sample minima: exact
+    from paper_2507_23480_b200 import quality
+    v = quality.avg_min_spacing(c, s)
+    assert abs(v - O.avg_min_spacing(c, s)) <= 1e-12 * abs(v)  # mean: reduction order only
+
+
+def test_errors_are_value_errors():
+    with pytest.raises(ValueError):
+        engine.FastPoint(1, 100, 10, exponent=None)
+    with pytest.raises(ValueError):
+        engine.fps(engine.as_xyz4(np.zeros((5, 3), np.float32)), 6)
+    fp = gpu_mdps(generate_cloud("uniform-box", 500, 1), 100, exponent=0.4, extra_radii=(0.1,))
+    with pytest.raises(ValueError, match="not baked"):
+        fp.group_rf(0.2, 8)
