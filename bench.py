@@ -1,0 +1,395 @@
+"""Benchmark: FastPoint sampling + grouping at N=24k on B200 (BASELINE.json
+metric "sampled pts/sec & us/cloud for FPS+ball-query at N=24k, 1-8 B200").
+
+Workload (BASELINE.json configs[2], "C3"): per GPU a batch of B=8 synthetic
+room-surface clouds (6 x 5 x 3 m, S3DIS-shape), N = 24000, stride 4 ->
+n = 6000 samples, FastPoint p = 0.1, nseg = 6, power-law estimator (exponent
+fitted offline on held-out clouds), then redundancy-free ball query r = 0.1 m,
+k = 32 from the cached distances.  One step = one pass of that path over the
+batch.  The exact-FPS + naive-ball-query B200 path is timed beside it.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1: launched by torch.distributed.run; each rank samples its own batch
+(batch sharding, no data-path collective; "scaling": "weak").
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+import numpy as np  # noqa: E402
+
+B_PER_GPU, N, STRIDE = 8, 24000, 4
+n_SAMPLES = N // STRIDE
+P, NSEG, RADIUS, K = 0.1, 6, 0.1, 32
+FAMILY = "room-surfaces"
+METRIC = "sampled pts/sec & us/cloud for FPS+ball-query at N=24k, 1-8 B200"
+UNIT = "sampled pts/s"
+WORKLOAD = ("C3 PointNeXt-L S3DIS-shape: B=8 clouds/GPU, N=24000 -> n=6000 (stride 4), FastPoint "
+            "(p=0.1, nseg=6, power estimator) + rf ball_query r=0.1 k=32")
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def clouds_for(rank: int, B: int):
+    from paper_2507_23480_b200.harness import generate_cloud
+
+    return np.stack([generate_cloud(FAMILY, N, 1000 * 3 + rank * B + b) for b in range(B)])
+
+
+def heldout_exponent():
+    """Offline exponent fit on 2 held-out clouds of the
+    family, from exact GPU FPS curves -- outside every timed region."""
+    import torch
+
+    from paper_2507_23480_b200 import curve, engine
+    from paper_2507_23480_b200.harness import generate_cloud
+
+    held = np.stack([generate_cloud(FAMILY, N, 99000 + i) for i in range(2)])
+    _, cv, _, _ = engine.fps(engine.as_xyz4(torch.from_numpy(held).cuda()), n_SAMPLES)
+    return curve.fit_power_exponent(cv.cpu().numpy())
+
+
+def heldout_exponent_cpu():
+    """Same offline fit as heldout_exponent(), from the CPU oracle's exact FPS
+    curves (bit-identical to the GPU's), for the reference arm."""
+    from oracle import oracle as O
+    from paper_2507_23480_b200 import curve
+    from paper_2507_23480_b200.harness import generate_cloud
+
+    curves = [O.fps(generate_cloud(FAMILY, N, 99000 + i), n_SAMPLES)[1] for i in range(2)]
+    return curve.fit_power_exponent(curves)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons, util = [], None, set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                s, m, u = float(f[0]), float(f[1]), float(f[6])
+            except ValueError:
+                continue
+            mx = m
+            util.append(u)
+            sm.append(s)
+            for nm, v in zip(names, f[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        loaded = [s for s, u in zip(sm, util) if u > 0] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
+    except OSError:
+        return {}
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference's CPU path (oracle port) on the host cores
+
+
+def cpu_run(clouds, exponent, threads):
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle as O
+
+    def one(b):
+        r = O.mdps(clouds[b], n_SAMPLES, p=P, nseg=NSEG, estimator="power", exponent=exponent, rng_seed=b,
+                   extra_radii=(RADIUS,))
+        O.rf_ball_query(r.excl, RADIUS, r.indices, K)
+        return r.indices
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        out = list(ex.map(one, range(clouds.shape[0])))
+    return time.perf_counter() - t0, out
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    clouds = clouds_for(0, B_PER_GPU)
+    exponent = heldout_exponent_cpu()
+    threads = min(os.cpu_count() or 1, B_PER_GPU)
+    for _ in range(max(args.warmup, 0)):
+        cpu_run(clouds[:1], exponent, 1)
+    times = []
+    for _ in range(args.steps):
+        dt, _ = cpu_run(clouds, exponent, threads)
+        times.append(dt)
+    t = sum(times)
+    value = B_PER_GPU * n_SAMPLES * args.steps / t
+    sample = f"{B_PER_GPU} clouds x (FastPoint + rf ball query) per step, one cloud per thread"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "family": FAMILY, "B": B_PER_GPU, "N": N, "n": n_SAMPLES},
+            "us_per_cloud": 1e6 * t / (args.steps * B_PER_GPU),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+
+def main_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_23480_b200 import _lib, engine
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    B = B_PER_GPU
+    clouds = clouds_for(rank, B)
+    exponent = heldout_exponent()
+
+    fp = engine.FastPoint(B, N, n_SAMPLES, p=P, nseg=NSEG, estimator="power", exponent=exponent,
+                          extra_radii=(RADIUS,), device=dev)
+    d_pts = torch.from_numpy(clouds).to(dev)
+    fp.set_points(d_pts)
+    seeds = [rank * B + b for b in range(B)]
+    grp = (torch.empty(B, n_SAMPLES, K, dtype=torch.int32, device=dev),
+           torch.empty(B, n_SAMPLES, K, dtype=torch.float64, device=dev),
+           torch.empty(B, n_SAMPLES, dtype=torch.int32, device=dev))
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(events=None):
+        fp.state.copy_(seed_t)
+        if events is None:
+            fp.sample()
+            fp.group_rf(RADIUS, K, out=grp)
+            return
+        events[0].record(stream)
+        fp._prefix()
+        events[1].record(stream)
+        fp._thresholds()
+        events[2].record(stream)
+        fp._exclusion()
+        events[3].record(stream)
+        fp._sampler()
+        events[4].record(stream)
+        fp._early_termination()
+        events[5].record(stream)
+        fp.group_rf(RADIUS, K, out=grp)
+        events[6].record(stream)
+
+    seed_t = torch.tensor(seeds, dtype=torch.int64, device=dev)
+    # warm-up (also grows CSR capacity if ever needed)
+    for _ in range(max(args.warmup, 3)):
+        step()
+    fp.check()
+    torch.cuda.synchronize()
+
+    stages = ["fps_prefix", "thresholds", "excl_build", "sampler", "early_term", "rf_ball_query"]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in range(args.steps)]
+    launches0 = _lib.launch_count()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for s in range(args.steps):
+            flush.zero_()  # L2 flush between steps (untimed: outside the events)
+            step(ev[s])
+        torch.cuda.synchronize()
+    launches = _lib.launch_count() - launches0
+    if ws > 1:
+        dist.barrier()
+    stage_ms = np.array([[ev[s][i].elapsed_time(ev[s][i + 1]) for i in range(6)] for s in range(args.steps)])
+    t_ms = float(stage_ms.sum())
+    if ws > 1:
+        tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    value = ws * B * n_SAMPLES * args.steps / (t_ms / 1e3)
+    per_stage = {nm: float(stage_ms[:, i].mean()) for i, nm in enumerate(stages)}
+
+    # parity spot check of this run (first cloud) is in tests/; here: sanity
+    reached = fp.reached.cpu().numpy()
+
+    # ---- exact-FPS + naive ball query comparator on the same batch -------------
+    for _ in range(2):
+        idx, _, _, _ = engine.fps(fp.xyz4, n_SAMPLES)
+        engine.ball_query_naive(fp.xyz4, idx, RADIUS, K)
+    torch.cuda.synchronize()
+    fps_ms, bqn_ms = [], []
+    for s in range(args.steps):
+        flush.zero_()
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record(stream)
+        idx, _, _, _ = engine.fps(fp.xyz4, n_SAMPLES)
+        e1.record(stream)
+        engine.ball_query_naive(fp.xyz4, idx, RADIUS, K)
+        e2.record(stream)
+        torch.cuda.synchronize()
+        fps_ms.append(e0.elapsed_time(e1))
+        bqn_ms.append(e1.elapsed_time(e2))
+    exact_ms = (sum(fps_ms) + sum(bqn_ms)) / args.steps
+
+    # ---- end to end through the public API: pinned host in, results out ---------
+    host_in = torch.from_numpy(clouds).pin_memory()
+    host_idx = torch.empty(B, n_SAMPLES, dtype=torch.int64).pin_memory()
+    host_grp = torch.empty(B, n_SAMPLES, K, dtype=torch.int32).pin_memory()
+    h2d = host_in.numel() * 4
+    d2h = host_idx.numel() * 8 + host_grp.numel() * 4
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e2e_ms = 0.0
+    for s in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        d_pts.copy_(host_in, non_blocking=True)
+        fp.set_points(d_pts)
+        step()
+        host_idx.copy_(fp.out, non_blocking=True)
+        host_grp.copy_(grp[0], non_blocking=True)
+        b_.record(stream)
+        b_.synchronize()
+        e2e_ms += a.elapsed_time(b_)
+    if ws > 1:
+        tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_value = ws * B * n_SAMPLES * args.steps / (e2e_ms / 1e3)
+
+    # ---- roofline for the dominant kernel ------------------------------------------
+    pk = peaks()
+    hbm = pk.get("hbm_gbs", 6650.0)
+    dom = max(per_stage, key=per_stage.get)
+    k0 = fp.k0
+    E = int(fp.csr.indptr[:, -1].sum().item())
+    alg = {  # algorithmic bytes per launch
+        "fps_prefix": 28.0 * N * (k0 - 1) * B,
+        "excl_build": 36.0 * E + 4.0 * N * fp.L * B + 12.0 * N * B,
+        "sampler": 4.0 * E + 4.0 * N * fp.L * B,
+        "early_term": 28.0 * N * float(np.sum(n_SAMPLES - reached)) + 12.0 * E,
+        "rf_ball_query": 24.0 * n_SAMPLES * K * B,
+        "thresholds": 8.0 * n_SAMPLES * B,
+    }
+    achieved = alg[dom] / (per_stage[dom] / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": None,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback 6.65 TB/s"}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        threads = min(os.cpu_count() or 1, B)
+        dt, cpu_idx = cpu_run(clouds, exponent, threads)
+        match = all(np.array_equal(cpu_idx[b], fp.out[b].cpu().numpy()) for b in range(B)) if \
+            int(seed_t[0].item()) == 0 else None
+        cpu = {"value": B * n_SAMPLES / dt, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{B} clouds (the rank-0 batch) FastPoint + rf ball query, one cloud per thread",
+               "seconds": dt, "indices_bit_exact_vs_gpu": match}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "family": FAMILY, "B_per_gpu": B, "global_batch": B * ws, "N": N,
+                       "n": n_SAMPLES, "p": P, "nseg": NSEG, "radius": RADIUS, "k": K,
+                       "exponent": round(exponent, 6), "parallelism": f"batch-shard x{ws}",
+                       "l2": "flushed between timed steps (512 MiB memset, untimed)"},
+            "us_per_cloud": 1e3 * t_ms / (args.steps * B),
+            "stage_ms": per_stage,
+            "exact_fps_path": {"ms_per_step": exact_ms, "fps_ms": float(np.mean(fps_ms)),
+                               "ball_query_naive_ms": float(np.mean(bqn_ms)),
+                               "value": ws * B * n_SAMPLES / (exact_ms / 1e3),
+                               "us_per_cloud": 1e3 * exact_ms / B},
+            "speedup_vs_exact_fps": exact_ms / (t_ms / args.steps),
+            "early_term_iters_mean": float(np.mean(n_SAMPLES - reached)),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": e2e_ms / args.steps},
+            "gpu_launches": int(launches),
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return main_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())
