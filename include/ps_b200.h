@@ -94,12 +94,18 @@ PS_API int ps_first_untaken(const uint8_t* taken, int64_t N, int64_t* out, void*
  * undirected edges per cloud and cap_entries the CSR entries per cloud
  * (< 2^31).  status int32[B] receives bit0 = edge overflow, bit1 = entry
  * overflow; an overflowed cloud's CSR is incomplete and must be rebuilt with
- * larger capacities. */
-PS_API int64_t ps_excl_workspace_bytes(int64_t B, int64_t N, int64_t cap_edges);
+ * larger capacities.  method 0 enumerates the i<j triangle (each pair
+ * evaluated once, the reference's accounting SPEC.md:438); method 1 enumerates
+ * candidates from a uniform grid of cell width >= R_max (cap_edges unused) --
+ * the CSR is byte-identical, only the number of evaluations differs. */
+PS_API int64_t ps_excl_workspace_bytes(int64_t B, int64_t N, int64_t cap_edges, int32_t method);
+/* Byte offset, inside a method-1 workspace, of the uint64[B] count of
+ * candidate pairs the grid build evaluated (pair_evals accounting). */
+PS_API int64_t ps_excl_grid_evals_offset(int64_t B, int64_t N);
 PS_API int ps_excl_build(const float* xyz4, int64_t B, int64_t N, const double* r2_levels, int32_t L,
                   int64_t levels_ld, int64_t* indptr, int32_t* nbr, double* d2, int32_t* counts,
                   int64_t cap_entries, void* work, int64_t cap_edges, int32_t* status,
-                  void* stream);
+                  int32_t method, void* stream);
 
 /* csr_sort_rows (_kernels.py:188-219): order every row by (d2, index) in
  * place.  work: >= 256 + 4*B*N bytes. */

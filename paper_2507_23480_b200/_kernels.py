@@ -97,7 +97,7 @@ def first_untaken(taken):
 # ---- exclusion lists (_kernels.py:111-234) --------------------------------------
 
 
-def build_csr(x, y, z, r2_levels, cap_entries=None):
+def build_csr(x, y, z, r2_levels, cap_entries=None, method=0):
     """Fused device build: (indptr int64[N+1], nbr int64[E], d2 float64[E],
     counts int64[L, N], evals).  The unit the reference orchestrator forms
     from excl_collect + csr_fill + csr_sort_rows + csr_level_counts."""
@@ -109,7 +109,7 @@ def build_csr(x, y, z, r2_levels, cap_entries=None):
     xyz4 = _xyz4(x, y, z)
     cap = N * min(N, 128) if cap_entries is None else int(cap_entries)
     while True:
-        csr = DeviceCsr.allocate(1, N, L, cap, cap // 2 + 1, xyz4.device)
+        csr = DeviceCsr.allocate(1, N, L, cap, cap // 2 + 1, xyz4.device, method)
         csr.levels.copy_(torch.from_numpy(lv))
         csr.build(xyz4)
         if not csr.overflowed():

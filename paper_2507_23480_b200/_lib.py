@@ -31,8 +31,10 @@ _SIGS = {
     "ps_fps": (_c_i32, [_p, _c_i64, _c_i64, _p, _p, _p, _p, _c_i64, _c_i64, _c_i64, _p, _p]),
     "ps_fps_update_chunk": (_c_i32, [_p, _c_i64, _c_f64, _c_f64, _c_f64, _p, _c_i64, _c_i64, _p, _p, _p]),
     "ps_first_untaken": (_c_i32, [_p, _c_i64, _p, _p]),
-    "ps_excl_workspace_bytes": (_c_i64, [_c_i64, _c_i64, _c_i64]),
-    "ps_excl_build": (_c_i32, [_p, _c_i64, _c_i64, _p, _c_i32, _c_i64, _p, _p, _p, _p, _c_i64, _p, _c_i64, _p, _p]),
+    "ps_excl_workspace_bytes": (_c_i64, [_c_i64, _c_i64, _c_i64, _c_i32]),
+    "ps_excl_grid_evals_offset": (_c_i64, [_c_i64, _c_i64]),
+    "ps_excl_build": (_c_i32, [_p, _c_i64, _c_i64, _p, _c_i32, _c_i64, _p, _p, _p, _p, _c_i64, _p, _c_i64, _p, _c_i32,
+                               _p]),
     "ps_csr_sort_rows": (_c_i32, [_p, _p, _p, _c_i64, _c_i64, _c_i64, _p, _p]),
     "ps_level_counts": (_c_i32, [_p, _p, _c_i64, _c_i64, _c_i64, _p, _c_i32, _c_i64, _p, _p]),
     "ps_thresholds": (_c_i32, [_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_i32, _p, _c_i32, _p, _p, _c_i64, _p,

@@ -140,39 +140,79 @@ int ps_first_untaken(const uint8_t* taken, int64_t N, int64_t* out, void* stream
 
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
-int64_t ps_excl_workspace_bytes(int64_t B, int64_t N, int64_t cap_edges) {
+static int grid_max_cells(int64_t N) {
+    const int64_t c = 4 * N + 64;
+    return (int)(c < ((int64_t)1 << 24) ? c : ((int64_t)1 << 24));
+}
+
+int64_t ps_excl_workspace_bytes(int64_t B, int64_t N, int64_t cap_edges, int32_t method) {
     size_t s = 0;
-    s += align_up(sizeof(uint32_t) * B * cap_edges) * 2;
-    s += align_up(sizeof(double) * B * cap_edges);
-    s += align_up(sizeof(unsigned long long) * B);
+    if (method == 0) {
+        s += align_up(sizeof(uint32_t) * B * cap_edges) * 2;
+        s += align_up(sizeof(double) * B * cap_edges);
+        s += align_up(sizeof(unsigned long long) * B);
+    } else {
+        const int64_t mc = grid_max_cells(N);
+        s += align_up(sizeof(ps::GridParams) * B);
+        s += align_up(sizeof(int) * B * (mc + 1));
+        s += align_up(sizeof(int) * B * mc);
+        s += align_up(sizeof(int32_t) * B * N) * 2;
+        s += align_up(sizeof(float4) * B * N);
+        s += align_up(sizeof(unsigned long long) * B);
+    }
     s += align_up(sizeof(int32_t) * B * N) * 2;
     s += align_up(sizeof(unsigned));
     return (int64_t)s;
 }
 
+int64_t ps_excl_grid_evals_offset(int64_t B, int64_t N) {
+    const int64_t mc = grid_max_cells(N);
+    size_t s = 0;
+    s += align_up(sizeof(ps::GridParams) * B);
+    s += align_up(sizeof(int) * B * (mc + 1));
+    s += align_up(sizeof(int) * B * mc);
+    s += align_up(sizeof(int32_t) * B * N) * 2;
+    s += align_up(sizeof(float4) * B * N);
+    return (int64_t)s;
+}
+
 int ps_excl_build(const float* xyz4, int64_t B, int64_t N, const double* r2_levels, int32_t L, int64_t levels_ld,
                   int64_t* indptr, int32_t* nbr, double* d2, int32_t* counts, int64_t cap_entries, void* work,
-                  int64_t cap_edges, int32_t* status, void* stream) {
+                  int64_t cap_edges, int32_t* status, int32_t method, void* stream) {
     CHECK_ARG(B >= 1 && N >= 1 && N <= kMaxN, "invalid batch shape");
     CHECK_ARG(L >= 1 && L <= levels_ld, "invalid level count %d", L);
     CHECK_ARG(cap_entries >= N && cap_entries < ((int64_t)1 << 31), "cap_entries must be in [N, 2^31)");
     CHECK_ARG(cap_edges >= 1, "cap_edges must be >= 1");
+    CHECK_ARG(method == 0 || method == 1, "method must be 0 (brute force) or 1 (grid)");
     CHECK_ARG(work && status && indptr && nbr && d2 && counts, "null pointer");
     unsigned char* w = static_cast<unsigned char*>(work);
     ps::ExclWork ew = {};
+    ps::GridWork gw = {};
     ew.cap_edges = cap_edges;
-    ew.edge_i = reinterpret_cast<uint32_t*>(w); w += align_up(sizeof(uint32_t) * B * cap_edges);
-    ew.edge_j = reinterpret_cast<uint32_t*>(w); w += align_up(sizeof(uint32_t) * B * cap_edges);
-    ew.edge_d2 = reinterpret_cast<double*>(w); w += align_up(sizeof(double) * B * cap_edges);
-    ew.edge_count = reinterpret_cast<unsigned long long*>(w); w += align_up(sizeof(unsigned long long) * B);
+    if (method == 0) {
+        ew.edge_i = reinterpret_cast<uint32_t*>(w); w += align_up(sizeof(uint32_t) * B * cap_edges);
+        ew.edge_j = reinterpret_cast<uint32_t*>(w); w += align_up(sizeof(uint32_t) * B * cap_edges);
+        ew.edge_d2 = reinterpret_cast<double*>(w); w += align_up(sizeof(double) * B * cap_edges);
+        ew.edge_count = reinterpret_cast<unsigned long long*>(w); w += align_up(sizeof(unsigned long long) * B);
+    } else {
+        const int64_t mc = grid_max_cells(N);
+        gw.max_cells = (int)mc;
+        gw.params = reinterpret_cast<ps::GridParams*>(w); w += align_up(sizeof(ps::GridParams) * B);
+        gw.cell_start = reinterpret_cast<int*>(w); w += align_up(sizeof(int) * B * (mc + 1));
+        gw.cursor = reinterpret_cast<int*>(w); w += align_up(sizeof(int) * B * mc);
+        gw.cell_of = reinterpret_cast<int32_t*>(w); w += align_up(sizeof(int32_t) * B * N);
+        gw.sorted_idx = reinterpret_cast<int32_t*>(w); w += align_up(sizeof(int32_t) * B * N);
+        gw.sorted_xyz = reinterpret_cast<float4*>(w); w += align_up(sizeof(float4) * B * N);
+        gw.evals = reinterpret_cast<unsigned long long*>(w); w += align_up(sizeof(unsigned long long) * B);
+    }
     ew.deg = reinterpret_cast<int32_t*>(w); w += align_up(sizeof(int32_t) * B * N);
     ew.long_rows = reinterpret_cast<int32_t*>(w); w += align_up(sizeof(int32_t) * B * N);
     ew.long_count = reinterpret_cast<unsigned*>(w);
     ew.status = status;
     ps::CsrView csr = {indptr, nbr, d2, counts, cap_entries, N, L};
     return cuda_status(ps::launch_excl_build(reinterpret_cast<const float4*>(xyz4), B, N, r2_levels, L, levels_ld,
-                                             csr, ew, S(stream)),
-                       "excl_build", 6);
+                                             csr, ew, gw, method, S(stream)),
+                       "excl_build", method == 0 ? 6 : 9);
 }
 
 int ps_csr_sort_rows(int64_t* indptr, int32_t* nbr, double* d2, int64_t cap_entries, int64_t B, int64_t N,

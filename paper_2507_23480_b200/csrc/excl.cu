@@ -144,7 +144,7 @@ __global__ void excl_degree_kernel(int64_t N, ExclWork w) {
 }
 
 // One CTA per cloud: indptr = exclusive scan of (deg + 1); deg <- indptr (cursor).
-__global__ void __launch_bounds__(1024) excl_scan_kernel(int64_t N, ExclWork w, CsrView csr) {
+__global__ void __launch_bounds__(1024) excl_scan_kernel(int64_t N, ExclWork w, CsrView csr, int add_self) {
     __shared__ int64_t warp_sums[32];
     __shared__ int64_t carry;
     const int64_t b = blockIdx.x;
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(1024) excl_scan_kernel(int64_t N, ExclWork w, 
     __syncthreads();
     for (int64_t base = 0; base < N; base += 1024) {
         const int64_t i = base + tid;
-        const int64_t v = i < N ? (int64_t)deg[i] + 1 : 0;
+        const int64_t v = i < N ? (int64_t)deg[i] + add_self : 0;
         int64_t x = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -214,6 +214,207 @@ __global__ void excl_fill_kernel(int64_t N, ExclWork w, CsrView csr) {
     }
 }
 
+
+// ---- uniform-grid candidate enumeration ---------------------------------------
+// Cell width h >= R_max * (1 + 1e-6): two points closer than R_max can only lie
+// in the same or adjacent cells, so scanning the 27-cell neighbourhood visits
+// every pair the brute-force triangle would accept; the CSR after the
+// (d2, index) row sort is byte-identical.  Evaluation count drops from
+// N(N-1)/2 to the neighbourhood candidates (reported in grid evals).
+
+__global__ void __launch_bounds__(1024) grid_setup_kernel(const float4* __restrict__ xyz, int64_t N,
+                                                          const double* __restrict__ r2_levels, int L,
+                                                          int64_t levels_ld, GridWork g) {
+    __shared__ float red[6][32];
+    const int64_t b = blockIdx.x;
+    const float4* cx = xyz + b * N;
+    float mn[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, mx[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
+    for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
+        const float4 p = cx[i];
+        mn[0] = fminf(mn[0], p.x); mn[1] = fminf(mn[1], p.y); mn[2] = fminf(mn[2], p.z);
+        mx[0] = fmaxf(mx[0], p.x); mx[1] = fmaxf(mx[1], p.y); mx[2] = fmaxf(mx[2], p.z);
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        for (int o = 16; o > 0; o >>= 1) {
+            mn[a] = fminf(mn[a], __shfl_xor_sync(kFull, mn[a], o));
+            mx[a] = fmaxf(mx[a], __shfl_xor_sync(kFull, mx[a], o));
+        }
+        if (lane == 0) { red[a][warp] = mn[a]; red[3 + a][warp] = mx[a]; }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int nw = blockDim.x >> 5;
+        double lo[3], ext[3];
+        for (int a = 0; a < 3; ++a) {
+            float m0 = FLT_MAX, m1 = -FLT_MAX;
+            for (int q = 0; q < nw; ++q) { m0 = fminf(m0, red[a][q]); m1 = fmaxf(m1, red[3 + a][q]); }
+            lo[a] = m0;
+            ext[a] = (double)m1 - (double)m0;
+        }
+        double r2 = 0.0;
+        for (int l = 0; l < L; ++l) r2 = fmax(r2, r2_levels[b * levels_ld + l]);
+        double h = sqrt(r2) * (1.0 + 1e-6);
+        if (!(h > 1e-30)) h = 1e-30;
+        int n[3];
+        for (int it = 0; it < 64; ++it) {
+            double tot = 1.0;
+            for (int a = 0; a < 3; ++a) {
+                const double c = floor(ext[a] / h) + 1.0;
+                n[a] = c > 1048576.0 ? 1048576 : (int)c;
+                tot *= (double)n[a];
+            }
+            if (tot <= (double)g.max_cells) break;
+            h *= cbrt(tot / (double)g.max_cells) * 1.001;
+        }
+        GridParams gp;
+        gp.ox = lo[0]; gp.oy = lo[1]; gp.oz = lo[2];
+        gp.inv_h = 1.0 / h;
+        gp.nx = n[0]; gp.ny = n[1]; gp.nz = n[2];
+        gp.ncells = n[0] * n[1] * n[2];
+        g.params[b] = gp;
+    }
+}
+
+__device__ __forceinline__ int cell_coord(double v, double o, double inv_h, int n) {
+    int c = (int)floor((v - o) * inv_h);
+    return c < 0 ? 0 : (c >= n ? n - 1 : c);
+}
+
+__global__ void grid_assign_kernel(const float4* __restrict__ xyz, int64_t B, int64_t N, GridWork g) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < B * N;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = t / N;
+        const GridParams gp = g.params[b];
+        const float4 p = xyz[t];
+        const int cx = cell_coord(p.x, gp.ox, gp.inv_h, gp.nx);
+        const int cy = cell_coord(p.y, gp.oy, gp.inv_h, gp.ny);
+        const int cz = cell_coord(p.z, gp.oz, gp.inv_h, gp.nz);
+        const int c = (cz * gp.ny + cy) * gp.nx + cx;
+        g.cell_of[t] = c;
+        atomicAdd(&g.cell_start[b * (g.max_cells + 1) + c], 1);
+    }
+}
+
+// per cloud: cell_start <- exclusive scan of counts; cursor <- copy
+__global__ void __launch_bounds__(1024) grid_scan_kernel(int64_t N, GridWork g) {
+    __shared__ int warp_sums[32];
+    __shared__ int carry;
+    const int64_t b = blockIdx.x;
+    const int nc = g.params[b].ncells;
+    int* cs = g.cell_start + b * (g.max_cells + 1);
+    int* cur = g.cursor + b * (int64_t)g.max_cells;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < nc; base += 1024) {
+        const int i = base + tid;
+        const int v = i < nc ? cs[i] : 0;
+        int x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) warp_sums[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            int s = warp_sums[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(kFull, s, o);
+                if (lane >= o) s += y;
+            }
+            warp_sums[lane] = s;
+        }
+        __syncthreads();
+        const int ex = carry + (warp ? warp_sums[warp - 1] : 0) + x - v;
+        if (i < nc) { cs[i] = ex; cur[i] = ex; }
+        __syncthreads();
+        if (tid == 0) carry += warp_sums[31];
+        __syncthreads();
+    }
+    if (tid == 0) cs[nc] = carry;
+}
+
+__global__ void grid_scatter_kernel(const float4* __restrict__ xyz, int64_t B, int64_t N, GridWork g) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < B * N;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = t / N;
+        const int c = g.cell_of[t];
+        const int pos = atomicAdd(&g.cursor[b * (int64_t)g.max_cells + c], 1);
+        g.sorted_idx[b * N + pos] = (int32_t)(t - b * N);
+        g.sorted_xyz[b * N + pos] = xyz[t];
+    }
+}
+
+// COUNT: deg[i] = #{j : d2(i, j) < r2max} (self included).  FILL: write row i.
+template <bool FILL>
+__global__ void __launch_bounds__(256) grid_pairs_kernel(int64_t B, int64_t N, const double* __restrict__ r2_levels,
+                                                         int L, int64_t levels_ld, GridWork g, ExclWork w,
+                                                         CsrView csr) {
+    const int64_t b = blockIdx.y;
+    const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    double r2 = 0.0;
+    for (int l = 0; l < L; ++l) r2 = fmax(r2, r2_levels[b * levels_ld + l]);
+    const float thr = prefilter_threshold(r2);
+    const bool no_filter = !(thr <= FLT_MAX);
+    if (s >= N) return;
+    const GridParams gp = g.params[b];
+    const float4* sx = g.sorted_xyz + b * N;
+    const int32_t* si = g.sorted_idx + b * N;
+    const int* cs = g.cell_start + b * (g.max_cells + 1);
+    const float4 p = sx[s];
+    const int32_t i = si[s];
+    const int cx = cell_coord(p.x, gp.ox, gp.inv_h, gp.nx);
+    const int cy = cell_coord(p.y, gp.oy, gp.inv_h, gp.ny);
+    const int cz = cell_coord(p.z, gp.oz, gp.inv_h, gp.nz);
+    int32_t* deg = w.deg + b * N;
+    int64_t pos = 0, end = 0;
+    int32_t* rn = nullptr;
+    double* rd = nullptr;
+    if (FILL) {
+        pos = csr.indptr[b * (N + 1) + i];
+        end = csr.indptr[b * (N + 1) + i + 1];
+        if (end > csr.cap_entries) return;  // overflow: status set by the scan
+        rn = csr.nbr + b * csr.cap_entries;
+        rd = csr.d2 + b * csr.cap_entries;
+    }
+    int cnt = 0;
+    unsigned long long cand = 0;
+    for (int dz = -1; dz <= 1; ++dz) {
+        const int z = cz + dz;
+        if (z < 0 || z >= gp.nz) continue;
+        for (int dy = -1; dy <= 1; ++dy) {
+            const int y = cy + dy;
+            if (y < 0 || y >= gp.ny) continue;
+            const int x0 = cx > 0 ? cx - 1 : 0, x1 = cx + 1 < gp.nx ? cx + 1 : gp.nx - 1;
+            const int row = (z * gp.ny + y) * gp.nx;
+            const int t0 = cs[row + x0], t1 = cs[row + x1 + 1];  // cells x0..x1 are contiguous
+            cand += (unsigned long long)(t1 - t0);
+            for (int t = t0; t < t1; ++t) {
+                const float4 q = sx[t];
+                if (no_filter || sqdist_f32(p, q) < thr) {
+                    const double d = sqdist4(p, q);
+                    if (d < r2) {
+                        if (FILL) {
+                            if (pos < end) { rn[pos] = si[t]; rd[pos] = d; }
+                            ++pos;
+                        } else {
+                            ++cnt;
+                        }
+                    }
+                }
+            }
+        }
+    }
+    if (!FILL) {
+        deg[i] = cnt;
+        atomicAdd(g.evals + b, cand);
+    }
+}
+
 // ---- row sort by (d2, index) + fused level counts -----------------------
 
 __device__ __forceinline__ bool key_less(double da, int32_t ia, double db, int32_t ib) {
@@ -245,6 +446,43 @@ constexpr int kSortWarps = 8;
 constexpr int kWarpRowCap = 256;
 constexpr int kCtaRowCap = 8192;
 
+// Warp bitonic network over 64 keys held two per lane (slot lane, lane+32),
+// padded with (+inf, INT_MAX).  All compare-exchanges are register shuffles.
+__device__ __forceinline__ void warp_bitonic64(double& d0, int32_t& i0, double& d1, int32_t& i1, int lane,
+                                               int n2) {
+#pragma unroll
+    for (int k = 2; k <= 64; k <<= 1) {
+        if (k > n2) break;
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j == 32) {
+                // partner of slot lane is slot lane+32, same thread
+                const bool up = ((lane & k) == 0);  // k == 64: always ascending
+                const bool sw = up ? key_less(d1, i1, d0, i0) : key_less(d0, i0, d1, i1);
+                if (sw) {
+                    const double td = d0; d0 = d1; d1 = td;
+                    const int32_t ti = i0; i0 = i1; i1 = ti;
+                }
+            } else {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    double& d = h ? d1 : d0;
+                    int32_t& ix = h ? i1 : i0;
+                    const int s = lane + 32 * h;
+                    const double od = __shfl_xor_sync(kFull, d, j);
+                    const int32_t oi = __shfl_xor_sync(kFull, ix, j);
+                    const bool lower = (s & j) == 0;
+                    const bool up = (s & k) == 0;
+                    // the lower slot keeps the min when ascending
+                    const bool mine_less = key_less(d, ix, od, oi);
+                    const bool keep_min = (lower == up);
+                    if (keep_min != mine_less) { d = od; ix = oi; }
+                }
+            }
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kSortWarps * 32) excl_sort_small_kernel(CsrView csr, int64_t B,
                                                                        const double* __restrict__ r2_levels,
                                                                        int64_t levels_ld, ExclWork w) {
@@ -253,11 +491,14 @@ __global__ void __launch_bounds__(kSortWarps * 32) excl_sort_small_kernel(CsrVie
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t N = csr.N;
     const int64_t rows = B * N;
+    const double kInf = __longlong_as_double(0x7ff0000000000000LL);
     for (int64_t gr = (int64_t)blockIdx.x * kSortWarps + warp; gr < rows;
          gr += (int64_t)gridDim.x * kSortWarps) {
         const int64_t b = gr / N, r = gr - b * N;
-        const int64_t lo = csr.indptr[b * (N + 1) + r];
-        const int64_t hi = csr.indptr[b * (N + 1) + r + 1];
+        int64_t bound = 0;
+        if (lane < 2) bound = csr.indptr[b * (N + 1) + r + lane];
+        const int64_t lo = __shfl_sync(kFull, bound, 0);
+        const int64_t hi = __shfl_sync(kFull, bound, 1);
         if (hi > csr.cap_entries) continue;  // overflowed cloud: status already set
         const int m = (int)(hi - lo);
         if (m > kWarpRowCap) {
@@ -269,21 +510,40 @@ __global__ void __launch_bounds__(kSortWarps * 32) excl_sort_small_kernel(CsrVie
         }
         int32_t* nbr = csr.nbr + b * csr.cap_entries + lo;
         double* d2 = csr.d2 + b * csr.cap_entries + lo;
+        const double* lv = r2_levels ? r2_levels + b * levels_ld : nullptr;
+        if (m <= 64) {
+            double d0 = lane < m ? d2[lane] : kInf;
+            int32_t i0 = lane < m ? nbr[lane] : 0x7fffffff;
+            double d1 = lane + 32 < m ? d2[lane + 32] : kInf;
+            int32_t i1 = lane + 32 < m ? nbr[lane + 32] : 0x7fffffff;
+            int n2 = 1;
+            while (n2 < m) n2 <<= 1;
+            if (m > 1) warp_bitonic64(d0, i0, d1, i1, lane, n2 < 2 ? 2 : n2);
+            if (lane < m) { d2[lane] = d0; nbr[lane] = i0; }
+            if (lane + 32 < m) { d2[lane + 32] = d1; nbr[lane + 32] = i1; }
+            for (int l = 0; l < csr.L; ++l) {
+                const double t = lv[l];
+                const int c = __popc(__ballot_sync(kFull, lane < m && d0 < t)) +
+                              __popc(__ballot_sync(kFull, lane + 32 < m && d1 < t));
+                if (lane == 0) csr.counts[(b * csr.L + l) * N + r] = c;
+            }
+            continue;
+        }
         int n2 = 1;
         while (n2 < m) n2 <<= 1;
         for (int k = lane; k < n2; k += 32) {
-            sd[warp][k] = k < m ? d2[k] : __longlong_as_double(0x7ff0000000000000LL);
+            sd[warp][k] = k < m ? d2[k] : kInf;
             si[warp][k] = k < m ? nbr[k] : 0x7fffffff;
         }
         __syncwarp();
-        if (m > 1) bitonic_smem(sd[warp], si[warp], n2, lane, 32, [] { __syncwarp(); });
+        bitonic_smem(sd[warp], si[warp], n2, lane, 32, [] { __syncwarp(); });
         for (int k = lane; k < m; k += 32) {
             d2[k] = sd[warp][k];
             nbr[k] = si[warp][k];
         }
         // fused level counts: #entries with d2 < r2_l (strict, _kernels.py:233)
         for (int l = 0; l < csr.L; ++l) {
-            const double t = r2_levels[b * levels_ld + l];
+            const double t = lv[l];
             int c = 0;
             for (int k = lane; k < m; k += 32) c += sd[warp][k] < t ? 1 : 0;
             c = __reduce_add_sync(kFull, c);
@@ -377,32 +637,52 @@ __global__ void level_counts_kernel(CsrView csr, int64_t B, const double* __rest
 
 }  // namespace
 
-cudaError_t launch_excl_build(const float4* xyz, int64_t B, int64_t N, const double* r2_levels, int L,
-                              int64_t levels_ld, CsrView csr, ExclWork w, cudaStream_t s) {
-    cudaError_t e;
-    if ((e = cudaMemsetAsync(w.edge_count, 0, sizeof(unsigned long long) * B, s)) != cudaSuccess) return e;
-    if ((e = cudaMemsetAsync(w.deg, 0, sizeof(int32_t) * B * N, s)) != cudaSuccess) return e;
-    if ((e = cudaMemsetAsync(w.long_count, 0, sizeof(unsigned), s)) != cudaSuccess) return e;
-    if ((e = cudaMemsetAsync(w.status, 0, sizeof(int32_t) * B, s)) != cudaSuccess) return e;
-    const int64_t nt = (N + kTile - 1) / kTile;
-    const int64_t npairs = nt * (nt + 1) / 2;
-    excl_pairs_kernel<<<dim3((unsigned)npairs, (unsigned)B), kPairThreads, 0, s>>>(xyz, N, r2_levels, L,
-                                                                                 levels_ld, w);
-    const unsigned g = (unsigned)std::min<int64_t>(148 * 8, (w.cap_edges + 255) / 256 + 1);
-    excl_degree_kernel<<<dim3(g, (unsigned)B), 256, 0, s>>>(N, w);
-    excl_scan_kernel<<<(unsigned)B, 1024, 0, s>>>(N, w, csr);
-    const unsigned g2 = (unsigned)std::min<int64_t>(148 * 8, (w.cap_edges + N + 255) / 256 + 1);
-    excl_fill_kernel<<<dim3(g2, (unsigned)B), 256, 0, s>>>(N, w, csr);
+static cudaError_t launch_sort(CsrView csr, int64_t B, const double* r2_levels, int64_t levels_ld, ExclWork w,
+                               cudaStream_t s) {
     excl_sort_small_kernel<<<148 * 8, kSortWarps * 32, 0, s>>>(csr, B, r2_levels, levels_ld, w);
     const size_t dsm = (sizeof(double) + sizeof(int32_t)) * kCtaRowCap;
     static bool attr_set = false;
     if (!attr_set) {
-        e = cudaFuncSetAttribute(excl_sort_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+        cudaError_t e = cudaFuncSetAttribute(excl_sort_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)dsm);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
     excl_sort_large_kernel<<<148, 1024, dsm, s>>>(csr, r2_levels, levels_ld, w);
     return cudaGetLastError();
+}
+
+cudaError_t launch_excl_build(const float4* xyz, int64_t B, int64_t N, const double* r2_levels, int L,
+                              int64_t levels_ld, CsrView csr, ExclWork w, GridWork g, int method, cudaStream_t s) {
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(w.deg, 0, sizeof(int32_t) * B * N, s)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(w.long_count, 0, sizeof(unsigned), s)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(w.status, 0, sizeof(int32_t) * B, s)) != cudaSuccess) return e;
+    const unsigned gpts = (unsigned)std::min<int64_t>(148 * 16, (B * N + 255) / 256 + 1);
+    if (method == 1) {
+        if ((e = cudaMemsetAsync(g.cell_start, 0, sizeof(int) * B * (g.max_cells + 1), s)) != cudaSuccess) return e;
+        if ((e = cudaMemsetAsync(g.evals, 0, sizeof(unsigned long long) * B, s)) != cudaSuccess) return e;
+        grid_setup_kernel<<<(unsigned)B, 1024, 0, s>>>(xyz, N, r2_levels, L, levels_ld, g);
+        grid_assign_kernel<<<gpts, 256, 0, s>>>(xyz, B, N, g);
+        grid_scan_kernel<<<(unsigned)B, 1024, 0, s>>>(N, g);
+        grid_scatter_kernel<<<gpts, 256, 0, s>>>(xyz, B, N, g);
+        const dim3 gp((unsigned)((N + 255) / 256), (unsigned)B);
+        grid_pairs_kernel<false><<<gp, 256, 0, s>>>(B, N, r2_levels, L, levels_ld, g, w, csr);
+        excl_scan_kernel<<<(unsigned)B, 1024, 0, s>>>(N, w, csr, 0);
+        grid_pairs_kernel<true><<<gp, 256, 0, s>>>(B, N, r2_levels, L, levels_ld, g, w, csr);
+        return launch_sort(csr, B, r2_levels, levels_ld, w, s);
+    }
+    if ((e = cudaMemsetAsync(w.edge_count, 0, sizeof(unsigned long long) * B, s)) != cudaSuccess) return e;
+    const int64_t nt = (N + kTile - 1) / kTile;
+    const int64_t npairs = nt * (nt + 1) / 2;
+    excl_pairs_kernel<<<dim3((unsigned)npairs, (unsigned)B), kPairThreads, 0, s>>>(xyz, N, r2_levels, L,
+                                                                                 levels_ld, w);
+    const unsigned g1 = (unsigned)std::min<int64_t>(148 * 8, (w.cap_edges + 255) / 256 + 1);
+    excl_degree_kernel<<<dim3(g1, (unsigned)B), 256, 0, s>>>(N, w);
+    excl_scan_kernel<<<(unsigned)B, 1024, 0, s>>>(N, w, csr, 1);
+    const unsigned g2 = (unsigned)std::min<int64_t>(148 * 8, (w.cap_edges + N + 255) / 256 + 1);
+    excl_fill_kernel<<<dim3(g2, (unsigned)B), 256, 0, s>>>(N, w, csr);
+    return launch_sort(csr, B, r2_levels, levels_ld, w, s);
 }
 
 cudaError_t launch_sort_rows(CsrView csr, int64_t B, ExclWork w, cudaStream_t s) {

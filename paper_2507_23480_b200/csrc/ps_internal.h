@@ -46,8 +46,27 @@ struct ExclWork {
     int32_t* status;      // [B] bit0: edge overflow, bit1: entry overflow
 };
 
+struct GridParams {
+    double ox, oy, oz, inv_h;
+    int nx, ny, nz, ncells;
+};
+
+struct GridWork {
+    GridParams* params;           // [B]
+    int* cell_start;              // [B][max_cells + 1]
+    int* cursor;                  // [B][max_cells]
+    int32_t* cell_of;             // [B][N]
+    int32_t* sorted_idx;          // [B][N]
+    float4* sorted_xyz;           // [B][N]
+    unsigned long long* evals;    // [B] candidate pairs evaluated
+    int max_cells;
+};
+
+// method 0: brute-force i<j triangle (every pair evaluated once)
+// method 1: uniform grid of cell width >= R_max (identical CSR)
 cudaError_t launch_excl_build(const float4* xyz, int64_t B, int64_t N, const double* r2_levels,
-                              int L, int64_t levels_ld, CsrView csr, ExclWork w, cudaStream_t s);
+                              int L, int64_t levels_ld, CsrView csr, ExclWork w, GridWork g, int method,
+                              cudaStream_t s);
 cudaError_t launch_sort_rows(CsrView csr, int64_t B, ExclWork w, cudaStream_t s);
 cudaError_t launch_level_counts(CsrView csr, int64_t B, const double* r2_levels, int64_t levels_ld,
                                 cudaStream_t s);

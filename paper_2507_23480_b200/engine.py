@@ -96,16 +96,18 @@ class DeviceCsr:
     work: torch.Tensor     # uint8 workspace
     cap_entries: int
     cap_edges: int
+    method: int = 1
 
     @property
     def L(self):
         return self.counts.shape[1]
 
     @staticmethod
-    def allocate(B, N, L, cap_entries, cap_edges, device):
+    def allocate(B, N, L, cap_entries, cap_edges, device, method=1):
+        """method 1 = uniform-grid candidates (default), 0 = brute-force triangle."""
         cap_entries = int(min(max(cap_entries, N), (1 << 31) - 1))
-        cap_edges = int(max(cap_edges, 1))
-        ws = int(_lib.raw("ps_excl_workspace_bytes", B, N, cap_edges))
+        cap_edges = int(max(cap_edges, 1)) if method == 0 else 1
+        ws = int(_lib.raw("ps_excl_workspace_bytes", B, N, cap_edges, method))
         return DeviceCsr(
             indptr=torch.zeros(B, N + 1, dtype=torch.int64, device=device),
             nbr=torch.empty(B, cap_entries, dtype=torch.int32, device=device),
@@ -114,13 +116,23 @@ class DeviceCsr:
             levels=torch.empty(B, L, dtype=torch.float64, device=device),
             status=torch.zeros(B, dtype=torch.int32, device=device),
             work=torch.empty(ws, dtype=torch.uint8, device=device),
-            cap_entries=cap_entries, cap_edges=cap_edges)
+            cap_entries=cap_entries, cap_edges=cap_edges, method=int(method))
 
     def build(self, xyz4):
         B, N, _ = xyz4.shape
         _lib.call("ps_excl_build", _p(xyz4), B, N, _p(self.levels), self.L, self.levels.shape[1], _p(self.indptr),
                   _p(self.nbr), _p(self.d2), _p(self.counts), self.cap_entries, _p(self.work), self.cap_edges,
-                  _p(self.status), _stream())
+                  _p(self.status), self.method, _stream())
+
+    def evaluated_pairs(self) -> list[int]:
+        """Pair distances the build evaluated per cloud (self pairs excluded)."""
+        B, N = self.indptr.shape[0], self.indptr.shape[1] - 1
+        if self.method == 0:
+            return [N * (N - 1) // 2] * B
+        off = int(_lib.raw("ps_excl_grid_evals_offset", B, N))
+        cand = self.work[off:off + 8 * B].view(torch.int64).tolist()
+        # the grid count pass visits ordered pairs including self: unordered = (c - N) / 2
+        return [(int(c) - N) // 2 for c in cand]
 
     def overflowed(self) -> bool:
         return bool(int(self.status.max().item()) != 0)
@@ -151,7 +163,7 @@ class FastPoint:
     exclusion lists."""
 
     def __init__(self, B, N, n, *, p=0.1, nseg=6, estimator="power", exponent=None, extra_radii=(),
-                 seed_index=0, pick_lowest=False, cap_entries=None, device="cuda"):
+                 seed_index=0, pick_lowest=False, cap_entries=None, excl_method="grid", device="cuda"):
         if not (1 <= n <= N):
             raise ValueError(f"n must be in [1, {N}]")
         if nseg < 1 or nseg > 16:
@@ -171,6 +183,9 @@ class FastPoint:
             raise ValueError("at most 8 extra radii")
         self.seed_index = int(seed_index)
         self.pick_lowest = bool(pick_lowest)
+        if excl_method not in ("grid", "bruteforce"):
+            raise ValueError("excl_method must be 'grid' or 'bruteforce'")
+        self.excl_method = 1 if excl_method == "grid" else 0
         self.device = torch.device(device)
         self.k0 = min(prefix_len(self.n, self.p), self.n)
         if self.k0 < 2:
@@ -196,7 +211,7 @@ class FastPoint:
                         if estimator == "power" else None)
         self.given_curve = torch.zeros(B, n, dtype=torch.float64, device=dev) if estimator == "curve" else None
         ce, cg = (default_capacity(N, n) if cap_entries is None else (int(cap_entries), int(cap_entries) // 2 + 1))
-        self.csr = DeviceCsr.allocate(B, N, self.L, ce, cg, dev)
+        self.csr = DeviceCsr.allocate(B, N, self.L, ce, cg, dev, self.excl_method)
         ws = int(_lib.raw("ps_sampler_workspace_bytes", B, N, self.nseg))
         self.samp_ws = torch.empty(max(ws, 1), dtype=torch.uint8, device=dev) if ws else None
         self._bnd_c = np.ascontiguousarray(self.boundaries, np.int64)
@@ -288,7 +303,7 @@ class FastPoint:
             return False
         E = int(self.csr.indptr[:, -1].max().item())
         grow = max(2 * self.csr.cap_entries, E + self.N)
-        self.csr = DeviceCsr.allocate(self.B, self.N, self.L, grow, grow // 2 + 1, self.device)
+        self.csr = DeviceCsr.allocate(self.B, self.N, self.L, grow, grow // 2 + 1, self.device, self.excl_method)
         self.graph = None
         self.sample()
         return True
@@ -333,12 +348,14 @@ class FastPoint:
 
     # -- accounting ---------------------------------------------------------------
     def pair_evals(self) -> list[int]:
-        """Per-cloud pair-distance evaluations (SPEC.md:438 accounting):
-        prefix N(k0-1) + exclusion N(N-1)/2 + N + early termination N(n-i)."""
+        """Per-cloud pair-distance evaluations: prefix N(k0-1) + exclusion
+        (brute force: N(N-1)/2, the SPEC.md:438 accounting; grid: the
+        candidate pairs actually evaluated) + N self pairs + early
+        termination N(n-i)."""
         reached = self.reached.tolist()
         N = self.N
-        base = N * (self.k0 - 1) + N * (N - 1) // 2 + N
-        return [base + N * (self.n - int(r)) for r in reached]
+        excl = self.csr.evaluated_pairs()
+        return [N * (self.k0 - 1) + excl[b] + N + N * (self.n - int(r)) for b, r in enumerate(reached)]
 
 
 def ball_query_naive(xyz4, centroids, radius, k):

@@ -43,7 +43,7 @@ def test_validation_without_device():
                                  100, None, 0, None, None, None, None, None)
     assert rc == _lib.PS_ERR_INVALID
     assert b"last segment boundary" in lib.ps_last_error()
-    assert lib.ps_excl_workspace_bytes(2, 100, 50) > 0
+    assert lib.ps_excl_workspace_bytes(2, 100, 50, 0) > 0 and lib.ps_excl_workspace_bytes(2, 100, 1, 1) > 0
     assert lib.ps_sampler_workspace_bytes(1, 24000, 6) == 0      # fits in shared memory
     assert lib.ps_sampler_workspace_bytes(2, 100000, 6) > 0     # global workspace
 
