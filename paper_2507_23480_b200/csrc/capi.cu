@@ -260,7 +260,7 @@ int ps_thresholds(const double* prefix_curve, int64_t curve_ld, int64_t B, int64
 
 int64_t ps_sampler_workspace_bytes(int64_t B, int64_t N, int32_t nseg) {
     const size_t per = ps::sampler_ws_bytes(N, nseg);
-    if (per <= 200 * 1024) return 0;
+    if (per <= 192 * 1024) return 0;
     return (int64_t)(per * B);
 }
 
@@ -286,7 +286,7 @@ int ps_sample_predicted(const int64_t* indptr, const int32_t* nbr, int64_t cap_e
     a.k0 = k0; a.n_total = n_total; a.N = N; a.out_idx = out_idx; a.ld_out = ld_out; a.state_io = state_io;
     a.pick_lowest = pick_lowest; a.reached = reached; a.exhausted = exhausted; a.entered = entered;
     const size_t per = ps::sampler_ws_bytes(N, nseg);
-    a.use_smem = per <= 200 * 1024 ? 1 : 0;
+    a.use_smem = per <= 192 * 1024 ? 1 : 0;
     if (!a.use_smem) {
         CHECK_ARG(work != nullptr, "sampler workspace required for N=%lld", (long long)N);
         a.gws = static_cast<unsigned char*>(work);

@@ -156,13 +156,21 @@ PS_DEV int block_excl_scan(int v, int* warp_tot, int* total) {
     return excl;
 }
 
+constexpr int kMaxPred = 8;
+constexpr uint8_t kPredOverflow = 0xff;
+
 struct SampView {
-    uint32_t* bm;      // [nseg][W]
-    int32_t* pool;     // [N]
-    uint16_t* rank;    // [N] draw rank within the current chunk
-    int32_t* cand;     // [kChunk]
-    uint8_t* st;       // [kChunk]
-    uint32_t* pos;     // [kChunk]
+    uint32_t* bm;      // [nseg][W] availability bits per segment
+    int32_t* pool;     // [N] segment pool (swap-remove array)
+    uint16_t* rank;    // [N] draw rank within the current chunk (0xffff = none)
+};
+
+struct ChunkSmem {
+    int32_t cand[kChunk];
+    uint32_t pos[kChunk];
+    uint16_t preds[kChunk][kMaxPred];  // earlier available in-chunk neighbours
+    uint8_t st[kChunk];
+    uint8_t npred[kChunk];
 };
 
 PS_DEV void build_pool(const SampView& v, int seg, int64_t W, SampCtl* ctl, int* warp_tot) {
@@ -186,20 +194,66 @@ PS_DEV void build_pool(const SampView& v, int seg, int64_t W, SampCtl* ctl, int*
     __syncthreads();
 }
 
-// clear the level-l row prefix of point p (plus p itself) for l in [l0, nseg)
+// Clear point p (and its level-l row prefix) in the bitmaps of levels
+// [l0, nseg).  Called by `nl` cooperating lanes; the row is re-read per level
+// from L1 (the first level's read brings it in).
 PS_DEV void clear_point_levels(const SampView& v, const SampArgs& a, int64_t b, int64_t W, int32_t p, int l0,
                                int lane, int nl) {
     const int64_t N = a.N;
     const int64_t base = a.indptr[b * (N + 1) + p];
     const int32_t* nbr = a.nbr + b * a.cap_entries + base;
+    const uint32_t pbit = ~(1u << (p & 31));
     for (int l = l0; l < a.nseg; ++l) {
         const int32_t c = a.counts[(b * a.L + a.seg_level_rows[l]) * N + p];
         uint32_t* bm = v.bm + (int64_t)l * W;
         for (int u = lane; u < c; u += nl) {
-            const int32_t q = nbr[u];
+            const int32_t q = __ldg(nbr + u);
             atomicAnd(&bm[q >> 5], ~(1u << (q & 31)));
         }
-        if (lane == 0) atomicAnd(&bm[p >> 5], ~(1u << (p & 31)));
+        if (lane == 0) atomicAnd(&bm[p >> 5], pbit);
+    }
+}
+
+// Swap-remove chain for draws k .. k+K-1 (pool length before draw t is L-t),
+// run by one warp: groups of up to 32 consecutive draws execute in parallel
+// up to the first draw whose read locations an earlier draw of the group
+// writes (same position, or a position equal to its last slot).  Identical
+// to the serial chain of _kernels.py:325-330.
+PS_DEV void swap_chain_warp(int32_t* pool, const uint32_t* pos, int32_t* cand, int64_t L, int64_t k, int K,
+                            int lane) {
+    const unsigned lt = (1u << lane) - 1u;
+    int g = 0;
+    while (g < K) {
+        const int t = g + lane;
+        const bool act = t < K;
+        const uint32_t p = act ? pos[t] : 0x80000000u | (uint32_t)lane;
+        const int64_t last0 = L - 1 - (k + g);               // last slot of draw g
+        const int64_t last = last0 - lane;                    // last slot of this draw
+        const unsigned same = __match_any_sync(kFull, p);
+        bool conflict = act && (same & lt) != 0;              // earlier draw wrote my position
+        // earlier draw i writes p_i == last_j for j = last0 - p_i > i
+        unsigned mark = 0;
+        if (act) {
+            const int64_t j = last0 - (int64_t)p;
+            if (j > lane && j < 32) mark = 1u << (int)j;
+        }
+        mark = __reduce_or_sync(kFull, mark);
+        conflict = conflict || ((mark >> lane) & 1u);
+        const unsigned cmask = __ballot_sync(kFull, conflict);
+        const int run = cmask ? (__ffs(cmask) - 1) : 32;      // >= 1 (lane 0 never conflicts)
+        const int nrun = min(run, K - g);
+        int32_t vp = 0, vl = 0;
+        if (lane < nrun) {
+            vp = pool[p];
+            vl = pool[last];
+        }
+        __syncwarp();
+        if (lane < nrun) {
+            pool[p] = vl;
+            cand[t] = vp;
+        }
+        __syncwarp();
+        g += nrun;
     }
 }
 
@@ -207,13 +261,14 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
     extern __shared__ __align__(16) unsigned char dyn[];
     __shared__ SampCtl ctl;
     __shared__ int warp_tot[32];
+    __shared__ ChunkSmem cs;
     const int64_t b = blockIdx.x;
     const int64_t N = a.N;
     const int64_t W = (N + 31) >> 5;
     const int nseg = a.nseg;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
 
-    // carve the workspace: shared memory when it fits, else this cloud's global slice
+    // big tables: shared memory when they fit, else this cloud's global slice
     unsigned char* ws = a.use_smem ? dyn : (a.gws + b * a.gws_stride);
     SampView v;
     {
@@ -221,11 +276,7 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
         v.bm = reinterpret_cast<uint32_t*>(ws + off); off += sizeof(uint32_t) * nseg * W;
         off = (off + 15) & ~size_t(15);
         v.pool = reinterpret_cast<int32_t*>(ws + off); off += sizeof(int32_t) * N;
-        v.rank = reinterpret_cast<uint16_t*>(ws + off); off += sizeof(uint16_t) * N;
-        off = (off + 15) & ~size_t(15);
-        v.cand = reinterpret_cast<int32_t*>(ws + off); off += sizeof(int32_t) * kChunk;
-        v.pos = reinterpret_cast<uint32_t*>(ws + off); off += sizeof(uint32_t) * kChunk;
-        v.st = reinterpret_cast<uint8_t*>(ws + off);
+        v.rank = reinterpret_cast<uint16_t*>(ws + off);
     }
     int64_t* out = a.out_idx + b * a.ld_out;
     const int64_t k0 = a.k0, n_total = a.n_total;
@@ -285,9 +336,9 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
         const int32_t* cnt_row = a.counts + (b * a.L + lvl) * N;
         const int64_t* indptr = a.indptr + b * (N + 1);
         const int32_t* nbr_all = a.nbr + b * a.cap_entries;
+        const uint32_t* bms = v.bm + (int64_t)seg * W;
         int64_t k = 0;  // draws consumed in this segment visit
-        bool seg_over = false;
-        while (!seg_over) {
+        for (;;) {
             if (k >= L) {
                 // pool exhausted: the picked < 0 path of _kernels.py:335-347
                 __syncthreads();
@@ -303,79 +354,115 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
                 }
                 __syncthreads();
                 if (!ctl.done) build_pool(v, ctl.seg, W, &ctl, warp_tot);
-                seg_over = true;
                 break;
             }
             const int K = (int)((L - k) < kChunk ? (L - k) : kChunk);
             // candidate order for draws k .. k+K-1
             if (a.pick_lowest) {
-                for (int t = tid; t < K; t += blockDim.x) v.cand[t] = v.pool[k + t];
+                for (int t = tid; t < K; t += blockDim.x) cs.cand[t] = v.pool[k + t];
             } else {
                 for (int t = tid; t < K; t += blockDim.x) {
                     const uint64_t z = mix64(state0 + (uint64_t)(k + t + 1) * kGolden);
-                    v.pos[t] = (uint32_t)(z % (uint64_t)(L - (k + t)));
+                    cs.pos[t] = (uint32_t)(z % (uint64_t)(L - (k + t)));
                 }
                 __syncthreads();
-                if (tid == 0) {
-                    int32_t* pool = v.pool;
-                    for (int t = 0; t < K; ++t) {
-                        const int64_t last = L - 1 - (k + t);
-                        const uint32_t p = v.pos[t];
-                        const int32_t c = pool[p];
-                        pool[p] = pool[last];
-                        v.cand[t] = c;
-                    }
-                }
+                if (warp == 0) swap_chain_warp(v.pool, cs.pos, cs.cand, L, k, K, lane);
             }
             __syncthreads();
             // availability + rank
-            const uint32_t* bms = v.bm + (int64_t)seg * W;
             for (int t = tid; t < K; t += blockDim.x) {
-                const int32_t c = v.cand[t];
+                const int32_t c = cs.cand[t];
                 const bool av = (bms[c >> 5] >> (c & 31)) & 1u;
-                v.st[t] = av ? kUndecided : kOut;
+                cs.st[t] = av ? kUndecided : kOut;
                 v.rank[c] = (uint16_t)t;
             }
             __syncthreads();
-            // greedy MIS rounds
-            for (;;) {
-                if (tid == 0) ctl.undecided = 0;
-                __syncthreads();
-                int und = 0;
-                for (int t = tid; t < K; t += blockDim.x) {
-                    if (v.st[t] != kUndecided) continue;
-                    const int32_t c = v.cand[t];
-                    const int64_t base = indptr[c];
-                    const int32_t m = cnt_row[c];
-                    const int32_t* row = nbr_all + base;
-                    bool out_ = false, blocked = false;
-                    for (int32_t u = 0; u < m; ++u) {
-                        const int32_t q = row[u];
-                        const uint32_t rq = v.rank[q];  // 0xffff = not in chunk
+            // greedy MIS, round 0: one pass over the level-seg row collects the
+            // earlier available in-chunk neighbours (the only ones that matter)
+            int und = 0;
+            for (int t = tid; t < K; t += blockDim.x) {
+                if (cs.st[t] != kUndecided) { cs.npred[t] = 0; continue; }
+                const int32_t c = cs.cand[t];
+                const int32_t m = cnt_row[c];
+                const int32_t* row = nbr_all + indptr[c];
+                int np = 0;
+                bool out_ = false, blocked = false;
+                for (int32_t u0 = 0; u0 < m; u0 += 8) {
+                    int32_t q[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) q[j] = (u0 + j < m) ? __ldg(row + u0 + j) : c;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const uint32_t rq = v.rank[q[j]];
                         if (rq < (uint32_t)t) {
-                            const uint8_t s = v.st[rq];
-                            if (s == kIn) { out_ = true; break; }
-                            if (s == kUndecided) blocked = true;
+                            // OUT is final and never matters; IN rejects; UNDECIDED is remembered
+                            const uint8_t sq = cs.st[rq];
+                            if (sq == kIn) {
+                                out_ = true;
+                            } else if (sq == kUndecided) {
+                                if (np < kMaxPred) cs.preds[t][np] = (uint16_t)rq;
+                                ++np;
+                                blocked = true;
+                            }
                         }
                     }
-                    if (out_) v.st[t] = kOut;
-                    else if (!blocked) v.st[t] = kIn;
-                    else ++und;
                 }
-                und = __reduce_add_sync(kFull, und);
-                if (lane == 0 && und) atomicAdd(&ctl.undecided, und);
+                cs.npred[t] = np > kMaxPred ? kPredOverflow : (uint8_t)np;
+                if (out_) cs.st[t] = kOut;
+                else if (!blocked) cs.st[t] = kIn;
+                else ++und;
+            }
+            und = __reduce_add_sync(kFull, und);
+            if (tid == 0) ctl.undecided = 0;
+            __syncthreads();
+            if (lane == 0 && und) atomicAdd(&ctl.undecided, und);
+            __syncthreads();
+            // later rounds over the short predecessor lists
+            while (ctl.undecided != 0) {
                 __syncthreads();
-                if (ctl.undecided == 0) break;
+                if (tid == 0) ctl.undecided = 0;
+                __syncthreads();
+                int u2 = 0;
+                for (int t = tid; t < K; t += blockDim.x) {
+                    if (cs.st[t] != kUndecided) continue;
+                    bool out_ = false, blocked = false;
+                    const uint8_t np = cs.npred[t];
+                    if (np != kPredOverflow) {
+                        for (int j = 0; j < np; ++j) {
+                            const uint8_t sq = cs.st[cs.preds[t][j]];
+                            if (sq == kIn) { out_ = true; break; }
+                            if (sq == kUndecided) blocked = true;
+                        }
+                    } else {
+                        const int32_t c = cs.cand[t];
+                        const int32_t m = cnt_row[c];
+                        const int32_t* row = nbr_all + indptr[c];
+                        for (int32_t u = 0; u < m; ++u) {
+                            const uint32_t rq = v.rank[row[u]];
+                            if (rq < (uint32_t)t) {
+                                const uint8_t sq = cs.st[rq];
+                                if (sq == kIn) { out_ = true; break; }
+                                if (sq == kUndecided) blocked = true;
+                            }
+                        }
+                    }
+                    if (out_) cs.st[t] = kOut;
+                    else if (!blocked) cs.st[t] = kIn;
+                    else ++u2;
+                }
+                u2 = __reduce_add_sync(kFull, u2);
+                if (lane == 0 && u2) atomicAdd(&ctl.undecided, u2);
+                __syncthreads();
             }
             // ordered compaction of accepted candidates
             const int64_t need = a.boundaries[seg] - ctl.i;
-            int flag = (tid < K && v.st[tid] == kIn) ? 1 : 0;
+            const int flag = (tid < K && cs.st[tid] == kIn) ? 1 : 0;
             int tot;
             const int ex = block_excl_scan(flag, warp_tot, &tot);
             const int64_t take = (int64_t)tot < need ? (int64_t)tot : need;
             const int64_t i0 = ctl.i;
             if (flag && ex < take) {
-                out[i0 + ex] = v.cand[tid];
+                out[i0 + ex] = cs.cand[tid];
                 if (ex == take - 1 && take == need) ctl.accepted = tid;  // draw of the last used accept
             }
             __syncthreads();
@@ -383,21 +470,20 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
             const bool ends = (take == need);
             const int l0 = ends ? seg + 1 : seg;
             if (l0 < nseg) {
-                for (int64_t x = warp; x < take; x += nwarps)
-                    clear_point_levels(v, a, b, W, (int32_t)out[i0 + x], l0, lane, 32);
+                // 4 points per warp, 8 lanes each
+                const int sub = lane >> 3, sl = lane & 7;
+                for (int64_t x = (int64_t)warp * 4 + sub; x < take; x += (int64_t)nwarps * 4)
+                    clear_point_levels(v, a, b, W, (int32_t)out[i0 + x], l0, sl, 8);
             }
-            for (int t = tid; t < K; t += blockDim.x) v.rank[v.cand[t]] = kNoRank;
+            for (int t = tid; t < K; t += blockDim.x) v.rank[cs.cand[t]] = kNoRank;
             __syncthreads();
             if (tid == 0) {
                 ctl.i = i0 + take;
                 if (ends && !a.pick_lowest) ctl.state = state0 + (uint64_t)(k + ctl.accepted + 1) * kGolden;
             }
             __syncthreads();
-            if (ends) {
-                seg_over = true;
-            } else {
-                k += K;
-            }
+            if (ends) break;
+            k += K;
         }
     }
     __syncthreads();
@@ -467,8 +553,6 @@ size_t sampler_ws_bytes(int64_t N, int nseg) {
     size_t off = sizeof(uint32_t) * nseg * W;
     off = (off + 15) & ~size_t(15);
     off += sizeof(int32_t) * N + sizeof(uint16_t) * N;
-    off = (off + 15) & ~size_t(15);
-    off += sizeof(int32_t) * kChunk + sizeof(uint32_t) * kChunk + kChunk;
     return (off + 255) & ~size_t(255);
 }
 
