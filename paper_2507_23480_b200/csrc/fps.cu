@@ -49,54 +49,48 @@ struct __align__(16) Rec {
 PS_DEV uint64_t dbits(double d) { return (uint64_t)__double_as_longlong(d); }
 PS_DEV double bitsd(uint64_t k) { return __longlong_as_double((long long)k); }
 
-// Reduce records rec[0..n) (n <= 32) held by lanes < n; returns winner in all lanes.
-PS_DEV Rec warp_reduce_recs(const Rec* recs, int n, int lane) {
-    uint64_t key = 0;
-    uint32_t idx = kNone;
-    Rec mine{};
-    if (lane < n) {
-        mine = recs[lane];
-        key = ((uint64_t)mine.khi << 32) | mine.klo;
-        idx = mine.idx;
-    }
-    const ArgMax am = warp_argmax(key, idx);
-    const uint32_t winmask = __ballot_sync(kFull, idx == am.idx && idx != kNone);
-    Rec out;
-    out.klo = (uint32_t)am.key;
-    out.khi = (uint32_t)(am.key >> 32);
-    out.idx = am.idx;
-    const int src = winmask ? __ffs(winmask) - 1 : 0;
-    out.taken = __shfl_sync(kFull, mine.taken, src);
-    out.x = __shfl_sync(kFull, mine.x, src);
-    out.y = __shfl_sync(kFull, mine.y, src);
-    out.z = __shfl_sync(kFull, mine.z, src);
-    out.pad = 0;
-    return out;
+// Winner lane of a warp argmax over (key, idx): max key, lowest idx on ties.
+// Fast path: one REDUX on the high key word; the full comparison only runs
+// when several lanes share that word.  Returns -1 if no lane has idx != kNone.
+PS_DEV int warp_argmax_lane(uint64_t key, uint32_t idx) {
+    const bool valid = idx != kNone;
+    const uint32_t hi = valid ? (uint32_t)(key >> 32) : 0u;
+    const uint32_t mhi = __reduce_max_sync(kFull, hi);
+    unsigned cand = __ballot_sync(kFull, valid && hi == mhi);
+    if (cand == 0) return -1;
+    if (__popc(cand) == 1) return __ffs(cand) - 1;
+    const bool c1 = (cand >> (threadIdx.x & 31)) & 1u;
+    const uint32_t lo = (uint32_t)key;
+    const uint32_t mlo = __reduce_max_sync(kFull, c1 ? lo : 0u);
+    const bool c2 = c1 && lo == mlo;
+    const uint32_t midx = __reduce_min_sync(kFull, c2 ? idx : kNone);
+    return __ffs(__ballot_sync(kFull, c2 && idx == midx)) - 1;
 }
 
-// Same, but minimum index (fallback: lowest untaken point).
+PS_DEV uint64_t rec_key(const Rec& r) { return ((uint64_t)r.khi << 32) | r.klo; }
+
+// Lowest-index record among recs[0..n), broadcast to every lane (fallback).
 PS_DEV Rec warp_min_idx_recs(const Rec* recs, int n, int lane) {
-    Rec mine{};
-    uint32_t idx = kNone;
-    if (lane < n) {
-        mine = recs[lane];
-        idx = mine.idx;
-    }
+    const uint32_t idx = lane < n ? recs[lane].idx : kNone;
     const uint32_t m = __reduce_min_sync(kFull, idx);
-    const uint32_t winmask = __ballot_sync(kFull, idx == m && idx != kNone);
-    const int src = winmask ? __ffs(winmask) - 1 : 0;
-    Rec out;
-    out.klo = __shfl_sync(kFull, mine.klo, src);
-    out.khi = __shfl_sync(kFull, mine.khi, src);
-    out.idx = m;
-    out.taken = __shfl_sync(kFull, mine.taken, src);
-    out.x = __shfl_sync(kFull, mine.x, src);
-    out.y = __shfl_sync(kFull, mine.y, src);
-    out.z = __shfl_sync(kFull, mine.z, src);
-    out.pad = 0;
-    return out;
+    const unsigned w = __ballot_sync(kFull, idx == m && idx != kNone);
+    if (!w) { Rec z{}; z.idx = kNone; return z; }
+    return recs[__ffs(w) - 1];
 }
 
+// conservative float32 skip threshold for "d < md" (see kernel comment)
+PS_DEV float skip_threshold(double md) {
+    if (md == 0.0) return -1.0f;                     // nothing is closer than 0
+    if (!(md >= 7.888609052210118e-31)) return __int_as_float(0x7f800000);  // tiny: always exact
+    return __fmul_ru(__double2float_ru(md), 1.0f + 3.814697265625e-06f);    // * (1 + 2^-18)
+}
+
+// Per point: the float32 distance to the new sample decides whether the exact
+// float64 fold can change md.  d32 carries relative error < 6 * 2^-24, so
+// d32 > f32_up(md) * (1 + 2^-18) proves d_exact > md and the fold is a no-op;
+// otherwise the float64 distance ((dx*dx + dy*dy) + dz*dz) is evaluated and
+// folded exactly as _kernels.py:55-60.  The float32 test only skips work --
+// md, the argmax and every output are the float64 reference values.
 template <int P>
 __global__ void __launch_bounds__(kFpsThreads, 1) fps_cluster_kernel(FpsArgs a) {
     __shared__ Rec warp_rec[kFpsWarps];
@@ -121,40 +115,44 @@ __global__ void __launch_bounds__(kFpsThreads, 1) fps_cluster_kernel(FpsArgs a) 
     const int64_t k_start = a.k_start_dev ? a.k_start_dev[b] : a.k_start;
     const int64_t k_stop = a.k_stop;
     const int64_t seed = a.seed_dev ? a.seed_dev[b] : a.seed;
+    const double kInf = __longlong_as_double(0x7ff0000000000000LL);
 
     // ---- state into registers -------------------------------------------
-    double px[P > 0 ? P : 1], py[P > 0 ? P : 1], pz[P > 0 ? P : 1], m[P > 0 ? P : 1];
-    uint32_t tk = 0;
+    constexpr int PP = P > 0 ? P : 1;
+    float fx[PP], fy[PP], fz[PP], thr[PP];
+    double m[PP];
+    uint32_t tk = 0, valid = 0;
     if constexpr (P > 0) {
 #pragma unroll
         for (int q = 0; q < P; ++q) {
             const int64_t j = lo + tid + (int64_t)q * kFpsThreads;
+            fx[q] = fy[q] = fz[q] = 0.f;
+            m[q] = 0.0;
             if (j < hi) {
+                valid |= 1u << q;
                 const float4 v = xyz[j];
-                px[q] = v.x; py[q] = v.y; pz[q] = v.z;
+                fx[q] = v.x; fy[q] = v.y; fz[q] = v.z;
                 if (a.fresh) {
-                    m[q] = __longlong_as_double(0x7ff0000000000000LL);
+                    m[q] = kInf;
                     tk |= (j == seed ? 1u : 0u) << q;
                 } else {
                     m[q] = md[j];
                     tk |= (taken[j] ? 1u : 0u) << q;
                 }
-            } else {
-                px[q] = py[q] = pz[q] = 0.0;
-                m[q] = 0.0;
             }
+            thr[q] = skip_threshold(m[q]);
         }
     } else {
         if (a.fresh) {
             for (int64_t j = lo + tid; j < hi; j += kFpsThreads) {
-                md[j] = __longlong_as_double(0x7ff0000000000000LL);
+                md[j] = kInf;
                 taken[j] = (j == seed) ? 1 : 0;
             }
         }
     }
     if (a.fresh && r == 0 && tid == 0) {
         out[0] = seed;
-        curve[0] = __longlong_as_double(0x7ff0000000000000LL);
+        curve[0] = kInf;
     }
 
     if (tid == 0) {
@@ -168,36 +166,48 @@ __global__ void __launch_bounds__(kFpsThreads, 1) fps_cluster_kernel(FpsArgs a) 
     cluster_sync_all();
 
     if (k_start < k_stop) {
-        // last sample coordinates
-        int64_t last = out[k_start - 1];
-        float4 lv = xyz[last];
-        double sx = lv.x, sy = lv.y, sz = lv.z;
+        const int64_t last = a.fresh ? seed : out[k_start - 1];
+        const float4 lv = xyz[last];
+        float sx32 = lv.x, sy32 = lv.y, sz32 = lv.z;
 
         for (int64_t it = k_start; it < k_stop; ++it) {
             const uint32_t t = (uint32_t)(it - k_start);
             const uint32_t par = t & 1u;
             const uint32_t phase = (t >> 1) & 1u;
+            const bool tdbg = a.dbg && b == 0 && r == 0 && tid == 0 && t < 256;
+            long long ts0 = 0;
+            if (tdbg) ts0 = clock64();
+            const double sx = sx32, sy = sy32, sz = sz32;
 
             // 1. fold + thread argmax
             uint64_t bkey = 0;
             uint32_t bidx = kNone;
-            float bx = 0.f, by = 0.f, bz = 0.f;
-            uint32_t btk = 0;
+            Rec mine;
+            mine.pad = 0;
             if constexpr (P > 0) {
+                int bq = -1;
 #pragma unroll
                 for (int q = 0; q < P; ++q) {
-                    const int64_t j = lo + tid + (int64_t)q * kFpsThreads;
-                    if (j < hi) {
-                        const double d = sqdist(sx, sy, sz, px[q], py[q], pz[q]);
-                        if (d < m[q]) m[q] = d;
-                        const uint64_t key = dbits(m[q]);
-                        if (bidx == kNone || key > bkey) {
-                            bkey = key;
-                            bidx = (uint32_t)j;
-                            bx = (float)px[q]; by = (float)py[q]; bz = (float)pz[q];
-                            btk = (tk >> q) & 1u;
+                    if ((valid >> q) & 1u) {
+                        const float dx = fx[q] - sx32, dy = fy[q] - sy32, dz = fz[q] - sz32;
+                        const float d32 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+                        if (!(d32 > thr[q])) {
+                            const double d = sqdist(sx, sy, sz, (double)fx[q], (double)fy[q], (double)fz[q]);
+                            if (d < m[q]) {
+                                m[q] = d;
+                                thr[q] = skip_threshold(d);
+                            }
                         }
+                        const uint64_t key = dbits(m[q]);
+                        if (bq < 0 || key > bkey) { bkey = key; bq = q; }
                     }
+                }
+                if (bq >= 0) {
+                    bidx = (uint32_t)(lo + tid + (int64_t)bq * kFpsThreads);
+#pragma unroll
+                    for (int q = 0; q < P; ++q)
+                        if (q == bq) { mine.x = fx[q]; mine.y = fy[q]; mine.z = fz[q]; }
+                    mine.taken = (tk >> bq) & 1u;
                 }
             } else {
                 for (int64_t j = lo + tid; j < hi; j += kFpsThreads) {
@@ -208,46 +218,53 @@ __global__ void __launch_bounds__(kFpsThreads, 1) fps_cluster_kernel(FpsArgs a) 
                     const uint64_t key = dbits(mj);
                     if (bidx == kNone || key > bkey) {
                         bkey = key; bidx = (uint32_t)j;
-                        bx = v.x; by = v.y; bz = v.z;
+                        mine.x = v.x; mine.y = v.y; mine.z = v.z;
                     }
                 }
-                if (bidx != kNone) btk = taken[bidx];
+                if (bidx != kNone) mine.taken = taken[bidx];
             }
+            mine.klo = (uint32_t)bkey;
+            mine.khi = (uint32_t)(bkey >> 32);
+            mine.idx = bidx;
+            if (tdbg) a.dbg[t * 8 + 0] = clock64() - ts0;
 
-            // 2. warp argmax
-            const ArgMax wa = warp_argmax(bkey, bidx);
-            if (bidx == wa.idx && bidx != kNone) {
-                Rec rr;
-                rr.klo = (uint32_t)wa.key; rr.khi = (uint32_t)(wa.key >> 32);
-                rr.idx = wa.idx; rr.taken = btk;
-                rr.x = bx; rr.y = by; rr.z = bz; rr.pad = 0;
-                warp_rec[warp] = rr;
-            } else if (lane == 0 && wa.idx == kNone) {
-                Rec rr{};
-                rr.idx = kNone;
-                warp_rec[warp] = rr;
+            // 2. warp argmax: the winning lane publishes its record
+            const int wl = warp_argmax_lane(bkey, bidx);
+            if (wl < 0) {
+                if (lane == 0) { Rec z{}; z.idx = kNone; warp_rec[warp] = z; }
+            } else if (lane == wl) {
+                warp_rec[warp] = mine;
             }
+            if (tdbg) a.dbg[t * 8 + 1] = clock64() - ts0;
             __syncthreads();
+            if (tdbg) a.dbg[t * 8 + 2] = clock64() - ts0;
 
-            // 3+4. block argmax, push record to every CTA of the cluster
+            // 3+4. block argmax, push the CTA record to every CTA of the cluster
             if (warp == 0) {
-                const Rec cr = warp_reduce_recs(warp_rec, kFpsWarps, lane);
+                const Rec wr = lane < kFpsWarps ? warp_rec[lane] : Rec{0, 0, kNone, 0, 0.f, 0.f, 0.f, 0};
+                const int cl = warp_argmax_lane(rec_key(wr), wr.idx);
+                const Rec cr = warp_rec[cl < 0 ? 0 : cl];
                 if (lane < (int)C) {
                     const uint32_t dst = mapa(smem_u32(&slots[par][r]), lane);
                     const uint32_t dbar = mapa(smem_u32(&bars[par]), lane);
-                    st_async_v4(dst, dbar, cr.klo, cr.khi, cr.idx, cr.taken);
+                    st_async_v4(dst, dbar, cr.klo, cr.khi, cl < 0 ? kNone : cr.idx, cr.taken);
                     st_async_v4(dst + 16, dbar, __float_as_uint(cr.x), __float_as_uint(cr.y),
                                 __float_as_uint(cr.z), 0u);
                 }
             }
+            if (tdbg) a.dbg[t * 8 + 3] = clock64() - ts0;
 
             // 5. wait for all C records, reduce identically in every warp
             mbar_wait_cluster(&bars[par], phase);
-            Rec win = warp_reduce_recs(slots[par], (int)C, lane);
+            if (tdbg) a.dbg[t * 8 + 4] = clock64() - ts0;
+            const Rec sr = lane < (int)C ? slots[par][lane] : Rec{0, 0, kNone, 0, 0.f, 0.f, 0.f, 0};
+            const int gl = warp_argmax_lane(rec_key(sr), sr.idx);
+            Rec win = slots[par][gl < 0 ? 0 : gl];
             __syncwarp();
             if (tid == 0) mbar_arrive_expect_tx(&bars[par], C * (uint32_t)sizeof(Rec));
+            if (tdbg) a.dbg[t * 8 + 5] = clock64() - ts0;
 
-            double best = bitsd(((uint64_t)win.khi << 32) | win.klo);
+            double best = bitsd(rec_key(win));
             if (best <= 0.0 || win.taken) {
                 // duplicate fallback (_kernels.py:65-70): lowest untaken index
                 uint32_t fidx = kNone;
@@ -255,12 +272,11 @@ __global__ void __launch_bounds__(kFpsThreads, 1) fps_cluster_kernel(FpsArgs a) 
                 if constexpr (P > 0) {
 #pragma unroll
                     for (int q = P - 1; q >= 0; --q) {
-                        const int64_t j = lo + tid + (int64_t)q * kFpsThreads;
-                        if (j < hi && !((tk >> q) & 1u)) {
-                            fidx = (uint32_t)j;
+                        if (((valid >> q) & 1u) && !((tk >> q) & 1u)) {
+                            fidx = (uint32_t)(lo + tid + (int64_t)q * kFpsThreads);
                             const uint64_t k = dbits(m[q]);
                             fr.klo = (uint32_t)k; fr.khi = (uint32_t)(k >> 32);
-                            fr.x = (float)px[q]; fr.y = (float)py[q]; fr.z = (float)pz[q];
+                            fr.x = fx[q]; fr.y = fy[q]; fr.z = fz[q];
                         }
                     }
                 } else {
@@ -295,27 +311,28 @@ __global__ void __launch_bounds__(kFpsThreads, 1) fps_cluster_kernel(FpsArgs a) 
                 const Rec fw = warp_min_idx_recs(fb_slots, (int)C, lane);
                 if (fw.idx != kNone) {
                     win = fw;
-                    best = bitsd(((uint64_t)fw.khi << 32) | fw.klo);
+                    best = bitsd(rec_key(fw));
                 }
             }
 
-            // record, mark taken, next sample
+            // record (curve holds squared values until the epilogue), mark taken
             if (r == 0 && tid == 0) {
                 out[it] = (int64_t)win.idx;
-                curve[it] = sqrt(best);
+                curve[it] = best;
             }
-            const int64_t wj = (int64_t)win.idx;
+            const int64_t off = (int64_t)win.idx - lo - tid;
             if constexpr (P > 0) {
-                if (wj >= lo && wj < hi && ((wj - lo) % kFpsThreads) == tid)
-                    tk |= 1u << (uint32_t)((wj - lo) / kFpsThreads);
+                if (off >= 0 && (off % kFpsThreads) == 0 && off < (int64_t)P * kFpsThreads)
+                    tk |= 1u << (uint32_t)(off / kFpsThreads);
             } else {
-                if (wj >= lo && wj < hi && ((wj - lo) % kFpsThreads) == tid) taken[wj] = 1;
+                if (off >= 0 && (off % kFpsThreads) == 0 && (int64_t)win.idx < hi) taken[win.idx] = 1;
             }
-            sx = win.x; sy = win.y; sz = win.z;
+            sx32 = win.x; sy32 = win.y; sz32 = win.z;
+            if (tdbg) a.dbg[t * 8 + 6] = clock64() - ts0;
         }
     }
 
-    // ---- write back md / taken ---------------------------------------------
+    // ---- write back md / taken; curve = sqrt(best) (_kernels.py:72) ---------
     if constexpr (P > 0) {
 #pragma unroll
         for (int q = 0; q < P; ++q) {
@@ -325,6 +342,10 @@ __global__ void __launch_bounds__(kFpsThreads, 1) fps_cluster_kernel(FpsArgs a) 
                 taken[j] = (tk >> q) & 1u;
             }
         }
+    }
+    if (r == 0 && k_start < k_stop) {
+        __syncthreads();  // thread 0's curve stores are visible block-wide
+        for (int64_t it = k_start + tid; it < k_stop; it += kFpsThreads) curve[it] = sqrt(curve[it]);
     }
     cluster_sync_all();  // no CTA leaves while peers may still target its smem
 }
@@ -379,10 +400,7 @@ int fps_choose_cluster(int64_t N, int64_t B, int* C_out, int* P_out) {
     return 0;
 }
 
-cudaError_t launch_fps(FpsArgs a, int64_t B, cudaStream_t s) {
-    int C = 1, P = 0;
-    fps_choose_cluster(a.N, B, &C, &P);
-    a.points_per_cta = (a.N + C - 1) / C;
+static cudaError_t launch_any(const FpsArgs& a, int64_t B, int C, int P, cudaStream_t s) {
     switch (P) {
         case 1: return launch_p<1>(a, B, C, s);
         case 2: return launch_p<2>(a, B, C, s);
@@ -394,6 +412,37 @@ cudaError_t launch_fps(FpsArgs a, int64_t B, cudaStream_t s) {
         case 16: return launch_p<16>(a, B, C, s);
         default: return launch_p<0>(a, B, C, s);
     }
+}
+
+cudaError_t launch_fps(FpsArgs a, int64_t B, cudaStream_t s) {
+    int C = 1, P = 0;
+    fps_choose_cluster(a.N, B, &C, &P);
+    a.points_per_cta = (a.N + C - 1) / C;
+    a.dbg = nullptr;
+    if (getenv("PS_FPS_TIMING")) {
+        // development aid: per-phase SM cycles of the first 256 iterations
+        // (cloud 0, CTA rank 0, thread 0) printed to stderr; synchronises.
+        static long long* dbg = nullptr;
+        if (!dbg) cudaMalloc(&dbg, sizeof(long long) * 256 * 8);
+        cudaMemsetAsync(dbg, 0, sizeof(long long) * 256 * 8, s);
+        a.dbg = dbg;
+        cudaError_t e = launch_any(a, B, C, P, s);
+        if (e != cudaSuccess) return e;
+        long long h[256 * 8];
+        cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        const int iters = (int)((a.k_stop - a.k_start) < 256 ? (a.k_stop - a.k_start) : 256);
+        double acc[7] = {0};
+        int cnt = 0;
+        for (int t = 8; t < iters; ++t, ++cnt)
+            for (int k = 0; k < 7; ++k) acc[k] += (double)h[t * 8 + k];
+        if (cnt)
+            fprintf(stderr, "[fps timing] C=%d P=%d N=%lld iters=%d cycles: compute %.0f warpred %.0f bar %.0f send %.0f wait %.0f final %.0f total %.0f\n",
+                    C, P, (long long)a.N, cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt,
+                    acc[4] / cnt, acc[5] / cnt, acc[6] / cnt);
+        return cudaSuccess;
+    }
+    return launch_any(a, B, C, P, s);
 }
 
 }  // namespace ps

@@ -18,6 +18,7 @@ struct FpsArgs {
     int64_t N, ld_out, k_start, k_stop, seed;
     int fresh;                  // 1: md=+inf, taken={seed}, out[0]=seed, curve[0]=+inf
     int64_t points_per_cta;     // set by the launcher
+    long long* dbg;             // development timing buffer (PS_FPS_TIMING)
 };
 
 cudaError_t launch_fps(FpsArgs a, int64_t B, cudaStream_t s);

@@ -25,7 +25,7 @@ def main():
     B = bench.B_PER_GPU
     clouds = bench.clouds_for(0, B)
     fp = engine.FastPoint(B, bench.N, bench.n_SAMPLES, p=bench.P, nseg=bench.NSEG, estimator="power",
-                          exponent=0.45, extra_radii=(bench.RADIUS,))
+                          exponent=bench.heldout_exponent(), extra_radii=(bench.RADIUS,))
     fp.set_points(torch.from_numpy(clouds).cuda())
     for _ in range(2):
         fp.set_rng(list(range(B)))
