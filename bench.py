@@ -78,7 +78,8 @@ def heldout_exponent_cpu():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled every 100 ms during the
+    timed region (written to a temp file: nvidia-smi block-buffers pipes)."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
@@ -86,35 +87,42 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.proc = None
-        self.lines = []
+        self.path = None
 
     def __enter__(self):
+        import tempfile
+
+        fd, self.path = tempfile.mkstemp(prefix="ps_clocks_", suffix=".csv")
+        os.close(fd)
         try:
+            self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)  # first sample before the timed region starts
         except OSError:
             self.proc = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *exc):
         if self.proc is not None:
+            time.sleep(0.15)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
+            self.fh.close()
 
     def summary(self):
         sm, mx, reasons, util = [], None, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        try:
+            lines = open(self.path).read().splitlines()
+            os.unlink(self.path)
+        except (OSError, TypeError):
+            lines = []
+        for ln in lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 7:
                 continue
@@ -130,7 +138,7 @@ class ClockSampler:
                     reasons.add(nm)
         loaded = [s for s, u in zip(sm, util) if u > 0] or sm
         return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "samples_loaded": len(loaded)}
 
 
 def peaks():

@@ -393,16 +393,21 @@ __global__ void __launch_bounds__(256) grid_pairs_kernel(int64_t B, int64_t N, c
             const int row = (z * gp.ny + y) * gp.nx;
             const int t0 = cs[row + x0], t1 = cs[row + x1 + 1];  // cells x0..x1 are contiguous
             cand += (unsigned long long)(t1 - t0);
-            for (int t = t0; t < t1; ++t) {
-                const float4 q = sx[t];
-                if (no_filter || sqdist_f32(p, q) < thr) {
-                    const double d = sqdist4(p, q);
-                    if (d < r2) {
-                        if (FILL) {
-                            if (pos < end) { rn[pos] = si[t]; rd[pos] = d; }
-                            ++pos;
-                        } else {
-                            ++cnt;
+            for (int t = t0; t < t1; t += 4) {
+                float4 q4[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) q4[u] = t + u < t1 ? sx[t + u] : p;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (t + u < t1 && (no_filter || sqdist_f32(p, q4[u]) < thr)) {
+                        const double d = sqdist4(p, q4[u]);
+                        if (d < r2) {
+                            if (FILL) {
+                                if (pos < end) { rn[pos] = si[t + u]; rd[pos] = d; }
+                                ++pos;
+                            } else {
+                                ++cnt;
+                            }
                         }
                     }
                 }
@@ -417,8 +422,12 @@ __global__ void __launch_bounds__(256) grid_pairs_kernel(int64_t B, int64_t N, c
 
 // ---- row sort by (d2, index) + fused level counts -----------------------
 
+// (d2, index) order.  d2 >= 0 (or +inf padding), so its bit pattern orders
+// like an unsigned integer: integer compares keep the sort off the FP64 pipe.
 __device__ __forceinline__ bool key_less(double da, int32_t ia, double db, int32_t ib) {
-    return da < db || (da == db && ia < ib);
+    const unsigned long long ua = (unsigned long long)__double_as_longlong(da);
+    const unsigned long long ub = (unsigned long long)__double_as_longlong(db);
+    return ua < ub || (ua == ub && ia < ib);
 }
 
 // Bitonic sort of n2 (power of two) entries in shared memory by `nthr`

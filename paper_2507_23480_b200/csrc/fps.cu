@@ -185,24 +185,45 @@ __global__ void __launch_bounds__(kFpsThreads, 1) fps_cluster_kernel(FpsArgs a) 
             Rec mine;
             mine.pad = 0;
             if constexpr (P > 0) {
-                int bq = -1;
+                // 1a. float32 screen: which of my points can the new sample move?
+                uint32_t need = 0;
 #pragma unroll
                 for (int q = 0; q < P; ++q) {
-                    if ((valid >> q) & 1u) {
-                        const float dx = fx[q] - sx32, dy = fy[q] - sy32, dz = fz[q] - sz32;
-                        const float d32 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
-                        if (!(d32 > thr[q])) {
+                    const float dx = fx[q] - sx32, dy = fy[q] - sy32, dz = fz[q] - sz32;
+                    const float d32 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+                    need |= (((valid >> q) & 1u) && !(d32 > thr[q]) ? 1u : 0u) << q;
+                }
+                // 1b. exact float64 fold where needed (warp-uniform branches, predicated update)
+                if (__any_sync(kFull, need != 0)) {
+#pragma unroll
+                    for (int q = 0; q < P; ++q) {
+                        if (__any_sync(kFull, (need >> q) & 1u)) {
                             const double d = sqdist(sx, sy, sz, (double)fx[q], (double)fy[q], (double)fz[q]);
-                            if (d < m[q]) {
+                            if (((need >> q) & 1u) && d < m[q]) {
                                 m[q] = d;
                                 thr[q] = skip_threshold(d);
                             }
                         }
-                        const uint64_t key = dbits(m[q]);
-                        if (bq < 0 || key > bkey) { bkey = key; bq = q; }
                     }
                 }
-                if (bq >= 0) {
+                // 1c. tree argmax over my points: max md, lowest index on ties
+                double bv[P];
+                int bi[P];
+#pragma unroll
+                for (int q = 0; q < P; ++q) {
+                    bv[q] = ((valid >> q) & 1u) ? m[q] : -1.0;
+                    bi[q] = q;
+                }
+#pragma unroll
+                for (int st = 1; st < P; st <<= 1) {
+#pragma unroll
+                    for (int q = 0; q + st < P; q += 2 * st) {
+                        if (bv[q + st] > bv[q]) { bv[q] = bv[q + st]; bi[q] = bi[q + st]; }
+                    }
+                }
+                if (bv[0] >= 0.0) {
+                    const int bq = bi[0];
+                    bkey = dbits(bv[0]);
                     bidx = (uint32_t)(lo + tid + (int64_t)bq * kFpsThreads);
 #pragma unroll
                     for (int q = 0; q < P; ++q)
@@ -375,28 +396,88 @@ cudaError_t launch_p(const FpsArgs& a, int64_t B, int C, cudaStream_t s) {
 
 }  // namespace
 
-int fps_choose_cluster(int64_t N, int64_t B, int* C_out, int* P_out) {
+static int choose_P(int64_t N, int C) {
     static const int kPs[] = {1, 2, 3, 4, 6, 8, 12, 16};
+    const int64_t S = (N + C - 1) / C;
+    for (int p : kPs)
+        if ((int64_t)p * kFpsThreads >= S) return p;
+    return 0;  // streaming
+}
+
+template <int P>
+static int max_clusters_p(int C) {
+    auto kern = fps_cluster_kernel<P>;
+    if (C > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(C * 64), 1, 1);
+    cfg.blockDim = dim3(kFpsThreads, 1, 1);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+// Co-resident clusters of size C for the instantiation serving N (cached;
+// depends on the GPU's GPC floor-sweeping, so it is queried, not assumed).
+static int max_active_clusters(int64_t N, int C) {
+    static int cache[17][9];
+    static bool init = false;
+    if (!init) { for (auto& row : cache) for (int& v : row) v = -1; init = true; }
+    const int P = choose_P(N, C);
+    const int pi = P == 0 ? 0 : (P <= 4 ? P : (P == 6 ? 5 : (P == 8 ? 6 : (P == 12 ? 7 : 8))));
+    if (cache[C][pi] >= 0) return cache[C][pi];
+    int n = 0;
+    switch (P) {
+        case 1: n = max_clusters_p<1>(C); break;
+        case 2: n = max_clusters_p<2>(C); break;
+        case 3: n = max_clusters_p<3>(C); break;
+        case 4: n = max_clusters_p<4>(C); break;
+        case 6: n = max_clusters_p<6>(C); break;
+        case 8: n = max_clusters_p<8>(C); break;
+        case 12: n = max_clusters_p<12>(C); break;
+        case 16: n = max_clusters_p<16>(C); break;
+        default: n = max_clusters_p<0>(C); break;
+    }
+    cache[C][pi] = n;
+    return n;
+}
+
+int fps_choose_cluster(int64_t N, int64_t B, int* C_out, int* P_out) {
     const char* env = getenv("PS_FPS_CLUSTER");
     int C = 1;
     if (env) {
         C = atoi(env);
     } else {
+        // widest cluster (<= ~4 points per thread) whose B clusters are all
+        // co-resident: one wave, every cloud progressing in lock step
         const int64_t target = (int64_t)kFpsThreads * 4;
         int64_t c = (N + target - 1) / target;
-        C = (int)(c < 1 ? 1 : (c > kMaxCluster ? kMaxCluster : c));
-        // more clusters than fit in one wave: trade cluster width for concurrency
-        while (C > 8 && B * C > 128) C /= 2;
+        int want = (int)(c < 1 ? 1 : (c > kMaxCluster ? kMaxCluster : c));
+        int pick = 0;
+        for (int cc : {16, 12, 8, 6, 4, 3, 2, 1}) {
+            if (cc > want) continue;
+            if (choose_P(N, cc) == 0 && cc != kMaxCluster) continue;
+            if (max_active_clusters(N, cc) >= B) { pick = cc; break; }
+        }
+        if (!pick) {
+            // batch larger than one wave at any width: keep clusters <= 8 wide
+            pick = want > 8 ? 8 : want;
+        }
+        C = pick;
     }
     if (C < 1) C = 1;
     if (C > kMaxCluster) C = kMaxCluster;
-    const int64_t S = (N + C - 1) / C;
-    int P = 0;
-    for (int p : kPs) {
-        if ((int64_t)p * kFpsThreads >= S) { P = p; break; }
-    }
     *C_out = C;
-    *P_out = P;  // 0 = streaming
+    *P_out = choose_P(N, C);
     return 0;
 }
 

@@ -29,6 +29,8 @@
 // K3d replaces _kernels.earlyterm_scan (_kernels.py:356-367).
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "ps_internal.h"
@@ -60,7 +62,15 @@ __global__ void __launch_bounds__(1024) thresholds_kernel(ThreshArgs a) {
     if (threadIdx.x < kMaxSeg) seg_min[threadIdx.x] = 0x7ff0000000000000ull;  // +inf bits
     if (a.mode == 0 && threadIdx.x == 0) {
         double s = 0.0;
-        for (int64_t i = 1; i < k0; ++i) s = __dadd_rn(s, __dmul_rn(v[i], a.pow_tab[i]));
+        int64_t i = 1;
+        for (; i + 8 <= k0; i += 8) {  // loads hoisted, additions kept in order
+            double pv[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) pv[j] = __dmul_rn(v[i + j], a.pow_tab[i + j]);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) s = __dadd_rn(s, pv[j]);
+        }
+        for (; i < k0; ++i) s = __dadd_rn(s, __dmul_rn(v[i], a.pow_tab[i]));
         s_a = __ddiv_rn(s, (double)(k0 - 1));
     }
     __syncthreads();
@@ -195,22 +205,32 @@ PS_DEV void build_pool(const SampView& v, int seg, int64_t W, SampCtl* ctl, int*
 }
 
 // Clear point p (and its level-l row prefix) in the bitmaps of levels
-// [l0, nseg).  Called by `nl` cooperating lanes; the row is re-read per level
-// from L1 (the first level's read brings it in).
+// [l0, nseg).  `nl` cooperating lanes (sub-lane sl).  Level counts are loaded
+// in parallel and the row prefix is read once for the widest level (radii
+// are non-increasing in s, so count(l0) >= count(l) for l > l0).
 PS_DEV void clear_point_levels(const SampView& v, const SampArgs& a, int64_t b, int64_t W, int32_t p, int l0,
-                               int lane, int nl) {
+                               int sl, int nl) {
     const int64_t N = a.N;
+    const int nseg = a.nseg;
     const int64_t base = a.indptr[b * (N + 1) + p];
     const int32_t* nbr = a.nbr + b * a.cap_entries + base;
     const uint32_t pbit = ~(1u << (p & 31));
-    for (int l = l0; l < a.nseg; ++l) {
-        const int32_t c = a.counts[(b * a.L + a.seg_level_rows[l]) * N + p];
-        uint32_t* bm = v.bm + (int64_t)l * W;
-        for (int u = lane; u < c; u += nl) {
+    for (int lb = l0; lb < nseg; lb += 8) {
+        int c[8];
+#pragma unroll
+        for (int l = 0; l < 8; ++l)
+            c[l] = (lb + l < nseg) ? a.counts[(b * a.L + a.seg_level_rows[lb + l]) * N + p] : 0;
+        const int cmax = c[0];
+        for (int u = sl; u < cmax; u += nl) {
             const int32_t q = __ldg(nbr + u);
-            atomicAnd(&bm[q >> 5], ~(1u << (q & 31)));
+            const uint32_t bit = ~(1u << (q & 31));
+            uint32_t* w = v.bm + (int64_t)lb * W + (q >> 5);
+#pragma unroll
+            for (int l = 0; l < 8; ++l)
+                if (u < c[l]) atomicAnd(w + (int64_t)l * W, bit);
         }
-        if (lane == 0) atomicAnd(&bm[p >> 5], pbit);
+        if (sl == 0)
+            for (int l = lb; l < nseg; ++l) atomicAnd(&v.bm[(int64_t)l * W + (p >> 5)], pbit);
     }
 }
 
@@ -280,6 +300,18 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
     }
     int64_t* out = a.out_idx + b * a.ld_out;
     const int64_t k0 = a.k0, n_total = a.n_total;
+    // development timing (PS_SAMPLER_TIMING): cycles per phase, cloud 0, thread 0
+    const bool tdbg = a.dbg && b == 0 && tid == 0;
+    long long tacc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    long long tlast = tdbg ? clock64() : 0;
+#define PS_TMARK(k)                                  \
+    do {                                             \
+        if (tdbg) {                                  \
+            const long long _n = clock64();          \
+            tacc[k] += _n - tlast;                   \
+            tlast = _n;                              \
+        }                                            \
+    } while (0)
 
     // ---- init: all bits set (valid points), rank table empty --------------
     for (int64_t w = tid; w < (int64_t)nseg * W; w += blockDim.x) {
@@ -296,7 +328,11 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
     }
     __syncthreads();
     // pre-clear every prefix point's rows at all levels (_kernels.py:273-276)
-    for (int64_t t = warp; t < k0; t += nwarps) clear_point_levels(v, a, b, W, (int32_t)out[t], 0, lane, 32);
+    {
+        const int sub = lane >> 3, sl = lane & 7;
+        for (int64_t t = (int64_t)warp * 4 + sub; t < k0; t += (int64_t)nwarps * 4)
+            clear_point_levels(v, a, b, W, (int32_t)out[t], 0, sl, 8);
+    }
     for (int64_t t = k0 + tid; t < n_total; t += blockDim.x) out[t] = -1;
     __syncthreads();
 
@@ -314,6 +350,7 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
     }
     __syncthreads();
     if (!ctl.done) build_pool(v, ctl.seg, W, &ctl, warp_tot);
+    PS_TMARK(0);
 
     // ---- main loop: one iteration per segment visit ----------------------
     while (!ctl.done) {
@@ -329,6 +366,7 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
             __syncthreads();
             build_pool(v, ctl.seg, W, &ctl, warp_tot);
         }
+        PS_TMARK(1);
         const int seg = ctl.seg;
         const int64_t L = ctl.pool_len;
         const uint64_t state0 = ctl.state;
@@ -366,9 +404,11 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
                     cs.pos[t] = (uint32_t)(z % (uint64_t)(L - (k + t)));
                 }
                 __syncthreads();
+                PS_TMARK(2);
                 if (warp == 0) swap_chain_warp(v.pool, cs.pos, cs.cand, L, k, K, lane);
             }
             __syncthreads();
+            PS_TMARK(3);
             // availability + rank
             for (int t = tid; t < K; t += blockDim.x) {
                 const int32_t c = cs.cand[t];
@@ -377,6 +417,7 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
                 v.rank[c] = (uint16_t)t;
             }
             __syncthreads();
+            PS_TMARK(4);
             // greedy MIS, round 0: one pass over the level-seg row collects the
             // earlier available in-chunk neighbours (the only ones that matter)
             int und = 0;
@@ -417,6 +458,7 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
             __syncthreads();
             if (lane == 0 && und) atomicAdd(&ctl.undecided, und);
             __syncthreads();
+            PS_TMARK(5);
             // later rounds over the short predecessor lists
             while (ctl.undecided != 0) {
                 __syncthreads();
@@ -454,6 +496,7 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
                 if (lane == 0 && u2) atomicAdd(&ctl.undecided, u2);
                 __syncthreads();
             }
+            PS_TMARK(6);
             // ordered compaction of accepted candidates
             const int64_t need = a.boundaries[seg] - ctl.i;
             const int flag = (tid < K && cs.st[tid] == kIn) ? 1 : 0;
@@ -466,6 +509,7 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
                 if (ex == take - 1 && take == need) ctl.accepted = tid;  // draw of the last used accept
             }
             __syncthreads();
+            PS_TMARK(7);
             // clears: levels seg.. when the segment continues, seg+1.. when it ends
             const bool ends = (take == need);
             const int l0 = ends ? seg + 1 : seg;
@@ -482,11 +526,16 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
                 if (ends && !a.pick_lowest) ctl.state = state0 + (uint64_t)(k + ctl.accepted + 1) * kGolden;
             }
             __syncthreads();
+            PS_TMARK(8);
+            if (tdbg) tacc[9] += 1;
             if (ends) break;
             k += K;
         }
     }
     __syncthreads();
+    if (tdbg)
+        for (int k2 = 0; k2 < 10; ++k2) a.dbg[k2] = tacc[k2];
+#undef PS_TMARK
     if (tid == 0) {
         a.reached[b] = ctl.i;
         a.exhausted[b] = ctl.exhausted;
@@ -562,6 +611,14 @@ cudaError_t launch_thresholds(const ThreshArgs& a, int64_t B, cudaStream_t s) {
 }
 
 cudaError_t launch_sampler(SampArgs a, int64_t B, cudaStream_t s) {
+    a.dbg = nullptr;
+    static long long* dbg = nullptr;
+    const bool timing = getenv("PS_SAMPLER_TIMING") != nullptr;
+    if (timing) {
+        if (!dbg) cudaMalloc(&dbg, sizeof(long long) * 16);
+        cudaMemsetAsync(dbg, 0, sizeof(long long) * 16, s);
+        a.dbg = dbg;
+    }
     const size_t need = sampler_ws_bytes(a.N, a.nseg);
     size_t dsm = 0;
     if (a.use_smem) {
@@ -570,6 +627,14 @@ cudaError_t launch_sampler(SampArgs a, int64_t B, cudaStream_t s) {
         if (e != cudaSuccess) return e;
     }
     sampler_kernel<<<(unsigned)B, kSampThreads, dsm, s>>>(a);
+    if (timing) {
+        long long h[16];
+        cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        fprintf(stderr, "[sampler timing] cycles: init+preclear %lld pool %lld positions %lld swap %lld avail %lld "
+                "mis0 %lld mis_rounds %lld compact %lld clears %lld chunks %lld\n", h[0], h[1], h[2], h[3], h[4],
+                h[5], h[6], h[7], h[8], h[9]);
+    }
     return cudaGetLastError();
 }
 

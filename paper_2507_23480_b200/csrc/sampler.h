@@ -46,6 +46,7 @@ struct SampArgs {
     int use_smem;
     unsigned char* gws;          // global workspace (use_smem == 0)
     int64_t gws_stride;
+    long long* dbg;              // development timing (PS_SAMPLER_TIMING)
 };
 
 struct EtArgs {
