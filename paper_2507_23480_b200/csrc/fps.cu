@@ -93,8 +93,9 @@ PS_DEV float skip_threshold(double md) {
 // md, the argmax and every output are the float64 reference values.
 template <int P>
 __global__ void __launch_bounds__(kFpsThreads, 1) fps_cluster_kernel(FpsArgs a) {
+    constexpr int kSlots = kMaxCluster * kFpsWarps;  // one record per (CTA, warp)
     __shared__ Rec warp_rec[kFpsWarps];
-    __shared__ Rec slots[2][kMaxCluster];
+    __shared__ Rec slots[2][kSlots];
     __shared__ Rec fb_slots[kMaxCluster];
     __shared__ __align__(8) uint64_t bars[2];
 
@@ -116,12 +117,16 @@ __global__ void __launch_bounds__(kFpsThreads, 1) fps_cluster_kernel(FpsArgs a) 
     const int64_t k_stop = a.k_stop;
     const int64_t seed = a.seed_dev ? a.seed_dev[b] : a.seed;
     const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+    const uint32_t nrec = C * kFpsWarps;
+    const uint32_t tx_bytes = nrec * (uint32_t)sizeof(Rec);
 
     // ---- state into registers -------------------------------------------
     constexpr int PP = P > 0 ? P : 1;
     float fx[PP], fy[PP], fz[PP], thr[PP];
     double m[PP];
     uint32_t tk = 0, valid = 0;
+    double bv = -1.0;  // cached thread-local max md (P > 0) and its slot
+    int bq = 0;
     if constexpr (P > 0) {
 #pragma unroll
         for (int q = 0; q < P; ++q) {
@@ -140,7 +145,7 @@ __global__ void __launch_bounds__(kFpsThreads, 1) fps_cluster_kernel(FpsArgs a) 
                     tk |= (taken[j] ? 1u : 0u) << q;
                 }
             }
-            thr[q] = skip_threshold(m[q]);
+            thr[q] = ((valid >> q) & 1u) ? skip_threshold(m[q]) : -1.0f;  // invalid: never folded
         }
     } else {
         if (a.fresh) {
@@ -159,8 +164,8 @@ __global__ void __launch_bounds__(kFpsThreads, 1) fps_cluster_kernel(FpsArgs a) 
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
         fence_mbar_init_cluster();
-        mbar_arrive_expect_tx(&bars[0], C * (uint32_t)sizeof(Rec));
-        mbar_arrive_expect_tx(&bars[1], C * (uint32_t)sizeof(Rec));
+        mbar_arrive_expect_tx(&bars[0], tx_bytes);
+        mbar_arrive_expect_tx(&bars[1], tx_bytes);
     }
     // also orders the fresh-mode md/taken init (P == 0) before the loop
     cluster_sync_all();
@@ -169,6 +174,7 @@ __global__ void __launch_bounds__(kFpsThreads, 1) fps_cluster_kernel(FpsArgs a) 
         const int64_t last = a.fresh ? seed : out[k_start - 1];
         const float4 lv = xyz[last];
         float sx32 = lv.x, sy32 = lv.y, sz32 = lv.z;
+        bool dirty = true;  // recompute the cached local max
 
         for (int64_t it = k_start; it < k_stop; ++it) {
             const uint32_t t = (uint32_t)(it - k_start);
@@ -184,6 +190,8 @@ __global__ void __launch_bounds__(kFpsThreads, 1) fps_cluster_kernel(FpsArgs a) 
             uint32_t bidx = kNone;
             Rec mine;
             mine.pad = 0;
+            mine.taken = 0;
+            mine.x = mine.y = mine.z = 0.f;
             if constexpr (P > 0) {
                 // 1a. float32 screen: which of my points can the new sample move?
                 uint32_t need = 0;
@@ -191,7 +199,7 @@ __global__ void __launch_bounds__(kFpsThreads, 1) fps_cluster_kernel(FpsArgs a) 
                 for (int q = 0; q < P; ++q) {
                     const float dx = fx[q] - sx32, dy = fy[q] - sy32, dz = fz[q] - sz32;
                     const float d32 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
-                    need |= (((valid >> q) & 1u) && !(d32 > thr[q]) ? 1u : 0u) << q;
+                    need |= (!(d32 > thr[q]) ? 1u : 0u) << q;
                 }
                 // 1b. exact float64 fold where needed (warp-uniform branches, predicated update)
                 if (__any_sync(kFull, need != 0)) {
@@ -202,33 +210,32 @@ __global__ void __launch_bounds__(kFpsThreads, 1) fps_cluster_kernel(FpsArgs a) 
                             if (((need >> q) & 1u) && d < m[q]) {
                                 m[q] = d;
                                 thr[q] = skip_threshold(d);
+                                dirty = dirty || (q == bq);
                             }
                         }
                     }
                 }
-                // 1c. tree argmax over my points: max md, lowest index on ties
-                double bv[P];
-                int bi[P];
+                // 1c. the cached local max only changes when its own point moved
+                if (__any_sync(kFull, dirty)) {
+                    double tv[P];
+                    int ti[P];
 #pragma unroll
-                for (int q = 0; q < P; ++q) {
-                    bv[q] = ((valid >> q) & 1u) ? m[q] : -1.0;
-                    bi[q] = q;
-                }
-#pragma unroll
-                for (int st = 1; st < P; st <<= 1) {
-#pragma unroll
-                    for (int q = 0; q + st < P; q += 2 * st) {
-                        if (bv[q + st] > bv[q]) { bv[q] = bv[q + st]; bi[q] = bi[q + st]; }
+                    for (int q = 0; q < P; ++q) {
+                        tv[q] = ((valid >> q) & 1u) ? m[q] : -1.0;
+                        ti[q] = q;
                     }
-                }
-                if (bv[0] >= 0.0) {
-                    const int bq = bi[0];
-                    bkey = dbits(bv[0]);
-                    bidx = (uint32_t)(lo + tid + (int64_t)bq * kFpsThreads);
 #pragma unroll
-                    for (int q = 0; q < P; ++q)
-                        if (q == bq) { mine.x = fx[q]; mine.y = fy[q]; mine.z = fz[q]; }
-                    mine.taken = (tk >> bq) & 1u;
+                    for (int st = 1; st < P; st <<= 1) {
+#pragma unroll
+                        for (int q = 0; q + st < P; q += 2 * st)
+                            if (tv[q + st] > tv[q]) { tv[q] = tv[q + st]; ti[q] = ti[q + st]; }
+                    }
+                    if (dirty) { bv = tv[0]; bq = ti[0]; }
+                    dirty = false;
+                }
+                if (bv >= 0.0) {
+                    bkey = dbits(bv);
+                    bidx = (uint32_t)(lo + tid + (int64_t)bq * kFpsThreads);
                 }
             } else {
                 for (int64_t j = lo + tid; j < hi; j += kFpsThreads) {
@@ -242,47 +249,59 @@ __global__ void __launch_bounds__(kFpsThreads, 1) fps_cluster_kernel(FpsArgs a) 
                         mine.x = v.x; mine.y = v.y; mine.z = v.z;
                     }
                 }
-                if (bidx != kNone) mine.taken = taken[bidx];
             }
-            mine.klo = (uint32_t)bkey;
-            mine.khi = (uint32_t)(bkey >> 32);
-            mine.idx = bidx;
             if (tdbg) a.dbg[t * 8 + 0] = clock64() - ts0;
 
-            // 2. warp argmax: the winning lane publishes its record
+            // 2. warp argmax; the winning lane's record goes to every CTA of the
+            //    cluster (slot r * W + warp) -- no block barrier on the critical path
             const int wl = warp_argmax_lane(bkey, bidx);
-            if (wl < 0) {
-                if (lane == 0) { Rec z{}; z.idx = kNone; warp_rec[warp] = z; }
-            } else if (lane == wl) {
-                warp_rec[warp] = mine;
-            }
-            if (tdbg) a.dbg[t * 8 + 1] = clock64() - ts0;
-            __syncthreads();
-            if (tdbg) a.dbg[t * 8 + 2] = clock64() - ts0;
-
-            // 3+4. block argmax, push the CTA record to every CTA of the cluster
-            if (warp == 0) {
-                const Rec wr = lane < kFpsWarps ? warp_rec[lane] : Rec{0, 0, kNone, 0, 0.f, 0.f, 0.f, 0};
-                const int cl = warp_argmax_lane(rec_key(wr), wr.idx);
-                const Rec cr = warp_rec[cl < 0 ? 0 : cl];
+            {
+                const int src = wl < 0 ? 0 : wl;
+                if constexpr (P > 0) {
+                    if (lane == src) {
+#pragma unroll
+                        for (int q = 0; q < P; ++q)
+                            if (q == bq) { mine.x = fx[q]; mine.y = fy[q]; mine.z = fz[q]; }
+                        mine.taken = (tk >> bq) & 1u;
+                    }
+                } else {
+                    if (lane == src && bidx != kNone) mine.taken = taken[bidx];
+                }
+                const uint32_t w0 = __shfl_sync(kFull, (uint32_t)bkey, src);
+                const uint32_t w1 = __shfl_sync(kFull, (uint32_t)(bkey >> 32), src);
+                const uint32_t w2 = wl < 0 ? kNone : __shfl_sync(kFull, bidx, src);
+                const uint32_t w3 = __shfl_sync(kFull, mine.taken, src);
+                const uint32_t w4 = __shfl_sync(kFull, __float_as_uint(mine.x), src);
+                const uint32_t w5 = __shfl_sync(kFull, __float_as_uint(mine.y), src);
+                const uint32_t w6 = __shfl_sync(kFull, __float_as_uint(mine.z), src);
+                if (tdbg) a.dbg[t * 8 + 1] = clock64() - ts0;
                 if (lane < (int)C) {
-                    const uint32_t dst = mapa(smem_u32(&slots[par][r]), lane);
+                    const uint32_t dst = mapa(smem_u32(&slots[par][r * kFpsWarps + warp]), lane);
                     const uint32_t dbar = mapa(smem_u32(&bars[par]), lane);
-                    st_async_v4(dst, dbar, cr.klo, cr.khi, cl < 0 ? kNone : cr.idx, cr.taken);
-                    st_async_v4(dst + 16, dbar, __float_as_uint(cr.x), __float_as_uint(cr.y),
-                                __float_as_uint(cr.z), 0u);
+                    st_async_v4(dst, dbar, w0, w1, w2, w3);
+                    st_async_v4(dst + 16, dbar, w4, w5, w6, 0u);
                 }
             }
+            if (tdbg) a.dbg[t * 8 + 2] = clock64() - ts0;
             if (tdbg) a.dbg[t * 8 + 3] = clock64() - ts0;
 
-            // 5. wait for all C records, reduce identically in every warp
+            // 3. wait for all C * W records, reduce identically in every warp
             mbar_wait_cluster(&bars[par], phase);
             if (tdbg) a.dbg[t * 8 + 4] = clock64() - ts0;
-            const Rec sr = lane < (int)C ? slots[par][lane] : Rec{0, 0, kNone, 0, 0.f, 0.f, 0.f, 0};
-            const int gl = warp_argmax_lane(rec_key(sr), sr.idx);
-            Rec win = slots[par][gl < 0 ? 0 : gl];
+            double gv = -1.0;
+            uint32_t gi = kNone;
+            int gr = 0;
+            for (uint32_t k = (uint32_t)lane; k < nrec; k += 32) {
+                const uint2 kw = *reinterpret_cast<const uint2*>(&slots[par][k].klo);
+                const uint32_t ix = slots[par][k].idx;
+                const double v = __longlong_as_double((long long)(((uint64_t)kw.y << 32) | kw.x));
+                if (ix != kNone && (gi == kNone || v > gv || (v == gv && ix < gi))) { gv = v; gi = ix; gr = (int)k; }
+            }
+            const int gl = warp_argmax_lane(gi == kNone ? 0ull : dbits(gv), gi);
+            const int wr = __shfl_sync(kFull, gr, gl < 0 ? 0 : gl);
+            Rec win = slots[par][wr];
             __syncwarp();
-            if (tid == 0) mbar_arrive_expect_tx(&bars[par], C * (uint32_t)sizeof(Rec));
+            if (tid == 0) mbar_arrive_expect_tx(&bars[par], tx_bytes);
             if (tdbg) a.dbg[t * 8 + 5] = clock64() - ts0;
 
             double best = bitsd(rec_key(win));
@@ -334,6 +353,7 @@ __global__ void __launch_bounds__(kFpsThreads, 1) fps_cluster_kernel(FpsArgs a) 
                     win = fw;
                     best = bitsd(rec_key(fw));
                 }
+                cluster_sync_all();  // fb_slots / warp_rec free for the next fallback
             }
 
             // record (curve holds squared values until the epilogue), mark taken
@@ -343,8 +363,10 @@ __global__ void __launch_bounds__(kFpsThreads, 1) fps_cluster_kernel(FpsArgs a) 
             }
             const int64_t off = (int64_t)win.idx - lo - tid;
             if constexpr (P > 0) {
-                if (off >= 0 && (off % kFpsThreads) == 0 && off < (int64_t)P * kFpsThreads)
-                    tk |= 1u << (uint32_t)(off / kFpsThreads);
+                if (off >= 0 && (off % kFpsThreads) == 0 && off < (int64_t)P * kFpsThreads) {
+                    const int q = (int)(off / kFpsThreads);
+                    tk |= 1u << q;
+                }
             } else {
                 if (off >= 0 && (off % kFpsThreads) == 0 && (int64_t)win.idx < hi) taken[win.idx] = 1;
             }
