@@ -93,9 +93,8 @@ PS_DEV float skip_threshold(double md) {
 // md, the argmax and every output are the float64 reference values.
 template <int P>
 __global__ void __launch_bounds__(kFpsThreads, 1) fps_cluster_kernel(FpsArgs a) {
-    constexpr int kSlots = kMaxCluster * kFpsWarps;  // one record per (CTA, warp)
     __shared__ Rec warp_rec[kFpsWarps];
-    __shared__ Rec slots[2][kSlots];
+    __shared__ Rec slots[2][kMaxCluster];
     __shared__ Rec fb_slots[kMaxCluster];
     __shared__ __align__(8) uint64_t bars[2];
 
@@ -117,8 +116,7 @@ __global__ void __launch_bounds__(kFpsThreads, 1) fps_cluster_kernel(FpsArgs a) 
     const int64_t k_stop = a.k_stop;
     const int64_t seed = a.seed_dev ? a.seed_dev[b] : a.seed;
     const double kInf = __longlong_as_double(0x7ff0000000000000LL);
-    const uint32_t nrec = C * kFpsWarps;
-    const uint32_t tx_bytes = nrec * (uint32_t)sizeof(Rec);
+    const uint32_t tx_bytes = C * (uint32_t)sizeof(Rec);
 
     // ---- state into registers -------------------------------------------
     constexpr int PP = P > 0 ? P : 1;
@@ -252,54 +250,49 @@ __global__ void __launch_bounds__(kFpsThreads, 1) fps_cluster_kernel(FpsArgs a) 
             }
             if (tdbg) a.dbg[t * 8 + 0] = clock64() - ts0;
 
-            // 2. warp argmax; the winning lane's record goes to every CTA of the
-            //    cluster (slot r * W + warp) -- no block barrier on the critical path
+            // 2. warp argmax: the winning lane publishes its record
             const int wl = warp_argmax_lane(bkey, bidx);
-            {
-                const int src = wl < 0 ? 0 : wl;
+            if (wl < 0) {
+                if (lane == 0) { Rec z{}; z.idx = kNone; warp_rec[warp] = z; }
+            } else if (lane == wl) {
                 if constexpr (P > 0) {
-                    if (lane == src) {
 #pragma unroll
-                        for (int q = 0; q < P; ++q)
-                            if (q == bq) { mine.x = fx[q]; mine.y = fy[q]; mine.z = fz[q]; }
-                        mine.taken = (tk >> bq) & 1u;
-                    }
+                    for (int q = 0; q < P; ++q)
+                        if (q == bq) { mine.x = fx[q]; mine.y = fy[q]; mine.z = fz[q]; }
+                    mine.taken = (tk >> bq) & 1u;
                 } else {
-                    if (lane == src && bidx != kNone) mine.taken = taken[bidx];
+                    mine.taken = taken[bidx];
                 }
-                const uint32_t w0 = __shfl_sync(kFull, (uint32_t)bkey, src);
-                const uint32_t w1 = __shfl_sync(kFull, (uint32_t)(bkey >> 32), src);
-                const uint32_t w2 = wl < 0 ? kNone : __shfl_sync(kFull, bidx, src);
-                const uint32_t w3 = __shfl_sync(kFull, mine.taken, src);
-                const uint32_t w4 = __shfl_sync(kFull, __float_as_uint(mine.x), src);
-                const uint32_t w5 = __shfl_sync(kFull, __float_as_uint(mine.y), src);
-                const uint32_t w6 = __shfl_sync(kFull, __float_as_uint(mine.z), src);
-                if (tdbg) a.dbg[t * 8 + 1] = clock64() - ts0;
+                mine.klo = (uint32_t)bkey;
+                mine.khi = (uint32_t)(bkey >> 32);
+                mine.idx = bidx;
+                warp_rec[warp] = mine;
+            }
+            if (tdbg) a.dbg[t * 8 + 1] = clock64() - ts0;
+            __syncthreads();
+            if (tdbg) a.dbg[t * 8 + 2] = clock64() - ts0;
+
+            // 3+4. block argmax, push the CTA record to every CTA of the cluster
+            if (warp == 0) {
+                const Rec wr = lane < kFpsWarps ? warp_rec[lane] : Rec{0, 0, kNone, 0, 0.f, 0.f, 0.f, 0};
+                const int cl = warp_argmax_lane(rec_key(wr), wr.idx);
+                const Rec cr = warp_rec[cl < 0 ? 0 : cl];
                 if (lane < (int)C) {
-                    const uint32_t dst = mapa(smem_u32(&slots[par][r * kFpsWarps + warp]), lane);
+                    const uint32_t dst = mapa(smem_u32(&slots[par][r]), lane);
                     const uint32_t dbar = mapa(smem_u32(&bars[par]), lane);
-                    st_async_v4(dst, dbar, w0, w1, w2, w3);
-                    st_async_v4(dst + 16, dbar, w4, w5, w6, 0u);
+                    st_async_v4(dst, dbar, cr.klo, cr.khi, cl < 0 ? kNone : cr.idx, cr.taken);
+                    st_async_v4(dst + 16, dbar, __float_as_uint(cr.x), __float_as_uint(cr.y),
+                                __float_as_uint(cr.z), 0u);
                 }
             }
-            if (tdbg) a.dbg[t * 8 + 2] = clock64() - ts0;
             if (tdbg) a.dbg[t * 8 + 3] = clock64() - ts0;
 
-            // 3. wait for all C * W records, reduce identically in every warp
+            // 5. wait for all C records, reduce identically in every warp
             mbar_wait_cluster(&bars[par], phase);
             if (tdbg) a.dbg[t * 8 + 4] = clock64() - ts0;
-            double gv = -1.0;
-            uint32_t gi = kNone;
-            int gr = 0;
-            for (uint32_t k = (uint32_t)lane; k < nrec; k += 32) {
-                const uint2 kw = *reinterpret_cast<const uint2*>(&slots[par][k].klo);
-                const uint32_t ix = slots[par][k].idx;
-                const double v = __longlong_as_double((long long)(((uint64_t)kw.y << 32) | kw.x));
-                if (ix != kNone && (gi == kNone || v > gv || (v == gv && ix < gi))) { gv = v; gi = ix; gr = (int)k; }
-            }
-            const int gl = warp_argmax_lane(gi == kNone ? 0ull : dbits(gv), gi);
-            const int wr = __shfl_sync(kFull, gr, gl < 0 ? 0 : gl);
-            Rec win = slots[par][wr];
+            const Rec sr = lane < (int)C ? slots[par][lane] : Rec{0, 0, kNone, 0, 0.f, 0.f, 0.f, 0};
+            const int gl = warp_argmax_lane(rec_key(sr), sr.idx);
+            Rec win = slots[par][gl < 0 ? 0 : gl];
             __syncwarp();
             if (tid == 0) mbar_arrive_expect_tx(&bars[par], tx_bytes);
             if (tdbg) a.dbg[t * 8 + 5] = clock64() - ts0;
@@ -363,10 +356,9 @@ __global__ void __launch_bounds__(kFpsThreads, 1) fps_cluster_kernel(FpsArgs a) 
             }
             const int64_t off = (int64_t)win.idx - lo - tid;
             if constexpr (P > 0) {
-                if (off >= 0 && (off % kFpsThreads) == 0 && off < (int64_t)P * kFpsThreads) {
-                    const int q = (int)(off / kFpsThreads);
-                    tk |= 1u << q;
-                }
+                const uint32_t o32 = (uint32_t)off;  // wraps for off < 0: fails the range test
+                if (o32 < (uint32_t)(P * kFpsThreads) && (o32 & (kFpsThreads - 1)) == 0)
+                    tk |= 1u << (o32 / kFpsThreads);
             } else {
                 if (off >= 0 && (off % kFpsThreads) == 0 && (int64_t)win.idx < hi) taken[win.idx] = 1;
             }
