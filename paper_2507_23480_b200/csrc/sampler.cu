@@ -126,9 +126,11 @@ constexpr int kSampThreads = 1024;
 constexpr int kChunk = 1024;
 constexpr uint8_t kUndecided = 0, kIn = 1, kOut = 2;
 constexpr uint16_t kNoRank = 0xffffu;
+constexpr uint16_t kAcceptedMark = 0xfffeu;  // accepted earlier in the current segment
 
 struct SampCtl {
     int64_t i;
+    int64_t seg_i0;     // out[] position where the current segment visit started
     int seg;
     int entered;
     int exhausted;
@@ -200,7 +202,10 @@ PS_DEV void build_pool(const SampView& v, int seg, int64_t W, SampCtl* ctl, int*
         }
         carry += tot;
     }
-    if (threadIdx.x == 0) ctl->pool_len = carry;
+    if (threadIdx.x == 0) {
+        ctl->pool_len = carry;
+        ctl->seg_i0 = ctl->i;
+    }
     __syncthreads();
 }
 
@@ -275,6 +280,22 @@ PS_DEV void swap_chain_warp(int32_t* pool, const uint32_t* pos, int32_t* cand, i
         __syncwarp();
         g += nrun;
     }
+}
+
+// End of a segment visit: the points accepted in it (out[seg_i0, i)) clear
+// their rows in the bitmaps of every later segment, in one parallel batch,
+// and leave the rank table.  (Bitmap `seg` itself is never read again.)
+PS_DEV void end_visit(const SampView& v, const SampArgs& a, int64_t b, int64_t W, int seg, const int64_t* out,
+                      int64_t i0, int64_t i1) {
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    if (seg + 1 < a.nseg) {
+        const int sub = lane >> 3, sl = lane & 7;
+        for (int64_t x = i0 + (int64_t)warp * 4 + sub; x < i1; x += (int64_t)nwarps * 4)
+            clear_point_levels(v, a, b, W, (int32_t)out[x], seg + 1, sl, 8);
+    }
+    for (int64_t x = i0 + threadIdx.x; x < i1; x += blockDim.x) v.rank[out[x]] = kNoRank;
+    __syncthreads();
 }
 
 __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
@@ -374,12 +395,11 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
         const int32_t* cnt_row = a.counts + (b * a.L + lvl) * N;
         const int64_t* indptr = a.indptr + b * (N + 1);
         const int32_t* nbr_all = a.nbr + b * a.cap_entries;
-        const uint32_t* bms = v.bm + (int64_t)seg * W;
         int64_t k = 0;  // draws consumed in this segment visit
         for (;;) {
             if (k >= L) {
                 // pool exhausted: the picked < 0 path of _kernels.py:335-347
-                __syncthreads();
+                end_visit(v, a, b, W, seg, out, ctl.seg_i0, ctl.i);
                 if (tid == 0) {
                     if (!a.pick_lowest) ctl.state = state0 + (uint64_t)L * kGolden;
                     ctl.seg += 1;
@@ -410,10 +430,12 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
             __syncthreads();
             PS_TMARK(3);
             // availability + rank
+            // every pool entry was set at segment start; within the visit a bit
+            // only drops through an accepted neighbour, which the MIS sees via
+            // kAcceptedMark (earlier chunks) or the in-chunk ranks
             for (int t = tid; t < K; t += blockDim.x) {
                 const int32_t c = cs.cand[t];
-                const bool av = (bms[c >> 5] >> (c & 31)) & 1u;
-                cs.st[t] = av ? kUndecided : kOut;
+                cs.st[t] = kUndecided;
                 v.rank[c] = (uint16_t)t;
             }
             __syncthreads();
@@ -435,7 +457,9 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         const uint32_t rq = v.rank[q[j]];
-                        if (rq < (uint32_t)t) {
+                        if (rq == kAcceptedMark) {
+                            out_ = true;
+                        } else if (rq < (uint32_t)t) {
                             // OUT is final and never matters; IN rejects; UNDECIDED is remembered
                             const uint8_t sq = cs.st[rq];
                             if (sq == kIn) {
@@ -481,6 +505,7 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
                         const int32_t* row = nbr_all + indptr[c];
                         for (int32_t u = 0; u < m; ++u) {
                             const uint32_t rq = v.rank[row[u]];
+                            if (rq == kAcceptedMark) { out_ = true; break; }
                             if (rq < (uint32_t)t) {
                                 const uint8_t sq = cs.st[rq];
                                 if (sq == kIn) { out_ = true; break; }
@@ -510,16 +535,13 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
             }
             __syncthreads();
             PS_TMARK(7);
-            // clears: levels seg.. when the segment continues, seg+1.. when it ends
             const bool ends = (take == need);
-            const int l0 = ends ? seg + 1 : seg;
-            if (l0 < nseg) {
-                // 4 points per warp, 8 lanes each
-                const int sub = lane >> 3, sl = lane & 7;
-                for (int64_t x = (int64_t)warp * 4 + sub; x < take; x += (int64_t)nwarps * 4)
-                    clear_point_levels(v, a, b, W, (int32_t)out[i0 + x], l0, sl, 8);
-            }
+            // chunk candidates leave the rank table; accepted ones stay marked
+            // for the rest of the segment visit (level-seg exclusion)
             for (int t = tid; t < K; t += blockDim.x) v.rank[cs.cand[t]] = kNoRank;
+            __syncthreads();
+            if (!ends)
+                for (int64_t x = tid; x < take; x += blockDim.x) v.rank[out[i0 + x]] = kAcceptedMark;
             __syncthreads();
             if (tid == 0) {
                 ctl.i = i0 + take;
@@ -528,7 +550,11 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
             __syncthreads();
             PS_TMARK(8);
             if (tdbg) tacc[9] += 1;
-            if (ends) break;
+            if (ends) {
+                end_visit(v, a, b, W, seg, out, ctl.seg_i0, ctl.i);
+                PS_TMARK(7);
+                break;
+            }
             k += K;
         }
     }
