@@ -212,7 +212,7 @@ int ps_excl_build(const float* xyz4, int64_t B, int64_t N, const double* r2_leve
     ps::CsrView csr = {indptr, nbr, d2, counts, cap_entries, N, L};
     return cuda_status(ps::launch_excl_build(reinterpret_cast<const float4*>(xyz4), B, N, r2_levels, L, levels_ld,
                                              csr, ew, gw, method, S(stream)),
-                       "excl_build", method == 0 ? 6 : 9);
+                       "excl_build", method == 0 ? 6 : 8);
 }
 
 int ps_csr_sort_rows(int64_t* indptr, int32_t* nbr, double* d2, int64_t cap_entries, int64_t B, int64_t N,

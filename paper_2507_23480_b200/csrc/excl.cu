@@ -349,77 +349,6 @@ __global__ void grid_scatter_kernel(const float4* __restrict__ xyz, int64_t B, i
     }
 }
 
-// COUNT: deg[i] = #{j : d2(i, j) < r2max} (self included).  FILL: write row i.
-template <bool FILL>
-__global__ void __launch_bounds__(256) grid_pairs_kernel(int64_t B, int64_t N, const double* __restrict__ r2_levels,
-                                                         int L, int64_t levels_ld, GridWork g, ExclWork w,
-                                                         CsrView csr) {
-    const int64_t b = blockIdx.y;
-    const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    double r2 = 0.0;
-    for (int l = 0; l < L; ++l) r2 = fmax(r2, r2_levels[b * levels_ld + l]);
-    const float thr = prefilter_threshold(r2);
-    const bool no_filter = !(thr <= FLT_MAX);
-    if (s >= N) return;
-    const GridParams gp = g.params[b];
-    const float4* sx = g.sorted_xyz + b * N;
-    const int32_t* si = g.sorted_idx + b * N;
-    const int* cs = g.cell_start + b * (g.max_cells + 1);
-    const float4 p = sx[s];
-    const int32_t i = si[s];
-    const int cx = cell_coord(p.x, gp.ox, gp.inv_h, gp.nx);
-    const int cy = cell_coord(p.y, gp.oy, gp.inv_h, gp.ny);
-    const int cz = cell_coord(p.z, gp.oz, gp.inv_h, gp.nz);
-    int32_t* deg = w.deg + b * N;
-    int64_t pos = 0, end = 0;
-    int32_t* rn = nullptr;
-    double* rd = nullptr;
-    if (FILL) {
-        pos = csr.indptr[b * (N + 1) + i];
-        end = csr.indptr[b * (N + 1) + i + 1];
-        if (end > csr.cap_entries) return;  // overflow: status set by the scan
-        rn = csr.nbr + b * csr.cap_entries;
-        rd = csr.d2 + b * csr.cap_entries;
-    }
-    int cnt = 0;
-    unsigned long long cand = 0;
-    for (int dz = -1; dz <= 1; ++dz) {
-        const int z = cz + dz;
-        if (z < 0 || z >= gp.nz) continue;
-        for (int dy = -1; dy <= 1; ++dy) {
-            const int y = cy + dy;
-            if (y < 0 || y >= gp.ny) continue;
-            const int x0 = cx > 0 ? cx - 1 : 0, x1 = cx + 1 < gp.nx ? cx + 1 : gp.nx - 1;
-            const int row = (z * gp.ny + y) * gp.nx;
-            const int t0 = cs[row + x0], t1 = cs[row + x1 + 1];  // cells x0..x1 are contiguous
-            cand += (unsigned long long)(t1 - t0);
-            for (int t = t0; t < t1; t += 4) {
-                float4 q4[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) q4[u] = t + u < t1 ? sx[t + u] : p;
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    if (t + u < t1 && (no_filter || sqdist_f32(p, q4[u]) < thr)) {
-                        const double d = sqdist4(p, q4[u]);
-                        if (d < r2) {
-                            if (FILL) {
-                                if (pos < end) { rn[pos] = si[t + u]; rd[pos] = d; }
-                                ++pos;
-                            } else {
-                                ++cnt;
-                            }
-                        }
-                    }
-                }
-            }
-        }
-    }
-    if (!FILL) {
-        deg[i] = cnt;
-        atomicAdd(g.evals + b, cand);
-    }
-}
-
 // ---- row sort by (d2, index) + fused level counts -----------------------
 
 // (d2, index) order.  d2 >= 0 (or +inf padding), so its bit pattern orders
@@ -646,6 +575,139 @@ __global__ void level_counts_kernel(CsrView csr, int64_t B, const double* __rest
 
 }  // namespace
 
+// Warp-per-point grid pass.  COUNT: deg[i] = #{j : d2(i, j) < r2max}.
+// FILL: the row of i is collected in shared memory, sorted by (d2, index)
+// in registers (<= 64 entries) or shared memory (<= 256), written once in
+// final order, and its level counts are taken with ballots -- fill, sort and
+// csr_level_counts fused.  Longer rows are written unsorted and queued for
+// the CTA sort kernel.
+constexpr int kRowWarps = 8;
+constexpr int kRowCap = 256;
+
+template <bool FILL>
+__global__ void __launch_bounds__(kRowWarps * 32) grid_rows_kernel(int64_t B, int64_t N,
+                                                                   const double* __restrict__ r2_levels, int L,
+                                                                   int64_t levels_ld, GridWork g, ExclWork w,
+                                                                   CsrView csr) {
+    __shared__ double hd[FILL ? kRowWarps : 1][FILL ? kRowCap : 1];
+    __shared__ int32_t hj[FILL ? kRowWarps : 1][FILL ? kRowCap : 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+    for (int64_t gs = (int64_t)blockIdx.x * kRowWarps + warp; gs < B * N; gs += (int64_t)gridDim.x * kRowWarps) {
+        const int64_t b = gs / N, s = gs - b * N;
+        double r2 = 0.0;
+        for (int l = 0; l < L; ++l) r2 = fmax(r2, r2_levels[b * levels_ld + l]);
+        const float thr = prefilter_threshold(r2);
+        const bool no_filter = !(thr <= FLT_MAX);
+        const GridParams gp = g.params[b];
+        const float4* sx = g.sorted_xyz + b * N;
+        const int32_t* si = g.sorted_idx + b * N;
+        const int* cs = g.cell_start + b * (g.max_cells + 1);
+        const float4 p = sx[s];
+        const int32_t i = si[s];
+        const int cx = cell_coord(p.x, gp.ox, gp.inv_h, gp.nx);
+        const int cy = cell_coord(p.y, gp.oy, gp.inv_h, gp.ny);
+        const int cz = cell_coord(p.z, gp.oz, gp.inv_h, gp.nz);
+        int64_t rlo = 0, m = 0;
+        bool direct = false;
+        if (FILL) {
+            rlo = csr.indptr[b * (N + 1) + i];
+            m = csr.indptr[b * (N + 1) + i + 1] - rlo;
+            if (rlo + m > csr.cap_entries) continue;  // overflow: status set by the scan
+            direct = m > kRowCap;
+        }
+        int32_t* rn = FILL ? csr.nbr + b * csr.cap_entries + rlo : nullptr;
+        double* rd = FILL ? csr.d2 + b * csr.cap_entries + rlo : nullptr;
+        int cnt = 0;
+        unsigned long long cand = 0;
+        for (int dz = -1; dz <= 1; ++dz) {
+            const int z = cz + dz;
+            if (z < 0 || z >= gp.nz) continue;
+            for (int dy = -1; dy <= 1; ++dy) {
+                const int y = cy + dy;
+                if (y < 0 || y >= gp.ny) continue;
+                const int x0 = cx > 0 ? cx - 1 : 0, x1 = cx + 1 < gp.nx ? cx + 1 : gp.nx - 1;
+                const int row = (z * gp.ny + y) * gp.nx;
+                const int t0 = cs[row + x0], t1 = cs[row + x1 + 1];
+                cand += (unsigned long long)(t1 - t0);
+                for (int tb = t0; tb < t1; tb += 32) {
+                    const int t = tb + lane;
+                    bool hit = false;
+                    double d = 0.0;
+                    if (t < t1) {
+                        const float4 q = sx[t];
+                        if (no_filter || sqdist_f32(p, q) < thr) {
+                            d = sqdist4(p, q);
+                            hit = d < r2;
+                        }
+                    }
+                    const unsigned hm = __ballot_sync(kFull, hit);
+                    if (FILL && hit) {
+                        const int slot = cnt + __popc(hm & lt);
+                        if (direct) {
+                            if (slot < m) { rn[slot] = si[t]; rd[slot] = d; }
+                        } else if (slot < kRowCap) {
+                            hd[warp][slot] = d;
+                            hj[warp][slot] = si[t];
+                        }
+                    }
+                    cnt += __popc(hm);
+                }
+            }
+        }
+        if (!FILL) {
+            if (lane == 0) {
+                w.deg[b * N + i] = cnt;
+                atomicAdd(g.evals + b, cand);
+            }
+            continue;
+        }
+        __syncwarp();
+        if (direct) {
+            if (lane == 0) {
+                const unsigned k = atomicAdd(w.long_count, 1u);
+                w.long_rows[k] = (int32_t)(b * N + i);
+            }
+            continue;
+        }
+        const int mm = (int)m;
+        const double* lv = r2_levels + b * levels_ld;
+        if (mm <= 64) {
+            double d0 = lane < mm ? hd[warp][lane] : kInf;
+            int32_t i0 = lane < mm ? hj[warp][lane] : 0x7fffffff;
+            double d1 = lane + 32 < mm ? hd[warp][lane + 32] : kInf;
+            int32_t i1 = lane + 32 < mm ? hj[warp][lane + 32] : 0x7fffffff;
+            int n2 = 2;
+            while (n2 < mm) n2 <<= 1;
+            if (mm > 1) warp_bitonic64(d0, i0, d1, i1, lane, n2);
+            if (lane < mm) { rd[lane] = d0; rn[lane] = i0; }
+            if (lane + 32 < mm) { rd[lane + 32] = d1; rn[lane + 32] = i1; }
+            for (int l = 0; l < csr.L; ++l) {
+                const double t = lv[l];
+                const int c = __popc(__ballot_sync(kFull, lane < mm && d0 < t)) +
+                              __popc(__ballot_sync(kFull, lane + 32 < mm && d1 < t));
+                if (lane == 0) csr.counts[(b * csr.L + l) * N + i] = c;
+            }
+        } else {
+            int n2 = 1;
+            while (n2 < mm) n2 <<= 1;
+            for (int k = mm + lane; k < n2; k += 32) { hd[warp][k] = kInf; hj[warp][k] = 0x7fffffff; }
+            __syncwarp();
+            bitonic_smem(hd[warp], hj[warp], n2, lane, 32, [] { __syncwarp(); });
+            for (int k = lane; k < mm; k += 32) { rd[k] = hd[warp][k]; rn[k] = hj[warp][k]; }
+            for (int l = 0; l < csr.L; ++l) {
+                const double t = lv[l];
+                int c = 0;
+                for (int k = lane; k < mm; k += 32) c += hd[warp][k] < t ? 1 : 0;
+                c = __reduce_add_sync(kFull, c);
+                if (lane == 0) csr.counts[(b * csr.L + l) * N + i] = c;
+            }
+        }
+        __syncwarp();
+    }
+}
+
 static cudaError_t launch_sort(CsrView csr, int64_t B, const double* r2_levels, int64_t levels_ld, ExclWork w,
                                cudaStream_t s) {
     excl_sort_small_kernel<<<148 * 8, kSortWarps * 32, 0, s>>>(csr, B, r2_levels, levels_ld, w);
@@ -676,10 +738,20 @@ cudaError_t launch_excl_build(const float4* xyz, int64_t B, int64_t N, const dou
         grid_scan_kernel<<<(unsigned)B, 1024, 0, s>>>(N, g);
         grid_scatter_kernel<<<gpts, 256, 0, s>>>(xyz, B, N, g);
         const dim3 gp((unsigned)((N + 255) / 256), (unsigned)B);
-        grid_pairs_kernel<false><<<gp, 256, 0, s>>>(B, N, r2_levels, L, levels_ld, g, w, csr);
+        (void)gp;
+        const unsigned grow = (unsigned)std::min<int64_t>(148 * 16, (B * N + kRowWarps - 1) / kRowWarps);
+        grid_rows_kernel<false><<<grow, kRowWarps * 32, 0, s>>>(B, N, r2_levels, L, levels_ld, g, w, csr);
         excl_scan_kernel<<<(unsigned)B, 1024, 0, s>>>(N, w, csr, 0);
-        grid_pairs_kernel<true><<<gp, 256, 0, s>>>(B, N, r2_levels, L, levels_ld, g, w, csr);
-        return launch_sort(csr, B, r2_levels, levels_ld, w, s);
+        grid_rows_kernel<true><<<grow, kRowWarps * 32, 0, s>>>(B, N, r2_levels, L, levels_ld, g, w, csr);
+        const size_t dsm = (sizeof(double) + sizeof(int32_t)) * kCtaRowCap;
+        static bool attr_set2 = false;
+        if (!attr_set2) {
+            e = cudaFuncSetAttribute(excl_sort_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+            if (e != cudaSuccess) return e;
+            attr_set2 = true;
+        }
+        excl_sort_large_kernel<<<148, 1024, dsm, s>>>(csr, r2_levels, levels_ld, w);
+        return cudaGetLastError();
     }
     if ((e = cudaMemsetAsync(w.edge_count, 0, sizeof(unsigned long long) * B, s)) != cudaSuccess) return e;
     const int64_t nt = (N + kTile - 1) / kTile;

@@ -123,7 +123,6 @@ __global__ void __launch_bounds__(1024) thresholds_kernel(ThreshArgs a) {
 // K3c: sampler
 
 constexpr int kSampThreads = 1024;
-constexpr int kChunk = 1024;
 constexpr uint8_t kUndecided = 0, kIn = 1, kOut = 2;
 constexpr uint16_t kNoRank = 0xffffu;
 constexpr uint16_t kAcceptedMark = 0xfffeu;  // accepted earlier in the current segment
@@ -177,13 +176,6 @@ struct SampView {
     uint16_t* rank;    // [N] draw rank within the current chunk (0xffff = none)
 };
 
-struct ChunkSmem {
-    int32_t cand[kChunk];
-    uint32_t pos[kChunk];
-    uint16_t preds[kChunk][kMaxPred];  // earlier available in-chunk neighbours
-    uint8_t st[kChunk];
-    uint8_t npred[kChunk];
-};
 
 PS_DEV void build_pool(const SampView& v, int seg, int64_t W, SampCtl* ctl, int* warp_tot) {
     const uint32_t* row = v.bm + (int64_t)seg * W;
@@ -239,24 +231,76 @@ PS_DEV void clear_point_levels(const SampView& v, const SampArgs& a, int64_t b, 
     }
 }
 
-// Swap-remove chain for draws k .. k+K-1 (pool length before draw t is L-t),
-// run by one warp: groups of up to 32 consecutive draws execute in parallel
-// up to the first draw whose read locations an earlier draw of the group
-// writes (same position, or a position equal to its last slot).  Identical
-// to the serial chain of _kernels.py:325-330.
-PS_DEV void swap_chain_warp(int32_t* pool, const uint32_t* pos, int32_t* cand, int64_t L, int64_t k, int K,
-                            int lane) {
+// ---- producer / consumer split -------------------------------------------
+// Warp 0 produces the candidate order (positions + swap-remove chain) for the
+// next chunk while warps 1..31 decide the current one, so the serial chain is
+// off the critical path.  Hand-off through two chunk buffers, volatile
+// counters in shared memory, and named barrier 1 among the 992 consumers.
+constexpr int kConsThreads = kSampThreads - 32;
+
+PS_DEV void cons_bar() { asm volatile("bar.sync 1, 992;" ::: "memory"); }
+
+PS_DEV int vload(const int* p) { return *(volatile const int*)p; }
+PS_DEV void vstore(int* p, int v) { *(volatile int*)p = v; }
+
+// exclusive scan of one int per consumer thread (ct in [0, 992))
+PS_DEV int cons_excl_scan(int v, int* warp_tot, int* total) {
+    const int lane = threadIdx.x & 31, cw = (threadIdx.x >> 5) - 1;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[cw] = x;
+    cons_bar();
+    if (cw == 0) {
+        int s = lane < 31 ? warp_tot[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, s, o);
+            if (lane >= o) s += y;
+        }
+        warp_tot[lane] = s;
+    }
+    cons_bar();
+    const int ex = (cw ? warp_tot[cw - 1] : 0) + x - v;
+    *total = warp_tot[30];
+    cons_bar();
+    return ex;
+}
+
+// Candidate order for draws k .. k+K-1 (pool length before draw t is L - t):
+// position z_t mod (L - t) with z_t = splitmix64(state0 + (t+1) GOLDEN), then
+// the swap-remove of _kernels.py:325-330.  Groups of up to 32 consecutive
+// draws run in parallel up to the first draw whose read locations an earlier
+// draw of the group writes (same position, or its last slot); positions of
+// the unexecuted draws carry over to the next group.
+PS_DEV void produce_chunk(int32_t* pool, int32_t* cand, uint64_t state0, int64_t L, int64_t k, int K, int lane,
+                          bool pick_lowest) {
+    if (pick_lowest) {
+        for (int t = lane; t < K; t += 32) cand[t] = pool[k + t];
+        __syncwarp();
+        return;
+    }
     const unsigned lt = (1u << lane) - 1u;
     int g = 0;
+    int have = 0;  // lanes [0, have) hold valid positions for draws g .. g+have-1
+    uint32_t p = 0;
     while (g < K) {
-        const int t = g + lane;
-        const bool act = t < K;
-        const uint32_t p = act ? pos[t] : 0x80000000u | (uint32_t)lane;
-        const int64_t last0 = L - 1 - (k + g);               // last slot of draw g
-        const int64_t last = last0 - lane;                    // last slot of this draw
-        const unsigned same = __match_any_sync(kFull, p);
-        bool conflict = act && (same & lt) != 0;              // earlier draw wrote my position
-        // earlier draw i writes p_i == last_j for j = last0 - p_i > i
+        if (lane >= have) {
+            const int64_t t = k + g + lane;
+            if (g + lane < K) {
+                const uint64_t z = mix64(state0 + (uint64_t)(t + 1) * kGolden);
+                p = (uint32_t)(z % (uint64_t)(L - t));
+            }
+        }
+        const bool act = g + lane < K;
+        const uint32_t key = act ? p : (0x80000000u | (uint32_t)lane);
+        const int64_t last0 = L - 1 - (k + g);
+        const int64_t last = last0 - lane;
+        const unsigned same = __match_any_sync(kFull, key);
+        bool conflict = act && (same & lt) != 0;
         unsigned mark = 0;
         if (act) {
             const int64_t j = last0 - (int64_t)p;
@@ -265,7 +309,7 @@ PS_DEV void swap_chain_warp(int32_t* pool, const uint32_t* pos, int32_t* cand, i
         mark = __reduce_or_sync(kFull, mark);
         conflict = conflict || ((mark >> lane) & 1u);
         const unsigned cmask = __ballot_sync(kFull, conflict);
-        const int run = cmask ? (__ffs(cmask) - 1) : 32;      // >= 1 (lane 0 never conflicts)
+        const int run = cmask ? (__ffs(cmask) - 1) : 32;
         const int nrun = min(run, K - g);
         int32_t vp = 0, vl = 0;
         if (lane < nrun) {
@@ -275,9 +319,11 @@ PS_DEV void swap_chain_warp(int32_t* pool, const uint32_t* pos, int32_t* cand, i
         __syncwarp();
         if (lane < nrun) {
             pool[p] = vl;
-            cand[t] = vp;
+            cand[g + lane] = vp;
         }
         __syncwarp();
+        p = __shfl_down_sync(kFull, p, nrun & 31);
+        have = 32 - nrun;
         g += nrun;
     }
 }
@@ -302,12 +348,17 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
     extern __shared__ __align__(16) unsigned char dyn[];
     __shared__ SampCtl ctl;
     __shared__ int warp_tot[32];
-    __shared__ ChunkSmem cs;
+    __shared__ int32_t cbuf[2][kConsThreads];
+    __shared__ uint16_t preds[kConsThreads][kMaxPred];
+    __shared__ uint8_t st[kConsThreads];
+    __shared__ uint8_t npred[kConsThreads];
+    __shared__ int prod_count, cons_count, stop_flag, visit_exhausted;
     const int64_t b = blockIdx.x;
     const int64_t N = a.N;
     const int64_t W = (N + 31) >> 5;
     const int nseg = a.nseg;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    const int ct = tid - 32;  // consumer thread index (warps 1..31)
 
     // big tables: shared memory when they fit, else this cloud's global slice
     unsigned char* ws = a.use_smem ? dyn : (a.gws + b * a.gws_stride);
@@ -321,8 +372,8 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
     }
     int64_t* out = a.out_idx + b * a.ld_out;
     const int64_t k0 = a.k0, n_total = a.n_total;
-    // development timing (PS_SAMPLER_TIMING): cycles per phase, cloud 0, thread 0
-    const bool tdbg = a.dbg && b == 0 && tid == 0;
+    // development timing (PS_SAMPLER_TIMING): cycles per phase, cloud 0, first consumer
+    const bool tdbg = a.dbg && b == 0 && tid == 32;
     long long tacc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     long long tlast = tdbg ? clock64() : 0;
 #define PS_TMARK(k)                                  \
@@ -395,168 +446,172 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
         const int32_t* cnt_row = a.counts + (b * a.L + lvl) * N;
         const int64_t* indptr = a.indptr + b * (N + 1);
         const int32_t* nbr_all = a.nbr + b * a.cap_entries;
-        int64_t k = 0;  // draws consumed in this segment visit
-        for (;;) {
-            if (k >= L) {
-                // pool exhausted: the picked < 0 path of _kernels.py:335-347
-                end_visit(v, a, b, W, seg, out, ctl.seg_i0, ctl.i);
-                if (tid == 0) {
-                    if (!a.pick_lowest) ctl.state = state0 + (uint64_t)L * kGolden;
-                    ctl.seg += 1;
-                    if (ctl.seg >= nseg) {
-                        ctl.exhausted = 1;
-                        ctl.done = 1;
-                    } else {
-                        ctl.entered += 1;
-                    }
+        if (tid == 0) {
+            prod_count = 0;
+            cons_count = 0;
+            stop_flag = 0;
+            visit_exhausted = 0;
+        }
+        __syncthreads();
+
+        if (warp == 0) {
+            // ---------------- producer ----------------
+            for (int c = 0;; ++c) {
+                const int64_t kc = (int64_t)c * kConsThreads;
+                if (kc >= L) break;
+                // buffer c&1 is free once chunk c-2 was released
+                while (vload(&cons_count) < c - 1 && !vload(&stop_flag)) __nanosleep(32);
+                if (vload(&stop_flag)) break;
+                const int K = (int)((L - kc) < kConsThreads ? (L - kc) : kConsThreads);
+                produce_chunk(v.pool, cbuf[c & 1], state0, L, kc, K, lane, a.pick_lowest != 0);
+                __threadfence_block();
+                if (lane == 0) vstore(&prod_count, c + 1);
+            }
+        } else {
+            // ---------------- consumers ----------------
+            for (int c = 0;; ++c) {
+                const int64_t kc = (int64_t)c * kConsThreads;
+                if (kc >= L) {
+                    // pool exhausted: the picked < 0 path of _kernels.py:335-347
+                    if (ct == 0) { vstore(&visit_exhausted, 1); vstore(&stop_flag, 1); }
+                    break;
                 }
-                __syncthreads();
-                if (!ctl.done) build_pool(v, ctl.seg, W, &ctl, warp_tot);
-                break;
-            }
-            const int K = (int)((L - k) < kChunk ? (L - k) : kChunk);
-            // candidate order for draws k .. k+K-1
-            if (a.pick_lowest) {
-                for (int t = tid; t < K; t += blockDim.x) cs.cand[t] = v.pool[k + t];
-            } else {
-                for (int t = tid; t < K; t += blockDim.x) {
-                    const uint64_t z = mix64(state0 + (uint64_t)(k + t + 1) * kGolden);
-                    cs.pos[t] = (uint32_t)(z % (uint64_t)(L - (k + t)));
+                const int K = (int)((L - kc) < kConsThreads ? (L - kc) : kConsThreads);
+                if (ct == 0)
+                    while (vload(&prod_count) <= c) __nanosleep(20);
+                cons_bar();
+                __threadfence_block();
+                PS_TMARK(3);
+                const int32_t* cand = cbuf[c & 1];
+                const int32_t cme = ct < K ? cand[ct] : 0;
+                if (ct < K) {
+                    st[ct] = kUndecided;
+                    v.rank[cme] = (uint16_t)ct;
                 }
-                __syncthreads();
-                PS_TMARK(2);
-                if (warp == 0) swap_chain_warp(v.pool, cs.pos, cs.cand, L, k, K, lane);
-            }
-            __syncthreads();
-            PS_TMARK(3);
-            // availability + rank
-            // every pool entry was set at segment start; within the visit a bit
-            // only drops through an accepted neighbour, which the MIS sees via
-            // kAcceptedMark (earlier chunks) or the in-chunk ranks
-            for (int t = tid; t < K; t += blockDim.x) {
-                const int32_t c = cs.cand[t];
-                cs.st[t] = kUndecided;
-                v.rank[c] = (uint16_t)t;
-            }
-            __syncthreads();
-            PS_TMARK(4);
-            // greedy MIS, round 0: one pass over the level-seg row collects the
-            // earlier available in-chunk neighbours (the only ones that matter)
-            int und = 0;
-            for (int t = tid; t < K; t += blockDim.x) {
-                if (cs.st[t] != kUndecided) { cs.npred[t] = 0; continue; }
-                const int32_t c = cs.cand[t];
-                const int32_t m = cnt_row[c];
-                const int32_t* row = nbr_all + indptr[c];
-                int np = 0;
-                bool out_ = false, blocked = false;
-                for (int32_t u0 = 0; u0 < m; u0 += 8) {
-                    int32_t q[8];
+                if (ct == 0) ctl.undecided = 0;
+                cons_bar();
+                // every consumer holds its candidate in a register now: release the buffer
+                if (ct == 0) vstore(&cons_count, c + 1);
+                PS_TMARK(4);
+                // greedy MIS, round 0: one pass over the level-seg row
+                int und = 0;
+                if (ct < K) {
+                    const int t = ct;
+                    const int32_t m = cnt_row[cme];
+                    const int32_t* row = nbr_all + indptr[cme];
+                    int np = 0;
+                    bool out_ = false, blocked = false;
+                    for (int32_t u0 = 0; u0 < m; u0 += 8) {
+                        int32_t q[8];
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) q[j] = (u0 + j < m) ? __ldg(row + u0 + j) : c;
+                        for (int j = 0; j < 8; ++j) q[j] = (u0 + j < m) ? __ldg(row + u0 + j) : cme;
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const uint32_t rq = v.rank[q[j]];
-                        if (rq == kAcceptedMark) {
-                            out_ = true;
-                        } else if (rq < (uint32_t)t) {
-                            // OUT is final and never matters; IN rejects; UNDECIDED is remembered
-                            const uint8_t sq = cs.st[rq];
-                            if (sq == kIn) {
+                        for (int j = 0; j < 8; ++j) {
+                            const uint32_t rq = v.rank[q[j]];
+                            if (rq == kAcceptedMark) {
                                 out_ = true;
-                            } else if (sq == kUndecided) {
-                                if (np < kMaxPred) cs.preds[t][np] = (uint16_t)rq;
-                                ++np;
-                                blocked = true;
+                            } else if (rq < (uint32_t)t) {
+                                // OUT is final and never matters; IN rejects; UNDECIDED is remembered
+                                const uint8_t sq = st[rq];
+                                if (sq == kIn) {
+                                    out_ = true;
+                                } else if (sq == kUndecided) {
+                                    if (np < kMaxPred) preds[t][np] = (uint16_t)rq;
+                                    ++np;
+                                    blocked = true;
+                                }
                             }
                         }
                     }
+                    npred[t] = np > kMaxPred ? kPredOverflow : (uint8_t)np;
+                    if (out_) st[t] = kOut;
+                    else if (!blocked) st[t] = kIn;
+                    else und = 1;
                 }
-                cs.npred[t] = np > kMaxPred ? kPredOverflow : (uint8_t)np;
-                if (out_) cs.st[t] = kOut;
-                else if (!blocked) cs.st[t] = kIn;
-                else ++und;
-            }
-            und = __reduce_add_sync(kFull, und);
-            if (tid == 0) ctl.undecided = 0;
-            __syncthreads();
-            if (lane == 0 && und) atomicAdd(&ctl.undecided, und);
-            __syncthreads();
-            PS_TMARK(5);
-            // later rounds over the short predecessor lists
-            while (ctl.undecided != 0) {
-                __syncthreads();
-                if (tid == 0) ctl.undecided = 0;
-                __syncthreads();
-                int u2 = 0;
-                for (int t = tid; t < K; t += blockDim.x) {
-                    if (cs.st[t] != kUndecided) continue;
-                    bool out_ = false, blocked = false;
-                    const uint8_t np = cs.npred[t];
-                    if (np != kPredOverflow) {
-                        for (int j = 0; j < np; ++j) {
-                            const uint8_t sq = cs.st[cs.preds[t][j]];
-                            if (sq == kIn) { out_ = true; break; }
-                            if (sq == kUndecided) blocked = true;
-                        }
-                    } else {
-                        const int32_t c = cs.cand[t];
-                        const int32_t m = cnt_row[c];
-                        const int32_t* row = nbr_all + indptr[c];
-                        for (int32_t u = 0; u < m; ++u) {
-                            const uint32_t rq = v.rank[row[u]];
-                            if (rq == kAcceptedMark) { out_ = true; break; }
-                            if (rq < (uint32_t)t) {
-                                const uint8_t sq = cs.st[rq];
+                und = __reduce_add_sync(kFull, und);
+                if (lane == 0 && und) atomicAdd(&ctl.undecided, und);
+                cons_bar();
+                PS_TMARK(5);
+                // later rounds over the short predecessor lists
+                while (ctl.undecided != 0) {
+                    cons_bar();
+                    if (ct == 0) ctl.undecided = 0;
+                    cons_bar();
+                    int u2 = 0;
+                    if (ct < K && st[ct] == kUndecided) {
+                        const int t = ct;
+                        bool out_ = false, blocked = false;
+                        const uint8_t np = npred[t];
+                        if (np != kPredOverflow) {
+                            for (int j = 0; j < np; ++j) {
+                                const uint8_t sq = st[preds[t][j]];
                                 if (sq == kIn) { out_ = true; break; }
                                 if (sq == kUndecided) blocked = true;
                             }
+                        } else {
+                            const int32_t m = cnt_row[cme];
+                            const int32_t* row = nbr_all + indptr[cme];
+                            for (int32_t u = 0; u < m; ++u) {
+                                const uint32_t rq = v.rank[row[u]];
+                                if (rq == kAcceptedMark) { out_ = true; break; }
+                                if (rq < (uint32_t)t) {
+                                    const uint8_t sq = st[rq];
+                                    if (sq == kIn) { out_ = true; break; }
+                                    if (sq == kUndecided) blocked = true;
+                                }
+                            }
                         }
+                        if (out_) st[t] = kOut;
+                        else if (!blocked) st[t] = kIn;
+                        else u2 = 1;
                     }
-                    if (out_) cs.st[t] = kOut;
-                    else if (!blocked) cs.st[t] = kIn;
-                    else ++u2;
+                    u2 = __reduce_add_sync(kFull, u2);
+                    if (lane == 0 && u2) atomicAdd(&ctl.undecided, u2);
+                    cons_bar();
                 }
-                u2 = __reduce_add_sync(kFull, u2);
-                if (lane == 0 && u2) atomicAdd(&ctl.undecided, u2);
-                __syncthreads();
-            }
-            PS_TMARK(6);
-            // ordered compaction of accepted candidates
-            const int64_t need = a.boundaries[seg] - ctl.i;
-            const int flag = (tid < K && cs.st[tid] == kIn) ? 1 : 0;
-            int tot;
-            const int ex = block_excl_scan(flag, warp_tot, &tot);
-            const int64_t take = (int64_t)tot < need ? (int64_t)tot : need;
-            const int64_t i0 = ctl.i;
-            if (flag && ex < take) {
-                out[i0 + ex] = cs.cand[tid];
-                if (ex == take - 1 && take == need) ctl.accepted = tid;  // draw of the last used accept
-            }
-            __syncthreads();
-            PS_TMARK(7);
-            const bool ends = (take == need);
-            // chunk candidates leave the rank table; accepted ones stay marked
-            // for the rest of the segment visit (level-seg exclusion)
-            for (int t = tid; t < K; t += blockDim.x) v.rank[cs.cand[t]] = kNoRank;
-            __syncthreads();
-            if (!ends)
-                for (int64_t x = tid; x < take; x += blockDim.x) v.rank[out[i0 + x]] = kAcceptedMark;
-            __syncthreads();
-            if (tid == 0) {
-                ctl.i = i0 + take;
-                if (ends && !a.pick_lowest) ctl.state = state0 + (uint64_t)(k + ctl.accepted + 1) * kGolden;
-            }
-            __syncthreads();
-            PS_TMARK(8);
-            if (tdbg) tacc[9] += 1;
-            if (ends) {
-                end_visit(v, a, b, W, seg, out, ctl.seg_i0, ctl.i);
+                PS_TMARK(6);
+                // ordered compaction of accepted candidates
+                const int64_t i0 = ctl.i;
+                const int64_t need = a.boundaries[seg] - i0;
+                const int flag = (ct < K && st[ct] == kIn) ? 1 : 0;
+                int tot;
+                const int ex = cons_excl_scan(flag, warp_tot, &tot);
+                const int64_t take = (int64_t)tot < need ? (int64_t)tot : need;
+                const bool ends = (take == need);
+                if (flag && ex < take) {
+                    out[i0 + ex] = cme;
+                    if (ex == take - 1 && ends) ctl.accepted = ct;  // draw of the last used accept
+                }
+                if (ct < K) v.rank[cme] = kNoRank;
+                cons_bar();
+                if (!ends)
+                    for (int64_t x = ct; x < take; x += kConsThreads) v.rank[out[i0 + x]] = kAcceptedMark;
+                if (ct == 0) {
+                    ctl.i = i0 + take;
+                    if (ends && !a.pick_lowest) ctl.state = state0 + (uint64_t)(kc + ctl.accepted + 1) * kGolden;
+                    if (ends) vstore(&stop_flag, 1);
+                }
+                cons_bar();
                 PS_TMARK(7);
-                break;
+                if (tdbg) tacc[9] += 1;
+                if (ends) break;
             }
-            k += K;
         }
+        __syncthreads();
+        end_visit(v, a, b, W, seg, out, ctl.seg_i0, ctl.i);
+        PS_TMARK(8);
+        if (tid == 0 && visit_exhausted) {
+            if (!a.pick_lowest) ctl.state = state0 + (uint64_t)L * kGolden;
+            ctl.seg += 1;
+            if (ctl.seg >= nseg) {
+                ctl.exhausted = 1;
+                ctl.done = 1;
+            } else {
+                ctl.entered += 1;
+            }
+        }
+        __syncthreads();
+        if (!ctl.done && visit_exhausted) build_pool(v, ctl.seg, W, &ctl, warp_tot);
     }
     __syncthreads();
     if (tdbg)
@@ -657,8 +712,8 @@ cudaError_t launch_sampler(SampArgs a, int64_t B, cudaStream_t s) {
         long long h[16];
         cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, s);
         cudaStreamSynchronize(s);
-        fprintf(stderr, "[sampler timing] cycles: init+preclear %lld pool %lld positions %lld swap %lld avail %lld "
-                "mis0 %lld mis_rounds %lld compact %lld clears %lld chunks %lld\n", h[0], h[1], h[2], h[3], h[4],
+        fprintf(stderr, "[sampler timing] cycles: init+preclear %lld pool %lld - wait_producer %lld rank %lld "
+                "mis0 %lld mis_rounds %lld compact %lld end_visit %lld chunks %lld\n", h[0], h[1], h[3], h[4],
                 h[5], h[6], h[7], h[8], h[9]);
     }
     return cudaGetLastError();
