@@ -585,7 +585,7 @@ constexpr int kRowWarps = 8;
 constexpr int kRowCap = 256;
 
 template <bool FILL>
-__global__ void __launch_bounds__(kRowWarps * 32) grid_rows_kernel(int64_t B, int64_t N,
+__global__ void __launch_bounds__(kRowWarps * 32, 4) grid_rows_kernel(int64_t B, int64_t N,
                                                                    const double* __restrict__ r2_levels, int L,
                                                                    int64_t levels_ld, GridWork g, ExclWork w,
                                                                    CsrView csr) {
@@ -619,42 +619,57 @@ __global__ void __launch_bounds__(kRowWarps * 32) grid_rows_kernel(int64_t B, in
         }
         int32_t* rn = FILL ? csr.nbr + b * csr.cap_entries + rlo : nullptr;
         double* rd = FILL ? csr.d2 + b * csr.cap_entries + rlo : nullptr;
-        int cnt = 0;
-        unsigned long long cand = 0;
-        for (int dz = -1; dz <= 1; ++dz) {
-            const int z = cz + dz;
-            if (z < 0 || z >= gp.nz) continue;
-            for (int dy = -1; dy <= 1; ++dy) {
-                const int y = cy + dy;
-                if (y < 0 || y >= gp.ny) continue;
+        // the 9 (dz, dy) cell rows: lanes 0..8 fetch their [t0, t1) in parallel
+        int r0 = 0, rlen = 0;
+        if (lane < 9) {
+            const int z = cz + lane / 3 - 1, y = cy + lane % 3 - 1;
+            if (z >= 0 && z < gp.nz && y >= 0 && y < gp.ny) {
                 const int x0 = cx > 0 ? cx - 1 : 0, x1 = cx + 1 < gp.nx ? cx + 1 : gp.nx - 1;
                 const int row = (z * gp.ny + y) * gp.nx;
-                const int t0 = cs[row + x0], t1 = cs[row + x1 + 1];
-                cand += (unsigned long long)(t1 - t0);
-                for (int tb = t0; tb < t1; tb += 32) {
-                    const int t = tb + lane;
-                    bool hit = false;
-                    double d = 0.0;
-                    if (t < t1) {
-                        const float4 q = sx[t];
-                        if (no_filter || sqdist_f32(p, q) < thr) {
-                            d = sqdist4(p, q);
-                            hit = d < r2;
-                        }
-                    }
-                    const unsigned hm = __ballot_sync(kFull, hit);
-                    if (FILL && hit) {
-                        const int slot = cnt + __popc(hm & lt);
-                        if (direct) {
-                            if (slot < m) { rn[slot] = si[t]; rd[slot] = d; }
-                        } else if (slot < kRowCap) {
-                            hd[warp][slot] = d;
-                            hj[warp][slot] = si[t];
-                        }
-                    }
-                    cnt += __popc(hm);
+                r0 = cs[row + x0];
+                rlen = cs[row + x1 + 1] - r0;
+            }
+        }
+        // flatten the candidate list: prefix over the 9 ranges
+        int incl = rlen;
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int total = __shfl_sync(kFull, incl, 8);
+        const int excl0 = incl - rlen;
+        int cnt = 0;
+        const unsigned long long cand = (unsigned long long)total;
+#pragma unroll 2
+        for (int tb = 0; tb < total; tb += 32) {
+            const int f = tb + lane;  // flat candidate index
+            // locate the range: first r with excl(r+1) > f
+            int rr = 0;
+#pragma unroll
+            for (int q = 1; q < 9; ++q) rr += (f >= __shfl_sync(kFull, excl0, q)) ? 1 : 0;
+            const int base = __shfl_sync(kFull, r0, rr) - __shfl_sync(kFull, excl0, rr);
+            const int t = base + f;
+            bool hit = false;
+            double d = 0.0;
+            if (f < total) {
+                const float4 q = sx[t];
+                if (no_filter || sqdist_f32(p, q) < thr) {
+                    d = sqdist4(p, q);
+                    hit = d < r2;
                 }
             }
+            const unsigned hm = __ballot_sync(kFull, hit);
+            if (FILL && hit) {
+                const int slot = cnt + __popc(hm & lt);
+                if (direct) {
+                    if (slot < m) { rn[slot] = si[t]; rd[slot] = d; }
+                } else if (slot < kRowCap) {
+                    hd[warp][slot] = d;
+                    hj[warp][slot] = si[t];
+                }
+            }
+            cnt += __popc(hm);
         }
         if (!FILL) {
             if (lane == 0) {

@@ -204,12 +204,13 @@ PS_DEV void build_pool(const SampView& v, int seg, int64_t W, SampCtl* ctl, int*
 // Clear point p (and its level-l row prefix) in the bitmaps of levels
 // [l0, nseg).  `nl` cooperating lanes (sub-lane sl).  Level counts are loaded
 // in parallel and the row prefix is read once for the widest level (radii
-// are non-increasing in s, so count(l0) >= count(l) for l > l0).
+// are non-increasing in s, so count(l0) >= count(l) for l > l0).  `base` is
+// the row offset (indptr[p]) when the caller prefetched it, else -1.
 PS_DEV void clear_point_levels(const SampView& v, const SampArgs& a, int64_t b, int64_t W, int32_t p, int l0,
-                               int sl, int nl) {
+                               int sl, int nl, int64_t base = -1) {
     const int64_t N = a.N;
     const int nseg = a.nseg;
-    const int64_t base = a.indptr[b * (N + 1) + p];
+    if (base < 0) base = a.indptr[b * (N + 1) + p];
     const int32_t* nbr = a.nbr + b * a.cap_entries + base;
     const uint32_t pbit = ~(1u << (p & 31));
     for (int lb = l0; lb < nseg; lb += 8) {
@@ -218,6 +219,7 @@ PS_DEV void clear_point_levels(const SampView& v, const SampArgs& a, int64_t b, 
         for (int l = 0; l < 8; ++l)
             c[l] = (lb + l < nseg) ? a.counts[(b * a.L + a.seg_level_rows[lb + l]) * N + p] : 0;
         const int cmax = c[0];
+#pragma unroll 2
         for (int u = sl; u < cmax; u += nl) {
             const int32_t q = __ldg(nbr + u);
             const uint32_t bit = ~(1u << (q & 31));
@@ -271,13 +273,19 @@ PS_DEV int cons_excl_scan(int v, int* warp_tot, int* total) {
 }
 
 // Candidate order for draws k .. k+K-1 (pool length before draw t is L - t):
-// position z_t mod (L - t) with z_t = splitmix64(state0 + (t+1) GOLDEN), then
-// the swap-remove of _kernels.py:325-330.  Groups of up to 32 consecutive
+// position z_t mod (L - t) with z_t = splitmix64(state0 + (t+1) GOLDEN)
+// (precomputed in parallel by the consumers, draw_position), then the
+// swap-remove of _kernels.py:325-330.  Groups of up to 32 consecutive
 // draws run in parallel up to the first draw whose read locations an earlier
 // draw of the group writes (same position, or its last slot); positions of
 // the unexecuted draws carry over to the next group.
-PS_DEV void produce_chunk(int32_t* pool, int32_t* cand, uint64_t state0, int64_t L, int64_t k, int K, int lane,
-                          bool pick_lowest) {
+PS_DEV uint32_t draw_position(uint64_t state0, int64_t L, int64_t t) {
+    const uint64_t z = mix64(state0 + (uint64_t)(t + 1) * kGolden);
+    return (uint32_t)(z % (uint64_t)(L - t));
+}
+
+PS_DEV void produce_chunk(int32_t* pool, int32_t* cand, const uint32_t* pos, int64_t L, int64_t k, int K,
+                          int lane, bool pick_lowest) {
     if (pick_lowest) {
         for (int t = lane; t < K; t += 32) cand[t] = pool[k + t];
         __syncwarp();
@@ -288,13 +296,7 @@ PS_DEV void produce_chunk(int32_t* pool, int32_t* cand, uint64_t state0, int64_t
     int have = 0;  // lanes [0, have) hold valid positions for draws g .. g+have-1
     uint32_t p = 0;
     while (g < K) {
-        if (lane >= have) {
-            const int64_t t = k + g + lane;
-            if (g + lane < K) {
-                const uint64_t z = mix64(state0 + (uint64_t)(t + 1) * kGolden);
-                p = (uint32_t)(z % (uint64_t)(L - t));
-            }
-        }
+        if (lane >= have && g + lane < K) p = pos[g + lane];
         const bool act = g + lane < K;
         const uint32_t key = act ? p : (0x80000000u | (uint32_t)lane);
         const int64_t last0 = L - 1 - (k + g);
@@ -332,13 +334,24 @@ PS_DEV void produce_chunk(int32_t* pool, int32_t* cand, uint64_t state0, int64_t
 // their rows in the bitmaps of every later segment, in one parallel batch,
 // and leave the rank table.  (Bitmap `seg` itself is never read again.)
 PS_DEV void end_visit(const SampView& v, const SampArgs& a, int64_t b, int64_t W, int seg, const int64_t* out,
-                      int64_t i0, int64_t i1) {
+                      int64_t i0, int64_t i1, int32_t* stage) {
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     if (seg + 1 < a.nseg) {
         const int sub = lane >> 3, sl = lane & 7;
-        for (int64_t x = i0 + (int64_t)warp * 4 + sub; x < i1; x += (int64_t)nwarps * 4)
-            clear_point_levels(v, a, b, W, (int32_t)out[x], seg + 1, sl, 8);
+        for (int64_t x0 = i0; x0 < i1; x0 += 2 * kConsThreads) {
+            const int64_t xn = (i1 - x0) < 2 * kConsThreads ? (i1 - x0) : 2 * kConsThreads;
+            // stage (point, row base) pairs: one latency for the whole batch
+            for (int64_t x = threadIdx.x; x < xn; x += blockDim.x) {
+                const int32_t p = (int32_t)out[x0 + x];
+                stage[2 * x] = p;
+                stage[2 * x + 1] = (int32_t)a.indptr[b * (a.N + 1) + p];
+            }
+            __syncthreads();
+            for (int64_t x = (int64_t)warp * 4 + sub; x < xn; x += (int64_t)nwarps * 4)
+                clear_point_levels(v, a, b, W, stage[2 * x], seg + 1, sl, 8, stage[2 * x + 1]);
+            __syncthreads();
+        }
     }
     for (int64_t x = i0 + threadIdx.x; x < i1; x += blockDim.x) v.rank[out[x]] = kNoRank;
     __syncthreads();
@@ -349,6 +362,7 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
     __shared__ SampCtl ctl;
     __shared__ int warp_tot[32];
     __shared__ int32_t cbuf[2][kConsThreads];
+    __shared__ uint32_t posbuf[2][kConsThreads];
     __shared__ uint16_t preds[kConsThreads][kMaxPred];
     __shared__ uint8_t st[kConsThreads];
     __shared__ uint8_t npred[kConsThreads];
@@ -374,7 +388,9 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
     const int64_t k0 = a.k0, n_total = a.n_total;
     // development timing (PS_SAMPLER_TIMING): cycles per phase, cloud 0, first consumer
     const bool tdbg = a.dbg && b == 0 && tid == 32;
-    long long tacc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    __shared__ long long tacc[10];
+    if (tdbg)
+        for (int k2 = 0; k2 < 10; ++k2) tacc[k2] = 0;
     long long tlast = tdbg ? clock64() : 0;
 #define PS_TMARK(k)                                  \
     do {                                             \
@@ -452,6 +468,9 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
             stop_flag = 0;
             visit_exhausted = 0;
         }
+        if (!a.pick_lowest)
+            for (int t = tid; t < 2 * kConsThreads; t += blockDim.x)
+                if (t < L) posbuf[t / kConsThreads][t % kConsThreads] = draw_position(state0, L, t);
         __syncthreads();
 
         if (warp == 0) {
@@ -463,7 +482,7 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
                 while (vload(&cons_count) < c - 1 && !vload(&stop_flag)) __nanosleep(32);
                 if (vload(&stop_flag)) break;
                 const int K = (int)((L - kc) < kConsThreads ? (L - kc) : kConsThreads);
-                produce_chunk(v.pool, cbuf[c & 1], state0, L, kc, K, lane, a.pick_lowest != 0);
+                produce_chunk(v.pool, cbuf[c & 1], posbuf[c & 1], L, kc, K, lane, a.pick_lowest != 0);
                 __threadfence_block();
                 if (lane == 0) vstore(&prod_count, c + 1);
             }
@@ -490,7 +509,14 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
                 }
                 if (ct == 0) ctl.undecided = 0;
                 cons_bar();
-                // every consumer holds its candidate in a register now: release the buffer
+                // every consumer holds its candidate in a register now: refill the
+                // position buffer with chunk c+2 and release both buffers of chunk c
+                if (!a.pick_lowest) {
+                    const int64_t t2 = kc + 2 * kConsThreads + ct;
+                    if (t2 < L) posbuf[c & 1][ct] = draw_position(state0, L, t2);
+                    __threadfence_block();
+                    cons_bar();
+                }
                 if (ct == 0) vstore(&cons_count, c + 1);
                 PS_TMARK(4);
                 // greedy MIS, round 0: one pass over the level-seg row
@@ -499,15 +525,24 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
                     const int t = ct;
                     const int32_t m = cnt_row[cme];
                     const int32_t* row = nbr_all + indptr[cme];
+                    // aligned 16-byte loads over [row, row + m): 16 entries per batch
+                    const uintptr_t ua = reinterpret_cast<uintptr_t>(row);
+                    const int4* ap = reinterpret_cast<const int4*>(ua & ~uintptr_t(15));
+                    const int skip = (int)((ua & 15) >> 2);
                     int np = 0;
                     bool out_ = false, blocked = false;
-                    for (int32_t u0 = 0; u0 < m; u0 += 8) {
-                        int32_t q[8];
+                    for (int e0 = -skip; e0 < m; e0 += 16) {
+                        int4 qv[4];
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) q[j] = (u0 + j < m) ? __ldg(row + u0 + j) : cme;
+                        for (int j = 0; j < 4; ++j)
+                            qv[j] = (e0 + 4 * j < m) ? __ldg(ap + (e0 + skip) / 4 + j) : make_int4(cme, cme, cme, cme);
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            const uint32_t rq = v.rank[q[j]];
+                        for (int j = 0; j < 16; ++j) {
+                            const int e = e0 + j;
+                            const int4 w4 = qv[j >> 2];
+                            const int32_t qq = (j & 3) == 0 ? w4.x : (j & 3) == 1 ? w4.y : (j & 3) == 2 ? w4.z : w4.w;
+                            const int32_t qj = (e >= 0 && e < m) ? qq : cme;
+                            const uint32_t rq = v.rank[qj];
                             if (rq == kAcceptedMark) {
                                 out_ = true;
                             } else if (rq < (uint32_t)t) {
@@ -598,7 +633,7 @@ __global__ void __launch_bounds__(kSampThreads, 1) sampler_kernel(SampArgs a) {
             }
         }
         __syncthreads();
-        end_visit(v, a, b, W, seg, out, ctl.seg_i0, ctl.i);
+        end_visit(v, a, b, W, seg, out, ctl.seg_i0, ctl.i, reinterpret_cast<int32_t*>(preds));
         PS_TMARK(8);
         if (tid == 0 && visit_exhausted) {
             if (!a.pick_lowest) ctl.state = state0 + (uint64_t)L * kGolden;
