@@ -100,7 +100,10 @@ def first_untaken(taken):
 def build_csr(x, y, z, r2_levels, cap_entries=None, method=0):
     """Fused device build: (indptr int64[N+1], nbr int64[E], d2 float64[E],
     counts int64[L, N], evals).  The unit the reference orchestrator forms
-    from excl_collect + csr_fill + csr_sort_rows + csr_level_counts."""
+    from excl_collect + csr_fill + csr_sort_rows + csr_level_counts.
+    method 0 = brute-force triangle, 1 = grid (identical CSR)."""
+    if method not in (0, 1):
+        raise ValueError("build_csr returns the reference CSR layout: method 0 or 1")
     from .engine import DeviceCsr
 
     N = int(np.asarray(x).shape[0])

@@ -183,7 +183,8 @@ int ps_excl_build(const float* xyz4, int64_t B, int64_t N, const double* r2_leve
     CHECK_ARG(L >= 1 && L <= levels_ld, "invalid level count %d", L);
     CHECK_ARG(cap_entries >= N && cap_entries < ((int64_t)1 << 31), "cap_entries must be in [N, 2^31)");
     CHECK_ARG(cap_edges >= 1, "cap_edges must be >= 1");
-    CHECK_ARG(method == 0 || method == 1, "method must be 0 (brute force) or 1 (grid)");
+    CHECK_ARG(method >= 0 && method <= 2, "method must be 0 (brute force), 1 (grid) or 2 (grid, strided bucket rows)");
+    CHECK_ARG(method != 2 || cap_entries / N <= 65535, "row stride too large");
     CHECK_ARG(work && status && indptr && nbr && d2 && counts, "null pointer");
     unsigned char* w = static_cast<unsigned char*>(work);
     ps::ExclWork ew = {};
@@ -212,7 +213,7 @@ int ps_excl_build(const float* xyz4, int64_t B, int64_t N, const double* r2_leve
     ps::CsrView csr = {indptr, nbr, d2, counts, cap_entries, N, L};
     return cuda_status(ps::launch_excl_build(reinterpret_cast<const float4*>(xyz4), B, N, r2_levels, L, levels_ld,
                                              csr, ew, gw, method, S(stream)),
-                       "excl_build", method == 0 ? 6 : 8);
+                       "excl_build", method == 0 ? 6 : (method == 1 ? 8 : 6));
 }
 
 int ps_csr_sort_rows(int64_t* indptr, int32_t* nbr, double* d2, int64_t cap_entries, int64_t B, int64_t N,

@@ -131,4 +131,50 @@ PS_DEV void st_async_v4(uint32_t remote_addr, uint32_t remote_bar, uint32_t a, u
         ::"r"(remote_addr), "r"(remote_bar), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 
+// ---- row ordering by (d2, index) ----------------------------------------
+// (d2, index) order.  d2 >= 0 (or +inf padding), so its bit pattern orders
+// like an unsigned integer: integer compares keep the sort off the FP64 pipe.
+__device__ __forceinline__ bool key_less(double da, int32_t ia, double db, int32_t ib) {
+    const unsigned long long ua = (unsigned long long)__double_as_longlong(da);
+    const unsigned long long ub = (unsigned long long)__double_as_longlong(db);
+    return ua < ub || (ua == ub && ia < ib);
+}
+
+// Warp bitonic network over 64 keys held two per lane (slot lane, lane+32),
+// padded with (+inf, INT_MAX).  All compare-exchanges are register shuffles.
+__device__ __forceinline__ void warp_bitonic64(double& d0, int32_t& i0, double& d1, int32_t& i1, int lane,
+                                               int n2) {
+#pragma unroll
+    for (int k = 2; k <= 64; k <<= 1) {
+        if (k > n2) break;
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j == 32) {
+                // partner of slot lane is slot lane+32, same thread
+                const bool up = ((lane & k) == 0);  // k == 64: always ascending
+                const bool sw = up ? key_less(d1, i1, d0, i0) : key_less(d0, i0, d1, i1);
+                if (sw) {
+                    const double td = d0; d0 = d1; d1 = td;
+                    const int32_t ti = i0; i0 = i1; i1 = ti;
+                }
+            } else {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    double& d = h ? d1 : d0;
+                    int32_t& ix = h ? i1 : i0;
+                    const int s = lane + 32 * h;
+                    const double od = __shfl_xor_sync(kFull, d, j);
+                    const int32_t oi = __shfl_xor_sync(kFull, ix, j);
+                    const bool lower = (s & j) == 0;
+                    const bool up = (s & k) == 0;
+                    // the lower slot keeps the min when ascending
+                    const bool mine_less = key_less(d, ix, od, oi);
+                    const bool keep_min = (lower == up);
+                    if (keep_min != mine_less) { d = od; ix = oi; }
+                }
+            }
+        }
+    }
+}
+
 }  // namespace ps

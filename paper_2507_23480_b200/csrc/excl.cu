@@ -351,14 +351,6 @@ __global__ void grid_scatter_kernel(const float4* __restrict__ xyz, int64_t B, i
 
 // ---- row sort by (d2, index) + fused level counts -----------------------
 
-// (d2, index) order.  d2 >= 0 (or +inf padding), so its bit pattern orders
-// like an unsigned integer: integer compares keep the sort off the FP64 pipe.
-__device__ __forceinline__ bool key_less(double da, int32_t ia, double db, int32_t ib) {
-    const unsigned long long ua = (unsigned long long)__double_as_longlong(da);
-    const unsigned long long ub = (unsigned long long)__double_as_longlong(db);
-    return ua < ub || (ua == ub && ia < ib);
-}
-
 // Bitonic sort of n2 (power of two) entries in shared memory by `nthr`
 // cooperating threads (thread rank t), synchronised with `sync`.
 template <typename Sync>
@@ -383,43 +375,6 @@ __device__ __forceinline__ void bitonic_smem(double* kd, int32_t* ki, int n2, in
 constexpr int kSortWarps = 8;
 constexpr int kWarpRowCap = 256;
 constexpr int kCtaRowCap = 8192;
-
-// Warp bitonic network over 64 keys held two per lane (slot lane, lane+32),
-// padded with (+inf, INT_MAX).  All compare-exchanges are register shuffles.
-__device__ __forceinline__ void warp_bitonic64(double& d0, int32_t& i0, double& d1, int32_t& i1, int lane,
-                                               int n2) {
-#pragma unroll
-    for (int k = 2; k <= 64; k <<= 1) {
-        if (k > n2) break;
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            if (j == 32) {
-                // partner of slot lane is slot lane+32, same thread
-                const bool up = ((lane & k) == 0);  // k == 64: always ascending
-                const bool sw = up ? key_less(d1, i1, d0, i0) : key_less(d0, i0, d1, i1);
-                if (sw) {
-                    const double td = d0; d0 = d1; d1 = td;
-                    const int32_t ti = i0; i0 = i1; i1 = ti;
-                }
-            } else {
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    double& d = h ? d1 : d0;
-                    int32_t& ix = h ? i1 : i0;
-                    const int s = lane + 32 * h;
-                    const double od = __shfl_xor_sync(kFull, d, j);
-                    const int32_t oi = __shfl_xor_sync(kFull, ix, j);
-                    const bool lower = (s & j) == 0;
-                    const bool up = (s & k) == 0;
-                    // the lower slot keeps the min when ascending
-                    const bool mine_less = key_less(d, ix, od, oi);
-                    const bool keep_min = (lower == up);
-                    if (keep_min != mine_less) { d = od; ix = oi; }
-                }
-            }
-        }
-    }
-}
 
 __global__ void __launch_bounds__(kSortWarps * 32) excl_sort_small_kernel(CsrView csr, int64_t B,
                                                                        const double* __restrict__ r2_levels,
@@ -723,6 +678,140 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) grid_rows_kernel(int64_t B,
     }
 }
 
+// Method 2 (hot path): single pass, fixed row stride.  Row i of cloud b
+// lives at b * cap_entries + i * stride (indptr[i] = i * stride), its entries
+// ordered by level bucket: bucket(e) = #{levels with r2 <= d2}, so that for
+// every level l the entries with d2 < r2_l are exactly the first counts[l]
+// -- the only row property the sampler, early termination and the
+// redundancy-free queries rely on (they read per-level prefixes as sets;
+// the queries order their small prefixes themselves).  Rows longer than the
+// stride set status bit 1 and are rebuilt by the host with a wider stride.
+constexpr int kEllWarps = 8;
+constexpr int kEllCap = 256;   // per-warp staging (rows above it: overflow)
+
+__global__ void __launch_bounds__(kEllWarps * 32, 4) grid_ell_kernel(int64_t B, int64_t N,
+                                                                     const double* __restrict__ r2_levels, int L,
+                                                                     int64_t levels_ld, int64_t stride, GridWork g,
+                                                                     ExclWork w, CsrView csr) {
+    __shared__ double hd[kEllWarps][kEllCap];
+    __shared__ int32_t hj[kEllWarps][kEllCap];
+    __shared__ uint8_t hb[kEllWarps][kEllCap];
+    __shared__ double lvs[kEllWarps][16];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int64_t gs = (int64_t)blockIdx.x * kEllWarps + warp; gs < B * N; gs += (int64_t)gridDim.x * kEllWarps) {
+        const int64_t b = gs / N, s = gs - b * N;
+        // level values of this cloud: lane l < L holds r2_l and its rank_lt
+        const double my_r2 = lane < L ? r2_levels[b * levels_ld + lane] : 0.0;
+        __syncwarp();
+        if (lane < L) lvs[warp][lane] = my_r2;
+        __syncwarp();
+        int rank_lt = 0;
+        double r2 = 0.0;
+        for (int l = 0; l < L; ++l) {
+            const double v = __shfl_sync(kFull, my_r2, l);
+            rank_lt += (v < my_r2) ? 1 : 0;
+            r2 = fmax(r2, v);
+        }
+        const float thr = prefilter_threshold(r2);
+        const bool no_filter = !(thr <= FLT_MAX);
+        const GridParams gp = g.params[b];
+        const float4* sx = g.sorted_xyz + b * N;
+        const int32_t* si = g.sorted_idx + b * N;
+        const int* cs = g.cell_start + b * (g.max_cells + 1);
+        const float4 p = sx[s];
+        const int32_t i = si[s];
+        const int cx = cell_coord(p.x, gp.ox, gp.inv_h, gp.nx);
+        const int cy = cell_coord(p.y, gp.oy, gp.inv_h, gp.ny);
+        const int cz = cell_coord(p.z, gp.oz, gp.inv_h, gp.nz);
+        int r0 = 0, rlen = 0;
+        if (lane < 9) {
+            const int z = cz + lane / 3 - 1, y = cy + lane % 3 - 1;
+            if (z >= 0 && z < gp.nz && y >= 0 && y < gp.ny) {
+                const int x0 = cx > 0 ? cx - 1 : 0, x1 = cx + 1 < gp.nx ? cx + 1 : gp.nx - 1;
+                const int row = (z * gp.ny + y) * gp.nx;
+                r0 = cs[row + x0];
+                rlen = cs[row + x1 + 1] - r0;
+            }
+        }
+        int incl = rlen;
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int total = __shfl_sync(kFull, incl, 8);
+        const int excl0 = incl - rlen;
+        int cnt = 0;
+#pragma unroll 2
+        for (int tb = 0; tb < total; tb += 32) {
+            const int f = tb + lane;
+            int rr = 0;
+#pragma unroll
+            for (int q = 1; q < 9; ++q) rr += (f >= __shfl_sync(kFull, excl0, q)) ? 1 : 0;
+            const int t = __shfl_sync(kFull, r0, rr) - __shfl_sync(kFull, excl0, rr) + f;
+            bool hit = false;
+            double d = 0.0;
+            if (f < total) {
+                const float4 q = sx[t];
+                if (no_filter || sqdist_f32(p, q) < thr) {
+                    d = sqdist4(p, q);
+                    hit = d < r2;
+                }
+            }
+            const unsigned hm = __ballot_sync(kFull, hit);
+            if (hit) {
+                const int slot = cnt + __popc(hm & lt);
+                if (slot < kEllCap) {
+                    int bk = 0;
+                    for (int l = 0; l < L; ++l) bk += (lvs[warp][l] <= d) ? 1 : 0;
+                    hd[warp][slot] = d;
+                    hj[warp][slot] = si[t];
+                    hb[warp][slot] = (uint8_t)bk;
+                }
+            }
+            cnt += __popc(hm);
+        }
+        if (lane == 0) atomicAdd(g.evals + b, (unsigned long long)total);
+        if (cnt > stride || cnt > kEllCap) {
+            if (lane == 0) atomicOr(&w.status[b], 2);
+            continue;
+        }
+        __syncwarp();
+        // counting sort by bucket (<= L + 1 buckets), stable in collection order
+        int32_t* rn = csr.nbr + b * csr.cap_entries + (int64_t)i * stride;
+        double* rd = csr.d2 + b * csr.cap_entries + (int64_t)i * stride;
+        int base = 0;
+        int hist_mine = 0;  // lane l: entries with bucket <= rank_lt(l)
+        for (int bk = 0; bk <= L; ++bk) {
+            int here = 0;
+            for (int e0 = 0; e0 < cnt; e0 += 32) {
+                const int e = e0 + lane;
+                const bool in = e < cnt && hb[warp][e] == bk;
+                const unsigned bm = __ballot_sync(kFull, in);
+                if (in) {
+                    const int pos = base + here + __popc(bm & lt);
+                    rd[pos] = hd[warp][e];
+                    rn[pos] = hj[warp][e];
+                }
+                here += __popc(bm);
+            }
+            base += here;
+            if (lane < L && bk == rank_lt) hist_mine = base;
+        }
+        if (lane < L) csr.counts[(b * csr.L + lane) * N + i] = hist_mine;
+        __syncwarp();
+    }
+}
+
+__global__ void ell_indptr_kernel(int64_t B, int64_t N, int64_t stride, CsrView csr) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < B * (N + 1);
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = t % (N + 1);
+        csr.indptr[t] = r * stride;
+    }
+}
+
 static cudaError_t launch_sort(CsrView csr, int64_t B, const double* r2_levels, int64_t levels_ld, ExclWork w,
                                cudaStream_t s) {
     excl_sort_small_kernel<<<148 * 8, kSortWarps * 32, 0, s>>>(csr, B, r2_levels, levels_ld, w);
@@ -745,13 +834,20 @@ cudaError_t launch_excl_build(const float4* xyz, int64_t B, int64_t N, const dou
     if ((e = cudaMemsetAsync(w.long_count, 0, sizeof(unsigned), s)) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(w.status, 0, sizeof(int32_t) * B, s)) != cudaSuccess) return e;
     const unsigned gpts = (unsigned)std::min<int64_t>(148 * 16, (B * N + 255) / 256 + 1);
-    if (method == 1) {
+    if (method == 1 || method == 2) {
         if ((e = cudaMemsetAsync(g.cell_start, 0, sizeof(int) * B * (g.max_cells + 1), s)) != cudaSuccess) return e;
         if ((e = cudaMemsetAsync(g.evals, 0, sizeof(unsigned long long) * B, s)) != cudaSuccess) return e;
         grid_setup_kernel<<<(unsigned)B, 1024, 0, s>>>(xyz, N, r2_levels, L, levels_ld, g);
         grid_assign_kernel<<<gpts, 256, 0, s>>>(xyz, B, N, g);
         grid_scan_kernel<<<(unsigned)B, 1024, 0, s>>>(N, g);
         grid_scatter_kernel<<<gpts, 256, 0, s>>>(xyz, B, N, g);
+        if (method == 2) {
+            const int64_t stride = csr.cap_entries / N;
+            ell_indptr_kernel<<<gpts, 256, 0, s>>>(B, N, stride, csr);
+            const unsigned gell = (unsigned)std::min<int64_t>(148 * 16, (B * N + kEllWarps - 1) / kEllWarps);
+            grid_ell_kernel<<<gell, kEllWarps * 32, 0, s>>>(B, N, r2_levels, L, levels_ld, stride, g, w, csr);
+            return cudaGetLastError();
+        }
         const dim3 gp((unsigned)((N + 255) / 256), (unsigned)B);
         (void)gp;
         const unsigned grow = (unsigned)std::min<int64_t>(148 * 16, (B * N + kRowWarps - 1) / kRowWarps);

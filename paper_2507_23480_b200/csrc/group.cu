@@ -35,34 +35,89 @@ PS_DEV bool kless(double da, int32_t ia, double db, int32_t ib) {
 PS_DEV double nan_d() { return __longlong_as_double(0x7ff8000000000000LL); }
 
 // ---- K4a -----------------------------------------------------------------
-__global__ void bq_rf_kernel(BqArgs a) {
-    const int lane = threadIdx.x & 31;
-    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t g = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); g < a.B * a.n;
-         g += nw) {
+// Warp per centroid.  The level-r entries are a row prefix of length c (a set:
+// the hot-path rows are level-bucketed, the reference-layout rows sorted);
+// the first min(c, k) in (d2, index) order are produced here -- in registers
+// for c <= 64, by a streaming warp top-k insertion otherwise.
+constexpr int kBqWarps = 8;
+constexpr int kBqMaxK = 128;
+
+// sorted top-K list (per warp, shared memory): insert (dn, jn) if it ranks < K
+PS_DEV void topk_warp_insert(double* ld, int32_t* li, int& len, int K, double dn, int32_t jn, int lane) {
+    int below = 0;
+    for (int s = lane; s < len; s += 32) below += key_less(ld[s], li[s], dn, jn) ? 1 : 0;
+    const int pos = __reduce_add_sync(kFull, below);
+    if (pos >= K) return;
+    const int newlen = len < K ? len + 1 : K;
+    double cd[kBqMaxK / 32];
+    int32_t ci[kBqMaxK / 32];
+#pragma unroll
+    for (int v = 0; v < kBqMaxK / 32; ++v) {
+        const int s = lane + 32 * v;
+        if (s > pos && s < newlen) { cd[v] = ld[s - 1]; ci[v] = li[s - 1]; }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int v = 0; v < kBqMaxK / 32; ++v) {
+        const int s = lane + 32 * v;
+        if (s > pos && s < newlen) { ld[s] = cd[v]; li[s] = ci[v]; }
+    }
+    if (lane == 0) { ld[pos] = dn; li[pos] = jn; }
+    __syncwarp();
+    len = newlen;
+}
+
+__global__ void __launch_bounds__(kBqWarps * 32) bq_rf_kernel(BqArgs a) {
+    __shared__ double ld[kBqWarps][kBqMaxK];
+    __shared__ int32_t li[kBqWarps][kBqMaxK];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t nw = (int64_t)gridDim.x * kBqWarps;
+    const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+    const int K = a.k;
+    for (int64_t g = blockIdx.x * (int64_t)kBqWarps + warp; g < a.B * a.n; g += nw) {
         const int64_t b = g / a.n, t = g - b * a.n;
         const int64_t c = a.centroids[b * a.cent_ld + t];
         const int32_t cnt = a.counts[(b * a.L + a.level) * a.N + c];
-        const int m = cnt < a.k ? cnt : a.k;
         const int64_t base = b * a.cap_entries + a.indptr[b * (a.N + 1) + c];
-        int32_t* oi = a.idx_out + g * a.k;
-        double* od = a.dist_out + g * a.k;
-        for (int s = lane; s < a.k; s += 32) {
-            if (s < m) {
-                oi[s] = a.nbr[base + s];
-                od[s] = sqrt(a.d2[base + s]);
-            } else {
-                oi[s] = -1;
-                od[s] = nan_d();
+        int32_t* oi = a.idx_out + g * K;
+        double* od = a.dist_out + g * K;
+        const int m = cnt < K ? cnt : K;
+        if (cnt <= 64) {
+            double d0 = lane < cnt ? a.d2[base + lane] : kInf;
+            int32_t i0 = lane < cnt ? a.nbr[base + lane] : 0x7fffffff;
+            double d1 = lane + 32 < cnt ? a.d2[base + lane + 32] : kInf;
+            int32_t i1 = lane + 32 < cnt ? a.nbr[base + lane + 32] : 0x7fffffff;
+            int n2 = 2;
+            while (n2 < cnt) n2 <<= 1;
+            if (cnt > 1) warp_bitonic64(d0, i0, d1, i1, lane, n2);
+            for (int s = lane; s < K; s += 32) {
+                const double d = s < 32 ? d0 : d1;  // valid for s < 64 only
+                const int32_t ix = s < 32 ? i0 : i1;
+                if (s < m) { oi[s] = ix; od[s] = sqrt(d); }
+                else { oi[s] = -1; od[s] = nan_d(); }
             }
+        } else {
+            int len = 0;
+            for (int64_t u0 = 0; u0 < cnt; u0 += 32) {
+                const int64_t u = u0 + lane;
+                const double dv = u < cnt ? a.d2[base + u] : kInf;
+                const int32_t jv = u < cnt ? a.nbr[base + u] : 0x7fffffff;
+                const int nval = (int)((cnt - u0) < 32 ? (cnt - u0) : 32);
+                for (int q = 0; q < nval; ++q)
+                    topk_warp_insert(ld[warp], li[warp], len, K, __shfl_sync(kFull, dv, q),
+                                     __shfl_sync(kFull, jv, q), lane);
+            }
+            for (int s = lane; s < K; s += 32) {
+                if (s < len) { oi[s] = li[warp][s]; od[s] = sqrt(ld[warp][s]); }
+                else { oi[s] = -1; od[s] = nan_d(); }
+            }
+            __syncwarp();
         }
         if (lane == 0) a.cnt_out[g] = m;
     }
 }
 
 // ---- K4c -----------------------------------------------------------------
-constexpr int kBqWarps = 8;
-constexpr int kBqMaxK = 128;
 
 __global__ void __launch_bounds__(kBqWarps * 32) bq_naive_kernel(BqArgs a) {
     __shared__ double ld[kBqWarps][kBqMaxK];
@@ -211,27 +266,30 @@ __global__ void __launch_bounds__(kKnnThreads) knn_rf_kernel(KnnArgs a) {
     const uint8_t* smp = a.sampled + b * a.N;
     const int k = a.k;
     const int64_t g = b * a.nq + q;
+    // the k nearest sampled points of the level-1 prefix (a set), by (d2, index)
+    TopK tk;
+    topk_init(tk);
     int found = 0;
-    for (int32_t u = 0; u < c && found < k; ++u) {
+    for (int32_t u = 0; u < c; ++u) {
         const int32_t j = a.nbr[base + u];
         if (smp[j]) {
-            a.idx_out[g * k + found] = j;
-            a.dist_out[g * k + found] = sqrt(a.d2[base + u]);
+            topk_insert(tk, k, a.d2[base + u], j);
             ++found;
         }
     }
-    if (found >= k) { a.cnt_out[g] = k; return; }
-    // fallback: exact brute force over the whole pool
-    atomicAdd(a.fallback_count + b, 1);
-    const float4* xyz = a.xyz + b * a.N;
-    const float4 pq = xyz[qp];
-    TopK tk;
-    topk_init(tk);
-    for (int64_t p = 0; p < a.npool; ++p) {
-        const int64_t j = a.pool[b * a.pool_ld + p];
-        topk_insert(tk, k, sqdist4(pq, xyz[j]), (int32_t)j);
+    if (found < k) {
+        // fallback: exact brute force over the whole pool
+        atomicAdd(a.fallback_count + b, 1);
+        const float4* xyz = a.xyz + b * a.N;
+        const float4 pq = xyz[qp];
+        topk_init(tk);
+        for (int64_t p = 0; p < a.npool; ++p) {
+            const int64_t j = a.pool[b * a.pool_ld + p];
+            topk_insert(tk, k, sqdist4(pq, xyz[j]), (int32_t)j);
+        }
+        found = (int)(a.npool < k ? a.npool : k);
     }
-    const int take = (int)(a.npool < k ? a.npool : k);
+    const int take = found < k ? found : k;
 #pragma unroll
     for (int s = 0; s < kKnnMaxK; ++s) {
         if (s < k) {

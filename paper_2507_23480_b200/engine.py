@@ -104,7 +104,10 @@ class DeviceCsr:
 
     @staticmethod
     def allocate(B, N, L, cap_entries, cap_edges, device, method=1):
-        """method 1 = uniform-grid candidates (default), 0 = brute-force triangle."""
+        """method 0 = brute-force triangle, 1 = uniform-grid candidates (both
+        give the reference CSR: rows sorted by (d2, index)); 2 = grid with a
+        fixed row stride cap_entries // N and level-bucketed rows (every
+        level's entries form the row prefix; the hot-path layout)."""
         cap_entries = int(min(max(cap_entries, N), (1 << 31) - 1))
         cap_edges = int(max(cap_edges, 1)) if method == 0 else 1
         ws = int(_lib.raw("ps_excl_workspace_bytes", B, N, cap_edges, method))
@@ -137,8 +140,12 @@ class DeviceCsr:
     def overflowed(self) -> bool:
         return bool(int(self.status.max().item()) != 0)
 
-    def row(self, b, i):
+    def row(self, b, i, level=None):
+        """Entries of row i (method 2: only the first counts[level] entries are
+        defined; pass the widest level)."""
         lo, hi = (int(v) for v in self.indptr[b, i:i + 2].tolist())
+        if level is not None:
+            hi = lo + int(self.counts[b, level, i].item())
         return self.nbr[b, lo:hi], self.d2[b, lo:hi]
 
 
@@ -183,9 +190,10 @@ class FastPoint:
             raise ValueError("at most 8 extra radii")
         self.seed_index = int(seed_index)
         self.pick_lowest = bool(pick_lowest)
-        if excl_method not in ("grid", "bruteforce"):
-            raise ValueError("excl_method must be 'grid' or 'bruteforce'")
-        self.excl_method = 1 if excl_method == "grid" else 0
+        methods = {"bruteforce": 0, "grid-sorted": 1, "grid": 2}
+        if excl_method not in methods:
+            raise ValueError(f"excl_method must be one of {sorted(methods)}")
+        self.excl_method = methods[excl_method]
         self.device = torch.device(device)
         self.k0 = min(prefix_len(self.n, self.p), self.n)
         if self.k0 < 2:

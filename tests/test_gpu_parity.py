@@ -152,6 +152,33 @@ def test_excl_matches_oracle(family, N, R):
         np.testing.assert_array_equal(counts, e.counts)
 
 
+def test_excl_bucketed_rows_match_oracle_sets():
+    # method 2 (hot path): fixed stride, rows bucketed by level -- every
+    # level's entries are the row prefix; as sets they equal the reference's
+    c = generate_cloud("room-surfaces", 5000, 5)
+    R = [0.3, 0.25, 0.2, 0.2, 0.15, 0.1]
+    e = O.build_exclusion_lists(c, R, (0.12,))
+    levels = np.array([O.radius_sq(r) for r in R] + [O.radius_sq(0.12)])
+    csr = engine.DeviceCsr.allocate(1, 5000, len(levels), 5000 * 256, 1, torch.device("cuda"), 2)
+    csr.levels.copy_(torch.from_numpy(levels.reshape(1, -1)))
+    csr.build(engine.as_xyz4(c))
+    assert not csr.overflowed()
+    counts = csr.counts[0].cpu().numpy()
+    nbr = csr.nbr[0].cpu().numpy()
+    d2 = csr.d2[0].cpu().numpy()
+    pos = {float(v): k for k, v in enumerate(e.r2_levels)}
+    for l, lv in enumerate(levels):
+        np.testing.assert_array_equal(counts[l], e.counts[pos[float(lv)]])
+    for i in range(0, 5000, 7):
+        m = counts[0]  # widest level is R[0]
+        got = sorted(zip(d2[i * 256:i * 256 + m[i]].tolist(), nbr[i * 256:i * 256 + m[i]].tolist()))
+        lo = e.indptr[i]
+        ref = list(zip(e.d2[lo:lo + m[i]].tolist(), e.nbr[lo:lo + m[i]].tolist()))
+        assert got == ref, i
+        for l, lv in enumerate(levels):  # each level is a prefix
+            assert np.all(d2[i * 256:i * 256 + counts[l][i]] < lv)
+
+
 def test_excl_prefilter_adversarial():
     # pairs placed at float64 distances straddling r exactly: the float32
     # pre-filter must never drop a pair whose exact d2 is below r2.
@@ -201,7 +228,7 @@ def test_dropin_collect_fill_sort_counts():
 
 # ---- K2/K3c/K3d full FastPoint pipeline --------------------------------------------
 
-@pytest.mark.parametrize("method", ["bruteforce", "grid"])
+@pytest.mark.parametrize("method", ["bruteforce", "grid-sorted", "grid"])
 def test_mdps_golden(golden, method):
     for t in cases(golden, "mdps"):
         k = f"mdps/{t}"
