@@ -180,7 +180,7 @@ int ps_excl_build(const float* xyz4, int64_t B, int64_t N, const double* r2_leve
                   int64_t* indptr, int32_t* nbr, double* d2, int32_t* counts, int64_t cap_entries, void* work,
                   int64_t cap_edges, int32_t* status, int32_t method, void* stream) {
     CHECK_ARG(B >= 1 && N >= 1 && N <= kMaxN, "invalid batch shape");
-    CHECK_ARG(L >= 1 && L <= levels_ld, "invalid level count %d", L);
+    CHECK_ARG(L >= 1 && L <= levels_ld && L <= 32, "invalid level count %d (1..32)", L);
     CHECK_ARG(cap_entries >= N && cap_entries < ((int64_t)1 << 31), "cap_entries must be in [N, 2^31)");
     CHECK_ARG(cap_edges >= 1, "cap_edges must be >= 1");
     CHECK_ARG(method >= 0 && method <= 2, "method must be 0 (brute force), 1 (grid) or 2 (grid, strided bucket rows)");

@@ -392,7 +392,10 @@ __global__ void __launch_bounds__(kSortWarps * 32) excl_sort_small_kernel(CsrVie
         if (lane < 2) bound = csr.indptr[b * (N + 1) + r + lane];
         const int64_t lo = __shfl_sync(kFull, bound, 0);
         const int64_t hi = __shfl_sync(kFull, bound, 1);
-        if (hi > csr.cap_entries) continue;  // overflowed cloud: status already set
+        if (hi > csr.cap_entries) {  // overflowed cloud: status already set; leave a safe row
+            if (lane < csr.L) csr.counts[(b * csr.L + lane) * N + r] = 0;
+            continue;
+        }
         const int m = (int)(hi - lo);
         if (m > kWarpRowCap) {
             if (lane == 0) {
@@ -569,7 +572,10 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) grid_rows_kernel(int64_t B,
         if (FILL) {
             rlo = csr.indptr[b * (N + 1) + i];
             m = csr.indptr[b * (N + 1) + i + 1] - rlo;
-            if (rlo + m > csr.cap_entries) continue;  // overflow: status set by the scan
+            if (rlo + m > csr.cap_entries) {  // overflow: status set by the scan; leave a safe row
+                if (lane < L) csr.counts[(b * csr.L + lane) * N + i] = 0;
+                continue;
+            }
             direct = m > kRowCap;
         }
         int32_t* rn = FILL ? csr.nbr + b * csr.cap_entries + rlo : nullptr;
@@ -696,7 +702,7 @@ __global__ void __launch_bounds__(kEllWarps * 32, 4) grid_ell_kernel(int64_t B, 
     __shared__ double hd[kEllWarps][kEllCap];
     __shared__ int32_t hj[kEllWarps][kEllCap];
     __shared__ uint8_t hb[kEllWarps][kEllCap];
-    __shared__ double lvs[kEllWarps][16];
+    __shared__ double lvs[kEllWarps][32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
     for (int64_t gs = (int64_t)blockIdx.x * kEllWarps + warp; gs < B * N; gs += (int64_t)gridDim.x * kEllWarps) {
@@ -774,7 +780,9 @@ __global__ void __launch_bounds__(kEllWarps * 32, 4) grid_ell_kernel(int64_t B, 
         }
         if (lane == 0) atomicAdd(g.evals + b, (unsigned long long)total);
         if (cnt > stride || cnt > kEllCap) {
+            // overflow: flag it and leave a safe (empty) row until the host rebuilds
             if (lane == 0) atomicOr(&w.status[b], 2);
+            if (lane < L) csr.counts[(b * csr.L + lane) * N + i] = 0;
             continue;
         }
         __syncwarp();

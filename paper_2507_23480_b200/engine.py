@@ -113,7 +113,9 @@ class DeviceCsr:
         ws = int(_lib.raw("ps_excl_workspace_bytes", B, N, cap_edges, method))
         return DeviceCsr(
             indptr=torch.zeros(B, N + 1, dtype=torch.int64, device=device),
-            nbr=torch.empty(B, cap_entries, dtype=torch.int32, device=device),
+            # +16 entries of tail padding: row scans use aligned 16-byte loads
+            nbr=torch.empty(B * cap_entries + 16, dtype=torch.int32, device=device)[:B * cap_entries].view(
+                B, cap_entries),
             d2=torch.empty(B, cap_entries, dtype=torch.float64, device=device),
             counts=torch.empty(B, L, N, dtype=torch.int32, device=device),
             levels=torch.empty(B, L, dtype=torch.float64, device=device),
