@@ -779,16 +779,55 @@ __global__ void __launch_bounds__(kEllWarps * 32, 4) grid_ell_kernel(int64_t B, 
             cnt += __popc(hm);
         }
         if (lane == 0) atomicAdd(g.evals + b, (unsigned long long)total);
-        if (cnt > stride || cnt > kEllCap) {
+        if (cnt > stride) {
             // overflow: flag it and leave a safe (empty) row until the host rebuilds
             if (lane == 0) atomicOr(&w.status[b], 2);
             if (lane < L) csr.counts[(b * csr.L + lane) * N + i] = 0;
             continue;
         }
         __syncwarp();
-        // counting sort by bucket (<= L + 1 buckets), stable in collection order
         int32_t* rn = csr.nbr + b * csr.cap_entries + (int64_t)i * stride;
         double* rd = csr.d2 + b * csr.cap_entries + (int64_t)i * stride;
+        if (cnt > kEllCap) {
+            // long row (beyond the staging buffer): one exact rescan per bucket,
+            // writing straight to the row -- only for very dense neighbourhoods
+            int base2 = 0, hist2 = 0;
+            for (int bk = 0; bk <= L; ++bk) {
+                int here = 0;
+                for (int tb = 0; tb < total; tb += 32) {
+                    const int f = tb + lane;
+                    int rr = 0;
+#pragma unroll
+                    for (int q = 1; q < 9; ++q) rr += (f >= __shfl_sync(kFull, excl0, q)) ? 1 : 0;
+                    const int t = __shfl_sync(kFull, r0, rr) - __shfl_sync(kFull, excl0, rr) + f;
+                    bool in = false;
+                    double d = 0.0;
+                    if (f < total) {
+                        const float4 q = sx[t];
+                        if (no_filter || sqdist_f32(p, q) < thr) {
+                            d = sqdist4(p, q);
+                            if (d < r2) {
+                                int bb = 0;
+                                for (int l = 0; l < L; ++l) bb += (lvs[warp][l] <= d) ? 1 : 0;
+                                in = bb == bk;
+                            }
+                        }
+                    }
+                    const unsigned bm = __ballot_sync(kFull, in);
+                    if (in) {
+                        const int pos = base2 + here + __popc(bm & lt);
+                        rd[pos] = d;
+                        rn[pos] = si[t];
+                    }
+                    here += __popc(bm);
+                }
+                base2 += here;
+                if (lane < L && bk == rank_lt) hist2 = base2;
+            }
+            if (lane < L) csr.counts[(b * csr.L + lane) * N + i] = hist2;
+            continue;
+        }
+        // counting sort by bucket (<= L + 1 buckets), stable in collection order
         int base = 0;
         int hist_mine = 0;  // lane l: entries with bucket <= rank_lt(l)
         for (int bk = 0; bk <= L; ++bk) {

@@ -306,17 +306,25 @@ class FastPoint:
         self.graph = g
         return g
 
-    def check(self):
-        """Host read of the CSR capacity status; grows buffers and re-runs on
-        overflow.  Returns True when a re-run happened."""
-        if not self.csr.overflowed():
-            return False
-        E = int(self.csr.indptr[:, -1].max().item())
-        grow = max(2 * self.csr.cap_entries, E + self.N)
-        self.csr = DeviceCsr.allocate(self.B, self.N, self.L, grow, grow // 2 + 1, self.device, self.excl_method)
-        self.graph = None
-        self.sample()
-        return True
+    def check(self, max_grow=8):
+        """Host read of the CSR capacity status; grows buffers and re-runs
+        until nothing overflows.  Returns True when a re-run happened."""
+        reran = False
+        for _ in range(max_grow):
+            if not self.csr.overflowed():
+                return reran
+            E = int(self.csr.indptr[:, -1].max().item())
+            grow = min(max(2 * self.csr.cap_entries, E + self.N), self.N * self.N + self.N)
+            if self.excl_method == 2:  # keep the row stride whole
+                grow = -(-grow // self.N) * self.N
+            self.csr = DeviceCsr.allocate(self.B, self.N, self.L, grow, grow // 2 + 1, self.device,
+                                          self.excl_method)
+            self.graph = None
+            self.sample()
+            reran = True
+        if self.csr.overflowed():
+            raise RuntimeError("exclusion lists still overflow after growing the capacity")
+        return reran
 
     # -- grouping ---------------------------------------------------------------
     def level_of_radius(self, r: float) -> int:
