@@ -239,10 +239,12 @@ class FastPoint:
         self.xyz4[..., :3].copy_(t, non_blocking=True)
 
     def set_rng(self, seeds):
+        """splitmix64 state per cloud (uint64); the sampler advances it in place."""
         s = np.asarray(seeds, dtype=np.uint64).reshape(-1)
         if s.shape[0] == 1:
             s = np.repeat(s, self.B)
         self.state.copy_(torch.from_numpy(s.view(np.int64).copy()), non_blocking=False)
+        self._state0 = self.state.clone()
 
     def set_curve(self, curves):
         if self.given_curve is None:
@@ -320,6 +322,8 @@ class FastPoint:
             self.csr = DeviceCsr.allocate(self.B, self.N, self.L, grow, grow // 2 + 1, self.device,
                                           self.excl_method)
             self.graph = None
+            if getattr(self, "_state0", None) is not None:
+                self.state.copy_(self._state0)  # replay from the same RNG state
             self.sample()
             reran = True
         if self.csr.overflowed():
