@@ -701,7 +701,9 @@ __global__ void __launch_bounds__(kEllWarps * 32, 4) grid_ell_kernel(int64_t B, 
                                                                      ExclWork w, CsrView csr) {
     __shared__ double hd[kEllWarps][kEllCap];
     __shared__ int32_t hj[kEllWarps][kEllCap];
-    __shared__ uint8_t hb[kEllWarps][kEllCap];
+    __shared__ uint8_t hb[kEllWarps][kEllCap];   // rank within its bucket
+    __shared__ uint8_t hk[kEllWarps][kEllCap];   // bucket
+    __shared__ int hcnt[kEllWarps][33];          // per-bucket counts
     __shared__ double lvs[kEllWarps][32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
@@ -711,6 +713,8 @@ __global__ void __launch_bounds__(kEllWarps * 32, 4) grid_ell_kernel(int64_t B, 
         const double my_r2 = lane < L ? r2_levels[b * levels_ld + lane] : 0.0;
         __syncwarp();
         if (lane < L) lvs[warp][lane] = my_r2;
+        hcnt[warp][lane] = 0;
+        if (lane == 0) hcnt[warp][32] = 0;
         __syncwarp();
         int rank_lt = 0;
         double r2 = 0.0;
@@ -773,7 +777,8 @@ __global__ void __launch_bounds__(kEllWarps * 32, 4) grid_ell_kernel(int64_t B, 
                     for (int l = 0; l < L; ++l) bk += (lvs[warp][l] <= d) ? 1 : 0;
                     hd[warp][slot] = d;
                     hj[warp][slot] = si[t];
-                    hb[warp][slot] = (uint8_t)bk;
+                    hb[warp][slot] = (uint8_t)atomicAdd(&hcnt[warp][bk], 1);  // rank within bucket
+                    hk[warp][slot] = (uint8_t)bk;
                 }
             }
             cnt += __popc(hm);
@@ -827,25 +832,27 @@ __global__ void __launch_bounds__(kEllWarps * 32, 4) grid_ell_kernel(int64_t B, 
             if (lane < L) csr.counts[(b * csr.L + lane) * N + i] = hist2;
             continue;
         }
-        // counting sort by bucket (<= L + 1 buckets), stable in collection order
-        int base = 0;
-        int hist_mine = 0;  // lane l: entries with bucket <= rank_lt(l)
-        for (int bk = 0; bk <= L; ++bk) {
-            int here = 0;
-            for (int e0 = 0; e0 < cnt; e0 += 32) {
-                const int e = e0 + lane;
-                const bool in = e < cnt && hb[warp][e] == bk;
-                const unsigned bm = __ballot_sync(kFull, in);
-                if (in) {
-                    const int pos = base + here + __popc(bm & lt);
-                    rd[pos] = hd[warp][e];
-                    rn[pos] = hj[warp][e];
-                }
-                here += __popc(bm);
-            }
-            base += here;
-            if (lane < L && bk == rank_lt) hist_mine = base;
+        // scatter by bucket: bucket bases from the per-bucket counts (exclusive
+        // prefix across lanes), each entry at base + its rank within the bucket
+        const int hc = lane <= L ? hcnt[warp][lane] : 0;
+        int hincl = hc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, hincl, o);
+            if (lane >= o) hincl += y;
         }
+        const int hbase = hincl - hc;
+        for (int e0 = 0; e0 < cnt; e0 += 32) {
+            const int e = e0 + lane;
+            const int bk = e < cnt ? hk[warp][e] : 0;
+            const int pos = __shfl_sync(kFull, hbase, bk) + (e < cnt ? hb[warp][e] : 0);
+            if (e < cnt) {
+                rd[pos] = hd[warp][e];
+                rn[pos] = hj[warp][e];
+            }
+        }
+        // level l holds buckets 0 .. rank_lt(l)
+        const int hist_mine = __shfl_sync(kFull, hincl, rank_lt < 31 ? rank_lt : 31);
         if (lane < L) csr.counts[(b * csr.L + lane) * N + i] = hist_mine;
         __syncwarp();
     }

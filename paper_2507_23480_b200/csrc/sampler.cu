@@ -60,18 +60,22 @@ __global__ void __launch_bounds__(1024) thresholds_kernel(ThreshArgs a) {
     const int64_t k0 = a.k0, n = a.n;
     const int nseg = a.nseg;
     if (threadIdx.x < kMaxSeg) seg_min[threadIdx.x] = 0x7ff0000000000000ull;  // +inf bits
-    if (a.mode == 0 && threadIdx.x == 0) {
+    if (a.mode == 0) {
+        // products v_i * i**e in parallel (exact per element), then one
+        // thread adds them in index order -- the oracle's sequential sum
+        __shared__ double prod[1024];
         double s = 0.0;
-        int64_t i = 1;
-        for (; i + 8 <= k0; i += 8) {  // loads hoisted, additions kept in order
-            double pv[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) pv[j] = __dmul_rn(v[i + j], a.pow_tab[i + j]);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) s = __dadd_rn(s, pv[j]);
+        for (int64_t c0 = 1; c0 < k0; c0 += 1024) {
+            const int64_t i = c0 + threadIdx.x;
+            if (i < k0) prod[threadIdx.x] = __dmul_rn(v[i], a.pow_tab[i]);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                const int m = (int)((k0 - c0) < 1024 ? (k0 - c0) : 1024);
+                for (int j = 0; j < m; ++j) s = __dadd_rn(s, prod[j]);
+            }
+            __syncthreads();
         }
-        for (; i < k0; ++i) s = __dadd_rn(s, __dmul_rn(v[i], a.pow_tab[i]));
-        s_a = __ddiv_rn(s, (double)(k0 - 1));
+        if (threadIdx.x == 0) s_a = __ddiv_rn(s, (double)(k0 - 1));
     }
     __syncthreads();
     double est_d[kMaxSeg];
@@ -688,11 +692,13 @@ __global__ void et_mark_kernel(EtArgs a) {
 }  // namespace
 
 // md[i] = min(md[i], min over the first lvl1[i] row entries j with taken[j] of d2)
+// Warp per row: coalesced entry loads, exact min (order-independent).
 __global__ void et_scan_kernel(EtScanArgs a) {
-    const int64_t total = a.B * (a.hi - a.lo);
+    const int lane = threadIdx.x & 31;
     const int64_t span = a.hi - a.lo;
-    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
-         g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t total = a.B * span;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; g < total; g += nw) {
         const int64_t b = g / span;
         if (a.reached && a.reached[b] >= a.n_total) continue;
         const int64_t i = a.lo + (g - b * span);
@@ -701,15 +707,24 @@ __global__ void et_scan_kernel(EtScanArgs a) {
         const int32_t* nbr = a.nbr + b * a.cap_entries + base;
         const double* d2 = a.d2 + b * a.cap_entries + base;
         const uint8_t* tk = a.taken + b * a.N;
-        double best = a.md[b * a.N + i];
-        for (int32_t u = 0; u < c; ++u) {
+        double best = __longlong_as_double(0x7ff0000000000000LL);
+        for (int32_t u = lane; u < c; u += 32) {
             const int32_t j = nbr[u];
             if (tk[j]) {
                 const double d = d2[u];
                 if (d < best) best = d;
             }
         }
-        a.md[b * a.N + i] = best;
+        // warp min of non-negative doubles via their bit patterns
+        const unsigned long long bits = (unsigned long long)__double_as_longlong(best);
+        const uint32_t hi = (uint32_t)(bits >> 32);
+        const uint32_t mhi = __reduce_min_sync(kFull, hi);
+        const uint32_t mlo = __reduce_min_sync(kFull, hi == mhi ? (uint32_t)bits : 0xffffffffu);
+        if (lane == 0) {
+            const double wmin = __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
+            double* mp = a.md + b * a.N + i;
+            if (wmin < *mp) *mp = wmin;
+        }
     }
 }
 
@@ -764,12 +779,13 @@ cudaError_t launch_et(const EtArgs& a, cudaStream_t s) {
     sa.lvl1_counts = a.lvl1_counts; sa.counts_stride = a.counts_stride;
     sa.taken = a.taken; sa.md = a.md; sa.reached = a.reached; sa.n_total = a.n_total;
     sa.B = a.B; sa.N = a.N; sa.lo = 0; sa.hi = a.N;
-    et_scan_kernel<<<g1, 256, 0, s>>>(sa);
+    const unsigned g3 = (unsigned)std::min<int64_t>(148 * 16, (a.B * a.N + 7) / 8 + 1);
+    et_scan_kernel<<<g3, 256, 0, s>>>(sa);
     return cudaGetLastError();
 }
 
 cudaError_t launch_et_scan(const EtScanArgs& a, cudaStream_t s) {
-    const unsigned g = (unsigned)std::min<int64_t>(148 * 8, (a.B * (a.hi - a.lo) + 255) / 256 + 1);
+    const unsigned g = (unsigned)std::min<int64_t>(148 * 16, (a.B * (a.hi - a.lo) + 7) / 8 + 1);
     et_scan_kernel<<<g, 256, 0, s>>>(a);
     return cudaGetLastError();
 }
