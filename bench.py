@@ -47,10 +47,28 @@ def dist_env():
     return ws, rank, local
 
 
-def clouds_for(rank: int, B: int):
+def shard_seeds(rank: int, B: int):
+    """Cloud seeds of one rank's shard: disjoint across ranks (batch sharding,
+    no data-path collective)."""
+    return [1000 * 3 + rank * B + b for b in range(B)]
+
+
+def clouds_for(rank: int, B: int, n_points: int = N):
     from paper_2507_23480_b200.harness import generate_cloud
 
-    return np.stack([generate_cloud(FAMILY, N, 1000 * 3 + rank * B + b) for b in range(B)])
+    return np.stack([generate_cloud(FAMILY, n_points, s) for s in shard_seeds(rank, B)])
+
+
+def max_over_ranks(value: float, device=None) -> float:
+    """Max of a per-rank time over the job (the contract's timing rule)."""
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 def heldout_exponent():
@@ -219,7 +237,7 @@ def main_ours(args):
                           extra_radii=(RADIUS,), device=dev)
     d_pts = torch.from_numpy(clouds).to(dev)
     fp.set_points(d_pts)
-    seeds = [rank * B + b for b in range(B)]
+    seeds = [rank * B + b for b in range(B)]  # sampler RNG seeds (clouds: shard_seeds)
     grp = (torch.empty(B, n_SAMPLES, K, dtype=torch.int32, device=dev),
            torch.empty(B, n_SAMPLES, K, dtype=torch.float64, device=dev),
            torch.empty(B, n_SAMPLES, dtype=torch.int32, device=dev))
@@ -268,11 +286,7 @@ def main_ours(args):
     if ws > 1:
         dist.barrier()
     stage_ms = np.array([[ev[s][i].elapsed_time(ev[s][i + 1]) for i in range(6)] for s in range(args.steps)])
-    t_ms = float(stage_ms.sum())
-    if ws > 1:
-        tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_ms = float(tt.item())
+    t_ms = max_over_ranks(float(stage_ms.sum()), dev)
     value = ws * B * n_SAMPLES * args.steps / (t_ms / 1e3)
     per_stage = {nm: float(stage_ms[:, i].mean()) for i, nm in enumerate(stages)}
 
@@ -321,10 +335,7 @@ def main_ours(args):
         b_.record(stream)
         b_.synchronize()
         e2e_ms += a.elapsed_time(b_)
-    if ws > 1:
-        tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = float(tt.item())
+    e2e_ms = max_over_ranks(e2e_ms, dev)
     e2e_value = ws * B * n_SAMPLES * args.steps / (e2e_ms / 1e3)
 
     # ---- roofline for the dominant kernel ------------------------------------------
