@@ -36,7 +36,7 @@ namespace ps {
 namespace {
 
 constexpr int kFpsThreads = 256;
-constexpr int kFpsWarps = kFpsThreads / 32;
+
 constexpr int kMaxCluster = 16;
 constexpr uint32_t kNone = 0xffffffffu;
 
@@ -91,8 +91,10 @@ PS_DEV float skip_threshold(double md) {
 // otherwise the float64 distance ((dx*dx + dy*dy) + dz*dz) is evaluated and
 // folded exactly as _kernels.py:55-60.  The float32 test only skips work --
 // md, the argmax and every output are the float64 reference values.
-template <int P>
-__global__ void __launch_bounds__(kFpsThreads, 1) fps_cluster_kernel(FpsArgs a) {
+template <int P, int T>
+__global__ void __launch_bounds__(T, 1) fps_cluster_kernel(FpsArgs a) {
+    constexpr int kFpsThreads = T;
+    constexpr int kFpsWarps = T / 32;
     __shared__ Rec warp_rec[kFpsWarps];
     __shared__ Rec slots[2][kMaxCluster];
     __shared__ Rec fb_slots[kMaxCluster];
@@ -386,9 +388,9 @@ __global__ void __launch_bounds__(kFpsThreads, 1) fps_cluster_kernel(FpsArgs a) 
     cluster_sync_all();  // no CTA leaves while peers may still target its smem
 }
 
-template <int P>
+template <int P, int T>
 cudaError_t launch_p(const FpsArgs& a, int64_t B, int C, cudaStream_t s) {
-    auto kern = fps_cluster_kernel<P>;
+    auto kern = fps_cluster_kernel<P, T>;
     cudaError_t e = cudaSuccess;
     if (C > 8) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -396,7 +398,7 @@ cudaError_t launch_p(const FpsArgs& a, int64_t B, int C, cudaStream_t s) {
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(B * C), 1, 1);
-    cfg.blockDim = dim3(kFpsThreads, 1, 1);
+    cfg.blockDim = dim3(T, 1, 1);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -411,21 +413,51 @@ cudaError_t launch_p(const FpsArgs& a, int64_t B, int C, cudaStream_t s) {
 
 }  // namespace
 
-static int choose_P(int64_t N, int C) {
+static int fps_threads() {
+    static int t = 0;
+    if (!t) {
+        const char* e = getenv("PS_FPS_THREADS");
+        t = (e && atoi(e) == 512) ? 512 : 256;
+    }
+    return t;
+}
+
+static int choose_P(int64_t N, int C, int T) {
     static const int kPs[] = {1, 2, 3, 4, 6, 8, 12, 16};
     const int64_t S = (N + C - 1) / C;
     for (int p : kPs)
-        if ((int64_t)p * kFpsThreads >= S) return p;
+        if ((int64_t)p * T >= S) return p;
     return 0;  // streaming
 }
 
-template <int P>
+// dispatch a functor over the (P, T) instantiations
+template <typename F>
+static auto with_kernel(int P, int T, F f) {
+#define PS_FPS_CASE(PP)                                        \
+    case PP:                                                   \
+        return T == 512 ? f.template run<PP, 512>() : f.template run<PP, 256>();
+    switch (P) {
+        PS_FPS_CASE(1)
+        PS_FPS_CASE(2)
+        PS_FPS_CASE(3)
+        PS_FPS_CASE(4)
+        PS_FPS_CASE(6)
+        PS_FPS_CASE(8)
+        PS_FPS_CASE(12)
+        PS_FPS_CASE(16)
+        default:
+            return T == 512 ? f.template run<0, 512>() : f.template run<0, 256>();
+    }
+#undef PS_FPS_CASE
+}
+
+template <int P, int T>
 static int max_clusters_p(int C) {
-    auto kern = fps_cluster_kernel<P>;
+    auto kern = fps_cluster_kernel<P, T>;
     if (C > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(C * 64), 1, 1);
-    cfg.blockDim = dim3(kFpsThreads, 1, 1);
+    cfg.blockDim = dim3(T, 1, 1);
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = (unsigned)C;
@@ -441,78 +473,75 @@ static int max_clusters_p(int C) {
     return n;
 }
 
+struct MaxClustersF {
+    int C;
+    template <int P, int T>
+    int run() const { return max_clusters_p<P, T>(C); }
+};
+
+struct LaunchF {
+    const FpsArgs* a;
+    int64_t B;
+    int C;
+    cudaStream_t s;
+    template <int P, int T>
+    cudaError_t run() const { return launch_p<P, T>(*a, B, C, s); }
+};
+
 // Co-resident clusters of size C for the instantiation serving N (cached;
 // depends on the GPU's GPC floor-sweeping, so it is queried, not assumed).
-static int max_active_clusters(int64_t N, int C) {
-    static int cache[17][9];
+static int max_active_clusters(int64_t N, int C, int T) {
+    static int cache[17][9][2];
     static bool init = false;
-    if (!init) { for (auto& row : cache) for (int& v : row) v = -1; init = true; }
-    const int P = choose_P(N, C);
-    const int pi = P == 0 ? 0 : (P <= 4 ? P : (P == 6 ? 5 : (P == 8 ? 6 : (P == 12 ? 7 : 8))));
-    if (cache[C][pi] >= 0) return cache[C][pi];
-    int n = 0;
-    switch (P) {
-        case 1: n = max_clusters_p<1>(C); break;
-        case 2: n = max_clusters_p<2>(C); break;
-        case 3: n = max_clusters_p<3>(C); break;
-        case 4: n = max_clusters_p<4>(C); break;
-        case 6: n = max_clusters_p<6>(C); break;
-        case 8: n = max_clusters_p<8>(C); break;
-        case 12: n = max_clusters_p<12>(C); break;
-        case 16: n = max_clusters_p<16>(C); break;
-        default: n = max_clusters_p<0>(C); break;
+    if (!init) {
+        for (auto& a2 : cache)
+            for (auto& row : a2)
+                for (int& v : row) v = -1;
+        init = true;
     }
-    cache[C][pi] = n;
+    const int P = choose_P(N, C, T);
+    const int pi = P == 0 ? 0 : (P <= 4 ? P : (P == 6 ? 5 : (P == 8 ? 6 : (P == 12 ? 7 : 8))));
+    const int ti = T == 512 ? 1 : 0;
+    if (cache[C][pi][ti] >= 0) return cache[C][pi][ti];
+    const int n = with_kernel(P, T, MaxClustersF{C});
+    cache[C][pi][ti] = n;
+    if (getenv("PS_FPS_VERBOSE")) fprintf(stderr, "[fps] N=%lld C=%d P=%d T=%d max_active_clusters=%d\n",
+                                          (long long)N, C, P, T, n);
     return n;
 }
 
 int fps_choose_cluster(int64_t N, int64_t B, int* C_out, int* P_out) {
+    const int T = fps_threads();
     const char* env = getenv("PS_FPS_CLUSTER");
     int C = 1;
     if (env) {
         C = atoi(env);
     } else {
-        // widest cluster (<= ~4 points per thread) whose B clusters are all
-        // co-resident: one wave, every cloud progressing in lock step
-        const int64_t target = (int64_t)kFpsThreads * 4;
+        // widest cluster (<= ~4 points per thread at 256 threads) whose B
+        // clusters are all co-resident: one wave, every cloud in lock step
+        const int64_t target = (int64_t)256 * 4;
         int64_t c = (N + target - 1) / target;
         int want = (int)(c < 1 ? 1 : (c > kMaxCluster ? kMaxCluster : c));
         int pick = 0;
-        for (int cc : {16, 12, 8, 6, 4, 3, 2, 1}) {
+        for (int cc : {16, 14, 12, 10, 8, 6, 4, 3, 2, 1}) {
             if (cc > want) continue;
-            if (choose_P(N, cc) == 0 && cc != kMaxCluster) continue;
-            if (max_active_clusters(N, cc) >= B) { pick = cc; break; }
+            if (choose_P(N, cc, T) == 0 && cc != kMaxCluster) continue;
+            if (max_active_clusters(N, cc, T) >= B) { pick = cc; break; }
         }
-        if (!pick) {
-            // batch larger than one wave at any width: keep clusters <= 8 wide
-            pick = want > 8 ? 8 : want;
-        }
+        if (!pick) pick = want > 8 ? 8 : want;  // batch larger than one wave at any width
         C = pick;
     }
     if (C < 1) C = 1;
     if (C > kMaxCluster) C = kMaxCluster;
     *C_out = C;
-    *P_out = choose_P(N, C);
+    *P_out = choose_P(N, C, T);
     return 0;
-}
-
-static cudaError_t launch_any(const FpsArgs& a, int64_t B, int C, int P, cudaStream_t s) {
-    switch (P) {
-        case 1: return launch_p<1>(a, B, C, s);
-        case 2: return launch_p<2>(a, B, C, s);
-        case 3: return launch_p<3>(a, B, C, s);
-        case 4: return launch_p<4>(a, B, C, s);
-        case 6: return launch_p<6>(a, B, C, s);
-        case 8: return launch_p<8>(a, B, C, s);
-        case 12: return launch_p<12>(a, B, C, s);
-        case 16: return launch_p<16>(a, B, C, s);
-        default: return launch_p<0>(a, B, C, s);
-    }
 }
 
 cudaError_t launch_fps(FpsArgs a, int64_t B, cudaStream_t s) {
     int C = 1, P = 0;
     fps_choose_cluster(a.N, B, &C, &P);
+    const int T = fps_threads();
     a.points_per_cta = (a.N + C - 1) / C;
     a.dbg = nullptr;
     if (getenv("PS_FPS_TIMING")) {
@@ -522,7 +551,7 @@ cudaError_t launch_fps(FpsArgs a, int64_t B, cudaStream_t s) {
         if (!dbg) cudaMalloc(&dbg, sizeof(long long) * 256 * 8);
         cudaMemsetAsync(dbg, 0, sizeof(long long) * 256 * 8, s);
         a.dbg = dbg;
-        cudaError_t e = launch_any(a, B, C, P, s);
+        cudaError_t e = with_kernel(P, T, LaunchF{&a, B, C, s});
         if (e != cudaSuccess) return e;
         long long h[256 * 8];
         cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, s);
@@ -533,12 +562,12 @@ cudaError_t launch_fps(FpsArgs a, int64_t B, cudaStream_t s) {
         for (int t = 8; t < iters; ++t, ++cnt)
             for (int k = 0; k < 7; ++k) acc[k] += (double)h[t * 8 + k];
         if (cnt)
-            fprintf(stderr, "[fps timing] C=%d P=%d N=%lld iters=%d cycles: compute %.0f warpred %.0f bar %.0f send %.0f wait %.0f final %.0f total %.0f\n",
-                    C, P, (long long)a.N, cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt,
+            fprintf(stderr, "[fps timing] C=%d P=%d T=%d N=%lld iters=%d cycles: compute %.0f warpred %.0f bar %.0f send %.0f wait %.0f final %.0f total %.0f\n",
+                    C, P, T, (long long)a.N, cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt,
                     acc[4] / cnt, acc[5] / cnt, acc[6] / cnt);
         return cudaSuccess;
     }
-    return launch_any(a, B, C, P, s);
+    return with_kernel(P, T, LaunchF{&a, B, C, s});
 }
 
 }  // namespace ps
