@@ -35,7 +35,6 @@ namespace ps {
 
 namespace {
 
-constexpr int kFpsThreads = 256;
 
 constexpr int kMaxCluster = 16;
 constexpr uint32_t kNone = 0xffffffffu;
@@ -274,6 +273,22 @@ __global__ void __launch_bounds__(T, 1) fps_cluster_kernel(FpsArgs a) {
             __syncthreads();
             if (tdbg) a.dbg[t * 8 + 2] = clock64() - ts0;
 
+            Rec win;
+            if (C == 1) {
+                // single-CTA cloud: the block argmax is the answer, no exchange
+                if (warp == kFpsWarps - 1) {
+                    const Rec wr = lane < kFpsWarps ? warp_rec[lane] : Rec{0, 0, kNone, 0, 0.f, 0.f, 0.f, 0};
+                    const int cl = warp_argmax_lane(rec_key(wr), wr.idx);
+                    if (lane == 0) {
+                        Rec cr = warp_rec[cl < 0 ? 0 : cl];
+                        if (cl < 0) cr.idx = kNone;
+                        slots[par][0] = cr;
+                    }
+                }
+                __syncthreads();
+                win = slots[par][0];
+                if (tdbg) { a.dbg[t * 8 + 3] = clock64() - ts0; a.dbg[t * 8 + 4] = a.dbg[t * 8 + 3]; a.dbg[t * 8 + 5] = a.dbg[t * 8 + 3]; }
+            } else {
             // 3+4. block argmax, push the CTA record to every CTA of the cluster
             // (the highest warp id leads: the SMSP arbiter favours high ids)
             if (warp == kFpsWarps - 1) {
@@ -295,10 +310,11 @@ __global__ void __launch_bounds__(T, 1) fps_cluster_kernel(FpsArgs a) {
             if (tdbg) a.dbg[t * 8 + 4] = clock64() - ts0;
             const Rec sr = lane < (int)C ? slots[par][lane] : Rec{0, 0, kNone, 0, 0.f, 0.f, 0.f, 0};
             const int gl = warp_argmax_lane(rec_key(sr), sr.idx);
-            Rec win = slots[par][gl < 0 ? 0 : gl];
+            win = slots[par][gl < 0 ? 0 : gl];
             __syncwarp();
             if (tid == 0) mbar_arrive_expect_tx(&bars[par], tx_bytes);
             if (tdbg) a.dbg[t * 8 + 5] = clock64() - ts0;
+            }
 
             double best = bitsd(rec_key(win));
             if (best <= 0.0 || win.taken) {
@@ -413,13 +429,9 @@ cudaError_t launch_p(const FpsArgs& a, int64_t B, int C, cudaStream_t s) {
 
 }  // namespace
 
-static int fps_threads() {
-    static int t = 0;
-    if (!t) {
-        const char* e = getenv("PS_FPS_THREADS");
-        t = (e && atoi(e) == 512) ? 512 : 256;
-    }
-    return t;
+static int fps_threads_env() {
+    const char* e = getenv("PS_FPS_THREADS");
+    return e ? (atoi(e) == 512 ? 512 : 256) : 0;
 }
 
 static int choose_P(int64_t N, int C, int T) {
@@ -443,10 +455,12 @@ static auto with_kernel(int P, int T, F f) {
         PS_FPS_CASE(4)
         PS_FPS_CASE(6)
         PS_FPS_CASE(8)
-        PS_FPS_CASE(12)
-        PS_FPS_CASE(16)
+        case 12:  // 512-thread CTAs only up to P = 8 (register budget)
+            return f.template run<12, 256>();
+        case 16:
+            return f.template run<16, 256>();
         default:
-            return T == 512 ? f.template run<0, 512>() : f.template run<0, 256>();
+            return f.template run<0, 256>();
     }
 #undef PS_FPS_CASE
 }
@@ -510,38 +524,47 @@ static int max_active_clusters(int64_t N, int C, int T) {
     return n;
 }
 
-int fps_choose_cluster(int64_t N, int64_t B, int* C_out, int* P_out) {
-    const int T = fps_threads();
+// Cluster width C and CTA size T: the widest cluster whose B clusters are
+// all co-resident (one wave, every cloud in lock step), preferring 512-thread
+// CTAs (more warps hide the fold's latency) while P <= 8 points per thread.
+int fps_choose_cluster(int64_t N, int64_t B, int* C_out, int* P_out, int* T_out) {
     const char* env = getenv("PS_FPS_CLUSTER");
-    int C = 1;
+    const int tenv = fps_threads_env();
+    const int64_t target = (int64_t)256 * 4;
+    const int64_t c0 = (N + target - 1) / target;
+    const int want = (int)(c0 < 1 ? 1 : (c0 > kMaxCluster ? kMaxCluster : c0));
+    int C = 0, T = 0;
     if (env) {
         C = atoi(env);
+        if (C < 1) C = 1;
+        if (C > kMaxCluster) C = kMaxCluster;
+        T = tenv ? tenv : (choose_P(N, C, 512) >= 1 && choose_P(N, C, 512) <= 8 ? 512 : 256);
     } else {
-        // widest cluster (<= ~4 points per thread at 256 threads) whose B
-        // clusters are all co-resident: one wave, every cloud in lock step
-        const int64_t target = (int64_t)256 * 4;
-        int64_t c = (N + target - 1) / target;
-        int want = (int)(c < 1 ? 1 : (c > kMaxCluster ? kMaxCluster : c));
-        int pick = 0;
-        for (int cc : {16, 14, 12, 10, 8, 6, 4, 3, 2, 1}) {
-            if (cc > want) continue;
-            if (choose_P(N, cc, T) == 0 && cc != kMaxCluster) continue;
-            if (max_active_clusters(N, cc, T) >= B) { pick = cc; break; }
+        for (int t : {512, 256}) {
+            if (tenv && t != tenv) continue;
+            for (int cc : {16, 14, 12, 10, 8, 6, 4, 3, 2, 1}) {
+                if (cc > want) continue;
+                const int p = choose_P(N, cc, t);
+                if (t == 512 && (p == 0 || p > 8)) continue;
+                if (p == 0 && cc != kMaxCluster) continue;
+                if (max_active_clusters(N, cc, t) >= B) { C = cc; T = t; break; }
+            }
+            if (C) break;
         }
-        if (!pick) pick = want > 8 ? 8 : want;  // batch larger than one wave at any width
-        C = pick;
+        if (!C) {  // batch larger than one wave at any width
+            C = want > 8 ? 8 : want;
+            T = tenv ? tenv : 256;
+        }
     }
-    if (C < 1) C = 1;
-    if (C > kMaxCluster) C = kMaxCluster;
     *C_out = C;
+    *T_out = T;
     *P_out = choose_P(N, C, T);
     return 0;
 }
 
 cudaError_t launch_fps(FpsArgs a, int64_t B, cudaStream_t s) {
-    int C = 1, P = 0;
-    fps_choose_cluster(a.N, B, &C, &P);
-    const int T = fps_threads();
+    int C = 1, P = 0, T = 256;
+    fps_choose_cluster(a.N, B, &C, &P, &T);
     a.points_per_cta = (a.N + C - 1) / C;
     a.dbg = nullptr;
     if (getenv("PS_FPS_TIMING")) {

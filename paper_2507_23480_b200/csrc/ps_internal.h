@@ -22,7 +22,7 @@ struct FpsArgs {
 };
 
 cudaError_t launch_fps(FpsArgs a, int64_t B, cudaStream_t s);
-int fps_choose_cluster(int64_t N, int64_t B, int* C_out, int* P_out);
+int fps_choose_cluster(int64_t N, int64_t B, int* C_out, int* P_out, int* T_out);
 
 // Exclusion-list CSR (one cloud = rows [b][0..N); entries at b*cap_entries).
 struct CsrView {
