@@ -821,7 +821,7 @@ __global__ void __launch_bounds__(kEllWarps * 32, 4) grid_ell_kernel(int64_t B, 
                     const unsigned bm = __ballot_sync(kFull, in);
                     if (in) {
                         const int pos = base2 + here + __popc(bm & lt);
-                        rd[pos] = d;
+                        __stcs(rd + pos, d);  // d2 streams to HBM: keep L2 for the nbr rows
                         rn[pos] = si[t];
                     }
                     here += __popc(bm);
@@ -847,7 +847,7 @@ __global__ void __launch_bounds__(kEllWarps * 32, 4) grid_ell_kernel(int64_t B, 
             const int bk = e < cnt ? hk[warp][e] : 0;
             const int pos = __shfl_sync(kFull, hbase, bk) + (e < cnt ? hb[warp][e] : 0);
             if (e < cnt) {
-                rd[pos] = hd[warp][e];
+                __stcs(rd + pos, hd[warp][e]);  // d2 streams to HBM: keep L2 for the nbr rows
                 rn[pos] = hj[warp][e];
             }
         }
