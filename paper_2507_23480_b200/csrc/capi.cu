@@ -259,10 +259,10 @@ int ps_thresholds(const double* prefix_curve, int64_t curve_ld, int64_t B, int64
     return cuda_status(ps::launch_thresholds(a, B, S(stream)), "thresholds", 1);
 }
 
+static bool sampler_fits_smem(int64_t N, int nseg) { return ps::sampler_ws_bytes(N, nseg) <= 176 * 1024; }
+
 int64_t ps_sampler_workspace_bytes(int64_t B, int64_t N, int32_t nseg) {
-    const size_t per = ps::sampler_ws_bytes(N, nseg);
-    if (per <= 192 * 1024) return 0;
-    return (int64_t)(per * B);
+    return (int64_t)ps::sampler_global_ws_bytes(B, N, !sampler_fits_smem(N, nseg));
 }
 
 int ps_sample_predicted(const int64_t* indptr, const int32_t* nbr, int64_t cap_entries, const int32_t* counts,
@@ -286,14 +286,11 @@ int ps_sample_predicted(const int64_t* indptr, const int32_t* nbr, int64_t cap_e
     }
     a.k0 = k0; a.n_total = n_total; a.N = N; a.out_idx = out_idx; a.ld_out = ld_out; a.state_io = state_io;
     a.pick_lowest = pick_lowest; a.reached = reached; a.exhausted = exhausted; a.entered = entered;
-    const size_t per = ps::sampler_ws_bytes(N, nseg);
-    a.use_smem = per <= 192 * 1024 ? 1 : 0;
-    if (!a.use_smem) {
-        CHECK_ARG(work != nullptr, "sampler workspace required for N=%lld", (long long)N);
-        a.gws = static_cast<unsigned char*>(work);
-        a.gws_stride = (int64_t)per;
-    }
-    return cuda_status(ps::launch_sampler(a, B, S(stream)), "sample_predicted", 1);
+    a.use_smem = sampler_fits_smem(N, nseg) ? 1 : 0;
+    CHECK_ARG(work != nullptr, "sampler workspace required (ps_sampler_workspace_bytes)");
+    a.gws = static_cast<unsigned char*>(work);
+    a.B = B;
+    return cuda_status(ps::launch_sampler(a, B, S(stream)), "sample_predicted", 2 + 3 * nseg);
 }
 
 int ps_earlyterm_scan(const int64_t* indptr, const int32_t* nbr, const double* d2, int64_t cap_entries,

@@ -35,7 +35,7 @@ struct SampArgs {
     int nseg;
     int seg_level_rows[kMaxSeg];
     int64_t boundaries[kMaxSeg]; // segment ends, last == n_total
-    int64_t k0, n_total, N;
+    int64_t k0, n_total, N, B;
     int64_t* out_idx;            // [B][ld_out]; [0, k0) = prefix on entry
     int64_t ld_out;
     uint64_t* state_io;          // [B]
@@ -44,7 +44,7 @@ struct SampArgs {
     int32_t* exhausted;          // [B]
     int32_t* entered;            // [B]
     int use_smem;
-    unsigned char* gws;          // global workspace (use_smem == 0)
+    unsigned char* gws;          // global workspace (always; tables too when use_smem == 0)
     int64_t gws_stride;
     long long* dbg;              // development timing (PS_SAMPLER_TIMING)
 };
@@ -77,7 +77,8 @@ struct EtScanArgs {
     int64_t n_total, B, N, lo, hi;
 };
 
-size_t sampler_ws_bytes(int64_t N, int nseg);
+size_t sampler_ws_bytes(int64_t N, int nseg);              // shared-memory tables per cloud
+size_t sampler_global_ws_bytes(int64_t B, int64_t N, bool big);  // global workspace
 cudaError_t launch_thresholds(const ThreshArgs& a, int64_t B, cudaStream_t s);
 cudaError_t launch_sampler(SampArgs a, int64_t B, cudaStream_t s);
 cudaError_t launch_et(const EtArgs& a, cudaStream_t s);
