@@ -234,6 +234,16 @@ __global__ void __launch_bounds__(kVThreads, 1) samp_visit_kernel(SampArgs a, Sa
     const int32_t* cnt_row = a.counts + (b * a.L + lvl) * N;
     const int64_t* indptr = a.indptr + b * (N + 1);
     const int32_t* nbr_all = a.nbr + b * a.cap_entries;
+    const bool tdbg = a.dbg && b == 0 && tid == 0;
+    long long tl = tdbg ? clock64() : 0;
+#define VT(k)                                              \
+    do {                                                   \
+        if (tdbg) {                                        \
+            const long long n_ = clock64();                \
+            a.dbg[k] += n_ - tl;                           \
+            tl = n_;                                       \
+        }                                                  \
+    } while (0)
 
     // pool = available points in index order (_kernels.py:293-298); rank table empty
     for (int64_t j = tid; j < N; j += kVThreads) rank[j] = kNoRank;
@@ -254,6 +264,7 @@ __global__ void __launch_bounds__(kVThreads, 1) samp_visit_kernel(SampArgs a, Sa
     }
     const int64_t L = carry;
     __syncthreads();
+    VT(0);
 
     const uint64_t state0 = st.rng;
     const int64_t i_start = st.i;
@@ -278,6 +289,7 @@ __global__ void __launch_bounds__(kVThreads, 1) samp_visit_kernel(SampArgs a, Sa
                 vs.keys[tid] = ~0ull;
             }
             __syncthreads();
+            VT(1);
             for (int kk = 2; kk <= kChunk; kk <<= 1) {
                 for (int jj = kk >> 1; jj > 0; jj >>= 1) {
                     const int ix = tid;
@@ -292,6 +304,7 @@ __global__ void __launch_bounds__(kVThreads, 1) samp_visit_kernel(SampArgs a, Sa
             }
             if (tid < K) vs.sidx[(unsigned)vs.keys[tid]] = (int16_t)tid;
             __syncthreads();
+            VT(2);
             if (tid < K) {
                 const int t = tid;
                 const uint32_t p = vs.pos[t];
@@ -313,6 +326,7 @@ __global__ void __launch_bounds__(kVThreads, 1) samp_visit_kernel(SampArgs a, Sa
                 vs.ptr[t] = (int16_t)(wl >= 0 ? wl : t);
             }
             __syncthreads();
+            VT(3);
             // pointer jumping to the chain root (a draw whose last slot was untouched)
             for (int r = 0; r < 11; ++r) {
                 int16_t np = 0;
@@ -323,6 +337,7 @@ __global__ void __launch_bounds__(kVThreads, 1) samp_visit_kernel(SampArgs a, Sa
             }
             if (tid < K) vs.wv[tid] = pool[m0 - 1 - vs.ptr[tid]];
             __syncthreads();
+            VT(4);
             if (tid < K) {
                 const int pv = vs.prv[tid];
                 vs.cand[tid] = pv >= 0 ? vs.wv[pv] : pool[vs.pos[tid]];
@@ -337,6 +352,7 @@ __global__ void __launch_bounds__(kVThreads, 1) samp_visit_kernel(SampArgs a, Sa
             }
         }
         __syncthreads();
+        VT(5);
         // ---- greedy MIS over the chunk -------------------------------------------------
         const int32_t cme = tid < K ? vs.cand[tid] : 0;
         if (tid < K) {
@@ -394,6 +410,7 @@ __global__ void __launch_bounds__(kVThreads, 1) samp_visit_kernel(SampArgs a, Sa
         und = __reduce_add_sync(kFull, und);
         if ((tid & 31) == 0 && und) atomicAdd(&s_und, und);
         __syncthreads();
+        VT(6);
         while (s_und != 0) {
             __syncthreads();
             if (tid == 0) s_und = 0;
@@ -439,6 +456,8 @@ __global__ void __launch_bounds__(kVThreads, 1) samp_visit_kernel(SampArgs a, Sa
             if ((tid & 31) == 0 && u2) atomicAdd(&s_und, u2);
             __syncthreads();
         }
+        VT(7);
+        if (tdbg) a.dbg[11] += 1;
         // ---- ordered compaction; truncation at the boundary -----------------------------
         const int64_t need = a.boundaries[st.seg] - i;
         const int flag = (tid < K && vs.st[tid] == kIn) ? 1 : 0;
@@ -458,6 +477,7 @@ __global__ void __launch_bounds__(kVThreads, 1) samp_visit_kernel(SampArgs a, Sa
             last_draw = k + s_acc;
         i += take;
         __syncthreads();
+        VT(8);
         if (ends) { ended = true; break; }
         k += K;
     }
@@ -501,6 +521,8 @@ __global__ void __launch_bounds__(kVThreads, 1) samp_visit_kernel(SampArgs a, Sa
         }
         w.st[b] = st;
     }
+    VT(9);
+#undef VT
 }
 
 }  // namespace
@@ -538,6 +560,13 @@ cudaError_t launch_sampler(SampArgs a, int64_t B, cudaStream_t s) {
         w.grank = reinterpret_cast<uint16_t*>(p);
     }
     a.B = B;
+    a.dbg = nullptr;
+    if (getenv("PS_SAMPLER_TIMING")) {  // development aid (synchronises)
+        static long long* dbg = nullptr;
+        if (!dbg) cudaMalloc(&dbg, sizeof(long long) * 16);
+        cudaMemsetAsync(dbg, 0, sizeof(long long) * 16, s);
+        a.dbg = dbg;
+    }
     const size_t dsm = a.use_smem ? sampler_ws_bytes(a.N, a.nseg) : 0;
     if (a.use_smem) {
         cudaError_t e = cudaFuncSetAttribute(samp_visit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
@@ -552,6 +581,14 @@ cudaError_t launch_sampler(SampArgs a, int64_t B, cudaStream_t s) {
         samp_visit_kernel<<<(unsigned)B, kVThreads, dsm, s>>>(a, w, sg);
     }
     samp_final_kernel<<<(unsigned)((B + 127) / 128), 128, 0, s>>>(a, w);
+    if (a.dbg) {
+        long long h[16];
+        cudaMemcpyAsync(h, a.dbg, sizeof(h), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        fprintf(stderr, "[visit timing] cycles: pool %lld positions %lld sort %lld links %lld jump+wv %lld "
+                "cand %lld mis0 %lld rounds %lld compact %lld final %lld chunks %lld\n", h[0], h[1], h[2], h[3],
+                h[4], h[5], h[6], h[7], h[8], h[9], h[11]);
+    }
     return cudaGetLastError();
 }
 

@@ -44,8 +44,8 @@ def test_validation_without_device():
     assert rc == _lib.PS_ERR_INVALID
     assert b"last segment boundary" in lib.ps_last_error()
     assert lib.ps_excl_workspace_bytes(2, 100, 50, 0) > 0 and lib.ps_excl_workspace_bytes(2, 100, 1, 1) > 0
-    assert lib.ps_sampler_workspace_bytes(1, 24000, 6) == 0      # fits in shared memory
-    assert lib.ps_sampler_workspace_bytes(2, 100000, 6) > 0     # global workspace
+    assert 0 < lib.ps_sampler_workspace_bytes(1, 24000, 6) < lib.ps_sampler_workspace_bytes(1, 40000, 6) / 1.5
+    assert lib.ps_sampler_workspace_bytes(2, 100000, 6) > 2 * lib.ps_sampler_workspace_bytes(1, 100000, 6) * 0.99
 
 
 def test_curve_helpers_match_oracle():
