@@ -562,7 +562,7 @@ int fps_choose_cluster(int64_t N, int64_t B, int* C_out, int* P_out, int* T_out)
     return 0;
 }
 
-cudaError_t launch_fps(FpsArgs a, int64_t B, cudaStream_t s) {
+cudaError_t launch_fps_legacy(FpsArgs a, int64_t B, cudaStream_t s) {
     int C = 1, P = 0, T = 256;
     fps_choose_cluster(a.N, B, &C, &P, &T);
     a.points_per_cta = (a.N + C - 1) / C;

@@ -1,0 +1,763 @@
+// fps_res.cu -- K1 v2: exact farthest-point sampling with the cloud resident
+// in shared memory, spatially ordered per CTA (B200 / sm_100a).
+//
+// Replaces _kernels.fps_loop (/root/reference/pkg/src/pointsample/_kernels.py:35-74)
+// and its chunked merge fps_update_chunk/first_untaken (:77-100).
+//
+// One thread-block cluster of C CTAs per cloud (per cloud shard when a cloud
+// is split over G ranks, see below).  CTA r of the cluster owns the points
+// with original index in [lo, hi) and, at launch, counting-sorts them by a
+// 12-bit Morton cell of their own bounding box into shared memory as
+// float4 {x, y, z, original index}.  Warp w owns the sorted range
+// [w*32P, (w+1)*32P): 32P spatially close points whose bounding box it keeps
+// in registers, together with the float64 min-distance md of each of its
+// points (registers, P per lane) and its cached argmax record (shared).
+//
+// Per iteration, with s the last sample:
+//   1. warp skip: a rounded-down lower bound of |s - box|^2 above the warp's
+//      skip threshold (>= max md of the warp) proves that no md in the warp
+//      can decrease -- the warp does nothing and its record stays valid;
+//   2. touched warps: float32 screen per point, exact float64 fold
+//      ((dx*dx + dy*dy) + dz*dz, no FMA, _kernels.py:55-60) where the screen
+//      cannot exclude an update; if an md changed, the thread max and the
+//      warp argmax (max md, lowest ORIGINAL index) are recomputed;
+//   3. the leader warp waits for the others on a named barrier (they do not
+//      wait), reduces the warp records and pushes the CTA record to every
+//      CTA of the cluster with st.async + mbarrier complete_tx;
+//   4. every warp reduces the C records identically (max md, lowest index);
+//   5. with G > 1 ranks, CTA 0 of every rank publishes the cluster record to
+//      every rank's global mailbox (peer memory over NVLink, or the same GPU
+//      for virtual ranks), each CTA's leader polls the G records of this
+//      iteration (sequence-tagged 16-byte halves) and broadcasts the winner.
+// The duplicate fallback of _kernels.py:65-70 (max <= 0 or winner taken ->
+// lowest untaken index) is a rare second exchange with the same structure.
+//
+// Bit-exactness: every md is the reference float64 value; the float32 tests
+// only skip folds that provably cannot change md (margins in common.cuh /
+// skip_threshold); ties resolve to the lowest original index at every level,
+// so any partition of the cloud gives the reference's choice.
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "ps_internal.h"
+
+namespace ps {
+
+namespace {
+
+constexpr int kT = 512;
+constexpr int kW = kT / 32;
+constexpr int kMaxC = 16;
+constexpr int kBins = 4096;  // 16^3 Morton cells per CTA bounding box
+constexpr uint32_t kNone = 0xffffffffu;
+constexpr int kMaxP = 24;
+constexpr uint32_t kForeign = 0x7fffffffu;  // owner field of another rank's point (g field all ones)
+
+struct __align__(16) Rec {
+    uint32_t klo, khi, idx, own;  // own: bit31 taken | rank g << 18 | cta r << 14 | local sorted pos
+    float x, y, z;
+    uint32_t pad;
+};
+
+PS_DEV uint64_t dbits(double d) { return (uint64_t)__double_as_longlong(d); }
+PS_DEV double bitsd(uint64_t k) { return __longlong_as_double((long long)k); }
+PS_DEV uint64_t rec_key(const Rec& r) { return ((uint64_t)r.khi << 32) | r.klo; }
+PS_DEV Rec none_rec() {
+    Rec z;
+    z.klo = z.khi = 0; z.idx = kNone; z.own = 0; z.x = z.y = z.z = 0.f; z.pad = 0;
+    return z;
+}
+
+// Winner lane of a warp argmax over (key, idx): max key, lowest idx on ties;
+// -1 if no lane has idx != kNone.
+PS_DEV int argmax_lane(uint64_t key, uint32_t idx) {
+    const bool valid = idx != kNone;
+    const uint32_t hi = valid ? (uint32_t)(key >> 32) : 0u;
+    const uint32_t mhi = __reduce_max_sync(kFull, hi);
+    unsigned cand = __ballot_sync(kFull, valid && hi == mhi);
+    if (cand == 0) return -1;
+    if (__popc(cand) == 1) return __ffs(cand) - 1;
+    const bool c1 = (cand >> (threadIdx.x & 31)) & 1u;
+    const uint32_t lo = (uint32_t)key;
+    const uint32_t mlo = __reduce_max_sync(kFull, c1 ? lo : 0u);
+    const bool c2 = c1 && lo == mlo;
+    const uint32_t midx = __reduce_min_sync(kFull, c2 ? idx : kNone);
+    return __ffs(__ballot_sync(kFull, c2 && idx == midx)) - 1;
+}
+
+// conservative float32 skip threshold for "d < md" (see fps.cu): any exact
+// float64 distance whose float32 evaluation (or rounded-down lower bound)
+// exceeds it is > md.
+PS_DEV float skip_thr(double md) {
+    if (md == 0.0) return -1.0f;
+    if (!(md >= 7.888609052210118e-31)) return __int_as_float(0x7f800000);
+    return __fmul_ru(__double2float_ru(md), 1.0f + 3.814697265625e-06f);  // * (1 + 2^-18)
+}
+
+// branch-free form of skip_thr for predicated folds (d > 0 finite or 0)
+PS_DEV float skip_thr_nb(double md) {
+    const float t = __fmul_ru(__double2float_ru(md), 1.0f + 3.814697265625e-06f);
+    const float u = md >= 7.888609052210118e-31 ? t : __int_as_float(0x7f800000);
+    return md == 0.0 ? -1.0f : u;
+}
+
+PS_DEV void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+PS_DEV void named_bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+PS_DEV uint32_t morton12(float x, float y, float z, float ox, float oy, float oz, float sx, float sy, float sz) {
+    const uint32_t qx = (uint32_t)min(15, max(0, (int)((x - ox) * sx)));
+    const uint32_t qy = (uint32_t)min(15, max(0, (int)((y - oy) * sy)));
+    const uint32_t qz = (uint32_t)min(15, max(0, (int)((z - oz) * sz)));
+    uint32_t c = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        c |= (((qx >> i) & 1u) << (3 * i)) | (((qy >> i) & 1u) << (3 * i + 1)) | (((qz >> i) & 1u) << (3 * i + 2));
+    return c;
+}
+
+// ---- global mailboxes (G > 1) ----------------------------------------------------
+// Mailbox of a rank: uint4[B][3][G][2]; set 0/1 = iteration parity, set 2 =
+// duplicate fallback.  A record is two 16-byte halves, each tagged with the
+// 32-bit sequence number, so a reader accepts it only when both halves carry
+// the expected tag (written by the owner with relaxed system-scope stores,
+// possibly from a peer GPU over NVLink).
+
+PS_DEV void st_sys_v4(uint4* p, uint4 v) {
+    asm volatile("st.relaxed.sys.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+PS_DEV uint4 ld_sys_v4(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.relaxed.sys.global.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p)
+                 : "memory");
+    return v;
+}
+
+// idx travels with the taken flag in bit 31 (indices are < 2^30)
+PS_DEV void mbox_put(uint4* slot, const Rec& r, uint32_t seq) {
+    const uint32_t ix = r.idx == kNone ? kNone : (r.idx | (r.own & 0x80000000u));
+    st_sys_v4(slot, make_uint4(r.klo, r.khi, ix, seq));
+    st_sys_v4(slot + 1, make_uint4(__float_as_uint(r.x), __float_as_uint(r.y), __float_as_uint(r.z), seq));
+}
+
+PS_DEV Rec mbox_get(const uint4* slot, uint32_t seq) {
+    uint4 h0, h1;
+    do {
+        h0 = ld_sys_v4(slot);
+        h1 = ld_sys_v4(slot + 1);
+    } while (h0.w != seq || h1.w != seq);
+    Rec r;
+    r.klo = h0.x; r.khi = h0.y;
+    r.idx = h0.z == kNone ? kNone : (h0.z & 0x7fffffffu);
+    r.own = h0.z == kNone ? 0u : ((h0.z & 0x80000000u) | kForeign);
+    r.x = __uint_as_float(h1.x); r.y = __uint_as_float(h1.y); r.z = __uint_as_float(h1.z); r.pad = 0;
+    return r;
+}
+
+template <int P>
+__global__ void __launch_bounds__(kT, 1) fps_res_kernel(FpsArgs a, FpsRanks rk) {
+    constexpr int QG = P <= 8 ? P : (P % 8 == 0 ? 8 : 6);  // slots per screen group
+    extern __shared__ __align__(16) unsigned char dsm[];
+    float4* pts = reinterpret_cast<float4*>(dsm);                // [P * kT] sorted points
+    uint32_t* hist = reinterpret_cast<uint32_t*>(pts + P * kT);  // [kBins]
+    __shared__ Rec warp_rec[kW];
+    __shared__ Rec fb_rec[kW];
+    __shared__ Rec slots[2][kMaxC];
+    __shared__ Rec fb_slots[kMaxC];
+    __shared__ Rec gslot;
+    __shared__ __align__(8) uint64_t bars[2];
+    __shared__ float red[6][kW];
+    __shared__ uint32_t scan_tot[kW];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t C = cluster_nctarank();
+    const uint32_t r = cluster_ctarank();
+    const int64_t cid = cluster_id_x();
+    const int G = rk.G;
+    const int64_t b = cid / rk.Gl;
+    const int g = rk.g_base + (int)(cid % rk.Gl);
+    const int64_t N = a.N;
+    const int64_t Ns = (N + G - 1) / G;
+    const int64_t shard_lo = min(N, (int64_t)g * Ns);
+    const int64_t shard_hi = min(N, shard_lo + Ns);
+    const int64_t S = a.points_per_cta;
+    const int64_t lo = min(shard_hi, shard_lo + (int64_t)r * S);
+    const int64_t hi = min(shard_hi, lo + S);
+    const int cnt = (int)(hi - lo);
+    const float4* __restrict__ xyz = a.xyz + b * N;
+    double* __restrict__ md = a.md + b * N;
+    uint8_t* __restrict__ taken = a.taken + b * N;
+    int64_t* __restrict__ out = a.out_idx + b * a.ld_out;
+    double* __restrict__ curve = a.curve + b * a.ld_out;
+    const bool writer = (g == 0 || rk.all_write) && r == 0;
+
+    const int64_t k_start = a.k_start_dev ? a.k_start_dev[b] : a.k_start;
+    const int64_t k_stop = a.k_stop;
+    const int64_t seed = a.seed_dev ? a.seed_dev[b] : a.seed;
+    const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+    const uint32_t tx_bytes = C * (uint32_t)sizeof(Rec);
+    uint4* mb_dst = nullptr;          // lane's destination rank mailbox (G > 1)
+    const uint4* mb_mine = nullptr;   // this rank's mailbox
+    if (G > 1) {
+        mb_dst = lane < G ? rk.mbox[lane] : nullptr;
+        mb_mine = rk.mbox[g];
+    }
+
+    // ---- 1. bounding box of my points, Morton counting sort into smem -----------
+    float bmn[3] = {INFINITY, INFINITY, INFINITY}, bmx[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int j = tid; j < cnt; j += kT) {
+        const float4 v = xyz[lo + j];
+        bmn[0] = fminf(bmn[0], v.x); bmn[1] = fminf(bmn[1], v.y); bmn[2] = fminf(bmn[2], v.z);
+        bmx[0] = fmaxf(bmx[0], v.x); bmx[1] = fmaxf(bmx[1], v.y); bmx[2] = fmaxf(bmx[2], v.z);
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            bmn[k] = fminf(bmn[k], __shfl_xor_sync(kFull, bmn[k], o));
+            bmx[k] = fmaxf(bmx[k], __shfl_xor_sync(kFull, bmx[k], o));
+        }
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) { red[k][warp] = bmn[k]; red[3 + k][warp] = bmx[k]; }
+    }
+    for (int i = tid; i < kBins; i += kT) hist[i] = 0u;
+    __syncthreads();
+    float ox, oy, oz, scx, scy, scz;
+    {
+        float mn[3], mx[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            mn[k] = INFINITY; mx[k] = -INFINITY;
+            for (int w = 0; w < kW; ++w) { mn[k] = fminf(mn[k], red[k][w]); mx[k] = fmaxf(mx[k], red[3 + k][w]); }
+        }
+        const float ex = fmaxf(mx[0] - mn[0], 1e-30f), ey = fmaxf(mx[1] - mn[1], 1e-30f),
+                    ez = fmaxf(mx[2] - mn[2], 1e-30f);
+        ox = mn[0]; oy = mn[1]; oz = mn[2];
+        scx = 16.f / ex; scy = 16.f / ey; scz = 16.f / ez;
+    }
+    for (int j = tid; j < cnt; j += kT) {
+        const float4 v = xyz[lo + j];
+        atomicAdd(&hist[morton12(v.x, v.y, v.z, ox, oy, oz, scx, scy, scz)], 1u);
+    }
+    __syncthreads();
+    {
+        // exclusive scan of the 4096 bins: 8 consecutive bins per thread
+        constexpr int kPer = kBins / kT;
+        uint32_t loc[kPer], s = 0;
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) { loc[i] = hist[tid * kPer + i]; s += loc[i]; }
+        uint32_t x = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) scan_tot[warp] = x;
+        __syncthreads();
+        uint32_t base = 0;
+        for (int w = 0; w < warp; ++w) base += scan_tot[w];
+        base += x - s;
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) { hist[tid * kPer + i] = base; base += loc[i]; }
+    }
+    __syncthreads();
+    for (int j = tid; j < cnt; j += kT) {
+        const float4 v = xyz[lo + j];
+        const uint32_t pos = atomicAdd(&hist[morton12(v.x, v.y, v.z, ox, oy, oz, scx, scy, scz)], 1u);
+        pts[pos] = make_float4(v.x, v.y, v.z, __int_as_float((int)(lo + j)));
+    }
+    for (int j = cnt + tid; j < P * kT; j += kT) pts[j] = make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
+    __syncthreads();
+
+    // ---- 2. per-slot state in registers, warp bounding boxes --------------------
+    const int wbase = warp * 32 * P;
+    double m[P];
+    float thr[P];
+    uint32_t tk = 0, valid = 0;
+    float wb[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+        const float4 v = pts[wbase + q * 32 + lane];
+        const int oi = __float_as_int(v.w);
+        m[q] = 0.0;
+        thr[q] = -1.0f;
+        if (oi >= 0) {
+            valid |= 1u << q;
+            if (a.fresh) {
+                m[q] = kInf;
+                tk |= (oi == seed ? 1u : 0u) << q;
+            } else {
+                m[q] = md[oi];
+                tk |= (taken[oi] ? 1u : 0u) << q;
+            }
+            thr[q] = skip_thr(m[q]);
+            wb[0] = fminf(wb[0], v.x); wb[1] = fminf(wb[1], v.y); wb[2] = fminf(wb[2], v.z);
+            wb[3] = fmaxf(wb[3], v.x); wb[4] = fmaxf(wb[4], v.y); wb[5] = fmaxf(wb[5], v.z);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            wb[k] = fminf(wb[k], __shfl_xor_sync(kFull, wb[k], o));
+            wb[3 + k] = fmaxf(wb[3 + k], __shfl_xor_sync(kFull, wb[3 + k], o));
+        }
+    }
+    const bool wvalid = __any_sync(kFull, valid != 0);
+    bool force = wvalid;           // recompute the warp record at the next iteration
+    float thr_w = wvalid ? __int_as_float(0x7f800000) : -1.0f;
+    uint64_t bk = 0;               // cached thread max: md bits, slot, original index (kNone: none)
+    int bq = 0;
+    uint32_t bo = kNone;
+    if (lane == 0) warp_rec[warp] = none_rec();
+    if (a.fresh && writer && tid == 0) {
+        out[0] = seed;
+        curve[0] = kInf;
+    }
+
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_mbar_init_cluster();
+        mbar_arrive_expect_tx(&bars[0], tx_bytes);
+        mbar_arrive_expect_tx(&bars[1], tx_bytes);
+    }
+    cluster_sync_all();
+
+    if (k_start < k_stop) {
+        const int64_t last = a.fresh ? seed : out[k_start - 1];
+        const float4 lv = xyz[last];
+        float sx32 = lv.x, sy32 = lv.y, sz32 = lv.z;
+
+        for (int64_t it = k_start; it < k_stop; ++it) {
+            const uint32_t t_abs = (uint32_t)(it - k_start);
+            const uint32_t par = t_abs & 1u;
+            const uint32_t phase = (t_abs >> 1) & 1u;
+            const uint32_t t = t_abs - (uint32_t)a.dbg_t0;
+            const bool tdbg = a.dbg && b == 0 && r == 0 && tid == kT - 32 && t_abs >= a.dbg_t0 && t < 256 && g == 0;
+            long long ts0 = 0;
+            if (tdbg) ts0 = clock64();
+
+            // 1. warp skip test: rounded-down |s - box|^2 against the warp threshold
+            const float gx = fmaxf(fmaxf(__fsub_rd(wb[0], sx32), __fsub_rd(sx32, wb[3])), 0.f);
+            const float gy = fmaxf(fmaxf(__fsub_rd(wb[1], sy32), __fsub_rd(sy32, wb[4])), 0.f);
+            const float gz = fmaxf(fmaxf(__fsub_rd(wb[2], sz32), __fsub_rd(sz32, wb[5])), 0.f);
+            const float lb = __fadd_rd(__fadd_rd(__fmul_rd(gx, gx), __fmul_rd(gy, gy)), __fmul_rd(gz, gz));
+            if (force || !(lb > thr_w)) {
+                const double sx = sx32, sy = sy32, sz = sz32;
+                uint32_t chg = 0;
+                uint32_t og[QG];  // original indices of the last group (all slots when QG == P)
+                // groups of QG slots: all loads and float32 screens first, one
+                // vote, then the group's float64 folds as independent,
+                // predicated chains (no per-slot branches)
+#pragma unroll
+                for (int q0 = 0; q0 < P; q0 += QG) {
+                    float4 v[QG];
+#pragma unroll
+                    for (int u = 0; u < QG; ++u) v[u] = pts[wbase + (q0 + u) * 32 + lane];
+                    uint32_t need = 0;
+#pragma unroll
+                    for (int u = 0; u < QG; ++u) {
+                        og[u] = __float_as_uint(v[u].w);
+                        const float dx = v[u].x - sx32, dy = v[u].y - sy32, dz = v[u].z - sz32;
+                        const float d32 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+                        need |= (!(d32 > thr[q0 + u]) ? 1u : 0u) << u;
+                    }
+                    if (__any_sync(kFull, need != 0)) {
+#pragma unroll
+                        for (int u = 0; u < QG; ++u) {
+                            const double d = sqdist(sx, sy, sz, (double)v[u].x, (double)v[u].y, (double)v[u].z);
+                            const bool upd = ((need >> u) & 1u) && d < m[q0 + u];
+                            m[q0 + u] = upd ? d : m[q0 + u];
+                            thr[q0 + u] = upd ? skip_thr_nb(d) : thr[q0 + u];
+                            chg |= (upd ? 1u : 0u) << (q0 + u);
+                        }
+                    }
+                }
+                const bool redo = force || ((chg >> bq) & 1u);  // my cached max slot moved
+                if (__any_sync(kFull, chg != 0 || force)) {
+                    if (redo) {
+                        // thread max over my slots: max md (bit order), lowest original index
+                        uint32_t o[P];
+#pragma unroll
+                        for (int q = 0; q < P; ++q)
+                            o[q] = QG == P ? og[q % QG] : __float_as_uint(pts[wbase + q * 32 + lane].w);
+                        bk = 0; bq = 0; bo = kNone;
+#pragma unroll
+                        for (int q = 0; q < P; ++q) {
+                            const uint64_t kq = dbits(m[q]);
+                            if (((valid >> q) & 1u) && (bo == kNone || kq > bk || (kq == bk && o[q] < bo))) {
+                                bk = kq; bq = q; bo = o[q];
+                            }
+                        }
+                    }
+                    const int wl = argmax_lane(bk, bo);
+                    if (wl < 0) {
+                        thr_w = -1.0f;
+                        if (lane == 0) warp_rec[warp] = none_rec();
+                    } else {
+                        const uint64_t wk = __shfl_sync(kFull, bk, wl);
+                        thr_w = skip_thr(bitsd(wk));
+                        if (lane == wl) {
+                            const int lp = wbase + bq * 32 + lane;
+                            const float4 v = pts[lp];
+                            Rec rr;
+                            rr.klo = (uint32_t)bk; rr.khi = (uint32_t)(bk >> 32);
+                            rr.idx = bo;
+                            rr.own = (((tk >> bq) & 1u) << 31) | ((uint32_t)g << 18) | (r << 14) | (uint32_t)lp;
+                            rr.x = v.x; rr.y = v.y; rr.z = v.z; rr.pad = 0;
+                            warp_rec[warp] = rr;
+                        }
+                    }
+                    force = false;
+                }
+            }
+            if (tdbg) a.dbg[t * 8 + 0] = clock64() - ts0;
+
+            // 2-4. the leader warp alone: block argmax, push the CTA record to the
+            // cluster, wait for the C records, (ranks) exchange through the
+            // mailboxes; the winner is broadcast through shared memory on a
+            // named barrier on which the other warps block in hardware
+            if (warp == kW - 1) {
+                named_bar_sync(1, kT);
+                if (tdbg) a.dbg[t * 8 + 1] = clock64() - ts0;
+                const Rec wr = lane < kW ? warp_rec[lane] : none_rec();
+                const int cl = argmax_lane(rec_key(wr), wr.idx);
+                if (tdbg) a.dbg[t * 8 + 6] = clock64() - ts0;
+                const Rec cr = warp_rec[cl < 0 ? 0 : cl];
+                if (tdbg) a.dbg[t * 8 + 7] = (long long)cr.idx * 0 + clock64() - ts0;
+                if (lane < (int)C) {
+                    const uint32_t dst = mapa(smem_u32(&slots[par][r]), lane);
+                    const uint32_t dbar = mapa(smem_u32(&bars[par]), lane);
+                    st_async_v4(dst, dbar, cr.klo, cr.khi, cl < 0 ? kNone : cr.idx, cr.own);
+                    st_async_v4(dst + 16, dbar, __float_as_uint(cr.x), __float_as_uint(cr.y), __float_as_uint(cr.z),
+                                0u);
+                }
+                if (tdbg) a.dbg[t * 8 + 2] = clock64() - ts0;
+                mbar_wait_cluster(&bars[par], phase);
+                if (tdbg) a.dbg[t * 8 + 3] = clock64() - ts0;
+                const Rec sr = lane < (int)C ? slots[par][lane] : none_rec();
+                const int gl = argmax_lane(rec_key(sr), sr.idx);
+                const Rec cw = gl < 0 ? none_rec() : slots[par][gl];
+                __syncwarp();
+                if (lane == 0) mbar_arrive_expect_tx(&bars[par], tx_bytes);
+                if (G > 1) {
+                    const uint32_t seq = rk.seq_base + (uint32_t)it;
+                    if (r == 0 && lane < G) mbox_put(mb_dst + ((b * 3 + par) * G + g) * 2, cw, seq);
+                    const Rec pr = lane < G ? mbox_get(mb_mine + ((b * 3 + par) * G + lane) * 2, seq) : none_rec();
+                    const int pl = argmax_lane(rec_key(pr), pr.idx);
+                    if (lane == (pl < 0 ? 0 : pl)) {
+                        Rec gw = pl < 0 ? none_rec() : pr;
+                        if (pl >= 0 && gw.idx == cw.idx) gw.own = cw.own;  // my rank's point: keep its owner
+                        gslot = gw;
+                    }
+                } else if (lane == 0) {
+                    gslot = cw;
+                }
+                if (tdbg) a.dbg[t * 8 + 4] = clock64() - ts0;
+                named_bar_arrive(2, kT);
+            } else {
+                named_bar_arrive(1, kT);
+                named_bar_sync(2, kT);
+            }
+            Rec win = gslot;
+
+            double best = bitsd(rec_key(win));
+            const bool win_taken = (win.own >> 31) & 1u;
+            if (win.idx == kNone || best <= 0.0 || win_taken) {
+                // duplicate fallback (_kernels.py:65-70): lowest untaken original index
+                uint32_t fidx = kNone;
+                int fq = -1;
+#pragma unroll
+                for (int q = 0; q < P; ++q) {
+                    if (((valid >> q) & 1u) && !((tk >> q) & 1u)) {
+                        const uint32_t o = __float_as_uint(pts[wbase + q * 32 + lane].w);
+                        if (o < fidx) { fidx = o; fq = q; }
+                    }
+                }
+                const uint32_t wm = __reduce_min_sync(kFull, fidx);
+                if (fidx == wm && fidx != kNone) {
+                    const int lp = wbase + fq * 32 + lane;
+                    const float4 v = pts[lp];
+                    double mv = 0.0;
+#pragma unroll
+                    for (int q = 0; q < P; ++q)
+                        if (q == fq) mv = m[q];
+                    const uint64_t k = dbits(mv);
+                    Rec fr;
+                    fr.klo = (uint32_t)k; fr.khi = (uint32_t)(k >> 32); fr.idx = fidx;
+                    fr.own = ((uint32_t)g << 18) | (r << 14) | (uint32_t)lp;
+                    fr.x = v.x; fr.y = v.y; fr.z = v.z; fr.pad = 0;
+                    fb_rec[warp] = fr;
+                } else if (lane == 0 && wm == kNone) {
+                    fb_rec[warp] = none_rec();
+                }
+                __syncthreads();
+                if (warp == 0) {
+                    const uint32_t ci = lane < kW ? fb_rec[lane].idx : kNone;
+                    const uint32_t cm = __reduce_min_sync(kFull, ci);
+                    const unsigned wv = __ballot_sync(kFull, ci == cm && ci != kNone);
+                    const Rec cr = wv ? fb_rec[__ffs(wv) - 1] : none_rec();
+                    if (lane < (int)C) {
+                        const uint32_t dst = mapa(smem_u32(&fb_slots[r]), lane);
+                        st_cluster_u64(dst, ((uint64_t)cr.khi << 32) | cr.klo);
+                        st_cluster_u64(dst + 8, ((uint64_t)cr.own << 32) | cr.idx);
+                        st_cluster_u64(dst + 16, ((uint64_t)__float_as_uint(cr.y) << 32) | __float_as_uint(cr.x));
+                        st_cluster_u64(dst + 24, (uint64_t)__float_as_uint(cr.z));
+                    }
+                }
+                cluster_sync_all();
+                Rec fw;
+                {
+                    const uint32_t ci = lane < (int)C ? fb_slots[lane].idx : kNone;
+                    const uint32_t cm = __reduce_min_sync(kFull, ci);
+                    const unsigned wv = __ballot_sync(kFull, ci == cm && ci != kNone);
+                    fw = wv ? fb_slots[__ffs(wv) - 1] : none_rec();
+                }
+                if (G > 1) {
+                    const uint32_t seq = rk.seq_base + (uint32_t)it;
+                    __syncthreads();
+                    if (warp == kW - 1) {
+                        if (r == 0 && lane < G) mbox_put(mb_dst + ((b * 3 + 2) * G + g) * 2, fw, seq);
+                        const Rec pr = lane < G ? mbox_get(mb_mine + ((b * 3 + 2) * G + lane) * 2, seq) : none_rec();
+                        const uint32_t pm = __reduce_min_sync(kFull, pr.idx);
+                        const unsigned wv = __ballot_sync(kFull, pr.idx == pm && pr.idx != kNone);
+                        if (lane == (wv ? __ffs(wv) - 1 : 0)) {
+                            Rec gw = wv ? pr : none_rec();
+                            if (wv && gw.idx == fw.idx) gw.own = fw.own;
+                            gslot = gw;
+                        }
+                    }
+                    __syncthreads();
+                    fw = gslot;
+                }
+                if (fw.idx != kNone) {
+                    win = fw;
+                    best = bitsd(rec_key(fw));
+                }
+                cluster_sync_all();  // fb_slots / fb_rec / gslot free for the next fallback
+            }
+
+            // record (curve holds squared values until the epilogue), mark taken
+            if (writer && tid == 0) {
+                out[it] = (int64_t)win.idx;
+                curve[it] = best;
+            }
+            const uint32_t own = win.own & 0x7fffffffu;
+            if (win.idx != kNone && (own >> 18) == (uint32_t)g && ((own >> 14) & 15u) == r) {
+                const uint32_t lp = own & 0x3fffu;
+                if ((int)(lp / (32 * P)) == warp) {
+                    force = true;  // the record's taken flag changes
+                    if ((int)(lp & 31u) == lane) tk |= 1u << ((lp >> 5) % P);
+                }
+            }
+            sx32 = win.x; sy32 = win.y; sz32 = win.z;
+            if (tdbg) a.dbg[t * 8 + 5] = clock64() - ts0;
+        }
+    }
+
+    // ---- write back md / taken; curve = sqrt(best) (_kernels.py:72) -------------
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+        if ((valid >> q) & 1u) {
+            const int oi = __float_as_int(pts[wbase + q * 32 + lane].w);
+            md[oi] = m[q];
+            taken[oi] = (tk >> q) & 1u;
+        }
+    }
+    if (writer && k_start < k_stop) {
+        __syncthreads();  // thread 0's curve stores are visible block-wide
+        for (int64_t it = k_start + tid; it < k_stop; it += kT) curve[it] = sqrt(curve[it]);
+    }
+    cluster_sync_all();  // no CTA leaves while peers may still target its smem
+}
+
+size_t res_smem_bytes(int P) { return (size_t)P * kT * sizeof(float4) + kBins * sizeof(uint32_t); }
+
+template <int P>
+cudaError_t launch_res_p(const FpsArgs& a, const FpsRanks& rk, int64_t nclusters, int C, cudaStream_t s,
+                         bool query_only, int* max_clusters) {
+    auto kern = fps_res_kernel<P>;
+    const size_t smem = res_smem_bytes(P);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    if (C > 8) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(nclusters * C), 1, 1);
+    cfg.blockDim = dim3(kT, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (query_only) {
+        int n = 0;
+        e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            n = 0;
+        }
+        *max_clusters = n;
+        return cudaSuccess;
+    }
+    return cudaLaunchKernelEx(&cfg, kern, a, rk);
+}
+
+template <typename F>
+cudaError_t with_res(int P, F f) {
+    switch (P) {
+        case 1: return f.template run<1>();
+        case 2: return f.template run<2>();
+        case 4: return f.template run<4>();
+        case 6: return f.template run<6>();
+        case 8: return f.template run<8>();
+        case 12: return f.template run<12>();
+        case 16: return f.template run<16>();
+        default: return f.template run<24>();
+    }
+}
+
+struct ResF {
+    const FpsArgs* a;
+    const FpsRanks* rk;
+    int64_t nclusters;
+    int C;
+    cudaStream_t s;
+    bool query;
+    int* maxc;
+    template <int P>
+    cudaError_t run() const { return launch_res_p<P>(*a, *rk, nclusters, C, s, query, maxc); }
+};
+
+int res_choose_P(int64_t S) {
+    static const int kPs[] = {1, 2, 4, 6, 8, 12, 16, 24};
+    for (int p : kPs)
+        if ((int64_t)p * kT >= S) return p;
+    return 0;
+}
+
+int res_max_clusters(int P, int C) {
+    static int cache[kMaxC + 1][kMaxP + 1];
+    static bool init = false;
+    if (!init) {
+        for (auto& row : cache)
+            for (int& v : row) v = -1;
+        init = true;
+    }
+    if (cache[C][P] >= 0) return cache[C][P];
+    FpsArgs a = {};
+    FpsRanks rk = {};
+    int n = 0;
+    with_res(P, ResF{&a, &rk, 64, C, nullptr, true, &n});
+    cache[C][P] = n;
+    return n;
+}
+
+}  // namespace
+
+// Resident plan for clouds of N points split over G ranks (G clusters per
+// cloud): cluster width C and points per thread P.  Returns false when no
+// width keeps every cluster of the launch co-resident.
+bool fps_res_plan(int64_t N, int64_t nclusters, int G, int* C_out, int* P_out) {
+    const char* env = getenv("PS_FPS_CLUSTER");
+    const char* tgt = getenv("PS_FPS_TARGET");
+    const int64_t Ns = (N + G - 1) / G;
+    const int64_t target = tgt ? atoll(tgt) : 2048;  // points per CTA
+    int want = (int)((Ns + target - 1) / target);
+    want = want < 1 ? 1 : (want > kMaxC ? kMaxC : want);
+    static const int kCs[] = {16, 14, 12, 10, 8, 7, 6, 5, 4, 3, 2, 1};
+    for (int C : kCs) {
+        if (env && C != atoi(env)) continue;
+        if (!env && C > want) continue;
+        const int64_t S = (Ns + C - 1) / C;
+        const int P = res_choose_P(S);
+        if (P == 0) {
+            if (C == kMaxC || env) return false;
+            continue;
+        }
+        if (res_max_clusters(P, C) >= nclusters) {
+            *C_out = C;
+            *P_out = P;
+            return true;
+        }
+        if (env) return false;
+    }
+    return false;
+}
+
+cudaError_t launch_fps_res(FpsArgs a, const FpsRanks& rk, int64_t B, int C, int P, cudaStream_t s) {
+    const int64_t Ns = (a.N + rk.G - 1) / rk.G;
+    a.points_per_cta = (Ns + C - 1) / C;
+    const int64_t nclusters = B * rk.Gl;
+    if (getenv("PS_FPS_TIMING")) {
+        // development aid: per-phase SM cycles of the first 256 iterations
+        // (cloud 0, rank 0, CTA 0, thread 0) printed to stderr; synchronises.
+        static long long* dbg = nullptr;
+        if (!dbg) cudaMalloc(&dbg, sizeof(long long) * 256 * 12);
+        cudaMemsetAsync(dbg, 0, sizeof(long long) * 256 * 12, s);
+        a.dbg = dbg;
+        a.dbg_t0 = getenv("PS_FPS_T0") ? atoll(getenv("PS_FPS_T0")) : 0;
+        cudaError_t e = with_res(P, ResF{&a, &rk, nclusters, C, s, false, nullptr});
+        if (e != cudaSuccess) return e;
+        static long long h[256 * 12];
+        cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        const int iters = (int)((a.k_stop - a.k_start - a.dbg_t0) < 256 ? (a.k_stop - a.k_start - a.dbg_t0) : 256);
+        for (int lo = 8; lo < iters; lo += 64) {
+            double acc[8] = {0};
+            int cnt = 0;
+            for (int t = lo; t < iters && t < lo + 64; ++t, ++cnt)
+                for (int k = 0; k < 8; ++k) acc[k] += (double)h[t * 8 + k];
+            if (cnt)
+                fprintf(stderr, "[fps-res timing] C=%d P=%d G=%d N=%lld iters %d-%d (leader) cycles: fold %.0f "
+                        "bar %.0f (argmax %.0f, rec %.0f) send %.0f wait %.0f bcast %.0f total %.0f\n", C, P, rk.G,
+                        (long long)a.N, lo, lo + cnt, acc[0] / cnt, acc[1] / cnt, acc[6] / cnt, acc[7] / cnt,
+                        acc[2] / cnt, acc[3] / cnt, acc[4] / cnt, acc[5] / cnt);
+        }
+        return cudaSuccess;
+    }
+    a.dbg = nullptr;
+    return with_res(P, ResF{&a, &rk, nclusters, C, s, false, nullptr});
+}
+
+cudaError_t launch_fps(FpsArgs a, int64_t B, cudaStream_t s) {
+    // The legacy register kernel (fps.cu) has the shorter per-iteration
+    // chain while a cluster holds the cloud in registers (<= 16 points per
+    // thread); beyond that it streams md/xyz through L2 and the resident
+    // kernel's warp skipping wins (measured: profiles/r01/fps_resident.log).
+    // PS_FPS_RESIDENT=1 / PS_FPS_LEGACY=1 force either kernel.
+    int C = 0, P = 0;
+    const bool force_res = getenv("PS_FPS_RESIDENT") != nullptr;
+    const bool force_leg = getenv("PS_FPS_LEGACY") != nullptr;
+    bool use_res = force_res;
+    if (!force_res && !force_leg) {
+        int lc = 0, lp = 0, lt = 0;
+        fps_choose_cluster(a.N, B, &lc, &lp, &lt);
+        use_res = lp == 0;
+    }
+    if (use_res && fps_res_plan(a.N, B, 1, &C, &P)) {
+        if (getenv("PS_FPS_VERBOSE"))
+            fprintf(stderr, "[fps-res] N=%lld B=%lld C=%d P=%d\n", (long long)a.N, (long long)B, C, P);
+        FpsRanks rk = {};
+        rk.G = 1; rk.Gl = 1; rk.g_base = 0;
+        return launch_fps_res(a, rk, B, C, P, s);
+    }
+    return launch_fps_legacy(a, B, s);
+}
+
+}  // namespace ps

@@ -19,9 +19,25 @@ struct FpsArgs {
     int fresh;                  // 1: md=+inf, taken={seed}, out[0]=seed, curve[0]=+inf
     int64_t points_per_cta;     // set by the launcher
     long long* dbg;             // development timing buffer (PS_FPS_TIMING)
+    int64_t dbg_t0;             // first recorded iteration offset (PS_FPS_T0)
 };
 
-cudaError_t launch_fps(FpsArgs a, int64_t B, cudaStream_t s);
+// Clouds split over G ranks (point-split FPS): rank g owns original indices
+// [g*ceil(N/G), (g+1)*ceil(N/G)).  A launch runs Gl ranks per cloud starting
+// at g_base (Gl == G: virtual ranks on one GPU; Gl == 1: one rank per GPU).
+// mbox: device array of G pointers to each rank's mailbox
+// (uint4[B][3][G][2], initialised to 0xff); seq_base makes every
+// (launch, iteration) tag unique.
+struct FpsRanks {
+    int G, Gl, g_base, all_write;
+    uint32_t seq_base;
+    uint4* const* mbox;
+};
+
+cudaError_t launch_fps(FpsArgs a, int64_t B, cudaStream_t s);          // resident kernel, else legacy
+cudaError_t launch_fps_legacy(FpsArgs a, int64_t B, cudaStream_t s);   // register / streaming kernel
+bool fps_res_plan(int64_t N, int64_t nclusters, int G, int* C_out, int* P_out);
+cudaError_t launch_fps_res(FpsArgs a, const FpsRanks& rk, int64_t B, int C, int P, cudaStream_t s);
 int fps_choose_cluster(int64_t N, int64_t B, int* C_out, int* P_out, int* T_out);
 
 // Exclusion-list CSR (one cloud = rows [b][0..N); entries at b*cap_entries).

@@ -72,6 +72,27 @@ def test_fps_matches_oracle_across_cluster_shapes(N, n, family):
     np.testing.assert_array_equal(taken, rtk)
 
 
+@pytest.mark.parametrize("C", ["1", "2", "3", "4", "8", "16", "legacy"])
+def test_fps_resident_cluster_widths(C, monkeypatch):
+    """K1 v2 (resident, spatially sorted, warp-skip) at every cluster width,
+    and the legacy register kernel, on tie-heavy and surface clouds."""
+    if C == "legacy":
+        monkeypatch.setenv("PS_FPS_LEGACY", "1")
+    else:
+        monkeypatch.setenv("PS_FPS_RESIDENT", "1")
+        monkeypatch.setenv("PS_FPS_CLUSTER", C)
+    for family, N, n in (("lattice", 4913, 1200), ("room-surfaces", 12000, 3000), ("gaussian-clusters", 9000, 900)):
+        c = generate_cloud(family, N, 7)
+        if family == "room-surfaces":
+            c = c[np.lexsort((c[:, 2], c[:, 1], c[:, 0]))].copy()  # spatially coherent index order
+        idx, curve, md, taken = gpu_fps(c, n, seed=N // 5)
+        ri, rc, rmd, rtk, _ = O.fps(c, n, N // 5)
+        np.testing.assert_array_equal(idx, ri, err_msg=f"{family} C={C}")
+        np.testing.assert_array_equal(curve, rc)
+        np.testing.assert_array_equal(md, rmd)
+        np.testing.assert_array_equal(taken, rtk)
+
+
 def test_fps_batched_and_duplicates():
     B, N = 5, 900
     base = generate_cloud("uniform-box", 300, 5)

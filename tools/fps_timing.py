@@ -28,7 +28,7 @@ for N, B, n in cases:
     ev[1].record()
     torch.cuda.synchronize()
     os.environ["PS_FPS_TIMING"] = "1"
-    engine.fps(x, min(n, 300))
+    engine.fps(x, min(n, 2000) if os.environ.get("PS_FPS_LATE") else min(n, 300))
     torch.cuda.synchronize()
     print(f"N={N} B={B} n={n} C={os.environ.get('PS_FPS_CLUSTER', 'auto')} T={os.environ.get('PS_FPS_THREADS', '256')}: "
           f"{ev[0].elapsed_time(ev[1]) * 1e3 / (n - 1):.3f} us/iter (full run)", flush=True)
