@@ -9,6 +9,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 
 #include "../../include/ps_b200.h"
 #include "common.cuh"
@@ -290,7 +291,9 @@ int ps_sample_predicted(const int64_t* indptr, const int32_t* nbr, int64_t cap_e
     CHECK_ARG(work != nullptr, "sampler workspace required (ps_sampler_workspace_bytes)");
     a.gws = static_cast<unsigned char*>(work);
     a.B = B;
-    return cuda_status(ps::launch_sampler(a, B, S(stream)), "sample_predicted", 2 + 3 * nseg);
+    const char* sv = getenv("PS_SAMPLER");
+    return cuda_status(ps::launch_sampler(a, B, S(stream)), "sample_predicted",
+                       (sv && atoi(sv) == 3) ? 2 + 3 * nseg : 1);
 }
 
 int ps_earlyterm_scan(const int64_t* indptr, const int32_t* nbr, const double* d2, int64_t cap_entries,

@@ -80,7 +80,10 @@ struct EtScanArgs {
 size_t sampler_ws_bytes(int64_t N, int nseg);              // shared-memory tables per cloud
 size_t sampler_global_ws_bytes(int64_t B, int64_t N, bool big);  // global workspace
 cudaError_t launch_thresholds(const ThreshArgs& a, int64_t B, cudaStream_t s);
-cudaError_t launch_sampler(SampArgs a, int64_t B, cudaStream_t s);
+cudaError_t launch_sampler(SampArgs a, int64_t B, cudaStream_t s);     // v4 unless PS_SAMPLER=3
+cudaError_t launch_sampler_v3(SampArgs a, int64_t B, cudaStream_t s);
+cudaError_t launch_sampler_v4(SampArgs a, int64_t B, cudaStream_t s);
+size_t sampler_v4_ws_bytes(int64_t B, int64_t N);
 cudaError_t launch_et(const EtArgs& a, cudaStream_t s);
 cudaError_t launch_et_scan(const EtScanArgs& a, cudaStream_t s);
 

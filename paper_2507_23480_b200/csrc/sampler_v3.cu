@@ -536,7 +536,7 @@ size_t sampler_ws_bytes(int64_t N, int nseg) {
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-size_t sampler_global_ws_bytes(int64_t B, int64_t N, bool big) {
+size_t sampler_v3_ws_bytes(int64_t B, int64_t N, bool big) {
     const int64_t W = (N + 31) >> 5;
     size_t s = align256(sizeof(SampState) * B);
     s += align256(sizeof(uint32_t) * B * W) * 2;
@@ -546,7 +546,7 @@ size_t sampler_global_ws_bytes(int64_t B, int64_t N, bool big) {
     return s;
 }
 
-cudaError_t launch_sampler(SampArgs a, int64_t B, cudaStream_t s) {
+cudaError_t launch_sampler_v3(SampArgs a, int64_t B, cudaStream_t s) {
     SampWork w = {};
     w.W = (a.N + 31) >> 5;
     unsigned char* p = a.gws;
@@ -590,6 +590,19 @@ cudaError_t launch_sampler(SampArgs a, int64_t B, cudaStream_t s) {
                 h[4], h[5], h[6], h[7], h[8], h[9], h[11]);
     }
     return cudaGetLastError();
+}
+
+size_t sampler_global_ws_bytes(int64_t B, int64_t N, bool big) {
+    const size_t a = sampler_v3_ws_bytes(B, N, big), b = sampler_v4_ws_bytes(B, N);
+    return a > b ? a : b;
+}
+
+// v4 (one persistent cluster kernel per batch, sampler_v4.cu) unless
+// PS_SAMPLER=3 selects this per-segment kernel sequence
+cudaError_t launch_sampler(SampArgs a, int64_t B, cudaStream_t s) {
+    const char* e = getenv("PS_SAMPLER");
+    if (e && atoi(e) == 3) return launch_sampler_v3(a, B, s);
+    return launch_sampler_v4(a, B, s);
 }
 
 }  // namespace ps

@@ -1,0 +1,812 @@
+// sampler_v4.cu -- K3c: the predicted-distance bitmap sampler
+// (_kernels.py:241-353, sample_predicted) as ONE persistent kernel: a
+// thread-block cluster of C CTAs per cloud walks all segment visits, with
+// cluster barriers between the phases of a visit and the cloud's working
+// arrays in global memory (L2-resident, a few MB for a batch).
+//
+// Reformulation (bit-exact with the reference):
+//   * bitmap of segment s at its entry == "no sampled point within the
+//     level-s radius": rebuilt per visit by clearing the level-s row prefix
+//     of every sampled point (prefix + accepted) -- the reference's
+//     _clear_entries of all earlier picks, in one pass of ~N stores;
+//   * the pool is the available points in index order (_kernels.py:293-298);
+//   * the candidate order of the whole visit is the swap-remove sequence of
+//     _kernels.py:322-333 with positions z_t mod (L - t),
+//     z_t = splitmix64(state + (t+1) G); it does not depend on acceptance, so
+//     all L draws are resolved at once: per-position writer lists
+//     (atomicExch), the latest earlier writer of a draw's position and of its
+//     tail slot, then the moved-value chains;
+//   * acceptance in draw order == greedy maximal independent set of the
+//     level-s graph on the pool in that order: parallel rounds (IN when every
+//     earlier neighbour is OUT, OUT when one is IN) until all are decided;
+//   * truncation: the first `boundary - i` accepts in draw order are taken;
+//     draws consumed = position of the last one + 1, or L when the pool runs
+//     dry (RNG state = state0 + draws * G);
+//   * segment / entered / exhausted bookkeeping of _kernels.py:303-351,
+//     evaluated identically by every thread.
+
+#include <cstdio>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "ps_internal.h"
+#include "sampler.h"
+
+namespace ps {
+
+namespace {
+
+constexpr uint64_t kGolden4 = 0x9E3779B97F4A7C15ull;
+constexpr int kT4 = 1024;
+constexpr int kW4 = kT4 / 32;
+constexpr int kAdj4 = 32;
+constexpr uint8_t kAdjOvf = 0xff;
+constexpr int kPred4 = 16;
+constexpr uint8_t kPredOvf = 0xff;
+constexpr uint8_t kUnd4 = 0, kIn4 = 1, kOut4 = 2;
+constexpr int kScr = 64;  // int32 scratch per cloud
+// scratch slots
+constexpr int kCnt0 = 0;    // [16] per-CTA available counts (pool)
+constexpr int kCnt1 = 16;   // [16] per-CTA accepted counts (truncation)
+constexpr int kDecided = 32;
+constexpr int kLast = 33;
+
+struct V4Work {
+    uint8_t* avail;    // [B][N]
+    int32_t* pool;     // [B][N]
+    uint32_t* pos;     // [B][N]
+    int32_t* head;     // [B][N]
+    int32_t* nxt;      // [B][N]
+    int32_t* prv;      // [B][N]
+    int32_t* lw;       // [B][N]
+    int32_t* cand;     // [B][N]
+    int32_t* rank;     // [B][N]
+    int32_t* adj;      // [B][N][kAdj4]
+    uint8_t* adjcnt;   // [B][N]
+    uint8_t* st;       // [B][N]
+    int32_t* preds;    // [B][N][kPred4]
+    uint8_t* npred;    // [B][N]
+    int32_t* scr;      // [B][kScr]
+};
+
+PS_DEV uint64_t mix64_4(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+PS_DEV uint8_t ld_st(const uint8_t* p) {
+    uint16_t v;
+    asm volatile("ld.relaxed.gpu.global.u8 %0, [%1];" : "=h"(v) : "l"(p) : "memory");
+    return (uint8_t)v;
+}
+PS_DEV void st_st(uint8_t* p, uint8_t v) {
+    asm volatile("st.relaxed.gpu.global.u8 [%0], %1;" ::"l"(p), "h"((uint16_t)v) : "memory");
+}
+
+constexpr int kRB = 8;  // row entries loaded per batch (independent loads in flight)
+
+// Load up to kRB row entries [u0, u0 + kRB) of a row with c entries; missing
+// entries are -1.
+PS_DEV void row_batch(const int32_t* row, int32_t u0, int32_t c, int32_t (&q)[kRB]) {
+#pragma unroll
+    for (int k = 0; k < kRB; ++k) q[k] = (u0 + k < c) ? __ldg(row + u0 + k) : -1;
+}
+
+// Lane groups of kG lanes scan one row each: lane gl of the group covers
+// entries [u0 + 4 gl, u0 + 4 gl + 4) (one 16-byte load when the row is
+// 16-byte aligned -- the ELL layout -- else four scalar loads); a warp thus
+// touches 32/kG rows per step instead of 32 scattered lines per load.
+constexpr int kG = 4;
+constexpr int kGStep = 4 * kG;
+PS_DEV int4 grp_load4(const int32_t* row, int32_t u, int32_t c, bool aligned) {
+    int4 v = make_int4(-1, -1, -1, -1);
+    if (u < c) {
+        if (aligned) {
+            v = __ldg(reinterpret_cast<const int4*>(row + u));
+        } else {
+            v.x = __ldg(row + u);
+            if (u + 1 < c) v.y = __ldg(row + u + 1);
+            if (u + 2 < c) v.z = __ldg(row + u + 2);
+            if (u + 3 < c) v.w = __ldg(row + u + 3);
+        }
+        if (u + 1 >= c) v.y = -1;
+        if (u + 2 >= c) v.z = -1;
+        if (u + 3 >= c) v.w = -1;
+    }
+    return v;
+}
+
+// exclusive block scan (kT4 threads); *total = block sum
+PS_DEV int bscan(int v, int* wt, int* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wt[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        int s = wt[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, s, o);
+            if (lane >= o) s += y;
+        }
+        wt[lane] = s;
+    }
+    __syncthreads();
+    const int ex = (warp ? wt[warp - 1] : 0) + x - v;
+    *total = wt[31];
+    __syncthreads();
+    return ex;
+}
+
+PS_DEV int bsum(int v, int* wt) {
+    int tot;
+    bscan(v, wt, &tot);
+    return tot;
+}
+
+PS_DEV void st_cluster_u8(uint32_t addr, uint8_t v) {
+    asm volatile("st.shared::cluster.u8 [%0], %1;" ::"r"(addr), "h"((uint16_t)v) : "memory");
+}
+PS_DEV uint4 ld_cluster_v4(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(addr)
+                 : "memory");
+    return v;
+}
+
+// kSm: the availability byte map and the rank table live in every CTA's
+// shared memory (N bytes + 4N bytes); the map is built by owner CTAs
+// (contiguous 16-byte-aligned index ranges, cleared through DSMEM stores)
+// and gathered by every CTA.  Otherwise both are global arrays.
+template <bool kSm>
+__global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
+    __shared__ int wt[kW4];
+    extern __shared__ __align__(16) uint8_t dsm4[];
+    const int tid = threadIdx.x;
+    const int C = (int)cluster_nctarank();
+    const int r = (int)cluster_ctarank();
+    const int64_t b = cluster_id_x();
+    const int gt = r * kT4 + tid, GT = C * kT4;
+    const int64_t N = a.N;
+    const int nseg = a.nseg;
+
+    const int64_t Npad = (N + 15) & ~(int64_t)15;
+    uint8_t* avail = kSm ? dsm4 : w.avail + b * N;
+    int32_t* pool = w.pool + b * N;
+    uint32_t* pos = w.pos + b * N;
+    int32_t* head = w.head + b * N;
+    int32_t* nxt = w.nxt + b * N;
+    int32_t* prv = w.prv + b * N;
+    int32_t* lw = w.lw + b * N;
+    int32_t* cand = w.cand + b * N;
+    int32_t* rank = kSm ? reinterpret_cast<int32_t*>(dsm4 + Npad) : w.rank + b * N;
+    uint32_t* tkb = reinterpret_cast<uint32_t*>(dsm4 + Npad + 4 * Npad);  // kSm: taken bitmap
+    const int64_t Wtk = (N + 31) / 32;
+    // kSm: witness row positions of my index range (a taken point at that
+    // position of the row; INT_MAX = none), persistent over the visits
+    int32_t* wpos = reinterpret_cast<int32_t*>(tkb + ((Wtk + 3) & ~(int64_t)3));
+    const int64_t span_sm = ((N + C - 1) / C + 15) & ~(int64_t)15;
+    int32_t* s_cnt = wpos + span_sm;  // kSm: this visit's level counts of my range
+    int32_t* s_list = s_cnt + span_sm;  // kSm: points of my range that need a row scan
+    int64_t* s_ip = reinterpret_cast<int64_t*>(s_list + span_sm);  // kSm: their row offsets
+    int64_t i_tk = 0;  // sampled points already in tkb
+    if (kSm) {
+        for (int64_t x = tid; x < Wtk; x += kT4) tkb[x] = 0u;
+        const int64_t span0 = ((N + C - 1) / C + 15) & ~(int64_t)15;
+        for (int64_t x = tid; x < span0; x += kT4) wpos[x] = 0x7fffffff;
+        __syncthreads();
+    }
+    int32_t* adj = w.adj + b * N * kAdj4;
+    uint8_t* adjcnt = w.adjcnt + b * N;
+    uint8_t* stt = w.st + b * N;
+    int32_t* preds = w.preds + b * N * kPred4;
+    uint8_t* npred = w.npred + b * N;
+    int32_t* scr = w.scr + b * kScr;
+    int64_t* out = a.out_idx + b * a.ld_out;
+    const int64_t* indptr = a.indptr + b * (N + 1);
+    const int32_t* nbr = a.nbr + b * a.cap_entries;
+
+    // ---- bookkeeping, evaluated identically by every thread ------------------------
+    int64_t i = a.k0;
+    uint64_t rng = a.state_io[b];
+    int seg = 0;
+    while (seg < nseg && a.k0 >= a.boundaries[seg]) ++seg;
+    int done = 0, exhausted = 0, entered = 0;
+    if (seg >= nseg) {
+        done = 1;
+        exhausted = 1;
+    } else {
+        entered = 1;
+    }
+    for (int64_t t = a.k0 + gt; t < a.n_total; t += GT) out[t] = -1;
+    const bool tdbg = a.dbg && b == 0 && gt == 0;
+    long long tl = tdbg ? clock64() : 0;
+#define VT4(k)                                             \
+    do {                                                   \
+        if (tdbg) {                                        \
+            const long long n_ = clock64();                \
+            a.dbg[k] += n_ - tl;                           \
+            tl = n_;                                       \
+        }                                                  \
+    } while (0)
+
+    while (!done) {
+        const int lvl = a.seg_level_rows[seg];
+        const int32_t* cnt_lvl = a.counts + (b * a.L + lvl) * N;
+
+        // ---- P1: availability = not within the level radius of a sampled point -------
+        // owner ranges: 16-byte aligned so a 16-byte chunk has one owner
+        const int64_t span = ((N + C - 1) / C + 15) & ~(int64_t)15;
+        const int64_t jlo = min(N, (int64_t)r * span), jhi = min(N, jlo + span);
+        for (int64_t j = gt; j < N; j += GT) {
+            if (!kSm) avail[j] = 1;
+            head[j] = -1;
+        }
+        if (gt == 0) scr[kDecided] = 0;
+        if (kSm) {
+            // taken bitmap (smem, every CTA): add the points sampled since the last visit
+            for (int64_t x = i_tk + tid; x < i; x += kT4) {
+                const int32_t q = (int32_t)out[x];
+                atomicOr(&tkb[q >> 5], 1u << (q & 31));
+            }
+            i_tk = i;
+            __syncthreads();
+            VT4(16);
+            // pull: my range's points are available iff untaken and no taken point
+            // in their level-s row prefix (lane groups, early exit on a hit)
+            const int lane = tid & 31, warp = tid >> 5, grp = lane / kG, gl = lane % kG;
+            const unsigned gmask = ((1u << kG) - 1u) << (grp * kG);
+            auto tkd = [&](int32_t q) { return q >= 0 && ((tkb[q >> 5] >> (q & 31)) & 1u); };
+            // this visit's level counts and row offsets of my range, staged once
+            for (int64_t x = tid; x < jhi - jlo; x += kT4) {
+                s_cnt[x] = cnt_lvl[jlo + x];
+                s_ip[x] = indptr[jlo + x];
+            }
+            __syncthreads();
+            VT4(17);
+            // points that need a row scan: untaken, no witness inside this prefix;
+            // the others are decided from shared memory alone
+            int nscan = 0;
+            for (int64_t base = jlo; base < jhi; base += kT4) {
+                const int64_t j = base + tid;
+                bool need = false;
+                if (j < jhi) {
+                    const bool tk = tkd((int32_t)j);
+                    const bool wit = wpos[j - jlo] < s_cnt[j - jlo];
+                    need = !tk && !wit && s_cnt[j - jlo] > 0;
+                    avail[j] = (!tk && !wit) ? 1 : 0;  // scanned points may still be cleared
+                }
+                int tot;
+                const int ex = bscan(need ? 1 : 0, wt, &tot);
+                if (need) s_list[nscan + ex] = (int32_t)(j - jlo);
+                nscan += tot;
+            }
+            for (int kb = warp * (32 / kG); kb < nscan; kb += kW4 * (32 / kG)) {
+                const int k = kb + grp;
+                const bool valid = k < nscan;
+                const int32_t lj = valid ? s_list[k] : 0;
+                const int32_t c = valid ? s_cnt[lj] : 0;
+                const int32_t* row = nbr + (valid ? s_ip[lj] : 0);
+                const bool al = (reinterpret_cast<uintptr_t>(row) & 15u) == 0;
+                bool av = valid;
+                // rounds of kPull entries per group: all loads of a round in flight together
+                constexpr int kPull = 4 * kGStep;
+                for (int32_t u0 = 0;; u0 += kPull) {
+                    const bool act = av && u0 < c;
+                    if (!__any_sync(kFull, act)) break;
+                    int hu = 0x7fffffff;  // lowest hit position of this lane
+                    if (act) {
+                        int4 v[4];
+#pragma unroll
+                        for (int q4 = 0; q4 < 4; ++q4) v[q4] = grp_load4(row, u0 + q4 * kGStep + 4 * gl, c, al);
+#pragma unroll
+                        for (int q4 = 3; q4 >= 0; --q4) {
+                            const int32_t u = u0 + q4 * kGStep + 4 * gl;
+                            hu = tkd(v[q4].w) ? u + 3 : hu;
+                            hu = tkd(v[q4].z) ? u + 2 : hu;
+                            hu = tkd(v[q4].y) ? u + 1 : hu;
+                            hu = tkd(v[q4].x) ? u : hu;
+                        }
+                    }
+                    // lowest hit position of the group (all lanes take part in the shuffles)
+                    int mu = hu;
+#pragma unroll
+                    for (int o = 1; o < kG; o <<= 1) mu = min(mu, __shfl_xor_sync(kFull, mu, o));
+                    if (mu != 0x7fffffff) {
+                        av = false;
+                        if (gl == 0) wpos[lj] = mu;
+                    }
+                }
+                if (valid && !av && gl == 0) avail[jlo + lj] = 0;
+            }
+        }
+        VT4(18);
+        cluster_sync_all();
+        VT4(13);
+        if (!kSm) {
+            for (int64_t x = gt; x < i; x += GT) {
+                const int32_t q = (int32_t)out[x];
+                const int32_t c = cnt_lvl[q];
+                const int32_t* row = nbr + indptr[q];
+                for (int32_t u0 = 0; u0 < c; u0 += 2 * kRB) {
+                    int32_t qq[kRB], q2[kRB];
+                    row_batch(row, u0, c, qq);
+                    row_batch(row, u0 + kRB, c, q2);
+#pragma unroll
+                    for (int k = 0; k < kRB; ++k)
+                        if (qq[k] >= 0) avail[qq[k]] = 0;
+#pragma unroll
+                    for (int k = 0; k < kRB; ++k)
+                        if (q2[k] >= 0) avail[q2[k]] = 0;
+                }
+                avail[q] = 0;
+            }
+        }
+        cluster_sync_all();
+        if (kSm) {
+            const uint32_t avail_base = smem_u32(avail);
+            // gather the other owners' ranges into my copy of the map
+            for (int64_t c16 = tid; c16 < Npad / 16; c16 += kT4) {
+                const int64_t j = c16 * 16;
+                const uint32_t owner = (uint32_t)(j / span);
+                if ((int)owner == r) continue;
+                const uint4 v = ld_cluster_v4(mapa(avail_base + (uint32_t)j, owner));
+                *reinterpret_cast<uint4*>(avail + j) = v;
+            }
+            __syncthreads();
+        }
+        VT4(0);
+
+        // ---- P2: pool (available points in index order) + compressed adjacency -------
+        // ---- P2: pool (available points in index order) + compressed adjacency -------
+        int mycnt = 0;
+        if (kSm) {
+            for (int64_t j = jlo + tid; j < jhi; j += kT4) mycnt += avail[j];
+        } else {
+            for (int64_t j = jlo + tid; j < jhi; j += kT4) {
+                if (!avail[j]) continue;
+                ++mycnt;
+                const int32_t c = cnt_lvl[j];
+                const int32_t* row = nbr + indptr[j];
+                int32_t* ao = adj + j * kAdj4;
+                int n = 0;
+                for (int32_t u0 = 0; u0 < c; u0 += kRB) {
+                    int32_t qq[kRB];
+                    row_batch(row, u0, c, qq);
+                    uint8_t av[kRB];
+#pragma unroll
+                    for (int k = 0; k < kRB; ++k) av[k] = (qq[k] >= 0 && qq[k] != (int32_t)j) ? avail[qq[k]] : 0;
+#pragma unroll
+                    for (int k = 0; k < kRB; ++k) {
+                        if (av[k]) {
+                            if (n < kAdj4) ao[n] = qq[k];
+                            ++n;
+                        }
+                    }
+                }
+                adjcnt[j] = n > kAdj4 ? kAdjOvf : (uint8_t)n;
+            }
+        }
+        mycnt = bsum(mycnt, wt);
+        if (tid == 0) scr[kCnt0 + r] = mycnt;
+        cluster_sync_all();
+        VT4(1);
+        int off = 0, L = 0;
+        for (int c2 = 0; c2 < C; ++c2) {
+            const int v = scr[kCnt0 + c2];
+            off += c2 < r ? v : 0;
+            L += v;
+        }
+        const int off0 = off;
+        for (int64_t base = jlo; base < jhi; base += kT4) {
+            const int64_t j = base + tid;
+            const int f = (j < jhi && avail[j]) ? 1 : 0;
+            int tot;
+            const int ex = bscan(f, wt, &tot);
+            if (f) pool[off + ex] = (int32_t)j;
+            off += tot;
+        }
+        if (kSm) {
+            // compressed adjacency of my range's available points (lane groups)
+            __syncthreads();
+            const int lane = tid & 31, warp = tid >> 5, grp = lane / kG, gl = lane % kG;
+            const unsigned gmask = ((1u << kG) - 1u) << (grp * kG);
+            const unsigned below = gmask & ((1u << lane) - 1u);
+            for (int kb = warp * (32 / kG); kb < mycnt; kb += kW4 * (32 / kG)) {
+                const int k = kb + grp;
+                const bool valid = k < mycnt;
+                int32_t j = 0, c = 0;
+                const int32_t* row = nbr;
+                if (valid) {
+                    j = pool[off0 + k];
+                    c = s_cnt[j - jlo];
+                    row = nbr + s_ip[j - jlo];
+                }
+                const bool al = (reinterpret_cast<uintptr_t>(row) & 15u) == 0;
+                int32_t* ao = adj + (int64_t)j * kAdj4;
+                int n = 0;
+                for (int32_t u0 = 0;; u0 += kGStep) {
+                    const bool act = valid && u0 < c;
+                    if (!__any_sync(kFull, act)) break;
+                    int4 v = make_int4(-1, -1, -1, -1);
+                    if (act) v = grp_load4(row, u0 + 4 * gl, c, al);
+                    const int32_t qv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int32_t q = qv[e];
+                        const bool h = q >= 0 && q != j && avail[q];
+                        const unsigned m = __ballot_sync(kFull, h) & gmask;
+                        if (h) {
+                            const int ps = n + __popc(m & below);
+                            if (ps < kAdj4) ao[ps] = q;
+                        }
+                        n += __popc(m);
+                    }
+                }
+                if (valid && gl == 0) adjcnt[j] = n > kAdj4 ? kAdjOvf : (uint8_t)n;
+            }
+        }
+        cluster_sync_all();
+        VT4(2);
+        if (tdbg) { a.dbg[10] += 1; a.dbg[11] += L; }
+
+        // ---- P3: candidate order of all L draws ----------------------------------------
+        if (a.pick_lowest) {
+            for (int t = gt; t < L; t += GT) {
+                const int32_t c = pool[t];
+                cand[t] = c;
+                if (!kSm) rank[c] = t;
+                stt[t] = kUnd4;
+            }
+        } else {
+            for (int t = gt; t < L; t += GT) {
+                const uint64_t z = mix64_4(rng + (uint64_t)(t + 1) * kGolden4);
+                const uint32_t p = (uint32_t)(z % (uint64_t)(L - t));
+                pos[t] = p;
+                nxt[t] = atomicExch(&head[p], t);
+            }
+            cluster_sync_all();
+            VT4(3);
+            for (int t = gt; t < L; t += GT) {
+                // latest earlier writer of my position, and of my tail slot L-1-t
+                int best = -1;
+                for (int x = head[pos[t]]; x >= 0; x = nxt[x])
+                    if (x < t && x > best) best = x;
+                prv[t] = best;
+                int bl = -1;
+                for (int x = head[L - 1 - t]; x >= 0; x = nxt[x])
+                    if (x < t && x > bl) bl = x;
+                lw[t] = bl;
+            }
+            cluster_sync_all();
+            VT4(4);
+            for (int t = gt; t < L; t += GT) {
+                // value at pos[t] before draw t: untouched -> pool; else the value
+                // moved in by its latest writer x, i.e. the value of slot L-1-x at
+                // draw x, found by following the tail-slot writers back
+                const int x = prv[t];
+                int32_t c;
+                if (x < 0) {
+                    c = pool[pos[t]];
+                } else {
+                    int y = x;
+                    for (int z = lw[y]; z >= 0; z = lw[y]) y = z;
+                    c = pool[L - 1 - y];
+                }
+                cand[t] = c;
+                if (!kSm) rank[c] = t;
+                stt[t] = kUnd4;
+            }
+        }
+        cluster_sync_all();
+        if (kSm) {
+            for (int t = tid; t < L; t += kT4) rank[cand[t]] = t;
+            __syncthreads();
+        }
+
+        VT4(5);
+        // ---- P4: greedy MIS in draw order, parallel rounds ------------------------------
+        int decided = 0;
+        for (int t = gt; t < L; t += GT) {
+            const int32_t c = cand[t];
+            const uint8_t nc = adjcnt[c];
+            bool outf = false, blocked = false;
+            int np = 0;
+            if (nc != kAdjOvf) {
+                // per 16 neighbours: three batches of independent loads (neighbours,
+                // their ranks, their states)
+                const int4* ap = reinterpret_cast<const int4*>(adj + (int64_t)c * kAdj4);
+                for (int h = 0; h < nc; h += 16) {
+                    int32_t q[16];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int4 v = h + 4 * k < nc ? ap[h / 4 + k] : make_int4(0, 0, 0, 0);
+                        q[4 * k] = v.x; q[4 * k + 1] = v.y; q[4 * k + 2] = v.z; q[4 * k + 3] = v.w;
+                    }
+                    int rq[16];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) rq[u] = h + u < nc ? rank[q[u]] : 0x7fffffff;
+                    uint8_t sq[16];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) sq[u] = rq[u] < t ? ld_st(stt + rq[u]) : kOut4;
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) {
+                        if (sq[u] == kIn4) outf = true;
+                        if (rq[u] < t && sq[u] == kUnd4) {
+                            if (np < kPred4) preds[(int64_t)t * kPred4 + np] = rq[u];
+                            ++np;
+                            blocked = true;
+                        }
+                    }
+                }
+            } else {
+                if (a.dbg && b == 0) atomicAdd((unsigned long long*)&a.dbg[14], 1ull);
+                const int32_t m = cnt_lvl[c];
+                const int32_t* row = nbr + indptr[c];
+                for (int32_t u0 = 0; u0 < m && !outf; u0 += kRB) {
+                    int32_t qq[kRB];
+                    row_batch(row, u0, m, qq);
+                    uint8_t av[kRB];
+#pragma unroll
+                    for (int k = 0; k < kRB; ++k) av[k] = (qq[k] >= 0 && qq[k] != c) ? avail[qq[k]] : 0;
+                    int rq[kRB];
+#pragma unroll
+                    for (int k = 0; k < kRB; ++k) rq[k] = av[k] ? rank[qq[k]] : 0x7fffffff;
+                    uint8_t sq[kRB];
+#pragma unroll
+                    for (int k = 0; k < kRB; ++k) sq[k] = rq[k] < t ? ld_st(stt + rq[k]) : kOut4;
+#pragma unroll
+                    for (int k = 0; k < kRB; ++k) {
+                        if (sq[k] == kIn4) outf = true;
+                        if (rq[k] < t && sq[k] == kUnd4) {
+                            if (np < kPred4) preds[(int64_t)t * kPred4 + np] = rq[k];
+                            ++np;
+                            blocked = true;
+                        }
+                    }
+                }
+            }
+            if (outf) {
+                st_st(stt + t, kOut4);
+                ++decided;
+            } else if (!blocked) {
+                st_st(stt + t, kIn4);
+                ++decided;
+            } else {
+                npred[t] = np > kPred4 ? kPredOvf : (uint8_t)np;
+            }
+        }
+        decided = bsum(decided, wt);
+        if (tid == 0 && decided) atomicAdd(&scr[kDecided], decided);
+        cluster_sync_all();
+        VT4(6);
+        while (scr[kDecided] < L) {
+            if (tdbg) a.dbg[12] += 1;
+            int dd = 0;
+            for (int t = gt; t < L; t += GT) {
+                if (ld_st(stt + t) != kUnd4) continue;
+                bool outf = false, blocked = false;
+                const uint8_t np = npred[t];
+                if (np != kPredOvf) {
+                    int pr[kPred4];
+#pragma unroll
+                    for (int k = 0; k < kPred4; ++k) pr[k] = k < np ? preds[(int64_t)t * kPred4 + k] : -1;
+                    uint8_t sq[kPred4];
+#pragma unroll
+                    for (int k = 0; k < kPred4; ++k) sq[k] = pr[k] >= 0 ? ld_st(stt + pr[k]) : kOut4;
+#pragma unroll
+                    for (int k = 0; k < kPred4; ++k) {
+                        outf = outf || sq[k] == kIn4;
+                        blocked = blocked || sq[k] == kUnd4;
+                    }
+                } else {
+                    if (a.dbg && b == 0) atomicAdd((unsigned long long*)&a.dbg[15], 1ull);
+                    // more than kPred4 undecided predecessors: rescan the neighbours
+                    const int32_t c = cand[t];
+                    const uint8_t nc = adjcnt[c];
+                    const int32_t m = nc != kAdjOvf ? (int32_t)nc : cnt_lvl[c];
+                    const int32_t* row = nc != kAdjOvf ? adj + (int64_t)c * kAdj4 : nbr + indptr[c];
+                    for (int32_t u0 = 0; u0 < m && !outf; u0 += kRB) {
+                        int32_t qq[kRB];
+#pragma unroll
+                        for (int k = 0; k < kRB; ++k) qq[k] = (u0 + k < m) ? row[u0 + k] : -1;
+                        uint8_t av[kRB];
+#pragma unroll
+                        for (int k = 0; k < kRB; ++k)
+                            av[k] = (qq[k] >= 0 && qq[k] != c) ? (nc != kAdjOvf ? 1 : avail[qq[k]]) : 0;
+                        int rq[kRB];
+#pragma unroll
+                        for (int k = 0; k < kRB; ++k) rq[k] = av[k] ? rank[qq[k]] : 0x7fffffff;
+                        uint8_t sq[kRB];
+#pragma unroll
+                        for (int k = 0; k < kRB; ++k) sq[k] = rq[k] < t ? ld_st(stt + rq[k]) : kOut4;
+#pragma unroll
+                        for (int k = 0; k < kRB; ++k) {
+                            outf = outf || sq[k] == kIn4;
+                            blocked = blocked || sq[k] == kUnd4;
+                        }
+                    }
+                }
+                if (outf) {
+                    st_st(stt + t, kOut4);
+                    ++dd;
+                } else if (!blocked) {
+                    st_st(stt + t, kIn4);
+                    ++dd;
+                }
+            }
+            dd = bsum(dd, wt);
+            if (tid == 0 && dd) atomicAdd(&scr[kDecided], dd);
+            cluster_sync_all();
+        }
+
+        VT4(7);
+        // ---- P5: truncation at the segment boundary --------------------------------------
+        const int64_t need = a.boundaries[seg] - i;
+        const int tspan = (L + C - 1) / C;
+        const int tlo = min(L, r * tspan), thi = min(L, tlo + tspan);
+        int nin = 0;
+        for (int t = tlo + tid; t < thi; t += kT4) nin += stt[t] == kIn4 ? 1 : 0;
+        nin = bsum(nin, wt);
+        if (tid == 0) scr[kCnt1 + r] = nin;
+        cluster_sync_all();
+        int aoff = 0, A = 0;
+        for (int c2 = 0; c2 < C; ++c2) {
+            const int v = scr[kCnt1 + c2];
+            aoff += c2 < r ? v : 0;
+            A += v;
+        }
+        const int64_t take = (int64_t)A < need ? (int64_t)A : need;
+        const bool ends = take == need;
+        for (int base = tlo; base < thi; base += kT4) {
+            const int t = base + tid;
+            const int f = (t < thi && stt[t] == kIn4) ? 1 : 0;
+            int tot;
+            const int ex = bscan(f, wt, &tot);
+            const int64_t k = aoff + ex;
+            if (f && k < take) {
+                out[i + k] = cand[t];
+                if (ends && k == take - 1) scr[kLast] = t;
+            }
+            aoff += tot;
+        }
+        cluster_sync_all();
+        VT4(8);
+        const int last = ends ? scr[kLast] : -1;
+        i += take;
+        if (ends) {
+            if (!a.pick_lowest) rng = rng + (uint64_t)(last + 1) * kGolden4;
+            if (i >= a.n_total) {
+                done = 1;
+            } else {
+                while (i >= a.boundaries[seg]) ++seg;
+                entered += 1;
+            }
+        } else {
+            if (!a.pick_lowest) rng = rng + (uint64_t)L * kGolden4;
+            seg += 1;
+            if (seg >= nseg) {
+                exhausted = 1;
+                done = 1;
+            } else {
+                entered += 1;
+                if (i >= a.boundaries[seg]) {
+                    while (i >= a.boundaries[seg]) ++seg;
+                    entered += 1;
+                }
+            }
+        }
+        // every thread evaluated the same bookkeeping; the next visit's P1 is
+        // ordered after this visit's reads of scr by its cluster barrier
+    }
+#undef VT4
+    if (r == 0 && tid == 0) {
+        a.reached[b] = i;
+        a.exhausted[b] = exhausted;
+        a.entered[b] = entered;
+        a.state_io[b] = rng;
+    }
+}
+
+size_t align256_4(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace
+
+size_t sampler_v4_ws_bytes(int64_t B, int64_t N) {
+    size_t s = 0;
+    s += align256_4(sizeof(uint8_t) * B * N);            // avail
+    s += align256_4(sizeof(int32_t) * B * N) * 8;        // pool pos head nxt prv lw cand rank
+    s += align256_4(sizeof(int32_t) * B * N * kAdj4);    // adj
+    s += align256_4(sizeof(uint8_t) * B * N) * 3;        // adjcnt st npred
+    s += align256_4(sizeof(int32_t) * B * N * kPred4);   // preds
+    s += align256_4(sizeof(int32_t) * B * kScr);         // scr
+    return s;
+}
+
+static int v4_cluster() {
+    const char* e = getenv("PS_SAMPLER_CLUSTER");
+    int c = e ? atoi(e) : 8;
+    return c < 1 ? 1 : (c > 16 ? 16 : c);
+}
+
+cudaError_t launch_sampler_v4(SampArgs a, int64_t B, cudaStream_t s) {
+    V4Work w = {};
+    const int64_t N = a.N;
+    unsigned char* p = a.gws;
+    w.avail = p; p += align256_4(sizeof(uint8_t) * B * N);
+    w.pool = reinterpret_cast<int32_t*>(p); p += align256_4(sizeof(int32_t) * B * N);
+    w.pos = reinterpret_cast<uint32_t*>(p); p += align256_4(sizeof(int32_t) * B * N);
+    w.head = reinterpret_cast<int32_t*>(p); p += align256_4(sizeof(int32_t) * B * N);
+    w.nxt = reinterpret_cast<int32_t*>(p); p += align256_4(sizeof(int32_t) * B * N);
+    w.prv = reinterpret_cast<int32_t*>(p); p += align256_4(sizeof(int32_t) * B * N);
+    w.lw = reinterpret_cast<int32_t*>(p); p += align256_4(sizeof(int32_t) * B * N);
+    w.cand = reinterpret_cast<int32_t*>(p); p += align256_4(sizeof(int32_t) * B * N);
+    w.rank = reinterpret_cast<int32_t*>(p); p += align256_4(sizeof(int32_t) * B * N);
+    w.adj = reinterpret_cast<int32_t*>(p); p += align256_4(sizeof(int32_t) * B * N * kAdj4);
+    w.adjcnt = p; p += align256_4(sizeof(uint8_t) * B * N);
+    w.st = p; p += align256_4(sizeof(uint8_t) * B * N);
+    w.npred = p; p += align256_4(sizeof(uint8_t) * B * N);
+    w.preds = reinterpret_cast<int32_t*>(p); p += align256_4(sizeof(int32_t) * B * N * kPred4);
+    w.scr = reinterpret_cast<int32_t*>(p);
+    a.B = B;
+    const int C = v4_cluster();
+    cudaError_t e = cudaSuccess;
+    const int64_t Npad = (N + 15) & ~(int64_t)15;
+    const int64_t span0 = ((N + C - 1) / C + 15) & ~(int64_t)15;
+    const size_t dsm = (size_t)(Npad + 4 * Npad + 4 * (((N + 31) / 32 + 3) & ~(int64_t)3) + 20 * span0);
+    const bool sm = dsm <= 200 * 1024 && !getenv("PS_SAMPLER_GLOBAL");
+    auto kern = sm ? samp4_kernel<true> : samp4_kernel<false>;
+    if (sm) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+        if (e != cudaSuccess) return e;
+    }
+    if (C > 8) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(B * C), 1, 1);
+    cfg.blockDim = dim3(kT4, 1, 1);
+    cfg.dynamicSmemBytes = sm ? dsm : 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    a.dbg = nullptr;
+    if (getenv("PS_SAMPLER_TIMING")) {  // development aid (synchronises)
+        static long long* dbg = nullptr;
+        if (!dbg) cudaMalloc(&dbg, sizeof(long long) * 32);
+        cudaMemsetAsync(dbg, 0, sizeof(long long) * 32, s);
+        a.dbg = dbg;
+        e = cudaLaunchKernelEx(&cfg, kern, a, w);
+        {
+            long long h2[32];
+            cudaMemcpyAsync(h2, dbg, sizeof(h2), cudaMemcpyDeviceToHost, s);
+            cudaStreamSynchronize(s);
+            fprintf(stderr, "[sampler v4] P1: head init + taken bits %lld, stage counts %lld, pull %lld, barrier %lld; "
+                    "adjacency overflows %lld, pred overflows %lld\n", h2[16], h2[17], h2[18], h2[13], h2[14], h2[15]);
+        }
+        long long h[16];
+        cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        fprintf(stderr, "[sampler v4 C=%d] cycles: avail %lld pool+adj %lld compact %lld positions %lld walks %lld "
+                "resolve %lld mis0 %lld rounds %lld trunc %lld | visits %lld sum L %lld rounds %lld\n", C, h[0], h[1],
+                h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[10], h[11], h[12]);
+        return e;
+    }
+    return cudaLaunchKernelEx(&cfg, kern, a, w);
+}
+
+}  // namespace ps
