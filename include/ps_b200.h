@@ -75,6 +75,33 @@ PS_API int ps_fps(const float* xyz4, int64_t B, int64_t N, double* md, uint8_t* 
            int64_t* out_idx, double* curve, int64_t ld_out, int64_t k_stop, int64_t seed,
            const int64_t* seed_dev, void* stream);
 
+/* ---- K1 point-split: one cloud split over G ranks --
+ * Rank g owns the original indices [g*ceil(N/G), (g+1)*ceil(N/G)) of each of
+ * the B clouds; every iteration each rank reduces its shard in one
+ * thread-block cluster, publishes the shard record (md, index, taken, xyz)
+ * into every rank's mailbox (peer memory over NVLink, 32 bytes, sequence
+ * tagged) and reduces the G records with the rule of the chunked merge in
+ * fps_update_chunk / first_untaken (_kernels.py:77-100; max md, lowest
+ * index; duplicate fallback = lowest untaken index) -- bit-identical to
+ * fps_loop for any G.  A launch runs Gl ranks starting at g_base: Gl == G
+ * puts all ranks on this GPU ("virtual ranks"), Gl == 1 is one rank per GPU.
+ * mbox_dev: device array of G device pointers, mailbox g of
+ * ps_fps_mailbox_bytes(B, G) bytes, filled with 0xff before first use;
+ * seq_base + k_stop must stay below 2^32 - 1 and grow by >= k_stop + 1
+ * between launches sharing the mailboxes.  all_write: every rank writes
+ * out_idx / curve (one process per GPU), else rank 0 only.  Fresh FPS as
+ * ps_fps; md / taken are written for each rank's own shard. */
+PS_API int64_t ps_fps_mailbox_bytes(int64_t B, int32_t G);
+PS_API int ps_fps_split_plan(int64_t N, int64_t B, int32_t G, int32_t Gl, int32_t* C_out, int32_t* P_out);
+PS_API int ps_fps_split(const float* xyz4, int64_t B, int64_t N, double* md, uint8_t* taken, int64_t* out_idx,
+                        double* curve, int64_t ld_out, int64_t k_stop, int64_t seed, int32_t G, int32_t g_base,
+                        int32_t Gl, void* const* mbox_dev, uint32_t seq_base, int32_t all_write, void* stream);
+/* CUDA IPC for the mailboxes of one-process-per-GPU ranks: 64-byte handle of
+ * a device allocation, opened in a peer process (peer access enabled). */
+PS_API int ps_ipc_handle(const void* dev_ptr, void* handle_out);
+PS_API int ps_ipc_open(const void* handle, void** dev_ptr_out);
+PS_API int ps_ipc_close(void* dev_ptr);
+
 /* fps_update_chunk (_kernels.py:77-92) for one cloud: folds (px,py,pz) into
  * md[lo:hi] and writes the slice argmax (best float64, index int64; lowest
  * index on ties) to best_out[0], arg_out[0]. */

@@ -125,6 +125,73 @@ int ps_fps(const float* xyz4, int64_t B, int64_t N, double* md, uint8_t* taken, 
     return cuda_status(ps::launch_fps(a, B, S(stream)), "fps", 1);
 }
 
+// ---- K1 point-split: one cloud split over G ranks ----------------------------------
+
+int64_t ps_fps_mailbox_bytes(int64_t B, int32_t G) {
+    if (B < 1 || G < 1) return 0;
+    return B * 3 * (int64_t)G * 2 * (int64_t)sizeof(uint4);
+}
+
+int ps_fps_split_plan(int64_t N, int64_t B, int32_t G, int32_t Gl, int32_t* C_out, int32_t* P_out) {
+    CHECK_ARG(B >= 1 && N >= 1 && N <= kMaxN && G >= 1 && Gl >= 1 && Gl <= G, "invalid split shape");
+    int C = 0, P = 0;
+    if (!ps::fps_res_plan(N, B * Gl, G, &C, &P))
+        return fail(PS_ERR_UNSUPPORTED, "no co-resident cluster plan for N=%lld over %d ranks (%d per launch)",
+                    (long long)N, G, Gl);
+    if (C_out) *C_out = C;
+    if (P_out) *P_out = P;
+    return PS_OK;
+}
+
+int ps_fps_split(const float* xyz4, int64_t B, int64_t N, double* md, uint8_t* taken, int64_t* out_idx, double* curve,
+                 int64_t ld_out, int64_t k_stop, int64_t seed, int32_t G, int32_t g_base, int32_t Gl,
+                 void* const* mbox_dev, uint32_t seq_base, int32_t all_write, void* stream) {
+    CHECK_ARG(B >= 1 && N >= 1 && N <= kMaxN, "invalid batch shape B=%lld N=%lld", (long long)B, (long long)N);
+    CHECK_ARG(k_stop >= 1 && k_stop <= ld_out && k_stop <= N, "k_stop %lld out of range", (long long)k_stop);
+    CHECK_ARG(seed >= 0 && seed < N, "seed index %lld out of range", (long long)seed);
+    CHECK_ARG(G >= 1 && G <= 64 && Gl >= 1 && g_base >= 0 && g_base + Gl <= G, "invalid ranks G=%d g_base=%d Gl=%d",
+              G, g_base, Gl);
+    CHECK_ARG(G == 1 || mbox_dev != nullptr, "mailbox pointer array required for G > 1");
+    CHECK_ARG((uint64_t)seq_base + (uint64_t)k_stop < 0xffffffffull, "sequence space exhausted; reset the mailboxes");
+    CHECK_ARG(xyz4 && md && taken && out_idx && curve, "null pointer");
+    int C = 0, P = 0;
+    if (!ps::fps_res_plan(N, B * Gl, G, &C, &P))
+        return fail(PS_ERR_UNSUPPORTED, "no co-resident cluster plan for N=%lld over %d ranks (%d per launch)",
+                    (long long)N, G, Gl);
+    ps::FpsArgs a = {};
+    a.xyz = reinterpret_cast<const float4*>(xyz4);
+    a.md = md; a.taken = taken; a.out_idx = out_idx; a.curve = curve;
+    a.N = N; a.ld_out = ld_out; a.k_start = 1; a.k_stop = k_stop; a.seed = seed; a.fresh = 1;
+    ps::FpsRanks rk = {};
+    rk.G = G; rk.Gl = Gl; rk.g_base = g_base; rk.all_write = all_write; rk.seq_base = seq_base;
+    rk.mbox = reinterpret_cast<uint4* const*>(mbox_dev);
+    return cuda_status(ps::launch_fps_res(a, rk, B, C, P, S(stream)), "fps_split", 1);
+}
+
+int ps_ipc_handle(const void* dev_ptr, void* handle_out) {
+    CHECK_ARG(dev_ptr && handle_out, "null pointer");
+    cudaIpcMemHandle_t h;
+    const cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr));
+    if (e != cudaSuccess) return fail(PS_ERR_CUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+    memcpy(handle_out, &h, sizeof(h));
+    return PS_OK;
+}
+
+int ps_ipc_open(const void* handle, void** dev_ptr_out) {
+    CHECK_ARG(handle && dev_ptr_out, "null pointer");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    const cudaError_t e = cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return fail(PS_ERR_CUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+    return PS_OK;
+}
+
+int ps_ipc_close(void* dev_ptr) {
+    const cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+    if (e != cudaSuccess) return fail(PS_ERR_CUDA, "cudaIpcCloseMemHandle: %s", cudaGetErrorString(e));
+    return PS_OK;
+}
+
 int ps_fps_update_chunk(const float* xyz4, int64_t N, double px, double py, double pz, double* md, int64_t lo,
                         int64_t hi, double* best_out, int64_t* arg_out, void* stream) {
     CHECK_ARG(N >= 1 && lo >= 0 && lo <= hi && hi <= N, "invalid slice [%lld, %lld)", (long long)lo, (long long)hi);

@@ -176,10 +176,11 @@ __global__ void __launch_bounds__(T, 1) fps_cluster_kernel(FpsArgs a) {
         bool dirty = true;  // recompute the cached local max
 
         for (int64_t it = k_start; it < k_stop; ++it) {
-            const uint32_t t = (uint32_t)(it - k_start);
-            const uint32_t par = t & 1u;
-            const uint32_t phase = (t >> 1) & 1u;
-            const bool tdbg = a.dbg && b == 0 && r == 0 && tid == 0 && t < 256;
+            const uint32_t t_abs = (uint32_t)(it - k_start);
+            const uint32_t par = t_abs & 1u;
+            const uint32_t phase = (t_abs >> 1) & 1u;
+            const uint32_t t = t_abs - (uint32_t)a.dbg_t0;
+            const bool tdbg = a.dbg && b == 0 && r == 0 && tid == 0 && t_abs >= a.dbg_t0 && t < 256;
             long long ts0 = 0;
             if (tdbg) ts0 = clock64();
             const double sx = sx32, sy = sy32, sz = sz32;
@@ -574,12 +575,13 @@ cudaError_t launch_fps_legacy(FpsArgs a, int64_t B, cudaStream_t s) {
         if (!dbg) cudaMalloc(&dbg, sizeof(long long) * 256 * 8);
         cudaMemsetAsync(dbg, 0, sizeof(long long) * 256 * 8, s);
         a.dbg = dbg;
+        a.dbg_t0 = getenv("PS_FPS_T0") ? atoll(getenv("PS_FPS_T0")) : 0;
         cudaError_t e = with_kernel(P, T, LaunchF{&a, B, C, s});
         if (e != cudaSuccess) return e;
         long long h[256 * 8];
         cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, s);
         cudaStreamSynchronize(s);
-        const int iters = (int)((a.k_stop - a.k_start) < 256 ? (a.k_stop - a.k_start) : 256);
+        const int iters = (int)((a.k_stop - a.k_start - a.dbg_t0) < 256 ? (a.k_stop - a.k_start - a.dbg_t0) : 256);
         double acc[7] = {0};
         int cnt = 0;
         for (int t = 8; t < iters; ++t, ++cnt)

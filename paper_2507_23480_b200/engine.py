@@ -75,6 +75,53 @@ def fps(xyz4: torch.Tensor, n: int, seed_index: int = 0, k_stop: int | None = No
     return out, curve, md, taken
 
 
+class SplitMailboxes:
+    """Mailboxes of G ranks living on this device ("virtual ranks"):
+    the point-split FPS protocol of ps_fps_split exercised on one GPU, each
+    rank a thread-block cluster exchanging its shard record through the same
+    sequence-tagged global-memory slots that peer GPUs use over NVLink."""
+
+    def __init__(self, B: int, G: int, device=None):
+        self.B, self.G = int(B), int(G)
+        nbytes = int(_lib.raw("ps_fps_mailbox_bytes", self.B, self.G))
+        dev = torch.device(device) if device is not None else torch.device("cuda")
+        self.boxes = [torch.full((nbytes,), 0xFF, dtype=torch.uint8, device=dev) for _ in range(self.G)]
+        self.ptrs = torch.tensor([b.data_ptr() for b in self.boxes], dtype=torch.int64, device=dev)
+        self.seq = 0
+
+    def next_seq(self, k_stop: int) -> int:
+        """Sequence base for a launch of k_stop iterations (tags stay unique)."""
+        if self.seq + k_stop + 1 >= 0xFFFFFFFF:
+            for b in self.boxes:
+                b.fill_(0xFF)
+            self.seq = 0
+        base = self.seq
+        self.seq += int(k_stop) + 1
+        return base
+
+
+def fps_split(xyz4: torch.Tensor, n: int, G: int, seed_index: int = 0, k_stop: int | None = None,
+              mailboxes: SplitMailboxes | None = None):
+    """Exact FPS with every cloud split over G virtual ranks on this GPU
+    (config C5's point split).  Bit-identical to ``fps`` for any G.  Returns
+    (idx, curve, md, taken) like ``fps``."""
+    B, N, _ = xyz4.shape
+    if not (1 <= n <= N):
+        raise ValueError(f"n must be in [1, {N}], got {n}")
+    stop = n if k_stop is None else int(k_stop)
+    dev = xyz4.device
+    mb = mailboxes if mailboxes is not None else SplitMailboxes(B, G, dev)
+    if mb.G != G or mb.B != B:
+        raise ValueError("mailboxes were made for another (B, G)")
+    md = torch.empty(B, N, dtype=torch.float64, device=dev)
+    taken = torch.empty(B, N, dtype=torch.uint8, device=dev)
+    out = torch.full((B, n), -1, dtype=torch.int64, device=dev)
+    curve = torch.full((B, n), math.inf, dtype=torch.float64, device=dev)
+    _lib.call("ps_fps_split", _p(xyz4), B, N, _p(md), _p(taken), _p(out), _p(curve), n, stop, int(seed_index),
+              G, 0, G, _p(mb.ptrs), mb.next_seq(stop), 0, _stream())
+    return out, curve, md, taken
+
+
 def fps_loop(xyz4, md, taken, out_idx, curve, k_start, n_total, k_start_dev=None):
     B, N, _ = xyz4.shape
     _lib.call("ps_fps_loop", _p(xyz4), B, N, _p(md), _p(taken), _p(out_idx), _p(curve), out_idx.shape[1],

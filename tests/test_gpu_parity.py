@@ -93,6 +93,44 @@ def test_fps_resident_cluster_widths(C, monkeypatch):
         np.testing.assert_array_equal(taken, rtk)
 
 
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("family,N,n,G,B", [
+    ("room-surfaces", 24000, 3000, 2, 1), ("room-surfaces", 24000, 3000, 4, 2), ("lattice", 4913, 1200, 3, 1),
+    ("uniform-box", 200000, 1500, 4, 1), ("gaussian-clusters", 9000, 900, 8, 1), ("uniform-box", 4096, 1024, 1, 1),
+])
+def test_fps_point_split_virtual_ranks(family, N, n, G, B):
+    """C5 point split: every cloud split over G ranks exchanging
+    shard records through the mailbox protocol (all ranks on this GPU) is
+    bit-identical to the single-rank reference FPS."""
+    clouds = np.stack([generate_cloud(family, N, 31 + b) for b in range(B)])
+    xyz4 = engine.as_xyz4(torch.from_numpy(clouds).cuda())
+    mb = engine.SplitMailboxes(B, G)
+    for rep in range(2):  # the second launch reuses the mailboxes (sequence tags)
+        idx, curve, md, taken = engine.fps_split(xyz4, n, G, seed_index=N // 7, mailboxes=mb)
+        for b in range(B):
+            ri, rc, rmd, rtk, _ = O.fps(clouds[b], n, N // 7)
+            np.testing.assert_array_equal(idx[b].cpu().numpy(), ri, err_msg=f"{family} G={G} rep={rep}")
+            np.testing.assert_array_equal(curve[b].cpu().numpy(), rc)
+            np.testing.assert_array_equal(md[b].cpu().numpy(), rmd)
+            np.testing.assert_array_equal(taken[b].cpu().numpy(), rtk)
+
+
+@pytest.mark.timeout(300)
+def test_fps_point_split_duplicates_fallback():
+    """All-duplicate tails force the lowest-untaken fallback to be exchanged
+    across ranks (_kernels.py:65-70)."""
+    B, N = 2, 900
+    base = generate_cloud("uniform-box", 300, 5)
+    clouds = np.stack([np.repeat(base, 3, axis=0)[np.random.default_rng(b).permutation(N)] for b in range(B)])
+    xyz4 = engine.as_xyz4(torch.from_numpy(clouds).cuda())
+    for G in (2, 3):
+        idx, curve, _, _ = engine.fps_split(xyz4, N, G, seed_index=4)
+        for b in range(B):
+            ri, rc, *_ = O.fps(clouds[b], N, 4)
+            np.testing.assert_array_equal(idx[b].cpu().numpy(), ri)
+            np.testing.assert_array_equal(curve[b].cpu().numpy(), rc)
+
+
 def test_fps_batched_and_duplicates():
     B, N = 5, 900
     base = generate_cloud("uniform-box", 300, 5)
