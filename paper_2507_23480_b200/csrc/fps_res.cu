@@ -174,6 +174,7 @@ __global__ void __launch_bounds__(kT, 1) fps_res_kernel(FpsArgs a, FpsRanks rk) 
     __shared__ __align__(8) uint64_t bars[2];
     __shared__ float red[6][kW];
     __shared__ uint32_t scan_tot[kW];
+    __shared__ uint32_t cbound[kMaxC + 1];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t C = cluster_nctarank();
@@ -189,7 +190,6 @@ __global__ void __launch_bounds__(kT, 1) fps_res_kernel(FpsArgs a, FpsRanks rk) 
     const int64_t S = a.points_per_cta;
     const int64_t lo = min(shard_hi, shard_lo + (int64_t)r * S);
     const int64_t hi = min(shard_hi, lo + S);
-    const int cnt = (int)(hi - lo);
     const float4* __restrict__ xyz = a.xyz + b * N;
     double* __restrict__ md = a.md + b * N;
     uint8_t* __restrict__ taken = a.taken + b * N;
@@ -209,70 +209,117 @@ __global__ void __launch_bounds__(kT, 1) fps_res_kernel(FpsArgs a, FpsRanks rk) 
         mb_mine = rk.mbox[g];
     }
 
-    // ---- 1. bounding box of my points, Morton counting sort into smem -----------
-    float bmn[3] = {INFINITY, INFINITY, INFINITY}, bmx[3] = {-INFINITY, -INFINITY, -INFINITY};
-    for (int j = tid; j < cnt; j += kT) {
-        const float4 v = xyz[lo + j];
-        bmn[0] = fminf(bmn[0], v.x); bmn[1] = fminf(bmn[1], v.y); bmn[2] = fminf(bmn[2], v.z);
-        bmx[0] = fmaxf(bmx[0], v.x); bmx[1] = fmaxf(bmx[1], v.y); bmx[2] = fmaxf(bmx[2], v.z);
-    }
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            bmn[k] = fminf(bmn[k], __shfl_xor_sync(kFull, bmn[k], o));
-            bmx[k] = fmaxf(bmx[k], __shfl_xor_sync(kFull, bmx[k], o));
-        }
-    }
-    if (lane == 0) {
-#pragma unroll
-        for (int k = 0; k < 3; ++k) { red[k][warp] = bmn[k]; red[3 + k][warp] = bmx[k]; }
-    }
-    for (int i = tid; i < kBins; i += kT) hist[i] = 0u;
-    __syncthreads();
-    float ox, oy, oz, scx, scy, scz;
+    // ---- 1. points of this CTA, Morton-ordered in shared memory -----------------------
+    // spatial partition (rk.spatial): every CTA histograms the whole shard over
+    // 4096 Morton cells of the shard's bounding box; cell c goes to CTA
+    // min(C-1, start(c) * C / Ns) (start = exclusive prefix count), so CTA
+    // ranges are contiguous runs of cells -- compact regions -- decided
+    // identically by every CTA.  If a CTA would exceed its P*kT slots, all CTAs
+    // fall back to index ranges [lo, hi) sorted locally.
+    int cnt = 0;
     {
-        float mn[3], mx[3];
+        const int64_t Nsh = shard_hi - shard_lo;
+        for (int attempt = rk.spatial && C > 1 ? 0 : 1; attempt < 2; ++attempt) {
+            const bool sp = attempt == 0;
+            const int64_t src_lo = sp ? shard_lo : lo, src_hi = sp ? shard_hi : hi;
+            float bmn[3] = {INFINITY, INFINITY, INFINITY}, bmx[3] = {-INFINITY, -INFINITY, -INFINITY};
+            for (int64_t j = src_lo + tid; j < src_hi; j += kT) {
+                const float4 v = xyz[j];
+                bmn[0] = fminf(bmn[0], v.x); bmn[1] = fminf(bmn[1], v.y); bmn[2] = fminf(bmn[2], v.z);
+                bmx[0] = fmaxf(bmx[0], v.x); bmx[1] = fmaxf(bmx[1], v.y); bmx[2] = fmaxf(bmx[2], v.z);
+            }
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            mn[k] = INFINITY; mx[k] = -INFINITY;
-            for (int w = 0; w < kW; ++w) { mn[k] = fminf(mn[k], red[k][w]); mx[k] = fmaxf(mx[k], red[3 + k][w]); }
+            for (int k = 0; k < 3; ++k) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    bmn[k] = fminf(bmn[k], __shfl_xor_sync(kFull, bmn[k], o));
+                    bmx[k] = fmaxf(bmx[k], __shfl_xor_sync(kFull, bmx[k], o));
+                }
+            }
+            __syncthreads();  // red / hist reuse across attempts
+            if (lane == 0) {
+#pragma unroll
+                for (int k = 0; k < 3; ++k) { red[k][warp] = bmn[k]; red[3 + k][warp] = bmx[k]; }
+            }
+            for (int i = tid; i < kBins; i += kT) hist[i] = 0u;
+            __syncthreads();
+            float ox, oy, oz, scx, scy, scz;
+            {
+                float mn[3], mx[3];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    mn[k] = INFINITY; mx[k] = -INFINITY;
+                    for (int w = 0; w < kW; ++w) { mn[k] = fminf(mn[k], red[k][w]); mx[k] = fmaxf(mx[k], red[3 + k][w]); }
+                }
+                const float ex = fmaxf(mx[0] - mn[0], 1e-30f), ey = fmaxf(mx[1] - mn[1], 1e-30f),
+                            ez = fmaxf(mx[2] - mn[2], 1e-30f);
+                ox = mn[0]; oy = mn[1]; oz = mn[2];
+                scx = 16.f / ex; scy = 16.f / ey; scz = 16.f / ez;
+            }
+            for (int64_t j = src_lo + tid; j < src_hi; j += kT) {
+                const float4 v = xyz[j];
+                atomicAdd(&hist[morton12(v.x, v.y, v.z, ox, oy, oz, scx, scy, scz)], 1u);
+            }
+            __syncthreads();
+            {
+                // exclusive scan of the 4096 bins: 8 consecutive bins per thread
+                constexpr int kPer = kBins / kT;
+                uint32_t loc[kPer], sum = 0;
+#pragma unroll
+                for (int i = 0; i < kPer; ++i) { loc[i] = hist[tid * kPer + i]; sum += loc[i]; }
+                uint32_t x = sum;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(kFull, x, o);
+                    if (lane >= o) x += y;
+                }
+                if (lane == 31) scan_tot[warp] = x;
+                __syncthreads();
+                uint32_t base = 0;
+                for (int w = 0; w < warp; ++w) base += scan_tot[w];
+                base += x - sum;
+#pragma unroll
+                for (int i = 0; i < kPer; ++i) { hist[tid * kPer + i] = base; base += loc[i]; }
+            }
+            __syncthreads();
+            uint32_t my_c0 = 0, my_c1 = kBins, my_s0 = 0;
+            if (sp) {
+                // first cell of every CTA (owner is non-decreasing in the cell index)
+                if (tid <= (int)C) {
+                    uint32_t l = 0, h2 = kBins;  // first c with owner(c) >= tid
+                    while (l < h2) {
+                        const uint32_t mid = (l + h2) >> 1;
+                        const int64_t ow = min((int64_t)C - 1, (int64_t)hist[mid] * C / max((int64_t)1, Nsh));
+                        if (ow >= tid) h2 = mid; else l = mid + 1;
+                    }
+                    cbound[tid] = tid == 0 ? 0u : (tid == (int)C ? (uint32_t)kBins : l);
+                }
+                __syncthreads();
+                bool fits = true;
+                for (uint32_t q = 0; q < C; ++q) {
+                    const uint32_t s0 = cbound[q] < kBins ? hist[cbound[q]] : (uint32_t)Nsh;
+                    const uint32_t s1 = cbound[q + 1] < kBins ? hist[cbound[q + 1]] : (uint32_t)Nsh;
+                    if (s1 - s0 > (uint32_t)(P * kT)) fits = false;
+                }
+                if (!fits) continue;  // uniform across the cluster: every CTA sees the same histogram
+                my_c0 = cbound[r];
+                my_c1 = cbound[r + 1];
+                my_s0 = my_c0 < kBins ? hist[my_c0] : (uint32_t)Nsh;
+                const uint32_t my_s1 = my_c1 < kBins ? hist[my_c1] : (uint32_t)Nsh;
+                cnt = (int)(my_s1 - my_s0);
+            } else {
+                cnt = (int)(hi - lo);
+            }
+            __syncthreads();
+            for (int64_t j = src_lo + tid; j < src_hi; j += kT) {
+                const float4 v = xyz[j];
+                const uint32_t c = morton12(v.x, v.y, v.z, ox, oy, oz, scx, scy, scz);
+                if (c < my_c0 || c >= my_c1) continue;
+                const uint32_t pos = atomicAdd(&hist[c], 1u) - my_s0;
+                pts[pos] = make_float4(v.x, v.y, v.z, __int_as_float((int)j));
+            }
+            break;
         }
-        const float ex = fmaxf(mx[0] - mn[0], 1e-30f), ey = fmaxf(mx[1] - mn[1], 1e-30f),
-                    ez = fmaxf(mx[2] - mn[2], 1e-30f);
-        ox = mn[0]; oy = mn[1]; oz = mn[2];
-        scx = 16.f / ex; scy = 16.f / ey; scz = 16.f / ez;
-    }
-    for (int j = tid; j < cnt; j += kT) {
-        const float4 v = xyz[lo + j];
-        atomicAdd(&hist[morton12(v.x, v.y, v.z, ox, oy, oz, scx, scy, scz)], 1u);
-    }
-    __syncthreads();
-    {
-        // exclusive scan of the 4096 bins: 8 consecutive bins per thread
-        constexpr int kPer = kBins / kT;
-        uint32_t loc[kPer], s = 0;
-#pragma unroll
-        for (int i = 0; i < kPer; ++i) { loc[i] = hist[tid * kPer + i]; s += loc[i]; }
-        uint32_t x = s;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(kFull, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane == 31) scan_tot[warp] = x;
-        __syncthreads();
-        uint32_t base = 0;
-        for (int w = 0; w < warp; ++w) base += scan_tot[w];
-        base += x - s;
-#pragma unroll
-        for (int i = 0; i < kPer; ++i) { hist[tid * kPer + i] = base; base += loc[i]; }
-    }
-    __syncthreads();
-    for (int j = tid; j < cnt; j += kT) {
-        const float4 v = xyz[lo + j];
-        const uint32_t pos = atomicAdd(&hist[morton12(v.x, v.y, v.z, ox, oy, oz, scx, scy, scz)], 1u);
-        pts[pos] = make_float4(v.x, v.y, v.z, __int_as_float((int)(lo + j)));
     }
     for (int j = cnt + tid; j < P * kT; j += kT) pts[j] = make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
     __syncthreads();
@@ -700,7 +747,10 @@ bool fps_res_plan(int64_t N, int64_t nclusters, int G, int* C_out, int* P_out) {
     return false;
 }
 
-cudaError_t launch_fps_res(FpsArgs a, const FpsRanks& rk, int64_t B, int C, int P, cudaStream_t s) {
+cudaError_t launch_fps_res(FpsArgs a, const FpsRanks& rk_in, int64_t B, int C, int P, cudaStream_t s) {
+    FpsRanks rk = rk_in;
+    const char* spe = getenv("PS_FPS_SPATIAL");
+    rk.spatial = spe ? atoi(spe) : 1;
     const int64_t Ns = (a.N + rk.G - 1) / rk.G;
     a.points_per_cta = (Ns + C - 1) / C;
     const int64_t nclusters = B * rk.Gl;

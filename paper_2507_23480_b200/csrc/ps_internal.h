@@ -30,6 +30,7 @@ struct FpsArgs {
 // (launch, iteration) tag unique.
 struct FpsRanks {
     int G, Gl, g_base, all_write;
+    int spatial;                // 1: spatial (Morton-cell) partition of the shard over the cluster's CTAs
     uint32_t seq_base;
     uint4* const* mbox;
 };
