@@ -366,9 +366,12 @@ def main_ours(args):
                          "iteration-latency bound")}
 
     # ---- C5 point split: one 2^20-point cloud -> 65536 samples ---------
-    c5 = None
+    c5 = c2 = c4 = None
     if not args.no_c5 and ws == 1:
         c5 = bench_c5_virtual(dev)
+    if not args.no_extra and ws == 1:
+        c2 = bench_c2_cascade(dev, args.steps)
+        c4 = bench_c4(dev, args.steps)
 
     cpu = None
     if rank == 0 and not args.no_cpu:
@@ -404,6 +407,8 @@ def main_ours(args):
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "c5_point_split": c5,
+            "c2_cascade": c2,
+            "c4_large_clouds": c4,
         }
         print(json.dumps(line), flush=True)
     if ws > 1:
@@ -412,6 +417,91 @@ def main_ours(args):
 
 
 C5_N, C5_n = 1 << 20, 65536
+
+
+def _time_graph(fn, reps=10):
+    import torch
+
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def bench_c2_cascade(dev, steps):
+    """C2: B=32 unit-sphere clouds, N=1024, four stride-2 set-abstraction
+    stages (1024->512->256->128->64), ball query r_s = 0.15*1.5^s, k=32:
+    FastPoint on stage 0 (rf grouping) + exact FPS later vs all-exact FPS +
+    naive grouping; each cascade one CUDA graph, inputs resident."""
+    import torch
+
+    from paper_2507_23480_b200 import curve, engine
+    from paper_2507_23480_b200.harness import generate_cloud
+
+    B, Nc = 32, 1024
+    held = np.stack([generate_cloud("unit-sphere", Nc, 77000 + i) for i in range(4)])
+    _, cv, _, _ = engine.fps(engine.as_xyz4(torch.from_numpy(held).to(dev)), Nc // 2)
+    e = curve.fit_power_exponent(cv.cpu().numpy())
+    clouds = np.stack([generate_cloud("unit-sphere", Nc, 2000 + b) for b in range(B)])
+    res = {}
+    for first in ("fastpoint", "fps"):
+        sa = engine.SACascade(B, Nc, first=first, exponent=e, device=dev)
+        sa.set_points(torch.from_numpy(clouds).to(dev))
+        sa.set_rng(list(range(B)))
+        sa.run()
+        sa.fp.check() if first == "fastpoint" else None
+        sa.capture()
+        res[first] = _time_graph(sa.run, max(steps, 5))
+    return {"workload": "C2: B=32 unit-sphere clouds N=1024, 4 SA stages stride 2 (->512->256->128->64), "
+                        "r_s=0.15*1.5^s, k=32", "exponent": round(e, 6),
+            "fastpoint_first_ms": res["fastpoint"], "all_exact_fps_ms": res["fps"],
+            "us_per_cloud": 1e3 * res["fastpoint"] / B, "speedup_vs_exact": res["fps"] / res["fastpoint"],
+            "sampled_pts_per_s": B * (512 + 256 + 128 + 64) / (res["fastpoint"] / 1e3),
+            "timing": "CUDA graph replay, mean of >=5"}
+
+
+def bench_c4(dev, steps):
+    """C4 per-GPU share at 8 GPUs: B=2 room clouds N=65536 -> n=16384
+    FastPoint + rf ball query (r=0.1, k=32) vs exact FPS + naive ball query."""
+    import torch
+
+    from paper_2507_23480_b200 import curve, engine
+    from paper_2507_23480_b200.harness import generate_cloud
+
+    B, Nc, nc = 2, 65536, 16384
+    held = np.stack([generate_cloud(FAMILY, Nc, 88000 + i) for i in range(2)])
+    _, cv, _, _ = engine.fps(engine.as_xyz4(torch.from_numpy(held).to(dev)), nc)
+    e = curve.fit_power_exponent(cv.cpu().numpy())
+    clouds = np.stack([generate_cloud(FAMILY, Nc, 3000 + b) for b in range(B)])
+    fp = engine.FastPoint(B, Nc, nc, p=P, nseg=NSEG, estimator="power", exponent=e, extra_radii=(RADIUS,), device=dev)
+    fp.set_points(torch.from_numpy(clouds).to(dev))
+    grp = (torch.empty(B, nc, K, dtype=torch.int32, device=dev), torch.empty(B, nc, K, dtype=torch.float64, device=dev),
+           torch.empty(B, nc, dtype=torch.int32, device=dev))
+    seeds = torch.arange(B, dtype=torch.int64, device=dev)
+
+    def ours():
+        fp.state.copy_(seeds)
+        fp.sample()
+        fp.group_rf(RADIUS, K, out=grp)
+
+    ours()
+    fp.check()
+    ms = _time_graph(ours, max(2, min(steps, 5)))
+
+    def exact():
+        idx, _, _, _ = engine.fps(fp.xyz4, nc)
+        engine.ball_query_naive(fp.xyz4, idx, RADIUS, K)
+
+    exact()
+    ms_x = _time_graph(exact, 2)
+    return {"workload": "C4 per-GPU share at 8 GPUs: B=2 room clouds N=65536 -> n=16384, FastPoint + rf ball "
+                        "query r=0.1 k=32", "ms": ms, "us_per_cloud": 1e3 * ms / B,
+            "sampled_pts_per_s": B * nc / (ms / 1e3), "exact_fps_path_ms": ms_x, "speedup_vs_exact": ms_x / ms,
+            "exponent": round(e, 6)}
 
 
 def bench_c5_virtual(dev, G=None):
@@ -463,6 +553,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 point-split line")
+    ap.add_argument("--no-extra", action="store_true", help="skip the C2 / C4 objects")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

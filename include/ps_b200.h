@@ -109,6 +109,11 @@ PS_API int ps_fps_update_chunk(const float* xyz4, int64_t N, double px, double p
                         double* md, int64_t lo, int64_t hi, double* best_out,
                         int64_t* arg_out, void* stream);
 
+/* Set-abstraction stage input: out4[b][t] = xyz4[b][idx[b][t]]
+ * (float[B][n][4], w = 0) for t < n; idx int64 with row stride idx_ld. */
+PS_API int ps_gather_xyz4(const float* xyz4, const int64_t* idx, int64_t idx_ld, int64_t B, int64_t N, int64_t n,
+                          float* out4, void* stream);
+
 /* first_untaken (_kernels.py:95-100): lowest j with taken[j] == 0, else -1. */
 PS_API int ps_first_untaken(const uint8_t* taken, int64_t N, int64_t* out, void* stream);
 

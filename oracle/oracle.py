@@ -580,3 +580,32 @@ def quality_ratio(coords, candidate, baseline):
     if b == 0:
         raise ValueError("zero baseline spacing")
     return 100.0 * avg_min_spacing(coords, candidate) / b
+
+
+# ---------------------------------------------------------------------------
+# multi-stage set abstraction (config C2)
+
+
+def sa_cascade(coords, strides=(2, 2, 2, 2), radii=None, k=32, first="fastpoint", p=0.1, nseg=6, exponent=None,
+               rng_seed=0, kernels=DEFAULT_KERNELS):
+    """Stage 0: FastPoint (first="fastpoint") or exact FPS on the cloud, then a
+    ball query of radius radii[0] (rf from the exclusion lists, or naive);
+    stage s > 0: exact FPS of the previous stage's samples (sample order) and
+    a naive ball query of radius radii[s].  Returns per stage
+    (indices into that stage's input, group idx, group counts)."""
+    radii = tuple(radii) if radii is not None else tuple(0.15 * 1.5 ** s for s in range(len(strides)))
+    pts = np.ascontiguousarray(coords, np.float32)
+    stages = []
+    for s, st in enumerate(strides):
+        n = pts.shape[0] // st
+        if s == 0 and first == "fastpoint":
+            res = mdps(pts, n, p=p, nseg=nseg, estimator="power", exponent=exponent, rng_seed=rng_seed,
+                       extra_radii=(radii[0],), kernels=kernels)
+            idx = res.indices
+            gi, _, gc = rf_ball_query(res.excl, radii[0], idx, k)
+        else:
+            idx = fps(pts, n, 0, kernels)[0]
+            gi, _, gc = ball_query_naive(pts, idx, radii[s], k)
+        stages.append((idx, gi, gc))
+        pts = np.ascontiguousarray(pts[idx])
+    return stages

@@ -5,6 +5,7 @@
 // CUDA failures into PS_ERR_CUDA with a message.  Nothing here allocates
 // device memory: buffers and workspaces are owned by the caller.
 
+#include <algorithm>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -74,6 +75,19 @@ __global__ void __launch_bounds__(1024) chunk_update_kernel(const float4* __rest
             if (a.idx == 0xffffffffu) { *best_out = -1.0; *arg_out = -1; }
             else { *best_out = __longlong_as_double((long long)a.key); *arg_out = lo + a.idx; }
         }
+    }
+}
+
+// out4[b][t] = xyz4[b][idx[b][t]] (w = 0): the next set-abstraction stage's
+// input, in sample order
+__global__ void gather_xyz4_kernel(const float4* __restrict__ xyz, const int64_t* __restrict__ idx, int64_t idx_ld,
+                                   int64_t B, int64_t N, int64_t n, float4* __restrict__ out) {
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < B * n; g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = g / n, t = g - b * n;
+        const int64_t j = idx[b * idx_ld + t];
+        float4 v = (j >= 0 && j < N) ? xyz[b * N + j] : make_float4(0.f, 0.f, 0.f, 0.f);
+        v.w = 0.f;
+        out[g] = v;
     }
 }
 
@@ -198,6 +212,17 @@ int ps_fps_update_chunk(const float* xyz4, int64_t N, double px, double py, doub
     chunk_update_kernel<<<1, 1024, 0, S(stream)>>>(reinterpret_cast<const float4*>(xyz4), px, py, pz, md, lo, hi,
                                                   best_out, arg_out);
     return cuda_status(cudaGetLastError(), "fps_update_chunk", 1);
+}
+
+int ps_gather_xyz4(const float* xyz4, const int64_t* idx, int64_t idx_ld, int64_t B, int64_t N, int64_t n,
+                   float* out4, void* stream) {
+    CHECK_ARG(B >= 1 && N >= 1 && n >= 0 && n <= idx_ld, "invalid gather shape");
+    CHECK_ARG(xyz4 && idx && out4, "null pointer");
+    if (n == 0) return PS_OK;
+    const unsigned g = (unsigned)std::min<int64_t>(148 * 8, (B * n + 255) / 256);
+    gather_xyz4_kernel<<<g, 256, 0, S(stream)>>>(reinterpret_cast<const float4*>(xyz4), idx, idx_ld, B, N, n,
+                                                 reinterpret_cast<float4*>(out4));
+    return cuda_status(cudaGetLastError(), "gather_xyz4", 1);
 }
 
 int ps_first_untaken(const uint8_t* taken, int64_t N, int64_t* out, void* stream) {

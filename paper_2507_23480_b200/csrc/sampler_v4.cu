@@ -162,6 +162,12 @@ PS_DEV uint4 ld_cluster_v4(uint32_t addr) {
     return v;
 }
 
+// cluster barrier, or the block barrier when a cloud has a single CTA
+PS_DEV void sync_all(int C) {
+    if (C == 1) __syncthreads();
+    else cluster_sync_all();
+}
+
 // kSm: the availability byte map and the rank table live in every CTA's
 // shared memory (N bytes + 4N bytes); the map is built by owner CTAs
 // (contiguous 16-byte-aligned index ranges, cleared through DSMEM stores)
@@ -329,7 +335,7 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
             }
         }
         VT4(18);
-        cluster_sync_all();
+        sync_all(C);
         VT4(13);
         if (!kSm) {
             for (int64_t x = gt; x < i; x += GT) {
@@ -350,7 +356,7 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
                 avail[q] = 0;
             }
         }
-        cluster_sync_all();
+        sync_all(C);
         if (kSm) {
             const uint32_t avail_base = smem_u32(avail);
             // gather the other owners' ranges into my copy of the map
@@ -397,7 +403,7 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
         }
         mycnt = bsum(mycnt, wt);
         if (tid == 0) scr[kCnt0 + r] = mycnt;
-        cluster_sync_all();
+        sync_all(C);
         VT4(1);
         int off = 0, L = 0;
         for (int c2 = 0; c2 < C; ++c2) {
@@ -454,7 +460,7 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
                 if (valid && gl == 0) adjcnt[j] = n > kAdj4 ? kAdjOvf : (uint8_t)n;
             }
         }
-        cluster_sync_all();
+        sync_all(C);
         VT4(2);
         if (tdbg) { a.dbg[10] += 1; a.dbg[11] += L; }
 
@@ -473,7 +479,7 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
                 pos[t] = p;
                 nxt[t] = atomicExch(&head[p], t);
             }
-            cluster_sync_all();
+            sync_all(C);
             VT4(3);
             for (int t = gt; t < L; t += GT) {
                 // latest earlier writer of my position, and of my tail slot L-1-t
@@ -486,7 +492,7 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
                     if (x < t && x > bl) bl = x;
                 lw[t] = bl;
             }
-            cluster_sync_all();
+            sync_all(C);
             VT4(4);
             for (int t = gt; t < L; t += GT) {
                 // value at pos[t] before draw t: untouched -> pool; else the value
@@ -506,7 +512,7 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
                 stt[t] = kUnd4;
             }
         }
-        cluster_sync_all();
+        sync_all(C);
         if (kSm) {
             for (int t = tid; t < L; t += kT4) rank[cand[t]] = t;
             __syncthreads();
@@ -586,7 +592,7 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
         }
         decided = bsum(decided, wt);
         if (tid == 0 && decided) atomicAdd(&scr[kDecided], decided);
-        cluster_sync_all();
+        sync_all(C);
         VT4(6);
         while (scr[kDecided] < L) {
             if (tdbg) a.dbg[12] += 1;
@@ -645,7 +651,7 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
             }
             dd = bsum(dd, wt);
             if (tid == 0 && dd) atomicAdd(&scr[kDecided], dd);
-            cluster_sync_all();
+            sync_all(C);
         }
 
         VT4(7);
@@ -657,7 +663,7 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
         for (int t = tlo + tid; t < thi; t += kT4) nin += stt[t] == kIn4 ? 1 : 0;
         nin = bsum(nin, wt);
         if (tid == 0) scr[kCnt1 + r] = nin;
-        cluster_sync_all();
+        sync_all(C);
         int aoff = 0, A = 0;
         for (int c2 = 0; c2 < C; ++c2) {
             const int v = scr[kCnt1 + c2];
@@ -678,7 +684,7 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
             }
             aoff += tot;
         }
-        cluster_sync_all();
+        sync_all(C);
         VT4(8);
         const int last = ends ? scr[kLast] : -1;
         i += take;
@@ -731,10 +737,15 @@ size_t sampler_v4_ws_bytes(int64_t B, int64_t N) {
     return s;
 }
 
-static int v4_cluster() {
+// CTAs per cloud: ~3000 points per CTA, at most 8, and at most one wave of
+// 148 SMs for the batch when that still leaves >= 1 CTA per cloud
+static int v4_cluster(int64_t N, int64_t B) {
     const char* e = getenv("PS_SAMPLER_CLUSTER");
-    int c = e ? atoi(e) : 8;
-    return c < 1 ? 1 : (c > 16 ? 16 : c);
+    int c = e ? atoi(e) : (int)((N + 2999) / 3000);
+    c = c < 1 ? 1 : (c > 8 ? 8 : c);
+    if (!e)
+        while (c > 1 && B * c > 148) --c;
+    return c;
 }
 
 cudaError_t launch_sampler_v4(SampArgs a, int64_t B, cudaStream_t s) {
@@ -757,7 +768,7 @@ cudaError_t launch_sampler_v4(SampArgs a, int64_t B, cudaStream_t s) {
     w.preds = reinterpret_cast<int32_t*>(p); p += align256_4(sizeof(int32_t) * B * N * kPred4);
     w.scr = reinterpret_cast<int32_t*>(p);
     a.B = B;
-    const int C = v4_cluster();
+    const int C = v4_cluster(N, B);
     cudaError_t e = cudaSuccess;
     const int64_t Npad = (N + 15) & ~(int64_t)15;
     const int64_t span0 = ((N + C - 1) / C + 15) & ~(int64_t)15;

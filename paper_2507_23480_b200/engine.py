@@ -455,3 +455,110 @@ def min_spacing_d2(xyz4, samples):
     out = torch.empty(B, n, dtype=torch.float64, device=xyz4.device)
     _lib.call("ps_min_spacing", _p(xyz4), _p(samples), samples.stride(0), n, B, N, _p(out), _stream())
     return out
+
+
+# ---------------------------------------------------------------------------
+# multi-stage set abstraction (config C2, SURVEY 8f-1)
+
+
+def gather_xyz4(xyz4: torch.Tensor, idx: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """[B, N, 4] points at idx [B, n] (sample order) -> [B, n, 4]."""
+    B, N, _ = xyz4.shape
+    n = idx.shape[1]
+    if out is None:
+        out = torch.empty(B, n, 4, dtype=torch.float32, device=xyz4.device)
+    _lib.call("ps_gather_xyz4", _p(xyz4), _p(idx), idx.stride(0), B, N, n, _p(out), _stream())
+    return out
+
+
+class SACascade:
+    """PointNet++ / PointNeXt set-abstraction sampling cascade on a batch
+    (config C2: B clouds of N points, stages of stride ``strides``, ball query
+    radius ``radii[s]`` with k neighbours per stage).
+
+    Stage 0 samples the input clouds with FastPoint and groups from the cached
+    distances (the paper applies FastPoint to the first layer, PAPER.md:275);
+    every later stage runs exact FPS on the previous stage's samples in sample
+    order, then a naive ball query.  ``first="fps"`` gives the all-exact
+    cascade the paper compares against.  Buffers are static, so ``capture``
+    records the whole cascade in one CUDA graph."""
+
+    def __init__(self, B, N, strides=(2, 2, 2, 2), radii=None, k=32, *, first="fastpoint", exponent=None, p=0.1,
+                 nseg=6, device="cuda"):
+        if first not in ("fastpoint", "fps"):
+            raise ValueError("first must be 'fastpoint' or 'fps'")
+        radii = tuple(radii) if radii is not None else tuple(0.15 * 1.5 ** s for s in range(len(strides)))
+        if len(radii) != len(strides):
+            raise ValueError("one radius per stage")
+        self.B, self.N, self.k, self.first = int(B), int(N), int(k), first
+        self.strides, self.radii = tuple(int(s) for s in strides), tuple(float(r) for r in radii)
+        dev = torch.device(device)
+        self.device = dev
+        self.sizes = [self.N]
+        for st in self.strides:
+            self.sizes.append(self.sizes[-1] // st)
+        if self.sizes[-1] < 1:
+            raise ValueError("cascade samples fewer than one point")
+        self.xyz = [torch.zeros(B, m, 4, dtype=torch.float32, device=dev) for m in self.sizes]
+        self.idx, self.groups, self.fps_bufs = [], [], []
+        for s, st in enumerate(self.strides):
+            n_in, n = self.sizes[s], self.sizes[s + 1]
+            self.groups.append((torch.empty(B, n, k, dtype=torch.int32, device=dev),
+                                torch.empty(B, n, k, dtype=torch.float64, device=dev),
+                                torch.empty(B, n, dtype=torch.int32, device=dev)))
+            if s == 0 and first == "fastpoint":
+                self.fp = FastPoint(B, n_in, n, p=p, nseg=nseg, estimator="power", exponent=exponent,
+                                    extra_radii=(self.radii[0],), device=dev)
+                self.idx.append(self.fp.out)
+                self.fps_bufs.append(None)
+            else:
+                self.fps_bufs.append((torch.empty(B, n_in, dtype=torch.float64, device=dev),
+                                      torch.empty(B, n_in, dtype=torch.uint8, device=dev),
+                                      torch.full((B, n), math.inf, dtype=torch.float64, device=dev)))
+                self.idx.append(torch.full((B, n), -1, dtype=torch.int64, device=dev))
+        self.graph = None
+
+    def set_points(self, coords):
+        x = as_xyz4(coords, self.device)
+        if tuple(x.shape[:2]) != (self.B, self.N):
+            raise ValueError(f"expected ({self.B}, {self.N}, 3) coordinates")
+        self.xyz[0].copy_(x)
+        if self.first == "fastpoint":
+            self.fp.set_points(coords)
+
+    def set_rng(self, seeds):
+        if self.first == "fastpoint":
+            self.fp.set_rng(seeds)
+
+    def run(self):
+        """All stages, stream-ordered, no host sync."""
+        if self.graph is not None:
+            self.graph.replay()
+            return
+        B, k = self.B, self.k
+        for s in range(len(self.strides)):
+            n_in, n = self.sizes[s], self.sizes[s + 1]
+            x = self.xyz[s]
+            gi, gd, gc = self.groups[s]
+            if s == 0 and self.first == "fastpoint":
+                self.fp.sample()
+                self.fp.group_rf(self.radii[0], k, out=self.groups[0])
+            else:
+                md, taken, curve = self.fps_bufs[s]
+                out = self.idx[s]
+                _lib.call("ps_fps", _p(x), B, n_in, _p(md), _p(taken), _p(out), _p(curve), n, n, 0, None, _stream())
+                _lib.call("ps_ball_query_naive", _p(x), _p(out), out.stride(0), B, n_in, n,
+                          radius_sq(self.radii[s]), k, _p(gi), _p(gd), _p(gc), _stream())
+            gather_xyz4(x, self.idx[s], out=self.xyz[s + 1])
+
+    def capture(self):
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self.run()
+        torch.cuda.current_stream().wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.run()
+        self.graph = g
+        return g

@@ -428,3 +428,61 @@ def test_errors_are_value_errors():
     fp = gpu_mdps(generate_cloud("uniform-box", 500, 1), 100, exponent=0.4, extra_radii=(0.1,))
     with pytest.raises(ValueError, match="not baked"):
         fp.group_rf(0.2, 8)
+
+
+# ---- C2: multi-stage set-abstraction cascade -----------------------------
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("first", ["fastpoint", "fps"])
+def test_sa_cascade_matches_oracle(first):
+    """Four stride-2 stages on unit-sphere clouds (C2 shape, B reduced):
+    stage 0 FastPoint + rf ball query (or exact FPS + naive), later stages
+    exact FPS + naive ball query on the previous samples -- every stage's
+    indices, group members and counts bit-identical to the oracle cascade;
+    the CUDA-graph replay reproduces them."""
+    B, N, k = 3, 1024, 32
+    clouds = np.stack([generate_cloud("unit-sphere", N, 70 + b) for b in range(B)])
+    exponent = 0.5
+    sa = engine.SACascade(B, N, k=k, first=first, exponent=exponent)
+    sa.set_points(torch.from_numpy(clouds).cuda())
+    sa.set_rng(list(range(B)))
+    sa.run()
+    torch.cuda.synchronize()
+    got = [(sa.idx[s].cpu().numpy(), sa.groups[s][0].cpu().numpy(), sa.groups[s][2].cpu().numpy())
+           for s in range(4)]
+    for b in range(B):
+        ref = O.sa_cascade(clouds[b], k=k, first=first, exponent=exponent, rng_seed=b)
+        for s, (ri, rg, rc) in enumerate(ref):
+            gi, gg, gc = got[s]
+            np.testing.assert_array_equal(gi[b], ri, err_msg=f"stage {s} indices, cloud {b}")
+            np.testing.assert_array_equal(gc[b], rc, err_msg=f"stage {s} counts")
+            for t in range(len(ri)):
+                m = int(rc[t])
+                np.testing.assert_array_equal(gg[b, t, :m], rg[t, :m])
+    sa.set_rng(list(range(B)))
+    sa.capture()
+    sa.set_rng(list(range(B)))
+    sa.run()
+    torch.cuda.synchronize()
+    for s in range(4):
+        np.testing.assert_array_equal(sa.idx[s].cpu().numpy(), got[s][0])
+
+
+@pytest.mark.timeout(600)
+def test_c4_shape_fastpoint_matches_oracle():
+    """C4 cloud shape (N = 65536 -> 16384, room surfaces): FastPoint indices,
+    reached count and RF groups bit-identical to the oracle (global-memory
+    sampler tables, large-N FPS plan)."""
+    N, n = 65536, 16384
+    c = generate_cloud("room-surfaces", N, 4242)
+    fp = engine.FastPoint(1, N, n, exponent=0.53, extra_radii=(0.1,))
+    fp.set_points(torch.from_numpy(c[None]).cuda())
+    fp.set_rng([5])
+    fp.sample()
+    fp.check()
+    gi, _, gc = fp.group_rf(0.1, 32)
+    ref = O.mdps(c, n, exponent=0.53, rng_seed=5, extra_radii=(0.1,))
+    np.testing.assert_array_equal(fp.out[0].cpu().numpy(), ref.indices)
+    assert int(fp.reached[0].item()) == ref.reached
+    oi, _, oc = O.rf_ball_query(ref.excl, 0.1, ref.indices, 32)
+    np.testing.assert_array_equal(gc[0].cpu().numpy(), oc)
