@@ -161,6 +161,19 @@ PS_API int ps_thresholds(const double* prefix_curve, int64_t curve_ld, int64_t B
                   const double* extra_r2_host, int32_t n_extra, double* R_out,
                   double* r2_levels, int64_t levels_ld, void* stream);
 
+/* SPEC.md:298-306 estimate_mlp + segment_thresholds: the measured prefix
+ * curve[b][1..k0) resampled to 32 values and divided by curve[b][k0-1], a
+ * 32-128-128-64 relu MLP (mlp_weights: device float64 W1[128][32], b1[128],
+ * W2[128][128], b2[128], W3[64][128], b3[64], the SPEC.md:357 layer order),
+ * outputs times curve[b][k0-1] resampled to the n-k0 tail positions, running
+ * minimum from curve[b][k0-1]; then radii / levels as ps_thresholds.  Fixed
+ * summation order (input order, bias last): bit-identical to the host
+ * curve.estimate_mlp.  k0 >= 3. */
+PS_API int ps_thresholds_mlp(const double* prefix_curve, int64_t curve_ld, int64_t B, int64_t k0, int64_t n,
+                             int32_t nseg, const int64_t* d_host, const double* mlp_weights,
+                             const double* extra_r2_host, int32_t n_extra, double* R_out, double* r2_levels,
+                             int64_t levels_ld, void* stream);
+
 /* ---- K3c: predicted-distance bitmap sampler ------------------------------
  * Replaces sample_predicted (_kernels.py:251-353).  out_idx[b][0..k0) holds
  * the FPS prefix on entry; entries [k0, n_total) are written (-1 beyond the

@@ -446,7 +446,7 @@ class MdpsResult:
 
 
 def mdps(coords, n, p=0.1, nseg=6, estimator="power", exponent=None, curve=None,
-         seed_index=0, rng_seed=0, extra_radii=(), pick_lowest=False, kernels=DEFAULT_KERNELS):
+         seed_index=0, rng_seed=0, extra_radii=(), pick_lowest=False, kernels=DEFAULT_KERNELS, mlp=None):
     """SPEC.md:425-433 composition (call stack B of SURVEY.md section 3)."""
     N = np.asarray(coords).shape[0]
     if not (1 <= n <= N):
@@ -464,6 +464,10 @@ def mdps(coords, n, p=0.1, nseg=6, estimator="power", exponent=None, curve=None,
     elif estimator == "curve":
         est = np.asarray(curve, np.float64).copy()
         est[:k0] = pre_curve
+    elif estimator == "mlp":
+        if mlp is None:
+            raise ValueError("mlp estimator needs a model")
+        est = estimate_mlp(pre_curve, n, mlp)
     else:
         raise ValueError(f"unknown estimator {estimator!r}")
     d, R = segment_thresholds(est, nseg)
@@ -609,3 +613,109 @@ def sa_cascade(coords, strides=(2, 2, 2, 2), radii=None, k=32, first="fastpoint"
         stages.append((idx, gi, gc))
         pts = np.ascontiguousarray(pts[idx])
     return stages
+
+
+# ---------------------------------------------------------------------------
+# MLP curve estimator, restated independently of the
+# product code.  Pinned where the SPEC is silent (SURVEY B):
+#   resample: u = (t * (S-1)) / (T-1); i0 = floor(u); frac = u - i0;
+#             out = v[i0] + frac * (v[i0+1] - v[i0]); t = T-1 -> v[S-1];
+#             T == 1 -> v[0]
+#   forward: every dot product summed in input order from 0.0, bias added
+#            last, relu(a) = a if a > 0 else 0.0, no FMA
+#   estimate: prefix positions 1..k0-1 -> 32 values / v[k0-1] -> forward ->
+#             * v[k0-1] -> resampled to the n-k0 tail positions -> running
+#             minimum from v[k0-1]
+
+
+@dataclass
+class OracleMlp:
+    W1: np.ndarray  # [128, 32]
+    b1: np.ndarray
+    W2: np.ndarray  # [128, 128]
+    b2: np.ndarray
+    W3: np.ndarray  # [64, 128]
+    b3: np.ndarray
+
+
+def read_mlp(path) -> OracleMlp:
+    """SPEC.md:357 text format: `MLP 32 128 128 64`, then per layer `W r c`
+    + r*c floats (row-major) and `B c` + c floats."""
+    tok = open(path).read().split()
+    if tok[:5] != ["MLP", "32", "128", "128", "64"]:
+        raise ValueError("not an MLP 32 128 128 64 file")
+    pos = 5
+    mats = []
+    for _ in range(3):
+        if tok[pos] != "W":
+            raise ValueError("expected W header")
+        r, c = int(tok[pos + 1]), int(tok[pos + 2])
+        W = np.array([float(x) for x in tok[pos + 3:pos + 3 + r * c]], np.float64).reshape(r, c)
+        pos += 3 + r * c
+        if tok[pos] != "B" or int(tok[pos + 1]) != r:
+            raise ValueError("expected B header")
+        bv = np.array([float(x) for x in tok[pos + 2:pos + 2 + r]], np.float64)
+        pos += 2 + r
+        mats += [W, bv]
+    return OracleMlp(*mats)
+
+
+def resample_pinned(v, T: int) -> np.ndarray:
+    v = [float(x) for x in v]
+    S = len(v)
+    if S < 2:
+        raise ValueError("need >= 2 values")
+    out = np.empty(T, np.float64)
+    if T == 1:
+        out[0] = v[0]
+        return out
+    for t in range(T):
+        u = (float(t) * float(S - 1)) / float(T - 1)
+        i0 = int(math.floor(u))
+        if i0 >= S - 1:
+            out[t] = v[S - 1]
+            continue
+        frac = u - float(i0)
+        out[t] = v[i0] + frac * (v[i0 + 1] - v[i0])
+    return out
+
+
+def mlp_forward_seq(m: OracleMlp, x) -> np.ndarray:
+    def layer(W, bv, inp, relu):
+        out = np.empty(W.shape[0], np.float64)
+        for j in range(W.shape[0]):
+            acc = 0.0
+            row = W[j]
+            for i in range(W.shape[1]):
+                acc = acc + float(row[i]) * float(inp[i])
+            acc = acc + float(bv[j])
+            out[j] = (acc if acc > 0.0 else 0.0) if relu else acc
+        return out
+
+    h1 = layer(m.W1, m.b1, x, True)
+    h2 = layer(m.W2, m.b2, h1, True)
+    return layer(m.W3, m.b3, h2, False)
+
+
+def estimate_mlp(prefix_curve, n: int, m: OracleMlp) -> np.ndarray:
+    v = np.asarray(prefix_curve, np.float64)
+    k0 = v.shape[0]
+    if k0 < 3:
+        raise ValueError("the MLP estimator needs >= 2 finite prefix values (k0 >= 3)")
+    scale = float(v[k0 - 1])
+    if not scale > 0:
+        raise ValueError("last measured prefix value must be > 0")
+    x = resample_pinned(v[1:k0], 32)
+    x = np.array([float(a) / scale for a in x])
+    y = mlp_forward_seq(m, x)
+    y = np.array([float(a) * scale for a in y])
+    out = np.empty(n, np.float64)
+    out[:k0] = v
+    if n > k0:
+        tail = resample_pinned(y, n - k0)
+        run = scale
+        for i in range(n - k0):
+            if tail[i] < run:
+                run = float(tail[i])
+            out[k0 + i] = run
+    return out

@@ -39,6 +39,8 @@ _SIGS = {
     "ps_level_counts": (_c_i32, [_p, _p, _c_i64, _c_i64, _c_i64, _p, _c_i32, _c_i64, _p, _p]),
     "ps_thresholds": (_c_i32, [_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_i32, _p, _c_i32, _p, _p, _c_i64, _p,
                                _c_i32, _p, _p, _c_i64, _p]),
+    "ps_thresholds_mlp": (_c_i32, [_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_i32, _p, _p, _p, _c_i32, _p, _p, _c_i64,
+                                   _p]),
     "ps_sampler_workspace_bytes": (_c_i64, [_c_i64, _c_i64, _c_i32]),
     "ps_sample_predicted": (_c_i32, [_p, _p, _c_i64, _p, _c_i32, _p, _p, _c_i32, _p, _c_i64, _c_i64, _c_i64,
                                      _c_i64, _c_i64, _p, _c_i32, _p, _p, _p, _p, _p]),

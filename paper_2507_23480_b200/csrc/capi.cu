@@ -352,6 +352,27 @@ int ps_thresholds(const double* prefix_curve, int64_t curve_ld, int64_t B, int64
     return cuda_status(ps::launch_thresholds(a, B, S(stream)), "thresholds", 1);
 }
 
+int ps_thresholds_mlp(const double* prefix_curve, int64_t curve_ld, int64_t B, int64_t k0, int64_t n, int32_t nseg,
+                      const int64_t* d_host, const double* mlp_weights, const double* extra_r2_host, int32_t n_extra,
+                      double* R_out, double* r2_levels, int64_t levels_ld, void* stream) {
+    CHECK_ARG(nseg >= 1 && nseg <= ps::kMaxSeg, "nseg must be in [1, %d]", ps::kMaxSeg);
+    CHECK_ARG(n_extra >= 0 && n_extra <= ps::kMaxExtra, "at most %d extra radii", ps::kMaxExtra);
+    CHECK_ARG(k0 >= 3 && k0 <= n, "the MLP estimator needs k0 in [3, n] (k0=%lld)", (long long)k0);
+    CHECK_ARG(levels_ld >= nseg + n_extra, "levels_ld too small");
+    CHECK_ARG(mlp_weights != nullptr, "missing MLP weights");
+    ps::ThreshArgs a = {};
+    a.prefix_curve = prefix_curve; a.curve_ld = curve_ld; a.mode = 2; a.mlp = mlp_weights;
+    a.k0 = k0; a.n = n; a.nseg = nseg;
+    for (int s = 0; s < nseg; ++s) {
+        CHECK_ARG(d_host[s] >= 0 && d_host[s] < n, "d[%d] out of range", s);
+        a.d[s] = d_host[s];
+    }
+    a.n_extra = n_extra;
+    for (int e = 0; e < n_extra; ++e) a.extra_r2[e] = extra_r2_host[e];
+    a.R_out = R_out; a.r2_levels = r2_levels; a.levels_ld = levels_ld;
+    return cuda_status(ps::launch_thresholds(a, B, S(stream)), "thresholds_mlp", 1);
+}
+
 static bool sampler_fits_smem(int64_t N, int nseg) { return ps::sampler_ws_bytes(N, nseg) <= 176 * 1024; }
 
 int64_t ps_sampler_workspace_bytes(int64_t B, int64_t N, int32_t nseg) {

@@ -31,6 +31,35 @@ constexpr double kTiny = 4.9406564584124654e-324;
 // ---------------------------------------------------------------------------
 // K2: thresholds
 
+// pinned linear resampling (curve.resample_curve, oracle.resample_pinned)
+PS_DEV double resample_at(const double* v, int64_t S, int64_t T, int64_t t) {
+    if (T == 1) return v[0];
+    const double u = __ddiv_rn(__dmul_rn((double)t, (double)(S - 1)), (double)(T - 1));
+    const int64_t i0 = (int64_t)floor(u);
+    if (i0 >= S - 1) return v[S - 1];
+    const double frac = __dsub_rn(u, (double)i0);
+    return __dadd_rn(v[i0], __dmul_rn(frac, __dsub_rn(v[i0 + 1], v[i0])));
+}
+
+// one MLP neuron: input-order dot product from 0.0, bias last, optional relu
+PS_DEV double mlp_neuron(const double* __restrict__ W, const double* __restrict__ bias, const double* x, int nin,
+                         int j, bool relu) {
+    double acc = 0.0;
+    const double* row = W + (int64_t)j * nin;
+    for (int i = 0; i < nin; ++i) acc = __dadd_rn(acc, __dmul_rn(row[i], x[i]));
+    acc = __dadd_rn(acc, bias[j]);
+    return relu ? (acc > 0.0 ? acc : 0.0) : acc;
+}
+
+// order-preserving key of any non-NaN double (for atomicMin)
+PS_DEV unsigned long long dkey(double d) {
+    const unsigned long long u = (unsigned long long)__double_as_longlong(d);
+    return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+PS_DEV double dunkey(unsigned long long k) {
+    return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
+}
+
 __global__ void __launch_bounds__(1024) thresholds_kernel(ThreshArgs a) {
     __shared__ unsigned long long seg_min[kMaxSeg];
     __shared__ double s_a;
@@ -76,6 +105,49 @@ __global__ void __launch_bounds__(1024) thresholds_kernel(ThreshArgs a) {
                     est_d[s] = v[a.d[s]];
                 } else {
                     const double m = __longlong_as_double((long long)seg_min[s]);
+                    if (m < run) run = m;
+                    est_d[s] = run;
+                }
+            }
+        }
+    } else if (a.mode == 2) {
+        // MLP estimator: prefix 1..k0-1 -> 32 values / v[k0-1]
+        // -> 32-128-128-64 relu MLP -> * v[k0-1] -> resampled to the n-k0 tail
+        // positions -> running minimum from v[k0-1] (pinned in curve.py / oracle)
+        __shared__ double xs[32], h1[128], h2[128], ys[64];
+        const double* W1 = a.mlp;
+        const double* b1 = W1 + 128 * 32;
+        const double* W2 = b1 + 128;
+        const double* b2 = W2 + 128 * 128;
+        const double* W3 = b2 + 128;
+        const double* b3 = W3 + 64 * 128;
+        const int64_t S = k0 - 1;
+        const double scale = v[k0 - 1];
+        const bool ok = scale > 0.0 && S >= 2;  // else the tail is 0 (degenerate, R -> tiny)
+        if (threadIdx.x < 32) xs[threadIdx.x] = ok ? __ddiv_rn(resample_at(v + 1, S, 32, threadIdx.x), scale) : 0.0;
+        __syncthreads();
+        if (threadIdx.x < 128) h1[threadIdx.x] = mlp_neuron(W1, b1, xs, 32, threadIdx.x, true);
+        __syncthreads();
+        if (threadIdx.x < 128) h2[threadIdx.x] = mlp_neuron(W2, b2, h1, 128, threadIdx.x, true);
+        __syncthreads();
+        if (threadIdx.x < 64) ys[threadIdx.x] = ok ? __dmul_rn(mlp_neuron(W3, b3, h2, 128, threadIdx.x, false), scale)
+                                                   : 0.0;
+        if (threadIdx.x < kMaxSeg) seg_min[threadIdx.x] = dkey(__longlong_as_double(0x7ff0000000000000LL));
+        __syncthreads();
+        for (int64_t i = k0 + threadIdx.x; i < n; i += blockDim.x) {
+            const double t = resample_at(ys, 64, n - k0, i - k0);
+            int s = 0;
+            while (s < nseg && a.d[s] < i) ++s;
+            if (s < nseg) atomicMin(&seg_min[s], dkey(t));
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double run = v[k0 - 1];
+            for (int s = 0; s < nseg; ++s) {
+                if (a.d[s] < k0) {
+                    est_d[s] = v[a.d[s]];
+                } else {
+                    const double m = dunkey(seg_min[s]);
                     if (m < run) run = m;
                     est_d[s] = run;
                 }

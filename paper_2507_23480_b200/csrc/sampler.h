@@ -15,7 +15,8 @@ struct ThreshArgs {
     const double* pow_tab;       // [n] i**e (mode 0)
     const double* given_curve;   // [B][given_ld] (mode 1)
     int64_t given_ld;
-    int mode;                    // 0 power, 1 given curve
+    int mode;                    // 0 power, 1 given curve, 2 MLP
+    const double* mlp;           // mode 2: packed W1 b1 W2 b2 W3 b3 (float64, row-major)
     int64_t k0, n;
     int nseg;
     int64_t d[kMaxSeg];          // min(floor(n s / nseg), n-1)

@@ -219,13 +219,15 @@ class FastPoint:
     exclusion lists."""
 
     def __init__(self, B, N, n, *, p=0.1, nseg=6, estimator="power", exponent=None, extra_radii=(),
-                 seed_index=0, pick_lowest=False, cap_entries=None, excl_method="grid", device="cuda"):
+                 seed_index=0, pick_lowest=False, cap_entries=None, excl_method="grid", device="cuda", mlp=None):
         if not (1 <= n <= N):
             raise ValueError(f"n must be in [1, {N}]")
         if nseg < 1 or nseg > 16:
             raise ValueError("nseg must be in [1, 16]")
-        if estimator not in ("power", "curve"):
+        if estimator not in ("power", "curve", "mlp"):
             raise ValueError(f"unknown estimator {estimator!r}")
+        if estimator == "mlp" and mlp is None:
+            raise ValueError("mlp estimator needs a model (curve.MlpModel)")
         if estimator == "power" and exponent is None:
             raise ValueError("power estimator needs an exponent (fit_power_exponent)")
         self.B, self.N, self.n = int(B), int(N), int(n)
@@ -267,6 +269,10 @@ class FastPoint:
         self.pow_tab = (torch.as_tensor(power_table(self.n, self.exponent), device=dev)
                         if estimator == "power" else None)
         self.given_curve = torch.zeros(B, n, dtype=torch.float64, device=dev) if estimator == "curve" else None
+        self.mlp_w = (torch.as_tensor(mlp.packed(), dtype=torch.float64, device=dev)
+                      if estimator == "mlp" else None)
+        if estimator == "mlp" and self.k0 < 3:
+            raise ValueError("the MLP estimator needs ceil(p*n) >= 3")
         ce, cg = (default_capacity(N, n) if cap_entries is None else (int(cap_entries), int(cap_entries) // 2 + 1))
         self.csr = DeviceCsr.allocate(B, N, self.L, ce, cg, dev, self.excl_method)
         ws = int(_lib.raw("ps_sampler_workspace_bytes", B, N, self.nseg))
@@ -304,8 +310,13 @@ class FastPoint:
                   _p(self.curve), self.n, self.k0, self.seed_index, None, _stream())
 
     def _thresholds(self):
-        mode = 0 if self.estimator == "power" else 1
         extra = np.ascontiguousarray(self.extra_r2) if len(self.extra_r2) else np.zeros(1)
+        if self.estimator == "mlp":
+            _lib.call("ps_thresholds_mlp", _p(self.curve), self.n, self.B, self.k0, self.n, self.nseg,
+                      self._d_c.ctypes.data, _p(self.mlp_w), extra.ctypes.data, len(self.extra_r2), _p(self.R),
+                      _p(self.csr.levels), self.L, _stream())
+            return
+        mode = 0 if self.estimator == "power" else 1
         _lib.call("ps_thresholds", _p(self.curve), self.n, self.B, self.k0, self.n, self.nseg,
                   self._d_c.ctypes.data, mode, _p(self.pow_tab), _p(self.given_curve), self.n,
                   extra.ctypes.data, len(self.extra_r2), _p(self.R), _p(self.csr.levels), self.L, _stream())

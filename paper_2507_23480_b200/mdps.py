@@ -46,16 +46,22 @@ def _cloud(cloud):
 
 
 def mdps(cloud, n: int, p: float = 0.1, nseg: int = 6, estimator: str = "power", exponent=None, curve=None,
-         seed_index: int = 0, rng=None, extra_radii=(), pick_lowest: bool = False, return_pipeline: bool = False):
+         seed_index: int = 0, rng=None, extra_radii=(), pick_lowest: bool = False, return_pipeline: bool = False,
+         model=None):
     """FastPoint sampling of one cloud.  ``estimator``: 'power' (needs
-    ``exponent``, see curve.fit_power_exponent) or 'curve' (a full estimated
-    curve, e.g. the oracle estimator's true FPS curve).  ``rng`` is a
-    core.Rng (advanced in place) or an integer seed."""
+    ``exponent``, see curve.fit_power_exponent), 'mlp' (needs ``model``, a
+    curve.MlpModel or the path of an SPEC.md:357 weight file) or 'curve' (a
+    full estimated curve, e.g. the oracle estimator's true FPS curve).
+    ``rng`` is a core.Rng (advanced in place) or an integer seed."""
+    from . import curve as _curve
+
+    if estimator == "mlp" and model is not None and not isinstance(model, _curve.MlpModel):
+        model = _curve.MlpModel.load(model)
     pc = _cloud(cloud)
     r = rng if isinstance(rng, core.Rng) else core.Rng(0 if rng is None else int(rng))
     t0 = time.perf_counter()
     fp = engine.FastPoint(1, pc.n, n, p=p, nseg=nseg, estimator=estimator, exponent=exponent,
-                          extra_radii=extra_radii, seed_index=seed_index, pick_lowest=pick_lowest)
+                          extra_radii=extra_radii, seed_index=seed_index, pick_lowest=pick_lowest, mlp=model)
     fp.set_points(torch.from_numpy(pc.coords.copy()).to(fp.device))
     fp.set_rng([r.state])
     if estimator == "curve":

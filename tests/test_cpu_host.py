@@ -124,3 +124,90 @@ def test_product_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(root, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "ps_oracle" not in txt, f
+
+
+# ---- MLP estimator host pieces (A8) --------------------------
+
+def test_resample_curve_spec_examples():
+    from paper_2507_23480_b200 import curve as Cv
+
+    np.testing.assert_array_equal(Cv.resample_curve([4, 2], 3), [4, 3, 2])
+    np.testing.assert_array_equal(Cv.resample_curve([4, 3, 2, 1], 4), [4, 3, 2, 1])
+    r = Cv.resample_curve(np.arange(10.0), 32)                                        # SPEC.md:296 (affine)
+    assert np.max(np.abs(r - np.linspace(0.0, 9.0, 32))) < 1e-13
+    v = np.random.default_rng(0).random(17)
+    assert Cv.resample_curve(v, 5)[0] == v[0] and Cv.resample_curve(v, 5)[-1] == v[-1]
+    with pytest.raises(ValueError):
+        Cv.resample_curve([1.0], 4)
+
+
+def test_mlp_model_file_roundtrip_and_zero_model(tmp_path):
+    from paper_2507_23480_b200 import curve as Cv
+
+    m = Cv.MlpModel.init(np.random.default_rng(4))
+    m.save(tmp_path / "m.txt")
+    m2 = Cv.MlpModel.load(tmp_path / "m.txt")
+    for a, b in zip(m.W + m.b, m2.W + m2.b):
+        np.testing.assert_array_equal(a, b)
+    assert open(tmp_path / "m.txt").readline().strip() == "MLP 32 128 128 64"
+    z = Cv.MlpModel(*[np.zeros_like(a) for k in range(3) for a in (m.W[k], m.b[k])])
+    np.testing.assert_array_equal(Cv.mlp_forward_exact(z, np.ones(32)), np.zeros(64))
+
+
+def test_mlp_gradients_match_finite_differences():
+    """SPEC.md:276 / A8(ii): every layer's gradient within 1e-4 relative of
+    central differences (eps = 1e-3)."""
+    from paper_2507_23480_b200 import curve as Cv
+
+    rng = np.random.default_rng(7)
+    m = Cv.MlpModel.init(rng)
+    for k in range(3):
+        m.b[k] = rng.normal(0, 0.1, m.b[k].shape)
+    x, y = rng.normal(size=32), rng.normal(size=64)
+    _, g = Cv.mlp_loss_grad(m, x, y)
+    eps = 1e-3
+    for k in range(3):
+        for (r, c) in ((0, 0), (5, 7), (m.W[k].shape[0] - 1, m.W[k].shape[1] - 1)):
+            w0 = m.W[k][r, c]
+            m.W[k][r, c] = w0 + eps
+            lp, _ = Cv.mlp_loss_grad(m, x, y)
+            m.W[k][r, c] = w0 - eps
+            lm, _ = Cv.mlp_loss_grad(m, x, y)
+            m.W[k][r, c] = w0
+            fd = (lp - lm) / (2 * eps)
+            an = g[2 * k][r, c]
+            assert abs(fd - an) <= 1e-4 * max(abs(fd), abs(an), 1e-8), (k, r, c, fd, an)
+
+
+def test_mlp_train_overfit_determinism_and_zero_lr():
+    from paper_2507_23480_b200 import curve as Cv
+
+    c = np.concatenate([[np.inf], 2.0 / np.arange(1, 400) ** 0.6])
+    pair = Cv.mlp_pair(c)
+    m0 = Cv.MlpModel.init(np.random.default_rng(1))
+    l0, _ = Cv.mlp_loss_grad(m0, *pair)
+    m1, losses = Cv.mlp_train([pair], epochs=200, lr=0.01, rng=np.random.default_rng(1))
+    assert losses[-1] * 10 <= l0                                              # SPEC.md:284
+    m2, _ = Cv.mlp_train([pair], epochs=200, lr=0.01, rng=np.random.default_rng(1))
+    for a, b in zip(m1.W + m1.b, m2.W + m2.b):                                # SPEC.md:286
+        np.testing.assert_array_equal(a, b)
+    m3, _ = Cv.mlp_train([pair], epochs=3, lr=0.0, rng=np.random.default_rng(1))
+    for a, b in zip(m0.W + m0.b, m3.W + m3.b):                                # SPEC.md:285
+        np.testing.assert_array_equal(a, b)
+
+
+def test_estimate_mlp_matches_oracle_and_is_scale_equivariant():
+    from oracle import oracle as O
+    from paper_2507_23480_b200 import curve as Cv
+
+    m = Cv.MlpModel.init(np.random.default_rng(9))
+    prefix = np.concatenate([[np.inf], 3.0 / np.arange(1, 60) ** 0.5])
+    import tempfile
+    p = tempfile.mktemp()
+    m.save(p)
+    est = Cv.estimate_mlp(prefix, 600, m)
+    np.testing.assert_array_equal(est, O.estimate_mlp(prefix, 600, O.read_mlp(p)))
+    np.testing.assert_array_equal(est[:60], prefix)
+    assert np.all(np.diff(est[59:]) <= 0)
+    est2 = Cv.estimate_mlp(2 * prefix, 600, m)                                # SPEC.md:304
+    np.testing.assert_allclose(est2[60:], 2 * est[60:], rtol=1e-12)

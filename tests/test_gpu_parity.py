@@ -486,3 +486,38 @@ def test_c4_shape_fastpoint_matches_oracle():
     assert int(fp.reached[0].item()) == ref.reached
     oi, _, oc = O.rf_ball_query(ref.excl, 0.1, ref.indices, 32)
     np.testing.assert_array_equal(gc[0].cpu().numpy(), oc)
+
+
+# ---- MLP estimator --------------------------------------
+
+@pytest.mark.timeout(300)
+def test_mlp_estimator_thresholds_and_sampling_match_oracle():
+    """FastPoint with the MLP estimator: K2 evaluates resample -> 32-128-128-64
+    MLP -> resample -> running min on the device; radii and sampled indices
+    bit-identical to the oracle's estimate_mlp path (model trained briefly on
+    exact curves of the family, saved and reloaded in the SPEC.md:357 format)."""
+    import tempfile
+
+    from paper_2507_23480_b200 import curve as Cv
+
+    N, n = 6000, 1500
+    train = [O.fps(generate_cloud("room-surfaces", N, 500 + i), n)[1] for i in range(3)]
+    model, losses = Cv.mlp_train([Cv.mlp_pair(c) for c in train], epochs=20, lr=0.01,
+                                 rng=np.random.default_rng(3))
+    assert losses[-1] <= losses[0]
+    path = tempfile.mktemp(suffix=".mlp")
+    model.save(path)
+    model = Cv.MlpModel.load(path)
+    om = O.read_mlp(path)
+    B = 2
+    clouds = np.stack([generate_cloud("room-surfaces", N, 600 + b) for b in range(B)])
+    fp = engine.FastPoint(B, N, n, estimator="mlp", mlp=model, extra_radii=(0.1,))
+    fp.set_points(torch.from_numpy(clouds).cuda())
+    fp.set_rng([0, 1])
+    fp.sample()
+    fp.check()
+    for b in range(B):
+        ref = O.mdps(clouds[b], n, estimator="mlp", mlp=om, rng_seed=b, extra_radii=(0.1,))
+        np.testing.assert_array_equal(fp.R[b].cpu().numpy(), ref.thresholds, err_msg="segment radii")
+        np.testing.assert_array_equal(fp.out[b].cpu().numpy(), ref.indices)
+        np.testing.assert_array_equal(Cv.estimate_mlp(ref.est_curve[:fp.k0], n, model), ref.est_curve)
