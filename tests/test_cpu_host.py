@@ -211,3 +211,27 @@ def test_estimate_mlp_matches_oracle_and_is_scale_equivariant():
     assert np.all(np.diff(est[59:]) <= 0)
     est2 = Cv.estimate_mlp(2 * prefix, 600, m)
     np.testing.assert_allclose(est2[60:], 2 * est[60:], rtol=1e-12)
+
+
+def test_random_and_grid_samplers_spec_examples():
+    """SPEC.md:144-171 comparison samplers (host utilities)."""
+    from paper_2507_23480_b200 import baselines, core
+
+    cube = np.array([[x, y, z] for x in (0, 1) for y in (0, 1) for z in (0, 1)], np.float32)
+    assert len(baselines.grid_sample(cube, 2.0).indices) == 1                       # SPEC.md:159
+    assert sorted(baselines.grid_sample(cube, 0.5).indices.tolist()) == list(range(8))  # SPEC.md:160
+    two = np.array([[0, 0, 0], [0.1, 0, 0]], np.float32)
+    assert baselines.grid_sample(two, 1.0).indices.tolist() == [0]                  # SPEC.md:161
+    with pytest.raises(ValueError):
+        baselines.grid_sample(cube, 0.0)
+    c = np.random.default_rng(0).random((100, 3), dtype=np.float32)
+    r1 = baselines.random_sample(c, 10, core.Rng(5)).indices
+    r2 = baselines.random_sample(c, 10, core.Rng(5)).indices
+    assert r1.tolist() == r2.tolist() and len(set(r1.tolist())) == 10               # SPEC.md:151
+    assert sorted(baselines.random_sample(c, 100, core.Rng(1)).indices.tolist()) == list(range(100))
+    with pytest.raises(ValueError):
+        baselines.random_sample(c, 0, core.Rng(1))
+    u = np.random.default_rng(2).random((10000, 3), dtype=np.float32)
+    g = baselines.grid_sample_to_count(u, 2500, 0.05)                               # SPEC.md:169
+    assert 2375 <= len(g.indices) <= 2625
+    assert baselines.grid_sample_to_count(u[:1], 1).indices.tolist() == [0]
