@@ -37,14 +37,15 @@ namespace ps {
 namespace {
 
 constexpr uint64_t kGolden4 = 0x9E3779B97F4A7C15ull;
-constexpr int kT4 = 1024;
+constexpr int kT4 = 512;
 constexpr int kW4 = kT4 / 32;
-constexpr int kAdj4 = 32;
+constexpr int kAdj4 = 64;
 constexpr uint8_t kAdjOvf = 0xff;
-constexpr int kPred4 = 16;
+constexpr int kPred4 = 32;
 constexpr uint8_t kPredOvf = 0xff;
 constexpr uint8_t kUnd4 = 0, kIn4 = 1, kOut4 = 2;
 constexpr int kScr = 64;  // int32 scratch per cloud
+constexpr int kMaxC4 = 16;
 // scratch slots
 constexpr int kCnt0 = 0;    // [16] per-CTA available counts (pool)
 constexpr int kCnt1 = 16;   // [16] per-CTA accepted counts (truncation)
@@ -129,7 +130,7 @@ PS_DEV int bscan(int v, int* wt, int* total) {
     if (lane == 31) wt[warp] = x;
     __syncthreads();
     if (warp == 0) {
-        int s = wt[lane];
+        int s = lane < kW4 ? wt[lane] : 0;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int y = __shfl_up_sync(kFull, s, o);
@@ -162,6 +163,18 @@ PS_DEV uint4 ld_cluster_v4(uint32_t addr) {
     return v;
 }
 
+PS_DEV uint8_t ld_cluster_u8(uint32_t addr) {
+    uint16_t v;
+    asm volatile("ld.shared::cluster.u8 %0, [%1];" : "=h"(v) : "r"(addr) : "memory");
+    return (uint8_t)v;
+}
+PS_DEV void red_cluster_max(uint32_t addr, uint32_t v) {
+    asm volatile("red.shared::cluster.max.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+PS_DEV void st_cluster_s32(uint32_t addr, int v) {
+    asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
 // cluster barrier, or the block barrier when a cloud has a single CTA
 PS_DEV void sync_all(int C) {
     if (C == 1) __syncthreads();
@@ -174,7 +187,8 @@ PS_DEV void sync_all(int C) {
 // and gathered by every CTA.  Otherwise both are global arrays.
 template <bool kSm>
 __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
-    __shared__ int wt[kW4];
+    __shared__ int wt[32];
+    __shared__ int s_dec[2][kMaxC4];
     extern __shared__ __align__(16) uint8_t dsm4[];
     const int tid = threadIdx.x;
     const int C = (int)cluster_nctarank();
@@ -203,11 +217,13 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
     int32_t* s_cnt = wpos + span_sm;  // kSm: this visit's level counts of my range
     int32_t* s_list = s_cnt + span_sm;  // kSm: points of my range that need a row scan
     int64_t* s_ip = reinterpret_cast<int64_t*>(s_list + span_sm);  // kSm: their row offsets
-    int64_t i_tk = 0;  // sampled points already in tkb
+    uint8_t* st_s = reinterpret_cast<uint8_t*>(s_ip + span_sm);      // kSm: MIS states of my draw range
+    int64_t i_tk = 0;  // sampled points already pushed
+    int prev_seg = 0;  // segment of the previous visit (its accepts are pushed next)
     if (kSm) {
         for (int64_t x = tid; x < Wtk; x += kT4) tkb[x] = 0u;
         const int64_t span0 = ((N + C - 1) / C + 15) & ~(int64_t)15;
-        for (int64_t x = tid; x < span0; x += kT4) wpos[x] = 0x7fffffff;
+        for (int64_t x = tid; x < span0; x += kT4) wpos[x] = 0;  // blv: coverage level
         __syncthreads();
     }
     int32_t* adj = w.adj + b * N * kAdj4;
@@ -235,11 +251,14 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
     for (int64_t t = a.k0 + gt; t < a.n_total; t += GT) out[t] = -1;
     const bool tdbg = a.dbg && b == 0 && gt == 0;
     long long tl = tdbg ? clock64() : 0;
+    __shared__ long long s_acc[24];
+    if (tdbg)
+        for (int k = 0; k < 24; ++k) s_acc[k] = 0;
 #define VT4(k)                                             \
     do {                                                   \
         if (tdbg) {                                        \
             const long long n_ = clock64();                \
-            a.dbg[k] += n_ - tl;                           \
+            s_acc[k] += n_ - tl;                           \
             tl = n_;                                       \
         }                                                  \
     } while (0)
@@ -258,83 +277,79 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
         }
         if (gt == 0) scr[kDecided] = 0;
         if (kSm) {
-            // taken bitmap (smem, every CTA): add the points sampled since the last visit
-            for (int64_t x = i_tk + tid; x < i; x += kT4) {
-                const int32_t q = (int32_t)out[x];
-                atomicOr(&tkb[q >> 5], 1u << (q & 31));
-            }
-            i_tk = i;
-            __syncthreads();
             VT4(16);
-            // pull: my range's points are available iff untaken and no taken point
-            // in their level-s row prefix (lane groups, early exit on a hit)
-            const int lane = tid & 31, warp = tid >> 5, grp = lane / kG, gl = lane % kG;
-            const unsigned gmask = ((1u << kG) - 1u) << (grp * kG);
-            auto tkd = [&](int32_t q) { return q >= 0 && ((tkb[q >> 5] >> (q & 31)) & 1u); };
-            // this visit's level counts and row offsets of my range, staged once
+            // this visit's level counts and row offsets of my range, staged once (P2)
             for (int64_t x = tid; x < jhi - jlo; x += kT4) {
                 s_cnt[x] = cnt_lvl[jlo + x];
                 s_ip[x] = indptr[jlo + x];
             }
-            __syncthreads();
             VT4(17);
-            // points that need a row scan: untaken, no witness inside this prefix;
-            // the others are decided from shared memory alone
-            int nscan = 0;
-            for (int64_t base = jlo; base < jhi; base += kT4) {
-                const int64_t j = base + tid;
-                bool need = false;
-                if (j < jhi) {
-                    const bool tk = tkd((int32_t)j);
-                    const bool wit = wpos[j - jlo] < s_cnt[j - jlo];
-                    need = !tk && !wit && s_cnt[j - jlo] > 0;
-                    avail[j] = (!tk && !wit) ? 1 : 0;  // scanned points may still be cleared
+            // push: every point sampled since the last visit (the FPS prefix at the
+            // first visit, else the previous visit's accepts) walks its row prefix
+            // at the level of the segment it was sampled in; entry j at row
+            // position u lies within the radius of every segment s' with
+            // u < counts[s'][q] -- a prefix of segments since the radii do not
+            // increase -- so blv[j] = max(blv[j], #such s') in j's owner CTA
+            // (DSMEM red.max).  j is unavailable in segment s iff blv[j] > s.
+            const int lane = tid & 31, warp = tid >> 5, grp = lane / kG, gl = lane % kG;
+            const int s_from = i_tk == 0 ? 0 : prev_seg;
+            const uint32_t blv_base = smem_u32(wpos);
+            const uint32_t span32 = (uint32_t)span;
+            const uint32_t inv_span = 0xffffffffu / span32 + 1u;
+            auto owner_of = [&](uint32_t j) {
+                uint32_t ow = __umulhi(j, inv_span);
+                if (ow * span32 > j) --ow;
+                else if ((ow + 1u) * span32 <= j) ++ow;
+                return ow;
+            };
+            const int64_t nnew = i - i_tk;
+            for (int64_t kb = (int64_t)r * (kT4 / kG) + warp * (32 / kG); kb < nnew;
+                 kb += (int64_t)C * (kT4 / kG)) {
+                const int64_t k = kb + grp;
+                const bool valid = k < nnew;
+                int32_t q = 0, c = 0;
+                int32_t cs[kMaxSeg];
+#pragma unroll
+                for (int s2 = 0; s2 < kMaxSeg; ++s2) cs[s2] = 0;
+                const int32_t* row = nbr;
+                if (valid) {
+                    q = (int32_t)out[i_tk + k];
+                    for (int s2 = s_from; s2 < nseg; ++s2)
+                        cs[s2] = a.counts[(b * a.L + a.seg_level_rows[s2]) * N + q];
+                    c = cs[s_from];
+                    row = nbr + indptr[q];
+                    if (gl == 0) {
+                        const uint32_t ow = owner_of((uint32_t)q);
+                        red_cluster_max(mapa(blv_base + 4u * ((uint32_t)q - ow * span32), ow), (uint32_t)nseg);
+                    }
                 }
-                int tot;
-                const int ex = bscan(need ? 1 : 0, wt, &tot);
-                if (need) s_list[nscan + ex] = (int32_t)(j - jlo);
-                nscan += tot;
-            }
-            for (int kb = warp * (32 / kG); kb < nscan; kb += kW4 * (32 / kG)) {
-                const int k = kb + grp;
-                const bool valid = k < nscan;
-                const int32_t lj = valid ? s_list[k] : 0;
-                const int32_t c = valid ? s_cnt[lj] : 0;
-                const int32_t* row = nbr + (valid ? s_ip[lj] : 0);
                 const bool al = (reinterpret_cast<uintptr_t>(row) & 15u) == 0;
-                bool av = valid;
-                // rounds of kPull entries per group: all loads of a round in flight together
-                constexpr int kPull = 4 * kGStep;
-                for (int32_t u0 = 0;; u0 += kPull) {
-                    const bool act = av && u0 < c;
+                constexpr int kPush = 4 * kGStep;
+                for (int32_t u0 = 0;; u0 += kPush) {
+                    const bool act = valid && u0 < c;
                     if (!__any_sync(kFull, act)) break;
-                    int hu = 0x7fffffff;  // lowest hit position of this lane
-                    if (act) {
-                        int4 v[4];
+                    if (!act) continue;
 #pragma unroll
-                        for (int q4 = 0; q4 < 4; ++q4) v[q4] = grp_load4(row, u0 + q4 * kGStep + 4 * gl, c, al);
+                    for (int q4 = 0; q4 < 4; ++q4) {
+                        const int32_t u = u0 + q4 * kGStep + 4 * gl;
+                        const int4 v = grp_load4(row, u, c, al);
+                        const int32_t jv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-                        for (int q4 = 3; q4 >= 0; --q4) {
-                            const int32_t u = u0 + q4 * kGStep + 4 * gl;
-                            hu = tkd(v[q4].w) ? u + 3 : hu;
-                            hu = tkd(v[q4].z) ? u + 2 : hu;
-                            hu = tkd(v[q4].y) ? u + 1 : hu;
-                            hu = tkd(v[q4].x) ? u : hu;
+                        for (int e = 0; e < 4; ++e) {
+                            const int32_t j = jv[e];
+                            if (j < 0) continue;
+                            uint32_t cov = 0;
+#pragma unroll
+                            for (int s2 = 0; s2 < kMaxSeg; ++s2) cov += (s2 >= s_from && s2 < nseg && u + e < cs[s2]) ? 1u : 0u;
+                            cov += (uint32_t)s_from;  // segments before s_from are past
+                            const uint32_t ow = owner_of((uint32_t)j);
+                            red_cluster_max(mapa(blv_base + 4u * ((uint32_t)j - ow * span32), ow), cov);
                         }
                     }
-                    // lowest hit position of the group (all lanes take part in the shuffles)
-                    int mu = hu;
-#pragma unroll
-                    for (int o = 1; o < kG; o <<= 1) mu = min(mu, __shfl_xor_sync(kFull, mu, o));
-                    if (mu != 0x7fffffff) {
-                        av = false;
-                        if (gl == 0) wpos[lj] = mu;
-                    }
                 }
-                if (valid && !av && gl == 0) avail[jlo + lj] = 0;
             }
+            i_tk = i;
         }
-        VT4(18);
         sync_all(C);
         VT4(13);
         if (!kSm) {
@@ -358,6 +373,8 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
         }
         sync_all(C);
         if (kSm) {
+            for (int64_t j = jlo + tid; j < jhi; j += kT4) avail[j] = (uint32_t)wpos[j - jlo] <= (uint32_t)seg ? 1 : 0;
+            sync_all(C);
             const uint32_t avail_base = smem_u32(avail);
             // gather the other owners' ranges into my copy of the map
             for (int64_t c16 = tid; c16 < Npad / 16; c16 += kT4) {
@@ -462,7 +479,7 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
         }
         sync_all(C);
         VT4(2);
-        if (tdbg) { a.dbg[10] += 1; a.dbg[11] += L; }
+        if (tdbg) { s_acc[10] += 1; s_acc[11] += L; }
 
         // ---- P3: candidate order of all L draws ----------------------------------------
         if (a.pick_lowest) {
@@ -470,7 +487,6 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
                 const int32_t c = pool[t];
                 cand[t] = c;
                 if (!kSm) rank[c] = t;
-                stt[t] = kUnd4;
             }
         } else {
             for (int t = gt; t < L; t += GT) {
@@ -509,8 +525,14 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
                 }
                 cand[t] = c;
                 if (!kSm) rank[c] = t;
-                stt[t] = kUnd4;
             }
+        }
+        // MIS states: CTA r owns the draws [tlo, thi) (also the truncation ranges)
+        const int tspan = (L + C - 1) / C;
+        const int tlo = min(L, r * tspan), thi = min(L, tlo + tspan);
+        for (int t = tlo + tid; t < thi; t += kT4) {
+            if (kSm) st_s[t - tlo] = kUnd4;
+            else stt[t] = kUnd4;
         }
         sync_all(C);
         if (kSm) {
@@ -520,9 +542,43 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
 
         VT4(5);
         // ---- P4: greedy MIS in draw order, parallel rounds ------------------------------
+        // state of draw q: my range -> local shared memory, a peer's -> DSMEM
+        // (kSm); global otherwise.  Reads may be stale within a round (IN/OUT
+        // are final, a stale UND only delays); the cluster barrier publishes.
+        const uint32_t st_base = kSm ? smem_u32(st_s) : 0u;
+        const uint32_t tspan32 = (uint32_t)max(tspan, 1);
+        const uint32_t inv_tspan = 0xffffffffu / tspan32 + 1u;
+        auto st_get = [&](int q) -> uint8_t {
+            if (!kSm) return ld_st(stt + q);
+            // owner = q / tspan by multiply-high (+-1 fix), read through the
+            // cluster window for every owner (no branch: independent loads pipeline)
+            uint32_t ow = __umulhi((uint32_t)q, inv_tspan);
+            ow -= (ow * tspan32 > (uint32_t)q) ? 1u : 0u;
+            ow += ((ow + 1u) * tspan32 <= (uint32_t)q) ? 1u : 0u;
+            const uint32_t lq = (uint32_t)q - ow * tspan32;
+            return ld_cluster_u8(mapa(st_base + lq, ow));
+        };
+        auto st_set = [&](int t, uint8_t v) {
+            if (kSm) *reinterpret_cast<volatile uint8_t*>(st_s + (t - tlo)) = v;
+            else st_st(stt + t, v);
+        };
+        // decided count: every CTA's cumulative count pushed into every CTA's
+        // shared slot (double-buffered by round parity), summed after the barrier
+        const uint32_t dec_base = smem_u32(&s_dec[0][0]);
+        int my_dec = 0, round = 0;
+        auto publish = [&](int add) {
+            add = bsum(add, wt);
+            my_dec += add;
+            if (tid < C) st_cluster_s32(mapa(dec_base + (uint32_t)(((round & 1) * kMaxC4 + r) * 4), (uint32_t)tid),
+                                         my_dec);
+            sync_all(C);
+            int tot = 0;
+            for (int q = 0; q < C; ++q) tot += s_dec[round & 1][q];
+            ++round;
+            return tot;
+        };
         int decided = 0;
-        for (int t = gt; t < L; t += GT) {
-            const int32_t c = cand[t];
+        for (int t = tlo + tid; t < thi; t += kT4) {            const int32_t c = cand[t];
             const uint8_t nc = adjcnt[c];
             bool outf = false, blocked = false;
             int np = 0;
@@ -542,7 +598,7 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
                     for (int u = 0; u < 16; ++u) rq[u] = h + u < nc ? rank[q[u]] : 0x7fffffff;
                     uint8_t sq[16];
 #pragma unroll
-                    for (int u = 0; u < 16; ++u) sq[u] = rq[u] < t ? ld_st(stt + rq[u]) : kOut4;
+                    for (int u = 0; u < 16; ++u) sq[u] = rq[u] < t ? st_get(rq[u]) : kOut4;
 #pragma unroll
                     for (int u = 0; u < 16; ++u) {
                         if (sq[u] == kIn4) outf = true;
@@ -568,7 +624,7 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
                     for (int k = 0; k < kRB; ++k) rq[k] = av[k] ? rank[qq[k]] : 0x7fffffff;
                     uint8_t sq[kRB];
 #pragma unroll
-                    for (int k = 0; k < kRB; ++k) sq[k] = rq[k] < t ? ld_st(stt + rq[k]) : kOut4;
+                    for (int k = 0; k < kRB; ++k) sq[k] = rq[k] < t ? st_get(rq[k]) : kOut4;
 #pragma unroll
                     for (int k = 0; k < kRB; ++k) {
                         if (sq[k] == kIn4) outf = true;
@@ -581,37 +637,38 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
                 }
             }
             if (outf) {
-                st_st(stt + t, kOut4);
+                st_set(t, kOut4);
                 ++decided;
             } else if (!blocked) {
-                st_st(stt + t, kIn4);
+                st_set(t, kIn4);
                 ++decided;
             } else {
                 npred[t] = np > kPred4 ? kPredOvf : (uint8_t)np;
             }
         }
-        decided = bsum(decided, wt);
-        if (tid == 0 && decided) atomicAdd(&scr[kDecided], decided);
-        sync_all(C);
+        VT4(19);
+        int total_dec = publish(decided);
         VT4(6);
-        while (scr[kDecided] < L) {
-            if (tdbg) a.dbg[12] += 1;
+        while (total_dec < L) {
+            if (tdbg) s_acc[12] += 1;
             int dd = 0;
-            for (int t = gt; t < L; t += GT) {
-                if (ld_st(stt + t) != kUnd4) continue;
+            for (int t = tlo + tid; t < thi; t += kT4) {
+                if (st_get(t) != kUnd4) continue;
                 bool outf = false, blocked = false;
                 const uint8_t np = npred[t];
                 if (np != kPredOvf) {
-                    int pr[kPred4];
+                    for (int k0p = 0; k0p < np && !outf; k0p += 16) {
+                        int pr[16];
 #pragma unroll
-                    for (int k = 0; k < kPred4; ++k) pr[k] = k < np ? preds[(int64_t)t * kPred4 + k] : -1;
-                    uint8_t sq[kPred4];
+                        for (int k = 0; k < 16; ++k) pr[k] = k0p + k < np ? preds[(int64_t)t * kPred4 + k0p + k] : -1;
+                        uint8_t sq[16];
 #pragma unroll
-                    for (int k = 0; k < kPred4; ++k) sq[k] = pr[k] >= 0 ? ld_st(stt + pr[k]) : kOut4;
+                        for (int k = 0; k < 16; ++k) sq[k] = pr[k] >= 0 ? st_get(pr[k]) : kOut4;
 #pragma unroll
-                    for (int k = 0; k < kPred4; ++k) {
-                        outf = outf || sq[k] == kIn4;
-                        blocked = blocked || sq[k] == kUnd4;
+                        for (int k = 0; k < 16; ++k) {
+                            outf = outf || sq[k] == kIn4;
+                            blocked = blocked || sq[k] == kUnd4;
+                        }
                     }
                 } else {
                     if (a.dbg && b == 0) atomicAdd((unsigned long long*)&a.dbg[15], 1ull);
@@ -633,7 +690,7 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
                         for (int k = 0; k < kRB; ++k) rq[k] = av[k] ? rank[qq[k]] : 0x7fffffff;
                         uint8_t sq[kRB];
 #pragma unroll
-                        for (int k = 0; k < kRB; ++k) sq[k] = rq[k] < t ? ld_st(stt + rq[k]) : kOut4;
+                        for (int k = 0; k < kRB; ++k) sq[k] = rq[k] < t ? st_get(rq[k]) : kOut4;
 #pragma unroll
                         for (int k = 0; k < kRB; ++k) {
                             outf = outf || sq[k] == kIn4;
@@ -642,25 +699,22 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
                     }
                 }
                 if (outf) {
-                    st_st(stt + t, kOut4);
+                    st_set(t, kOut4);
                     ++dd;
                 } else if (!blocked) {
-                    st_st(stt + t, kIn4);
+                    st_set(t, kIn4);
                     ++dd;
                 }
             }
-            dd = bsum(dd, wt);
-            if (tid == 0 && dd) atomicAdd(&scr[kDecided], dd);
-            sync_all(C);
+            VT4(20);
+            total_dec = publish(dd);
         }
 
         VT4(7);
         // ---- P5: truncation at the segment boundary --------------------------------------
         const int64_t need = a.boundaries[seg] - i;
-        const int tspan = (L + C - 1) / C;
-        const int tlo = min(L, r * tspan), thi = min(L, tlo + tspan);
         int nin = 0;
-        for (int t = tlo + tid; t < thi; t += kT4) nin += stt[t] == kIn4 ? 1 : 0;
+        for (int t = tlo + tid; t < thi; t += kT4) nin += st_get(t) == kIn4 ? 1 : 0;
         nin = bsum(nin, wt);
         if (tid == 0) scr[kCnt1 + r] = nin;
         sync_all(C);
@@ -674,7 +728,7 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
         const bool ends = take == need;
         for (int base = tlo; base < thi; base += kT4) {
             const int t = base + tid;
-            const int f = (t < thi && stt[t] == kIn4) ? 1 : 0;
+            const int f = (t < thi && st_get(t) == kIn4) ? 1 : 0;
             int tot;
             const int ex = bscan(f, wt, &tot);
             const int64_t k = aoff + ex;
@@ -687,6 +741,7 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
         sync_all(C);
         VT4(8);
         const int last = ends ? scr[kLast] : -1;
+        prev_seg = seg;
         i += take;
         if (ends) {
             if (!a.pick_lowest) rng = rng + (uint64_t)(last + 1) * kGolden4;
@@ -714,6 +769,8 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
         // ordered after this visit's reads of scr by its cluster barrier
     }
 #undef VT4
+    if (tdbg)
+        for (int k = 0; k < 24; ++k) a.dbg[k] += s_acc[k];
     if (r == 0 && tid == 0) {
         a.reached[b] = i;
         a.exhausted[b] = exhausted;
@@ -772,7 +829,7 @@ cudaError_t launch_sampler_v4(SampArgs a, int64_t B, cudaStream_t s) {
     cudaError_t e = cudaSuccess;
     const int64_t Npad = (N + 15) & ~(int64_t)15;
     const int64_t span0 = ((N + C - 1) / C + 15) & ~(int64_t)15;
-    const size_t dsm = (size_t)(Npad + 4 * Npad + 4 * (((N + 31) / 32 + 3) & ~(int64_t)3) + 20 * span0);
+    const size_t dsm = (size_t)(Npad + 4 * Npad + 4 * (((N + 31) / 32 + 3) & ~(int64_t)3) + 21 * span0);
     const bool sm = dsm <= 200 * 1024 && !getenv("PS_SAMPLER_GLOBAL");
     auto kern = sm ? samp4_kernel<true> : samp4_kernel<false>;
     if (sm) {
@@ -806,8 +863,10 @@ cudaError_t launch_sampler_v4(SampArgs a, int64_t B, cudaStream_t s) {
             long long h2[32];
             cudaMemcpyAsync(h2, dbg, sizeof(h2), cudaMemcpyDeviceToHost, s);
             cudaStreamSynchronize(s);
-            fprintf(stderr, "[sampler v4] P1: head init + taken bits %lld, stage counts %lld, pull %lld, barrier %lld; "
-                    "adjacency overflows %lld, pred overflows %lld\n", h2[16], h2[17], h2[18], h2[13], h2[14], h2[15]);
+            fprintf(stderr, "[sampler v4] P1 %lld (taken bits %lld, stage %lld, pull %lld) | mis0 own %lld + publish %lld | "
+                    "rounds own %lld + publish %lld | overflows adj %lld pred %lld\n",
+                    h2[13] + h2[16] + h2[17] + h2[18], h2[16], h2[17], h2[18], h2[19], h2[6], h2[20], h2[7],
+                    h2[14], h2[15]);
         }
         long long h[16];
         cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, s);
