@@ -199,6 +199,34 @@ __global__ void et_mark_kernel(EtArgs a) {
     }
 }
 
+// Push form of the early-termination seeding: every sampled point q walks its
+// own level-1 row prefix and lowers md[j] to d2(q, j) for each entry j.  By
+// the symmetry of the rows (j in row_1(q) <=> q in row_1(j), same d2), this is
+// exactly earlyterm_scan's min over taken row entries of every point, but reads
+// only the sampled points' rows (reached of N).  md >= 0, so the min is an
+// unsigned atomicMin on the bit patterns (order-independent, exact).
+// Lane groups of 8 per row.
+__global__ void et_push_kernel(EtArgs a) {
+    const int gl = threadIdx.x & 7;
+    const int64_t total = a.B * a.n_total;
+    const int64_t ng = ((int64_t)gridDim.x * blockDim.x) >> 3;
+    for (int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3; g < total; g += ng) {
+        const int64_t b = g / a.n_total, t = g - b * a.n_total;
+        if (a.reached[b] >= a.n_total || t >= a.reached[b]) continue;
+        const int64_t q = a.out_idx[b * a.ld_out + t];
+        const int64_t base = a.indptr[b * (a.N + 1) + q];
+        const int32_t c = a.lvl1_counts[b * a.counts_stride + q];
+        const int32_t* nbr = a.nbr + b * a.cap_entries + base;
+        const double* d2 = a.d2 + b * a.cap_entries + base;
+        unsigned long long* md = reinterpret_cast<unsigned long long*>(a.md + b * a.N);
+        for (int32_t u = gl; u < c; u += 8) {
+            const int32_t j = __ldg(nbr + u);
+            const double d = __ldg(d2 + u);
+            atomicMin(md + j, (unsigned long long)__double_as_longlong(d));
+        }
+    }
+}
+
 }  // namespace
 
 // md[i] = min(md[i], min over the first lvl1[i] row entries j with taken[j] of d2)
@@ -248,6 +276,11 @@ cudaError_t launch_et(const EtArgs& a, cudaStream_t s) {
     et_prepare_kernel<<<g1, 256, 0, s>>>(a);
     const unsigned g2 = (unsigned)std::min<int64_t>(148 * 8, (a.B * a.n_total + 255) / 256 + 1);
     et_mark_kernel<<<g2, 256, 0, s>>>(a);
+    if (!getenv("PS_ET_PULL")) {
+        const unsigned g3 = (unsigned)std::min<int64_t>(148 * 16, (a.B * a.n_total + 31) / 32 + 1);
+        et_push_kernel<<<g3, 256, 0, s>>>(a);
+        return cudaGetLastError();
+    }
     EtScanArgs sa;
     sa.indptr = a.indptr; sa.nbr = a.nbr; sa.d2 = a.d2; sa.cap_entries = a.cap_entries;
     sa.lvl1_counts = a.lvl1_counts; sa.counts_stride = a.counts_stride;
