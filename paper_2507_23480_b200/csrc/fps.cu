@@ -37,6 +37,10 @@ namespace {
 
 
 constexpr int kMaxCluster = 16;
+#ifndef PS_TIMING
+#define PS_TIMING 0
+#endif
+constexpr bool kTiming = PS_TIMING;  // per-iteration cycle stamps (make TIMING=1)
 constexpr uint32_t kNone = 0xffffffffu;
 
 struct __align__(16) Rec {
@@ -124,8 +128,9 @@ __global__ void __launch_bounds__(T, 1) fps_cluster_kernel(FpsArgs a) {
     float fx[PP], fy[PP], fz[PP], thr[PP];
     double m[PP];
     uint32_t tk = 0, valid = 0;
-    double bv = -1.0;  // cached thread-local max md (P > 0) and its slot
+    double bv = -1.0;  // cached thread-local max md (P > 0), its slot and coordinates
     int bq = 0;
+    float bx = 0.f, by = 0.f, bz = 0.f;
     if constexpr (P > 0) {
 #pragma unroll
         for (int q = 0; q < P; ++q) {
@@ -174,13 +179,17 @@ __global__ void __launch_bounds__(T, 1) fps_cluster_kernel(FpsArgs a) {
         const float4 lv = xyz[last];
         float sx32 = lv.x, sy32 = lv.y, sz32 = lv.z;
         bool dirty = true;  // recompute the cached local max
+        // exchange addresses of this lane's destination CTA (leader warp, lane < C)
+        const uint32_t dl = (uint32_t)lane < C ? (uint32_t)lane : 0u;
+        const uint32_t dst0 = mapa(smem_u32(&slots[0][r]), dl), dst1 = mapa(smem_u32(&slots[1][r]), dl);
+        const uint32_t dbar0 = mapa(smem_u32(&bars[0]), dl), dbar1 = mapa(smem_u32(&bars[1]), dl);
 
         for (int64_t it = k_start; it < k_stop; ++it) {
             const uint32_t t_abs = (uint32_t)(it - k_start);
             const uint32_t par = t_abs & 1u;
             const uint32_t phase = (t_abs >> 1) & 1u;
             const uint32_t t = t_abs - (uint32_t)a.dbg_t0;
-            const bool tdbg = a.dbg && b == 0 && r == 0 && tid == 0 && t_abs >= a.dbg_t0 && t < 256;
+            const bool tdbg = kTiming && a.dbg && b == 0 && r == 0 && tid == 0 && t_abs >= a.dbg_t0 && t < 256;
             long long ts0 = 0;
             if (tdbg) ts0 = clock64();
             const double sx = sx32, sy = sy32, sz = sz32;
@@ -230,7 +239,13 @@ __global__ void __launch_bounds__(T, 1) fps_cluster_kernel(FpsArgs a) {
                         for (int q = 0; q + st < P; q += 2 * st)
                             if (tv[q + st] > tv[q]) { tv[q] = tv[q + st]; ti[q] = ti[q + st]; }
                     }
-                    if (dirty) { bv = tv[0]; bq = ti[0]; }
+                    if (dirty) {
+                        bv = tv[0];
+                        bq = ti[0];
+#pragma unroll
+                        for (int q = 0; q < P; ++q)
+                            if (q == bq) { bx = fx[q]; by = fy[q]; bz = fz[q]; }
+                    }
                     dirty = false;
                 }
                 if (bv >= 0.0) {
@@ -258,9 +273,7 @@ __global__ void __launch_bounds__(T, 1) fps_cluster_kernel(FpsArgs a) {
                 if (lane == 0) { Rec z{}; z.idx = kNone; warp_rec[warp] = z; }
             } else if (lane == wl) {
                 if constexpr (P > 0) {
-#pragma unroll
-                    for (int q = 0; q < P; ++q)
-                        if (q == bq) { mine.x = fx[q]; mine.y = fy[q]; mine.z = fz[q]; }
+                    mine.x = bx; mine.y = by; mine.z = bz;
                     mine.taken = (tk >> bq) & 1u;
                 } else {
                     mine.taken = taken[bidx];
@@ -297,8 +310,8 @@ __global__ void __launch_bounds__(T, 1) fps_cluster_kernel(FpsArgs a) {
                 const int cl = warp_argmax_lane(rec_key(wr), wr.idx);
                 const Rec cr = warp_rec[cl < 0 ? 0 : cl];
                 if (lane < (int)C) {
-                    const uint32_t dst = mapa(smem_u32(&slots[par][r]), lane);
-                    const uint32_t dbar = mapa(smem_u32(&bars[par]), lane);
+                    const uint32_t dst = par ? dst1 : dst0;
+                    const uint32_t dbar = par ? dbar1 : dbar0;
                     st_async_v4(dst, dbar, cr.klo, cr.khi, cl < 0 ? kNone : cr.idx, cr.taken);
                     st_async_v4(dst + 16, dbar, __float_as_uint(cr.x), __float_as_uint(cr.y),
                                 __float_as_uint(cr.z), 0u);
@@ -568,7 +581,7 @@ cudaError_t launch_fps_legacy(FpsArgs a, int64_t B, cudaStream_t s) {
     fps_choose_cluster(a.N, B, &C, &P, &T);
     a.points_per_cta = (a.N + C - 1) / C;
     a.dbg = nullptr;
-    if (getenv("PS_FPS_TIMING")) {
+    if (kTiming && getenv("PS_FPS_TIMING")) {
         // development aid: per-phase SM cycles of the first 256 iterations
         // (cloud 0, CTA rank 0, thread 0) printed to stderr; synchronises.
         static long long* dbg = nullptr;

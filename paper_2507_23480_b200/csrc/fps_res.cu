@@ -54,6 +54,10 @@ constexpr int kMaxC = 16;
 constexpr int kBins = 4096;  // 16^3 Morton cells per CTA bounding box
 constexpr uint32_t kNone = 0xffffffffu;
 constexpr int kMaxP = 24;
+#ifndef PS_TIMING
+#define PS_TIMING 0
+#endif
+constexpr bool kTiming = PS_TIMING;  // per-iteration cycle stamps (make TIMING=1)
 constexpr uint32_t kForeign = 0x7fffffffu;  // owner field of another rank's point (g field all ones)
 
 struct __align__(16) Rec {
@@ -389,7 +393,7 @@ __global__ void __launch_bounds__(kT, 1) fps_res_kernel(FpsArgs a, FpsRanks rk) 
             const uint32_t par = t_abs & 1u;
             const uint32_t phase = (t_abs >> 1) & 1u;
             const uint32_t t = t_abs - (uint32_t)a.dbg_t0;
-            const bool tdbg = a.dbg && b == 0 && r == 0 && tid == kT - 32 && t_abs >= a.dbg_t0 && t < 256 && g == 0;
+            const bool tdbg = kTiming && a.dbg && b == 0 && r == 0 && tid == kT - 32 && t_abs >= a.dbg_t0 && t < 256 && g == 0;
             long long ts0 = 0;
             if (tdbg) ts0 = clock64();
 
@@ -754,7 +758,7 @@ cudaError_t launch_fps_res(FpsArgs a, const FpsRanks& rk_in, int64_t B, int C, i
     const int64_t Ns = (a.N + rk.G - 1) / rk.G;
     a.points_per_cta = (Ns + C - 1) / C;
     const int64_t nclusters = B * rk.Gl;
-    if (getenv("PS_FPS_TIMING")) {
+    if (kTiming && getenv("PS_FPS_TIMING")) {
         // development aid: per-phase SM cycles of the first 256 iterations
         // (cloud 0, rank 0, CTA 0, thread 0) printed to stderr; synchronises.
         static long long* dbg = nullptr;
