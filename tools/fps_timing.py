@@ -1,4 +1,5 @@
-"""Per-phase cycle breakdown of the cluster FPS iteration (PS_FPS_TIMING=1).
+"""Per-phase cycle breakdown of the cluster FPS iteration (PS_FPS_TIMING=1; needs
+a library built with `make -C paper_2507_23480_b200/csrc TIMING=1`).
 
   python tools/fps_timing.py [N B n] ...   (env PS_FPS_CLUSTER / PS_FPS_THREADS honoured)
 """
