@@ -151,9 +151,6 @@ PS_DEV int bsum(int v, int* wt) {
     return tot;
 }
 
-PS_DEV void st_cluster_u8(uint32_t addr, uint8_t v) {
-    asm volatile("st.shared::cluster.u8 [%0], %1;" ::"r"(addr), "h"((uint16_t)v) : "memory");
-}
 PS_DEV uint4 ld_cluster_v4(uint32_t addr) {
     uint4 v;
     asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];"
@@ -428,7 +425,6 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
             off += c2 < r ? v : 0;
             L += v;
         }
-        const int off0 = off;
         for (int64_t base = jlo; base < jhi; base += kT4) {
             const int64_t j = base + tid;
             const int f = (j < jhi && avail[j]) ? 1 : 0;
@@ -436,46 +432,6 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
             const int ex = bscan(f, wt, &tot);
             if (f) pool[off + ex] = (int32_t)j;
             off += tot;
-        }
-        if (kSm) {
-            // compressed adjacency of my range's available points (lane groups)
-            __syncthreads();
-            const int lane = tid & 31, warp = tid >> 5, grp = lane / kG, gl = lane % kG;
-            const unsigned gmask = ((1u << kG) - 1u) << (grp * kG);
-            const unsigned below = gmask & ((1u << lane) - 1u);
-            for (int kb = warp * (32 / kG); kb < mycnt; kb += kW4 * (32 / kG)) {
-                const int k = kb + grp;
-                const bool valid = k < mycnt;
-                int32_t j = 0, c = 0;
-                const int32_t* row = nbr;
-                if (valid) {
-                    j = pool[off0 + k];
-                    c = s_cnt[j - jlo];
-                    row = nbr + s_ip[j - jlo];
-                }
-                const bool al = (reinterpret_cast<uintptr_t>(row) & 15u) == 0;
-                int32_t* ao = adj + (int64_t)j * kAdj4;
-                int n = 0;
-                for (int32_t u0 = 0;; u0 += kGStep) {
-                    const bool act = valid && u0 < c;
-                    if (!__any_sync(kFull, act)) break;
-                    int4 v = make_int4(-1, -1, -1, -1);
-                    if (act) v = grp_load4(row, u0 + 4 * gl, c, al);
-                    const int32_t qv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int32_t q = qv[e];
-                        const bool h = q >= 0 && q != j && avail[q];
-                        const unsigned m = __ballot_sync(kFull, h) & gmask;
-                        if (h) {
-                            const int ps = n + __popc(m & below);
-                            if (ps < kAdj4) ao[ps] = q;
-                        }
-                        n += __popc(m);
-                    }
-                }
-                if (valid && gl == 0) adjcnt[j] = n > kAdj4 ? kAdjOvf : (uint8_t)n;
-            }
         }
         sync_all(C);
         VT4(2);
@@ -578,8 +534,11 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
             return tot;
         };
         int decided = 0;
-        for (int t = tlo + tid; t < thi; t += kT4) {            const int32_t c = cand[t];
-            const uint8_t nc = adjcnt[c];
+        for (int t = tlo + tid; t < thi; t += kT4) {
+            const int32_t c = cand[t];
+            // kSm: no adjacency lists -- the candidate scans its own row prefix
+            // (availability and ranks in shared memory, states through DSMEM)
+            const uint8_t nc = kSm ? kAdjOvf : adjcnt[c];
             bool outf = false, blocked = false;
             int np = 0;
             if (nc != kAdjOvf) {
@@ -610,23 +569,29 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
                     }
                 }
             } else {
-                if (a.dbg && b == 0) atomicAdd((unsigned long long*)&a.dbg[14], 1ull);
+                if (!kSm && a.dbg && b == 0) atomicAdd((unsigned long long*)&a.dbg[14], 1ull);
                 const int32_t m = cnt_lvl[c];
                 const int32_t* row = nbr + indptr[c];
-                for (int32_t u0 = 0; u0 < m && !outf; u0 += kRB) {
-                    int32_t qq[kRB];
-                    row_batch(row, u0, m, qq);
-                    uint8_t av[kRB];
+                const bool al = (reinterpret_cast<uintptr_t>(row) & 15u) == 0;
+                constexpr int kRow = 16;
+                for (int32_t u0 = 0; u0 < m && !outf; u0 += kRow) {
+                    int32_t qq[kRow];
 #pragma unroll
-                    for (int k = 0; k < kRB; ++k) av[k] = (qq[k] >= 0 && qq[k] != c) ? avail[qq[k]] : 0;
-                    int rq[kRB];
+                    for (int k4 = 0; k4 < kRow / 4; ++k4) {
+                        const int4 v = grp_load4(row, u0 + 4 * k4, m, al);
+                        qq[4 * k4] = v.x; qq[4 * k4 + 1] = v.y; qq[4 * k4 + 2] = v.z; qq[4 * k4 + 3] = v.w;
+                    }
+                    uint8_t av[kRow];
 #pragma unroll
-                    for (int k = 0; k < kRB; ++k) rq[k] = av[k] ? rank[qq[k]] : 0x7fffffff;
-                    uint8_t sq[kRB];
+                    for (int k = 0; k < kRow; ++k) av[k] = (qq[k] >= 0 && qq[k] != c) ? avail[qq[k]] : 0;
+                    int rq[kRow];
 #pragma unroll
-                    for (int k = 0; k < kRB; ++k) sq[k] = rq[k] < t ? st_get(rq[k]) : kOut4;
+                    for (int k = 0; k < kRow; ++k) rq[k] = av[k] ? rank[qq[k]] : 0x7fffffff;
+                    uint8_t sq[kRow];
 #pragma unroll
-                    for (int k = 0; k < kRB; ++k) {
+                    for (int k = 0; k < kRow; ++k) sq[k] = rq[k] < t ? st_get(rq[k]) : kOut4;
+#pragma unroll
+                    for (int k = 0; k < kRow; ++k) {
                         if (sq[k] == kIn4) outf = true;
                         if (rq[k] < t && sq[k] == kUnd4) {
                             if (np < kPred4) preds[(int64_t)t * kPred4 + np] = rq[k];
@@ -674,7 +639,7 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
                     if (a.dbg && b == 0) atomicAdd((unsigned long long*)&a.dbg[15], 1ull);
                     // more than kPred4 undecided predecessors: rescan the neighbours
                     const int32_t c = cand[t];
-                    const uint8_t nc = adjcnt[c];
+                    const uint8_t nc = kSm ? kAdjOvf : adjcnt[c];
                     const int32_t m = nc != kAdjOvf ? (int32_t)nc : cnt_lvl[c];
                     const int32_t* row = nc != kAdjOvf ? adj + (int64_t)c * kAdj4 : nbr + indptr[c];
                     for (int32_t u0 = 0; u0 < m && !outf; u0 += kRB) {
