@@ -705,6 +705,8 @@ __global__ void __launch_bounds__(kEllWarps * 32, 4) grid_ell_kernel(int64_t B, 
     __shared__ uint8_t hk[kEllWarps][kEllCap];   // bucket
     __shared__ int hcnt[kEllWarps][33];          // per-bucket counts
     __shared__ double lvs[kEllWarps][32];
+    __shared__ unsigned long long lvb[kEllWarps][32];
+    __shared__ int tbase[kEllWarps][9];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
     for (int64_t gs = (int64_t)blockIdx.x * kEllWarps + warp; gs < B * N; gs += (int64_t)gridDim.x * kEllWarps) {
@@ -712,7 +714,10 @@ __global__ void __launch_bounds__(kEllWarps * 32, 4) grid_ell_kernel(int64_t B, 
         // level values of this cloud: lane l < L holds r2_l and its rank_lt
         const double my_r2 = lane < L ? r2_levels[b * levels_ld + lane] : 0.0;
         __syncwarp();
-        if (lane < L) lvs[warp][lane] = my_r2;
+        if (lane < L) {
+            lvs[warp][lane] = my_r2;
+            lvb[warp][lane] = (unsigned long long)__double_as_longlong(my_r2);
+        }
         hcnt[warp][lane] = 0;
         if (lane == 0) hcnt[warp][32] = 0;
         __syncwarp();
@@ -752,14 +757,21 @@ __global__ void __launch_bounds__(kEllWarps * 32, 4) grid_ell_kernel(int64_t B, 
         }
         const int total = __shfl_sync(kFull, incl, 8);
         const int excl0 = incl - rlen;
+        // range of flattened candidate f: #(later range starts <= f), from registers;
+        // sorted position = base[range] + f (per-warp table)
+        if (lane < 9) tbase[warp][lane] = r0 - excl0;
+        int e[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) e[q] = __shfl_sync(kFull, excl0, q + 1);
+        __syncwarp();
         int cnt = 0;
 #pragma unroll 2
         for (int tb = 0; tb < total; tb += 32) {
             const int f = tb + lane;
             int rr = 0;
 #pragma unroll
-            for (int q = 1; q < 9; ++q) rr += (f >= __shfl_sync(kFull, excl0, q)) ? 1 : 0;
-            const int t = __shfl_sync(kFull, r0, rr) - __shfl_sync(kFull, excl0, rr) + f;
+            for (int q = 0; q < 8; ++q) rr += (f >= e[q]) ? 1 : 0;
+            const int t = tbase[warp][rr] + f;
             bool hit = false;
             double d = 0.0;
             if (f < total) {
@@ -773,8 +785,10 @@ __global__ void __launch_bounds__(kEllWarps * 32, 4) grid_ell_kernel(int64_t B, 
             if (hit) {
                 const int slot = cnt + __popc(hm & lt);
                 if (slot < kEllCap) {
+                    // bucket by integer compares of the bit patterns (d, r2 >= 0): ALU, not FP64
+                    const unsigned long long db = (unsigned long long)__double_as_longlong(d);
                     int bk = 0;
-                    for (int l = 0; l < L; ++l) bk += (lvs[warp][l] <= d) ? 1 : 0;
+                    for (int l = 0; l < L; ++l) bk += (lvb[warp][l] <= db) ? 1 : 0;
                     hd[warp][slot] = d;
                     hj[warp][slot] = si[t];
                     hb[warp][slot] = (uint8_t)atomicAdd(&hcnt[warp][bk], 1);  // rank within bucket
