@@ -521,3 +521,36 @@ def test_mlp_estimator_thresholds_and_sampling_match_oracle():
         np.testing.assert_array_equal(fp.R[b].cpu().numpy(), ref.thresholds, err_msg="segment radii")
         np.testing.assert_array_equal(fp.out[b].cpu().numpy(), ref.indices)
         np.testing.assert_array_equal(Cv.estimate_mlp(ref.est_curve[:fp.k0], n, model), ref.est_curve)
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("variant", ["global-workspace", "v3", "many-levels", "many-small-clouds", "exhausting"])
+def test_sampler_variants_match_oracle(variant, monkeypatch):
+    """Sampler code paths beyond the default: the global-memory mode of v4,
+    the per-segment v3 kernels, 12 segments + 3 baked radii (L = 15 levels),
+    a batch of many single-CTA clouds (block barriers), and tight radii that
+    exhaust segment pools (entered / exhausted bookkeeping)."""
+    B, N, n, nseg, extra, family, e = 3, 6000, 1500, 6, (0.1,), "room-surfaces", 0.45
+    if variant == "global-workspace":
+        monkeypatch.setenv("PS_SAMPLER_GLOBAL", "1")
+    elif variant == "v3":
+        monkeypatch.setenv("PS_SAMPLER", "3")
+    elif variant == "many-levels":
+        nseg, extra = 12, (0.05, 0.1, 0.2)
+    elif variant == "many-small-clouds":
+        B, N, n, family = 24, 1500, 400, "unit-sphere"
+    elif variant == "exhausting":
+        family, e = "lattice", 0.9
+    clouds = np.stack([generate_cloud(family, N, 4000 + b) for b in range(B)])
+    fp = engine.FastPoint(B, N, n, nseg=nseg, exponent=e, extra_radii=extra)
+    fp.set_points(torch.from_numpy(clouds).cuda())
+    fp.set_rng([3 + b for b in range(B)])
+    fp.sample()
+    fp.check()
+    for b in range(B):
+        ref = O.mdps(clouds[b], n, nseg=nseg, exponent=e, rng_seed=3 + b, extra_radii=extra)
+        np.testing.assert_array_equal(fp.out[b].cpu().numpy(), ref.indices, err_msg=f"{variant} cloud {b}")
+        assert int(fp.reached[b].item()) == ref.reached
+        assert bool(fp.exhausted[b].item()) == ref.exhausted
+        assert int(fp.entered[b].item()) == ref.entered
+        assert int(np.int64(fp.state[b].item()).view(np.uint64)) == ref.rng_state
