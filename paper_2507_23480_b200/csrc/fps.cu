@@ -88,6 +88,16 @@ PS_DEV float skip_threshold(double md) {
     return __fmul_ru(__double2float_ru(md), 1.0f + 3.814697265625e-06f);    // * (1 + 2^-18)
 }
 
+// Same threshold from the float32 distance already computed for the screen:
+// d32 >= d (1 - 6 * 2^-24), so f32_ru(d32 * (1 + 2^-17)) >= d (1 + 2^-18) and
+// the skip argument above holds; d = 0 -> never fold, tiny/overflowing ->
+// always fold exactly.  Avoids a float64->float32 conversion per update.
+PS_DEV float skip_threshold_d32(double d, float d32) {
+    if (dbits(d) == 0) return -1.0f;
+    if (!(d32 >= 7.888609052210118e-31f) || !(d32 < 1e38f)) return __int_as_float(0x7f800000);
+    return __fmul_ru(d32, 1.0f + 7.62939453125e-06f);  // * (1 + 2^-17)
+}
+
 // Per point: the float32 distance to the new sample decides whether the exact
 // float64 fold can change md.  d32 carries relative error < 6 * 2^-24, so
 // d32 > f32_up(md) * (1 + 2^-18) proves d_exact > md and the fold is a no-op;
@@ -204,10 +214,12 @@ __global__ void __launch_bounds__(T, 1) fps_cluster_kernel(FpsArgs a) {
             if constexpr (P > 0) {
                 // 1a. float32 screen: which of my points can the new sample move?
                 uint32_t need = 0;
+                float d32s[P];
 #pragma unroll
                 for (int q = 0; q < P; ++q) {
                     const float dx = fx[q] - sx32, dy = fy[q] - sy32, dz = fz[q] - sz32;
                     const float d32 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+                    d32s[q] = d32;
                     need |= (!(d32 > thr[q]) ? 1u : 0u) << q;
                 }
                 // 1b. exact float64 fold where needed (warp-uniform branches, predicated update)
@@ -216,9 +228,10 @@ __global__ void __launch_bounds__(T, 1) fps_cluster_kernel(FpsArgs a) {
                     for (int q = 0; q < P; ++q) {
                         if (__any_sync(kFull, (need >> q) & 1u)) {
                             const double d = sqdist(sx, sy, sz, (double)fx[q], (double)fy[q], (double)fz[q]);
-                            if (((need >> q) & 1u) && d < m[q]) {
+                            // d, m >= 0: the bit patterns order like the values (ALU compare)
+                            if (((need >> q) & 1u) && dbits(d) < dbits(m[q])) {
                                 m[q] = d;
-                                thr[q] = skip_threshold(d);
+                                thr[q] = skip_threshold_d32(d, d32s[q]);
                                 dirty = dirty || (q == bq);
                             }
                         }
