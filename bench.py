@@ -434,6 +434,7 @@ def main_ours(args):
                                "value": ws * B * n_SAMPLES / (exact_ms / 1e3),
                                "us_per_cloud": 1e3 * exact_ms / B},
             "speedup_vs_exact_fps": exact_ms / (t_ms / args.steps),
+            "speedup_vs_exact_fps_kernel_only": float(np.mean(fps_ms)) / (t_ms / args.steps),
             "early_term_iters_mean": float(np.mean(n_SAMPLES - reached)),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_ms / args.steps, "results_match_device": e2e_ok,
