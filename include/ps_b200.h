@@ -97,7 +97,12 @@ PS_API int ps_fps_split(const float* xyz4, int64_t B, int64_t N, double* md, uin
                         double* curve, int64_t ld_out, int64_t k_stop, int64_t seed, int32_t G, int32_t g_base,
                         int32_t Gl, void* const* mbox_dev, uint32_t seq_base, int32_t all_write, void* stream);
 /* CUDA IPC for the mailboxes of one-process-per-GPU ranks: 64-byte handle of
- * a device allocation, opened in a peer process (peer access enabled). */
+ * a device allocation, opened in a peer process (peer access enabled).  The
+ * handle describes a whole cudaMalloc allocation and opens at its base, so
+ * mailboxes are allocated with ps_device_alloc (plain cudaMalloc, optionally
+ * filled with fill_byte), not carved out of a caching allocator. */
+PS_API int ps_device_alloc(int64_t bytes, int32_t fill_byte, void** dev_ptr_out);
+PS_API int ps_device_free(void* dev_ptr);
 PS_API int ps_ipc_handle(const void* dev_ptr, void* handle_out);
 PS_API int ps_ipc_open(const void* handle, void** dev_ptr_out);
 PS_API int ps_ipc_close(void* dev_ptr);

@@ -182,6 +182,28 @@ int ps_fps_split(const float* xyz4, int64_t B, int64_t N, double* md, uint8_t* t
     return cuda_status(ps::launch_fps_res(a, rk, B, C, P, S(stream)), "fps_split", 1);
 }
 
+int ps_device_alloc(int64_t bytes, int32_t fill_byte, void** dev_ptr_out) {
+    CHECK_ARG(bytes > 0 && dev_ptr_out, "invalid allocation request");
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, (size_t)bytes);
+    if (e != cudaSuccess) return fail(PS_ERR_CUDA, "cudaMalloc(%lld): %s", (long long)bytes, cudaGetErrorString(e));
+    if (fill_byte >= 0) {
+        e = cudaMemset(p, fill_byte & 0xff, (size_t)bytes);
+        if (e != cudaSuccess) {
+            cudaFree(p);
+            return fail(PS_ERR_CUDA, "cudaMemset: %s", cudaGetErrorString(e));
+        }
+    }
+    *dev_ptr_out = p;
+    return PS_OK;
+}
+
+int ps_device_free(void* dev_ptr) {
+    const cudaError_t e = cudaFree(dev_ptr);
+    if (e != cudaSuccess) return fail(PS_ERR_CUDA, "cudaFree: %s", cudaGetErrorString(e));
+    return PS_OK;
+}
+
 int ps_ipc_handle(const void* dev_ptr, void* handle_out) {
     CHECK_ARG(dev_ptr && handle_out, "null pointer");
     cudaIpcMemHandle_t h;

@@ -43,17 +43,20 @@ class PointSplitFPS:
         self.g = dist.get_rank(group)
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         nbytes = int(_lib.raw("ps_fps_mailbox_bytes", self.B, self.G))
-        self.box = torch.full((nbytes,), 0xFF, dtype=torch.uint8, device=self.device)
-        torch.cuda.synchronize(self.device)
+        # a dedicated cudaMalloc allocation: an IPC handle opens at the base of
+        # the allocation it names, which a caching-allocator tensor is not
+        box = ctypes.c_void_p()
+        _lib.call("ps_device_alloc", nbytes, 0xFF, ctypes.byref(box))
+        self.box_ptr = box.value
         handle = ctypes.create_string_buffer(64)
-        _lib.call("ps_ipc_handle", _p(self.box), handle)
+        _lib.call("ps_ipc_handle", self.box_ptr, handle)
         handles = [None] * self.G
         dist.all_gather_object(handles, bytes(handle.raw), group=group)
         self._opened = []
         ptrs = []
         for r, h in enumerate(handles):
             if r == self.g:
-                ptrs.append(self.box.data_ptr())
+                ptrs.append(self.box_ptr)
                 continue
             out = ctypes.c_void_p()
             _lib.call("ps_ipc_open", ctypes.create_string_buffer(h, 64), ctypes.byref(out))
@@ -64,9 +67,14 @@ class PointSplitFPS:
         dist.barrier(group=group)
 
     def close(self):
+        """Collective: unmap the peers' mailboxes, then free this rank's."""
         for p in self._opened:
             _lib.call("ps_ipc_close", p)
         self._opened = []
+        dist.barrier(group=self.group)
+        if self.box_ptr:
+            _lib.call("ps_device_free", self.box_ptr)
+            self.box_ptr = 0
 
     def run(self, xyz4: torch.Tensor, n: int, seed_index: int = 0, k_stop: int | None = None):
         """Collective exact FPS of every cloud; returns (idx, curve, md, taken)

@@ -554,3 +554,24 @@ def test_sampler_variants_match_oracle(variant, monkeypatch):
         assert bool(fp.exhausted[b].item()) == ref.exhausted
         assert int(fp.entered[b].item()) == ref.entered
         assert int(np.int64(fp.state[b].item()).view(np.uint64)) == ref.rng_state
+
+
+@pytest.mark.timeout(240)
+def test_point_split_two_processes_cuda_ipc():
+    """The one-process-per-GPU point split (pointsplit.PointSplitFPS): two
+    processes exchange their cudaMalloc mailboxes through CUDA IPC and peer
+    stores; here both live on the same GPU (their kernels alternate by
+    time-slicing, hence few iterations).  Identical to the single-rank FPS on
+    every rank."""
+    import subprocess
+    import sys as _sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, IPC_N="64")
+    port = 29000 + os.getpid() % 1000
+    out = subprocess.run([_sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port),
+                          os.path.join(root, "tools", "ipc_selftest.py")],
+                         env=env, capture_output=True, text=True, timeout=200, cwd=root)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert out.stdout.count("identical to single-rank: True") == 2
