@@ -3,6 +3,8 @@ and the golden vectors of the real reference.  Indices, counts and RNG state
 are compared bit-exactly; float64 distances / curves bit-exactly too (same
 operation sequence, IEEE sqrt/div)."""
 
+import os
+
 import numpy as np
 import pytest
 
