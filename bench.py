@@ -404,6 +404,8 @@ def main_ours(args):
     c5 = c2 = c4 = None
     if not args.no_c5 and ws == 1:
         c5 = bench_c5_virtual(dev)
+    elif args.c5_split and ws > 1:
+        c5 = bench_c5_split(dev, ws)
     if not args.no_extra and ws == 1:
         c2 = bench_c2_cascade(dev, args.steps)
         c4 = bench_c4(dev, args.steps)
@@ -583,6 +585,37 @@ def bench_c5_virtual(dev, G=None):
             "parity": "bit-identical to the single-rank kernel (tests/test_gpu_parity.py, tools/c5_split.py)"}
 
 
+def bench_c5_split(dev, ws):
+    """C5 over the job's GPUs, one process per GPU (pointsplit.PointSplitFPS:
+    cudaMalloc mailboxes mapped into every peer through CUDA IPC, NVLink
+    stores; no NCCL on the data path).  Device time, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_23480_b200 import engine, pointsplit
+    from paper_2507_23480_b200.harness import generate_cloud
+
+    cloud = generate_cloud("uniform-box", C5_N, 5000)
+    x = engine.as_xyz4(torch.from_numpy(cloud[None]).to(dev))
+    ps = pointsplit.PointSplitFPS(1, C5_N, device=dev)
+    ps.run(x, C5_n, k_stop=1024)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    idx, curve, _, _ = ps.run(x, C5_n)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1), dev)
+    ok = int(torch.unique(idx).numel()) == C5_n
+    dist.barrier()
+    ps.close()
+    return {"workload": "C5: 1 cloud N=2^20 uniform-box -> n=65536 exact FPS, point split", "ranks": ws,
+            "mode": "one process per GPU, CUDA-IPC mailboxes over NVLink", "ms": ms,
+            "us_per_iter": 1e3 * ms / (C5_n - 1), "sampled_pts_per_s": C5_n / (ms / 1e3),
+            "checks": "distinct indices" if ok else "FAILED property checks"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -592,6 +625,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 point-split line")
     ap.add_argument("--no-extra", action="store_true", help="skip the C2 / C4 objects")
+    ap.add_argument("--c5-split", action="store_true",
+                    help="N > 1: also run C5 point-split over the job's GPUs (CUDA IPC + NVLink)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
