@@ -12,7 +12,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libps_b200.so")
+LIB_PATH = os.environ.get("PS_B200_LIB") or os.path.join(_HERE, "libps_b200.so")  # override: dev builds (TIMING=1)
 
 PS_OK = 0
 PS_ERR_INVALID = -1

@@ -122,6 +122,20 @@ PS_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
         "@!P1 bra WAIT_%=;\n"
         "}\n" ::"r"(a), "r"(parity) : "memory");
 }
+// Same wait with CTA-scope acquire: enough for bytes delivered into this
+// CTA's shared memory by st.async / cp.async.bulk complete_tx (the
+// transaction mechanism makes them visible), and ptxas emits no L1
+// invalidation (CCTL.IVALL) for it, unlike the cluster-scope acquire.
+PS_DEV void mbar_wait_cta(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(a), "r"(parity) : "memory");
+}
 // 16-byte asynchronous store into a peer CTA's shared memory that signals
 // the peer's mbarrier with complete_tx(16).
 PS_DEV void st_async_v4(uint32_t remote_addr, uint32_t remote_bar, uint32_t a, uint32_t b,
@@ -129,6 +143,34 @@ PS_DEV void st_async_v4(uint32_t remote_addr, uint32_t remote_bar, uint32_t a, u
     asm volatile(
         "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%2, %3, %4, %5}, [%1];"
         ::"r"(remote_addr), "r"(remote_bar), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
+// Remote arrive on a peer CTA's mbarrier that also raises its expected
+// transaction bytes: a sender announces a variable-length st.async payload
+// (barrier initialised with one arrival per sender).
+PS_DEV void mbar_remote_arrive_expect_tx(uint32_t remote_bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.relaxed.cluster.shared::cluster.b64 _, [%0], %1;"
+                 ::"r"(remote_bar), "r"(bytes) : "memory");
+}
+
+// CTA-scope release store / acquire load on shared memory (producer warp
+// publishing to consumer warps without a block barrier).
+PS_DEV void st_release_cta(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+PS_DEV uint32_t ld_acquire_cta(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+    return v;
+}
+
+// Named barriers (ids 1..15; 0 is __syncthreads): producer arrives without
+// waiting, consumers sync; nthreads counts both sides.
+PS_DEV void named_bar_arrive(int id, int nthreads) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+PS_DEV void named_bar_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 // ---- row ordering by (d2, index) ----------------------------------------

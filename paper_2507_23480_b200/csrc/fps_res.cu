@@ -811,6 +811,10 @@ cudaError_t launch_fps(FpsArgs a, int64_t B, cudaStream_t s) {
         rk.G = 1; rk.Gl = 1; rk.g_base = 0;
         return launch_fps_res(a, rk, B, C, P, s);
     }
+    if (!getenv("PS_FPS_NOSPEC")) {
+        const cudaError_t e = launch_fps_spec(a, B, s);
+        if (e != cudaErrorNotSupported) return e;
+    }
     return launch_fps_legacy(a, B, s);
 }
 
