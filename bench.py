@@ -311,6 +311,23 @@ def main_ours(args):
         fps_ms.append(e0.elapsed_time(e1))
         bqn_ms.append(e1.elapsed_time(e2))
     exact_ms = (sum(fps_ms) + sum(bqn_ms)) / args.steps
+    # the one-exchange-per-sample exact kernel (fps.cu; north_star piece (1)
+    # as first built) on the same batch, for the ratio against it as well
+    os.environ["PS_FPS_NOSPEC"] = "1"
+    try:
+        engine.fps(fp.xyz4, n_SAMPLES)
+        torch.cuda.synchronize()
+        fps1_ms = []
+        for s in range(args.steps):
+            flush.zero_()
+            e0, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+            e0.record(stream)
+            engine.fps(fp.xyz4, n_SAMPLES)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            fps1_ms.append(e0.elapsed_time(e1))
+    finally:
+        del os.environ["PS_FPS_NOSPEC"]
 
     # ---- end to end through the public API: pinned host in, results out ---------
     # Every step uploads its clouds from pinned host memory and downloads its
@@ -437,6 +454,12 @@ def main_ours(args):
                                "us_per_cloud": 1e3 * exact_ms / B},
             "speedup_vs_exact_fps": exact_ms / (t_ms / args.steps),
             "speedup_vs_exact_fps_kernel_only": float(np.mean(fps_ms)) / (t_ms / args.steps),
+            "exact_fps_one_sample_kernel": {
+                "fps_ms": float(np.mean(fps1_ms)),
+                "speedup_vs_it": float(np.mean(fps1_ms)) / (t_ms / args.steps),
+                "speedup_vs_it_plus_naive_bq": (float(np.mean(fps1_ms)) + float(np.mean(bqn_ms))) / (t_ms / args.steps),
+                "note": "fps.cu, one cluster exchange per sample; exact_fps_path uses the speculative "
+                        "exact kernel (fps_spec.cu), bit-identical output"},
             "early_term_iters_mean": float(np.mean(n_SAMPLES - reached)),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_ms / args.steps, "results_match_device": e2e_ok,
