@@ -96,6 +96,36 @@ def test_fps_resident_cluster_widths(C, monkeypatch):
 
 
 @pytest.mark.timeout(300)
+@pytest.mark.parametrize("kernel", ["speculative", "one-sample"])
+@pytest.mark.parametrize("C", ["1", "2", "5", "10", "16"])
+def test_fps_register_kernels_across_cluster_widths(kernel, C, monkeypatch):
+    """Both register-resident exact kernels -- the speculative one (default,
+    fps_spec.cu) and the one-exchange-per-sample one (fps.cu) -- at forced
+    cluster widths, on tie-heavy (lattice), surface, clustered and
+    half-duplicate clouds (the fallback of _kernels.py:65-70 mid-run and at
+    the tail), full runs and a run stopped early, against the oracle:
+    indices, curve, md and taken bit for bit."""
+    monkeypatch.setenv("PS_FPS_CLUSTER", C)
+    if kernel == "one-sample":
+        monkeypatch.setenv("PS_FPS_NOSPEC", "1")
+    dup = generate_cloud("uniform-box", 1500, 3)
+    dup = np.concatenate([dup, dup[::2]])[np.random.default_rng(1).permutation(2250)].copy()
+    cases = (("lattice", generate_cloud("lattice", 4913, 7), 1200), ("room", generate_cloud("room-surfaces", 12000, 7), 3000),
+             ("clusters", generate_cloud("gaussian-clusters", 9000, 7), 900), ("dup", dup, 2250))
+    for name, c, n in cases:
+        N = len(c)
+        for k_stop in (n, max(2, n // 3)):
+            xyz4 = engine.as_xyz4(torch.from_numpy(c[None]).cuda())
+            idx, curve, md, taken = engine.fps(xyz4, n, seed_index=N // 5, k_stop=k_stop)
+            ri, rc, rmd, rtk, _ = O.fps(c, n, N // 5, k_stop=k_stop)
+            msg = f"{name} {kernel} C={C} k_stop={k_stop}"
+            np.testing.assert_array_equal(idx[0].cpu().numpy()[:k_stop], ri[:k_stop], err_msg=msg)
+            np.testing.assert_array_equal(curve[0].cpu().numpy()[:k_stop], rc[:k_stop], err_msg=msg)
+            np.testing.assert_array_equal(md[0].cpu().numpy(), rmd, err_msg=msg)
+            np.testing.assert_array_equal(taken[0].cpu().numpy(), rtk, err_msg=msg)
+
+
+@pytest.mark.timeout(300)
 @pytest.mark.parametrize("family,N,n,G,B", [
     ("room-surfaces", 24000, 3000, 2, 1), ("room-surfaces", 24000, 3000, 4, 2), ("lattice", 4913, 1200, 3, 1),
     ("uniform-box", 200000, 1500, 4, 1), ("gaussian-clusters", 9000, 900, 8, 1), ("uniform-box", 4096, 1024, 1, 1),
