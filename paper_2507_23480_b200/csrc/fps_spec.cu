@@ -16,16 +16,19 @@
 // next (lowest index on ties).  tau only decides how many picks one exchange
 // certifies, never which point is picked, so a poor tau costs speed only.
 //
-// Layout: C CTAs of T threads per cloud.  Warps 0..kW-2 own P points per
-// thread in registers (float32 xyz, float64 md, taken bits); the last warp
-// (the lead) owns none and runs, per exchange:
+// Layout: C CTAs of T threads per cloud.  Each CTA counting-sorts its index
+// range by a 16^3 Morton cell so that worker warp w (0..kW-2) owns 32P
+// spatially compact points in registers (float32 xyz, float64 md, taken
+// bits); a sample farther from a warp's box than every skip threshold of the
+// warp is skipped by the whole warp.  The last warp (the lead) owns none and
+// runs, per exchange:
 //   C. CTA argmax over the warp records + the CTA's candidates (<= kR-1),
 //      pushed to every CTA with st.async; each sender announces its byte
 //      count on the peer's mbarrier (remote arrive.expect_tx);
-//   D. headers in lanes < C, candidates compacted one per lane, and their
-//      pairwise float64 distances in shared memory (dm_s);
+//   D. headers in lanes < C, candidates compacted one per lane;
 //   E. picks: the first over headers + candidates, then the best candidate
-//      while >= tau, each lowering the others by its dm_s row.  Each pick is
+//      while >= tau, each lowering the others by its exact float64 distance
+//      to them (the reference's update, same operation order).  Each pick is
 //      published to the CTA (release store); the worker warps fold it into
 //      their md as soon as it appears, overlapping the lead's serial chain.
 //   tau for the next exchange: kTarget samples ahead along the recent curve
@@ -33,6 +36,9 @@
 // The duplicate fallback of _kernels.py:65-70 (max <= 0 or winner already
 // taken -> lowest untaken index) runs as a cluster-wide exchange when the
 // first pick needs it; a later pick that would need it ends the run.
+// Development knobs: PS_SPEC_TARGET=<samples> overrides kTarget (< 0: no
+// speculation); PS_FPS_NOSPEC=1 selects fps.cu; make TIMING=1 +
+// PS_FPS_TIMING=1 prints per-phase cycles (tools/fps_spec_timing.py).
 // Measured (profiles/r01/fps_spec.log): 0.50 us/iteration for a full
 // 6000-of-24000 FPS on the C3 batch vs 1.13 for the one-sample kernel
 // (fps.cu), 0.94 vs 1.37 over the 600-iteration FastPoint prefix.
@@ -57,6 +63,8 @@ constexpr int kR = 8;             // records per CTA per exchange: its max + kR-
 constexpr int kRunMax = 31;       // samples per exchange (one lane each)
 constexpr double kTarget = 22.0;  // threshold candidates aimed for per exchange
 constexpr uint64_t kTauOff = ~0ull;  // threshold disabled (above every md bit pattern)
+constexpr int kMaxS = 4096;          // points per CTA the spatial sort holds
+constexpr float kInfF = __builtin_huge_valf();
 
 template <int P, int T>
 __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
@@ -78,15 +86,18 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
     __shared__ float4 run_s[32];
     __shared__ uint8_t map_s[kMaxCluster * kR];
     __shared__ double hist_s[32];
-    __shared__ double dm_s[32 * 32];  // candidate pair distances, row = picked candidate
     __shared__ unsigned long long tau_s;
     __shared__ int cnt_s;
     __shared__ uint32_t pub_s;
+    __shared__ uint32_t bin_s[4096];    // spatial sort: cell counts / offsets
+    __shared__ uint16_t ord_s[kMaxS];   // sorted position -> local index
+    __shared__ uint16_t pos_s[kMaxS];   // local index -> sorted position
+    __shared__ float red_s[kW][6], bb_s[6];
+    __shared__ uint32_t wsum_s[kW];
     __shared__ __align__(8) uint64_t bars[2];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool worker = warp != kLead;
-    const int wt = tid;  // worker thread index
     const uint32_t C = cluster_nctarank();
     const uint32_t r = cluster_ctarank();
     const int64_t b = cluster_id_x();
@@ -106,16 +117,107 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
     const double kInf = __longlong_as_double(0x7ff0000000000000LL);
     const bool writer = r == 0 && warp == kLead && lane == 0;
 
-    // ---- state into registers (as fps.cu) ---------------------------------
+    // ---- spatial order -----------------------------------------------------
+    // Counting sort of this CTA's points by the Morton code of a 16^3 grid over
+    // their bounding box: worker warp w owns sorted positions [w*32P, (w+1)*32P),
+    // a compact region, so a pick far from a warp's box skips the whole warp
+    // (fold_one).  The order inside a cell follows shared-memory atomics and may
+    // differ between runs; no result depends on it (every choice is by
+    // (md, original index)).
+    static_assert(kMaxS >= P * TW, "sort capacity");
+    const int ncta = hi > lo ? (int)(hi - lo) : 0;
+    {
+        float mn[3] = {kInfF, kInfF, kInfF}, mx[3] = {-kInfF, -kInfF, -kInfF};
+        for (int i = tid; i < ncta; i += T) {
+            const float4 v = xyz[lo + i];
+            mn[0] = fminf(mn[0], v.x); mn[1] = fminf(mn[1], v.y); mn[2] = fminf(mn[2], v.z);
+            mx[0] = fmaxf(mx[0], v.x); mx[1] = fmaxf(mx[1], v.y); mx[2] = fmaxf(mx[2], v.z);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                mn[d] = fminf(mn[d], __shfl_xor_sync(kFull, mn[d], o));
+                mx[d] = fmaxf(mx[d], __shfl_xor_sync(kFull, mx[d], o));
+            }
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int d = 0; d < 3; ++d) { red_s[warp][d] = mn[d]; red_s[warp][3 + d] = mx[d]; }
+        }
+        for (int i = tid; i < 4096; i += T) bin_s[i] = 0u;
+        __syncthreads();
+        if (tid < 6) {
+            float r = red_s[0][tid];
+            for (int w = 1; w < kW; ++w) r = tid < 3 ? fminf(r, red_s[w][tid]) : fmaxf(r, red_s[w][tid]);
+            bb_s[tid] = r;
+        }
+        __syncthreads();
+        float org[3], sc[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            org[d] = bb_s[d];
+            const float ext = bb_s[3 + d] - bb_s[d];
+            sc[d] = ext > 0.f ? 16.0f / ext : 0.f;
+        }
+        auto cell_of = [&](float4 v) {
+            auto q4 = [&](float x, int d) {
+                const int c = (int)((x - org[d]) * sc[d]);
+                return (uint32_t)(c < 0 ? 0 : (c > 15 ? 15 : c));
+            };
+            auto spread = [](uint32_t b) { return (b & 1u) | ((b & 2u) << 2) | ((b & 4u) << 4) | ((b & 8u) << 6); };
+            return spread(q4(v.x, 0)) | (spread(q4(v.y, 1)) << 1) | (spread(q4(v.z, 2)) << 2);
+        };
+        for (int i = tid; i < ncta; i += T) {
+            const uint32_t c = cell_of(xyz[lo + i]);
+            pos_s[i] = (uint16_t)c;
+            atomicAdd(&bin_s[c], 1u);
+        }
+        __syncthreads();
+        // exclusive scan of the 4096 bins: kPer consecutive bins per thread
+        constexpr int kPer = 4096 / T;
+        uint32_t loc = 0;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) loc += bin_s[tid * kPer + k];
+        uint32_t inc = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(kFull, inc, o);
+            if (lane >= o) inc += t;
+        }
+        if (lane == 31) wsum_s[warp] = inc;
+        __syncthreads();
+        uint32_t wbase = 0;
+        for (int w = 0; w < warp; ++w) wbase += wsum_s[w];
+        uint32_t run = wbase + inc - loc;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const uint32_t c = bin_s[tid * kPer + k];
+            bin_s[tid * kPer + k] = run;
+            run += c;
+        }
+        __syncthreads();
+        for (int i = tid; i < ncta; i += T) {
+            const uint32_t sp = atomicAdd(&bin_s[pos_s[i]], 1u);
+            ord_s[sp] = (uint16_t)i;
+            pos_s[i] = (uint16_t)sp;
+        }
+        __syncthreads();
+    }
+    // original index of my slot q
+    auto oid = [&](int q) -> uint32_t { return (uint32_t)(lo + ord_s[warp * 32 * P + q * 32 + lane]); };
+
+    // ---- state into registers ---------------------------------------------
     float fx[P], fy[P], fz[P], thr[P];
     double m[P];
     uint32_t tk = 0, valid = 0;
 #pragma unroll
     for (int q = 0; q < P; ++q) {
-        const int64_t j = lo + wt + (int64_t)q * TW;
+        const int sp = warp * 32 * P + q * 32 + lane;
         fx[q] = fy[q] = fz[q] = 0.f;
         m[q] = 0.0;
-        if (worker && j < hi) {
+        if (worker && sp < ncta) {
+            const int64_t j = lo + ord_s[sp];
             valid |= 1u << q;
             const float4 v = xyz[j];
             fx[q] = v.x; fy[q] = v.y; fz[q] = v.z;
@@ -129,6 +231,32 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
         }
         thr[q] = ((valid >> q) & 1u) ? skip_threshold(m[q]) : -1.0f;
     }
+    // the warp's bounding box and the largest skip threshold of its points
+    float wb[6] = {kInfF, kInfF, kInfF, -kInfF, -kInfF, -kInfF};
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+        if ((valid >> q) & 1u) {
+            wb[0] = fminf(wb[0], fx[q]); wb[1] = fminf(wb[1], fy[q]); wb[2] = fminf(wb[2], fz[q]);
+            wb[3] = fmaxf(wb[3], fx[q]); wb[4] = fmaxf(wb[4], fy[q]); wb[5] = fmaxf(wb[5], fz[q]);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            wb[d] = fminf(wb[d], __shfl_xor_sync(kFull, wb[d], o));
+            wb[3 + d] = fmaxf(wb[3 + d], __shfl_xor_sync(kFull, wb[3 + d], o));
+        }
+    }
+    auto warp_thr_max = [&]() {
+        float t = -1.0f;
+#pragma unroll
+        for (int q = 0; q < P; ++q)
+            if ((valid >> q) & 1u) t = fmaxf(t, thr[q]);
+        const uint32_t k = __reduce_max_sync(kFull, t < 0.f ? 0u : __float_as_uint(t));  // t >= 0: bits order
+        return k == 0u ? -1.0f : __uint_as_float(k);
+    };
+    float wthr = warp_thr_max();
     if (a.fresh && writer) {
         out[0] = seed;
         curve[0] = kInf;
@@ -165,9 +293,22 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
     // mark sample sidx taken if it is mine; fold it into md unless it is the
     // last sample of this call (the reference folds that one at the next call)
     auto fold_one = [&](float sx32, float sy32, float sz32, uint32_t sidx, bool do_fold) {
-        const uint32_t o32 = (uint32_t)((int64_t)sidx - lo - wt);  // wraps below lo
-        if (o32 < (uint32_t)(P * TW) && o32 % TW == 0) tk |= 1u << (o32 / TW);
+        const int64_t li = (int64_t)sidx - lo;
+        if (li >= 0 && li < ncta) {
+            const int sp = pos_s[li];
+            if (worker && sp / (32 * P) == warp && (sp & 31) == lane) tk |= 1u << ((sp % (32 * P)) >> 5);
+        }
         if (!do_fold) return;
+        // whole-warp skip: a rounded-down lower bound of the squared distance
+        // from the sample to the warp's box above every skip threshold of the
+        // warp proves, as the per-point screen does, that no md can change
+        {
+            const float ex = fmaxf(fmaxf(__fsub_rd(wb[0], sx32), __fsub_rd(sx32, wb[3])), 0.f);
+            const float ey = fmaxf(fmaxf(__fsub_rd(wb[1], sy32), __fsub_rd(sy32, wb[4])), 0.f);
+            const float ez = fmaxf(fmaxf(__fsub_rd(wb[2], sz32), __fsub_rd(sz32, wb[5])), 0.f);
+            const float dbox = __fadd_rd(__fadd_rd(__fmul_rd(ex, ex), __fmul_rd(ey, ey)), __fmul_rd(ez, ez));
+            if (dbox > wthr) return;
+        }
         uint32_t need = 0;
         float d32s[P];
 #pragma unroll
@@ -209,7 +350,9 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
         long long t0 = 0, t1 = 0;
         if (tdbg) t0 = clock64();
 
-        // B. thread max (cached), threshold candidates, warp argmax
+        // B. thread max (cached), threshold candidates, warp argmax; the
+        // warp's skip bound for the next exchange's folds (thr only falls)
+        wthr = warp_thr_max();
         if (__any_sync(kFull, dirty)) {
             double tv[P];
             int ti[P];
@@ -221,8 +364,11 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
 #pragma unroll
             for (int st = 1; st < P; st <<= 1) {
 #pragma unroll
-                for (int q = 0; q + st < P; q += 2 * st)
-                    if (tv[q + st] > tv[q]) { tv[q] = tv[q + st]; ti[q] = ti[q + st]; }
+                for (int q = 0; q + st < P; q += 2 * st) {
+                    bool take = tv[q + st] > tv[q];
+                    if (tv[q + st] == tv[q] && tv[q] >= 0.0) take = oid(ti[q + st]) < oid(ti[q]);  // lowest index
+                    if (take) { tv[q] = tv[q + st]; ti[q] = ti[q + st]; }
+                }
             }
             if (dirty) {
                 bv = tv[0];
@@ -246,14 +392,14 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
                             const uint64_t kq = dbits(m[q]);
                             uint4* c4 = reinterpret_cast<uint4*>(&cand[slot]);
                             c4[0] = make_uint4((uint32_t)kq, (uint32_t)(kq >> 32),
-                                               (uint32_t)(lo + wt + (int64_t)q * TW), (tk >> q) & 1u);
+                                               oid(q), (tk >> q) & 1u);
                             c4[1] = make_uint4(__float_as_uint(fx[q]), __float_as_uint(fy[q]), __float_as_uint(fz[q]), 0u);
                         }
                     }
                 }
             }
             const uint64_t bkey = bv >= 0.0 ? dbits(bv) : 0ull;
-            const uint32_t bidx = bv >= 0.0 ? (uint32_t)(lo + wt + (int64_t)bq * TW) : kNone;
+            const uint32_t bidx = bv >= 0.0 ? oid(bq) : kNone;
             const int wl = warp_argmax_lane(bkey, bidx);
             if (wl < 0) {
                 if (lane == 0) { Rec z{}; z.idx = kNone; wrec[warp] = z; }
@@ -356,20 +502,6 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
             overflow = overflow || __any_sync(kFull, lane < ncand && ct);
             bool alive = lane < ncand;
             if (tdbg) { t1 = clock64(); tacc[0] += t1 - t0; t0 = t1; }
-            // distances between candidates, exactly the float64 update a pick applies
-            if (!overflow) {
-                const double dcx = cx, dcy = cy, dcz = cz;
-                for (int w0 = 0; w0 < ncand; w0 += 8) {  // chunks of 8 independent rows
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const float wx = __shfl_sync(kFull, cx, w0 + i);
-                        const float wy = __shfl_sync(kFull, cy, w0 + i);
-                        const float wz = __shfl_sync(kFull, cz, w0 + i);
-                        const double d = sqdist((double)wx, (double)wy, (double)wz, dcx, dcy, dcz);
-                        if (alive && w0 + i < ncand) dm_s[(w0 + i) * 32 + lane] = d;
-                    }
-                }
-            }
             __syncwarp();
             if (tdbg) { t1 = clock64(); tacc[6] += t1 - t0; t0 = t1; }
 
@@ -388,7 +520,6 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
                     const uint64_t wk = __shfl_sync(kFull, k0, wl);
                     const uint32_t wi = __shfl_sync(kFull, i0, wl);
                     const uint32_t wt = __shfl_sync(kFull, use_c ? ct : ht, wl);
-                    const bool wc = __shfl_sync(kFull, use_c ? 1 : 0, wl);
                     const float sx = __shfl_sync(kFull, use_c ? cx : hx, wl);
                     const float sy = __shfl_sync(kFull, use_c ? cy : hy, wl);
                     const float sz = __shfl_sync(kFull, use_c ? cz : hz, wl);
@@ -411,30 +542,25 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
                         rnl = 1;
                         alive = alive && ci != wi && !overflow;
                         if (alive) {
-                            const double d = wc ? dm_s[wl * 32 + lane]
-                                                : sqdist((double)sx, (double)sy, (double)sz, (double)cx, (double)cy,
-                                                         (double)cz);
+                            const double d = sqdist((double)sx, (double)sy, (double)sz, (double)cx, (double)cy,
+                                                    (double)cz);
                             if (dbits(d) < dbits(cm)) cm = d;
                         }
                     }
                 }
             }
             if (tdbg) { t1 = clock64(); tacc[7] += t1 - t0; t0 = t1; }
-            // Later picks, in rounds: rank the candidates still above the
-            // threshold, follow that order with every key updated exactly
-            // (dm_s rows, the same float64 values a pick-by-pick loop
-            // applies), and accept the order up to the first step at which a
-            // later candidate would outrank the pick, or a pick would fall
-            // below the threshold.
-            // later picks: the best candidate while it clears the threshold;
-            // the others' keys are lowered by its dm_s row (the exact float64
-            // update the reference applies)
+            // later picks: the best candidate while it clears the threshold
             while (rnl > 0 && itl < k_stop && rnl < kRunMax) {
                 alive = alive && dbits(cm) >= tau;
                 const int wl = warp_argmax_lane(alive ? dbits(cm) : 0ull, alive ? ci : kNone);
                 if (wl < 0) break;
                 const bool win = lane == wl;
-                const double d = dm_s[wl * 32 + lane];
+                const float sx = __shfl_sync(kFull, cx, wl);
+                const float sy = __shfl_sync(kFull, cy, wl);
+                const float sz = __shfl_sync(kFull, cz, wl);
+                // the reference's float64 update of every other candidate
+                const double d = sqdist((double)sx, (double)sy, (double)sz, (double)cx, (double)cy, (double)cz);
                 if (win) {
                     run_s[rnl] = make_float4(cx, cy, cz, __uint_as_float(ci));
                     hist_s[(hc + rnl) & 31] = cm;
@@ -453,14 +579,15 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
 
             // next threshold: the curve is non-increasing; aim kTarget samples
             // ahead along its recent slope, gain corrected by the observed count
-            const double target = kTarget;
+            // development override (PS_SPEC_TARGET; < 0: no speculation)
+            const double target = a.dbg_t0 > 0 ? (double)a.dbg_t0 * 1e-3 : (a.dbg_t0 == -1 ? -1.0 : kTarget);
             if (tau != kTauOff) {
                 if (overflow || ctot > (int)(2 * target)) gain *= 0.7f;
                 else if (ctot < (int)(target / 2)) gain *= 1.3f;
                 gain = fminf(fmaxf(gain, 0.05f), 20.0f);
             }
             uint64_t tnew = kTauOff;
-            if (hc >= 3) {
+            if (hc >= 3 && target > 0.0) {
                 const int L = hc - 1 < 16 ? hc - 1 : 16;
                 const double m0 = hist_s[(hc - 1) & 31];
                 const double mL = hist_s[(hc - 1 - L) & 31];
@@ -509,9 +636,9 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
             uint32_t fidx = kNone;
             Rec fr{};
 #pragma unroll
-            for (int q = P - 1; q >= 0; --q) {
-                if (((valid >> q) & 1u) && !((tk >> q) & 1u)) {
-                    fidx = (uint32_t)(lo + wt + (int64_t)q * TW);
+            for (int q = 0; q < P; ++q) {
+                if (((valid >> q) & 1u) && !((tk >> q) & 1u) && oid(q) < fidx) {
+                    fidx = oid(q);
                     const uint64_t kk = dbits(m[q]);
                     fr.klo = (uint32_t)kk; fr.khi = (uint32_t)(kk >> 32);
                     fr.x = fx[q]; fr.y = fy[q]; fr.z = fz[q];
@@ -560,8 +687,8 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
     // ---- write back md / taken; curve = sqrt(best) (_kernels.py:72) ---------
 #pragma unroll
     for (int q = 0; q < P; ++q) {
-        const int64_t j = lo + wt + (int64_t)q * TW;
-        if (worker && j < hi) {
+        if ((valid >> q) & 1u) {
+            const int64_t j = oid(q);
             md[j] = m[q];
             taken[j] = (tk >> q) & 1u;
         }
@@ -619,6 +746,8 @@ cudaError_t launch_fps_spec(FpsArgs a, int64_t B, cudaStream_t s) {
     if (P == 0) return cudaErrorNotSupported;
     a.points_per_cta = S;
     a.dbg = nullptr;
+    a.dbg_t0 = getenv("PS_SPEC_TARGET") ? (int64_t)(atof(getenv("PS_SPEC_TARGET")) * 1000.0) : 0;
+    if (getenv("PS_SPEC_TARGET") && atof(getenv("PS_SPEC_TARGET")) < 0) a.dbg_t0 = -1;
     static long long* dbg = nullptr;
     const bool timing = kTiming && getenv("PS_FPS_TIMING");
     if (timing) {
