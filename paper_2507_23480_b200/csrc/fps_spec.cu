@@ -64,6 +64,7 @@ constexpr int kRunMax = 31;       // samples per exchange (one lane each)
 constexpr double kTarget = 22.0;  // threshold candidates aimed for per exchange
 constexpr uint64_t kTauOff = ~0ull;  // threshold disabled (above every md bit pattern)
 constexpr int kMaxS = 4096;          // points per CTA the spatial sort holds
+constexpr int64_t kSortMinIters = 256;  // runs shorter than this keep the index order
 constexpr float kInfF = __builtin_huge_valf();
 
 template <int P, int T>
@@ -126,7 +127,11 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
     // (md, original index)).
     static_assert(kMaxS >= P * TW, "sort capacity");
     const int ncta = hi > lo ? (int)(hi - lo) : 0;
-    {
+    if (k_stop - k_start < kSortMinIters) {
+        // short runs (early-termination tails) do not repay the sort
+        for (int i = tid; i < ncta; i += T) { ord_s[i] = (uint16_t)i; pos_s[i] = (uint16_t)i; }
+        __syncthreads();
+    } else {
         float mn[3] = {kInfF, kInfF, kInfF}, mx[3] = {-kInfF, -kInfF, -kInfF};
         for (int i = tid; i < ncta; i += T) {
             const float4 v = xyz[lo + i];

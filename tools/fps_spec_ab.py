@@ -1,6 +1,6 @@
-"""A/B the K1 variants on the bench batch in one process: PS_SPEC_EXP bits
-(1: one pick at a time, 2: lead warp alone on its SMSP, 8/16: candidate
-target 16/22) and PS_FPS_NOSPEC (one-sample kernel).  Prints us/iteration
+"""A/B K1 variants on the bench batch in one process: environment settings
+given as KEY=VAL[,KEY=VAL] arguments (e.g. PS_FPS_CLUSTER=12), against the
+default and PS_FPS_NOSPEC=1 (one-sample kernel).  Prints us/iteration
 for the FastPoint prefix (600) and a full exact FPS (6000), and whether the
 indices/curve equal the one-sample kernel's."""
 import os
@@ -16,7 +16,7 @@ x = engine.as_xyz4(torch.from_numpy(bench.clouds_for(0, bench.B_PER_GPU)).cuda()
 
 
 def run(env):
-    for k in ("PS_SPEC_EXP", "PS_FPS_NOSPEC"):
+    for k in ("PS_FPS_NOSPEC", "PS_FPS_CLUSTER", "PS_FPS_THREADS", "PS_SPEC_TARGET"):
         os.environ.pop(k, None)
     os.environ.update(env)
     res = []
@@ -37,13 +37,13 @@ def run(env):
     return res, idx, curve
 
 
-variants = [("one-sample", {"PS_FPS_NOSPEC": "1"})]
-for v in sys.argv[1:] or ["0", "1", "2", "3", "8", "10"]:
-    variants.append((f"exp={v}", {"PS_SPEC_EXP": v}))
+variants = [("one-sample", {"PS_FPS_NOSPEC": "1"}), ("default", {})]
+for v in sys.argv[1:]:  # KEY=VAL[,KEY=VAL...] environment variants
+    variants.append((v, dict(kv.split("=", 1) for kv in v.split(","))))
 ref = None
 for name, env in variants:
     (p, f), idx, curve = run(env)
     if ref is None:
         ref = (idx, curve)
     ok = torch.equal(idx, ref[0]) and torch.equal(curve, ref[1])
-    print(f"{name:>12}: prefix {p:.3f} us/it  full {f:.3f} us/it  bit-equal {ok}", flush=True)
+    print(f"{name:>24}: prefix {p:.3f} us/it  full {f:.3f} us/it  bit-equal {ok}", flush=True)
