@@ -209,8 +209,12 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
         }
         __syncthreads();
     }
+    // 32-bit shared addresses of the hot arrays (see sts_*/lds_* in common.cuh)
+    const uint32_t a_ord = smem_u32(ord_s), a_pos = smem_u32(pos_s), a_wrec = smem_u32(wrec),
+                   a_cand = smem_u32(cand), a_map = smem_u32(map_s), a_run = smem_u32(run_s),
+                   a_hist = smem_u32(hist_s), a_cnt = smem_u32(&cnt_s);
     // original index of my slot q
-    auto oid = [&](int q) -> uint32_t { return (uint32_t)(lo + ord_s[warp * 32 * P + q * 32 + lane]); };
+    auto oid = [&](int q) -> uint32_t { return (uint32_t)lo + lds_u16(a_ord + 2u * (warp * 32 * P + q * 32 + lane)); };
 
     // ---- state into registers ---------------------------------------------
     float fx[P], fy[P], fz[P], thr[P];
@@ -300,7 +304,7 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
     auto fold_one = [&](float sx32, float sy32, float sz32, uint32_t sidx, bool do_fold) {
         const int64_t li = (int64_t)sidx - lo;
         if (li >= 0 && li < ncta) {
-            const int sp = pos_s[li];
+            const int sp = (int)lds_u16(a_pos + 2u * (uint32_t)li);
             if (worker && sp / (32 * P) == warp && (sp & 31) == lane) tk |= 1u << ((sp % (32 * P)) >> 5);
         }
         if (!do_fold) return;
@@ -395,10 +399,10 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
                         const int slot = atomicAdd(&cnt_s, 1);
                         if (slot < kR - 1) {
                             const uint64_t kq = dbits(m[q]);
-                            uint4* c4 = reinterpret_cast<uint4*>(&cand[slot]);
-                            c4[0] = make_uint4((uint32_t)kq, (uint32_t)(kq >> 32),
-                                               oid(q), (tk >> q) & 1u);
-                            c4[1] = make_uint4(__float_as_uint(fx[q]), __float_as_uint(fy[q]), __float_as_uint(fz[q]), 0u);
+                            const uint32_t ca = a_cand + 32u * (uint32_t)slot;
+                            sts_v4(ca, make_uint4((uint32_t)kq, (uint32_t)(kq >> 32), oid(q), (tk >> q) & 1u));
+                            sts_v4(ca + 16u, make_uint4(__float_as_uint(fx[q]), __float_as_uint(fy[q]),
+                                                         __float_as_uint(fz[q]), 0u));
                         }
                     }
                 }
@@ -407,11 +411,11 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
             const uint32_t bidx = bv >= 0.0 ? oid(bq) : kNone;
             const int wl = warp_argmax_lane(bkey, bidx);
             if (wl < 0) {
-                if (lane == 0) { Rec z{}; z.idx = kNone; wrec[warp] = z; }
+                if (lane == 0) sts_v4(a_wrec + 32u * warp, make_uint4(0u, 0u, kNone, 0u));
             } else if (lane == wl) {
-                uint4* w4 = reinterpret_cast<uint4*>(&wrec[warp]);
-                w4[0] = make_uint4((uint32_t)bkey, (uint32_t)(bkey >> 32), bidx, (tk >> bq) & 1u);
-                w4[1] = make_uint4(__float_as_uint(bx), __float_as_uint(by), __float_as_uint(bz), 0u);
+                sts_v4(a_wrec + 32u * warp, make_uint4((uint32_t)bkey, (uint32_t)(bkey >> 32), bidx, (tk >> bq) & 1u));
+                sts_v4(a_wrec + 32u * warp + 16u,
+                       make_uint4(__float_as_uint(bx), __float_as_uint(by), __float_as_uint(bz), 0u));
             }
         }
         if (tdbg) { t1 = clock64(); tacc[1] += t1 - t0; t0 = t1; }
@@ -425,13 +429,19 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
             // C. CTA record set: header (the CTA max, candidate count) and
             // up to kR-1 threshold candidates, pushed to every CTA; each
             // sender announces its byte count on the peer's mbarrier.
-            const Rec wr = lane < kW ? wrec[lane] : Rec{0, 0, kNone, 0, 0.f, 0.f, 0.f, 0};
-            const int cl = warp_argmax_lane(rec_key(wr), wr.idx);
-            const Rec cr = wrec[cl < 0 ? 0 : cl];
+            const uint4 wr = lane < kW ? lds_v4(a_wrec + 32u * lane) : make_uint4(0u, 0u, kNone, 0u);
+            const int cl = warp_argmax_lane(((uint64_t)wr.y << 32) | wr.x, wr.z);
+            Rec cr;
+            {
+                const uint32_t ra = a_wrec + 32u * (uint32_t)(cl < 0 ? 0 : cl);
+                const uint4 c0 = lds_v4(ra), c1 = lds_v4(ra + 16u);
+                cr.klo = c0.x; cr.khi = c0.y; cr.idx = c0.z; cr.taken = c0.w;
+                cr.x = __uint_as_float(c1.x); cr.y = __uint_as_float(c1.y); cr.z = __uint_as_float(c1.z); cr.pad = 0;
+            }
             const uint32_t cr_idx = cl < 0 ? kNone : cr.idx;
-            const int n = cnt_s;
+            const int n = (int)lds_u32(a_cnt);
             __syncwarp();
-            if (lane == 0) cnt_s = 0;
+            if (lane == 0) sts_u32(a_cnt, 0u);
             const int nsend = n < kR - 1 ? n : kR - 1;
             if (tdbg) { t1 = clock64(); tacc[3] += t1 - t0; t0 = t1; }
             if (C == 1) {
@@ -442,7 +452,7 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
                         w = half ? make_uint4(__float_as_uint(cr.x), __float_as_uint(cr.y), __float_as_uint(cr.z), (uint32_t)n)
                                  : make_uint4(cr.klo, cr.khi, cr_idx, cr.taken);
                     else
-                        w = reinterpret_cast<const uint4*>(&cand[k - 1])[half];
+                        w = lds_v4(a_cand + 32u * (k - 1) + 16u * half);
                     reinterpret_cast<uint4*>(&slots[par][k])[half] = w;
                 }
                 __syncwarp();
@@ -455,8 +465,8 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
                     st_async_v4(rbase + 16, rbar, __float_as_uint(cr.x), __float_as_uint(cr.y), __float_as_uint(cr.z),
                                 (uint32_t)n);
                     for (int k = 0; k < nsend; ++k) {
-                        const uint4 w0 = reinterpret_cast<const uint4*>(&cand[k])[0];
-                        const uint4 w1 = reinterpret_cast<const uint4*>(&cand[k])[1];
+                        const uint4 w0 = lds_v4(a_cand + 32u * k);
+                        const uint4 w1 = lds_v4(a_cand + 32u * k + 16u);
                         st_async_v4(rbase + 32u * (k + 1), rbar, w0.x, w0.y, w0.z, w0.w);
                         st_async_v4(rbase + 32u * (k + 1) + 16, rbar, w1.x, w1.y, w1.z, w1.w);
                     }
@@ -467,14 +477,14 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
             if (tdbg) { t1 = clock64(); tacc[5] += t1 - t0; t0 = t1; }
 
             // D. headers in lanes < C; candidates compacted one per lane
-            const Rec* sl = slots[par];
+            const uint32_t a_sl = smem_u32(slots[par]);
             uint64_t hk = 0;
             uint32_t hidx = kNone, ht = 0;
             float hx = 0.f, hy = 0.f, hz = 0.f;
             int hcnt = 0;
             if (lane < (int)C) {
-                const uint4 h0 = reinterpret_cast<const uint4*>(&sl[lane * kR])[0];
-                const uint4 h1 = reinterpret_cast<const uint4*>(&sl[lane * kR])[1];
+                const uint4 h0 = lds_v4(a_sl + 32u * (lane * kR));
+                const uint4 h1 = lds_v4(a_sl + 32u * (lane * kR) + 16u);
                 hk = ((uint64_t)h0.y << 32) | h0.x;
                 hidx = h0.z; ht = h0.w;
                 hx = __uint_as_float(h1.x); hy = __uint_as_float(h1.y); hz = __uint_as_float(h1.z);
@@ -488,7 +498,7 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
             const int base = __popc(b0 & lt) + 2 * __popc(b1 & lt) + 4 * __popc(b2 & lt);
             const int ncand_all = __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
             for (int k = 0; k < hn; ++k)
-                if (base + k < 32) map_s[base + k] = (uint8_t)(lane * kR + 1 + k);
+                if (base + k < 32) sts_u8(a_map + base + k, (uint32_t)(lane * kR + 1 + k));
             overflow = overflow || ncand_all > 32;
             const int ncand = ncand_all < 32 ? ncand_all : 32;
             __syncwarp();
@@ -496,9 +506,9 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
             uint32_t ci = kNone, ct = 0;
             float cx = 0.f, cy = 0.f, cz = 0.f;
             if (lane < ncand) {
-                const int j = map_s[lane];
-                const uint4 c0 = reinterpret_cast<const uint4*>(&sl[j])[0];
-                const uint4 c1 = reinterpret_cast<const uint4*>(&sl[j])[1];
+                const int j = (int)lds_u8(a_map + lane);
+                const uint4 c0 = lds_v4(a_sl + 32u * j);
+                const uint4 c1 = lds_v4(a_sl + 32u * j + 16u);
                 cm = bitsd(((uint64_t)c0.y << 32) | c0.x);
                 ci = c0.z; ct = c0.w;
                 cx = __uint_as_float(c1.x); cy = __uint_as_float(c1.y); cz = __uint_as_float(c1.z);
@@ -539,8 +549,8 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
                         }
                     } else {
                         if (lane == 0) {
-                            run_s[0] = make_float4(sx, sy, sz, __uint_as_float(wi));
-                            hist_s[hc & 31] = wm;
+                            sts_v4(a_run, make_uint4(__float_as_uint(sx), __float_as_uint(sy), __float_as_uint(sz), wi));
+                            sts_f64(a_hist + 8u * (hc & 31), wm);
                             st_release_cta(&pub_s, tag | 1u);
                         }
                         ++itl;
@@ -567,8 +577,8 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
                 // the reference's float64 update of every other candidate
                 const double d = sqdist((double)sx, (double)sy, (double)sz, (double)cx, (double)cy, (double)cz);
                 if (win) {
-                    run_s[rnl] = make_float4(cx, cy, cz, __uint_as_float(ci));
-                    hist_s[(hc + rnl) & 31] = cm;
+                    sts_v4(a_run + 16u * rnl, make_uint4(__float_as_uint(cx), __float_as_uint(cy), __float_as_uint(cz), ci));
+                    sts_f64(a_hist + 8u * ((hc + rnl) & 31), cm);
                     st_release_cta(&pub_s, tag | (uint32_t)(rnl + 1));
                 }
                 alive = alive && !win;
@@ -594,8 +604,8 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
             uint64_t tnew = kTauOff;
             if (hc >= 3 && target > 0.0) {
                 const int L = hc - 1 < 16 ? hc - 1 : 16;
-                const double m0 = hist_s[(hc - 1) & 31];
-                const double mL = hist_s[(hc - 1 - L) & 31];
+                const double m0 = lds_f64(a_hist + 8u * ((hc - 1) & 31));
+                const double mL = lds_f64(a_hist + 8u * ((hc - 1 - L) & 31));
                 const double stepv = fmax((mL - m0) * (double)__frcp_rn((float)L), m0 * 2.44140625e-4);
                 const double tv = m0 - (double)gain * target * stepv;
                 if (tv > 0.0 && tv < kInf) tnew = dbits(tv);
@@ -608,8 +618,8 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
             // the run's out / curve entries, one store batch (after the
             // release stores, so no publish waits on global stores)
             if (r == 0 && lane < rnl) {
-                out[it + lane] = (int64_t)__float_as_uint(run_s[lane].w);
-                curve[it + lane] = hist_s[(hbase + lane) & 31];
+                out[it + lane] = (int64_t)lds_u32(a_run + 16u * lane + 12u);
+                curve[it + lane] = lds_f64(a_hist + 8u * ((hbase + lane) & 31));
             }
         } else {
             // fold each pick as soon as the lead warp publishes it
@@ -624,8 +634,9 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
                     continue;
                 }
                 for (; k < n; ++k) {
-                    const float4 rv = run_s[k];
-                    fold_one(rv.x, rv.y, rv.z, __float_as_uint(rv.w), it + k < k_stop - 1);
+                    const uint4 rv = lds_v4(a_run + 16u * k);
+                    fold_one(__uint_as_float(rv.x), __uint_as_float(rv.y), __uint_as_float(rv.z), rv.w,
+                             it + k < k_stop - 1);
                 }
                 if ((pw & 0xffff0000u) == tag && (pw & 0x100u)) break;
             }
