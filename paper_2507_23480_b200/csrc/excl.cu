@@ -345,7 +345,9 @@ __global__ void grid_scatter_kernel(const float4* __restrict__ xyz, int64_t B, i
         const int c = g.cell_of[t];
         const int pos = atomicAdd(&g.cursor[b * (int64_t)g.max_cells + c], 1);
         g.sorted_idx[b * N + pos] = (int32_t)(t - b * N);
-        g.sorted_xyz[b * N + pos] = xyz[t];
+        float4 v = xyz[t];
+        v.w = __int_as_float((int)(t - b * N));  // the original index rides in w (no second load per hit)
+        g.sorted_xyz[b * N + pos] = v;
     }
 }
 
@@ -774,11 +776,13 @@ __global__ void __launch_bounds__(kEllWarps * 32, 4) grid_ell_kernel(int64_t B, 
             const int t = tbase[warp][rr] + f;
             bool hit = false;
             double d = 0.0;
+            int32_t qi = 0;
             if (f < total) {
                 const float4 q = sx[t];
                 if (no_filter || sqdist_f32(p, q) < thr) {
                     d = sqdist4(p, q);
                     hit = d < r2;
+                    qi = __float_as_int(q.w);
                 }
             }
             const unsigned hm = __ballot_sync(kFull, hit);
@@ -790,7 +794,7 @@ __global__ void __launch_bounds__(kEllWarps * 32, 4) grid_ell_kernel(int64_t B, 
                     int bk = 0;
                     for (int l = 0; l < L; ++l) bk += (lvb[warp][l] <= db) ? 1 : 0;
                     hd[warp][slot] = d;
-                    hj[warp][slot] = si[t];
+                    hj[warp][slot] = qi;
                     hb[warp][slot] = (uint8_t)atomicAdd(&hcnt[warp][bk], 1);  // rank within bucket
                     hk[warp][slot] = (uint8_t)bk;
                 }
