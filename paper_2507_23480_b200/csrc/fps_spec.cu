@@ -67,7 +67,7 @@ constexpr int kMaxS = 4096;          // points per CTA the spatial sort holds
 constexpr int64_t kSortMinIters = 256;  // runs shorter than this keep the index order
 constexpr float kInfF = __builtin_huge_valf();
 
-template <int P, int T>
+template <int P, int T, bool kLeadPts>
 __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
     static_assert(P > 0 && P <= 16, "register-resident clouds only");
     constexpr int kW = T / 32;
@@ -78,7 +78,8 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
     // pick_micro.cu -- but idling its SMSP's three other warps cost more
     // fold throughput than it saved: profiles/r01/fps_spec.log.)
     constexpr int kLead = kW - 1;
-    constexpr int TW = T - 32;  // point-owning (worker) threads
+    // kLeadPts: the lead warp owns points too (clouds that need all T threads)
+    constexpr int TW = kLeadPts ? T : T - 32;  // point-owning (worker) threads
     __shared__ Rec wrec[kW];
     __shared__ Rec cand[kR - 1];
     __shared__ Rec slots[2][kMaxCluster * kR];
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
     __shared__ __align__(8) uint64_t bars[2];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const bool worker = warp != kLead;
+    const bool worker = kLeadPts || warp != kLead;
     const uint32_t C = cluster_nctarank();
     const uint32_t r = cluster_ctarank();
     const int64_t b = cluster_id_x();
@@ -621,6 +622,13 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
                 out[it + lane] = (int64_t)lds_u32(a_run + 16u * lane + 12u);
                 curve[it + lane] = lds_f64(a_hist + 8u * ((hbase + lane) & 31));
             }
+            if (kLeadPts) {  // the lead's own points
+                for (int k = 0; k < rnl; ++k) {
+                    const uint4 rv = lds_v4(a_run + 16u * k);
+                    fold_one(__uint_as_float(rv.x), __uint_as_float(rv.y), __uint_as_float(rv.z), rv.w,
+                             it + k < k_stop - 1);
+                }
+            }
         } else {
             // fold each pick as soon as the lead warp publishes it
             int k = 0;
@@ -716,9 +724,9 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
     cluster_sync_all();
 }
 
-template <int P, int T>
+template <int P, int T, bool kLeadPts>
 cudaError_t launch_spec(const FpsArgs& a, int64_t B, int C, cudaStream_t s) {
-    auto kern = fps_spec_kernel<P, T>;
+    auto kern = fps_spec_kernel<P, T, kLeadPts>;
     cudaError_t e = cudaSuccess;
     if (C > 8) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -746,7 +754,7 @@ cudaError_t launch_fps_spec(FpsArgs a, int64_t B, cudaStream_t s) {
     int C = 1, P = 0, T = 256;
     fps_choose_cluster(a.N, B, &C, &P, &T);
     if (P == 0) return cudaErrorNotSupported;
-    // one warp per CTA leads the exchange and owns no points
+    // one warp per CTA leads the exchange and owns no points (below)
     const int64_t S = (a.N + C - 1) / C;
     P = 0;
     for (int t : {512, 256}) {
@@ -759,6 +767,9 @@ cudaError_t launch_fps_spec(FpsArgs a, int64_t B, cudaStream_t s) {
             if ((int64_t)ps[i] * tw >= S) { P = ps[i]; T = t; }
         if (P) break;
     }
+    // up to 4096 points per CTA: the lead warp owns points as well
+    const bool lead_pts = P == 0 && S <= 8 * 512;
+    if (lead_pts) { P = 8; T = 512; }
     if (P == 0) return cudaErrorNotSupported;
     a.points_per_cta = S;
     a.dbg = nullptr;
@@ -774,10 +785,12 @@ cudaError_t launch_fps_spec(FpsArgs a, int64_t B, cudaStream_t s) {
         a.dbg = dbg;
     }
     if (getenv("PS_FPS_VERBOSE"))
-        fprintf(stderr, "[fps-spec] N=%lld B=%lld C=%d P=%d T=%d\n", (long long)a.N, (long long)B, C, P, T);
+        fprintf(stderr, "[fps-spec] N=%lld B=%lld C=%d P=%d T=%d lead_pts=%d\n", (long long)a.N, (long long)B, C, P,
+                T, (int)lead_pts);
     cudaError_t e = cudaErrorNotSupported;
 #define PS_SPEC_CASE(PP, TT) \
-    case PP: e = launch_spec<PP, TT>(a, B, C, s); break;
+    case PP: e = launch_spec<PP, TT, false>(a, B, C, s); break;
+    if (lead_pts) return launch_spec<8, 512, true>(a, B, C, s);
     switch (P) {
         PS_SPEC_CASE(1, 512)
         PS_SPEC_CASE(2, 512)

@@ -126,6 +126,30 @@ def test_fps_register_kernels_across_cluster_widths(kernel, C, monkeypatch):
 
 
 @pytest.mark.timeout(300)
+@pytest.mark.parametrize("family", ["room-surfaces", "lattice", "half-duplicates"])
+def test_fps_speculative_lead_owns_points(family, monkeypatch):
+    """The speculative kernel's variant for 3841..4096 points per CTA (the
+    lead warp owns points too; C4-sized clouds at C = 16) against the oracle,
+    full run and early stop."""
+    monkeypatch.setenv("PS_FPS_CLUSTER", "16")
+    N = 64000
+    if family == "half-duplicates":
+        base = generate_cloud("uniform-box", N // 2, 11)
+        c = np.concatenate([base, base])[np.random.default_rng(3).permutation(N)].copy()
+    else:
+        c = generate_cloud(family, N, 11)
+    for n, k_stop in ((1200, 1200), (1200, 500)):
+        xyz4 = engine.as_xyz4(torch.from_numpy(c[None]).cuda())
+        idx, curve, md, taken = engine.fps(xyz4, n, seed_index=N // 9, k_stop=k_stop)
+        ri, rc, rmd, rtk, _ = O.fps(c, n, N // 9, k_stop=k_stop)
+        msg = f"{family} k_stop={k_stop}"
+        np.testing.assert_array_equal(idx[0].cpu().numpy()[:k_stop], ri[:k_stop], err_msg=msg)
+        np.testing.assert_array_equal(curve[0].cpu().numpy()[:k_stop], rc[:k_stop], err_msg=msg)
+        np.testing.assert_array_equal(md[0].cpu().numpy(), rmd, err_msg=msg)
+        np.testing.assert_array_equal(taken[0].cpu().numpy(), rtk, err_msg=msg)
+
+
+@pytest.mark.timeout(300)
 @pytest.mark.parametrize("family,N,n,G,B", [
     ("room-surfaces", 24000, 3000, 2, 1), ("room-surfaces", 24000, 3000, 4, 2), ("lattice", 4913, 1200, 3, 1),
     ("uniform-box", 200000, 1500, 4, 1), ("gaussian-clusters", 9000, 900, 8, 1), ("uniform-box", 4096, 1024, 1, 1),
