@@ -284,12 +284,15 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
     // lead warp: ring of the last 32 squared curve values, for the threshold
     int hc = 0;
     float gain = 1.0f;
+    bool tau_boot = false;  // lead: the threshold in use came from the CTA maxima
     if (warp == kLead && !a.fresh && k_start < k_stop) {
-        const int nh = k_start - 1 >= 32 ? 32 : (k_start - 1 > 0 ? (int)(k_start - 1) : 0);
-        if (lane < nh) {
-            const double c = curve[k_start - 1 - lane];  // previous call's epilogue stored sqrt
-            hist_s[(nh - 1 - lane) & 31] = c * c;
-        }
+        // the most recent finite curve values only: positions filled by the
+        // sampler carry +inf and say nothing about the current md
+        const int avail = k_start - 1 >= 32 ? 32 : (k_start - 1 > 0 ? (int)(k_start - 1) : 0);
+        const double c = lane < avail ? curve[k_start - 1 - lane] : kInf;  // previous epilogue stored sqrt
+        const uint32_t fin = __ballot_sync(kFull, lane < avail && c < kInf);
+        const int nh = __ffs(~fin) - 1 < 0 ? 32 : __ffs(~fin) - 1;  // unbroken finite run from the end
+        if (lane < nh) hist_s[(nh - 1 - lane) & 31] = c * c;
         hc = nh;
     }
     uint64_t tau = kTauOff;
@@ -597,12 +600,27 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
             // ahead along its recent slope, gain corrected by the observed count
             // development override (PS_SPEC_TARGET; < 0: no speculation)
             const double target = a.dbg_t0 > 0 ? (double)a.dbg_t0 * 1e-3 : (a.dbg_t0 == -1 ? -1.0 : kTarget);
-            if (tau != kTauOff) {
+            if (tau != kTauOff && !tau_boot) {  // a bootstrap threshold says nothing about the gain
                 if (overflow || ctot > (int)(2 * target)) gain *= 0.7f;
                 else if (ctot < (int)(target / 2)) gain *= 1.3f;
                 gain = fminf(fmaxf(gain, 0.05f), 20.0f);
             }
             uint64_t tnew = kTauOff;
+            tau_boot = hc < 3 && target > 0.0;
+            if (tau_boot) {
+                // no curve history yet: the third-largest CTA maximum of this
+                // exchange (a few candidates per exchange until the slope exists)
+                uint64_t hk2 = hidx != kNone ? hk : 0ull;
+                uint32_t hi2 = hidx;
+#pragma unroll
+                for (int rep3 = 0; rep3 < 3; ++rep3) {
+                    const int wl = warp_argmax_lane(hk2, hi2);
+                    if (wl < 0) { hk2 = 0ull; break; }
+                    const uint64_t top = __shfl_sync(kFull, hk2, wl);
+                    if (rep3 == 2) { tnew = top > 0ull ? top : kTauOff; break; }
+                    if (lane == wl) { hk2 = 0ull; hi2 = kNone; }
+                }
+            }
             if (hc >= 3 && target > 0.0) {
                 const int L = hc - 1 < 16 ? hc - 1 : 16;
                 const double m0 = lds_f64(a_hist + 8u * ((hc - 1) & 31));
