@@ -413,9 +413,11 @@ def main_ours(args):
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": traffic, "algorithmic_bytes": alg[dom],
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if "hbm_gbs" in pk else "fallback 6.65 TB/s",
-                "note": ("algorithmic bytes per SURVEY 8d (28 B per point-iteration for FPS); the K1 kernel keeps "
-                         "xyz/md in registers, so measured DRAM traffic is ~1000x lower and the kernel is "
-                         "iteration-latency bound")}
+                "note": ("algorithmic bytes per SURVEY 8d (28 B per point-iteration for FPS, the bytes a kernel "
+                         "streaming xyz/md every iteration would move); K1 keeps xyz/md in registers (measured "
+                         "DRAM traffic ~1000x lower) and certifies several samples per exchange, so frac compares "
+                         "it with such a streaming kernel at HBM speed -- it is bound by its exchange/pick "
+                         "latency chain, not by DRAM")}
 
     # ---- C5 point split: one 2^20-point cloud -> 65536 samples ---------
     c5 = c2 = c4 = None
