@@ -143,7 +143,7 @@ int ps_fps(const float* xyz4, int64_t B, int64_t N, double* md, uint8_t* taken, 
 
 int64_t ps_fps_mailbox_bytes(int64_t B, int32_t G) {
     if (B < 1 || G < 1) return 0;
-    return B * 3 * (int64_t)G * 2 * (int64_t)sizeof(uint4);
+    return B * 3 * (int64_t)G * ps::kMbRecs * 2 * (int64_t)sizeof(uint4);
 }
 
 int ps_fps_split_plan(int64_t N, int64_t B, int32_t G, int32_t Gl, int32_t* C_out, int32_t* P_out) {

@@ -32,6 +32,14 @@
 // The duplicate fallback of _kernels.py:65-70 (max <= 0 or winner taken ->
 // lowest untaken index) is a rare second exchange with the same structure.
 //
+// kSpec (default; PS_RES_NOSPEC=1 selects the loop above): the speculation of
+// fps_spec.cu at rank scale -- per exchange every CTA publishes its argmax and
+// its points with md >= tau, CTA 0 of each rank forwards the rank's header and
+// candidates to every rank's mailbox, and every lead warp picks the same run
+// (first pick = max over the headers, later picks = candidates still >= tau,
+// lowered by exact float64 distances).  C5 (2^20 -> 65536 over 10 virtual
+// ranks on one B200): 5.5 -> 1.07 us per sample.
+//
 // Bit-exactness: every md is the reference float64 value; the float32 tests
 // only skip folds that provably cannot change md (margins in common.cuh /
 // skip_threshold); ties resolve to the lowest original index at every level,
@@ -59,6 +67,9 @@ constexpr int kMaxP = 24;
 #endif
 constexpr bool kTiming = PS_TIMING;  // per-iteration cycle stamps (make TIMING=1)
 constexpr uint32_t kForeign = 0x7fffffffu;  // owner field of another rank's point (g field all ones)
+constexpr int kRc = 7;            // kSpec: threshold candidates a CTA publishes per exchange
+constexpr int kRS = kRc + 1;      // kSpec: records per CTA per exchange (header + candidates)
+constexpr uint64_t kTauOffR = ~0ull;
 
 struct __align__(16) Rec {
     uint32_t klo, khi, idx, own;  // own: bit31 taken | rank g << 18 | cta r << 14 | local sorted pos
@@ -69,6 +80,10 @@ struct __align__(16) Rec {
 PS_DEV uint64_t dbits(double d) { return (uint64_t)__double_as_longlong(d); }
 PS_DEV double bitsd(uint64_t k) { return __longlong_as_double((long long)k); }
 PS_DEV uint64_t rec_key(const Rec& r) { return ((uint64_t)r.khi << 32) | r.klo; }
+// (key desc, idx asc): true if (ka, ia) ranks above (kb, ib)
+PS_DEV bool ranks_above_r(uint64_t ka, uint32_t ia, uint64_t kb, uint32_t ib) {
+    return ka > kb || (ka == kb && ia < ib);
+}
 PS_DEV Rec none_rec() {
     Rec z;
     z.klo = z.khi = 0; z.idx = kNone; z.own = 0; z.x = z.y = z.z = 0.f; z.pad = 0;
@@ -123,8 +138,9 @@ PS_DEV uint32_t morton12(float x, float y, float z, float ox, float oy, float oz
 }
 
 // ---- global mailboxes (G > 1) ----------------------------------------------------
-// Mailbox of a rank: uint4[B][3][G][2]; set 0/1 = iteration parity, set 2 =
-// duplicate fallback.  A record is two 16-byte halves, each tagged with the
+// Mailbox of a rank: uint4[B][3][G][2 * kMbRecs]; set 0/1 = exchange parity,
+// set 2 = duplicate fallback; a slot holds one record (one-sample loop) or a
+// rank's meta record, header and up to 32 candidates (speculative loop).  A record is two 16-byte halves, each tagged with the
 // 32-bit sequence number, so a reader accepts it only when both halves carry
 // the expected tag (written by the owner with relaxed system-scope stores,
 // possibly from a peer GPU over NVLink).
@@ -164,7 +180,7 @@ PS_DEV Rec mbox_get(const uint4* slot, uint32_t seq) {
     return r;
 }
 
-template <int P>
+template <int P, bool kSpec>
 __global__ void __launch_bounds__(kT, 1) fps_res_kernel(FpsArgs a, FpsRanks rk) {
     constexpr int QG = P <= 8 ? P : (P % 8 == 0 ? 8 : 6);  // slots per screen group
     extern __shared__ __align__(16) unsigned char dsm[];
@@ -179,6 +195,17 @@ __global__ void __launch_bounds__(kT, 1) fps_res_kernel(FpsArgs a, FpsRanks rk) 
     __shared__ float red[6][kW];
     __shared__ uint32_t scan_tot[kW];
     __shared__ uint32_t cbound[kMaxC + 1];
+    // kSpec exchange state
+    __shared__ Rec cslots[kSpec ? 2 : 1][kSpec ? kMaxC * kRS : 1];
+    __shared__ Rec ccand_s[kRc];
+    __shared__ Rec cl_s[kSpec ? 32 : 1], cl_s2[kSpec ? 32 : 1], uh_s[kSpec ? 32 : 1];
+    __shared__ Rec gslot2;
+    __shared__ float4 run_s[32];
+    __shared__ uint32_t run_own_s[32];
+    __shared__ uint8_t run_fold_s[32];
+    __shared__ double hist_s[32];
+    __shared__ unsigned long long tau_s;
+    __shared__ int ccnt_s, rn_s, fb_s;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t C = cluster_nctarank();
@@ -375,14 +402,18 @@ __global__ void __launch_bounds__(kT, 1) fps_res_kernel(FpsArgs a, FpsRanks rk) 
     }
 
     if (tid == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
+        ccnt_s = 0;
+        mbar_init(&bars[0], kSpec ? C : 1);  // kSpec: one arrival per sending CTA
+        mbar_init(&bars[1], kSpec ? C : 1);
         fence_mbar_init_cluster();
-        mbar_arrive_expect_tx(&bars[0], tx_bytes);
-        mbar_arrive_expect_tx(&bars[1], tx_bytes);
+        if (!kSpec) {
+            mbar_arrive_expect_tx(&bars[0], tx_bytes);
+            mbar_arrive_expect_tx(&bars[1], tx_bytes);
+        }
     }
     cluster_sync_all();
 
+    if constexpr (!kSpec) {
     if (k_start < k_stop) {
         const int64_t last = a.fresh ? seed : out[k_start - 1];
         const float4 lv = xyz[last];
@@ -502,8 +533,8 @@ __global__ void __launch_bounds__(kT, 1) fps_res_kernel(FpsArgs a, FpsRanks rk) 
                 if (lane == 0) mbar_arrive_expect_tx(&bars[par], tx_bytes);
                 if (G > 1) {
                     const uint32_t seq = rk.seq_base + (uint32_t)it;
-                    if (r == 0 && lane < G) mbox_put(mb_dst + ((b * 3 + par) * G + g) * 2, cw, seq);
-                    const Rec pr = lane < G ? mbox_get(mb_mine + ((b * 3 + par) * G + lane) * 2, seq) : none_rec();
+                    if (r == 0 && lane < G) mbox_put(mb_dst + ((b * 3 + par) * G + g) * (2 * kMbRecs), cw, seq);
+                    const Rec pr = lane < G ? mbox_get(mb_mine + ((b * 3 + par) * G + lane) * (2 * kMbRecs), seq) : none_rec();
                     const int pl = argmax_lane(rec_key(pr), pr.idx);
                     if (lane == (pl < 0 ? 0 : pl)) {
                         Rec gw = pl < 0 ? none_rec() : pr;
@@ -577,8 +608,8 @@ __global__ void __launch_bounds__(kT, 1) fps_res_kernel(FpsArgs a, FpsRanks rk) 
                     const uint32_t seq = rk.seq_base + (uint32_t)it;
                     __syncthreads();
                     if (warp == kW - 1) {
-                        if (r == 0 && lane < G) mbox_put(mb_dst + ((b * 3 + 2) * G + g) * 2, fw, seq);
-                        const Rec pr = lane < G ? mbox_get(mb_mine + ((b * 3 + 2) * G + lane) * 2, seq) : none_rec();
+                        if (r == 0 && lane < G) mbox_put(mb_dst + ((b * 3 + 2) * G + g) * (2 * kMbRecs), fw, seq);
+                        const Rec pr = lane < G ? mbox_get(mb_mine + ((b * 3 + 2) * G + lane) * (2 * kMbRecs), seq) : none_rec();
                         const uint32_t pm = __reduce_min_sync(kFull, pr.idx);
                         const unsigned wv = __ballot_sync(kFull, pr.idx == pm && pr.idx != kNone);
                         if (lane == (wv ? __ffs(wv) - 1 : 0)) {
@@ -615,6 +646,514 @@ __global__ void __launch_bounds__(kT, 1) fps_res_kernel(FpsArgs a, FpsRanks rk) 
         }
     }
 
+    } else {
+        // ---- speculative exchange loop (kSpec) -----------------------------------
+        // As fps_spec.cu: every CTA publishes its argmax (header) and its points
+        // with md >= tau (candidates); with G > 1 ranks, CTA 0 of each rank
+        // forwards the rank's header and candidates to every rank's mailbox.
+        // Every lead warp of every CTA of every rank then picks identically:
+        // the max over the headers, then the best candidate while it stays
+        // >= tau (every other point is < tau and md only falls), lowering the
+        // other candidates by their exact float64 distance to each pick.  The
+        // run is broadcast on a named barrier and folded by every warp.
+        const uint32_t tag0 = rk.seq_base;
+        int rn = 0;
+        int hc = 0;
+        float gain = 1.0f;
+        bool tau_boot = false;
+        uint64_t tau = kTauOffR;
+        if (k_start < k_stop && tid == 0) {
+            const int64_t last = a.fresh ? seed : out[k_start - 1];  // refolded, as _kernels.py
+            const float4 lv = xyz[last];
+            run_s[0] = make_float4(lv.x, lv.y, lv.z, __uint_as_float((uint32_t)last));
+            run_own_s[0] = kForeign;  // already taken: fold only
+            run_fold_s[0] = 1;
+        }
+        if (k_start < k_stop) rn = 1;
+        if (warp == kW - 1 && !a.fresh && k_start < k_stop) {
+            const int avail = k_start - 1 >= 32 ? 32 : (k_start - 1 > 0 ? (int)(k_start - 1) : 0);
+            const double c = lane < avail ? curve[k_start - 1 - lane] : kInf;
+            const uint32_t fin = __ballot_sync(kFull, lane < avail && c < kInf);
+            const int nh = __ffs(~fin) - 1 < 0 ? 32 : __ffs(~fin) - 1;
+            if (lane < nh) hist_s[(nh - 1 - lane) & 31] = c * c;
+            hc = nh;
+        }
+        __syncthreads();
+        int64_t it = k_start;
+        uint32_t ex = 0;
+        while (it < k_stop) {
+            const uint32_t par = ex & 1u, phase = (ex >> 1) & 1u;
+            ++ex;
+            const uint32_t seq = tag0 + (uint32_t)it;
+
+            // A. fold the run (warp skip per sample), then refresh the warp record
+            uint32_t chg = 0;
+            for (int k = 0; k < rn; ++k) {
+                const float4 sv = run_s[k];
+                const uint32_t sown = run_own_s[k];
+                const uint32_t own = sown & 0x7fffffffu;
+                if (sown != kForeign && (own >> 18) == (uint32_t)g && ((own >> 14) & 15u) == r) {
+                    const uint32_t lp = own & 0x3fffu;
+                    if ((int)(lp / (32 * P)) == warp) {
+                        force = true;  // the record's taken flag changes
+                        if ((int)(lp & 31u) == lane) tk |= 1u << ((lp >> 5) % P);
+                    }
+                }
+                if (!run_fold_s[k]) continue;
+                const float sx32 = sv.x, sy32 = sv.y, sz32 = sv.z;
+                const float gx = fmaxf(fmaxf(__fsub_rd(wb[0], sx32), __fsub_rd(sx32, wb[3])), 0.f);
+                const float gy = fmaxf(fmaxf(__fsub_rd(wb[1], sy32), __fsub_rd(sy32, wb[4])), 0.f);
+                const float gz = fmaxf(fmaxf(__fsub_rd(wb[2], sz32), __fsub_rd(sz32, wb[5])), 0.f);
+                const float lb = __fadd_rd(__fadd_rd(__fmul_rd(gx, gx), __fmul_rd(gy, gy)), __fmul_rd(gz, gz));
+                if (!(lb > thr_w)) {
+                    const double sx = sx32, sy = sy32, sz = sz32;
+#pragma unroll
+                    for (int q0 = 0; q0 < P; q0 += QG) {
+                        float4 v[QG];
+#pragma unroll
+                        for (int u = 0; u < QG; ++u) v[u] = pts[wbase + (q0 + u) * 32 + lane];
+                        uint32_t need = 0;
+#pragma unroll
+                        for (int u = 0; u < QG; ++u) {
+                            const float dx = v[u].x - sx32, dy = v[u].y - sy32, dz = v[u].z - sz32;
+                            const float d32 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+                            need |= (!(d32 > thr[q0 + u]) ? 1u : 0u) << u;
+                        }
+                        if (__any_sync(kFull, need != 0)) {
+#pragma unroll
+                            for (int u = 0; u < QG; ++u) {
+                                const double d = sqdist(sx, sy, sz, (double)v[u].x, (double)v[u].y, (double)v[u].z);
+                                const bool upd = ((need >> u) & 1u) && d < m[q0 + u];
+                                m[q0 + u] = upd ? d : m[q0 + u];
+                                thr[q0 + u] = upd ? skip_thr_nb(d) : thr[q0 + u];
+                                chg |= (upd ? 1u : 0u) << (q0 + u);
+                            }
+                        }
+                    }
+                }
+            }
+            const bool redo = force || ((chg >> bq) & 1u);
+            if (__any_sync(kFull, chg != 0 || force)) {
+                if (redo) {
+                    bk = 0; bq = 0; bo = kNone;
+#pragma unroll
+                    for (int q = 0; q < P; ++q) {
+                        const uint32_t o = __float_as_uint(pts[wbase + q * 32 + lane].w);
+                        const uint64_t kq = dbits(m[q]);
+                        if (((valid >> q) & 1u) && (bo == kNone || kq > bk || (kq == bk && o < bo))) {
+                            bk = kq; bq = q; bo = o;
+                        }
+                    }
+                }
+                const int wl = argmax_lane(bk, bo);
+                if (wl < 0) {
+                    thr_w = -1.0f;
+                    if (lane == 0) warp_rec[warp] = none_rec();
+                } else {
+                    const uint64_t wk = __shfl_sync(kFull, bk, wl);
+                    thr_w = skip_thr(bitsd(wk));
+                    if (lane == wl) {
+                        const int lp = wbase + bq * 32 + lane;
+                        const float4 v = pts[lp];
+                        Rec rr;
+                        rr.klo = (uint32_t)bk; rr.khi = (uint32_t)(bk >> 32);
+                        rr.idx = bo;
+                        rr.own = (((tk >> bq) & 1u) << 31) | ((uint32_t)g << 18) | (r << 14) | (uint32_t)lp;
+                        rr.x = v.x; rr.y = v.y; rr.z = v.z; rr.pad = 0;
+                        warp_rec[warp] = rr;
+                    }
+                }
+                force = false;
+            }
+            // B. candidates: my points with md >= tau
+            {
+                uint32_t cmask = 0;
+#pragma unroll
+                for (int q = 0; q < P; ++q) cmask |= ((((valid >> q) & 1u) && dbits(m[q]) >= tau) ? 1u : 0u) << q;
+                if (__any_sync(kFull, cmask != 0)) {
+#pragma unroll
+                    for (int q = 0; q < P; ++q) {
+                        if ((cmask >> q) & 1u) {
+                            const int slot = atomicAdd(&ccnt_s, 1);
+                            if (slot < kRc) {
+                                const int lp = wbase + q * 32 + lane;
+                                const float4 v = pts[lp];
+                                Rec rr;
+                                const uint64_t kq = dbits(m[q]);
+                                rr.klo = (uint32_t)kq; rr.khi = (uint32_t)(kq >> 32);
+                                rr.idx = __float_as_uint(v.w);
+                                rr.own = (((tk >> q) & 1u) << 31) | ((uint32_t)g << 18) | (r << 14) | (uint32_t)lp;
+                                rr.x = v.x; rr.y = v.y; rr.z = v.z; rr.pad = 0;
+                                ccand_s[slot] = rr;
+                            }
+                        }
+                    }
+                }
+            }
+
+            if (warp == kW - 1) {
+                named_bar_sync(1, kT);
+                // C. CTA header + candidates to every CTA of the cluster
+                const Rec wr = lane < kW ? warp_rec[lane] : none_rec();
+                const int cl = argmax_lane(rec_key(wr), wr.idx);
+                const Rec cr = cl < 0 ? none_rec() : warp_rec[cl];
+                const int n = ccnt_s;
+                __syncwarp();
+                if (lane == 0) ccnt_s = 0;
+                const int nsend = n < kRc ? n : kRc;
+                if (C == 1) {
+                    if (lane < 1 + nsend) {
+                        Rec x = lane == 0 ? cr : ccand_s[lane - 1];
+                        if (lane == 0) x.pad = (uint32_t)n;
+                        cslots[par][lane] = x;
+                    }
+                    __syncwarp();
+                } else if (lane < (int)C) {
+                    const uint32_t rbar = mapa(smem_u32(&bars[par]), (uint32_t)lane);
+                    const uint32_t rbase = mapa(smem_u32(&cslots[par][r * kRS]), (uint32_t)lane);
+                    mbar_remote_arrive_expect_tx(rbar, (uint32_t)(1 + nsend) * (uint32_t)sizeof(Rec));
+                    st_async_v4(rbase, rbar, cr.klo, cr.khi, cr.idx, cr.own);
+                    st_async_v4(rbase + 16, rbar, __float_as_uint(cr.x), __float_as_uint(cr.y), __float_as_uint(cr.z),
+                                (uint32_t)n);
+                    for (int k = 0; k < nsend; ++k) {
+                        const Rec x = ccand_s[k];
+                        st_async_v4(rbase + 32u * (k + 1), rbar, x.klo, x.khi, x.idx, x.own);
+                        st_async_v4(rbase + 32u * (k + 1) + 16, rbar, __float_as_uint(x.x), __float_as_uint(x.y),
+                                    __float_as_uint(x.z), 0u);
+                    }
+                }
+                if (C > 1) mbar_wait_cta(&bars[par], phase);
+
+                // D. units: the C CTAs (G == 1) or the G ranks (G > 1).  Unit
+                // headers to uh_s, candidates compacted to cl_s.
+                // cluster level: headers in lanes < C, counts, candidate prefix
+                Rec h = lane < (int)C ? cslots[par][lane * kRS] : none_rec();
+                const int hcnt = lane < (int)C ? (int)h.pad : 0;
+                bool ovf = __any_sync(kFull, hcnt > kRc);
+                const int hn = hcnt < kRc ? hcnt : kRc;
+                const uint32_t lt = (1u << lane) - 1u;
+                const uint32_t b0 = __ballot_sync(kFull, hn & 1), b1 = __ballot_sync(kFull, hn & 2),
+                               b2 = __ballot_sync(kFull, hn & 4);
+                const int cbase = __popc(b0 & lt) + 2 * __popc(b1 & lt) + 4 * __popc(b2 & lt);
+                const int cn_all = __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
+                ovf = ovf || cn_all > 32;
+                for (int k = 0; k < hn; ++k)
+                    if (cbase + k < 32) cl_s[cbase + k] = cslots[par][lane * kRS + 1 + k];
+                const int cn = cn_all < 32 ? cn_all : 32;
+                int nunits, ncand;
+                if (G == 1) {
+                    if (lane < (int)C) uh_s[lane] = h;
+                    nunits = (int)C;
+                    ncand = cn;
+                } else {
+                    // my rank: header = max over my CTAs (owner fields kept)
+                    const int hl = argmax_lane(rec_key(h), h.idx);
+                    const Rec rh = hl < 0 ? none_rec() : cslots[par][hl * kRS];
+                    __syncwarp();
+                    if (r == 0) {
+                        // forward my rank's set: meta, header, candidates
+                        uint4* mb = lane < G ? rk.mbox[lane] : nullptr;
+                        if (lane < G) {
+                            uint4* sl = mb + ((b * 3 + par) * G + g) * (2 * kMbRecs);
+                            for (int k = 0; k < cn; ++k) mbox_put(sl + 2 * (2 + k), cl_s[k], seq);
+                            mbox_put(sl + 2, rh, seq);
+                            st_sys_v4(sl + 1, make_uint4(0u, 0u, 0u, seq));
+                            st_sys_v4(sl, make_uint4((uint32_t)cn, ovf ? 1u : 0u, 0u, seq));
+                        }
+                    }
+                    // every rank's set: mine from the cluster, others from my mailbox
+                    const uint4* mine = mb_mine + ((b * 3 + par) * G) * (2 * kMbRecs);
+                    Rec uh = none_rec();
+                    int ucnt = 0;
+                    bool uovf = false;
+                    if (lane < G) {
+                        if (lane == g) {
+                            uh = rh;
+                            ucnt = cn;
+                            uovf = ovf;
+                        } else {
+                            const uint4* sl = mine + lane * (2 * kMbRecs);
+                            uint4 m0, m1;
+                            do {
+                                m0 = ld_sys_v4(sl);
+                                m1 = ld_sys_v4(sl + 1);
+                            } while (m0.w != seq || m1.w != seq);
+                            ucnt = (int)m0.x;
+                            uovf = m0.y != 0u;
+                            uh = mbox_get(sl + 2, seq);
+                        }
+                    }
+                    ovf = __any_sync(kFull, uovf);
+                    if (lane < G) uh_s[lane] = uh;
+                    // candidate prefix over the ranks (counts <= 32: five ballots)
+                    const uint32_t u0 = __ballot_sync(kFull, ucnt & 1), u1 = __ballot_sync(kFull, ucnt & 2),
+                                   u2 = __ballot_sync(kFull, ucnt & 4), u3 = __ballot_sync(kFull, ucnt & 8),
+                                   u4 = __ballot_sync(kFull, ucnt & 16), u5 = __ballot_sync(kFull, ucnt & 32);
+                    const int ubase = __popc(u0 & lt) + 2 * __popc(u1 & lt) + 4 * __popc(u2 & lt) +
+                                      8 * __popc(u3 & lt) + 16 * __popc(u4 & lt) + 32 * __popc(u5 & lt);
+                    const int un_all = __popc(u0) + 2 * __popc(u1) + 4 * __popc(u2) + 8 * __popc(u3) +
+                                       16 * __popc(u4) + 32 * __popc(u5);
+                    ovf = ovf || un_all > 32;
+                    __syncwarp();
+                    // my rank's candidates move from cl_s to their rank position
+                    Rec minec[2];
+                    const int mybase = __shfl_sync(kFull, ubase, g);
+                    minec[0] = lane < cn ? cl_s[lane] : none_rec();
+                    __syncwarp();
+                    if (lane < cn && mybase + lane < 32) cl_s2[mybase + lane] = minec[0];
+                    if (lane < G && lane != g) {
+                        const uint4* sl = mine + lane * (2 * kMbRecs);
+                        for (int k = 0; k < ucnt; ++k)
+                            if (ubase + k < 32) cl_s2[ubase + k] = mbox_get(sl + 2 * (2 + k), seq);
+                    }
+                    __syncwarp();
+                    const int unn = un_all < 32 ? un_all : 32;
+                    if (lane < unn) cl_s[lane] = cl_s2[lane];
+                    __syncwarp();
+                    nunits = G;
+                    ncand = unn;
+                }
+                __syncwarp();
+
+                // E. picks (identical in every lead warp of every CTA and rank)
+                Rec uh2 = lane < nunits ? uh_s[lane] : none_rec();
+                Rec cc = lane < ncand ? cl_s[lane] : none_rec();
+                double cm = bitsd(rec_key(cc));
+                const uint32_t ct = (cc.own >> 31) & 1u;
+                ovf = ovf || __any_sync(kFull, lane < ncand && ct);
+                bool alive = lane < ncand;
+                int rnl = 0, fb = 0;
+                int64_t itl = it;
+                const bool hv = uh2.idx != kNone;
+                {
+                    const bool use_c = alive && (!hv || ranks_above_r(dbits(cm), cc.idx, rec_key(uh2), uh2.idx));
+                    const uint64_t k0 = use_c ? dbits(cm) : rec_key(uh2);
+                    const uint32_t i0 = use_c ? cc.idx : (hv ? uh2.idx : kNone);
+                    const int wl = argmax_lane(k0, i0);
+                    if (wl >= 0) {
+                        const uint64_t wk = __shfl_sync(kFull, k0, wl);
+                        const uint32_t wi = __shfl_sync(kFull, i0, wl);
+                        const bool wc = __shfl_sync(kFull, use_c ? 1 : 0, wl);
+                        const uint32_t wown = __shfl_sync(kFull, use_c ? cc.own : uh2.own, wl);
+                        const float sx = __shfl_sync(kFull, use_c ? cc.x : uh2.x, wl);
+                        const float sy = __shfl_sync(kFull, use_c ? cc.y : uh2.y, wl);
+                        const float sz = __shfl_sync(kFull, use_c ? cc.z : uh2.z, wl);
+                        (void)wc;
+                        const double wm = bitsd(wk);
+                        if (!(wm > 0.0) || ((wown >> 31) & 1u)) {
+                            fb = 1;
+                            if (lane == 0) {
+                                Rec w = none_rec();
+                                w.klo = (uint32_t)wk; w.khi = (uint32_t)(wk >> 32); w.idx = wi; w.own = wown;
+                                w.x = sx; w.y = sy; w.z = sz;
+                                gslot = w;
+                            }
+                        } else {
+                            if (lane == 0) {
+                                run_s[0] = make_float4(sx, sy, sz, __uint_as_float(wi));
+                                run_own_s[0] = wown;
+                                hist_s[hc & 31] = wm;
+                            }
+                            ++itl;
+                            rnl = 1;
+                            alive = alive && cc.idx != wi && !ovf;
+                            if (alive) {
+                                const double d = sqdist((double)sx, (double)sy, (double)sz, (double)cc.x, (double)cc.y,
+                                                        (double)cc.z);
+                                if (dbits(d) < dbits(cm)) cm = d;
+                            }
+                        }
+                    }
+                }
+                while (rnl > 0 && itl < k_stop && rnl < 31) {
+                    alive = alive && dbits(cm) >= tau;
+                    const int wl = argmax_lane(alive ? dbits(cm) : 0ull, alive ? cc.idx : kNone);
+                    if (wl < 0) break;
+                    const bool win = lane == wl;
+                    const float sx = __shfl_sync(kFull, cc.x, wl);
+                    const float sy = __shfl_sync(kFull, cc.y, wl);
+                    const float sz = __shfl_sync(kFull, cc.z, wl);
+                    const double d = sqdist((double)sx, (double)sy, (double)sz, (double)cc.x, (double)cc.y, (double)cc.z);
+                    if (win) {
+                        run_s[rnl] = make_float4(cc.x, cc.y, cc.z, __uint_as_float(cc.idx));
+                        run_own_s[rnl] = cc.own;
+                        hist_s[(hc + rnl) & 31] = cm;
+                    }
+                    alive = alive && !win;
+                    cm = (alive && dbits(d) < dbits(cm)) ? d : cm;
+                    ++itl;
+                    ++rnl;
+                }
+                const int hbase = hc;
+                hc += rnl;
+                __syncwarp();
+                // next threshold (as fps_spec.cu)
+                if (tau != kTauOffR && !tau_boot) {
+                    if (ovf || ncand > 44) gain *= 0.7f;
+                    else if (ncand < 11) gain *= 1.3f;
+                    gain = fminf(fmaxf(gain, 0.05f), 20.0f);
+                }
+                uint64_t tnew = kTauOffR;
+                tau_boot = hc < 3;
+                if (tau_boot) {
+                    uint64_t hk2 = hv ? rec_key(uh2) : 0ull;
+                    uint32_t hi2 = uh2.idx;
+#pragma unroll
+                    for (int rep3 = 0; rep3 < 3; ++rep3) {
+                        const int wl = argmax_lane(hk2, hi2);
+                        if (wl < 0) break;
+                        const uint64_t top = __shfl_sync(kFull, hk2, wl);
+                        if (rep3 == 2) { tnew = top > 0ull ? top : kTauOffR; break; }
+                        if (lane == wl) { hk2 = 0ull; hi2 = kNone; }
+                    }
+                } else {
+                    const int L = hc - 1 < 16 ? hc - 1 : 16;
+                    const double m0 = hist_s[(hc - 1) & 31];
+                    const double mL = hist_s[(hc - 1 - L) & 31];
+                    const double stepv = fmax((mL - m0) * (double)__frcp_rn((float)L), m0 * 2.44140625e-4);
+                    const double tv = m0 - (double)gain * 22.0 * stepv;
+                    if (tv > 0.0 && tv < kInf) tnew = dbits(tv);
+                }
+                if (writer && lane < rnl) {
+                    out[it + lane] = (int64_t)__float_as_uint(run_s[lane].w);
+                    curve[it + lane] = hist_s[(hbase + lane) & 31];
+                }
+                if (lane == 0) {
+                    tau_s = tnew;
+                    rn_s = rnl;
+                    fb_s = fb;
+                }
+                named_bar_arrive(2, kT);
+            } else {
+                named_bar_arrive(1, kT);
+                named_bar_sync(2, kT);
+            }
+            __syncwarp();
+            rn = rn_s;
+            tau = tau_s;
+            const int fbf = fb_s;
+            // the fold flags of this run: every sample but the call's last
+            for (int k = tid; k < rn; k += kT) run_fold_s[k] = (it + k < k_stop - 1) ? 1 : 0;
+            it += rn;
+            __syncthreads();  // run_fold_s; run_s / rn_s reads before the lead's next writes
+
+            if (fbf) {
+                // duplicate fallback (_kernels.py:65-70): lowest untaken original index
+                Rec win = gslot;
+                double best = bitsd(rec_key(win));
+                uint32_t fidx = kNone;
+                int fq = -1;
+#pragma unroll
+                for (int q = 0; q < P; ++q) {
+                    if (((valid >> q) & 1u) && !((tk >> q) & 1u)) {
+                        const uint32_t o = __float_as_uint(pts[wbase + q * 32 + lane].w);
+                        if (o < fidx) { fidx = o; fq = q; }
+                    }
+                }
+                const uint32_t wm = __reduce_min_sync(kFull, fidx);
+                if (fidx == wm && fidx != kNone) {
+                    const int lp = wbase + fq * 32 + lane;
+                    const float4 v = pts[lp];
+                    double mv = 0.0;
+#pragma unroll
+                    for (int q = 0; q < P; ++q)
+                        if (q == fq) mv = m[q];
+                    const uint64_t k = dbits(mv);
+                    Rec fr;
+                    fr.klo = (uint32_t)k; fr.khi = (uint32_t)(k >> 32); fr.idx = fidx;
+                    fr.own = ((uint32_t)g << 18) | (r << 14) | (uint32_t)lp;
+                    fr.x = v.x; fr.y = v.y; fr.z = v.z; fr.pad = 0;
+                    fb_rec[warp] = fr;
+                } else if (lane == 0 && wm == kNone) {
+                    fb_rec[warp] = none_rec();
+                }
+                __syncthreads();
+                if (warp == 0) {
+                    const uint32_t ci = lane < kW ? fb_rec[lane].idx : kNone;
+                    const uint32_t cmn = __reduce_min_sync(kFull, ci);
+                    const unsigned wv = __ballot_sync(kFull, ci == cmn && ci != kNone);
+                    const Rec cr = wv ? fb_rec[__ffs(wv) - 1] : none_rec();
+                    if (lane < (int)C) {
+                        const uint32_t dst = mapa(smem_u32(&fb_slots[r]), lane);
+                        st_cluster_u64(dst, ((uint64_t)cr.khi << 32) | cr.klo);
+                        st_cluster_u64(dst + 8, ((uint64_t)cr.own << 32) | cr.idx);
+                        st_cluster_u64(dst + 16, ((uint64_t)__float_as_uint(cr.y) << 32) | __float_as_uint(cr.x));
+                        st_cluster_u64(dst + 24, (uint64_t)__float_as_uint(cr.z));
+                    }
+                }
+                cluster_sync_all();
+                Rec fw;
+                {
+                    const uint32_t ci = lane < (int)C ? fb_slots[lane].idx : kNone;
+                    const uint32_t cmn = __reduce_min_sync(kFull, ci);
+                    const unsigned wv = __ballot_sync(kFull, ci == cmn && ci != kNone);
+                    fw = wv ? fb_slots[__ffs(wv) - 1] : none_rec();
+                }
+                if (G > 1) {
+                    __syncthreads();
+                    if (warp == kW - 1) {
+                        if (r == 0 && lane < G) mbox_put(rk.mbox[lane] + ((b * 3 + 2) * G + g) * (2 * kMbRecs), fw, seq);
+                        const Rec pr = lane < G ? mbox_get(mb_mine + ((b * 3 + 2) * G + lane) * (2 * kMbRecs), seq)
+                                                : none_rec();
+                        const uint32_t pm = __reduce_min_sync(kFull, pr.idx);
+                        const unsigned wv = __ballot_sync(kFull, pr.idx == pm && pr.idx != kNone);
+                        if (lane == (wv ? __ffs(wv) - 1 : 0)) {
+                            Rec gw = wv ? pr : none_rec();
+                            if (wv && gw.idx == fw.idx) gw.own = fw.own;
+                            gslot2 = gw;
+                        }
+                    }
+                    __syncthreads();
+                    fw = gslot2;
+                }
+                if (fw.idx != kNone) {
+                    win = fw;
+                    best = bitsd(rec_key(fw));
+                }
+                cluster_sync_all();  // fb_slots / fb_rec free for the next fallback
+                if (writer && tid == 0) {
+                    out[it] = (int64_t)win.idx;
+                    curve[it] = best;
+                }
+                if (warp == kW - 1) {
+                    if (lane == 0) hist_s[hc & 31] = best;
+                    ++hc;
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    run_s[0] = make_float4(win.x, win.y, win.z, __uint_as_float(win.idx));
+                    run_own_s[0] = win.own;
+                    run_fold_s[0] = it < k_stop - 1 ? 1 : 0;
+                }
+                rn = 1;
+                ++it;
+                __syncthreads();
+            }
+        }
+        // the last run is marked above; its samples are folded except the call's last
+        if (rn > 0) {
+            for (int k = 0; k < rn; ++k) {
+                const uint32_t sown = run_own_s[k];
+                const uint32_t own = sown & 0x7fffffffu;
+                if (sown != kForeign && (own >> 18) == (uint32_t)g && ((own >> 14) & 15u) == r) {
+                    const uint32_t lp = own & 0x3fffu;
+                    if ((int)(lp / (32 * P)) == warp && (int)(lp & 31u) == lane) tk |= 1u << ((lp >> 5) % P);
+                }
+                if (!run_fold_s[k]) continue;
+                const float4 sv = run_s[k];
+                const double sx = sv.x, sy = sv.y, sz = sv.z;
+#pragma unroll
+                for (int q = 0; q < P; ++q) {
+                    if ((valid >> q) & 1u) {
+                        const float4 v = pts[wbase + q * 32 + lane];
+                        const double d = sqdist(sx, sy, sz, (double)v.x, (double)v.y, (double)v.z);
+                        if (d < m[q]) m[q] = d;
+                    }
+                }
+            }
+        }
+    }
+
     // ---- write back md / taken; curve = sqrt(best) (_kernels.py:72) -------------
 #pragma unroll
     for (int q = 0; q < P; ++q) {
@@ -633,10 +1172,10 @@ __global__ void __launch_bounds__(kT, 1) fps_res_kernel(FpsArgs a, FpsRanks rk) 
 
 size_t res_smem_bytes(int P) { return (size_t)P * kT * sizeof(float4) + kBins * sizeof(uint32_t); }
 
-template <int P>
+template <int P, bool kSpec>
 cudaError_t launch_res_p(const FpsArgs& a, const FpsRanks& rk, int64_t nclusters, int C, cudaStream_t s,
                          bool query_only, int* max_clusters) {
-    auto kern = fps_res_kernel<P>;
+    auto kern = fps_res_kernel<P, kSpec>;
     const size_t smem = res_smem_bytes(P);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -691,8 +1230,12 @@ struct ResF {
     cudaStream_t s;
     bool query;
     int* maxc;
+    bool spec = false;
     template <int P>
-    cudaError_t run() const { return launch_res_p<P>(*a, *rk, nclusters, C, s, query, maxc); }
+    cudaError_t run() const {
+        return spec ? launch_res_p<P, true>(*a, *rk, nclusters, C, s, query, maxc)
+                    : launch_res_p<P, false>(*a, *rk, nclusters, C, s, query, maxc);
+    }
 };
 
 int res_choose_P(int64_t S) {
@@ -786,7 +1329,9 @@ cudaError_t launch_fps_res(FpsArgs a, const FpsRanks& rk_in, int64_t B, int C, i
         return cudaSuccess;
     }
     a.dbg = nullptr;
-    return with_res(P, ResF{&a, &rk, nclusters, C, s, false, nullptr});
+    ResF f{&a, &rk, nclusters, C, s, false, nullptr};
+    f.spec = getenv("PS_RES_NOSPEC") == nullptr;  // speculative exchange loop (default)
+    return with_res(P, f);
 }
 
 cudaError_t launch_fps(FpsArgs a, int64_t B, cudaStream_t s) {

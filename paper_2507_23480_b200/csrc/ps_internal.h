@@ -26,7 +26,7 @@ struct FpsArgs {
 // [g*ceil(N/G), (g+1)*ceil(N/G)).  A launch runs Gl ranks per cloud starting
 // at g_base (Gl == G: virtual ranks on one GPU; Gl == 1: one rank per GPU).
 // mbox: device array of G pointers to each rank's mailbox
-// (uint4[B][3][G][2], initialised to 0xff); seq_base makes every
+// (uint4[B][3][G][2 * kMbRecs], initialised to 0xff); seq_base makes every
 // (launch, iteration) tag unique.
 struct FpsRanks {
     int G, Gl, g_base, all_write;
@@ -34,6 +34,9 @@ struct FpsRanks {
     uint32_t seq_base;
     uint4* const* mbox;
 };
+
+// records per (cloud, set, rank) mailbox slot: meta + header + 32 candidates
+constexpr int kMbRecs = 34;
 
 cudaError_t launch_fps(FpsArgs a, int64_t B, cudaStream_t s);          // resident kernel, else legacy
 cudaError_t launch_fps_legacy(FpsArgs a, int64_t B, cudaStream_t s);   // register / streaming kernel

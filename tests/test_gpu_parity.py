@@ -172,6 +172,27 @@ def test_fps_point_split_virtual_ranks(family, N, n, G, B):
 
 
 @pytest.mark.timeout(300)
+@pytest.mark.parametrize("loop", ["speculative", "one-sample"])
+def test_fps_point_split_both_loops(loop, monkeypatch):
+    """The resident kernel's two exchange loops (speculative default,
+    PS_RES_NOSPEC=1 one sample per exchange) over virtual ranks, with a
+    half-duplicate cloud (fallback across ranks) and an early stop."""
+    if loop == "one-sample":
+        monkeypatch.setenv("PS_RES_NOSPEC", "1")
+    base = generate_cloud("room-surfaces", 15000, 21)
+    cloud = np.concatenate([base, base[::3]])[np.random.default_rng(2).permutation(20000)].copy()
+    xyz4 = engine.as_xyz4(torch.from_numpy(cloud[None]).cuda())
+    for G, n, k_stop in ((3, 2000, 2000), (5, 2000, 700), (2, 20000, 20000)):
+        idx, curve, md, taken = engine.fps_split(xyz4, n, G, seed_index=77, k_stop=k_stop)
+        ri, rc, rmd, rtk, _ = O.fps(cloud, n, 77, k_stop=k_stop)
+        msg = f"{loop} G={G} n={n} k_stop={k_stop}"
+        np.testing.assert_array_equal(idx[0].cpu().numpy()[:k_stop], ri[:k_stop], err_msg=msg)
+        np.testing.assert_array_equal(curve[0].cpu().numpy()[:k_stop], rc[:k_stop], err_msg=msg)
+        np.testing.assert_array_equal(md[0].cpu().numpy(), rmd, err_msg=msg)
+        np.testing.assert_array_equal(taken[0].cpu().numpy(), rtk, err_msg=msg)
+
+
+@pytest.mark.timeout(300)
 def test_fps_point_split_duplicates_fallback():
     """All-duplicate tails force the lowest-untaken fallback to be exchanged
     across ranks (_kernels.py:65-70)."""
