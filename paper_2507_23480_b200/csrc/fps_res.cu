@@ -1334,6 +1334,67 @@ cudaError_t launch_fps_res(FpsArgs a, const FpsRanks& rk_in, int64_t B, int C, i
     return with_res(P, f);
 }
 
+// Clouds too large for one cluster (> 16 CTAs x 24 points per thread): the
+// point split over G co-resident virtual ranks on this GPU -- the protocol of
+// ps_fps_split with mailboxes owned here: one buffer per (device, B, G),
+// reused in stream order (launches that share it must be stream-ordered;
+// the first use allocates, so it must not happen inside a graph capture).
+static cudaError_t launch_fps_virtual_split(FpsArgs a, int64_t B, cudaStream_t s) {
+    static const int kGs[] = {10, 12, 16, 8, 20, 24, 32};
+    int C = 0, P = 0, G = 0;
+    for (int gg : kGs) {
+        if (fps_res_plan(a.N, B * gg, gg, &C, &P)) { G = gg; break; }
+    }
+    if (G == 0) return cudaErrorNotSupported;
+    struct Box {
+        int dev;
+        int64_t B;
+        int G;
+        uint8_t* buf;
+        uint4** ptrs;
+        size_t per_rank;
+        uint32_t seq;
+    };
+    static Box boxes[8];
+    static int nboxes = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    Box* bx = nullptr;
+    for (int i = 0; i < nboxes; ++i)
+        if (boxes[i].dev == dev && boxes[i].B == B && boxes[i].G == G) bx = &boxes[i];
+    const size_t per_rank = (size_t)B * 3 * (size_t)G * kMbRecs * 2 * sizeof(uint4);
+    if (!bx) {
+        if (nboxes == 8) return cudaErrorNotSupported;
+        Box nb = {dev, B, G, nullptr, nullptr, per_rank, 0u};
+        cudaError_t e = cudaMalloc(&nb.buf, per_rank * G);
+        if (e != cudaSuccess) return e;
+        e = cudaMalloc(&nb.ptrs, sizeof(uint4*) * G);
+        if (e != cudaSuccess) return e;
+        uint4* hp[64];
+        for (int g = 0; g < G; ++g) hp[g] = reinterpret_cast<uint4*>(nb.buf + per_rank * g);
+        e = cudaMemcpy(nb.ptrs, hp, sizeof(uint4*) * G, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return e;
+        e = cudaMemset(nb.buf, 0xff, per_rank * G);
+        if (e != cudaSuccess) return e;
+        boxes[nboxes] = nb;
+        bx = &boxes[nboxes++];
+    }
+    if ((uint64_t)bx->seq + (uint64_t)a.k_stop + 1 >= 0xffffffffull) {  // tag space: wipe and restart
+        cudaError_t e = cudaMemsetAsync(bx->buf, 0xff, bx->per_rank * G, s);
+        if (e != cudaSuccess) return e;
+        bx->seq = 0;
+    }
+    FpsRanks rk = {};
+    rk.G = G; rk.Gl = G; rk.g_base = 0; rk.all_write = 0;
+    rk.seq_base = bx->seq;
+    rk.mbox = bx->ptrs;
+    bx->seq += (uint32_t)a.k_stop + 1;
+    if (getenv("PS_FPS_VERBOSE"))
+        fprintf(stderr, "[fps-split] N=%lld B=%lld G=%d C=%d P=%d (virtual ranks)\n", (long long)a.N,
+                (long long)B, G, C, P);
+    return launch_fps_res(a, rk, B, C, P, s);
+}
+
 cudaError_t launch_fps(FpsArgs a, int64_t B, cudaStream_t s) {
     // The legacy register kernel (fps.cu) has the shorter per-iteration
     // chain while a cluster holds the cloud in registers (<= 16 points per
@@ -1358,6 +1419,10 @@ cudaError_t launch_fps(FpsArgs a, int64_t B, cudaStream_t s) {
     }
     if (!getenv("PS_FPS_NOSPEC")) {
         const cudaError_t e = launch_fps_spec(a, B, s);
+        if (e != cudaErrorNotSupported) return e;
+    }
+    if (use_res && !force_leg && !getenv("PS_FPS_NOSPLIT")) {
+        const cudaError_t e = launch_fps_virtual_split(a, B, s);
         if (e != cudaErrorNotSupported) return e;
     }
     return launch_fps_legacy(a, B, s);

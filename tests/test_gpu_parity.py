@@ -193,6 +193,29 @@ def test_fps_point_split_both_loops(loop, monkeypatch):
 
 
 @pytest.mark.timeout(300)
+def test_fps_huge_cloud_internal_virtual_split():
+    """Clouds beyond one cluster (here N = 300000) run ps_fps as the point
+    split over co-resident virtual ranks with internal mailboxes: oracle
+    parity for a full prefix, an early stop, and a resumed fps_loop."""
+    N, n = 300000, 800
+    c = generate_cloud("room-surfaces", N, 33)
+    xyz4 = engine.as_xyz4(torch.from_numpy(c[None]).cuda())
+    for k_stop in (n, 300):
+        idx, curve, md, taken = engine.fps(xyz4, n, seed_index=N // 3, k_stop=k_stop)
+        ri, rc, rmd, rtk, _ = O.fps(c, n, N // 3, k_stop=k_stop)
+        np.testing.assert_array_equal(idx[0].cpu().numpy()[:k_stop], ri[:k_stop], err_msg=f"k_stop={k_stop}")
+        np.testing.assert_array_equal(curve[0].cpu().numpy()[:k_stop], rc[:k_stop])
+        np.testing.assert_array_equal(md[0].cpu().numpy(), rmd)
+        np.testing.assert_array_equal(taken[0].cpu().numpy(), rtk)
+    # resume the early-stopped run to n through the fps_loop drop-in path
+    idx, curve, md, taken = engine.fps(xyz4, n, seed_index=N // 3, k_stop=300)
+    engine.fps_loop(xyz4, md, taken, idx, curve, 300, n)
+    ri, rc, rmd, rtk, _ = O.fps(c, n, N // 3)
+    np.testing.assert_array_equal(idx[0].cpu().numpy(), ri)
+    np.testing.assert_array_equal(md[0].cpu().numpy(), rmd)
+
+
+@pytest.mark.timeout(300)
 def test_fps_point_split_duplicates_fallback():
     """All-duplicate tails force the lowest-untaken fallback to be exchanged
     across ranks (_kernels.py:65-70)."""
