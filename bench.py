@@ -571,8 +571,9 @@ def bench_c4(dev, steps):
 
 def bench_c5_virtual(dev, G=None):
     """C5: exact FPS of one N = 2^20 uniform-box cloud to n = 65536, the cloud
-    split over G ranks that exchange shard records every iteration through
-    the NVLink mailbox protocol -- here all ranks on this GPU (virtual ranks;
+    split over G ranks that exchange shard headers and candidate sets through
+    the NVLink mailbox protocol (one exchange per certified run of samples)
+    -- here all ranks on this GPU (virtual ranks;
     the one-process-per-GPU run is pointsplit.PointSplitFPS).  Timed with CUDA
     events on the launching stream; inputs resident."""
     import ctypes
