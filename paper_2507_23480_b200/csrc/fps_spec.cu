@@ -598,8 +598,7 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
 
             // next threshold: the curve is non-increasing; aim kTarget samples
             // ahead along its recent slope, gain corrected by the observed count
-            // development override (PS_SPEC_TARGET; < 0: no speculation)
-            const double target = a.dbg_t0 > 0 ? (double)a.dbg_t0 * 1e-3 : (a.dbg_t0 == -1 ? -1.0 : kTarget);
+            const double target = a.spec_target != 0.0 ? a.spec_target : kTarget;  // PS_SPEC_TARGET
             if (tau != kTauOff && !tau_boot) {  // a bootstrap threshold says nothing about the gain
                 if (overflow || ctot > (int)(2 * target)) gain *= 0.7f;
                 else if (ctot < (int)(target / 2)) gain *= 1.3f;
@@ -791,8 +790,7 @@ cudaError_t launch_fps_spec(FpsArgs a, int64_t B, cudaStream_t s) {
     if (P == 0) return cudaErrorNotSupported;
     a.points_per_cta = S;
     a.dbg = nullptr;
-    a.dbg_t0 = getenv("PS_SPEC_TARGET") ? (int64_t)(atof(getenv("PS_SPEC_TARGET")) * 1000.0) : 0;
-    if (getenv("PS_SPEC_TARGET") && atof(getenv("PS_SPEC_TARGET")) < 0) a.dbg_t0 = -1;
+    a.spec_target = getenv("PS_SPEC_TARGET") ? atof(getenv("PS_SPEC_TARGET")) : 0.0;  // development override
     static long long* dbg = nullptr;
     const bool timing = kTiming && getenv("PS_FPS_TIMING");
     if (timing) {

@@ -20,6 +20,7 @@ struct FpsArgs {
     int64_t points_per_cta;     // set by the launcher
     long long* dbg;             // development timing buffer (PS_FPS_TIMING)
     int64_t dbg_t0;             // first recorded iteration offset (PS_FPS_T0)
+    double spec_target;         // fps_spec: candidates aimed for per exchange (0: default, < 0: no speculation)
 };
 
 // Clouds split over G ranks (point-split FPS): rank g owns original indices
