@@ -520,6 +520,23 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
             // a taken candidate (resumed state only) would need the fallback: no speculation
             overflow = overflow || __any_sync(kFull, lane < ncand && ct);
             bool alive = lane < ncand;
+            // float32 screen bound of my candidate's md (as the fold's): a pick
+            // whose float32 distance exceeds it cannot lower md
+            float cthr = alive ? skip_threshold(cm) : -1.0f;
+            // lower my candidate by the pick at (sx, sy, sz): float32 screen,
+            // the exact float64 update only where the screen cannot exclude it
+            auto lower_by = [&](float sx, float sy, float sz) {
+                const float dx = cx - sx, dy = cy - sy, dz = cz - sz;
+                const float d32 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+                const bool need = alive && !(d32 > cthr);
+                if (__any_sync(kFull, need)) {
+                    const double d = sqdist((double)sx, (double)sy, (double)sz, (double)cx, (double)cy, (double)cz);
+                    if (need && dbits(d) < dbits(cm)) {
+                        cm = d;
+                        cthr = skip_threshold_d32(d, d32);
+                    }
+                }
+            };
             if (tdbg) { t1 = clock64(); tacc[0] += t1 - t0; t0 = t1; }
             __syncwarp();
             if (tdbg) { t1 = clock64(); tacc[6] += t1 - t0; t0 = t1; }
@@ -560,11 +577,7 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
                         ++itl;
                         rnl = 1;
                         alive = alive && ci != wi && !overflow;
-                        if (alive) {
-                            const double d = sqdist((double)sx, (double)sy, (double)sz, (double)cx, (double)cy,
-                                                    (double)cz);
-                            if (dbits(d) < dbits(cm)) cm = d;
-                        }
+                        lower_by(sx, sy, sz);
                     }
                 }
             }
@@ -578,15 +591,13 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
                 const float sx = __shfl_sync(kFull, cx, wl);
                 const float sy = __shfl_sync(kFull, cy, wl);
                 const float sz = __shfl_sync(kFull, cz, wl);
-                // the reference's float64 update of every other candidate
-                const double d = sqdist((double)sx, (double)sy, (double)sz, (double)cx, (double)cy, (double)cz);
                 if (win) {
                     sts_v4(a_run + 16u * rnl, make_uint4(__float_as_uint(cx), __float_as_uint(cy), __float_as_uint(cz), ci));
                     sts_f64(a_hist + 8u * ((hc + rnl) & 31), cm);
                     st_release_cta(&pub_s, tag | (uint32_t)(rnl + 1));
                 }
                 alive = alive && !win;
-                cm = (alive && dbits(d) < dbits(cm)) ? d : cm;
+                lower_by(sx, sy, sz);  // the reference's update of every other candidate
                 ++itl;
                 ++rnl;
             }
