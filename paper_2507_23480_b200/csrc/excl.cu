@@ -711,31 +711,32 @@ __global__ void __launch_bounds__(kEllWarps * 32, 4) grid_ell_kernel(int64_t B, 
     __shared__ int tbase[kEllWarps][9];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
-    for (int64_t gs = (int64_t)blockIdx.x * kEllWarps + warp; gs < B * N; gs += (int64_t)gridDim.x * kEllWarps) {
-        const int64_t b = gs / N, s = gs - b * N;
-        // level values of this cloud: lane l < L holds r2_l and its rank_lt
-        const double my_r2 = lane < L ? r2_levels[b * levels_ld + lane] : 0.0;
-        __syncwarp();
-        if (lane < L) {
-            lvs[warp][lane] = my_r2;
-            lvb[warp][lane] = (unsigned long long)__double_as_longlong(my_r2);
-        }
+    // one cloud per grid row: the cloud's level values and grid parameters
+    // are set up once per warp; warps stride over the cloud's sorted points
+    const int64_t b = blockIdx.y;
+    const double my_r2 = lane < L ? r2_levels[b * levels_ld + lane] : 0.0;
+    if (lane < L) {
+        lvs[warp][lane] = my_r2;
+        lvb[warp][lane] = (unsigned long long)__double_as_longlong(my_r2);
+    }
+    int rank_lt = 0;
+    double r2 = 0.0;
+    for (int l = 0; l < L; ++l) {
+        const double v = __shfl_sync(kFull, my_r2, l);
+        rank_lt += (v < my_r2) ? 1 : 0;
+        r2 = fmax(r2, v);
+    }
+    const float thr = prefilter_threshold(r2);
+    const bool no_filter = !(thr <= FLT_MAX);
+    const GridParams gp = g.params[b];
+    const float4* sx = g.sorted_xyz + b * N;
+    const int32_t* si = g.sorted_idx + b * N;
+    const int* cs = g.cell_start + b * (g.max_cells + 1);
+    __syncwarp();
+    for (int64_t s = (int64_t)blockIdx.x * kEllWarps + warp; s < N; s += (int64_t)gridDim.x * kEllWarps) {
         hcnt[warp][lane] = 0;
         if (lane == 0) hcnt[warp][32] = 0;
         __syncwarp();
-        int rank_lt = 0;
-        double r2 = 0.0;
-        for (int l = 0; l < L; ++l) {
-            const double v = __shfl_sync(kFull, my_r2, l);
-            rank_lt += (v < my_r2) ? 1 : 0;
-            r2 = fmax(r2, v);
-        }
-        const float thr = prefilter_threshold(r2);
-        const bool no_filter = !(thr <= FLT_MAX);
-        const GridParams gp = g.params[b];
-        const float4* sx = g.sorted_xyz + b * N;
-        const int32_t* si = g.sorted_idx + b * N;
-        const int* cs = g.cell_start + b * (g.max_cells + 1);
         const float4 p = sx[s];
         const int32_t i = si[s];
         const int cx = cell_coord(p.x, gp.ox, gp.inv_h, gp.nx);
@@ -916,8 +917,10 @@ cudaError_t launch_excl_build(const float4* xyz, int64_t B, int64_t N, const dou
         if (method == 2) {
             const int64_t stride = csr.cap_entries / N;
             ell_indptr_kernel<<<gpts, 256, 0, s>>>(B, N, stride, csr);
-            const unsigned gell = (unsigned)std::min<int64_t>(148 * 16, (B * N + kEllWarps - 1) / kEllWarps);
-            grid_ell_kernel<<<gell, kEllWarps * 32, 0, s>>>(B, N, r2_levels, L, levels_ld, stride, g, w, csr);
+            const int64_t gx = std::max<int64_t>(1, std::min<int64_t>((148 * 16 + B - 1) / B,
+                                                                      (N + kEllWarps - 1) / kEllWarps));
+            grid_ell_kernel<<<dim3((unsigned)gx, (unsigned)B), kEllWarps * 32, 0, s>>>(B, N, r2_levels, L, levels_ld,
+                                                                                     stride, g, w, csr);
             return cudaGetLastError();
         }
         const dim3 gp((unsigned)((N + 255) / 256), (unsigned)B);
