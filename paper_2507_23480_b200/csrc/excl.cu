@@ -768,7 +768,7 @@ __global__ void __launch_bounds__(kEllWarps * 32, 4) grid_ell_kernel(int64_t B, 
         for (int q = 0; q < 8; ++q) e[q] = __shfl_sync(kFull, excl0, q + 1);
         __syncwarp();
         int cnt = 0;
-#pragma unroll 2
+#pragma unroll 4
         for (int tb = 0; tb < total; tb += 32) {
             const int f = tb + lane;
             int rr = 0;
