@@ -48,6 +48,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 
 #include "common.cuh"
 #include "ps_internal.h"
@@ -1336,9 +1337,9 @@ cudaError_t launch_fps_res(FpsArgs a, const FpsRanks& rk_in, int64_t B, int C, i
 
 // Clouds too large for one cluster (> 16 CTAs x 24 points per thread): the
 // point split over G co-resident virtual ranks on this GPU -- the protocol of
-// ps_fps_split with mailboxes owned here: one buffer per (device, B, G),
-// reused in stream order (launches that share it must be stream-ordered;
-// the first use allocates, so it must not happen inside a graph capture).
+// ps_fps_split with mailboxes owned here: one buffer per (device, stream, B,
+// G), so launches that share one are ordered by their stream; the first use
+// allocates, so it must not happen inside a graph capture.
 static cudaError_t launch_fps_virtual_split(FpsArgs a, int64_t B, cudaStream_t s) {
     static const int kGs[] = {10, 12, 16, 8, 20, 24, 32};
     int C = 0, P = 0, G = 0;
@@ -1348,6 +1349,7 @@ static cudaError_t launch_fps_virtual_split(FpsArgs a, int64_t B, cudaStream_t s
     if (G == 0) return cudaErrorNotSupported;
     struct Box {
         int dev;
+        cudaStream_t stream;
         int64_t B;
         int G;
         uint8_t* buf;
@@ -1355,17 +1357,19 @@ static cudaError_t launch_fps_virtual_split(FpsArgs a, int64_t B, cudaStream_t s
         size_t per_rank;
         uint32_t seq;
     };
-    static Box boxes[8];
+    static Box boxes[16];
     static int nboxes = 0;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
     int dev = 0;
     cudaGetDevice(&dev);
     Box* bx = nullptr;
     for (int i = 0; i < nboxes; ++i)
-        if (boxes[i].dev == dev && boxes[i].B == B && boxes[i].G == G) bx = &boxes[i];
+        if (boxes[i].dev == dev && boxes[i].stream == s && boxes[i].B == B && boxes[i].G == G) bx = &boxes[i];
     const size_t per_rank = (size_t)B * 3 * (size_t)G * kMbRecs * 2 * sizeof(uint4);
     if (!bx) {
-        if (nboxes == 8) return cudaErrorNotSupported;
-        Box nb = {dev, B, G, nullptr, nullptr, per_rank, 0u};
+        if (nboxes == 16) return cudaErrorNotSupported;  // the streaming kernel serves the rest
+        Box nb = {dev, s, B, G, nullptr, nullptr, per_rank, 0u};
         cudaError_t e = cudaMalloc(&nb.buf, per_rank * G);
         if (e != cudaSuccess) return e;
         e = cudaMalloc(&nb.ptrs, sizeof(uint4*) * G);
