@@ -149,6 +149,41 @@ def test_fps_speculative_lead_owns_points(family, monkeypatch):
         np.testing.assert_array_equal(taken[0].cpu().numpy(), rtk, err_msg=msg)
 
 
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("case", range(24))
+def test_fps_randomized_against_oracle(case, monkeypatch):
+    """Seeded random cases for the exact FPS dispatch (speculative register
+    kernel, its lead-owns-points variant, the resident kernel, the internal
+    virtual-rank split): random N (1 .. 300000), n, seed, early stop, forced
+    cluster width, cloud family incl. integer grids (exact md ties) and heavy
+    duplicates; indices, curve, md, taken against the oracle bit for bit."""
+    rng = np.random.default_rng(1000 + case)
+    N = int(rng.choice([1, 2, 7, 33, 500, 1023, 4096, 12000, 24000, 40000, 65000, 120000, 300000]))
+    kind = case % 4
+    if kind == 0:
+        c = generate_cloud("uniform-box", N, 50 + case)
+    elif kind == 1:  # integer grid: many exactly tied distances
+        c = rng.integers(0, 12, size=(N, 3)).astype(np.float32)
+    elif kind == 2:  # heavy duplicates
+        base = generate_cloud("room-surfaces", max(1, N // 3), 60 + case)
+        c = base[rng.integers(0, base.shape[0], size=N)].copy()
+    else:
+        c = generate_cloud("gaussian-clusters", N, 70 + case)
+    n = int(rng.integers(1, min(N, 1500) + 1))
+    k_stop = n if rng.random() < 0.6 else int(rng.integers(1, n + 1))
+    seed = int(rng.integers(0, N))
+    if N <= 65536 and rng.random() < 0.4:
+        monkeypatch.setenv("PS_FPS_CLUSTER", str(int(rng.choice([1, 2, 4, 8, 10, 16]))))
+    xyz4 = engine.as_xyz4(torch.from_numpy(c[None]).cuda())
+    idx, curve, md, taken = engine.fps(xyz4, n, seed_index=seed, k_stop=k_stop)
+    ri, rc, rmd, rtk, _ = O.fps(c, n, seed, k_stop=k_stop)
+    msg = f"case {case}: N={N} n={n} k_stop={k_stop} seed={seed} kind={kind}"
+    np.testing.assert_array_equal(idx[0].cpu().numpy()[:k_stop], ri[:k_stop], err_msg=msg)
+    np.testing.assert_array_equal(curve[0].cpu().numpy()[:k_stop], rc[:k_stop], err_msg=msg)
+    np.testing.assert_array_equal(md[0].cpu().numpy(), rmd, err_msg=msg)
+    np.testing.assert_array_equal(taken[0].cpu().numpy(), rtk, err_msg=msg)
+
+
 @pytest.mark.timeout(300)
 @pytest.mark.parametrize("family,N,n,G,B", [
     ("room-surfaces", 24000, 3000, 2, 1), ("room-surfaces", 24000, 3000, 4, 2), ("lattice", 4913, 1200, 3, 1),
