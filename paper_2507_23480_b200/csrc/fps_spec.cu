@@ -643,7 +643,7 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
             pw = tag | (uint32_t)rnl | 0x100u | ((uint32_t)fb << 9);
             __syncwarp();
             if (lane == 0) st_release_cta(&pub_s, pw);
-            if (tdbg) { t1 = clock64(); tacc[8] += t1 - t0; t0 = t1; }
+            if (tdbg) { t1 = clock64(); tacc[9] += t1 - t0; t0 = t1; }
             // the run's out / curve entries, one store batch (after the
             // release stores, so no publish waits on global stores)
             if (r == 0 && lane < rnl) {
@@ -681,7 +681,6 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
         const int rn = (int)(pw & 0xffu);
         it += rn;
         tau = tau_s;
-        if (tdbg) { t1 = clock64(); tacc[9] += t1 - t0; t0 = t1; }
 
         if (pw & 0x200u) {
             // duplicate fallback (_kernels.py:65-70): lowest untaken index
@@ -838,8 +837,8 @@ cudaError_t launch_fps_spec(FpsArgs a, int64_t B, cudaStream_t s) {
         cudaStreamSynchronize(s);
         const double nx = h[0] > 0 ? (double)h[0] : 1.0;
         fprintf(stderr, "[fps-spec timing] C=%d P=%d T=%d N=%lld iters=%lld exchanges=%lld taken/ex=%.2f "
-                "cycles/ex: compact %.0f max+cand %.0f bar1 %.0f ctamax %.0f send %.0f wait %.0f recv %.0f pick0 %.0f "
-                "picks %.0f tau+bar2 %.0f\n",
+                "cycles/ex: compact %.0f max+cand %.0f bar1 %.0f ctamax %.0f send %.0f wait %.0f gather %.0f pick0 %.0f "
+                "picks %.0f tau+publish %.0f\n",
                 C, P, T, (long long)a.N, (long long)(a.k_stop - a.k_start), h[0], (double)h[1] / nx,
                 h[2] / nx, h[3] / nx, h[4] / nx, h[5] / nx, h[6] / nx, h[7] / nx, h[8] / nx, h[9] / nx, h[10] / nx,
                 h[11] / nx);
