@@ -425,12 +425,23 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
             off += c2 < r ? v : 0;
             L += v;
         }
-        for (int64_t base = jlo; base < jhi; base += kT4) {
-            const int64_t j = base + tid;
-            const int f = (j < jhi && avail[j]) ? 1 : 0;
+        {
+            // one block scan: each thread takes a contiguous run of my range
+            // (runs in thread order keep the pool in index order)
+            const int64_t len = jhi - jlo;
+            const int E = (int)((len + kT4 - 1) / kT4);
+            const int64_t j0 = jlo + (int64_t)tid * E;
+            int cl = 0;
+            for (int e = 0; e < E; ++e) {
+                const int64_t j = j0 + e;
+                cl += (j < jhi && avail[j]) ? 1 : 0;
+            }
             int tot;
-            const int ex = bscan(f, wt, &tot);
-            if (f) pool[off + ex] = (int32_t)j;
+            int pos = off + bscan(cl, wt, &tot);
+            for (int e = 0; e < E; ++e) {
+                const int64_t j = j0 + e;
+                if (j < jhi && avail[j]) pool[pos++] = (int32_t)j;
+            }
             off += tot;
         }
         sync_all(C);

@@ -25,7 +25,7 @@ fp._exclusion()
 torch.cuda.synchronize()
 ts = []
 ref = None
-for _ in range(30):
+for _ in range(int(os.environ.get("REPS", "30"))):
     fp.state.copy_(s0)
     e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     e[0].record()
@@ -37,4 +37,4 @@ for _ in range(30):
         ref = fp.out.clone()
     assert torch.equal(ref, fp.out)
 ts.sort()
-print(f"{os.environ.get('PS_B200_LIB', 'default')}: sampler {1e3 * ts[15]:.1f} us (min {1e3 * ts[0]:.1f})")
+print(f"{os.environ.get('PS_B200_LIB', 'default')}: sampler {1e3 * ts[len(ts) // 2]:.1f} us (min {1e3 * ts[0]:.1f})")
