@@ -783,17 +783,12 @@ cudaError_t launch_fps_spec(FpsArgs a, int64_t B, cudaStream_t s) {
     if (P == 0) return cudaErrorNotSupported;
     // one warp per CTA leads the exchange and owns no points (below)
     const int64_t S = (a.N + C - 1) / C;
+    // 512 threads, 15 worker warps, P <= 8 points per thread (beyond that the
+    // register budget spills): up to 3840 points per CTA
     P = 0;
-    for (int t : {512, 256}) {
-        static const int kP512[] = {1, 2, 3, 4, 5, 6, 7, 8};
-        static const int kP256[] = {12, 16};
-        const int* ps = t == 512 ? kP512 : kP256;
-        const int np = t == 512 ? 8 : 2;
-        const int tw = t - 32;
-        for (int i = 0; i < np && !P; ++i)
-            if ((int64_t)ps[i] * tw >= S) { P = ps[i]; T = t; }
-        if (P) break;
-    }
+    T = 512;
+    for (int p : {1, 2, 3, 4, 5, 6, 7, 8})
+        if (!P && (int64_t)p * (T - 32) >= S) P = p;
     // up to 4096 points per CTA: the lead warp owns points as well
     const bool lead_pts = P == 0 && S <= 8 * 512;
     if (lead_pts) { P = 8; T = 512; }
@@ -826,8 +821,6 @@ cudaError_t launch_fps_spec(FpsArgs a, int64_t B, cudaStream_t s) {
         PS_SPEC_CASE(6, 512)
         PS_SPEC_CASE(7, 512)
         PS_SPEC_CASE(8, 512)
-        PS_SPEC_CASE(12, 256)
-        PS_SPEC_CASE(16, 256)
         default: break;
     }
 #undef PS_SPEC_CASE

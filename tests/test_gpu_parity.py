@@ -149,6 +149,23 @@ def test_fps_speculative_lead_owns_points(family, monkeypatch):
         np.testing.assert_array_equal(taken[0].cpu().numpy(), rtk, err_msg=msg)
 
 
+@pytest.mark.timeout(300)
+def test_fps_batch_beyond_one_wave():
+    """40 clouds of 24000 points: more clusters than fit co-resident, so the
+    speculative kernel runs in waves; FastPoint-prefix-length FPS, spot-checked
+    clouds against the oracle."""
+    B, N, n = 40, 24000, 600
+    clouds = np.stack([generate_cloud("room-surfaces", N, 900 + b) for b in range(B)])
+    xyz4 = engine.as_xyz4(torch.from_numpy(clouds).cuda())
+    idx, curve, md, taken = engine.fps(xyz4, n, seed_index=5)
+    for b in (0, 17, 39):
+        ri, rc, rmd, rtk, _ = O.fps(clouds[b], n, 5)
+        np.testing.assert_array_equal(idx[b].cpu().numpy(), ri, err_msg=f"cloud {b}")
+        np.testing.assert_array_equal(curve[b].cpu().numpy(), rc)
+        np.testing.assert_array_equal(md[b].cpu().numpy(), rmd)
+        np.testing.assert_array_equal(taken[b].cpu().numpy(), rtk)
+
+
 @pytest.mark.timeout(600)
 @pytest.mark.parametrize("case", range(24))
 def test_fps_randomized_against_oracle(case, monkeypatch):
