@@ -781,6 +781,11 @@ cudaError_t launch_fps_spec(FpsArgs a, int64_t B, cudaStream_t s) {
     int C = 1, P = 0, T = 256;
     fps_choose_cluster(a.N, B, &C, &P, &T);
     if (P == 0) return cudaErrorNotSupported;
+    // clouds of one or two CTAs: the one-sample kernel has no cluster
+    // exchange to amortise and is faster (profiles/r01/fps_spec.log: 0.65-0.86
+    // vs 0.9-1.7 us per iteration up to N = 2048; from C = 4 speculation wins
+    // up to 2.2x); PS_FPS_SPEC=1 forces speculation
+    if (C <= 2 && !getenv("PS_FPS_SPEC")) return cudaErrorNotSupported;
     // one warp per CTA leads the exchange and owns no points (below)
     const int64_t S = (a.N + C - 1) / C;
     // 512 threads, 15 worker warps, P <= 8 points per thread (beyond that the

@@ -108,6 +108,8 @@ def test_fps_register_kernels_across_cluster_widths(kernel, C, monkeypatch):
     monkeypatch.setenv("PS_FPS_CLUSTER", C)
     if kernel == "one-sample":
         monkeypatch.setenv("PS_FPS_NOSPEC", "1")
+    else:
+        monkeypatch.setenv("PS_FPS_SPEC", "1")  # also at C = 1, 2 (dispatched to one-sample by default)
     dup = generate_cloud("uniform-box", 1500, 3)
     dup = np.concatenate([dup, dup[::2]])[np.random.default_rng(1).permutation(2250)].copy()
     cases = (("lattice", generate_cloud("lattice", 4913, 7), 1200), ("room", generate_cloud("room-surfaces", 12000, 7), 3000),
