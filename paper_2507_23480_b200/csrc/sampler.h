@@ -48,6 +48,7 @@ struct SampArgs {
     unsigned char* gws;          // global workspace (always; tables too when use_smem == 0)
     int64_t gws_stride;
     long long* dbg;              // development timing (PS_SAMPLER_TIMING)
+    int tiny;                    // v4, one CTA per cloud: the per-cloud arrays live in shared memory
 };
 
 struct EtArgs {

@@ -204,6 +204,22 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
     int32_t* prv = w.prv + b * N;
     int32_t* lw = w.lw + b * N;
     int32_t* cand = w.cand + b * N;
+    if (kSm && a.tiny) {
+        // one CTA per cloud: every access to these arrays is CTA-local, so
+        // they live in shared memory after the kSm layout (L2 round trips ->
+        // shared-memory latency for the draw resolution and the pool)
+        const int64_t Np = (N + 15) & ~(int64_t)15;
+        const int64_t sp0 = ((N + 15) & ~(int64_t)15);
+        const int64_t base0 = Np + 4 * Np + 4 * (((N + 31) / 32 + 3) & ~(int64_t)3) + 21 * sp0;
+        int32_t* t0 = reinterpret_cast<int32_t*>(dsm4 + ((base0 + 15) & ~(int64_t)15));
+        pool = t0;
+        pos = reinterpret_cast<uint32_t*>(t0 + Np);
+        head = t0 + 2 * Np;
+        nxt = t0 + 3 * Np;
+        prv = t0 + 4 * Np;
+        lw = t0 + 5 * Np;
+        cand = t0 + 6 * Np;
+    }
     int32_t* rank = kSm ? reinterpret_cast<int32_t*>(dsm4 + Npad) : w.rank + b * N;
     uint32_t* tkb = reinterpret_cast<uint32_t*>(dsm4 + Npad + 4 * Npad);  // kSm: taken bitmap
     const int64_t Wtk = (N + 31) / 32;
@@ -229,6 +245,11 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
     int32_t* preds = w.preds + b * N * kPred4;
     uint8_t* npred = w.npred + b * N;
     int32_t* scr = w.scr + b * kScr;
+    if (kSm && a.tiny) {
+        const int64_t Np = (N + 15) & ~(int64_t)15;
+        const int64_t base0 = Np + 4 * Np + 4 * (((N + 31) / 32 + 3) & ~(int64_t)3) + 21 * Np;
+        scr = reinterpret_cast<int32_t*>(dsm4 + ((base0 + 15) & ~(int64_t)15)) + 7 * Np;
+    }
     int64_t* out = a.out_idx + b * a.ld_out;
     const int64_t* indptr = a.indptr + b * (N + 1);
     const int32_t* nbr = a.nbr + b * a.cap_entries;
@@ -807,9 +828,13 @@ cudaError_t launch_sampler_v4(SampArgs a, int64_t B, cudaStream_t s) {
     const int64_t span0 = ((N + C - 1) / C + 15) & ~(int64_t)15;
     const size_t dsm = (size_t)(Npad + 4 * Npad + 4 * (((N + 31) / 32 + 3) & ~(int64_t)3) + 21 * span0);
     const bool sm = dsm <= 200 * 1024 && !getenv("PS_SAMPLER_GLOBAL");
+    // one CTA per cloud and room for 7 int32 arrays of N + the scratch: tiny layout
+    const size_t dsm_tiny = ((dsm + 15) & ~(size_t)15) + 7 * 4 * (size_t)Npad + 4 * kScr;
+    a.tiny = (sm && C == 1 && dsm_tiny <= 200 * 1024 && !getenv("PS_SAMPLER_NOTINY")) ? 1 : 0;
+    const size_t dsm_used = a.tiny ? dsm_tiny : dsm;
     auto kern = sm ? samp4_kernel<true> : samp4_kernel<false>;
     if (sm) {
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm_used);
         if (e != cudaSuccess) return e;
     }
     if (C > 8) {
@@ -819,7 +844,7 @@ cudaError_t launch_sampler_v4(SampArgs a, int64_t B, cudaStream_t s) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(B * C), 1, 1);
     cfg.blockDim = dim3(kT4, 1, 1);
-    cfg.dynamicSmemBytes = sm ? dsm : 0;
+    cfg.dynamicSmemBytes = sm ? dsm_used : 0;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
