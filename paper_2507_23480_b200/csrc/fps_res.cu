@@ -1408,6 +1408,10 @@ cudaError_t launch_fps(FpsArgs a, int64_t B, cudaStream_t s) {
     int C = 0, P = 0;
     const bool force_res = getenv("PS_FPS_RESIDENT") != nullptr;
     const bool force_leg = getenv("PS_FPS_LEGACY") != nullptr;
+    if (!force_res && !force_leg && !getenv("PS_FPS_NOSMALL") && !getenv("PS_FPS_NOSPEC") && !getenv("PS_FPS_SPEC")) {
+        const cudaError_t e = launch_fps_small(a, B, s);  // small clouds: one CTA each, registers
+        if (e != cudaErrorNotSupported) return e;
+    }
     bool use_res = force_res;
     if (!force_res && !force_leg) {
         int lc = 0, lp = 0, lt = 0;

@@ -41,7 +41,8 @@ constexpr int kMbRecs = 34;
 
 cudaError_t launch_fps(FpsArgs a, int64_t B, cudaStream_t s);          // resident kernel, else legacy
 cudaError_t launch_fps_legacy(FpsArgs a, int64_t B, cudaStream_t s);   // register / streaming kernel
-cudaError_t launch_fps_spec(FpsArgs a, int64_t B, cudaStream_t s);     // register kernel, top-K speculation
+cudaError_t launch_fps_spec(FpsArgs a, int64_t B, cudaStream_t s);     // register kernel, speculation
+cudaError_t launch_fps_small(FpsArgs a, int64_t B, cudaStream_t s);    // one CTA per small cloud, points in registers
 bool fps_res_plan(int64_t N, int64_t nclusters, int G, int* C_out, int* P_out);
 cudaError_t launch_fps_res(FpsArgs a, const FpsRanks& rk, int64_t B, int C, int P, cudaStream_t s);
 int fps_choose_cluster(int64_t N, int64_t B, int* C_out, int* P_out, int* T_out);

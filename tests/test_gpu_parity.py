@@ -152,6 +152,59 @@ def test_fps_speculative_lead_owns_points(family, monkeypatch):
 
 
 @pytest.mark.timeout(300)
+@pytest.mark.parametrize("W", [1, 2, 4, 8])
+def test_fps_small_cloud_kernel(W, monkeypatch):
+    """The small-cloud kernel (fps_small.cu: one CTA of W warps per cloud,
+    points in registers) at every points-per-lane width it instantiates, on
+    tie-heavy, half-duplicate (fallback of _kernels.py:65-70, also when every
+    point is taken) and uniform clouds, full runs, early stops and a resumed
+    loop (fps_loop from a partial state), against the oracle bit for bit."""
+    monkeypatch.setenv("PS_FPS_SMALL_W", str(W))
+    rng = np.random.default_rng(W)
+    for R in (1, 2, 4, 8, 16):
+        N = max(3, W * 32 * R - int(rng.integers(0, W * 16 * R)))
+        half = generate_cloud("uniform-box", (N + 1) // 2, 5)
+        dup = np.concatenate([half, half])[:N][rng.permutation(N)].copy()
+        cases = (("lattice", generate_cloud("lattice", N, 7)), ("dup", dup), ("box", generate_cloud("uniform-box", N, 9)))
+        for name, c in cases:
+            for n, k_stop in ((N, N), (max(2, N // 2), max(2, N // 5))):
+                msg = f"W={W} R={R} N={N} {name} n={n} k_stop={k_stop}"
+                xyz4 = engine.as_xyz4(torch.from_numpy(c[None]).cuda())
+                seed = N // 3
+                idx, curve, md, taken = engine.fps(xyz4, n, seed_index=seed, k_stop=k_stop)
+                ri, rc, rmd, rtk, _ = O.fps(c, n, seed, k_stop=k_stop)
+                np.testing.assert_array_equal(idx[0].cpu().numpy()[:k_stop], ri[:k_stop], err_msg=msg)
+                np.testing.assert_array_equal(curve[0].cpu().numpy()[:k_stop], rc[:k_stop], err_msg=msg)
+                np.testing.assert_array_equal(md[0].cpu().numpy(), rmd, err_msg=msg)
+                np.testing.assert_array_equal(taken[0].cpu().numpy(), rtk, err_msg=msg)
+                if k_stop < n:  # resume to n from the partial state
+                    engine.fps_loop(xyz4, md, taken, idx, curve, k_stop, n)
+                    ri, rc, rmd, rtk, _ = O.fps(c, n, seed)
+                    np.testing.assert_array_equal(idx[0].cpu().numpy(), ri, err_msg=msg + " resumed")
+                    np.testing.assert_array_equal(curve[0].cpu().numpy(), rc, err_msg=msg + " resumed")
+                    np.testing.assert_array_equal(md[0].cpu().numpy(), rmd, err_msg=msg + " resumed")
+                    np.testing.assert_array_equal(taken[0].cpu().numpy(), rtk, err_msg=msg + " resumed")
+
+
+@pytest.mark.timeout(300)
+def test_fps_small_cloud_batches():
+    """Default small-cloud dispatch over batches (C2's stage sizes, and 4096
+    points at a chip-filling batch, which takes W = 8): every cloud against
+    the oracle."""
+    for B, N, n in ((32, 1024, 512), (32, 512, 256), (32, 256, 128), (32, 128, 64), (160, 4096, 300), (200, 600, 600)):
+        clouds = np.stack([generate_cloud("room-surfaces", N, 40 + b) for b in range(B)])
+        xyz4 = engine.as_xyz4(torch.from_numpy(clouds).cuda())
+        idx, curve, md, taken = engine.fps(xyz4, n, seed_index=1)
+        for b in sorted({0, B // 2, B - 1}):
+            ri, rc, rmd, rtk, _ = O.fps(clouds[b], n, 1)
+            msg = f"B={B} N={N} cloud {b}"
+            np.testing.assert_array_equal(idx[b].cpu().numpy(), ri, err_msg=msg)
+            np.testing.assert_array_equal(curve[b].cpu().numpy(), rc, err_msg=msg)
+            np.testing.assert_array_equal(md[b].cpu().numpy(), rmd, err_msg=msg)
+            np.testing.assert_array_equal(taken[b].cpu().numpy(), rtk, err_msg=msg)
+
+
+@pytest.mark.timeout(300)
 def test_fps_batch_beyond_one_wave():
     """40 clouds of 24000 points: more clusters than fit co-resident, so the
     speculative kernel runs in waves; FastPoint-prefix-length FPS, spot-checked

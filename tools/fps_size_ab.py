@@ -1,4 +1,4 @@
-"""Speculative vs one-sample exact FPS by cloud size (B clouds, n = N/2):
+"""Default dispatch vs one-sample vs no warp-per-cloud kernel, exact FPS by cloud size (B clouds, n = N/2):
 us per iteration, CUDA events, to place the dispatch crossover."""
 import os
 import sys
@@ -10,13 +10,14 @@ from paper_2507_23480_b200 import engine  # noqa: E402
 from paper_2507_23480_b200.harness import generate_cloud  # noqa: E402
 
 B = int(os.environ.get("B", "32"))
-for N in (256, 512, 1024, 2048, 4096, 8192, 16384):
+for N in (64, 128, 256, 512, 1024, 2048, 4096):
     import numpy as np
     c = np.stack([generate_cloud("unit-sphere", N, 7 + b) for b in range(B)])
     x = engine.as_xyz4(torch.from_numpy(c).cuda())
     row = []
-    for env in ({}, {"PS_FPS_NOSPEC": "1"}):
+    for env in ({}, {"PS_FPS_NOSPEC": "1"}, {"PS_FPS_NOWARP": "1"}):
         os.environ.pop("PS_FPS_NOSPEC", None)
+        os.environ.pop("PS_FPS_NOWARP", None)
         os.environ.update(env)
         engine.fps(x, N // 2)
         torch.cuda.synchronize()
@@ -28,4 +29,5 @@ for N in (256, 512, 1024, 2048, 4096, 8192, 16384):
         torch.cuda.synchronize()
         row.append(e[0].elapsed_time(e[1]) / 3 * 1e3 / (N // 2 - 1))
     os.environ.pop("PS_FPS_NOSPEC", None)
-    print(f"B={B} N={N:6d}: speculative {row[0]:.3f} us/it, one-sample {row[1]:.3f} us/it", flush=True)
+    os.environ.pop("PS_FPS_NOWARP", None)
+    print(f"B={B} N={N:6d}: default {row[0]:.3f} us/it, one-sample {row[1]:.3f}, without warp kernel {row[2]:.3f}", flush=True)
