@@ -708,6 +708,7 @@ __global__ void __launch_bounds__(kEllWarps * 32, 4) grid_ell_kernel(int64_t B, 
     __shared__ int hcnt[kEllWarps][33];          // per-bucket counts
     __shared__ double lvs[kEllWarps][32];
     __shared__ unsigned long long lvb[kEllWarps][32];
+    __shared__ unsigned long long lvsort[kEllWarps][16];  // levels ascending, padded (L <= 16)
     __shared__ int tbase[kEllWarps][9];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
@@ -719,13 +720,18 @@ __global__ void __launch_bounds__(kEllWarps * 32, 4) grid_ell_kernel(int64_t B, 
         lvs[warp][lane] = my_r2;
         lvb[warp][lane] = (unsigned long long)__double_as_longlong(my_r2);
     }
-    int rank_lt = 0;
+    int rank_lt = 0, rank_st = 0;
     double r2 = 0.0;
     for (int l = 0; l < L; ++l) {
         const double v = __shfl_sync(kFull, my_r2, l);
         rank_lt += (v < my_r2) ? 1 : 0;
+        rank_st += (v < my_r2 || (v == my_r2 && l < lane)) ? 1 : 0;  // stable sort position
         r2 = fmax(r2, v);
     }
+    const bool sorted_lv = L <= 16;
+    if (lane < 16) lvsort[warp][lane] = ~0ull;
+    __syncwarp();
+    if (lane < L && sorted_lv) lvsort[warp][rank_st] = (unsigned long long)__double_as_longlong(my_r2);
     const float thr = prefilter_threshold(r2);
     const bool no_filter = !(thr <= FLT_MAX);
     const GridParams gp = g.params[b];
@@ -793,7 +799,17 @@ __global__ void __launch_bounds__(kEllWarps * 32, 4) grid_ell_kernel(int64_t B, 
                     // bucket by integer compares of the bit patterns (d, r2 >= 0): ALU, not FP64
                     const unsigned long long db = (unsigned long long)__double_as_longlong(d);
                     int bk = 0;
-                    for (int l = 0; l < L; ++l) bk += (lvb[warp][l] <= db) ? 1 : 0;
+                    if (sorted_lv) {
+                        // #levels <= d: branch-free upper bound over the sorted,
+                        // padded levels (a hit is below the largest, so <= 15)
+                        const unsigned long long* ls = lvsort[warp];
+                        bk = (ls[7] <= db) ? 8 : 0;
+                        bk += (ls[bk + 3] <= db) ? 4 : 0;
+                        bk += (ls[bk + 1] <= db) ? 2 : 0;
+                        bk += (ls[bk] <= db) ? 1 : 0;
+                    } else {
+                        for (int l = 0; l < L; ++l) bk += (lvb[warp][l] <= db) ? 1 : 0;
+                    }
                     hd[warp][slot] = d;
                     hj[warp][slot] = qi;
                     hb[warp][slot] = (uint8_t)atomicAdd(&hcnt[warp][bk], 1);  // rank within bucket
