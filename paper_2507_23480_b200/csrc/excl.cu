@@ -739,12 +739,13 @@ __global__ void __launch_bounds__(kEllWarps * 32, 4) grid_ell_kernel(int64_t B, 
     const int32_t* si = g.sorted_idx + b * N;
     const int* cs = g.cell_start + b * (g.max_cells + 1);
     __syncwarp();
+    unsigned long long evals = 0;  // candidates visited by this warp (one atomic at the end)
     for (int64_t s = (int64_t)blockIdx.x * kEllWarps + warp; s < N; s += (int64_t)gridDim.x * kEllWarps) {
         hcnt[warp][lane] = 0;
         if (lane == 0) hcnt[warp][32] = 0;
         __syncwarp();
         const float4 p = sx[s];
-        const int32_t i = si[s];
+        const int32_t i = __float_as_int(p.w);  // original index (grid_scatter_kernel)
         const int cx = cell_coord(p.x, gp.ox, gp.inv_h, gp.nx);
         const int cy = cell_coord(p.y, gp.oy, gp.inv_h, gp.ny);
         const int cz = cell_coord(p.z, gp.oz, gp.inv_h, gp.nz);
@@ -777,9 +778,14 @@ __global__ void __launch_bounds__(kEllWarps * 32, 4) grid_ell_kernel(int64_t B, 
 #pragma unroll 4
         for (int tb = 0; tb < total; tb += 32) {
             const int f = tb + lane;
-            int rr = 0;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) rr += (f >= e[q]) ? 1 : 0;
+            // rr = #(e[q] <= f) over the 8 sorted range starts: branch-free
+            // binary search by selects on registers
+            const bool c4 = f >= e[3];
+            int rr = c4 ? 4 : 0;
+            const bool c2 = f >= (c4 ? e[5] : e[1]);
+            rr += c2 ? 2 : 0;
+            rr += (f >= (c4 ? (c2 ? e[6] : e[4]) : (c2 ? e[2] : e[0]))) ? 1 : 0;
+            rr += (rr == 7 && f >= e[7]) ? 1 : 0;
             const int t = tbase[warp][rr] + f;
             bool hit = false;
             double d = 0.0;
@@ -818,7 +824,7 @@ __global__ void __launch_bounds__(kEllWarps * 32, 4) grid_ell_kernel(int64_t B, 
             }
             cnt += __popc(hm);
         }
-        if (lane == 0) atomicAdd(g.evals + b, (unsigned long long)total);
+        evals += (unsigned long long)total;
         if (cnt > stride) {
             // overflow: flag it and leave a safe (empty) row until the host rebuilds
             if (lane == 0) atomicOr(&w.status[b], 2);
@@ -891,6 +897,7 @@ __global__ void __launch_bounds__(kEllWarps * 32, 4) grid_ell_kernel(int64_t B, 
         if (lane < L) csr.counts[(b * csr.L + lane) * N + i] = hist_mine;
         __syncwarp();
     }
+    if (lane == 0 && evals) atomicAdd(g.evals + b, evals);
 }
 
 __global__ void ell_indptr_kernel(int64_t B, int64_t N, int64_t stride, CsrView csr) {
