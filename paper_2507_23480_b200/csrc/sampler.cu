@@ -89,13 +89,28 @@ __global__ void __launch_bounds__(1024) thresholds_kernel(ThreshArgs a) {
     double est_d[kMaxSeg];
     if (a.mode == 0) {
         const double amp = s_a;
-        // min over tail positions i in [k0, d_s] for every s (prefix-min by segment)
-        for (int64_t i = k0 + threadIdx.x; i < n; i += blockDim.x) {
-            const double t = __ddiv_rn(amp, a.pow_tab[i]);
-            int s = 0;
-            while (s < nseg && a.d[s] < i) ++s;
-            if (s < nseg) atomicMin(&seg_min[s], (unsigned long long)__double_as_longlong(t));
+        // min over tail positions i in [k0, d_s] for every s (prefix-min by
+        // segment): each thread takes a contiguous run of positions, keeps a
+        // running min per segment and publishes it once per segment it
+        // touches (a few shared atomics per thread instead of one per
+        // position; min is order-free, so the result is unchanged)
+        const int64_t per = (n - k0 + blockDim.x - 1) / blockDim.x;
+        const int64_t i0 = k0 + (int64_t)threadIdx.x * per;
+        const int64_t i1 = i0 + per < n ? i0 + per : n;
+        int s = 0;
+        while (s < nseg && a.d[s] < i0) ++s;
+        unsigned long long run = 0x7ff0000000000000ull;
+        for (int64_t i = i0; i < i1 && s < nseg; ++i) {
+            if (a.d[s] < i) {
+                atomicMin(&seg_min[s], run);
+                run = 0x7ff0000000000000ull;
+                while (s < nseg && a.d[s] < i) ++s;
+                if (s >= nseg) break;
+            }
+            const unsigned long long t = (unsigned long long)__double_as_longlong(__ddiv_rn(amp, a.pow_tab[i]));
+            run = t < run ? t : run;
         }
+        if (s < nseg && i0 < i1) atomicMin(&seg_min[s], run);
         __syncthreads();
         if (threadIdx.x == 0) {
             double run = v[k0 - 1];
