@@ -351,6 +351,143 @@ __global__ void grid_scatter_kernel(const float4* __restrict__ xyz, int64_t B, i
     }
 }
 
+// ---- fused grid build: one 1024-thread CTA per cloud ---------------------------
+// Bounding box + grid parameters (identical arithmetic to grid_setup_kernel),
+// cell assignment, exclusive scan and scatter in one launch, with the cell
+// counters in shared memory when the cloud's grid fits (else in its global
+// cell_start range); also zeroes the per-cloud bookkeeping the build reads
+// (evals, status) and, for method 2, writes the fixed-stride indptr.  Replaces
+// five launches and two memsets for clouds up to kGridFusedMaxN points (the
+// multi-kernel path above serves larger clouds and PS_GRID_MULTI=1).
+constexpr int kGridSmemCells = 48 * 1024;
+constexpr int64_t kGridFusedMaxN = 4096;
+
+__global__ void __launch_bounds__(1024) grid_build_kernel(const float4* __restrict__ xyz, int64_t N,
+                                                          const double* __restrict__ r2_levels, int L,
+                                                          int64_t levels_ld, GridWork g, ExclWork w, CsrView csr,
+                                                          int64_t stride, int write_indptr) {
+    extern __shared__ int cnt_s[];
+    __shared__ float red[6][32];
+    __shared__ GridParams gps;
+    __shared__ int warp_sums[32];
+    __shared__ int carry;
+    const int64_t b = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const float4* cx = xyz + b * N;
+    if (tid == 0) {
+        g.evals[b] = 0;
+        w.status[b] = 0;
+        if (b == 0) *w.long_count = 0;
+    }
+    // 1. bounding box and grid parameters
+    float mn[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, mx[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
+    for (int64_t i = tid; i < N; i += 1024) {
+        const float4 p = cx[i];
+        mn[0] = fminf(mn[0], p.x); mn[1] = fminf(mn[1], p.y); mn[2] = fminf(mn[2], p.z);
+        mx[0] = fmaxf(mx[0], p.x); mx[1] = fmaxf(mx[1], p.y); mx[2] = fmaxf(mx[2], p.z);
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        for (int o = 16; o > 0; o >>= 1) {
+            mn[a] = fminf(mn[a], __shfl_xor_sync(kFull, mn[a], o));
+            mx[a] = fmaxf(mx[a], __shfl_xor_sync(kFull, mx[a], o));
+        }
+        if (lane == 0) { red[a][warp] = mn[a]; red[3 + a][warp] = mx[a]; }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double lo[3], ext[3];
+        for (int a = 0; a < 3; ++a) {
+            float m0 = FLT_MAX, m1 = -FLT_MAX;
+            for (int q = 0; q < 32; ++q) { m0 = fminf(m0, red[a][q]); m1 = fmaxf(m1, red[3 + a][q]); }
+            lo[a] = m0;
+            ext[a] = (double)m1 - (double)m0;
+        }
+        double r2 = 0.0;
+        for (int l = 0; l < L; ++l) r2 = fmax(r2, r2_levels[b * levels_ld + l]);
+        double h = sqrt(r2) * (1.0 + 1e-6);
+        if (!(h > 1e-30)) h = 1e-30;
+        int n[3];
+        for (int it = 0; it < 64; ++it) {
+            double tot = 1.0;
+            for (int a = 0; a < 3; ++a) {
+                const double c = floor(ext[a] / h) + 1.0;
+                n[a] = c > 1048576.0 ? 1048576 : (int)c;
+                tot *= (double)n[a];
+            }
+            if (tot <= (double)g.max_cells) break;
+            h *= cbrt(tot / (double)g.max_cells) * 1.001;
+        }
+        GridParams gp;
+        gp.ox = lo[0]; gp.oy = lo[1]; gp.oz = lo[2];
+        gp.inv_h = 1.0 / h;
+        gp.nx = n[0]; gp.ny = n[1]; gp.nz = n[2];
+        gp.ncells = n[0] * n[1] * n[2];
+        g.params[b] = gp;
+        gps = gp;
+        carry = 0;
+    }
+    __syncthreads();
+    const GridParams gp = gps;
+    const int nc = gp.ncells;
+    const bool sm = nc <= kGridSmemCells;
+    int* cs = g.cell_start + b * (g.max_cells + 1);
+    int* cnt = sm ? cnt_s : cs;
+    int* cur = sm ? cnt_s : g.cursor + b * (int64_t)g.max_cells;
+    for (int i = tid; i < nc; i += 1024) cnt[i] = 0;
+    __syncthreads();
+    // 2. cell of every point, counts
+    int32_t* cell_of = g.cell_of + b * N;
+    for (int64_t i = tid; i < N; i += 1024) {
+        const float4 p = cx[i];
+        const int c = (cell_coord(p.z, gp.oz, gp.inv_h, gp.nz) * gp.ny + cell_coord(p.y, gp.oy, gp.inv_h, gp.ny)) *
+                          gp.nx + cell_coord(p.x, gp.ox, gp.inv_h, gp.nx);
+        cell_of[i] = c;
+        atomicAdd(&cnt[c], 1);
+    }
+    __syncthreads();
+    // 3. exclusive scan -> cell_start (global) and the scatter cursors
+    for (int base = 0; base < nc; base += 1024) {
+        const int i = base + tid;
+        const int v = i < nc ? cnt[i] : 0;
+        int x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) warp_sums[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            int t = warp_sums[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(kFull, t, o);
+                if (lane >= o) t += y;
+            }
+            warp_sums[lane] = t;
+        }
+        __syncthreads();
+        const int ex = carry + (warp ? warp_sums[warp - 1] : 0) + x - v;
+        if (i < nc) { cs[i] = ex; cur[i] = ex; }
+        __syncthreads();
+        if (tid == 0) carry += warp_sums[31];
+        __syncthreads();
+    }
+    if (tid == 0) cs[nc] = carry;
+    // 4. scatter into cell order (original index in w)
+    for (int64_t i = tid; i < N; i += 1024) {
+        const int pos = atomicAdd(&cur[cell_of[i]], 1);
+        g.sorted_idx[b * N + pos] = (int32_t)i;
+        float4 v = cx[i];
+        v.w = __int_as_float((int)i);
+        g.sorted_xyz[b * N + pos] = v;
+    }
+    // 5. method 2: fixed-stride row pointers
+    if (write_indptr)
+        for (int64_t r = tid; r <= N; r += 1024) csr.indptr[b * (N + 1) + r] = r * stride;
+}
+
 // ---- row sort by (d2, index) + fused level counts -----------------------
 
 // Bitonic sort of n2 (power of two) entries in shared memory by `nthr`
@@ -926,20 +1063,43 @@ static cudaError_t launch_sort(CsrView csr, int64_t B, const double* r2_levels, 
 cudaError_t launch_excl_build(const float4* xyz, int64_t B, int64_t N, const double* r2_levels, int L,
                               int64_t levels_ld, CsrView csr, ExclWork w, GridWork g, int method, cudaStream_t s) {
     cudaError_t e;
-    if ((e = cudaMemsetAsync(w.deg, 0, sizeof(int32_t) * B * N, s)) != cudaSuccess) return e;
-    if ((e = cudaMemsetAsync(w.long_count, 0, sizeof(unsigned), s)) != cudaSuccess) return e;
-    if ((e = cudaMemsetAsync(w.status, 0, sizeof(int32_t) * B, s)) != cudaSuccess) return e;
+    // method 2 never reads the degrees; the fused grid build (methods 1, 2)
+    // zeroes status / long_count itself
+    // (one CTA per cloud: wins for small clouds -- C2 cascade 0.488 -> 0.474 ms
+    // -- and loses 11 us at C3's 24000 points, where the multi-kernel build
+    // spreads assignment and scatter over the whole GPU)
+    const bool fused_grid = (method == 1 || method == 2) && N <= kGridFusedMaxN && !getenv("PS_GRID_MULTI");
+    if (method != 2 && (e = cudaMemsetAsync(w.deg, 0, sizeof(int32_t) * B * N, s)) != cudaSuccess) return e;
+    if (!fused_grid) {
+        if ((e = cudaMemsetAsync(w.long_count, 0, sizeof(unsigned), s)) != cudaSuccess) return e;
+        if ((e = cudaMemsetAsync(w.status, 0, sizeof(int32_t) * B, s)) != cudaSuccess) return e;
+    }
     const unsigned gpts = (unsigned)std::min<int64_t>(148 * 16, (B * N + 255) / 256 + 1);
     if (method == 1 || method == 2) {
-        if ((e = cudaMemsetAsync(g.cell_start, 0, sizeof(int) * B * (g.max_cells + 1), s)) != cudaSuccess) return e;
-        if ((e = cudaMemsetAsync(g.evals, 0, sizeof(unsigned long long) * B, s)) != cudaSuccess) return e;
-        grid_setup_kernel<<<(unsigned)B, 1024, 0, s>>>(xyz, N, r2_levels, L, levels_ld, g);
-        grid_assign_kernel<<<gpts, 256, 0, s>>>(xyz, B, N, g);
-        grid_scan_kernel<<<(unsigned)B, 1024, 0, s>>>(N, g);
-        grid_scatter_kernel<<<gpts, 256, 0, s>>>(xyz, B, N, g);
+        const int64_t stride = csr.cap_entries / N;
+        const bool multi = !fused_grid;
+        if (multi) {
+            if ((e = cudaMemsetAsync(g.cell_start, 0, sizeof(int) * B * (g.max_cells + 1), s)) != cudaSuccess)
+                return e;
+            if ((e = cudaMemsetAsync(g.evals, 0, sizeof(unsigned long long) * B, s)) != cudaSuccess) return e;
+            grid_setup_kernel<<<(unsigned)B, 1024, 0, s>>>(xyz, N, r2_levels, L, levels_ld, g);
+            grid_assign_kernel<<<gpts, 256, 0, s>>>(xyz, B, N, g);
+            grid_scan_kernel<<<(unsigned)B, 1024, 0, s>>>(N, g);
+            grid_scatter_kernel<<<gpts, 256, 0, s>>>(xyz, B, N, g);
+            if (method == 2) ell_indptr_kernel<<<gpts, 256, 0, s>>>(B, N, stride, csr);
+        } else {
+            const size_t dsm = sizeof(int) * (size_t)kGridSmemCells;
+            static bool attr = false;
+            if (!attr) {
+                if ((e = cudaFuncSetAttribute(grid_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)dsm)) != cudaSuccess)
+                    return e;
+                attr = true;
+            }
+            grid_build_kernel<<<(unsigned)B, 1024, dsm, s>>>(xyz, N, r2_levels, L, levels_ld, g, w, csr, stride,
+                                                             method == 2 ? 1 : 0);
+        }
         if (method == 2) {
-            const int64_t stride = csr.cap_entries / N;
-            ell_indptr_kernel<<<gpts, 256, 0, s>>>(B, N, stride, csr);
             const int64_t gx = std::max<int64_t>(1, std::min<int64_t>((148 * 16 + B - 1) / B,
                                                                       (N + kEllWarps - 1) / kEllWarps));
             grid_ell_kernel<<<dim3((unsigned)gx, (unsigned)B), kEllWarps * 32, 0, s>>>(B, N, r2_levels, L, levels_ld,
