@@ -224,8 +224,9 @@ __global__ void excl_fill_kernel(int64_t N, ExclWork w, CsrView csr) {
 
 __global__ void __launch_bounds__(1024) grid_setup_kernel(const float4* __restrict__ xyz, int64_t N,
                                                           const double* __restrict__ r2_levels, int L,
-                                                          int64_t levels_ld, GridWork g) {
+                                                          int64_t levels_ld, GridWork g, ExclWork w, int zero) {
     __shared__ float red[6][32];
+    __shared__ int nc_s;
     const int64_t b = blockIdx.x;
     const float4* cx = xyz + b * N;
     float mn[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, mx[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
@@ -274,6 +275,18 @@ __global__ void __launch_bounds__(1024) grid_setup_kernel(const float4* __restri
         gp.nx = n[0]; gp.ny = n[1]; gp.nz = n[2];
         gp.ncells = n[0] * n[1] * n[2];
         g.params[b] = gp;
+        nc_s = gp.ncells;
+        if (zero) {
+            g.evals[b] = 0;
+            w.status[b] = 0;
+            if (b == 0) *w.long_count = 0;
+        }
+    }
+    if (zero) {
+        // this cloud's cell counters (grid_assign_kernel adds into them)
+        __syncthreads();
+        int* cs = g.cell_start + b * (g.max_cells + 1);
+        for (int i = threadIdx.x; i <= nc_s; i += blockDim.x) cs[i] = 0;
     }
 }
 
@@ -1070,7 +1083,7 @@ cudaError_t launch_excl_build(const float4* xyz, int64_t B, int64_t N, const dou
     // spreads assignment and scatter over the whole GPU)
     const bool fused_grid = (method == 1 || method == 2) && N <= kGridFusedMaxN && !getenv("PS_GRID_MULTI");
     if (method != 2 && (e = cudaMemsetAsync(w.deg, 0, sizeof(int32_t) * B * N, s)) != cudaSuccess) return e;
-    if (!fused_grid) {
+    if (method == 0) {  // the grid kernels (methods 1, 2) zero these themselves
         if ((e = cudaMemsetAsync(w.long_count, 0, sizeof(unsigned), s)) != cudaSuccess) return e;
         if ((e = cudaMemsetAsync(w.status, 0, sizeof(int32_t) * B, s)) != cudaSuccess) return e;
     }
@@ -1079,10 +1092,8 @@ cudaError_t launch_excl_build(const float4* xyz, int64_t B, int64_t N, const dou
         const int64_t stride = csr.cap_entries / N;
         const bool multi = !fused_grid;
         if (multi) {
-            if ((e = cudaMemsetAsync(g.cell_start, 0, sizeof(int) * B * (g.max_cells + 1), s)) != cudaSuccess)
-                return e;
-            if ((e = cudaMemsetAsync(g.evals, 0, sizeof(unsigned long long) * B, s)) != cudaSuccess) return e;
-            grid_setup_kernel<<<(unsigned)B, 1024, 0, s>>>(xyz, N, r2_levels, L, levels_ld, g);
+            // grid_setup_kernel zeroes the counters and bookkeeping it owns
+            grid_setup_kernel<<<(unsigned)B, 1024, 0, s>>>(xyz, N, r2_levels, L, levels_ld, g, w, 1);
             grid_assign_kernel<<<gpts, 256, 0, s>>>(xyz, B, N, g);
             grid_scan_kernel<<<(unsigned)B, 1024, 0, s>>>(N, g);
             grid_scatter_kernel<<<gpts, 256, 0, s>>>(xyz, B, N, g);
