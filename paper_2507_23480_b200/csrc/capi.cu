@@ -328,7 +328,7 @@ int ps_excl_build(const float* xyz4, int64_t B, int64_t N, const double* r2_leve
     ps::CsrView csr = {indptr, nbr, d2, counts, cap_entries, N, L};
     return cuda_status(ps::launch_excl_build(reinterpret_cast<const float4*>(xyz4), B, N, r2_levels, L, levels_ld,
                                              csr, ew, gw, method, S(stream)),
-                       "excl_build", method == 0 ? 6 : (method == 1 ? 8 : 6));
+                       "excl_build", ps::excl_build_launches(N, method));
 }
 
 int ps_csr_sort_rows(int64_t* indptr, int32_t* nbr, double* d2, int64_t cap_entries, int64_t B, int64_t N,
@@ -452,7 +452,7 @@ int ps_early_termination_prepare(const int64_t* indptr, const int32_t* nbr, cons
     a.indptr = indptr; a.nbr = nbr; a.d2 = d2; a.cap_entries = cap_entries; a.lvl1_counts = lvl1_counts;
     a.counts_stride = counts_stride; a.taken = taken; a.md = md; a.out_idx = out_idx; a.ld_out = ld_out;
     a.reached = reached; a.n_total = n_total; a.B = B; a.N = N;
-    return cuda_status(ps::launch_et(a, S(stream)), "early_termination_prepare", 3);
+    return cuda_status(ps::launch_et(a, S(stream)), "early_termination_prepare", ps::et_launches());
 }
 
 int ps_ball_query_rf(const int64_t* indptr, const int32_t* nbr, const double* d2, int64_t cap_entries,

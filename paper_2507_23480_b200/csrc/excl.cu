@@ -1073,6 +1073,14 @@ static cudaError_t launch_sort(CsrView csr, int64_t B, const double* r2_levels, 
     return cudaGetLastError();
 }
 
+// kernels one launch_excl_build issues (for ps_launch_count)
+int excl_build_launches(int64_t N, int method) {
+    const bool fused = (method == 1 || method == 2) && N <= kGridFusedMaxN && !getenv("PS_GRID_MULTI");
+    if (method == 0) return 6;
+    if (method == 1) return fused ? 5 : 8;
+    return fused ? 2 : 6;
+}
+
 cudaError_t launch_excl_build(const float4* xyz, int64_t B, int64_t N, const double* r2_levels, int L,
                               int64_t levels_ld, CsrView csr, ExclWork w, GridWork g, int method, cudaStream_t s) {
     cudaError_t e;

@@ -88,6 +88,7 @@ struct GridWork {
 
 // method 0: brute-force i<j triangle (every pair evaluated once)
 // method 1: uniform grid of cell width >= R_max (identical CSR)
+int excl_build_launches(int64_t N, int method);
 cudaError_t launch_excl_build(const float4* xyz, int64_t B, int64_t N, const double* r2_levels,
                               int L, int64_t levels_ld, CsrView csr, ExclWork w, GridWork g, int method,
                               cudaStream_t s);

@@ -229,6 +229,7 @@ __global__ void et_push_kernel(EtArgs a) {
         const int64_t b = g / a.n_total, t = g - b * a.n_total;
         if (a.reached[b] >= a.n_total || t >= a.reached[b]) continue;
         const int64_t q = a.out_idx[b * a.ld_out + t];
+        if (gl == 0) a.taken[b * a.N + q] = 1;  // et_mark's job, fused (push never reads taken)
         const int64_t base = a.indptr[b * (a.N + 1) + q];
         const int32_t c = a.lvl1_counts[b * a.counts_stride + q];
         const int32_t* nbr = a.nbr + b * a.cap_entries + base;
@@ -286,16 +287,20 @@ cudaError_t launch_thresholds(const ThreshArgs& a, int64_t B, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// kernels one launch_et issues (for ps_launch_count): reset + push (which also
+// marks the sampled points), or reset + mark + pull scan
+int et_launches() { return getenv("PS_ET_PULL") ? 3 : 2; }
+
 cudaError_t launch_et(const EtArgs& a, cudaStream_t s) {
     const unsigned g1 = (unsigned)std::min<int64_t>(148 * 8, (a.B * a.N + 255) / 256 + 1);
     et_prepare_kernel<<<g1, 256, 0, s>>>(a);
     const unsigned g2 = (unsigned)std::min<int64_t>(148 * 8, (a.B * a.n_total + 255) / 256 + 1);
-    et_mark_kernel<<<g2, 256, 0, s>>>(a);
     if (!getenv("PS_ET_PULL")) {
         const unsigned g3 = (unsigned)std::min<int64_t>(148 * 16, (a.B * a.n_total + 31) / 32 + 1);
         et_push_kernel<<<g3, 256, 0, s>>>(a);
         return cudaGetLastError();
     }
+    et_mark_kernel<<<g2, 256, 0, s>>>(a);
     EtScanArgs sa;
     sa.indptr = a.indptr; sa.nbr = a.nbr; sa.d2 = a.d2; sa.cap_entries = a.cap_entries;
     sa.lvl1_counts = a.lvl1_counts; sa.counts_stride = a.counts_stride;

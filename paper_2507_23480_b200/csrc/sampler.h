@@ -87,6 +87,7 @@ cudaError_t launch_sampler_v3(SampArgs a, int64_t B, cudaStream_t s);
 cudaError_t launch_sampler_v4(SampArgs a, int64_t B, cudaStream_t s);
 size_t sampler_v4_ws_bytes(int64_t B, int64_t N);
 cudaError_t launch_et(const EtArgs& a, cudaStream_t s);
+int et_launches();
 cudaError_t launch_et_scan(const EtScanArgs& a, cudaStream_t s);
 
 }  // namespace ps

@@ -351,7 +351,7 @@ class FastPoint:
         self._sampler()
         self._early_termination()
 
-    KERNELS_PER_SAMPLE = 1 + 1 + 6 + 1 + 3 + 1
+    KERNELS_PER_SAMPLE = 1 + 1 + 6 + 1 + 2 + 1  # prefix, thresholds, exclusion (N > 4096), sampler, ET seed, ET FPS
 
     def capture(self):
         """Capture ``sample`` into a CUDA graph (buffers are static)."""
