@@ -310,45 +310,50 @@ __global__ void grid_assign_kernel(const float4* __restrict__ xyz, int64_t B, in
     }
 }
 
-// per cloud: cell_start <- exclusive scan of counts; cursor <- copy
-__global__ void __launch_bounds__(1024) grid_scan_kernel(int64_t N, GridWork g) {
+// per cloud: cell_start <- exclusive scan of counts; cursor <- copy.  Each
+// thread scans a contiguous run of cells, so one block scan covers the whole
+// grid; method 2's fixed-stride row pointers are written here too
+// (write_indptr), saving a launch.
+__global__ void __launch_bounds__(1024) grid_scan_kernel(int64_t N, GridWork g, CsrView csr, int64_t stride,
+                                                         int write_indptr) {
     __shared__ int warp_sums[32];
-    __shared__ int carry;
     const int64_t b = blockIdx.x;
     const int nc = g.params[b].ncells;
     int* cs = g.cell_start + b * (g.max_cells + 1);
     int* cur = g.cursor + b * (int64_t)g.max_cells;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) carry = 0;
+    const int per = (nc + 1023) / 1024;
+    const int c0 = tid * per, c1 = c0 + per < nc ? c0 + per : nc;
+    int run = 0;
+    for (int i = c0; i < c1; ++i) run += cs[i];
+    int x = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[warp] = x;
     __syncthreads();
-    for (int base = 0; base < nc; base += 1024) {
-        const int i = base + tid;
-        const int v = i < nc ? cs[i] : 0;
-        int x = v;
+    if (warp == 0) {
+        int t = warp_sums[lane];
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(kFull, x, o);
-            if (lane >= o) x += y;
+            const int y = __shfl_up_sync(kFull, t, o);
+            if (lane >= o) t += y;
         }
-        if (lane == 31) warp_sums[warp] = x;
-        __syncthreads();
-        if (warp == 0) {
-            int s = warp_sums[lane];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(kFull, s, o);
-                if (lane >= o) s += y;
-            }
-            warp_sums[lane] = s;
-        }
-        __syncthreads();
-        const int ex = carry + (warp ? warp_sums[warp - 1] : 0) + x - v;
-        if (i < nc) { cs[i] = ex; cur[i] = ex; }
-        __syncthreads();
-        if (tid == 0) carry += warp_sums[31];
-        __syncthreads();
+        warp_sums[lane] = t;
     }
-    if (tid == 0) cs[nc] = carry;
+    __syncthreads();
+    int ex = (warp ? warp_sums[warp - 1] : 0) + x - run;
+    for (int i = c0; i < c1; ++i) {
+        const int v = cs[i];
+        cs[i] = ex;
+        cur[i] = ex;
+        ex += v;
+    }
+    if (tid == 1023) cs[nc] = warp_sums[31];
+    if (write_indptr)
+        for (int64_t r = tid; r <= N; r += 1024) csr.indptr[b * (N + 1) + r] = r * stride;
 }
 
 __global__ void grid_scatter_kernel(const float4* __restrict__ xyz, int64_t B, int64_t N, GridWork g) {
@@ -1050,14 +1055,6 @@ __global__ void __launch_bounds__(kEllWarps * 32, 4) grid_ell_kernel(int64_t B, 
     if (lane == 0 && evals) atomicAdd(g.evals + b, evals);
 }
 
-__global__ void ell_indptr_kernel(int64_t B, int64_t N, int64_t stride, CsrView csr) {
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < B * (N + 1);
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = t % (N + 1);
-        csr.indptr[t] = r * stride;
-    }
-}
-
 static cudaError_t launch_sort(CsrView csr, int64_t B, const double* r2_levels, int64_t levels_ld, ExclWork w,
                                cudaStream_t s) {
     excl_sort_small_kernel<<<148 * 8, kSortWarps * 32, 0, s>>>(csr, B, r2_levels, levels_ld, w);
@@ -1078,7 +1075,7 @@ int excl_build_launches(int64_t N, int method) {
     const bool fused = (method == 1 || method == 2) && N <= kGridFusedMaxN && !getenv("PS_GRID_MULTI");
     if (method == 0) return 6;
     if (method == 1) return fused ? 5 : 8;
-    return fused ? 2 : 6;
+    return fused ? 2 : 5;
 }
 
 cudaError_t launch_excl_build(const float4* xyz, int64_t B, int64_t N, const double* r2_levels, int L,
@@ -1103,9 +1100,8 @@ cudaError_t launch_excl_build(const float4* xyz, int64_t B, int64_t N, const dou
             // grid_setup_kernel zeroes the counters and bookkeeping it owns
             grid_setup_kernel<<<(unsigned)B, 1024, 0, s>>>(xyz, N, r2_levels, L, levels_ld, g, w, 1);
             grid_assign_kernel<<<gpts, 256, 0, s>>>(xyz, B, N, g);
-            grid_scan_kernel<<<(unsigned)B, 1024, 0, s>>>(N, g);
+            grid_scan_kernel<<<(unsigned)B, 1024, 0, s>>>(N, g, csr, stride, method == 2 ? 1 : 0);
             grid_scatter_kernel<<<gpts, 256, 0, s>>>(xyz, B, N, g);
-            if (method == 2) ell_indptr_kernel<<<gpts, 256, 0, s>>>(B, N, stride, csr);
         } else {
             const size_t dsm = sizeof(int) * (size_t)kGridSmemCells;
             static bool attr = false;
