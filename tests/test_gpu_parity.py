@@ -418,14 +418,16 @@ def test_excl_matches_oracle(family, N, R):
         np.testing.assert_array_equal(counts, e.counts)
 
 
-def test_excl_bucketed_rows_match_oracle_sets():
+@pytest.mark.parametrize("N", [5000, 4096, 1000])
+def test_excl_bucketed_rows_match_oracle_sets(N):
     # method 2 (hot path): fixed stride, rows bucketed by level -- every
-    # level's entries are the row prefix; as sets they equal the reference's
-    c = generate_cloud("room-surfaces", 5000, 5)
+    # level's entries are the row prefix; as sets they equal the reference's.
+    # N <= 4096 takes the fused one-CTA grid build, 5000 the multi-kernel one.
+    c = generate_cloud("room-surfaces", N, 5)
     R = [0.3, 0.25, 0.2, 0.2, 0.15, 0.1]
     e = O.build_exclusion_lists(c, R, (0.12,))
     levels = np.array([O.radius_sq(r) for r in R] + [O.radius_sq(0.12)])
-    csr = engine.DeviceCsr.allocate(1, 5000, len(levels), 5000 * 256, 1, torch.device("cuda"), 2)
+    csr = engine.DeviceCsr.allocate(1, N, len(levels), N * 256, 1, torch.device("cuda"), 2)
     csr.levels.copy_(torch.from_numpy(levels.reshape(1, -1)))
     csr.build(engine.as_xyz4(c))
     assert not csr.overflowed()
@@ -435,7 +437,7 @@ def test_excl_bucketed_rows_match_oracle_sets():
     pos = {float(v): k for k, v in enumerate(e.r2_levels)}
     for l, lv in enumerate(levels):
         np.testing.assert_array_equal(counts[l], e.counts[pos[float(lv)]])
-    for i in range(0, 5000, 7):
+    for i in range(0, N, 7):
         m = counts[0]  # widest level is R[0]
         got = sorted(zip(d2[i * 256:i * 256 + m[i]].tolist(), nbr[i * 256:i * 256 + m[i]].tolist()))
         lo = e.indptr[i]
