@@ -412,28 +412,44 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
         if (kSm) {
             for (int64_t j = jlo + tid; j < jhi; j += kT4) mycnt += avail[j];
         } else {
-            for (int64_t j = jlo + tid; j < jhi; j += kT4) {
-                if (!avail[j]) continue;
-                ++mycnt;
-                const int32_t c = cnt_lvl[j];
-                const int32_t* row = nbr + indptr[j];
-                int32_t* ao = adj + j * kAdj4;
-                int n = 0;
-                for (int32_t u0 = 0; u0 < c; u0 += kRB) {
-                    int32_t qq[kRB];
-                    row_batch(row, u0, c, qq);
-                    uint8_t av[kRB];
-#pragma unroll
-                    for (int k = 0; k < kRB; ++k) av[k] = (qq[k] >= 0 && qq[k] != (int32_t)j) ? avail[qq[k]] : 0;
+            // two points per thread in flight (j, j + kT4): their L2 round trips
+            // (availability, counts, row entries, neighbours' availability) overlap
+            for (int64_t j = jlo + tid; j < jhi; j += 2 * kT4) {
+                const int64_t j2 = j + kT4;
+                const bool a1 = avail[j] != 0;
+                const bool a2 = j2 < jhi && avail[j2] != 0;
+                mycnt += (a1 ? 1 : 0) + (a2 ? 1 : 0);
+                const int32_t c1 = a1 ? cnt_lvl[j] : 0, c2 = a2 ? cnt_lvl[j2] : 0;
+                const int32_t* row1 = nbr + (a1 ? indptr[j] : 0);
+                const int32_t* row2 = nbr + (a2 ? indptr[j2] : 0);
+                int32_t* ao1 = adj + j * kAdj4;
+                int32_t* ao2 = adj + j2 * kAdj4;
+                int n1 = 0, n2 = 0;
+                const int32_t cm = c1 > c2 ? c1 : c2;
+                for (int32_t u0 = 0; u0 < cm; u0 += kRB) {
+                    int32_t q1[kRB], q2[kRB];
+                    row_batch(row1, u0, c1, q1);
+                    row_batch(row2, u0, c2, q2);
+                    uint8_t v1[kRB], v2[kRB];
 #pragma unroll
                     for (int k = 0; k < kRB; ++k) {
-                        if (av[k]) {
-                            if (n < kAdj4) ao[n] = qq[k];
-                            ++n;
+                        v1[k] = (q1[k] >= 0 && q1[k] != (int32_t)j) ? avail[q1[k]] : 0;
+                        v2[k] = (q2[k] >= 0 && q2[k] != (int32_t)j2) ? avail[q2[k]] : 0;
+                    }
+#pragma unroll
+                    for (int k = 0; k < kRB; ++k) {
+                        if (v1[k]) {
+                            if (n1 < kAdj4) ao1[n1] = q1[k];
+                            ++n1;
+                        }
+                        if (v2[k]) {
+                            if (n2 < kAdj4) ao2[n2] = q2[k];
+                            ++n2;
                         }
                     }
                 }
-                adjcnt[j] = n > kAdj4 ? kAdjOvf : (uint8_t)n;
+                if (a1) adjcnt[j] = n1 > kAdj4 ? kAdjOvf : (uint8_t)n1;
+                if (a2) adjcnt[j2] = n2 > kAdj4 ? kAdjOvf : (uint8_t)n2;
             }
         }
         mycnt = bsum(mycnt, wt);
