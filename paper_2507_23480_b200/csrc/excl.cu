@@ -310,50 +310,50 @@ __global__ void grid_assign_kernel(const float4* __restrict__ xyz, int64_t B, in
     }
 }
 
-// per cloud: cell_start <- exclusive scan of counts; cursor <- copy.  Each
-// thread scans a contiguous run of cells, so one block scan covers the whole
-// grid; method 2's fixed-stride row pointers are written here too
-// (write_indptr), saving a launch.
+// per cloud: cell_start <- exclusive scan of counts; cursor <- copy (coalesced
+// 1024-cell rounds); method 2's fixed-stride row pointers are written here
+// too (write_indptr), saving a launch.
 __global__ void __launch_bounds__(1024) grid_scan_kernel(int64_t N, GridWork g, CsrView csr, int64_t stride,
                                                          int write_indptr) {
     __shared__ int warp_sums[32];
+    __shared__ int carry;
     const int64_t b = blockIdx.x;
     const int nc = g.params[b].ncells;
     int* cs = g.cell_start + b * (g.max_cells + 1);
     int* cur = g.cursor + b * (int64_t)g.max_cells;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int per = (nc + 1023) / 1024;
-    const int c0 = tid * per, c1 = c0 + per < nc ? c0 + per : nc;
-    int run = 0;
-    for (int i = c0; i < c1; ++i) run += cs[i];
-    int x = run;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(kFull, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) warp_sums[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-        int t = warp_sums[lane];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(kFull, t, o);
-            if (lane >= o) t += y;
-        }
-        warp_sums[lane] = t;
-    }
-    __syncthreads();
-    int ex = (warp ? warp_sums[warp - 1] : 0) + x - run;
-    for (int i = c0; i < c1; ++i) {
-        const int v = cs[i];
-        cs[i] = ex;
-        cur[i] = ex;
-        ex += v;
-    }
-    if (tid == 1023) cs[nc] = warp_sums[31];
     if (write_indptr)
         for (int64_t r = tid; r <= N; r += 1024) csr.indptr[b * (N + 1) + r] = r * stride;
+    if (tid == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < nc; base += 1024) {
+        const int i = base + tid;
+        const int v = i < nc ? cs[i] : 0;
+        int x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) warp_sums[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            int t = warp_sums[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(kFull, t, o);
+                if (lane >= o) t += y;
+            }
+            warp_sums[lane] = t;
+        }
+        __syncthreads();
+        const int ex = carry + (warp ? warp_sums[warp - 1] : 0) + x - v;
+        if (i < nc) { cs[i] = ex; cur[i] = ex; }
+        __syncthreads();
+        if (tid == 0) carry += warp_sums[31];
+        __syncthreads();
+    }
+    if (tid == 0) cs[nc] = carry;
 }
 
 __global__ void grid_scatter_kernel(const float4* __restrict__ xyz, int64_t B, int64_t N, GridWork g) {
