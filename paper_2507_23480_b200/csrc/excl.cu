@@ -295,10 +295,18 @@ __device__ __forceinline__ int cell_coord(double v, double o, double inv_h, int 
     return c < 0 ? 0 : (c >= n ? n - 1 : c);
 }
 
-__global__ void grid_assign_kernel(const float4* __restrict__ xyz, int64_t B, int64_t N, GridWork g) {
+// (method 2: also the fixed-stride row pointers, indptr[b][i] = i * stride,
+// spread over the whole grid instead of a launch of their own)
+__global__ void grid_assign_kernel(const float4* __restrict__ xyz, int64_t B, int64_t N, GridWork g, CsrView csr,
+                                   int64_t stride, int write_indptr) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < B * N;
          t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t b = t / N;
+        if (write_indptr) {
+            const int64_t i = t - b * N;
+            csr.indptr[b * (N + 1) + i] = i * stride;
+            if (i == N - 1) csr.indptr[b * (N + 1) + N] = N * stride;
+        }
         const GridParams gp = g.params[b];
         const float4 p = xyz[t];
         const int cx = cell_coord(p.x, gp.ox, gp.inv_h, gp.nx);
@@ -311,10 +319,8 @@ __global__ void grid_assign_kernel(const float4* __restrict__ xyz, int64_t B, in
 }
 
 // per cloud: cell_start <- exclusive scan of counts; cursor <- copy (coalesced
-// 1024-cell rounds); method 2's fixed-stride row pointers are written here
-// too (write_indptr), saving a launch.
-__global__ void __launch_bounds__(1024) grid_scan_kernel(int64_t N, GridWork g, CsrView csr, int64_t stride,
-                                                         int write_indptr) {
+// 1024-cell rounds).
+__global__ void __launch_bounds__(1024) grid_scan_kernel(int64_t N, GridWork g) {
     __shared__ int warp_sums[32];
     __shared__ int carry;
     const int64_t b = blockIdx.x;
@@ -322,8 +328,6 @@ __global__ void __launch_bounds__(1024) grid_scan_kernel(int64_t N, GridWork g, 
     int* cs = g.cell_start + b * (g.max_cells + 1);
     int* cur = g.cursor + b * (int64_t)g.max_cells;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (write_indptr)
-        for (int64_t r = tid; r <= N; r += 1024) csr.indptr[b * (N + 1) + r] = r * stride;
     if (tid == 0) carry = 0;
     __syncthreads();
     for (int base = 0; base < nc; base += 1024) {
@@ -1099,8 +1103,8 @@ cudaError_t launch_excl_build(const float4* xyz, int64_t B, int64_t N, const dou
         if (multi) {
             // grid_setup_kernel zeroes the counters and bookkeeping it owns
             grid_setup_kernel<<<(unsigned)B, 1024, 0, s>>>(xyz, N, r2_levels, L, levels_ld, g, w, 1);
-            grid_assign_kernel<<<gpts, 256, 0, s>>>(xyz, B, N, g);
-            grid_scan_kernel<<<(unsigned)B, 1024, 0, s>>>(N, g, csr, stride, method == 2 ? 1 : 0);
+            grid_assign_kernel<<<gpts, 256, 0, s>>>(xyz, B, N, g, csr, stride, method == 2 ? 1 : 0);
+            grid_scan_kernel<<<(unsigned)B, 1024, 0, s>>>(N, g);
             grid_scatter_kernel<<<gpts, 256, 0, s>>>(xyz, B, N, g);
         } else {
             const size_t dsm = sizeof(int) * (size_t)kGridSmemCells;
