@@ -59,7 +59,7 @@ PS_DEV bool ranks_above(uint64_t ka, uint32_t ia, uint64_t kb, uint32_t ib) {
     return ka > kb || (ka == kb && ia < ib);
 }
 
-constexpr int kR = 8;             // records per CTA per exchange: its max + kR-1 threshold candidates
+constexpr int kR = 10;            // records per CTA per exchange: its max + kR-1 threshold candidates
 constexpr int kRunMax = 31;       // samples per exchange (one lane each)
 constexpr double kTarget = 22.0;  // threshold candidates aimed for per exchange
 constexpr uint64_t kTauOff = ~0ull;  // threshold disabled (above every md bit pattern)
@@ -495,12 +495,13 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
                 hcnt = (int)h1.w;
             }
             bool overflow = __any_sync(kFull, hcnt > kR - 1);
-            const int hn = hcnt < kR - 1 ? hcnt : kR - 1;  // <= 7: prefix sum from three ballots
+            const int hn = hcnt < kR - 1 ? hcnt : kR - 1;  // prefix sum from one ballot per bit of kR - 1
+            static_assert(kR - 1 < 16, "four ballots");
             const uint32_t lt = (1u << lane) - 1u;
             const uint32_t b0 = __ballot_sync(kFull, hn & 1), b1 = __ballot_sync(kFull, hn & 2),
-                           b2 = __ballot_sync(kFull, hn & 4);
-            const int base = __popc(b0 & lt) + 2 * __popc(b1 & lt) + 4 * __popc(b2 & lt);
-            const int ncand_all = __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
+                           b2 = __ballot_sync(kFull, hn & 4), b3 = kR - 1 > 7 ? __ballot_sync(kFull, hn & 8) : 0u;
+            const int base = __popc(b0 & lt) + 2 * __popc(b1 & lt) + 4 * __popc(b2 & lt) + 8 * __popc(b3 & lt);
+            const int ncand_all = __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2) + 8 * __popc(b3);
             for (int k = 0; k < hn; ++k)
                 if (base + k < 32) sts_u8(a_map + base + k, (uint32_t)(lane * kR + 1 + k));
             overflow = overflow || ncand_all > 32;
