@@ -833,10 +833,11 @@ __global__ void __launch_bounds__(kT, 1) fps_res_kernel(FpsArgs a, FpsRanks rk) 
                 bool ovf = __any_sync(kFull, hcnt > kRc);
                 const int hn = hcnt < kRc ? hcnt : kRc;
                 const uint32_t lt = (1u << lane) - 1u;
+                static_assert(kRc < 16, "four ballots");
                 const uint32_t b0 = __ballot_sync(kFull, hn & 1), b1 = __ballot_sync(kFull, hn & 2),
-                               b2 = __ballot_sync(kFull, hn & 4);
-                const int cbase = __popc(b0 & lt) + 2 * __popc(b1 & lt) + 4 * __popc(b2 & lt);
-                const int cn_all = __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
+                               b2 = __ballot_sync(kFull, hn & 4), b3 = kRc > 7 ? __ballot_sync(kFull, hn & 8) : 0u;
+                const int cbase = __popc(b0 & lt) + 2 * __popc(b1 & lt) + 4 * __popc(b2 & lt) + 8 * __popc(b3 & lt);
+                const int cn_all = __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2) + 8 * __popc(b3);
                 ovf = ovf || cn_all > 32;
                 for (int k = 0; k < hn; ++k)
                     if (cbase + k < 32) cl_s[cbase + k] = cslots[par][lane * kRS + 1 + k];
