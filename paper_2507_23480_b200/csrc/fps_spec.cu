@@ -64,7 +64,7 @@ constexpr int kRunMax = 31;       // samples per exchange (one lane each)
 constexpr double kTarget = 22.0;  // threshold candidates aimed for per exchange
 constexpr uint64_t kTauOff = ~0ull;  // threshold disabled (above every md bit pattern)
 constexpr int kMaxS = 4096;          // points per CTA the spatial sort holds
-constexpr int64_t kSortMinIters = 256;  // runs shorter than this keep the index order
+constexpr int64_t kSortMinIters = 64;  // runs shorter than this keep the index order
 constexpr float kInfF = __builtin_huge_valf();
 
 template <int P, int T, bool kLeadPts>
