@@ -170,10 +170,31 @@ def peaks():
 # reference arm: the reference's CPU path (oracle port) on the host cores
 
 
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
 def cpu_run(clouds, exponent, threads):
+    """The reference's CPU path on `threads` host threads: one cloud per pool
+    thread (the kernels release the GIL, like the reference's nogil numba
+    kernels) and, when there are more threads than clouds, the reference's
+    per-cloud worker split of FPS and excl_collect (core.workers,
+    core.py:71-101) over the rest."""
     from concurrent.futures import ThreadPoolExecutor
 
     from oracle import oracle as O
+
+    B = clouds.shape[0]
+    pool = max(1, min(threads, B))
+    old = O.set_threads(max(1, threads // pool))
 
     def one(b):
         r = O.mdps(clouds[b], n_SAMPLES, p=P, nseg=NSEG, estimator="power", exponent=exponent, rng_seed=b,
@@ -181,10 +202,38 @@ def cpu_run(clouds, exponent, threads):
         O.rf_ball_query(r.excl, RADIUS, r.indices, K)
         return r.indices
 
-    t0 = time.perf_counter()
-    with ThreadPoolExecutor(threads) as ex:
-        out = list(ex.map(one, range(clouds.shape[0])))
-    return time.perf_counter() - t0, out
+    try:
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(pool) as ex:
+            out = list(ex.map(one, range(B)))
+        return time.perf_counter() - t0, out
+    finally:
+        O.set_threads(old)
+
+
+def cpu_baseline(clouds, exponent, gpu_idx, runs):
+    """threads = 1 and threads = os.cpu_count(), one
+    warm-up then the median of `runs` timed runs each, CPU model named; the
+    indices are checked against the GPU run of the same batch."""
+    res = {}
+    match = None
+    for t in sorted({1, os.cpu_count() or 1}):
+        cpu_run(clouds[:1], exponent, 1)  # warm-up (oracle load, page-in)
+        times = []
+        for _ in range(max(1, runs)):
+            dt, idx = cpu_run(clouds, exponent, t)
+            times.append(dt)
+        if match is None and gpu_idx is not None:
+            match = all(np.array_equal(idx[b], gpu_idx[b]) for b in range(clouds.shape[0]))
+        med = statistics.median(times)
+        res[t] = {"value": clouds.shape[0] * n_SAMPLES / med, "median_s": med, "runs_s": times}
+    tmax = max(res)
+    return {"value": res[tmax]["value"], "unit": UNIT, "cores": tmax, "kind": "port",
+            "cpu": cpu_model(), "threads_1": res[1], f"threads_{tmax}": res[tmax],
+            "sample": (f"the rank-0 batch ({clouds.shape[0]} clouds) FastPoint + rf ball query per run, one cloud per "
+                       "thread plus the reference's per-cloud worker split; warm-up + median of "
+                       f"{max(1, runs)} runs per thread count"),
+            "indices_bit_exact_vs_gpu": match}
 
 
 def run_reference(args):
@@ -193,7 +242,7 @@ def run_reference(args):
         return 0
     clouds = clouds_for(0, B_PER_GPU)
     exponent = heldout_exponent_cpu()
-    threads = min(os.cpu_count() or 1, B_PER_GPU)
+    threads = os.cpu_count() or 1
     for _ in range(max(args.warmup, 0)):
         cpu_run(clouds[:1], exponent, 1)
     times = []
@@ -202,13 +251,16 @@ def run_reference(args):
         times.append(dt)
     t = sum(times)
     value = B_PER_GPU * n_SAMPLES * args.steps / t
-    sample = f"{B_PER_GPU} clouds x (FastPoint + rf ball query) per step, one cloud per thread"
+    sample = (f"{B_PER_GPU} clouds x (FastPoint + rf ball query) per step on all {threads} host threads: one cloud "
+              "per pool thread plus the reference's per-cloud worker split")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "family": FAMILY, "B": B_PER_GPU, "N": N, "n": n_SAMPLES},
+            "config": {"workload": WORKLOAD, "family": FAMILY, "B": B_PER_GPU, "B_per_gpu": B_PER_GPU, "N": N,
+                       "n": n_SAMPLES},
             "us_per_cloud": 1e6 * t / (args.steps * B_PER_GPU),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+                             "cpu": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -216,6 +268,87 @@ def run_reference(args):
 
 # ---------------------------------------------------------------------------
 # our arm
+
+
+L2_BYTES = 126 << 20  # B200 L2 (126 MB)
+
+
+def input_ring(rank: int, B: int):
+    """Distinct input batches whose float32 coordinates together exceed L2,
+    so that no timed step re-reads an input batch L2 still holds (the
+    contract's alternative to a flush).  Batch 0 is the rank's shard batch."""
+    per = B * N * 3 * 4
+    R = -(-int(1.25 * L2_BYTES) // per)
+    from paper_2507_23480_b200.harness import generate_cloud
+
+    ring = [clouds_for(rank, B)]
+    for k in range(1, R):
+        ring.append(np.stack([generate_cloud(FAMILY, N, 7_000_000 + (rank * R + k) * B + b) for b in range(B)]))
+    return np.stack(ring)  # [R, B, N, 3]
+
+
+class Chain:
+    """One FastPoint pipeline (buffers, stream, CUDA graph of sample + rf
+    grouping) -- the unit the bench runs S of concurrently."""
+
+    def __init__(self, B, exponent, dev, seeds):
+        import torch
+
+        from paper_2507_23480_b200 import engine
+
+        self.fp = engine.FastPoint(B, N, n_SAMPLES, p=P, nseg=NSEG, estimator="power", exponent=exponent,
+                                   extra_radii=(RADIUS,), device=dev)
+        self.grp = (torch.empty(B, n_SAMPLES, K, dtype=torch.int32, device=dev),
+                    torch.empty(B, n_SAMPLES, K, dtype=torch.float64, device=dev),
+                    torch.empty(B, n_SAMPLES, dtype=torch.int32, device=dev))
+        self.seed_t = torch.tensor(seeds, dtype=torch.int64, device=dev)
+        self.stream = torch.cuda.Stream(device=dev)
+        self.graph = None
+
+    def body(self):
+        self.fp.state.copy_(self.seed_t)
+        self.fp.sample()
+        self.fp.group_rf(RADIUS, K, out=self.grp)
+
+    def capture(self):
+        import torch
+
+        s = self.stream
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self.body()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        self.fp.check()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            self.body()
+        self.graph = g
+
+
+def run_chains(chains, steps, feed, after=None):
+    """Steps round-robin over the chains' streams (step s on chain s % S):
+    feed(chain, s) enqueues the step's input, the graph the step, after(chain,
+    s) its output.  Device wall time between events around the whole loop."""
+    import torch
+
+    main = torch.cuda.current_stream()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(main)
+    for c in chains:
+        c.stream.wait_event(a)
+    for s in range(steps):
+        c = chains[s % len(chains)]
+        with torch.cuda.stream(c.stream):
+            feed(c, s)
+            c.graph.replay()
+            if after is not None:
+                after(c, s)
+    for c in chains:
+        main.wait_stream(c.stream)
+    b.record(main)
+    b.synchronize()
+    return a.elapsed_time(b)
 
 
 def main_ours(args):
@@ -230,26 +363,26 @@ def main_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     B = B_PER_GPU
-    clouds = clouds_for(rank, B)
+    ring_h = input_ring(rank, B)
+    R = ring_h.shape[0]
+    clouds = ring_h[0]
     exponent = heldout_exponent()
-
-    fp = engine.FastPoint(B, N, n_SAMPLES, p=P, nseg=NSEG, estimator="power", exponent=exponent,
-                          extra_radii=(RADIUS,), device=dev)
-    d_pts = torch.from_numpy(clouds).to(dev)
-    fp.set_points(d_pts)
+    S = max(1, args.streams)
     seeds = [rank * B + b for b in range(B)]  # sampler RNG seeds (clouds: shard_seeds)
-    grp = (torch.empty(B, n_SAMPLES, K, dtype=torch.int32, device=dev),
-           torch.empty(B, n_SAMPLES, K, dtype=torch.float64, device=dev),
-           torch.empty(B, n_SAMPLES, dtype=torch.int32, device=dev))
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    chains = [Chain(B, exponent, dev, seeds) for _ in range(S)]
+    ring_d = torch.from_numpy(ring_h).to(dev)  # [R, B, N, 3] resident inputs
+    for c in chains:
+        c.fp.set_points(ring_d[0])
+        c.capture()
+    fp = chains[0].fp
     stream = torch.cuda.current_stream()
 
-    def step(events=None):
-        fp.state.copy_(seed_t)
-        if events is None:
-            fp.sample()
-            fp.group_rf(RADIUS, K, out=grp)
-            return
+    # ---- stage breakdown: one chain, per-stage events, L2 flushed between steps ----
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    stages = ["fps_prefix", "thresholds", "excl_build", "sampler", "early_term", "rf_ball_query"]
+
+    def staged(events):
+        fp.state.copy_(chains[0].seed_t)
         events[0].record(stream)
         fp._prefix()
         events[1].record(stream)
@@ -261,161 +394,160 @@ def main_ours(args):
         events[4].record(stream)
         fp._early_termination()
         events[5].record(stream)
-        fp.group_rf(RADIUS, K, out=grp)
+        fp.group_rf(RADIUS, K, out=chains[0].grp)
         events[6].record(stream)
 
-    seed_t = torch.tensor(seeds, dtype=torch.int64, device=dev)
-    # warm-up (also grows CSR capacity if ever needed)
+    fp.set_points(ring_d[0])
     for _ in range(max(args.warmup, 3)):
-        step()
-    fp.check()
+        staged([torch.cuda.Event(enable_timing=True) for _ in range(7)])
     torch.cuda.synchronize()
-
-    stages = ["fps_prefix", "thresholds", "excl_build", "sampler", "early_term", "rf_ball_query"]
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in range(args.steps)]
+    for s in range(args.steps):
+        fp.set_points(ring_d[s % R])
+        flush.zero_()  # L2 flush between steps, outside the events
+        staged(ev[s])
+    torch.cuda.synchronize()
+    stage_ms = np.array([[ev[s][i].elapsed_time(ev[s][i + 1]) for i in range(6)] for s in range(args.steps)])
+    per_stage = {nm: float(stage_ms[:, i].mean()) for i, nm in enumerate(stages)}
+    del flush
+
+    # ---- headline: S concurrent chains, steps back to back, inputs cold (ring > L2) ----
+    def feed_dev(c, s):
+        c.fp.set_points(ring_d[s % R])
+
+    for _ in range(max(args.warmup, 3)):
+        run_chains(chains, S, feed_dev)
     launches0 = _lib.launch_count()
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        for s in range(args.steps):
-            flush.zero_()  # L2 flush between steps (untimed: outside the events)
-            step(ev[s])
-        torch.cuda.synchronize()
-    launches = _lib.launch_count() - launches0
-    if ws > 1:
-        dist.barrier()
-    stage_ms = np.array([[ev[s][i].elapsed_time(ev[s][i + 1]) for i in range(6)] for s in range(args.steps)])
-    t_ms = max_over_ranks(float(stage_ms.sum()), dev)
+        t_ms = run_chains(chains, args.steps, feed_dev)
+    launches = (_lib.launch_count() - launches0)
+    t_ms = max_over_ranks(t_ms, dev)
     value = ws * B * n_SAMPLES * args.steps / (t_ms / 1e3)
-    per_stage = {nm: float(stage_ms[:, i].mean()) for i, nm in enumerate(stages)}
+    # one chain alone (no cross-step overlap), same loop
+    t1_ms = max_over_ranks(run_chains(chains[:1], args.steps, feed_dev), dev)
 
-    # parity spot check of this run (first cloud) is in tests/; here: sanity
+    # results of the last step of each chain: valid (status clear) and
+    # identical to a fresh un-captured run of the same batch
+    for c in chains:
+        if c.fp.csr.overflowed():
+            raise RuntimeError("exclusion capacity exhausted in a timed replay")
+    last = args.steps - 1
+    fp.set_points(ring_d[last % R])
+    chains[0].body()
+    torch.cuda.synchronize()
+    cl = chains[last % S]
+    replay_ok = bool(torch.equal(cl.fp.out, fp.out)) if cl is not chains[0] else True
+    fp.set_points(ring_d[0])
+    chains[0].body()
+    torch.cuda.synchronize()
     reached = fp.reached.cpu().numpy()
 
-    # ---- exact-FPS + naive ball query comparator on the same batch -------------
-    for _ in range(2):
-        idx, _, _, _ = engine.fps(fp.xyz4, n_SAMPLES)
-        engine.ball_query_naive(fp.xyz4, idx, RADIUS, K)
-    torch.cuda.synchronize()
+    # ---- exact-FPS + naive ball query comparator, same loop and ring ---------------------
+    class ExactChain:
+        def __init__(self):
+            self.x4 = torch.zeros(B, N, 4, dtype=torch.float32, device=dev)
+            self.stream = torch.cuda.Stream(device=dev)
+            self.graph = None
+
+        def body(self):
+            idx, _, _, _ = engine.fps(self.x4, n_SAMPLES)
+            self.out = engine.ball_query_naive(self.x4, idx, RADIUS, K)
+            self.idx = idx
+
+    ex = [ExactChain() for _ in range(S)]
+    for c in ex:
+        c.x4[..., :3].copy_(ring_d[0])
+        c.stream.wait_stream(stream)
+        with torch.cuda.stream(c.stream):
+            c.body()
+        stream.wait_stream(c.stream)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=c.stream):
+            c.body()
+        c.graph = g
+
+    def feed_exact(c, s):
+        c.x4[..., :3].copy_(ring_d[s % R])
+
+    run_chains(ex, S, feed_exact)
+    exact_ms = max_over_ranks(run_chains(ex, args.steps, feed_exact), dev) / args.steps
+    exact1_ms = max_over_ranks(run_chains(ex[:1], args.steps, feed_exact), dev) / args.steps
+    # kernel split of the exact path (one chain, per-kernel events)
     fps_ms, bqn_ms = [], []
-    for s in range(args.steps):
-        flush.zero_()
+    x4 = ex[0].x4
+    for s in range(min(args.steps, 5)):
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record(stream)
-        idx, _, _, _ = engine.fps(fp.xyz4, n_SAMPLES)
+        idx, _, _, _ = engine.fps(x4, n_SAMPLES)
         e1.record(stream)
-        engine.ball_query_naive(fp.xyz4, idx, RADIUS, K)
+        engine.ball_query_naive(x4, idx, RADIUS, K)
         e2.record(stream)
         torch.cuda.synchronize()
         fps_ms.append(e0.elapsed_time(e1))
         bqn_ms.append(e1.elapsed_time(e2))
-    exact_ms = (sum(fps_ms) + sum(bqn_ms)) / args.steps
-    # the one-exchange-per-sample exact kernel (fps.cu; north_star piece (1)
-    # as first built) on the same batch, for the ratio against it as well
-    os.environ["PS_FPS_NOSPEC"] = "1"
-    try:
-        engine.fps(fp.xyz4, n_SAMPLES)
-        torch.cuda.synchronize()
-        fps1_ms = []
-        for s in range(args.steps):
-            flush.zero_()
-            e0, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
-            e0.record(stream)
-            engine.fps(fp.xyz4, n_SAMPLES)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            fps1_ms.append(e0.elapsed_time(e1))
-    finally:
-        del os.environ["PS_FPS_NOSPEC"]
+    del ex
 
     # ---- end to end through the public API: pinned host in, results out ---------
-    # Every step uploads its clouds from pinned host memory and downloads its
-    # sample indices and groups; copies run on a second stream, double-buffered
-    # so that step s+1's upload and step s's download overlap compute.  Each
-    # step starts with an L2 flush (160 MiB memset, inside the timed region).
-    host_in = torch.from_numpy(clouds).pin_memory()
-    host_idx = [torch.empty(B, n_SAMPLES, dtype=torch.int64).pin_memory() for _ in range(2)]
-    host_grp = [torch.empty(B, n_SAMPLES, K, dtype=torch.int32).pin_memory() for _ in range(2)]
-    h2d = host_in.numel() * 4
-    d2h = host_idx[0].numel() * 8 + host_grp[0].numel() * 4
-    d_in = [torch.empty(B, N, 3, dtype=torch.float32, device=dev) for _ in range(2)]
-    res_idx = [torch.empty(B, n_SAMPLES, dtype=torch.int64, device=dev) for _ in range(2)]
-    grps = [grp, (torch.empty_like(grp[0]), torch.empty_like(grp[1]), torch.empty_like(grp[2]))]
-    flush_e2e = torch.empty(160 << 20, dtype=torch.uint8, device=dev)
-    cstream = torch.cuda.Stream(device=dev)
+    # every step uploads its batch from pinned host memory (the ring), runs
+    # set_points + sample + group_rf, and downloads indices, groups and the
+    # exclusion status; chains run concurrently on their streams, so one
+    # chain's copies overlap the others' kernels
+    host_ring = torch.from_numpy(ring_h).pin_memory()
+    d_stage = [torch.empty(B, N, 3, dtype=torch.float32, device=dev) for _ in range(S)]
+    host_idx = [torch.empty(B, n_SAMPLES, dtype=torch.int64).pin_memory() for _ in range(S)]
+    host_grp = [torch.empty(B, n_SAMPLES, K, dtype=torch.int32).pin_memory() for _ in range(S)]
+    host_st = [torch.empty(B, dtype=torch.int32).pin_memory() for _ in range(S)]
+    h2d = B * N * 3 * 4
+    d2h = host_idx[0].numel() * 8 + host_grp[0].numel() * 4 + B * 4
+    ci = {id(c): i for i, c in enumerate(chains)}
 
-    def step_into(g):
-        fp.state.copy_(seed_t)
-        fp.sample()
-        fp.group_rf(RADIUS, K, out=g)
+    def feed_host(c, s):
+        i = ci[id(c)]
+        d_stage[i].copy_(host_ring[s % R], non_blocking=True)
+        c.fp.set_points(d_stage[i])
 
-    # each buffer's step (points in, sampling, grouping, result copy) as one
-    # CUDA graph of the public API calls; copies and waits stay on the streams
-    graphs = []
-    for k in range(2):
-        d_in[k].copy_(host_in)
-        gs = torch.cuda.Stream(device=dev)
-        gs.wait_stream(stream)
-        with torch.cuda.stream(gs):
-            fp.set_points(d_in[k])
-            step_into(grps[k])
-            res_idx[k].copy_(fp.out)
-        stream.wait_stream(gs)
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            fp.set_points(d_in[k])
-            step_into(grps[k])
-            res_idx[k].copy_(fp.out)
-        graphs.append(g)
-    torch.cuda.synchronize()
-    ev = lambda: torch.cuda.Event()  # noqa: E731
-    ev_in, ev_used, ev_out, ev_d2h = [ev(), ev()], [ev(), ev()], [ev(), ev()], [ev(), ev()]
+    def out_host(c, s):
+        i = ci[id(c)]
+        host_idx[i].copy_(c.fp.out, non_blocking=True)
+        host_grp[i].copy_(c.grp[0], non_blocking=True)
+        host_st[i].copy_(c.fp.csr.status, non_blocking=True)
+
+    run_chains(chains, S, feed_host, out_host)
     if ws > 1:
         dist.barrier()
-    torch.cuda.synchronize()
-    a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(stream)
-    cstream.wait_stream(stream)
-    with torch.cuda.stream(cstream):
-        d_in[0].copy_(host_in, non_blocking=True)
-        ev_in[0].record(cstream)
-    for s in range(args.steps):
-        k = s % 2
-        if s + 1 < args.steps:  # prefetch the next step's clouds
-            with torch.cuda.stream(cstream):
-                if s >= 1:
-                    cstream.wait_event(ev_used[(s + 1) % 2])
-                d_in[(s + 1) % 2].copy_(host_in, non_blocking=True)
-                ev_in[(s + 1) % 2].record(cstream)
-        flush_e2e.zero_()
-        stream.wait_event(ev_in[k])
-        if s >= 2:
-            stream.wait_event(ev_d2h[k])  # result buffers k are free again
-        graphs[k].replay()  # set_points(d_in[k]) + sample + group_rf + result copy
-        ev_used[k].record(stream)
-        ev_out[k].record(stream)
-        with torch.cuda.stream(cstream):
-            cstream.wait_event(ev_out[k])
-            host_idx[k].copy_(res_idx[k], non_blocking=True)
-            host_grp[k].copy_(grps[k][0], non_blocking=True)
-            ev_d2h[k].record(cstream)
-    stream.wait_stream(cstream)
-    b_.record(stream)
-    b_.synchronize()
-    e2e_ms = max_over_ranks(a.elapsed_time(b_), dev)
+    e2e_ms = max_over_ranks(run_chains(chains, args.steps, feed_host, out_host), dev)
     e2e_value = ws * B * n_SAMPLES * args.steps / (e2e_ms / 1e3)
-    e2e_ok = bool(np.array_equal(host_idx[(args.steps - 1) % 2].numpy(), fp.out.cpu().numpy()))
+    if any(int(h.max()) != 0 for h in host_st):
+        raise RuntimeError("exclusion capacity exhausted during the e2e run (status set)")
+    # the last step's downloaded indices equal a fresh run on its batch
+    fp.set_points(ring_d[last % R])
+    chains[0].body()
+    torch.cuda.synchronize()
+    e2e_ok = bool(np.array_equal(host_idx[last % S].numpy(), fp.out.cpu().numpy()))
+    fp.set_points(ring_d[0])
+    chains[0].body()
+    torch.cuda.synchronize()
+
+    # ---- quality and early termination on the rank-0 batch --------
+    exact_idx, _, _, _ = engine.fps(fp.xyz4, n_SAMPLES)
+    sp_f = engine.min_spacing_d2(fp.xyz4, fp.out).sqrt().mean(dim=1)
+    sp_x = engine.min_spacing_d2(fp.xyz4, exact_idx).sqrt().mean(dim=1)
+    quality = (sp_f / sp_x).cpu().numpy()
+    et_frac = (n_SAMPLES - reached) / n_SAMPLES
 
     # ---- roofline for the dominant kernel ------------------------------------------
     pk = peaks()
     hbm = pk.get("hbm_gbs", 6650.0)
     dom = max(per_stage, key=per_stage.get)
     k0 = fp.k0
-    E = int(fp.csr.indptr[:, -1].sum().item())
-    alg = {  # algorithmic bytes per launch (DESIGN.md section 4)
+    E = int(fp.csr.counts.amax(dim=1).sum().item())  # entries of the widest level, all clouds
+    alg = {  # algorithmic bytes per launch (DESIGN.md section 5)
         "fps_prefix": 28.0 * N * (k0 - 1) * B,
-        "excl_build": 36.0 * E + 4.0 * N * fp.L * B + 12.0 * N * B,
+        "excl_build": 12.0 * E + 4.0 * N * fp.L * B + 16.0 * N * B,
         "sampler": 4.0 * E + 4.0 * N * fp.L * B,
         "early_term": 28.0 * N * float(np.sum(n_SAMPLES - reached)) + 12.0 * E,
         "rf_ball_query": 24.0 * n_SAMPLES * K * B,
@@ -423,10 +555,13 @@ def main_ours(args):
     }
     achieved = alg[dom] / (per_stage[dom] / 1e3) / 1e9
     traffic = None
-    try:  # measured DRAM bytes per launch from the committed ncu --set full capture
-        traffic = json.load(open(os.path.join(REPO, "profiles", "r01", "traffic.json"))).get(dom)
-    except (OSError, ValueError):
-        pass
+    for rnd in ("r02", "r01"):
+        try:  # measured DRAM bytes per launch from the committed ncu --set full capture
+            traffic = json.load(open(os.path.join(REPO, "profiles", rnd, "traffic.json"))).get(dom)
+            if traffic is not None:
+                break
+        except (OSError, ValueError):
+            pass
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": traffic, "algorithmic_bytes": alg[dom],
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if "hbm_gbs" in pk else "fallback 6.65 TB/s",
@@ -436,10 +571,11 @@ def main_ours(args):
                          "it with such a streaming kernel at HBM speed -- it is bound by its exchange/pick "
                          "latency chain, not by DRAM")}
 
-    # ---- C5 point split: one 2^20-point cloud -> 65536 samples ---------
-    c5 = c2 = c4 = None
+    # ---- other configs ------------------------------------------------------------------
+    c5 = c5f = c2 = c4 = None
     if not args.no_c5 and ws == 1:
         c5 = bench_c5_virtual(dev)
+        c5f = bench_c5_fastpoint(dev)
     elif args.c5_split and ws > 1:
         c5 = bench_c5_split(dev, ws)
     if not args.no_extra and ws == 1:
@@ -448,49 +584,49 @@ def main_ours(args):
 
     cpu = None
     if rank == 0 and not args.no_cpu:
-        threads = min(os.cpu_count() or 1, B)
-        dt, cpu_idx = cpu_run(clouds, exponent, threads)
-        match = all(np.array_equal(cpu_idx[b], fp.out[b].cpu().numpy()) for b in range(B)) if \
-            int(seed_t[0].item()) == 0 else None
-        cpu = {"value": B * n_SAMPLES / dt, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"{B} clouds (the rank-0 batch) FastPoint + rf ball query, one cloud per thread",
-               "seconds": dt, "indices_bit_exact_vs_gpu": match}
+        cpu = cpu_baseline(clouds, exponent, fp.out.cpu().numpy(), args.cpu_runs)
 
     if rank == 0:
+        ms_step = t_ms / args.steps
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": max(args.warmup, 3), "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "family": FAMILY, "B_per_gpu": B, "global_batch": B * ws, "N": N,
-                       "n": n_SAMPLES, "p": P, "nseg": NSEG, "radius": RADIUS, "k": K,
+            "config": {"workload": WORKLOAD, "family": FAMILY, "B_per_gpu": B, "B": B, "global_batch": B * ws,
+                       "N": N, "n": n_SAMPLES, "p": P, "nseg": NSEG, "radius": RADIUS, "k": K,
                        "exponent": round(exponent, 6), "parallelism": f"batch-shard x{ws}",
-                       "l2": "flushed between timed steps (512 MiB memset, untimed)"},
-            "us_per_cloud": 1e3 * t_ms / (args.steps * B),
+                       "streams": S,
+                       "l2": (f"inputs larger than L2: a ring of {R} distinct batches "
+                              f"({R * B * N * 12 / 2**20:.0f} MiB of float32 coordinates) cycled step by step; "
+                              "stage breakdown: 512 MiB flush between steps")},
+            "timing": (f"device events around the whole loop of K steps (steps back to back on {S} streams, "
+                       "step s on stream s % S, each step = set_points + one CUDA graph of sample + rf grouping)"),
+            "us_per_cloud": 1e3 * ms_step / B,
+            "one_stream": {"ms_per_step": t1_ms / args.steps, "value": ws * B * n_SAMPLES / (t1_ms / args.steps / 1e3)},
             "stage_ms": per_stage,
-            "exact_fps_path": {"ms_per_step": exact_ms, "fps_ms": float(np.mean(fps_ms)),
-                               "ball_query_naive_ms": float(np.mean(bqn_ms)),
-                               "value": ws * B * n_SAMPLES / (exact_ms / 1e3),
-                               "us_per_cloud": 1e3 * exact_ms / B},
-            "speedup_vs_exact_fps": exact_ms / (t_ms / args.steps),
-            "speedup_vs_exact_fps_kernel_only": float(np.mean(fps_ms)) / (t_ms / args.steps),
-            "exact_fps_one_sample_kernel": {
-                "fps_ms": float(np.mean(fps1_ms)),
-                "speedup_vs_it": float(np.mean(fps1_ms)) / (t_ms / args.steps),
-                "speedup_vs_it_plus_naive_bq": (float(np.mean(fps1_ms)) + float(np.mean(bqn_ms))) / (t_ms / args.steps),
-                "note": "fps.cu, one cluster exchange per sample; exact_fps_path uses the speculative "
-                        "exact kernel (fps_spec.cu), bit-identical output"},
-            "early_term_iters_mean": float(np.mean(n_SAMPLES - reached)),
+            "stage_sum_ms": float(sum(per_stage.values())),
+            "exact_fps_path": {"ms_per_step": exact_ms, "ms_per_step_one_stream": exact1_ms,
+                               "fps_ms": float(np.mean(fps_ms)), "ball_query_naive_ms": float(np.mean(bqn_ms)),
+                               "value": ws * B * n_SAMPLES / (exact_ms / 1e3), "us_per_cloud": 1e3 * exact_ms / B,
+                               "kernels": "fps_spec (speculative exact FPS) + bq_naive, same loop, ring and streams"},
+            "speedup_vs_exact_fps": exact_ms / ms_step,
+            "speedup_vs_exact_fps_one_stream": exact1_ms / (t1_ms / args.steps),
+            "speedup_vs_exact_fps_kernel_only": float(np.mean(fps_ms)) / (t1_ms / args.steps),
+            "quality_ratio": {"mean": float(np.mean(quality)), "min": float(np.min(quality)),
+                              "def": "avg_min_spacing(FastPoint) / avg_min_spacing(exact FPS), SPEC.md:573-581"},
+            "early_term_frac": {"mean": float(np.mean(et_frac)), "max": float(np.max(et_frac)),
+                                "def": "(n - reached) / n, SPEC.md:703"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ms_per_step": e2e_ms / args.steps, "results_match_device": e2e_ok,
-                    "note": "pinned H2D + D2H every step on a copy stream, double-buffered across steps; each "
-                            "buffer's step (set_points + sample + group_rf + result copy) replayed as one CUDA "
-                            "graph; "
-                            "160 MiB L2 flush per step inside the timed region"},
+                    "ms_per_step": e2e_ms / args.steps, "results_match_device": e2e_ok and replay_ok,
+                    "note": (f"pinned H2D of the step's batch (ring of {R}) + set_points + sample + group_rf + D2H of "
+                             f"indices, groups and exclusion status, every step, {S} chains on their own streams "
+                             "(copies of one overlap the kernels of the others)")},
             "gpu_launches": int(launches),
             "roofline": roofline,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "c5_point_split": c5,
+            "c5_fastpoint": c5f,
             "c2_cascade": c2,
             "c4_large_clouds": c4,
         }
@@ -630,6 +766,79 @@ def bench_c5_virtual(dev, G=None):
             "parity": "bit-identical to the single-rank kernel (tests/test_gpu_parity.py, tools/c5_split.py)"}
 
 
+C5_EXPONENT, C5_RADIUS = 0.368508, 0.04  # tests/golden/make_c5_digest.py (fitted on a held-out cloud)
+
+
+def bench_c5_fastpoint(dev, reps=3):
+    """C5 FastPoint on one GPU: one N = 2^20 uniform-box cloud -> n = 65536,
+    p = 0.1, nseg = 6, power estimator, rf ball query r = 0.04 k = 32 -- the
+    prefix and the early-termination tail run as the point split over
+    virtual ranks inside ps_fps.  One CUDA graph per sample + grouping,
+    inputs resident, device events; against exact FPS + naive ball query on
+    the same cloud.  Indices are compared with the oracle digest."""
+    import hashlib
+
+    import torch
+
+    from paper_2507_23480_b200 import engine
+    from paper_2507_23480_b200.harness import generate_cloud
+
+    cloud = generate_cloud("uniform-box", C5_N, 5000)
+    fp = engine.FastPoint(1, C5_N, C5_n, p=P, nseg=NSEG, exponent=C5_EXPONENT, extra_radii=(C5_RADIUS,), device=dev)
+    fp.set_points(torch.from_numpy(cloud[None]).to(dev))
+    grp = (torch.empty(1, C5_n, K, dtype=torch.int32, device=dev),
+           torch.empty(1, C5_n, K, dtype=torch.float64, device=dev),
+           torch.empty(1, C5_n, dtype=torch.int32, device=dev))
+    seed = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    def body():
+        fp.state.copy_(seed)
+        fp.sample()
+        fp.group_rf(C5_RADIUS, K, out=grp)
+
+    body()
+    torch.cuda.synchronize()
+    fp.check()
+    s = torch.cuda.Stream(device=dev)
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        body()
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        body()
+    g.replay()
+    ms = _time_graph(g.replay, reps)
+    try:
+        dig = json.load(open(os.path.join(REPO, "tests", "golden", "c5_digest.json")))["fastpoint"]["idx_sha256"]
+    except (OSError, ValueError, KeyError):
+        dig = None
+    got = hashlib.sha256(fp.out[0].cpu().numpy().astype(np.int64).tobytes()).hexdigest()
+    reached = int(fp.reached[0].item())
+
+    def exact():
+        idx, _, _, _ = engine.fps(fp.xyz4, C5_n)
+        engine.ball_query_naive(fp.xyz4, idx, C5_RADIUS, K)
+
+    exact()
+    e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    e0.record()
+    idx, _, _, _ = engine.fps(fp.xyz4, C5_n)
+    e1.record()
+    engine.ball_query_naive(fp.xyz4, idx, C5_RADIUS, K)
+    e2.record()
+    torch.cuda.synchronize()
+    fps_ms, bq_ms = e0.elapsed_time(e1), e1.elapsed_time(e2)
+    return {"workload": "C5 FastPoint: 1 cloud N=2^20 uniform-box -> n=65536, p=0.1, nseg=6, power estimator "
+                        f"(e={C5_EXPONENT}), rf ball query r={C5_RADIUS} k={K}; one GPU",
+            "ms": ms, "sampled_pts_per_s": C5_n / (ms / 1e3), "reached": reached,
+            "early_term_frac": (C5_n - reached) / C5_n, "entries": int(fp.csr.counts[0].amax(dim=0).sum().item()),
+            "exact_fps_ms": fps_ms, "ball_query_naive_ms": bq_ms,
+            "speedup_vs_exact_fps": (fps_ms + bq_ms) / ms, "speedup_vs_exact_fps_kernel_only": fps_ms / ms,
+            "indices_match_oracle_digest": (got == dig) if dig else None,
+            "timing": f"CUDA graph replay (sample + rf grouping), mean of {reps}; exact path eager, one run"}
+
+
 def bench_c5_split(dev, ws):
     """C5 over the job's GPUs, one process per GPU (pointsplit.PointSplitFPS:
     cudaMalloc mailboxes mapped into every peer through CUDA IPC, NVLink
@@ -670,6 +879,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 point-split line")
     ap.add_argument("--no-extra", action="store_true", help="skip the C2 / C4 objects")
+    ap.add_argument("--streams", type=int, default=2, help="concurrent FastPoint chains (streams)")
+    ap.add_argument("--cpu-runs", type=int, default=5, help="timed CPU-baseline runs per thread setting (median)")
     ap.add_argument("--c5-split", action="store_true",
                     help="N > 1: also run C5 point-split over the job's GPUs (CUDA IPC + NVLink)")
     args = ap.parse_args()

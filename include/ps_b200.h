@@ -134,7 +134,16 @@ PS_API int ps_first_untaken(const uint8_t* taken, int64_t N, int64_t* out, void*
  * larger capacities.  method 0 enumerates the i<j triangle (each pair
  * evaluated once, the reference's accounting SPEC.md:438); method 1 enumerates
  * candidates from a uniform grid of cell width >= R_max (cap_edges unused) --
- * the CSR is byte-identical, only the number of evaluations differs. */
+ * the CSR is byte-identical, only the number of evaluations differs.
+ * method 2 (the FastPoint hot path) uses the same grid candidates but writes
+ * fixed-stride rows: row i starts at indptr[i] = i * ps_excl_row_stride(N,
+ * cap_entries), entries bucketed by level (each level's entries are the row
+ * prefix of length counts[l][i]); a row longer than the stride takes a run
+ * of the spill arena behind the N strided rows (indptr[i] then points
+ * there), so only an exhausted arena sets status bit 1.  Consumers that take
+ * a status pointer (sampler, rf queries) turn a failed cloud into explicit
+ * error outputs instead of reading its incomplete rows. */
+PS_API int64_t ps_excl_row_stride(int64_t N, int64_t cap_entries);
 PS_API int64_t ps_excl_workspace_bytes(int64_t B, int64_t N, int64_t cap_edges, int32_t method);
 /* Byte offset, inside a method-1 workspace, of the uint64[B] count of
  * candidate pairs the grid build evaluated (pair_evals accounting). */
@@ -143,6 +152,16 @@ PS_API int ps_excl_build(const float* xyz4, int64_t B, int64_t N, const double* 
                   int64_t levels_ld, int64_t* indptr, int32_t* nbr, double* d2, int32_t* counts,
                   int64_t cap_entries, void* work, int64_t cap_edges, int32_t* status,
                   int32_t method, void* stream);
+
+/* csr_fill (_kernels.py:164-185): scatter the M undirected edges (ei, ej
+ * int32, ed float64; excl_collect's emission order) into both rows of a CSR
+ * whose indptr (int64[N+1]) counts self + degree per row: row r = r (d2 0),
+ * then the other endpoint of every edge touching r in edge order.  out_idx
+ * int64[E], out_d2 float64[E].  work: ps_csr_fill_workspace_bytes(M, N)
+ * device bytes (stable radix sort of the half-edges by row). */
+PS_API int64_t ps_csr_fill_workspace_bytes(int64_t M, int64_t N);
+PS_API int ps_csr_fill(const int32_t* ei, const int32_t* ej, const double* ed, int64_t M, const int64_t* indptr,
+                       int64_t N, int64_t* out_idx, double* out_d2, void* work, int64_t work_bytes, void* stream);
 
 /* csr_sort_rows (_kernels.py:188-219): order every row by (d2, index) in
  * place.  work: >= 256 + 4*B*N bytes. */
@@ -185,15 +204,19 @@ PS_API int ps_thresholds_mlp(const double* prefix_curve, int64_t curve_ld, int64
  * count reached).  seg_level_rows_host / boundaries_host are host arrays of
  * nseg entries; boundaries are segment ends and the last must equal n_total
  * (SURVEY 0.4).  state_io (uint64[B], device) is the splitmix64 state in/out.
- * work: ps_sampler_workspace_bytes(B, N, nseg) bytes (may be 0 when the
- * per-cloud tables fit in shared memory; pass NULL then). */
+ * work: ps_sampler_workspace_bytes(B, N, nseg) bytes.  excl_status (int32[B]
+ * from ps_excl_build, nullable): a cloud whose build failed gets
+ * out_idx[b][k0..n_total) = -1, reached[b] = n_total (nothing left for early
+ * termination) and entered[b] = -1 -- an explicit error state that stays
+ * visible through CUDA-graph replays. */
 PS_API int64_t ps_sampler_workspace_bytes(int64_t B, int64_t N, int32_t nseg);
 PS_API int ps_sample_predicted(const int64_t* indptr, const int32_t* nbr, int64_t cap_entries,
                         const int32_t* counts, int32_t L, const int32_t* seg_level_rows_host,
                         const int64_t* boundaries_host, int32_t nseg, int64_t* out_idx,
                         int64_t ld_out, int64_t k0, int64_t n_total, int64_t B, int64_t N,
                         uint64_t* state_io, int32_t pick_lowest, int64_t* reached,
-                        int32_t* exhausted, int32_t* entered, void* work, void* stream);
+                        int32_t* exhausted, int32_t* entered, void* work, const int32_t* excl_status,
+                        void* stream);
 
 /* ---- K3d: early termination ----------------------------------------------
  * earlyterm_scan (_kernels.py:356-367) over points [lo, hi) of every cloud:
@@ -217,12 +240,14 @@ PS_API int ps_early_termination_prepare(const int64_t* indptr, const int32_t* nb
  * Outputs idx int32[B][n][k] (-1 padded), dist float64[B][n][k] (sqrt(d2),
  * NaN padded), cnt int32[B][n].  Order (d2, index), strict d2 < r^2. */
 /* rf_ball_query: level = the level row the radius was baked
- * into; zero distance evaluations. */
+ * into; zero distance evaluations; k <= 128 (PS_ERR_INVALID otherwise).
+ * A centroid outside [0, N), or any centroid of a cloud whose excl_status
+ * (nullable) is nonzero, gets cnt = -1 and an empty (-1 / NaN) group. */
 PS_API int ps_ball_query_rf(const int64_t* indptr, const int32_t* nbr, const double* d2,
                      int64_t cap_entries, const int32_t* counts, int32_t L, int32_t level,
                      const int64_t* centroids, int64_t cent_ld, int64_t B, int64_t N, int64_t n,
                      int32_t k, int32_t* idx_out, double* dist_out, int32_t* cnt_out,
-                     void* stream);
+                     const int32_t* excl_status, void* stream);
 /* ball_query_naive; k <= 128. */
 PS_API int ps_ball_query_naive(const float* xyz4, const int64_t* centroids, int64_t cent_ld, int64_t B,
                         int64_t N, int64_t n, double r2, int32_t k, int32_t* idx_out,
@@ -233,13 +258,14 @@ PS_API int ps_knn_naive(const float* xyz4, const int64_t* queries, int64_t q_ld,
                  const int64_t* pool, int64_t pool_ld, int64_t npool, int64_t B, int64_t N,
                  int32_t k, int32_t* idx_out, double* dist_out, int32_t* cnt_out, void* stream);
 /* rf_knn: level-1 rows filtered by sampled (u8[B][N]);
- * brute-force fallback over pool; fallback_count int32[B] is incremented. */
+ * brute-force fallback over pool; fallback_count int32[B] is incremented.
+ * A cloud whose excl_status (nullable) is nonzero gets cnt = -1 everywhere. */
 PS_API int ps_knn_rf(const float* xyz4, const int64_t* indptr, const int32_t* nbr, const double* d2,
               int64_t cap_entries, const int32_t* lvl1_counts, int64_t counts_stride,
               const uint8_t* sampled, const int64_t* queries, int64_t q_ld, int64_t nq,
               const int64_t* pool, int64_t pool_ld, int64_t npool, int64_t B, int64_t N,
               int32_t k, int32_t* idx_out, double* dist_out, int32_t* cnt_out,
-              int32_t* fallback_count, void* stream);
+              int32_t* fallback_count, const int32_t* excl_status, void* stream);
 
 /* ---- K6: quality -----------------------------------------------------------
  * avg_min_spacing helper: out_d2[b][s] = squared distance

@@ -67,6 +67,10 @@ def _load():
     lib.ora_fps_update_chunk.restype = None
     lib.ora_fps_update_chunk.argtypes = [_f64p, _f64p, _f64p, _f64, _f64, _f64, _f64p, _i64, _i64,
                                          ctypes.POINTER(_f64), ctypes.POINTER(_i64)]
+    lib.ora_fps_loop_mt.restype = _i64
+    lib.ora_fps_loop_mt.argtypes = [_f64p, _f64p, _f64p, _i64, _f64p, _u8p, _i64p, _f64p, _i64, _i64, ctypes.c_int32]
+    lib.ora_excl_build_mt.restype = ctypes.c_void_p
+    lib.ora_excl_build_mt.argtypes = [_f64p, _f64p, _f64p, _i64, _f64, ctypes.c_int32]
     lib.ora_first_untaken.restype = _i64
     lib.ora_first_untaken.argtypes = [_u8p, _i64]
     lib.ora_excl_build.restype = ctypes.c_void_p
@@ -99,6 +103,17 @@ def _load():
 
 _LIB = None
 
+# worker threads of the reference's multi-worker form (core.workers,
+# core.py:71-101): FPS slices merged by the chunk rule and the
+# excl_collect task split.  1 = the serial kernels.  Results are identical.
+THREADS = max(1, int(os.environ.get("PS_ORACLE_THREADS", "1")))
+
+
+def set_threads(t: int) -> int:
+    global THREADS
+    old, THREADS = THREADS, max(1, int(t))
+    return old
+
 
 def lib():
     global _LIB
@@ -127,6 +142,9 @@ class CKernels:
     @staticmethod
     def fps_loop(x, y, z, md, taken, out_idx, curve, k_start, n_total):
         # _kernels.py:35-74
+        if THREADS > 1:
+            return int(lib().ora_fps_loop_mt(x, y, z, x.shape[0], md, taken, out_idx, curve,
+                                             int(k_start), int(n_total), THREADS))
         return int(lib().ora_fps_loop(x, y, z, x.shape[0], md, taken, out_idx, curve,
                                       int(k_start), int(n_total)))
 
@@ -149,7 +167,7 @@ class CKernels:
         """excl_collect over all tasks + csr_fill + csr_sort_rows
         (_kernels.py:111-219).  Returns (indptr, nbr, d2, evals)."""
         L = lib()
-        h = L.ora_excl_build(x, y, z, x.shape[0], float(r2max))
+        h = L.ora_excl_build_mt(x, y, z, x.shape[0], float(r2max), THREADS)
         try:
             N = L.ora_csr_N(h)
             E = L.ora_csr_E(h)

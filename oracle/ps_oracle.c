@@ -18,8 +18,15 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <pthread.h>
 
 #define ORA_API __attribute__((visibility("default")))
+
+ORA_API int64_t ora_first_untaken(const uint8_t* taken, int64_t N);
+ORA_API int64_t ora_fps_loop(const double* x, const double* y, const double* z,
+                             int64_t N, double* md, uint8_t* taken,
+                             int64_t* out_idx, double* curve,
+                             int64_t k_start, int64_t n_total);
 
 static inline double sqdist(double ax, double ay, double az,
                             double bx, double by, double bz) {
@@ -80,6 +87,93 @@ ORA_API int64_t ora_fps_loop(const double* x, const double* y, const double* z,
     return evals;
 }
 
+/* Threaded exact FPS: the reference's multi-worker form (
+ * core.workers, core.py:71-101) -- every iteration runs fps_update_chunk
+ * (_kernels.py:77-92) on nthreads contiguous slices and merges the slice
+ * results by (max md, lowest index: strict > in slice order), then the
+ * duplicate fallback through first_untaken (_kernels.py:95-100).  Identical
+ * output to ora_fps_loop for any slice count. */
+typedef struct {
+    const double *x, *y, *z;
+    double* md;
+    const int64_t* out_idx;
+    int64_t N, chunk, k_start, n_total;
+    int T;
+    double* bests;
+    int64_t* args;
+    pthread_barrier_t* bar;  /* two waits per iteration: slices done / merge done */
+} fps_mt_ctx;
+
+typedef struct { fps_mt_ctx* c; int t; } fps_mt_arg;
+
+static void fps_slice(fps_mt_ctx* c, int t, int64_t it) {
+    const int64_t s = c->out_idx[it - 1];
+    const double px = c->x[s], py = c->y[s], pz = c->z[s];
+    const int64_t lo = t * c->chunk < c->N ? t * c->chunk : c->N;
+    const int64_t hi = lo + c->chunk < c->N ? lo + c->chunk : c->N;
+    double best = -1.0;
+    int64_t arg = -1;
+    for (int64_t j = lo; j < hi; ++j) {
+        const double d = sqdist(px, py, pz, c->x[j], c->y[j], c->z[j]);
+        if (d < c->md[j]) c->md[j] = d;
+        if (c->md[j] > best) { best = c->md[j]; arg = j; }
+    }
+    c->bests[t] = best;
+    c->args[t] = arg;
+}
+
+static void* fps_mt_worker(void* p) {
+    fps_mt_arg* a = (fps_mt_arg*)p;
+    for (int64_t it = a->c->k_start; it < a->c->n_total; ++it) {
+        fps_slice(a->c, a->t, it);
+        pthread_barrier_wait(a->c->bar);  /* slices done */
+        pthread_barrier_wait(a->c->bar);  /* thread 0 merged and wrote out_idx[it] */
+    }
+    return NULL;
+}
+
+ORA_API int64_t ora_fps_loop_mt(const double* x, const double* y, const double* z,
+                                int64_t N, double* md, uint8_t* taken,
+                                int64_t* out_idx, double* curve,
+                                int64_t k_start, int64_t n_total, int32_t nthreads) {
+    const int T = nthreads > 64 ? 64 : nthreads;
+    if (T < 2 || N < 4096 || k_start >= n_total)
+        return ora_fps_loop(x, y, z, N, md, taken, out_idx, curve, k_start, n_total);
+    double bests[64];
+    int64_t args[64];
+    pthread_barrier_t bar;
+    pthread_barrier_init(&bar, NULL, (unsigned)T);
+    fps_mt_ctx c = {x, y, z, md, out_idx, N, (N + T - 1) / T, k_start, n_total, T, bests, args, &bar};
+    pthread_t th[64];
+    fps_mt_arg wa[64];
+    for (int t = 1; t < T; ++t) {
+        wa[t].c = &c;
+        wa[t].t = t;
+        pthread_create(&th[t], NULL, fps_mt_worker, &wa[t]);
+    }
+    int64_t evals = 0;
+    for (int64_t it = k_start; it < n_total; ++it) {
+        fps_slice(&c, 0, it);
+        pthread_barrier_wait(&bar);
+        double best = -1.0;
+        int64_t arg = -1;
+        for (int t = 0; t < T; ++t)  /* strict > in slice order: lowest index on ties */
+            if (bests[t] > best) { best = bests[t]; arg = args[t]; }
+        evals += N;
+        if (best <= 0.0 || taken[arg]) {  /* _kernels.py:65-70 */
+            const int64_t f = ora_first_untaken(taken, N);
+            if (f >= 0) { arg = f; best = md[f]; }
+        }
+        out_idx[it] = arg;
+        curve[it] = sqrt(best);
+        taken[arg] = 1;
+        pthread_barrier_wait(&bar);
+    }
+    for (int t = 1; t < T; ++t) pthread_join(th[t], NULL);
+    pthread_barrier_destroy(&bar);
+    return evals;
+}
+
 /* Slice update + argmax, _kernels.py:77-92. best/arg returned via pointers. */
 ORA_API void ora_fps_update_chunk(const double* x, const double* y, const double* z,
                                   double px, double py, double pz, double* md,
@@ -128,30 +222,115 @@ static int entry_cmp(const void* a, const void* b) {
     return (p->j > q->j) - (p->j < q->j);
 }
 
+typedef struct { int64_t cap, cnt; int32_t* ei; int32_t* ej; double* ed; } edge_buf;
+
+static void collect_rows(const double* x, const double* y, const double* z, int64_t N, double r2max,
+                         int64_t i, edge_buf* b) {
+    const double xi = x[i], yi = y[i], zi = z[i];
+    for (int64_t j = i + 1; j < N; ++j) {
+        /* _kernels.py:149-152: dx = x[jj] - xi */
+        const double d = sqdist(xi, yi, zi, x[j], y[j], z[j]);
+        if (d < r2max) {
+            if (b->cnt == b->cap) {
+                b->cap = b->cap ? 2 * b->cap : 1024;
+                b->ei = (int32_t*)realloc(b->ei, sizeof(int32_t) * b->cap);
+                b->ej = (int32_t*)realloc(b->ej, sizeof(int32_t) * b->cap);
+                b->ed = (double*)realloc(b->ed, sizeof(double) * b->cap);
+            }
+            b->ei[b->cnt] = (int32_t)i; b->ej[b->cnt] = (int32_t)j; b->ed[b->cnt] = d; ++b->cnt;
+        }
+    }
+}
+
+typedef struct { ora_csr* c; int64_t maxrow; int T, t; } sort_arg;
+
+static void* sort_worker(void* p) {
+    sort_arg* a = (sort_arg*)p;
+    ora_entry* tmp = (ora_entry*)malloc(sizeof(ora_entry) * (size_t)(a->maxrow ? a->maxrow : 1));
+    for (int64_t i = a->t; i < a->c->N; i += a->T) {
+        const int64_t lo = a->c->indptr[i], m = a->c->indptr[i + 1] - lo;
+        if (m < 2) continue;
+        for (int64_t q = 0; q < m; ++q) { tmp[q].d = a->c->d2[lo + q]; tmp[q].j = a->c->nbr[lo + q]; }
+        qsort(tmp, (size_t)m, sizeof(ora_entry), entry_cmp);
+        for (int64_t q = 0; q < m; ++q) { a->c->d2[lo + q] = tmp[q].d; a->c->nbr[lo + q] = tmp[q].j; }
+    }
+    free(tmp);
+    return NULL;
+}
+
+static void sort_rows_mt(ora_csr* c, int64_t maxrow, int T) {
+    sort_arg sa[64];
+    pthread_t th[64];
+    for (int t = 0; t < T; ++t) {
+        sort_arg v = {c, maxrow, T, t};
+        sa[t] = v;
+        if (t > 0) pthread_create(&th[t], NULL, sort_worker, &sa[t]);
+    }
+    sort_worker(&sa[0]);
+    for (int t = 1; t < T; ++t) pthread_join(th[t], NULL);
+}
+
+/* nthreads > 1: the reference's worker split of excl_collect (balanced
+ * row-pair tasks k, N-1-k, _kernels.py:103-108, over core.workers) with one
+ * edge buffer per worker; the CSR is identical because every row is then
+ * ordered by (d2, index), which does not depend on the emission order. */
+ORA_API ora_csr* ora_excl_build_mt(const double* x, const double* y, const double* z,
+                                   int64_t N, double r2max, int32_t nthreads);
+
 ORA_API ora_csr* ora_excl_build(const double* x, const double* y, const double* z,
                                 int64_t N, double r2max) {
-    int64_t cap = 1024, cnt = 0;
-    int32_t* ei = (int32_t*)malloc(sizeof(int32_t) * cap);
-    int32_t* ej = (int32_t*)malloc(sizeof(int32_t) * cap);
-    double* ed = (double*)malloc(sizeof(double) * cap);
-    int64_t evals = 0;
-    for (int64_t i = 0; i < N; ++i) {
-        const double xi = x[i], yi = y[i], zi = z[i];
-        for (int64_t j = i + 1; j < N; ++j) {
-            /* _kernels.py:149-152: dx = x[jj] - xi */
-            const double d = sqdist(xi, yi, zi, x[j], y[j], z[j]);
-            if (d < r2max) {
-                if (cnt == cap) {
-                    cap *= 2;
-                    ei = (int32_t*)realloc(ei, sizeof(int32_t) * cap);
-                    ej = (int32_t*)realloc(ej, sizeof(int32_t) * cap);
-                    ed = (double*)realloc(ed, sizeof(double) * cap);
-                }
-                ei[cnt] = (int32_t)i; ej[cnt] = (int32_t)j; ed[cnt] = d; ++cnt;
-            }
-        }
-        evals += N - 1 - i;
+    return ora_excl_build_mt(x, y, z, N, r2max, 1);
+}
+
+typedef struct {
+    const double *x, *y, *z;
+    int64_t N, ntask;
+    double r2max;
+    int T, t;
+    edge_buf* b;
+} collect_arg;
+
+static void* collect_worker(void* p) {
+    collect_arg* a = (collect_arg*)p;
+    /* tasks t, t + T, ...: interleaved so every worker gets long and short rows */
+    for (int64_t k = a->t; k < a->ntask; k += a->T) {
+        collect_rows(a->x, a->y, a->z, a->N, a->r2max, k, a->b);
+        if (a->N - 1 - k != k) collect_rows(a->x, a->y, a->z, a->N, a->r2max, a->N - 1 - k, a->b);
     }
+    return NULL;
+}
+
+ORA_API ora_csr* ora_excl_build_mt(const double* x, const double* y, const double* z,
+                                   int64_t N, double r2max, int32_t nthreads) {
+    const int T = nthreads < 1 ? 1 : (nthreads > 64 ? 64 : nthreads);
+    edge_buf* bufs = (edge_buf*)calloc((size_t)T, sizeof(edge_buf));
+    const int64_t ntask = (N + 1) / 2;
+    collect_arg ca[64];
+    pthread_t th[64];
+    for (int t = 0; t < T; ++t) {
+        collect_arg v = {x, y, z, N, ntask, r2max, T, t, &bufs[t]};
+        ca[t] = v;
+        if (t > 0) pthread_create(&th[t], NULL, collect_worker, &ca[t]);
+    }
+    collect_worker(&ca[0]);
+    for (int t = 1; t < T; ++t) pthread_join(th[t], NULL);
+    int64_t cnt = 0;
+    for (int t = 0; t < T; ++t) cnt += bufs[t].cnt;
+    int32_t* ei = (int32_t*)malloc(sizeof(int32_t) * (size_t)(cnt ? cnt : 1));
+    int32_t* ej = (int32_t*)malloc(sizeof(int32_t) * (size_t)(cnt ? cnt : 1));
+    double* ed = (double*)malloc(sizeof(double) * (size_t)(cnt ? cnt : 1));
+    int64_t off = 0;
+    for (int t = 0; t < T; ++t) {
+        if (bufs[t].cnt) {
+            memcpy(ei + off, bufs[t].ei, sizeof(int32_t) * (size_t)bufs[t].cnt);
+            memcpy(ej + off, bufs[t].ej, sizeof(int32_t) * (size_t)bufs[t].cnt);
+            memcpy(ed + off, bufs[t].ed, sizeof(double) * (size_t)bufs[t].cnt);
+        }
+        off += bufs[t].cnt;
+        free(bufs[t].ei); free(bufs[t].ej); free(bufs[t].ed);
+    }
+    free(bufs);
+    const int64_t evals = N * (N - 1) / 2;
     ora_csr* c = (ora_csr*)calloc(1, sizeof(ora_csr));
     c->N = N;
     c->evals = evals;
@@ -181,15 +360,7 @@ ORA_API ora_csr* ora_excl_build(const double* x, const double* y, const double* 
         int64_t m = c->indptr[i + 1] - c->indptr[i];
         if (m > maxrow) maxrow = m;
     }
-    ora_entry* tmp = (ora_entry*)malloc(sizeof(ora_entry) * (size_t)(maxrow ? maxrow : 1));
-    for (int64_t i = 0; i < N; ++i) {
-        const int64_t lo = c->indptr[i], m = c->indptr[i + 1] - lo;
-        if (m < 2) continue;
-        for (int64_t t = 0; t < m; ++t) { tmp[t].d = c->d2[lo + t]; tmp[t].j = c->nbr[lo + t]; }
-        qsort(tmp, (size_t)m, sizeof(ora_entry), entry_cmp);
-        for (int64_t t = 0; t < m; ++t) { c->d2[lo + t] = tmp[t].d; c->nbr[lo + t] = tmp[t].j; }
-    }
-    free(tmp);
+    sort_rows_mt(c, maxrow, T);
     return c;
 }
 

@@ -150,19 +150,25 @@ def excl_collect(x, y, z, klo, khi, r2max, cap_hint):
 
 
 def csr_fill(ei, ej, ed, indptr, out_idx, out_d2):
-    """Scatter (host data movement only): self first, then edges in order."""
+    """Scatter the edges into both rows, self first, edges in emission order
+    (_kernels.py:164-185) -- on the device (ps_csr_fill)."""
+    indptr = np.asarray(indptr, np.int64)
     N = indptr.shape[0] - 1
-    cur = np.asarray(indptr[:N], np.int64).copy()
-    out_idx[cur] = np.arange(N)
-    out_d2[cur] = 0.0
-    cur += 1
-    for a, b, d in zip(np.asarray(ei), np.asarray(ej), np.asarray(ed)):
-        out_idx[cur[a]] = b
-        out_d2[cur[a]] = d
-        cur[a] += 1
-        out_idx[cur[b]] = a
-        out_d2[cur[b]] = d
-        cur[b] += 1
+    M = int(np.asarray(ei).shape[0])
+    E = int(indptr[-1])
+    dev = _dev()
+    d_ei = _to(ei if M else np.zeros(1), np.int32)
+    d_ej = _to(ej if M else np.zeros(1), np.int32)
+    d_ed = _to(ed if M else np.zeros(1), np.float64)
+    d_ip = _to(indptr, np.int64)
+    d_idx = torch.empty(max(E, 1), dtype=torch.int64, device=dev)
+    d_d2 = torch.empty(max(E, 1), dtype=torch.float64, device=dev)
+    wb = int(_lib.raw("ps_csr_fill_workspace_bytes", M, max(N, 1)))
+    work = torch.empty(max(wb, 1), dtype=torch.uint8, device=dev)
+    _lib.call("ps_csr_fill", _p(d_ei), _p(d_ej), _p(d_ed), M, _p(d_ip), N, _p(d_idx), _p(d_d2), _p(work), wb,
+              _stream())
+    out_idx[:E] = d_idx[:E].cpu().numpy()
+    out_d2[:E] = d_d2[:E].cpu().numpy()
 
 
 def csr_sort_rows(indptr, d2, idx):
@@ -222,7 +228,7 @@ def sample_predicted(indptr, nbr_idx, level_counts, seg_level_rows, boundaries, 
     bnd = np.ascontiguousarray(boundaries, np.int64)
     _lib.call("ps_sample_predicted", _p(d_ip), _p(d_nb), d_nb.shape[1], _p(d_ct), L, rows.ctypes.data,
               bnd.ctypes.data, nseg, _p(out), out.shape[1], k0, n_total, 1, N, _p(st), 1 if pick_lowest else 0,
-              _p(reached), _p(ex), _p(en), _p(work), _stream())
+              _p(reached), _p(ex), _p(en), _p(work), None, _stream())
     o = out[0, :n_total].cpu().numpy()
     state_out = np.uint64(np.int64(st.item()).view(np.uint64))
     return o, int(reached.item()), bool(ex.item()), int(en.item()), state_out

@@ -33,8 +33,11 @@ _SIGS = {
     "ps_first_untaken": (_c_i32, [_p, _c_i64, _p, _p]),
     "ps_excl_workspace_bytes": (_c_i64, [_c_i64, _c_i64, _c_i64, _c_i32]),
     "ps_excl_grid_evals_offset": (_c_i64, [_c_i64, _c_i64]),
+    "ps_excl_row_stride": (_c_i64, [_c_i64, _c_i64]),
     "ps_excl_build": (_c_i32, [_p, _c_i64, _c_i64, _p, _c_i32, _c_i64, _p, _p, _p, _p, _c_i64, _p, _c_i64, _p, _c_i32,
                                _p]),
+    "ps_csr_fill_workspace_bytes": (_c_i64, [_c_i64, _c_i64]),
+    "ps_csr_fill": (_c_i32, [_p, _p, _p, _c_i64, _p, _c_i64, _p, _p, _p, _c_i64, _p]),
     "ps_csr_sort_rows": (_c_i32, [_p, _p, _p, _c_i64, _c_i64, _c_i64, _p, _p]),
     "ps_level_counts": (_c_i32, [_p, _p, _c_i64, _c_i64, _c_i64, _p, _c_i32, _c_i64, _p, _p]),
     "ps_thresholds": (_c_i32, [_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_i32, _p, _c_i32, _p, _p, _c_i64, _p,
@@ -43,17 +46,17 @@ _SIGS = {
                                    _p]),
     "ps_sampler_workspace_bytes": (_c_i64, [_c_i64, _c_i64, _c_i32]),
     "ps_sample_predicted": (_c_i32, [_p, _p, _c_i64, _p, _c_i32, _p, _p, _c_i32, _p, _c_i64, _c_i64, _c_i64,
-                                     _c_i64, _c_i64, _p, _c_i32, _p, _p, _p, _p, _p]),
+                                     _c_i64, _c_i64, _p, _c_i32, _p, _p, _p, _p, _p, _p]),
     "ps_earlyterm_scan": (_c_i32, [_p, _p, _p, _c_i64, _p, _c_i64, _p, _p, _c_i64, _c_i64, _c_i64, _c_i64, _p]),
     "ps_early_termination_prepare": (_c_i32, [_p, _p, _p, _c_i64, _p, _c_i64, _p, _p, _p, _c_i64, _p, _c_i64,
                                               _c_i64, _c_i64, _p]),
     "ps_ball_query_rf": (_c_i32, [_p, _p, _p, _c_i64, _p, _c_i32, _c_i32, _p, _c_i64, _c_i64, _c_i64, _c_i64,
-                                  _c_i32, _p, _p, _p, _p]),
+                                  _c_i32, _p, _p, _p, _p, _p]),
     "ps_ball_query_naive": (_c_i32, [_p, _p, _c_i64, _c_i64, _c_i64, _c_i64, _c_f64, _c_i32, _p, _p, _p, _p]),
     "ps_knn_naive": (_c_i32, [_p, _p, _c_i64, _c_i64, _p, _c_i64, _c_i64, _c_i64, _c_i64, _c_i32, _p, _p, _p,
                               _p]),
     "ps_knn_rf": (_c_i32, [_p, _p, _p, _p, _c_i64, _p, _c_i64, _p, _p, _c_i64, _c_i64, _p, _c_i64, _c_i64,
-                           _c_i64, _c_i64, _c_i32, _p, _p, _p, _p, _p]),
+                           _c_i64, _c_i64, _c_i32, _p, _p, _p, _p, _p, _p]),
     "ps_min_spacing": (_c_i32, [_p, _p, _c_i64, _c_i64, _c_i64, _c_i64, _p, _p]),
     "ps_fps_mailbox_bytes": (_c_i64, [_c_i64, _c_i32]),
     "ps_fps_split_plan": (_c_i32, [_c_i64, _c_i64, _c_i32, _c_i32, _p, _p]),

@@ -143,11 +143,12 @@ int ps_fps(const float* xyz4, int64_t B, int64_t N, double* md, uint8_t* taken, 
 
 int64_t ps_fps_mailbox_bytes(int64_t B, int32_t G) {
     if (B < 1 || G < 1) return 0;
-    return B * 3 * (int64_t)G * ps::kMbRecs * 2 * (int64_t)sizeof(uint4);
+    return B * 3 * (int64_t)G * ps::kMbRecs * ps::kRecU4 * (int64_t)sizeof(uint4);
 }
 
 int ps_fps_split_plan(int64_t N, int64_t B, int32_t G, int32_t Gl, int32_t* C_out, int32_t* P_out) {
-    CHECK_ARG(B >= 1 && N >= 1 && N <= kMaxN && G >= 1 && Gl >= 1 && Gl <= G, "invalid split shape");
+    CHECK_ARG(B >= 1 && N >= 1 && N <= kMaxN && G >= 1 && G <= ps::kMaxRanks && Gl >= 1 && Gl <= G,
+              "invalid split shape (1 <= Gl <= G <= %d)", ps::kMaxRanks);
     int C = 0, P = 0;
     if (!ps::fps_res_plan(N, B * Gl, G, &C, &P))
         return fail(PS_ERR_UNSUPPORTED, "no co-resident cluster plan for N=%lld over %d ranks (%d per launch)",
@@ -163,8 +164,8 @@ int ps_fps_split(const float* xyz4, int64_t B, int64_t N, double* md, uint8_t* t
     CHECK_ARG(B >= 1 && N >= 1 && N <= kMaxN, "invalid batch shape B=%lld N=%lld", (long long)B, (long long)N);
     CHECK_ARG(k_stop >= 1 && k_stop <= ld_out && k_stop <= N, "k_stop %lld out of range", (long long)k_stop);
     CHECK_ARG(seed >= 0 && seed < N, "seed index %lld out of range", (long long)seed);
-    CHECK_ARG(G >= 1 && G <= 64 && Gl >= 1 && g_base >= 0 && g_base + Gl <= G, "invalid ranks G=%d g_base=%d Gl=%d",
-              G, g_base, Gl);
+    CHECK_ARG(G >= 1 && G <= ps::kMaxRanks && Gl >= 1 && g_base >= 0 && g_base + Gl <= G,
+              "invalid ranks G=%d g_base=%d Gl=%d (G <= %d: one warp lane per rank)", G, g_base, Gl, ps::kMaxRanks);
     CHECK_ARG(G == 1 || mbox_dev != nullptr, "mailbox pointer array required for G > 1");
     CHECK_ARG((uint64_t)seq_base + (uint64_t)k_stop < 0xffffffffull, "sequence space exhausted; reset the mailboxes");
     CHECK_ARG(xyz4 && md && taken && out_idx && curve, "null pointer");
@@ -179,6 +180,7 @@ int ps_fps_split(const float* xyz4, int64_t B, int64_t N, double* md, uint8_t* t
     ps::FpsRanks rk = {};
     rk.G = G; rk.Gl = Gl; rk.g_base = g_base; rk.all_write = all_write; rk.seq_base = seq_base;
     rk.mbox = reinterpret_cast<uint4* const*>(mbox_dev);
+    rk.timeout_ns = ps::split_timeout_ns();
     return cuda_status(ps::launch_fps_res(a, rk, B, C, P, S(stream)), "fps_split", 1);
 }
 
@@ -273,11 +275,15 @@ int64_t ps_excl_workspace_bytes(int64_t B, int64_t N, int64_t cap_edges, int32_t
         s += align_up(sizeof(int) * B * mc);
         s += align_up(sizeof(int32_t) * B * N) * 2;
         s += align_up(sizeof(float4) * B * N);
-        s += align_up(sizeof(unsigned long long) * B);
+        s += align_up(sizeof(unsigned long long) * B) * 2;  // evals, spill
     }
     s += align_up(sizeof(int32_t) * B * N) * 2;
     s += align_up(sizeof(unsigned));
     return (int64_t)s;
+}
+
+int64_t ps_excl_row_stride(int64_t N, int64_t cap_entries) {
+    return N >= 1 ? ps::ell_row_stride(cap_entries, N) : 0;
 }
 
 int64_t ps_excl_grid_evals_offset(int64_t B, int64_t N) {
@@ -299,7 +305,7 @@ int ps_excl_build(const float* xyz4, int64_t B, int64_t N, const double* r2_leve
     CHECK_ARG(cap_entries >= N && cap_entries < ((int64_t)1 << 31), "cap_entries must be in [N, 2^31)");
     CHECK_ARG(cap_edges >= 1, "cap_edges must be >= 1");
     CHECK_ARG(method >= 0 && method <= 2, "method must be 0 (brute force), 1 (grid) or 2 (grid, strided bucket rows)");
-    CHECK_ARG(method != 2 || cap_entries / N <= 65535, "row stride too large");
+    CHECK_ARG(method != 2 || ps::ell_row_stride(cap_entries, N) <= 65535, "row stride too large");
     CHECK_ARG(work && status && indptr && nbr && d2 && counts, "null pointer");
     unsigned char* w = static_cast<unsigned char*>(work);
     ps::ExclWork ew = {};
@@ -320,6 +326,7 @@ int ps_excl_build(const float* xyz4, int64_t B, int64_t N, const double* r2_leve
         gw.sorted_idx = reinterpret_cast<int32_t*>(w); w += align_up(sizeof(int32_t) * B * N);
         gw.sorted_xyz = reinterpret_cast<float4*>(w); w += align_up(sizeof(float4) * B * N);
         gw.evals = reinterpret_cast<unsigned long long*>(w); w += align_up(sizeof(unsigned long long) * B);
+        ew.spill = reinterpret_cast<unsigned long long*>(w); w += align_up(sizeof(unsigned long long) * B);
     }
     ew.deg = reinterpret_cast<int32_t*>(w); w += align_up(sizeof(int32_t) * B * N);
     ew.long_rows = reinterpret_cast<int32_t*>(w); w += align_up(sizeof(int32_t) * B * N);
@@ -329,6 +336,21 @@ int ps_excl_build(const float* xyz4, int64_t B, int64_t N, const double* r2_leve
     return cuda_status(ps::launch_excl_build(reinterpret_cast<const float4*>(xyz4), B, N, r2_levels, L, levels_ld,
                                              csr, ew, gw, method, S(stream)),
                        "excl_build", ps::excl_build_launches(N, method));
+}
+
+int64_t ps_csr_fill_workspace_bytes(int64_t M, int64_t N) {
+    if (M < 0 || N < 1) return 0;
+    return (int64_t)ps::csr_fill_ws_bytes(M, N);
+}
+
+int ps_csr_fill(const int32_t* ei, const int32_t* ej, const double* ed, int64_t M, const int64_t* indptr, int64_t N,
+                int64_t* out_idx, double* out_d2, void* work, int64_t work_bytes, void* stream) {
+    CHECK_ARG(N >= 1 && N < ((int64_t)1 << 31) && M >= 0 && 2 * M < ((int64_t)1 << 31), "invalid sizes");
+    CHECK_ARG(indptr && out_idx && out_d2 && (M == 0 || (ei && ej && ed)), "null pointer");
+    CHECK_ARG(work && work_bytes >= ps_csr_fill_workspace_bytes(M, N), "workspace too small (ps_csr_fill_workspace_bytes)");
+    return cuda_status(ps::launch_csr_fill(ei, ej, ed, M, indptr, N, out_idx, out_d2, work, (size_t)work_bytes,
+                                           S(stream)),
+                       "csr_fill", M > 0 ? 3 : 1);
 }
 
 int ps_csr_sort_rows(int64_t* indptr, int32_t* nbr, double* d2, int64_t cap_entries, int64_t B, int64_t N,
@@ -395,17 +417,16 @@ int ps_thresholds_mlp(const double* prefix_curve, int64_t curve_ld, int64_t B, i
     return cuda_status(ps::launch_thresholds(a, B, S(stream)), "thresholds_mlp", 1);
 }
 
-static bool sampler_fits_smem(int64_t N, int nseg) { return ps::sampler_ws_bytes(N, nseg) <= 176 * 1024; }
-
 int64_t ps_sampler_workspace_bytes(int64_t B, int64_t N, int32_t nseg) {
-    return (int64_t)ps::sampler_global_ws_bytes(B, N, !sampler_fits_smem(N, nseg));
+    (void)nseg;
+    return (int64_t)ps::sampler_global_ws_bytes(B, N, true);
 }
 
 int ps_sample_predicted(const int64_t* indptr, const int32_t* nbr, int64_t cap_entries, const int32_t* counts,
                         int32_t L, const int32_t* seg_level_rows_host, const int64_t* boundaries_host, int32_t nseg,
                         int64_t* out_idx, int64_t ld_out, int64_t k0, int64_t n_total, int64_t B, int64_t N,
                         uint64_t* state_io, int32_t pick_lowest, int64_t* reached, int32_t* exhausted,
-                        int32_t* entered, void* work, void* stream) {
+                        int32_t* entered, void* work, const int32_t* excl_status, void* stream) {
     CHECK_ARG(B >= 1 && N >= 1 && N <= kMaxN, "invalid batch shape");
     CHECK_ARG(nseg >= 1 && nseg <= ps::kMaxSeg, "nseg must be in [1, %d]", ps::kMaxSeg);
     CHECK_ARG(k0 >= 0 && k0 <= n_total && n_total <= ld_out && n_total <= N, "invalid k0/n_total");
@@ -422,13 +443,11 @@ int ps_sample_predicted(const int64_t* indptr, const int32_t* nbr, int64_t cap_e
     }
     a.k0 = k0; a.n_total = n_total; a.N = N; a.out_idx = out_idx; a.ld_out = ld_out; a.state_io = state_io;
     a.pick_lowest = pick_lowest; a.reached = reached; a.exhausted = exhausted; a.entered = entered;
-    a.use_smem = sampler_fits_smem(N, nseg) ? 1 : 0;
+    a.excl_status = excl_status;
     CHECK_ARG(work != nullptr, "sampler workspace required (ps_sampler_workspace_bytes)");
     a.gws = static_cast<unsigned char*>(work);
     a.B = B;
-    const char* sv = getenv("PS_SAMPLER");
-    return cuda_status(ps::launch_sampler(a, B, S(stream)), "sample_predicted",
-                       (sv && atoi(sv) == 3) ? 2 + 3 * nseg : 1);
+    return cuda_status(ps::launch_sampler(a, B, S(stream)), "sample_predicted", 1);
 }
 
 int ps_earlyterm_scan(const int64_t* indptr, const int32_t* nbr, const double* d2, int64_t cap_entries,
@@ -458,13 +477,13 @@ int ps_early_termination_prepare(const int64_t* indptr, const int32_t* nbr, cons
 int ps_ball_query_rf(const int64_t* indptr, const int32_t* nbr, const double* d2, int64_t cap_entries,
                      const int32_t* counts, int32_t L, int32_t level, const int64_t* centroids, int64_t cent_ld,
                      int64_t B, int64_t N, int64_t n, int32_t k, int32_t* idx_out, double* dist_out, int32_t* cnt_out,
-                     void* stream) {
-    CHECK_ARG(k >= 1, "k must be >= 1");
+                     const int32_t* excl_status, void* stream) {
+    CHECK_ARG(k >= 1 && k <= 128, "k must be in [1, 128]");
     CHECK_ARG(level >= 0 && level < L, "level %d out of range [0, %d)", level, L);
     ps::BqArgs a = {};
     a.indptr = indptr; a.nbr = nbr; a.d2 = d2; a.cap_entries = cap_entries; a.counts = counts; a.L = L;
     a.level = level; a.centroids = centroids; a.cent_ld = cent_ld; a.B = B; a.N = N; a.n = n; a.k = k;
-    a.idx_out = idx_out; a.dist_out = dist_out; a.cnt_out = cnt_out;
+    a.idx_out = idx_out; a.dist_out = dist_out; a.cnt_out = cnt_out; a.status = excl_status;
     if (B * n == 0) return PS_OK;
     return cuda_status(ps::launch_bq_rf(a, S(stream)), "ball_query_rf", 1);
 }
@@ -498,7 +517,7 @@ int ps_knn_rf(const float* xyz4, const int64_t* indptr, const int32_t* nbr, cons
               const int32_t* lvl1_counts, int64_t counts_stride, const uint8_t* sampled, const int64_t* queries,
               int64_t q_ld, int64_t nq, const int64_t* pool, int64_t pool_ld, int64_t npool, int64_t B, int64_t N,
               int32_t k, int32_t* idx_out, double* dist_out, int32_t* cnt_out, int32_t* fallback_count,
-              void* stream) {
+              const int32_t* excl_status, void* stream) {
     CHECK_ARG(k >= 1 && k <= 16, "k must be in [1, 16]");
     CHECK_ARG(npool >= 1, "empty pool");
     ps::KnnArgs a = {};
@@ -507,6 +526,7 @@ int ps_knn_rf(const float* xyz4, const int64_t* indptr, const int32_t* nbr, cons
     a.sampled = sampled; a.indptr = indptr; a.nbr = nbr; a.d2 = d2; a.cap_entries = cap_entries;
     a.lvl1_counts = lvl1_counts; a.counts_stride = counts_stride; a.B = B; a.N = N; a.k = k;
     a.idx_out = idx_out; a.dist_out = dist_out; a.cnt_out = cnt_out; a.fallback_count = fallback_count;
+    a.status = excl_status;
     if (B * nq == 0) return PS_OK;
     return cuda_status(ps::launch_knn_rf(a, S(stream)), "knn_rf", 1);
 }

@@ -279,6 +279,7 @@ __global__ void __launch_bounds__(1024) grid_setup_kernel(const float4* __restri
         if (zero) {
             g.evals[b] = 0;
             w.status[b] = 0;
+            if (w.spill) w.spill[b] = 0;
             if (b == 0) *w.long_count = 0;
         }
     }
@@ -399,6 +400,7 @@ __global__ void __launch_bounds__(1024) grid_build_kernel(const float4* __restri
     if (tid == 0) {
         g.evals[b] = 0;
         w.status[b] = 0;
+        if (w.spill) w.spill[b] = 0;
         if (b == 0) *w.long_count = 0;
     }
     // 1. bounding box and grid parameters
@@ -852,7 +854,9 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) grid_rows_kernel(int64_t B,
 // -- the only row property the sampler, early termination and the
 // redundancy-free queries rely on (they read per-level prefixes as sets;
 // the queries order their small prefixes themselves).  Rows longer than the
-// stride set status bit 1 and are rebuilt by the host with a wider stride.
+// stride move to the cloud's spill arena (ell_row_stride); only a full arena
+// sets status bit 1 (the sampler and the queries then emit error states and
+// the host rebuilds with a larger capacity).
 constexpr int kEllWarps = 8;
 constexpr int kEllCap = 256;   // per-warp staging (rows above it: overflow)
 
@@ -984,15 +988,27 @@ __global__ void __launch_bounds__(kEllWarps * 32, 4) grid_ell_kernel(int64_t B, 
             cnt += __popc(hm);
         }
         evals += (unsigned long long)total;
+        int64_t row_off = (int64_t)i * stride;
         if (cnt > stride) {
-            // overflow: flag it and leave a safe (empty) row until the host rebuilds
-            if (lane == 0) atomicOr(&w.status[b], 2);
-            if (lane < L) csr.counts[(b * csr.L + lane) * N + i] = 0;
-            continue;
+            // longer than the stride: the row takes a run of the cloud's spill
+            // arena (after the N strided rows) and indptr[i] points there; only
+            // when the arena is exhausted does the build fail -- status bit 1,
+            // an empty row, and consumers (sampler, queries) see the status
+            unsigned long long o = 0;
+            if (lane == 0) o = atomicAdd(&w.spill[b], (unsigned long long)((cnt + 3) & ~3));
+            o = __shfl_sync(kFull, o, 0);
+            const int64_t off = N * stride + (int64_t)o;
+            if (off + cnt > csr.cap_entries) {
+                if (lane == 0) atomicOr(&w.status[b], 2);
+                if (lane < L) csr.counts[(b * csr.L + lane) * N + i] = 0;
+                continue;
+            }
+            row_off = off;
+            if (lane == 0) csr.indptr[b * (N + 1) + i] = off;
         }
         __syncwarp();
-        int32_t* rn = csr.nbr + b * csr.cap_entries + (int64_t)i * stride;
-        double* rd = csr.d2 + b * csr.cap_entries + (int64_t)i * stride;
+        int32_t* rn = csr.nbr + b * csr.cap_entries + row_off;
+        double* rd = csr.d2 + b * csr.cap_entries + row_off;
         if (cnt > kEllCap) {
             // long row (beyond the staging buffer): one exact rescan per bucket,
             // writing straight to the row -- only for very dense neighbourhoods
@@ -1098,7 +1114,7 @@ cudaError_t launch_excl_build(const float4* xyz, int64_t B, int64_t N, const dou
     }
     const unsigned gpts = (unsigned)std::min<int64_t>(148 * 16, (B * N + 255) / 256 + 1);
     if (method == 1 || method == 2) {
-        const int64_t stride = csr.cap_entries / N;
+        const int64_t stride = method == 2 ? ell_row_stride(csr.cap_entries, N) : 0;
         const bool multi = !fused_grid;
         if (multi) {
             // grid_setup_kernel zeroes the counters and bookkeeping it owns

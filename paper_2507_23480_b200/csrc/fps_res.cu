@@ -139,46 +139,118 @@ PS_DEV uint32_t morton12(float x, float y, float z, float ox, float oy, float oz
 }
 
 // ---- global mailboxes (G > 1) ----------------------------------------------------
-// Mailbox of a rank: uint4[B][3][G][2 * kMbRecs]; set 0/1 = exchange parity,
-// set 2 = duplicate fallback; a slot holds one record (one-sample loop) or a
-// rank's meta record, header and up to 32 candidates (speculative loop).  A record is two 16-byte halves, each tagged with the
-// 32-bit sequence number, so a reader accepts it only when both halves carry
-// the expected tag (written by the owner with relaxed system-scope stores,
-// possibly from a peer GPU over NVLink).
+// Mailbox of a rank: uint4[B][3][G][kRecU4 * kMbRecs]; set 0/1 = exchange
+// parity, set 2 = duplicate fallback; a slot holds one record (one-sample
+// loop) or a rank's meta record, header and up to 32 candidates (speculative
+// loop).  Every 64-bit word of a record carries its 32-bit payload next to the
+// 32-bit sequence tag and is written with a relaxed system-scope store
+// (possibly from a peer GPU over NVLink): naturally aligned 64-bit accesses
+// are single-copy atomic, so a word whose tag matches holds this exchange's
+// payload whatever order the words land in -- the reader accepts a record
+// when all six tags match.  Waits are bounded (FpsRanks::timeout_ns).
 
-PS_DEV void st_sys_v4(uint4* p, uint4 v) {
-    asm volatile("st.relaxed.sys.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
-                 "r"(v.w)
-                 : "memory");
+PS_DEV void st_sys_v2(uint4* p, uint64_t a, uint64_t b) {
+    asm volatile("st.relaxed.sys.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
 }
-PS_DEV uint4 ld_sys_v4(const uint4* p) {
-    uint4 v;
-    asm volatile("ld.relaxed.sys.global.v4.b32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "l"(p)
-                 : "memory");
-    return v;
+PS_DEV void ld_sys_v2(const uint4* p, uint64_t& a, uint64_t& b) {
+    asm volatile("ld.relaxed.sys.global.v2.b64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
+PS_DEV uint64_t tagw(uint32_t v, uint32_t seq) { return ((uint64_t)seq << 32) | v; }
+PS_DEV bool tag_ok(uint64_t w, uint32_t seq) { return (uint32_t)(w >> 32) == seq; }
+PS_DEV unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// bounded wait bookkeeping: called every poll that found a stale record
+struct MboxWait {
+    unsigned long long t0 = 0;
+    uint32_t polls = 0;
+    PS_DEV void tick(const FpsRanks& rk, uint32_t seq) {
+        if ((++polls & 1023u) != 0u) return;
+        const unsigned long long now = globaltimer_ns();
+        if (t0 == 0) { t0 = now; return; }
+        if (now - t0 > rk.timeout_ns) {
+            if (rk.err) atomicCAS(rk.err, 0u, seq | 0x80000000u);
+            printf("ps fps split: mailbox wait for tag %u exceeded %llu ns (peer dead or late)\n", seq,
+                   rk.timeout_ns);
+            __trap();
+        }
+    }
+};
 
 // idx travels with the taken flag in bit 31 (indices are < 2^30)
 PS_DEV void mbox_put(uint4* slot, const Rec& r, uint32_t seq) {
     const uint32_t ix = r.idx == kNone ? kNone : (r.idx | (r.own & 0x80000000u));
-    st_sys_v4(slot, make_uint4(r.klo, r.khi, ix, seq));
-    st_sys_v4(slot + 1, make_uint4(__float_as_uint(r.x), __float_as_uint(r.y), __float_as_uint(r.z), seq));
+    st_sys_v2(slot, tagw(r.klo, seq), tagw(r.khi, seq));
+    st_sys_v2(slot + 1, tagw(ix, seq), tagw(__float_as_uint(r.x), seq));
+    st_sys_v2(slot + 2, tagw(__float_as_uint(r.y), seq), tagw(__float_as_uint(r.z), seq));
 }
 
-PS_DEV Rec mbox_get(const uint4* slot, uint32_t seq) {
-    uint4 h0, h1;
-    do {
-        h0 = ld_sys_v4(slot);
-        h1 = ld_sys_v4(slot + 1);
-    } while (h0.w != seq || h1.w != seq);
+PS_DEV Rec mbox_get(const uint4* slot, uint32_t seq, const FpsRanks& rk) {
+    uint64_t w[6];
+    MboxWait wt;
+    while (true) {
+        ld_sys_v2(slot, w[0], w[1]);
+        ld_sys_v2(slot + 1, w[2], w[3]);
+        ld_sys_v2(slot + 2, w[4], w[5]);
+        if (tag_ok(w[0], seq) && tag_ok(w[1], seq) && tag_ok(w[2], seq) && tag_ok(w[3], seq) &&
+            tag_ok(w[4], seq) && tag_ok(w[5], seq))
+            break;
+        wt.tick(rk, seq);
+    }
+    const uint32_t ix = (uint32_t)w[2];
     Rec r;
-    r.klo = h0.x; r.khi = h0.y;
-    r.idx = h0.z == kNone ? kNone : (h0.z & 0x7fffffffu);
-    r.own = h0.z == kNone ? 0u : ((h0.z & 0x80000000u) | kForeign);
-    r.x = __uint_as_float(h1.x); r.y = __uint_as_float(h1.y); r.z = __uint_as_float(h1.z); r.pad = 0;
+    r.klo = (uint32_t)w[0]; r.khi = (uint32_t)w[1];
+    r.idx = ix == kNone ? kNone : (ix & 0x7fffffffu);
+    r.own = ix == kNone ? 0u : ((ix & 0x80000000u) | kForeign);
+    r.x = __uint_as_float((uint32_t)w[3]); r.y = __uint_as_float((uint32_t)w[4]); r.z = __uint_as_float((uint32_t)w[5]);
+    r.pad = 0;
     return r;
+}
+
+// meta record of a speculative exchange: candidate count and overflow flag
+PS_DEV void mbox_put_meta(uint4* slot, uint32_t cn, uint32_t ovf, uint32_t seq) {
+    st_sys_v2(slot, tagw(cn, seq), tagw(ovf, seq));
+}
+PS_DEV void mbox_get_meta(const uint4* slot, uint32_t seq, const FpsRanks& rk, uint32_t& cn, uint32_t& ovf) {
+    uint64_t a, b;
+    MboxWait wt;
+    while (true) {
+        ld_sys_v2(slot, a, b);
+        if (tag_ok(a, seq) && tag_ok(b, seq)) break;
+        wt.tick(rk, seq);
+    }
+    cn = (uint32_t)a;
+    ovf = (uint32_t)b;
+}
+
+// slot of (cloud b, set, from-rank f) inside a rank's mailbox; record k of it
+PS_DEV size_t mb_slot(int64_t b, int set, int G, int f) {
+    return (size_t)(((b * 3 + set) * G + f)) * (size_t)(kRecU4 * kMbRecs);
+}
+
+// Per-launch tag base for the internal virtual-rank split (graph-replay
+// safe): seq[0] = base of this launch, seq[1] = next base; when the 32-bit
+// tag space would wrap, the mailboxes are wiped (0xff) first.
+__global__ void mbox_epoch_kernel(uint32_t* seq, uint4* buf, size_t n_u4, uint32_t span) {
+    __shared__ uint32_t base;
+    if (threadIdx.x == 0) {
+        const uint32_t nx = seq[1];
+        base = ((uint64_t)nx + span + 1 >= 0xffffffffull) ? 0xffffffffu : nx;
+    }
+    __syncthreads();
+    if (base == 0xffffffffu) {
+        for (size_t i = threadIdx.x; i < n_u4; i += blockDim.x) buf[i] = make_uint4(~0u, ~0u, ~0u, ~0u);
+        __syncthreads();
+        if (threadIdx.x == 0) base = 0;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        seq[0] = base;
+        seq[1] = base + span + 1;
+    }
 }
 
 template <int P, bool kSpec>
@@ -228,6 +300,7 @@ __global__ void __launch_bounds__(kT, 1) fps_res_kernel(FpsArgs a, FpsRanks rk) 
     int64_t* __restrict__ out = a.out_idx + b * a.ld_out;
     double* __restrict__ curve = a.curve + b * a.ld_out;
     const bool writer = (g == 0 || rk.all_write) && r == 0;
+    const uint32_t seq_base = rk.seq_dev ? *reinterpret_cast<const volatile uint32_t*>(rk.seq_dev) : rk.seq_base;
 
     const int64_t k_start = a.k_start_dev ? a.k_start_dev[b] : a.k_start;
     const int64_t k_stop = a.k_stop;
@@ -533,9 +606,9 @@ __global__ void __launch_bounds__(kT, 1) fps_res_kernel(FpsArgs a, FpsRanks rk) 
                 __syncwarp();
                 if (lane == 0) mbar_arrive_expect_tx(&bars[par], tx_bytes);
                 if (G > 1) {
-                    const uint32_t seq = rk.seq_base + (uint32_t)it;
-                    if (r == 0 && lane < G) mbox_put(mb_dst + ((b * 3 + par) * G + g) * (2 * kMbRecs), cw, seq);
-                    const Rec pr = lane < G ? mbox_get(mb_mine + ((b * 3 + par) * G + lane) * (2 * kMbRecs), seq) : none_rec();
+                    const uint32_t seq = seq_base + (uint32_t)it;
+                    if (r == 0 && lane < G) mbox_put(mb_dst + mb_slot(b, par, G, g), cw, seq);
+                    const Rec pr = lane < G ? mbox_get(mb_mine + mb_slot(b, par, G, lane), seq, rk) : none_rec();
                     const int pl = argmax_lane(rec_key(pr), pr.idx);
                     if (lane == (pl < 0 ? 0 : pl)) {
                         Rec gw = pl < 0 ? none_rec() : pr;
@@ -606,11 +679,11 @@ __global__ void __launch_bounds__(kT, 1) fps_res_kernel(FpsArgs a, FpsRanks rk) 
                     fw = wv ? fb_slots[__ffs(wv) - 1] : none_rec();
                 }
                 if (G > 1) {
-                    const uint32_t seq = rk.seq_base + (uint32_t)it;
+                    const uint32_t seq = seq_base + (uint32_t)it;
                     __syncthreads();
                     if (warp == kW - 1) {
-                        if (r == 0 && lane < G) mbox_put(mb_dst + ((b * 3 + 2) * G + g) * (2 * kMbRecs), fw, seq);
-                        const Rec pr = lane < G ? mbox_get(mb_mine + ((b * 3 + 2) * G + lane) * (2 * kMbRecs), seq) : none_rec();
+                        if (r == 0 && lane < G) mbox_put(mb_dst + mb_slot(b, 2, G, g), fw, seq);
+                        const Rec pr = lane < G ? mbox_get(mb_mine + mb_slot(b, 2, G, lane), seq, rk) : none_rec();
                         const uint32_t pm = __reduce_min_sync(kFull, pr.idx);
                         const unsigned wv = __ballot_sync(kFull, pr.idx == pm && pr.idx != kNone);
                         if (lane == (wv ? __ffs(wv) - 1 : 0)) {
@@ -657,7 +730,7 @@ __global__ void __launch_bounds__(kT, 1) fps_res_kernel(FpsArgs a, FpsRanks rk) 
         // >= tau (every other point is < tau and md only falls), lowering the
         // other candidates by their exact float64 distance to each pick.  The
         // run is broadcast on a named barrier and folded by every warp.
-        const uint32_t tag0 = rk.seq_base;
+        const uint32_t tag0 = seq_base;
         int rn = 0;
         int hc = 0;
         float gain = 1.0f;
@@ -856,15 +929,14 @@ __global__ void __launch_bounds__(kT, 1) fps_res_kernel(FpsArgs a, FpsRanks rk) 
                         // forward my rank's set: meta, header, candidates
                         uint4* mb = lane < G ? rk.mbox[lane] : nullptr;
                         if (lane < G) {
-                            uint4* sl = mb + ((b * 3 + par) * G + g) * (2 * kMbRecs);
-                            for (int k = 0; k < cn; ++k) mbox_put(sl + 2 * (2 + k), cl_s[k], seq);
-                            mbox_put(sl + 2, rh, seq);
-                            st_sys_v4(sl + 1, make_uint4(0u, 0u, 0u, seq));
-                            st_sys_v4(sl, make_uint4((uint32_t)cn, ovf ? 1u : 0u, 0u, seq));
+                            uint4* sl = mb + mb_slot(b, par, G, g);
+                            for (int k = 0; k < cn; ++k) mbox_put(sl + kRecU4 * (2 + k), cl_s[k], seq);
+                            mbox_put(sl + kRecU4, rh, seq);
+                            mbox_put_meta(sl, (uint32_t)cn, ovf ? 1u : 0u, seq);
                         }
                     }
                     // every rank's set: mine from the cluster, others from my mailbox
-                    const uint4* mine = mb_mine + ((b * 3 + par) * G) * (2 * kMbRecs);
+                    const uint4* mine = mb_mine + mb_slot(b, par, G, 0);
                     Rec uh = none_rec();
                     int ucnt = 0;
                     bool uovf = false;
@@ -874,15 +946,12 @@ __global__ void __launch_bounds__(kT, 1) fps_res_kernel(FpsArgs a, FpsRanks rk) 
                             ucnt = cn;
                             uovf = ovf;
                         } else {
-                            const uint4* sl = mine + lane * (2 * kMbRecs);
-                            uint4 m0, m1;
-                            do {
-                                m0 = ld_sys_v4(sl);
-                                m1 = ld_sys_v4(sl + 1);
-                            } while (m0.w != seq || m1.w != seq);
-                            ucnt = (int)m0.x;
-                            uovf = m0.y != 0u;
-                            uh = mbox_get(sl + 2, seq);
+                            const uint4* sl = mine + (size_t)lane * (kRecU4 * kMbRecs);
+                            uint32_t mc, mo;
+                            mbox_get_meta(sl, seq, rk, mc, mo);
+                            ucnt = (int)mc;
+                            uovf = mo != 0u;
+                            uh = mbox_get(sl + kRecU4, seq, rk);
                         }
                     }
                     ovf = __any_sync(kFull, uovf);
@@ -904,9 +973,9 @@ __global__ void __launch_bounds__(kT, 1) fps_res_kernel(FpsArgs a, FpsRanks rk) 
                     __syncwarp();
                     if (lane < cn && mybase + lane < 32) cl_s2[mybase + lane] = minec[0];
                     if (lane < G && lane != g) {
-                        const uint4* sl = mine + lane * (2 * kMbRecs);
+                        const uint4* sl = mine + (size_t)lane * (kRecU4 * kMbRecs);
                         for (int k = 0; k < ucnt; ++k)
-                            if (ubase + k < 32) cl_s2[ubase + k] = mbox_get(sl + 2 * (2 + k), seq);
+                            if (ubase + k < 32) cl_s2[ubase + k] = mbox_get(sl + kRecU4 * (2 + k), seq, rk);
                     }
                     __syncwarp();
                     const int unn = un_all < 32 ? un_all : 32;
@@ -1094,8 +1163,8 @@ __global__ void __launch_bounds__(kT, 1) fps_res_kernel(FpsArgs a, FpsRanks rk) 
                 if (G > 1) {
                     __syncthreads();
                     if (warp == kW - 1) {
-                        if (r == 0 && lane < G) mbox_put(rk.mbox[lane] + ((b * 3 + 2) * G + g) * (2 * kMbRecs), fw, seq);
-                        const Rec pr = lane < G ? mbox_get(mb_mine + ((b * 3 + 2) * G + lane) * (2 * kMbRecs), seq)
+                        if (r == 0 && lane < G) mbox_put(rk.mbox[lane] + mb_slot(b, 2, G, g), fw, seq);
+                        const Rec pr = lane < G ? mbox_get(mb_mine + mb_slot(b, 2, G, lane), seq, rk)
                                                 : none_rec();
                         const uint32_t pm = __reduce_min_sync(kFull, pr.idx);
                         const unsigned wv = __ballot_sync(kFull, pr.idx == pm && pr.idx != kNone);
@@ -1338,9 +1407,19 @@ cudaError_t launch_fps_res(FpsArgs a, const FpsRanks& rk_in, int64_t B, int C, i
 
 // Clouds too large for one cluster (> 16 CTAs x 24 points per thread): the
 // point split over G co-resident virtual ranks on this GPU -- the protocol of
-// ps_fps_split with mailboxes owned here: one buffer per (device, stream, B,
-// G), so launches that share one are ordered by their stream; the first use
-// allocates, so it must not happen inside a graph capture.
+unsigned long long split_timeout_ns() {
+    const char* e = getenv("PS_SPLIT_TIMEOUT_MS");
+    return e ? (unsigned long long)atoll(e) * 1000000ull : kMboxTimeoutNs;
+}
+
+// ps_fps on a cloud too large for one cluster: the point split over G
+// virtual ranks with mailboxes owned here, one buffer per (device, stream, B,
+// G), so launches that share one are ordered by their stream.  The first use
+// allocates; inside a graph capture (no allocation possible) the capture
+// borrows the buffer last made for (device, B, G) -- the eager warm-up run
+// that precedes a capture -- or, without one, declines (the streaming
+// kernel runs instead).
+
 static cudaError_t launch_fps_virtual_split(FpsArgs a, int64_t B, cudaStream_t s) {
     static const int kGs[] = {10, 12, 16, 8, 20, 24, 32};
     int C = 0, P = 0, G = 0;
@@ -1356,7 +1435,7 @@ static cudaError_t launch_fps_virtual_split(FpsArgs a, int64_t B, cudaStream_t s
         uint8_t* buf;
         uint4** ptrs;
         size_t per_rank;
-        uint32_t seq;
+        uint32_t* seq;  // device: [0] tag base of the current launch, [1] next base
     };
     static Box boxes[16];
     static int nboxes = 0;
@@ -1367,33 +1446,45 @@ static cudaError_t launch_fps_virtual_split(FpsArgs a, int64_t B, cudaStream_t s
     Box* bx = nullptr;
     for (int i = 0; i < nboxes; ++i)
         if (boxes[i].dev == dev && boxes[i].stream == s && boxes[i].B == B && boxes[i].G == G) bx = &boxes[i];
-    const size_t per_rank = (size_t)B * 3 * (size_t)G * kMbRecs * 2 * sizeof(uint4);
+    const size_t per_rank = (size_t)B * 3 * (size_t)G * kMbRecs * kRecU4 * sizeof(uint4);
+    if (!bx) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+            for (int i = nboxes - 1; i >= 0 && !bx; --i)
+                if (boxes[i].dev == dev && boxes[i].B == B && boxes[i].G == G) bx = &boxes[i];
+            if (!bx) return cudaErrorNotSupported;
+        }
+    }
     if (!bx) {
         if (nboxes == 16) return cudaErrorNotSupported;  // the streaming kernel serves the rest
-        Box nb = {dev, s, B, G, nullptr, nullptr, per_rank, 0u};
+        Box nb = {dev, s, B, G, nullptr, nullptr, per_rank, nullptr};
         cudaError_t e = cudaMalloc(&nb.buf, per_rank * G);
         if (e != cudaSuccess) return e;
         e = cudaMalloc(&nb.ptrs, sizeof(uint4*) * G);
         if (e != cudaSuccess) return e;
-        uint4* hp[64];
+        e = cudaMalloc(&nb.seq, sizeof(uint32_t) * 2);
+        if (e != cudaSuccess) return e;
+        uint4* hp[kMaxRanks];
         for (int g = 0; g < G; ++g) hp[g] = reinterpret_cast<uint4*>(nb.buf + per_rank * g);
         e = cudaMemcpy(nb.ptrs, hp, sizeof(uint4*) * G, cudaMemcpyHostToDevice);
         if (e != cudaSuccess) return e;
         e = cudaMemset(nb.buf, 0xff, per_rank * G);
         if (e != cudaSuccess) return e;
+        e = cudaMemset(nb.seq, 0, sizeof(uint32_t) * 2);
+        if (e != cudaSuccess) return e;
         boxes[nboxes] = nb;
         bx = &boxes[nboxes++];
     }
-    if ((uint64_t)bx->seq + (uint64_t)a.k_stop + 1 >= 0xffffffffull) {  // tag space: wipe and restart
-        cudaError_t e = cudaMemsetAsync(bx->buf, 0xff, bx->per_rank * G, s);
-        if (e != cudaSuccess) return e;
-        bx->seq = 0;
-    }
+    // the tag base is advanced on the device, in stream order, so that every
+    // launch -- also every replay of a captured graph -- gets fresh tags
+    mbox_epoch_kernel<<<1, 256, 0, s>>>(bx->seq, reinterpret_cast<uint4*>(bx->buf), bx->per_rank * G / sizeof(uint4),
+                                        (uint32_t)a.k_stop);
     FpsRanks rk = {};
     rk.G = G; rk.Gl = G; rk.g_base = 0; rk.all_write = 0;
-    rk.seq_base = bx->seq;
+    rk.seq_base = 0;
+    rk.seq_dev = bx->seq;
+    rk.timeout_ns = split_timeout_ns();
     rk.mbox = bx->ptrs;
-    bx->seq += (uint32_t)a.k_stop + 1;
     if (getenv("PS_FPS_VERBOSE"))
         fprintf(stderr, "[fps-split] N=%lld B=%lld G=%d C=%d P=%d (virtual ranks)\n", (long long)a.N,
                 (long long)B, G, C, P);

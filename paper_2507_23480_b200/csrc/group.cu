@@ -77,10 +77,16 @@ __global__ void __launch_bounds__(kBqWarps * 32) bq_rf_kernel(BqArgs a) {
     for (int64_t g = blockIdx.x * (int64_t)kBqWarps + warp; g < a.B * a.n; g += nw) {
         const int64_t b = g / a.n, t = g - b * a.n;
         const int64_t c = a.centroids[b * a.cent_ld + t];
-        const int32_t cnt = a.counts[(b * a.L + a.level) * a.N + c];
-        const int64_t base = b * a.cap_entries + a.indptr[b * (a.N + 1) + c];
         int32_t* oi = a.idx_out + g * K;
         double* od = a.dist_out + g * K;
+        if (c < 0 || c >= a.N || (a.status && a.status[b] != 0)) {
+            // no valid row (invalid centroid, or the cloud's build failed): error state
+            for (int s = lane; s < K; s += 32) { oi[s] = -1; od[s] = nan_d(); }
+            if (lane == 0) a.cnt_out[g] = -1;
+            continue;
+        }
+        const int32_t cnt = a.counts[(b * a.L + a.level) * a.N + c];
+        const int64_t base = b * a.cap_entries + a.indptr[b * (a.N + 1) + c];
         const int m = cnt < K ? cnt : K;
         if (cnt <= 64) {
             double d0 = lane < cnt ? a.d2[base + lane] : kInf;
@@ -261,11 +267,16 @@ __global__ void __launch_bounds__(kKnnThreads) knn_rf_kernel(KnnArgs a) {
     const int64_t q = blockIdx.x * (int64_t)kKnnThreads + threadIdx.x;
     if (q >= a.nq) return;
     const int64_t qp = a.queries ? a.queries[b * a.q_ld + q] : q;
+    const int k = a.k;
+    const int64_t g = b * a.nq + q;
+    if (qp < 0 || qp >= a.N || (a.status && a.status[b] != 0)) {
+        for (int s = 0; s < k; ++s) { a.idx_out[g * k + s] = -1; a.dist_out[g * k + s] = nan_d(); }
+        a.cnt_out[g] = -1;
+        return;
+    }
     const int64_t base = b * a.cap_entries + a.indptr[b * (a.N + 1) + qp];
     const int32_t c = a.lvl1_counts[b * a.counts_stride + qp];
     const uint8_t* smp = a.sampled + b * a.N;
-    const int k = a.k;
-    const int64_t g = b * a.nq + q;
     // the k nearest sampled points of the level-1 prefix (a set), by (d2, index)
     TopK tk;
     topk_init(tk);
@@ -328,6 +339,7 @@ __global__ void __launch_bounds__(kKnnThreads) min_spacing_kernel(SpacingArgs a)
 }  // namespace
 
 cudaError_t launch_bq_rf(const BqArgs& a, cudaStream_t s) {
+    if (a.k < 1 || a.k > kBqMaxK) return cudaErrorInvalidValue;  // per-warp top-k lists hold kBqMaxK
     const unsigned g = (unsigned)std::min<int64_t>(148 * 16, (a.B * a.n + 7) / 8 + 1);
     bq_rf_kernel<<<g, 256, 0, s>>>(a);
     return cudaGetLastError();

@@ -22,6 +22,7 @@ struct BqArgs {
     int32_t* idx_out;           // [B][n][k]
     double* dist_out;           // [B][n][k]
     int32_t* cnt_out;           // [B][n]
+    const int32_t* status;      // [B] exclusion-build status (rf; nullable): nonzero -> error outputs
 };
 
 struct KnnArgs {
@@ -43,6 +44,7 @@ struct KnnArgs {
     double* dist_out;
     int32_t* cnt_out;
     int32_t* fallback_count;    // [B] (rf)
+    const int32_t* status;      // [B] exclusion-build status (rf; nullable)
 };
 
 struct SpacingArgs {

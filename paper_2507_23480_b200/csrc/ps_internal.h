@@ -27,23 +27,40 @@ struct FpsArgs {
 // [g*ceil(N/G), (g+1)*ceil(N/G)).  A launch runs Gl ranks per cloud starting
 // at g_base (Gl == G: virtual ranks on one GPU; Gl == 1: one rank per GPU).
 // mbox: device array of G pointers to each rank's mailbox
-// (uint4[B][3][G][2 * kMbRecs], initialised to 0xff); seq_base makes every
-// (launch, iteration) tag unique.
+// (uint4[B][3][G][kRecU4 * kMbRecs], initialised to 0xff); the tag of every
+// (launch, iteration) is unique: seq_base, or -- when seq_dev is set -- the
+// word seq_dev[0] written by mbox_epoch_kernel in the same stream (so CUDA
+// graph replays never meet a previous replay's records).  A mailbox wait
+// longer than timeout_ns (globaltimer) records the failing iteration in
+// err[0] (nullable) and traps: a dead or late peer becomes a launch error,
+// not a hang.
 struct FpsRanks {
     int G, Gl, g_base, all_write;
     int spatial;                // 1: spatial (Morton-cell) partition of the shard over the cluster's CTAs
     uint32_t seq_base;
     uint4* const* mbox;
+    const uint32_t* seq_dev;    // nullable: device-side tag base
+    unsigned long long timeout_ns;
+    unsigned int* err;          // nullable
 };
 
-// records per (cloud, set, rank) mailbox slot: meta + header + 32 candidates
+// records per (cloud, set, rank) mailbox slot: meta + header + 32 candidates;
+// a record is six 64-bit words {payload u32, tag u32} (kRecU4 uint4s)
 constexpr int kMbRecs = 34;
+constexpr int kRecU4 = 3;
+constexpr int kMaxRanks = 32;   // one warp lane per rank in every exchange
+constexpr unsigned long long kMboxTimeoutNs = 10ull * 1000 * 1000 * 1000;
 
 cudaError_t launch_fps(FpsArgs a, int64_t B, cudaStream_t s);          // resident kernel, else legacy
 cudaError_t launch_fps_legacy(FpsArgs a, int64_t B, cudaStream_t s);   // register / streaming kernel
 cudaError_t launch_fps_spec(FpsArgs a, int64_t B, cudaStream_t s);     // register kernel, speculation
 cudaError_t launch_fps_small(FpsArgs a, int64_t B, cudaStream_t s);    // one CTA per small cloud, points in registers
 bool fps_res_plan(int64_t N, int64_t nclusters, int G, int* C_out, int* P_out);
+unsigned long long split_timeout_ns();
+size_t csr_fill_ws_bytes(int64_t M, int64_t N);
+cudaError_t launch_csr_fill(const int32_t* ei, const int32_t* ej, const double* ed, int64_t M, const int64_t* indptr,
+                            int64_t N, int64_t* out_idx, double* out_d2, void* work, size_t work_bytes,
+                            cudaStream_t s);  // PS_SPLIT_TIMEOUT_MS, default kMboxTimeoutNs
 cudaError_t launch_fps_res(FpsArgs a, const FpsRanks& rk, int64_t B, int C, int P, cudaStream_t s);
 int fps_choose_cluster(int64_t N, int64_t B, int* C_out, int* P_out, int* T_out);
 
@@ -68,7 +85,17 @@ struct ExclWork {
     int32_t* long_rows;   // [B*N] rows too long for the warp sort (b*N + i)
     unsigned int* long_count;  // [1]
     int32_t* status;      // [B] bit0: edge overflow, bit1: entry overflow
+    unsigned long long* spill;  // [B] method 2: entries taken from the spill arena (rows longer than the stride)
 };
+
+// Method 2 (fixed-stride rows): row i at i * stride; the entries beyond
+// N * stride are the spill arena, from which rows longer than the stride take
+// a 16-byte aligned run of their own (indptr[i] then points there).  About
+// 1/9 of the capacity is spill.
+inline int64_t ell_row_stride(int64_t cap_entries, int64_t N) {
+    const int64_t s = (cap_entries / N) * 8 / 9;
+    return s >= 4 ? (s & ~int64_t(3)) : s;
+}
 
 struct GridParams {
     double ox, oy, oz, inv_h;

@@ -9,7 +9,7 @@
 // (__ddiv_rn) and min is exact, so the parallel evaluation is bit-identical
 // to the sequential oracle.
 //
-// K3c (the sampler, _kernels.py:241-353) lives in sampler_v3.cu.
+// K3c (the sampler, _kernels.py:241-353) lives in sampler_v4.cu.
 //
 // K3d replaces _kernels.earlyterm_scan (_kernels.py:356-367).
 

@@ -44,11 +44,11 @@ struct SampArgs {
     int64_t* reached;            // [B]
     int32_t* exhausted;          // [B]
     int32_t* entered;            // [B]
-    int use_smem;
-    unsigned char* gws;          // global workspace (always; tables too when use_smem == 0)
+    unsigned char* gws;          // global workspace (per-cloud tables that do not fit in shared memory)
     int64_t gws_stride;
     long long* dbg;              // development timing (PS_SAMPLER_TIMING)
     int tiny;                    // v4, one CTA per cloud: the per-cloud arrays live in shared memory
+    const int32_t* excl_status;  // [B] nullable: nonzero -> the cloud's rows are incomplete (error outputs)
 };
 
 struct EtArgs {
@@ -79,11 +79,9 @@ struct EtScanArgs {
     int64_t n_total, B, N, lo, hi;
 };
 
-size_t sampler_ws_bytes(int64_t N, int nseg);              // shared-memory tables per cloud
 size_t sampler_global_ws_bytes(int64_t B, int64_t N, bool big);  // global workspace
 cudaError_t launch_thresholds(const ThreshArgs& a, int64_t B, cudaStream_t s);
-cudaError_t launch_sampler(SampArgs a, int64_t B, cudaStream_t s);     // v4 unless PS_SAMPLER=3
-cudaError_t launch_sampler_v3(SampArgs a, int64_t B, cudaStream_t s);
+cudaError_t launch_sampler(SampArgs a, int64_t B, cudaStream_t s);     // v4 (sampler_v4.cu)
 cudaError_t launch_sampler_v4(SampArgs a, int64_t B, cudaStream_t s);
 size_t sampler_v4_ws_bytes(int64_t B, int64_t N);
 cudaError_t launch_et(const EtArgs& a, cudaStream_t s);

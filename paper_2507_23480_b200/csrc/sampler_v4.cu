@@ -260,7 +260,16 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
     int seg = 0;
     while (seg < nseg && a.k0 >= a.boundaries[seg]) ++seg;
     int done = 0, exhausted = 0, entered = 0;
-    if (seg >= nseg) {
+    // a cloud whose exclusion build failed (spill arena exhausted) has
+    // incomplete rows: emit the error state instead of sampling from them
+    // (out = -1 past the prefix, reached = n_total so early termination has
+    // nothing to do, entered = -1); uniform over the cluster
+    const bool failed = a.excl_status && a.excl_status[b] != 0;
+    if (failed) {
+        done = 1;
+        i = a.n_total;
+        entered = -1;
+    } else if (seg >= nseg) {
         done = 1;
         exhausted = 1;
     } else {
@@ -895,5 +904,9 @@ cudaError_t launch_sampler_v4(SampArgs a, int64_t B, cudaStream_t s) {
     }
     return cudaLaunchKernelEx(&cfg, kern, a, w);
 }
+
+size_t sampler_global_ws_bytes(int64_t B, int64_t N, bool) { return sampler_v4_ws_bytes(B, N); }
+
+cudaError_t launch_sampler(SampArgs a, int64_t B, cudaStream_t s) { return launch_sampler_v4(a, B, s); }
 
 }  // namespace ps

@@ -32,6 +32,35 @@ def prefix_len(n: int, p: float) -> int:
     return int(math.ceil(p * n))
 
 
+class FpsState:
+    """Live FPS state after a prefix: float64 min-distances
+    and the taken mask, reusable to continue the run (fps_loop k_start)."""
+
+    def __init__(self, md, taken):
+        self.md = md
+        self.taken = taken
+
+
+def extract_prefix(cloud, n: int, p: float = 0.1, seed_index: int = 0):
+    """SPEC.md:238-246 on the device (K1 with k_stop = ceil(p n)) ->
+    (prefix curve float64[k0] with [0] = +inf, FpsState, SampleResult of the
+    k0 prefix indices)."""
+    from . import core, engine
+
+    pc = cloud if isinstance(cloud, core.PointCloud) else core.PointCloud(cloud)
+    k0 = prefix_len(n, p)
+    if k0 < 2:
+        raise ValueError("ceil(p*n) must be >= 2 (SPEC.md:240)")
+    if not (1 <= n <= pc.n):
+        raise ValueError(f"n must be in [1, {pc.n}], got {n}")
+    k0 = min(k0, n)
+    xyz4 = engine.as_xyz4(pc.coords)
+    idx, cv, md, taken = engine.fps(xyz4, n, seed_index, k_stop=k0)
+    core.add_pair_evals(pc.n * (k0 - 1))
+    res = core.SampleResult(idx[0, :k0].cpu().numpy(), "fps", {"fps_prefix_iters": k0})
+    return cv[0, :k0].cpu().numpy(), FpsState(md[0].cpu().numpy(), taken[0].cpu().numpy()), res
+
+
 def power_table(n: int, exponent: float) -> np.ndarray:
     """i**e as float64 for i in [0, n) (entry 0 unused)."""
     return np.power(np.arange(n, dtype=np.float64), np.float64(exponent))

@@ -186,6 +186,13 @@ class DeviceCsr:
         # the grid count pass visits ordered pairs including self: unordered = (c - N) / 2
         return [(int(c) - N) // 2 for c in cand]
 
+    @property
+    def stride(self) -> int:
+        """Method 2: entries per strided row (rows beyond it spill, see
+        ps_excl_row_stride); 0 for the sorted-CSR methods."""
+        N = self.indptr.shape[1] - 1
+        return int(_lib.raw("ps_excl_row_stride", N, self.cap_entries)) if self.method == 2 else 0
+
     def overflowed(self) -> bool:
         return bool(int(self.status.max().item()) != 0)
 
@@ -200,10 +207,12 @@ class DeviceCsr:
 
 def default_capacity(N: int, n: int) -> tuple[int, int]:
     """CSR entries per cloud: rows average ~14 x stride at the first segment
-    radius; start with a generous bound, grow on overflow."""
+    radius; start with a generous bound, grow on overflow.
+    The method-2 row stride comes out near ``per_point`` and the extra ninth
+    is the spill arena for longer rows (ps_excl_row_stride)."""
     stride = max(1, N // max(n, 1))
     per_point = min(N, max(96, 48 * stride))
-    cap_entries = N * per_point
+    cap_entries = N * (-(-per_point * 9 // 8) + 4)
     return cap_entries, max(1, (cap_entries - N) // 2 + 1)
 
 
@@ -329,7 +338,7 @@ class FastPoint:
         _lib.call("ps_sample_predicted", _p(c.indptr), _p(c.nbr), c.cap_entries, _p(c.counts), self.L,
                   self._rows_c.ctypes.data, self._bnd_c.ctypes.data, self.nseg, _p(self.out), self.n, self.k0,
                   self.n, self.B, self.N, _p(self.state), 1 if self.pick_lowest else 0, _p(self.reached),
-                  _p(self.exhausted), _p(self.entered), _p(self.samp_ws), _stream())
+                  _p(self.exhausted), _p(self.entered), _p(self.samp_ws), _p(c.status), _stream())
 
     def _early_termination(self):
         c = self.csr
@@ -354,7 +363,14 @@ class FastPoint:
     KERNELS_PER_SAMPLE = 1 + 1 + 6 + 1 + 2 + 1  # prefix, thresholds, exclusion (N > 4096), sampler, ET seed, ET FPS
 
     def capture(self):
-        """Capture ``sample`` into a CUDA graph (buffers are static)."""
+        """Capture ``sample`` into a CUDA graph (buffers are static).
+
+        A replay on new points whose exclusion rows outgrow the capacity
+        stays safe: rows longer than the stride spill into the arena inside
+        the same launch sequence (identical results), and only an exhausted
+        arena leaves the error state (``csr.status`` set, sampled indices -1
+        past the prefix, ``entered`` -1, rf groups with count -1) that
+        ``check`` turns into a rebuild -- it re-runs and re-captures."""
         s = torch.cuda.Stream(device=self.device)
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
@@ -367,16 +383,20 @@ class FastPoint:
         return g
 
     def check(self, max_grow=8):
-        """Host read of the CSR capacity status; grows buffers and re-runs
-        until nothing overflows.  Returns True when a re-run happened."""
+        """Host read of the exclusion-build status (one int per cloud).  On
+        an exhausted capacity: grow the buffers, re-run ``sample`` from the
+        RNG state of the last ``set_rng`` (and re-capture the CUDA graph if
+        one was captured) until nothing overflows.  Returns True when a
+        re-run happened; raises RuntimeError if the capacity cannot grow."""
         reran = False
+        had_graph = self.graph is not None
         for _ in range(max_grow):
             if not self.csr.overflowed():
-                return reran
-            E = int(self.csr.indptr[:, -1].max().item())
-            grow = min(max(2 * self.csr.cap_entries, E + self.N), self.N * self.N + self.N)
-            if self.excl_method == 2:  # keep the row stride whole
-                grow = -(-grow // self.N) * self.N
+                break
+            full = self.N * (self.N + 1) + 16 * self.N  # every pair, any stride rounding
+            if self.csr.cap_entries >= min(full, (1 << 31) - 1):
+                raise RuntimeError("exclusion lists overflow at the largest capacity")
+            grow = min(2 * self.csr.cap_entries, full, (1 << 31) - 1)
             self.csr = DeviceCsr.allocate(self.B, self.N, self.L, grow, grow // 2 + 1, self.device,
                                           self.excl_method)
             self.graph = None
@@ -386,6 +406,13 @@ class FastPoint:
             reran = True
         if self.csr.overflowed():
             raise RuntimeError("exclusion lists still overflow after growing the capacity")
+        if reran and had_graph:
+            if getattr(self, "_state0", None) is not None:
+                self.state.copy_(self._state0)
+            self.capture()
+            if getattr(self, "_state0", None) is not None:
+                self.state.copy_(self._state0)
+            self.sample()
         return reran
 
     # -- grouping ---------------------------------------------------------------
@@ -406,7 +433,8 @@ class FastPoint:
                    torch.empty(B, n, dtype=torch.int32, device=self.device))
         c = self.csr
         _lib.call("ps_ball_query_rf", _p(c.indptr), _p(c.nbr), _p(c.d2), c.cap_entries, _p(c.counts), self.L, lvl,
-                  _p(cent), cent.stride(0), B, self.N, n, int(k), _p(out[0]), _p(out[1]), _p(out[2]), _stream())
+                  _p(cent), cent.stride(0), B, self.N, n, int(k), _p(out[0]), _p(out[1]), _p(out[2]), _p(c.status),
+                  _stream())
         return out
 
     def knn_rf(self, k, queries=None):
@@ -423,7 +451,8 @@ class FastPoint:
         lvl1 = c.counts[:, int(self.seg_level_rows[0]), :]
         _lib.call("ps_knn_rf", _p(self.xyz4), _p(c.indptr), _p(c.nbr), _p(c.d2), c.cap_entries, _p(lvl1),
                   self.L * N, _p(sampled), _p(queries), 0 if queries is None else queries.stride(0), nq,
-                  _p(self.out), self.n, self.n, B, N, int(k), _p(idx), _p(dist), _p(cnt), _p(fb), _stream())
+                  _p(self.out), self.n, self.n, B, N, int(k), _p(idx), _p(dist), _p(cnt), _p(fb), _p(c.status),
+                  _stream())
         return idx, dist, cnt, fb
 
     # -- accounting ---------------------------------------------------------------

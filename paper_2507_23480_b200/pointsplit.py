@@ -3,9 +3,9 @@
 Every rank holds the whole cloud (N float4, 16 MB at N = 2^20) and owns the
 original indices [g*ceil(N/G), (g+1)*ceil(N/G)).  Each FPS iteration every
 rank reduces its shard inside one thread-block cluster and writes its
-32-byte shard record into every rank's mailbox -- device memory of the
-receiving GPU, mapped into the sender through CUDA IPC, written with
-system-scope stores over NVLink -- then reduces the G records with the
+shard record (six tagged 64-bit words) into every rank's mailbox -- device
+memory of the receiving GPU, mapped into the sender through CUDA IPC, written
+with system-scope stores over NVLink -- then reduces the G records with the
 chunk-merge rule of _kernels.fps_update_chunk / first_untaken
 (/root/reference/pkg/src/pointsample/_kernels.py:77-100).  There is no NCCL
 call on the data path; ``torch.distributed`` only exchanges the IPC handles
@@ -41,7 +41,17 @@ class PointSplitFPS:
         self.group = group
         self.G = dist.get_world_size(group)
         self.g = dist.get_rank(group)
+        if self.G > 32:
+            raise ValueError("the point split exchanges one warp lane per rank: at most 32 ranks")
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        # every peer GPU must be reachable with peer stores (NVLink / P2P);
+        # ranks sharing a GPU (tests) need nothing
+        devs = [None] * self.G
+        dist.all_gather_object(devs, self.device.index, group=group)
+        for r, d in enumerate(devs):
+            if r != self.g and d != self.device.index and not torch.cuda.can_device_access_peer(self.device, d):
+                raise RuntimeError(f"rank {self.g}: GPU {self.device.index} cannot access peer GPU {d} "
+                                   "(the point split needs P2P / NVLink between all ranks)")
         nbytes = int(_lib.raw("ps_fps_mailbox_bytes", self.B, self.G))
         # a dedicated cudaMalloc allocation: an IPC handle opens at the base of
         # the allocation it names, which a caching-allocator tensor is not
@@ -67,7 +77,11 @@ class PointSplitFPS:
         dist.barrier(group=group)
 
     def close(self):
-        """Collective: unmap the peers' mailboxes, then free this rank's."""
+        """Collective: wait for this rank's launches (they write the peers'
+        mailboxes), unmap the peers' mailboxes, then -- after every rank did
+        the same -- free this rank's."""
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)
         for p in self._opened:
             _lib.call("ps_ipc_close", p)
         self._opened = []

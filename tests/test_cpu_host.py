@@ -40,9 +40,16 @@ def test_validation_without_device():
     rows = np.zeros(6, np.int32)
     bnd = np.array([1, 2, 3, 4, 5, 9], np.int64)  # last != n_total
     rc = lib.ps_sample_predicted(None, None, 0, None, 6, rows.ctypes.data, bnd.ctypes.data, 6, None, 10, 2, 10, 1,
-                                 100, None, 0, None, None, None, None, None)
+                                 100, None, 0, None, None, None, None, None, None)
     assert rc == _lib.PS_ERR_INVALID
     assert b"last segment boundary" in lib.ps_last_error()
+    # rf ball query: the per-warp top-k lists hold 128 entries
+    rc = lib.ps_ball_query_rf(None, None, None, 0, None, 7, 6, None, 1, 1, 100, 10, 200, None, None, None, None, None)
+    assert rc == _lib.PS_ERR_INVALID and b"k must be in [1, 128]" in lib.ps_last_error()
+    # method-2 rows: 16-byte aligned stride, about 1/9 of the capacity left as spill arena
+    for N, per in ((24000, 216), (1000, 100), (7, 3)):
+        st = lib.ps_excl_row_stride(N, N * per)
+        assert st <= per * 8 // 9 and (st % 4 == 0 or st < 4) and N * per - N * st >= N * per // 9 - N
     assert lib.ps_excl_workspace_bytes(2, 100, 50, 0) > 0 and lib.ps_excl_workspace_bytes(2, 100, 1, 1) > 0
     assert 0 < lib.ps_sampler_workspace_bytes(1, 24000, 6) < lib.ps_sampler_workspace_bytes(1, 40000, 6) / 1.5
     assert lib.ps_sampler_workspace_bytes(2, 100000, 6) > 2 * lib.ps_sampler_workspace_bytes(1, 100000, 6) * 0.99
@@ -235,3 +242,21 @@ def test_random_and_grid_samplers_spec_examples():
     g = baselines.grid_sample_to_count(u, 2500, 0.05)
     assert 2375 <= len(g.indices) <= 2625
     assert baselines.grid_sample_to_count(u[:1], 1).indices.tolist() == [0]
+
+
+def test_pointsample_import_alias():
+    """The reference package name resolves to the B200 modules (drop-in swap
+    by import path, pkg/pyproject.toml:6)."""
+    import importlib
+
+    ps = importlib.import_module("pointsample")
+    from paper_2507_23480_b200 import _kernels as K
+    from paper_2507_23480_b200 import core as C
+
+    assert importlib.import_module("pointsample._kernels") is K
+    assert ps.core is C
+    for name in ("fps_loop", "fps_update_chunk", "first_untaken", "excl_collect", "csr_fill", "csr_sort_rows",
+                 "csr_level_counts", "sample_predicted", "earlyterm_scan"):
+        assert callable(getattr(K, name)), name
+    from pointsample.mdps import early_termination, mdps, sample_with_predicted_distance  # noqa: F401
+    from pointsample.curve import extract_prefix, segment_thresholds  # noqa: F401

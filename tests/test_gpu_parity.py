@@ -437,14 +437,19 @@ def test_excl_bucketed_rows_match_oracle_sets(N):
     pos = {float(v): k for k, v in enumerate(e.r2_levels)}
     for l, lv in enumerate(levels):
         np.testing.assert_array_equal(counts[l], e.counts[pos[float(lv)]])
+    ip = csr.indptr[0].cpu().numpy()
+    stride = csr.stride
+    assert np.all(ip[:N] % 4 == 0)  # 16-byte aligned rows (strided or spilled)
     for i in range(0, N, 7):
         m = counts[0]  # widest level is R[0]
-        got = sorted(zip(d2[i * 256:i * 256 + m[i]].tolist(), nbr[i * 256:i * 256 + m[i]].tolist()))
+        a = ip[i]
+        assert a == i * stride or (a >= N * stride and m[i] > stride)  # spilled rows are the long ones
+        got = sorted(zip(d2[a:a + m[i]].tolist(), nbr[a:a + m[i]].tolist()))
         lo = e.indptr[i]
         ref = list(zip(e.d2[lo:lo + m[i]].tolist(), e.nbr[lo:lo + m[i]].tolist()))
         assert got == ref, i
         for l, lv in enumerate(levels):  # each level is a prefix
-            assert np.all(d2[i * 256:i * 256 + counts[l][i]] < lv)
+            assert np.all(d2[a:a + counts[l][i]] < lv)
 
 
 def test_excl_prefilter_adversarial():
@@ -486,6 +491,18 @@ def test_dropin_collect_fill_sort_counts():
     nbr = np.empty(indptr[-1], np.int64)
     d2 = np.empty(indptr[-1], np.float64)
     GK.csr_fill(ei, ej, ed, indptr, nbr, d2)
+    # the fill order itself (before sorting): _kernels.py:164-185 restated
+    ref_nbr, ref_d2 = np.empty_like(nbr), np.empty_like(d2)
+    cur = indptr[:N].copy()
+    ref_nbr[cur], ref_d2[cur] = np.arange(N), 0.0
+    cur += 1
+    for a, b, d in zip(ei, ej, ed):
+        ref_nbr[cur[a]], ref_d2[cur[a]] = b, d
+        cur[a] += 1
+        ref_nbr[cur[b]], ref_d2[cur[b]] = a, d
+        cur[b] += 1
+    np.testing.assert_array_equal(nbr, ref_nbr)
+    np.testing.assert_array_equal(d2, ref_d2)
     GK.csr_sort_rows(indptr, d2, nbr)
     np.testing.assert_array_equal(indptr, e.indptr)
     np.testing.assert_array_equal(nbr, e.nbr)
@@ -580,6 +597,116 @@ def test_mdps_cuda_graph_replay_identical():
         fp.sample()
         torch.cuda.synchronize()
         assert torch.equal(fp.out, first)
+
+
+def _dense_cloud(N, n_dup, seed):
+    """Uniform box with n_dup copies of one point: n_dup rows of >= n_dup
+    entries, far beyond the default row stride."""
+    c = generate_cloud("uniform-box", N, seed)
+    c[:n_dup] = c[0]
+    return c[np.random.default_rng(seed).permutation(N)].copy()
+
+
+@pytest.mark.timeout(300)
+def test_graph_replay_spill_and_exhausted_capacity():
+    """A FastPoint CUDA graph captured on an ordinary cloud and replayed on
+    new points: (1) rows beyond the stride spill into the arena inside the
+    same launch sequence -- replay output equals the oracle, no host step;
+    (2) rows beyond the whole arena leave an explicit error state (indices -1
+    past the prefix, entered -1, rf counts -1) that survives the replay, and
+    check() rebuilds with a larger capacity, re-captures, and then matches."""
+    N, n, e, r = 4096, 1024, 0.4, 0.05
+    fp = engine.FastPoint(1, N, n, exponent=e, extra_radii=(r,))
+    stride = fp.csr.stride
+    spill = fp.csr.cap_entries - N * stride
+    fp.set_points(torch.from_numpy(generate_cloud("uniform-box", N, 5)[None]).cuda())
+    fp.set_rng([9])
+    fp.sample()
+    fp.check()
+    fp.capture()
+    grp = (torch.empty(1, n, 16, dtype=torch.int32, device="cuda"),
+           torch.empty(1, n, 16, dtype=torch.float64, device="cuda"),
+           torch.empty(1, n, dtype=torch.int32, device="cuda"))
+    n_spill = stride + stride // 4  # rows of ~n_spill entries: they spill, and fit the arena
+    assert n_spill > stride and n_spill * (n_spill + 4) < spill
+    n_big = int(1.2 * spill ** 0.5) + stride  # rows beyond the whole arena
+    for name, n_dup in (("spill", n_spill), ("exhausted", n_big)):
+        c = _dense_cloud(N, n_dup, 17)
+        fp.set_points(torch.from_numpy(c[None]).cuda())
+        fp.set_rng([9])
+        fp.sample()  # graph replay
+        fp.group_rf(r, 16, out=grp)
+        torch.cuda.synchronize()
+        ref = O.mdps(c, n, exponent=e, rng_seed=9, extra_radii=(r,))
+        if name == "spill":
+            assert not fp.csr.overflowed()
+            np.testing.assert_array_equal(fp.out[0].cpu().numpy(), ref.indices, err_msg="spilled rows")
+            oi, _, oc = O.rf_ball_query(ref.excl, r, ref.indices, 16)
+            np.testing.assert_array_equal(grp[2][0].cpu().numpy().astype(np.int64), oc)
+            continue
+        assert fp.csr.overflowed()
+        out = fp.out[0].cpu().numpy()
+        assert np.all(out[fp.k0:] == -1) and int(fp.entered[0].item()) == -1
+        assert int(fp.reached[0].item()) == n
+        cnt = grp[2][0].cpu().numpy()
+        assert np.all(cnt == -1)
+        assert fp.check() is True  # grow + re-run + re-capture
+        assert fp.graph is not None and not fp.csr.overflowed()
+        np.testing.assert_array_equal(fp.out[0].cpu().numpy(), ref.indices, err_msg="after check()")
+        fp.set_rng([9])
+        fp.out.fill_(-7)
+        fp.sample()  # the re-captured graph
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(fp.out[0].cpu().numpy(), ref.indices, err_msg="re-captured graph")
+
+
+def test_ball_query_rf_rejects_k_beyond_128():
+    fp = gpu_mdps(generate_cloud("uniform-box", 2000, 3), 500, exponent=0.4, extra_radii=(0.2,))
+    with pytest.raises(ValueError, match=r"k must be in \[1, 128\]"):
+        fp.group_rf(0.2, 200)
+    gi, gd, gc = fp.group_rf(0.2, 128)  # the bound itself: dense rows, exact vs oracle
+    ref = O.mdps(generate_cloud("uniform-box", 2000, 3), 500, exponent=0.4, rng_seed=0, extra_radii=(0.2,))
+    oi, od, oc = O.rf_ball_query(ref.excl, 0.2, ref.indices, 128)
+    assert int(oc.max()) > 64
+    np.testing.assert_array_equal(gc[0].cpu().numpy().astype(np.int64), oc)
+    np.testing.assert_array_equal(gi[0].cpu().numpy().astype(np.int64), oi)
+
+
+@pytest.mark.timeout(300)
+def test_virtual_split_graph_replay_changing_inputs():
+    """ps_fps on a cloud beyond one cluster runs the virtual-rank point split;
+    captured in a CUDA graph and replayed on changing points, every replay
+    gets fresh mailbox tags (device-side epoch) and matches the oracle."""
+    N, n = 300000, 400
+    clouds = [generate_cloud(f, N, 8) for f in ("room-surfaces", "uniform-box", "gaussian-clusters")]
+    x = engine.as_xyz4(torch.from_numpy(clouds[0][None]).cuda())
+    md = torch.empty(1, N, dtype=torch.float64, device="cuda")
+    taken = torch.empty(1, N, dtype=torch.uint8, device="cuda")
+    out = torch.full((1, n), -1, dtype=torch.int64, device="cuda")
+    curve = torch.full((1, n), np.inf, dtype=torch.float64, device="cuda")
+    from paper_2507_23480_b200 import _lib
+
+    def run():
+        _lib.call("ps_fps", x.data_ptr(), 1, N, md.data_ptr(), taken.data_ptr(), out.data_ptr(), curve.data_ptr(),
+                  n, n, 5, None, torch.cuda.current_stream().cuda_stream)
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        run()
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        run()
+    for rep in range(2):
+        for c in clouds[1:] + clouds[:1]:
+            x[0, :, :3].copy_(torch.from_numpy(c))
+            out.fill_(-7)
+            g.replay()
+            torch.cuda.synchronize()
+            ri, rc, *_ = O.fps(c, n, 5)
+            np.testing.assert_array_equal(out[0].cpu().numpy(), ri, err_msg=f"replay {rep}")
+            np.testing.assert_array_equal(curve[0].cpu().numpy(), rc)
 
 
 # ---- K4 grouping and K6 quality ------------------------------------------------------
@@ -733,17 +860,15 @@ def test_mlp_estimator_thresholds_and_sampling_match_oracle():
 
 
 @pytest.mark.timeout(600)
-@pytest.mark.parametrize("variant", ["global-workspace", "v3", "many-levels", "many-small-clouds", "exhausting"])
+@pytest.mark.parametrize("variant", ["global-workspace", "many-levels", "many-small-clouds", "exhausting"])
 def test_sampler_variants_match_oracle(variant, monkeypatch):
     """Sampler code paths beyond the default: the global-memory mode of v4,
-    the per-segment v3 kernels, 12 segments + 3 baked radii (L = 15 levels),
+    12 segments + 3 baked radii (L = 15 levels),
     a batch of many single-CTA clouds (block barriers), and tight radii that
     exhaust segment pools (entered / exhausted bookkeeping)."""
     B, N, n, nseg, extra, family, e = 3, 6000, 1500, 6, (0.1,), "room-surfaces", 0.45
     if variant == "global-workspace":
         monkeypatch.setenv("PS_SAMPLER_GLOBAL", "1")
-    elif variant == "v3":
-        monkeypatch.setenv("PS_SAMPLER", "3")
     elif variant == "many-levels":
         nseg, extra = 12, (0.05, 0.1, 0.2)
     elif variant == "many-small-clouds":
