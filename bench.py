@@ -313,6 +313,8 @@ class Chain:
     def capture(self):
         import torch
 
+        from paper_2507_23480_b200 import _lib
+
         s = self.stream
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
@@ -321,8 +323,10 @@ class Chain:
         torch.cuda.synchronize()
         self.fp.check()
         g = torch.cuda.CUDAGraph()
+        k0 = _lib.launch_count()
         with torch.cuda.graph(g, stream=s):
             self.body()
+        self.kernels = _lib.launch_count() - k0  # our kernels per replay (ps_launch_count)
         self.graph = g
 
 
@@ -423,7 +427,10 @@ def main_ours(args):
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         t_ms = run_chains(chains, args.steps, feed_dev)
-    launches = (_lib.launch_count() - launches0)
+    # eager calls count themselves; each graph replay launches the kernels its
+    # capture counted
+    launches = (_lib.launch_count() - launches0) + sum(
+        chains[s % S].kernels for s in range(args.steps))
     t_ms = max_over_ranks(t_ms, dev)
     value = ws * B * n_SAMPLES * args.steps / (t_ms / 1e3)
     # one chain alone (no cross-step overlap), same loop
@@ -799,6 +806,26 @@ def bench_c5_fastpoint(dev, reps=3):
     body()
     torch.cuda.synchronize()
     fp.check()
+    # stage breakdown (one eager run, events on the launching stream)
+    st = torch.cuda.current_stream()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
+    fp.state.copy_(seed)
+    ev[0].record(st)
+    fp._prefix()
+    ev[1].record(st)
+    fp._thresholds()
+    ev[2].record(st)
+    fp._exclusion()
+    ev[3].record(st)
+    fp._sampler()
+    ev[4].record(st)
+    fp._early_termination()
+    ev[5].record(st)
+    fp.group_rf(C5_RADIUS, K, out=grp)
+    ev[6].record(st)
+    torch.cuda.synchronize()
+    stage_ms = {nm: ev[i].elapsed_time(ev[i + 1]) for i, nm in enumerate(
+        ["fps_prefix", "thresholds", "excl_build", "sampler", "early_term", "rf_ball_query"])}
     s = torch.cuda.Stream(device=dev)
     s.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(s):
@@ -831,7 +858,7 @@ def bench_c5_fastpoint(dev, reps=3):
     fps_ms, bq_ms = e0.elapsed_time(e1), e1.elapsed_time(e2)
     return {"workload": "C5 FastPoint: 1 cloud N=2^20 uniform-box -> n=65536, p=0.1, nseg=6, power estimator "
                         f"(e={C5_EXPONENT}), rf ball query r={C5_RADIUS} k={K}; one GPU",
-            "ms": ms, "sampled_pts_per_s": C5_n / (ms / 1e3), "reached": reached,
+            "ms": ms, "stage_ms": stage_ms, "sampled_pts_per_s": C5_n / (ms / 1e3), "reached": reached,
             "early_term_frac": (C5_n - reached) / C5_n, "entries": int(fp.csr.counts[0].amax(dim=0).sum().item()),
             "exact_fps_ms": fps_ms, "ball_query_naive_ms": bq_ms,
             "speedup_vs_exact_fps": (fps_ms + bq_ms) / ms, "speedup_vs_exact_fps_kernel_only": fps_ms / ms,

@@ -96,6 +96,16 @@ PS_API int ps_fps_split_plan(int64_t N, int64_t B, int32_t G, int32_t Gl, int32_
 PS_API int ps_fps_split(const float* xyz4, int64_t B, int64_t N, double* md, uint8_t* taken, int64_t* out_idx,
                         double* curve, int64_t ld_out, int64_t k_stop, int64_t seed, int32_t G, int32_t g_base,
                         int32_t Gl, void* const* mbox_dev, uint32_t seq_base, int32_t all_write, void* stream);
+/* fps_loop (_kernels.py:35-74) resumed from a partial state over the same
+ * point split: iterations [k_start, n_total) (k_start_dev: per-cloud int64
+ * device values, e.g. the sampler's reached counts) continue from md/taken
+ * (valid on the launching ranks' shards) and out_idx/curve[0 .. k_start)
+ * (replicated); the early-termination tail of FastPoint at C5.  Tags as
+ * ps_fps_split: seq_base + iteration, unique per mailbox use. */
+PS_API int ps_fps_split_loop(const float* xyz4, int64_t B, int64_t N, double* md, uint8_t* taken,
+                             int64_t* out_idx, double* curve, int64_t ld_out, int64_t k_start,
+                             const int64_t* k_start_dev, int64_t n_total, int32_t G, int32_t g_base, int32_t Gl,
+                             void* const* mbox_dev, uint32_t seq_base, int32_t all_write, void* stream);
 /* CUDA IPC for the mailboxes of one-process-per-GPU ranks: 64-byte handle of
  * a device allocation, opened in a peer process (peer access enabled).  The
  * handle describes a whole cudaMalloc allocation and opens at its base, so

@@ -62,6 +62,8 @@ _SIGS = {
     "ps_fps_split_plan": (_c_i32, [_c_i64, _c_i64, _c_i32, _c_i32, _p, _p]),
     "ps_fps_split": (_c_i32, [_p, _c_i64, _c_i64, _p, _p, _p, _p, _c_i64, _c_i64, _c_i64, _c_i32, _c_i32, _c_i32,
                               _p, ctypes.c_uint32, _c_i32, _p]),
+    "ps_fps_split_loop": (_c_i32, [_p, _c_i64, _c_i64, _p, _p, _p, _p, _c_i64, _c_i64, _p, _c_i64, _c_i32, _c_i32,
+                                   _c_i32, _p, ctypes.c_uint32, _c_i32, _p]),
     "ps_gather_xyz4": (_c_i32, [_p, _p, _c_i64, _c_i64, _c_i64, _c_i64, _p, _p]),
     "ps_device_alloc": (_c_i32, [_c_i64, _c_i32, _p]),
     "ps_device_free": (_c_i32, [_p]),

@@ -184,6 +184,34 @@ int ps_fps_split(const float* xyz4, int64_t B, int64_t N, double* md, uint8_t* t
     return cuda_status(ps::launch_fps_res(a, rk, B, C, P, S(stream)), "fps_split", 1);
 }
 
+int ps_fps_split_loop(const float* xyz4, int64_t B, int64_t N, double* md, uint8_t* taken, int64_t* out_idx,
+                      double* curve, int64_t ld_out, int64_t k_start, const int64_t* k_start_dev, int64_t n_total,
+                      int32_t G, int32_t g_base, int32_t Gl, void* const* mbox_dev, uint32_t seq_base,
+                      int32_t all_write, void* stream) {
+    CHECK_ARG(B >= 1 && N >= 1 && N <= kMaxN, "invalid batch shape B=%lld N=%lld", (long long)B, (long long)N);
+    CHECK_ARG(n_total >= 1 && n_total <= ld_out && n_total <= N, "n_total %lld out of range", (long long)n_total);
+    CHECK_ARG(k_start_dev || k_start >= 1, "k_start must be >= 1");
+    CHECK_ARG(G >= 1 && G <= ps::kMaxRanks && Gl >= 1 && g_base >= 0 && g_base + Gl <= G,
+              "invalid ranks G=%d g_base=%d Gl=%d (G <= %d: one warp lane per rank)", G, g_base, Gl, ps::kMaxRanks);
+    CHECK_ARG(G == 1 || mbox_dev != nullptr, "mailbox pointer array required for G > 1");
+    CHECK_ARG((uint64_t)seq_base + (uint64_t)n_total < 0xffffffffull, "sequence space exhausted; reset the mailboxes");
+    CHECK_ARG(xyz4 && md && taken && out_idx && curve, "null pointer");
+    int C = 0, P = 0;
+    if (!ps::fps_res_plan(N, B * Gl, G, &C, &P))
+        return fail(PS_ERR_UNSUPPORTED, "no co-resident cluster plan for N=%lld over %d ranks (%d per launch)",
+                    (long long)N, G, Gl);
+    ps::FpsArgs a = {};
+    a.xyz = reinterpret_cast<const float4*>(xyz4);
+    a.md = md; a.taken = taken; a.out_idx = out_idx; a.curve = curve;
+    a.k_start_dev = k_start_dev;
+    a.N = N; a.ld_out = ld_out; a.k_start = k_start; a.k_stop = n_total; a.seed = 0; a.fresh = 0;
+    ps::FpsRanks rk = {};
+    rk.G = G; rk.Gl = Gl; rk.g_base = g_base; rk.all_write = all_write; rk.seq_base = seq_base;
+    rk.mbox = reinterpret_cast<uint4* const*>(mbox_dev);
+    rk.timeout_ns = ps::split_timeout_ns();
+    return cuda_status(ps::launch_fps_res(a, rk, B, C, P, S(stream)), "fps_split_loop", 1);
+}
+
 int ps_device_alloc(int64_t bytes, int32_t fill_byte, void** dev_ptr_out) {
     CHECK_ARG(bytes > 0 && dev_ptr_out, "invalid allocation request");
     void* p = nullptr;

@@ -857,16 +857,18 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) grid_rows_kernel(int64_t B,
 // stride move to the cloud's spill arena (ell_row_stride); only a full arena
 // sets status bit 1 (the sampler and the queries then emit error states and
 // the host rebuilds with a larger capacity).
-constexpr int kEllWarps = 8;
-constexpr int kEllCap = 256;   // per-warp staging (rows above it: overflow)
-
-__global__ void __launch_bounds__(kEllWarps * 32, 4) grid_ell_kernel(int64_t B, int64_t N,
-                                                                     const double* __restrict__ r2_levels, int L,
-                                                                     int64_t levels_ld, int64_t stride, GridWork g,
-                                                                     ExclWork w, CsrView csr) {
+// Staging: kEllCap entries per warp in shared memory; rows beyond it take
+// the rescan path (one pass per bucket, straight to the row).  Two
+// instances: 8 warps x 256 entries for short rows (C1-C4), 4 warps x 512
+// for strides above 256 (C5-sized clouds, ~270 entries per row), so that
+// the rescan stays rare.
+template <int kEllWarps, int kEllCap>
+__global__ void __launch_bounds__(kEllWarps * 32, 1024 / (kEllWarps * 32)) grid_ell_kernel(
+    int64_t B, int64_t N, const double* __restrict__ r2_levels, int L, int64_t levels_ld, int64_t stride, GridWork g,
+    ExclWork w, CsrView csr) {
     __shared__ double hd[kEllWarps][kEllCap];
     __shared__ int32_t hj[kEllWarps][kEllCap];
-    __shared__ uint8_t hb[kEllWarps][kEllCap];   // rank within its bucket
+    __shared__ uint16_t hb[kEllWarps][kEllCap];  // rank within its bucket
     __shared__ uint8_t hk[kEllWarps][kEllCap];   // bucket
     __shared__ int hcnt[kEllWarps][33];          // per-bucket counts
     __shared__ double lvs[kEllWarps][32];
@@ -981,7 +983,7 @@ __global__ void __launch_bounds__(kEllWarps * 32, 4) grid_ell_kernel(int64_t B, 
                     }
                     hd[warp][slot] = d;
                     hj[warp][slot] = qi;
-                    hb[warp][slot] = (uint8_t)atomicAdd(&hcnt[warp][bk], 1);  // rank within bucket
+                    hb[warp][slot] = (uint16_t)atomicAdd(&hcnt[warp][bk], 1);  // rank within bucket
                     hk[warp][slot] = (uint8_t)bk;
                 }
             }
@@ -1135,10 +1137,17 @@ cudaError_t launch_excl_build(const float4* xyz, int64_t B, int64_t N, const dou
                                                              method == 2 ? 1 : 0);
         }
         if (method == 2) {
-            const int64_t gx = std::max<int64_t>(1, std::min<int64_t>((148 * 16 + B - 1) / B,
-                                                                      (N + kEllWarps - 1) / kEllWarps));
-            grid_ell_kernel<<<dim3((unsigned)gx, (unsigned)B), kEllWarps * 32, 0, s>>>(B, N, r2_levels, L, levels_ld,
-                                                                                     stride, g, w, csr);
+            if (stride <= 256) {
+                constexpr int kW = 8;
+                const int64_t gx = std::max<int64_t>(1, std::min<int64_t>((148 * 16 + B - 1) / B, (N + kW - 1) / kW));
+                grid_ell_kernel<kW, 256><<<dim3((unsigned)gx, (unsigned)B), kW * 32, 0, s>>>(
+                    B, N, r2_levels, L, levels_ld, stride, g, w, csr);
+            } else {
+                constexpr int kW = 4;
+                const int64_t gx = std::max<int64_t>(1, std::min<int64_t>((148 * 32 + B - 1) / B, (N + kW - 1) / kW));
+                grid_ell_kernel<kW, 512><<<dim3((unsigned)gx, (unsigned)B), kW * 32, 0, s>>>(
+                    B, N, r2_levels, L, levels_ld, stride, g, w, csr);
+            }
             return cudaGetLastError();
         }
         const dim3 gp((unsigned)((N + 255) / 256), (unsigned)B);

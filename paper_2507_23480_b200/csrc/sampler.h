@@ -49,6 +49,7 @@ struct SampArgs {
     long long* dbg;              // development timing (PS_SAMPLER_TIMING)
     int tiny;                    // v4, one CTA per cloud: the per-cloud arrays live in shared memory
     const int32_t* excl_status;  // [B] nullable: nonzero -> the cloud's rows are incomplete (error outputs)
+    int grid_c;                  // v4 grid mode: CTAs per cloud (0: cluster mode)
 };
 
 struct EtArgs {

@@ -46,11 +46,25 @@ constexpr uint8_t kPredOvf = 0xff;
 constexpr uint8_t kUnd4 = 0, kIn4 = 1, kOut4 = 2;
 constexpr int kScr = 64;  // int32 scratch per cloud
 constexpr int kMaxC4 = 16;
-// scratch slots
-constexpr int kCnt0 = 0;    // [16] per-CTA available counts (pool)
-constexpr int kCnt1 = 16;   // [16] per-CTA accepted counts (truncation)
-constexpr int kDecided = 32;
-constexpr int kLast = 33;
+// Grid mode (one or a few huge clouds, C4 / C5): the CTAs of a cloud are a
+// slice of one cooperative grid of up to kMaxCG CTAs instead of a cluster;
+// their barrier is a global arrive counter + generation word and the
+// per-round decided counts go through global slots.
+constexpr int kMaxCG = 160;
+// scratch slots: cluster mode in kScr ints, grid mode in kScrG ints
+template <bool kGrid>
+struct Scr {
+    enum : int {
+        cnt0 = 0,                               // per-CTA available counts (pool)
+        cnt1 = kGrid ? kMaxCG : 16,             // per-CTA accepted counts (truncation)
+        decided = kGrid ? 2 * kMaxCG : 32,
+        last = decided + 1,
+        dec = decided + 2,                      // grid: [2][kMaxCG] cumulative decided counts
+        bar = dec + 2 * kMaxCG,                 // grid: barrier {count, generation}
+        size = kGrid ? bar + 2 : kScr
+    };
+};
+constexpr int kScrG = Scr<true>::size;
 
 struct V4Work {
     uint8_t* avail;    // [B][N]
@@ -68,6 +82,7 @@ struct V4Work {
     int32_t* preds;    // [B][N][kPred4]
     uint8_t* npred;    // [B][N]
     int32_t* scr;      // [B][kScr]
+    int32_t* gscr;     // [B][kScrG] (grid mode)
 };
 
 PS_DEV uint64_t mix64_4(uint64_t z) {
@@ -178,19 +193,63 @@ PS_DEV void sync_all(int C) {
     else cluster_sync_all();
 }
 
+// Grid mode: barrier of the C co-resident CTAs of one cloud (cooperative
+// launch) -- arrive on a global counter, the last arrival resets it and
+// bumps the generation.  The gpu-scope fence before the arrival publishes
+// the CTA's writes (cumulative over the preceding block barrier); the
+// acquire load of the generation orders the reads after it.
+PS_DEV void group_sync(int32_t* barw, int C) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned* cnt = reinterpret_cast<unsigned*>(barw);
+        unsigned* gen = reinterpret_cast<unsigned*>(barw + 1);
+        unsigned g0;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g0) : "l"(gen) : "memory");
+        __threadfence();
+        if (atomicAdd(cnt, 1u) == (unsigned)C - 1u) {
+            *reinterpret_cast<volatile unsigned*>(cnt) = 0u;
+            __threadfence();
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(gen), "r"(g0 + 1u) : "memory");
+        } else {
+            unsigned g;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(gen) : "memory");
+            } while (g == g0);
+        }
+    }
+    __syncthreads();
+}
+
+// prefix (over CTAs c < r) and total of per-CTA values v[0..C) in global
+// scratch, with one block scan (grid mode: C up to kMaxCG)
+PS_DEV void group_prefix(const int32_t* v, int C, int r, int* wt, int* s_tmp, int* off, int* tot) {
+    const int tid = threadIdx.x;
+    const int x = tid < C ? *reinterpret_cast<const volatile int32_t*>(v + tid) : 0;
+    int t;
+    const int ex = bscan(x, wt, &t);
+    if (tid == r) *s_tmp = ex;
+    __syncthreads();
+    *off = *s_tmp;
+    *tot = t;
+    __syncthreads();
+}
+
 // kSm: the availability byte map and the rank table live in every CTA's
 // shared memory (N bytes + 4N bytes); the map is built by owner CTAs
 // (contiguous 16-byte-aligned index ranges, cleared through DSMEM stores)
 // and gathered by every CTA.  Otherwise both are global arrays.
-template <bool kSm>
+template <bool kSm, bool kGrid>
 __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
+    static_assert(!(kSm && kGrid), "grid mode keeps the per-cloud arrays in global memory");
+    using SL = Scr<kGrid>;
     __shared__ int wt[32];
     __shared__ int s_dec[2][kMaxC4];
+    __shared__ int s_tmp;
     extern __shared__ __align__(16) uint8_t dsm4[];
     const int tid = threadIdx.x;
-    const int C = (int)cluster_nctarank();
-    const int r = (int)cluster_ctarank();
-    const int64_t b = cluster_id_x();
+    const int C = kGrid ? a.grid_c : (int)cluster_nctarank();
+    const int r = kGrid ? (int)(blockIdx.x % (unsigned)a.grid_c) : (int)cluster_ctarank();
+    const int64_t b = kGrid ? (int64_t)(blockIdx.x / (unsigned)a.grid_c) : cluster_id_x();
     const int gt = r * kT4 + tid, GT = C * kT4;
     const int64_t N = a.N;
     const int nseg = a.nseg;
@@ -244,7 +303,11 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
     uint8_t* stt = w.st + b * N;
     int32_t* preds = w.preds + b * N * kPred4;
     uint8_t* npred = w.npred + b * N;
-    int32_t* scr = w.scr + b * kScr;
+    int32_t* scr = kGrid ? w.gscr + b * kScrG : w.scr + b * kScr;
+    auto sync_grp = [&]() {
+        if constexpr (kGrid) group_sync(scr + SL::bar, C);
+        else sync_all(C);
+    };
     if (kSm && a.tiny) {
         const int64_t Np = (N + 15) & ~(int64_t)15;
         const int64_t base0 = Np + 4 * Np + 4 * (((N + 31) / 32 + 3) & ~(int64_t)3) + 21 * Np;
@@ -302,7 +365,7 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
             if (!kSm) avail[j] = 1;
             head[j] = -1;
         }
-        if (gt == 0) scr[kDecided] = 0;
+        if (gt == 0) scr[SL::decided] = 0;
         if (kSm) {
             VT4(16);
             // this visit's level counts and row offsets of my range, staged once (P2)
@@ -377,7 +440,7 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
             }
             i_tk = i;
         }
-        sync_all(C);
+        sync_grp();
         VT4(13);
         if (!kSm) {
             for (int64_t x = gt; x < i; x += GT) {
@@ -398,10 +461,10 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
                 avail[q] = 0;
             }
         }
-        sync_all(C);
+        sync_grp();
         if (kSm) {
             for (int64_t j = jlo + tid; j < jhi; j += kT4) avail[j] = (uint32_t)wpos[j - jlo] <= (uint32_t)seg ? 1 : 0;
-            sync_all(C);
+            sync_grp();
             const uint32_t avail_base = smem_u32(avail);
             // gather the other owners' ranges into my copy of the map
             for (int64_t c16 = tid; c16 < Npad / 16; c16 += kT4) {
@@ -462,14 +525,18 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
             }
         }
         mycnt = bsum(mycnt, wt);
-        if (tid == 0) scr[kCnt0 + r] = mycnt;
-        sync_all(C);
+        if (tid == 0) scr[SL::cnt0 + r] = mycnt;
+        sync_grp();
         VT4(1);
         int off = 0, L = 0;
-        for (int c2 = 0; c2 < C; ++c2) {
-            const int v = scr[kCnt0 + c2];
-            off += c2 < r ? v : 0;
-            L += v;
+        if constexpr (kGrid) {
+            group_prefix(scr + SL::cnt0, C, r, wt, &s_tmp, &off, &L);
+        } else {
+            for (int c2 = 0; c2 < C; ++c2) {
+                const int v = scr[SL::cnt0 + c2];
+                off += c2 < r ? v : 0;
+                L += v;
+            }
         }
         {
             // one block scan: each thread takes a contiguous run of my range
@@ -490,7 +557,7 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
             }
             off += tot;
         }
-        sync_all(C);
+        sync_grp();
         VT4(2);
         if (tdbg) { s_acc[10] += 1; s_acc[11] += L; }
 
@@ -508,7 +575,7 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
                 pos[t] = p;
                 nxt[t] = atomicExch(&head[p], t);
             }
-            sync_all(C);
+            sync_grp();
             VT4(3);
             for (int t = gt; t < L; t += GT) {
                 // latest earlier writer of my position, and of my tail slot L-1-t
@@ -521,7 +588,7 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
                     if (x < t && x > bl) bl = x;
                 lw[t] = bl;
             }
-            sync_all(C);
+            sync_grp();
             VT4(4);
             for (int t = gt; t < L; t += GT) {
                 // value at pos[t] before draw t: untouched -> pool; else the value
@@ -547,7 +614,7 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
             if (kSm) st_s[t - tlo] = kUnd4;
             else stt[t] = kUnd4;
         }
-        sync_all(C);
+        sync_grp();
         if (kSm) {
             for (int t = tid; t < L; t += kT4) rank[cand[t]] = t;
             __syncthreads();
@@ -582,13 +649,24 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
         auto publish = [&](int add) {
             add = bsum(add, wt);
             my_dec += add;
-            if (tid < C) st_cluster_s32(mapa(dec_base + (uint32_t)(((round & 1) * kMaxC4 + r) * 4), (uint32_t)tid),
-                                         my_dec);
-            sync_all(C);
-            int tot = 0;
-            for (int q = 0; q < C; ++q) tot += s_dec[round & 1][q];
-            ++round;
-            return tot;
+            if constexpr (kGrid) {
+                // cumulative count into this round parity's global slot; a slot is
+                // rewritten two rounds later, after every CTA read it
+                if (tid == 0) scr[SL::dec + (round & 1) * kMaxCG + r] = my_dec;
+                sync_grp();
+                int o2, tot;
+                group_prefix(scr + SL::dec + (round & 1) * kMaxCG, C, r, wt, &s_tmp, &o2, &tot);
+                ++round;
+                return tot;
+            } else {
+                if (tid < C)
+                    st_cluster_s32(mapa(dec_base + (uint32_t)(((round & 1) * kMaxC4 + r) * 4), (uint32_t)tid), my_dec);
+                sync_grp();
+                int tot = 0;
+                for (int q = 0; q < C; ++q) tot += s_dec[round & 1][q];
+                ++round;
+                return tot;
+            }
         };
         int decided = 0;
         for (int t = tlo + tid; t < thi; t += kT4) {
@@ -738,13 +816,17 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
         int nin = 0;
         for (int t = tlo + tid; t < thi; t += kT4) nin += st_get(t) == kIn4 ? 1 : 0;
         nin = bsum(nin, wt);
-        if (tid == 0) scr[kCnt1 + r] = nin;
-        sync_all(C);
+        if (tid == 0) scr[SL::cnt1 + r] = nin;
+        sync_grp();
         int aoff = 0, A = 0;
-        for (int c2 = 0; c2 < C; ++c2) {
-            const int v = scr[kCnt1 + c2];
-            aoff += c2 < r ? v : 0;
-            A += v;
+        if constexpr (kGrid) {
+            group_prefix(scr + SL::cnt1, C, r, wt, &s_tmp, &aoff, &A);
+        } else {
+            for (int c2 = 0; c2 < C; ++c2) {
+                const int v = scr[SL::cnt1 + c2];
+                aoff += c2 < r ? v : 0;
+                A += v;
+            }
         }
         const int64_t take = (int64_t)A < need ? (int64_t)A : need;
         const bool ends = take == need;
@@ -756,13 +838,13 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
             const int64_t k = aoff + ex;
             if (f && k < take) {
                 out[i + k] = cand[t];
-                if (ends && k == take - 1) scr[kLast] = t;
+                if (ends && k == take - 1) scr[SL::last] = t;
             }
             aoff += tot;
         }
-        sync_all(C);
+        sync_grp();
         VT4(8);
-        const int last = ends ? scr[kLast] : -1;
+        const int last = ends ? scr[SL::last] : -1;
         prev_seg = seg;
         i += take;
         if (ends) {
@@ -813,6 +895,7 @@ size_t sampler_v4_ws_bytes(int64_t B, int64_t N) {
     s += align256_4(sizeof(uint8_t) * B * N) * 3;        // adjcnt st npred
     s += align256_4(sizeof(int32_t) * B * N * kPred4);   // preds
     s += align256_4(sizeof(int32_t) * B * kScr);         // scr
+    s += align256_4(sizeof(int32_t) * B * kScrG);        // gscr
     return s;
 }
 
@@ -845,8 +928,10 @@ cudaError_t launch_sampler_v4(SampArgs a, int64_t B, cudaStream_t s) {
     w.st = p; p += align256_4(sizeof(uint8_t) * B * N);
     w.npred = p; p += align256_4(sizeof(uint8_t) * B * N);
     w.preds = reinterpret_cast<int32_t*>(p); p += align256_4(sizeof(int32_t) * B * N * kPred4);
-    w.scr = reinterpret_cast<int32_t*>(p);
+    w.scr = reinterpret_cast<int32_t*>(p); p += align256_4(sizeof(int32_t) * B * kScr);
+    w.gscr = reinterpret_cast<int32_t*>(p);
     a.B = B;
+    a.grid_c = 0;
     const int C = v4_cluster(N, B);
     cudaError_t e = cudaSuccess;
     const int64_t Npad = (N + 15) & ~(int64_t)15;
@@ -857,7 +942,35 @@ cudaError_t launch_sampler_v4(SampArgs a, int64_t B, cudaStream_t s) {
     const size_t dsm_tiny = ((dsm + 15) & ~(size_t)15) + 7 * 4 * (size_t)Npad + 4 * kScr;
     a.tiny = (sm && C == 1 && dsm_tiny <= 200 * 1024 && !getenv("PS_SAMPLER_NOTINY")) ? 1 : 0;
     const size_t dsm_used = a.tiny ? dsm_tiny : dsm;
-    auto kern = sm ? samp4_kernel<true> : samp4_kernel<false>;
+    if (!sm && !getenv("PS_SAMPLER_NOGRID")) {
+        // grid mode: few clouds too large for shared memory -- spread each over
+        // (SMs / B) co-resident CTAs instead of one cluster of <= 8
+        int dev = 0, nsm = 0, occ = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, samp4_kernel<false, true>, kT4, 0);
+        const int64_t per = (int64_t)nsm * (occ > 0 ? occ : 1) / B;
+        const char* ge = getenv("PS_SAMPLER_GRID_CTAS");
+        int64_t cg = ge ? atoi(ge) : std::min<int64_t>(per, std::min<int64_t>(kMaxCG, (N + 2047) / 2048));
+        cg = std::min<int64_t>(cg, std::min<int64_t>(per, kMaxCG));
+        if (cg > 2 * C) a.grid_c = (int)cg;
+    }
+    if (a.grid_c > 0) {
+        cudaError_t e2 = cudaMemsetAsync(w.gscr, 0, sizeof(int32_t) * B * kScrG, s);  // barrier words
+        if (e2 != cudaSuccess) return e2;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(B * a.grid_c), 1, 1);
+        cfg.blockDim = dim3(kT4, 1, 1);
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident: the group barrier spins
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        a.dbg = nullptr;
+        return cudaLaunchKernelEx(&cfg, samp4_kernel<false, true>, a, w);
+    }
+    auto kern = sm ? samp4_kernel<true, false> : samp4_kernel<false, false>;
     if (sm) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm_used);
         if (e != cudaSuccess) return e;

@@ -860,15 +860,23 @@ def test_mlp_estimator_thresholds_and_sampling_match_oracle():
 
 
 @pytest.mark.timeout(600)
-@pytest.mark.parametrize("variant", ["global-workspace", "many-levels", "many-small-clouds", "exhausting"])
+@pytest.mark.parametrize("variant", ["global-workspace", "grid-mode", "grid-mode-lattice", "many-levels",
+                                     "many-small-clouds", "exhausting"])
 def test_sampler_variants_match_oracle(variant, monkeypatch):
-    """Sampler code paths beyond the default: the global-memory mode of v4,
-    12 segments + 3 baked radii (L = 15 levels),
+    """Sampler code paths beyond the default: the global-memory mode of v4
+    (one cluster per cloud, and the grid mode: a cooperative grid slice per
+    cloud with a global barrier), 12 segments + 3 baked radii (L = 15 levels),
     a batch of many single-CTA clouds (block barriers), and tight radii that
     exhaust segment pools (entered / exhausted bookkeeping)."""
     B, N, n, nseg, extra, family, e = 3, 6000, 1500, 6, (0.1,), "room-surfaces", 0.45
     if variant == "global-workspace":
         monkeypatch.setenv("PS_SAMPLER_GLOBAL", "1")
+        monkeypatch.setenv("PS_SAMPLER_NOGRID", "1")
+    elif variant.startswith("grid-mode"):  # cooperative grid of 12 CTAs per cloud, global barrier
+        monkeypatch.setenv("PS_SAMPLER_GLOBAL", "1")
+        monkeypatch.setenv("PS_SAMPLER_GRID_CTAS", "12")
+        if variant.endswith("lattice"):
+            family, e = "lattice", 0.9
     elif variant == "many-levels":
         nseg, extra = 12, (0.05, 0.1, 0.2)
     elif variant == "many-small-clouds":
