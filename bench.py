@@ -891,10 +891,32 @@ def bench_c5_split(dev, ws):
     ok = int(torch.unique(idx).numel()) == C5_n
     dist.barrier()
     ps.close()
+    # C5 FastPoint over the same ranks (pointsplit.PointSplitFastPoint: split
+    # prefix + tail, row-sharded build, rows to rank 0 for the sampler,
+    # centroid-sharded grouping); host-timed collectives included
+    mp = pointsplit.PointSplitFastPoint(C5_N, C5_n, exponent=C5_EXPONENT, extra_radii=(C5_RADIUS,), device=dev)
+    mp.run(x, 0, K, C5_RADIUS)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0.record()
+    fidx, _ = mp.run(x, 0, K, C5_RADIUS)
+    e1.record()
+    torch.cuda.synchronize()
+    fms = max_over_ranks(e0.elapsed_time(e1), dev)
+    import hashlib
+
+    try:
+        dig = json.load(open(os.path.join(REPO, "tests", "golden", "c5_digest.json")))["fastpoint"]["idx_sha256"]
+    except (OSError, ValueError, KeyError):
+        dig = None
+    got = hashlib.sha256(fidx.cpu().numpy().astype(np.int64).tobytes()).hexdigest()
+    mp.close()
     return {"workload": "C5: 1 cloud N=2^20 uniform-box -> n=65536 exact FPS, point split", "ranks": ws,
             "mode": "one process per GPU, CUDA-IPC mailboxes over NVLink", "ms": ms,
             "us_per_iter": 1e3 * ms / (C5_n - 1), "sampled_pts_per_s": C5_n / (ms / 1e3),
-            "checks": "distinct indices" if ok else "FAILED property checks"}
+            "checks": "distinct indices" if ok else "FAILED property checks",
+            "fastpoint_ms": fms, "fastpoint_sampled_pts_per_s": C5_n / (fms / 1e3),
+            "fastpoint_matches_oracle_digest": (got == dig) if dig else None}
 
 
 def main():

@@ -163,6 +163,18 @@ PS_API int ps_excl_build(const float* xyz4, int64_t B, int64_t N, const double* 
                   int64_t cap_entries, void* work, int64_t cap_edges, int32_t* status,
                   int32_t method, void* stream);
 
+/* One rank's share of the method-2 build for a point split (MDPS
+ * at C5): every point is a candidate, but only rows [row_lo, row_hi) are
+ * written (their indptr, entries and counts) and rows longer than the
+ * stride take spill entries [spill_lo, spill_hi) of the arena (offsets past
+ * N * ps_excl_row_stride(N, cap_entries)), so G ranks with disjoint ranges
+ * fill one CSR without coordination.  work: ps_excl_workspace_bytes(B, N, 1,
+ * 2) bytes per rank; status as ps_excl_build. */
+PS_API int ps_excl_build_shard(const float* xyz4, int64_t B, int64_t N, const double* r2_levels, int32_t L,
+                               int64_t levels_ld, int64_t row_lo, int64_t row_hi, int64_t spill_lo,
+                               int64_t spill_hi, int64_t* indptr, int32_t* nbr, double* d2, int32_t* counts,
+                               int64_t cap_entries, void* work, int32_t* status, void* stream);
+
 /* csr_fill (_kernels.py:164-185): scatter the M undirected edges (ei, ej
  * int32, ed float64; excl_collect's emission order) into both rows of a CSR
  * whose indptr (int64[N+1]) counts self + degree per row: row r = r (d2 0),
@@ -245,6 +257,16 @@ PS_API int ps_early_termination_prepare(const int64_t* indptr, const int32_t* nb
                                  int64_t counts_stride, uint8_t* taken, double* md,
                                  const int64_t* out_idx, int64_t ld_out, const int64_t* reached,
                                  int64_t n_total, int64_t B, int64_t N, void* stream);
+
+/* early_termination seeding for one rank of a point split: taken = the
+ * first reached[b] samples (all N points), md = +inf and the level-1 row
+ * pull of earlyterm_scan (_kernels.py:356-367) for the rank's points
+ * [lo, hi) only -- the rows it built.  Continue with ps_fps_split_loop. */
+PS_API int ps_early_termination_shard(const int64_t* indptr, const int32_t* nbr, const double* d2,
+                                      int64_t cap_entries, const int32_t* lvl1_counts, int64_t counts_stride,
+                                      uint8_t* taken, double* md, const int64_t* out_idx, int64_t ld_out,
+                                      const int64_t* reached, int64_t n_total, int64_t B, int64_t N, int64_t lo,
+                                      int64_t hi, void* stream);
 
 /* ---- K4: grouping ---------------------------------------------------------
  * Outputs idx int32[B][n][k] (-1 padded), dist float64[B][n][k] (sqrt(d2),

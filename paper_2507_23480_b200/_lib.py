@@ -36,6 +36,10 @@ _SIGS = {
     "ps_excl_row_stride": (_c_i64, [_c_i64, _c_i64]),
     "ps_excl_build": (_c_i32, [_p, _c_i64, _c_i64, _p, _c_i32, _c_i64, _p, _p, _p, _p, _c_i64, _p, _c_i64, _p, _c_i32,
                                _p]),
+    "ps_excl_build_shard": (_c_i32, [_p, _c_i64, _c_i64, _p, _c_i32, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _p, _p,
+                                     _p, _p, _c_i64, _p, _p, _p]),
+    "ps_early_termination_shard": (_c_i32, [_p, _p, _p, _c_i64, _p, _c_i64, _p, _p, _p, _c_i64, _p, _c_i64, _c_i64,
+                                            _c_i64, _c_i64, _c_i64, _p]),
     "ps_csr_fill_workspace_bytes": (_c_i64, [_c_i64, _c_i64]),
     "ps_csr_fill": (_c_i32, [_p, _p, _p, _c_i64, _p, _c_i64, _p, _p, _p, _c_i64, _p]),
     "ps_csr_sort_rows": (_c_i32, [_p, _p, _p, _c_i64, _c_i64, _c_i64, _p, _p]),

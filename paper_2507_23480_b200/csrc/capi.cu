@@ -502,6 +502,58 @@ int ps_early_termination_prepare(const int64_t* indptr, const int32_t* nbr, cons
     return cuda_status(ps::launch_et(a, S(stream)), "early_termination_prepare", ps::et_launches());
 }
 
+int ps_early_termination_shard(const int64_t* indptr, const int32_t* nbr, const double* d2, int64_t cap_entries,
+                               const int32_t* lvl1_counts, int64_t counts_stride, uint8_t* taken, double* md,
+                               const int64_t* out_idx, int64_t ld_out, const int64_t* reached, int64_t n_total,
+                               int64_t B, int64_t N, int64_t lo, int64_t hi, void* stream) {
+    CHECK_ARG(B >= 1 && N >= 1, "invalid shape");
+    CHECK_ARG(0 <= lo && lo < hi && hi <= N, "invalid point range [%lld, %lld)", (long long)lo, (long long)hi);
+    CHECK_ARG(indptr && nbr && d2 && lvl1_counts && taken && md && out_idx && reached, "null pointer");
+    ps::EtArgs a = {};
+    a.indptr = indptr; a.nbr = nbr; a.d2 = d2; a.cap_entries = cap_entries; a.lvl1_counts = lvl1_counts;
+    a.counts_stride = counts_stride; a.taken = taken; a.md = md; a.out_idx = out_idx; a.ld_out = ld_out;
+    a.reached = reached; a.n_total = n_total; a.B = B; a.N = N;
+    return cuda_status(ps::launch_et_shard(a, lo, hi, S(stream)), "early_termination_shard", 3);
+}
+
+int ps_excl_build_shard(const float* xyz4, int64_t B, int64_t N, const double* r2_levels, int32_t L, int64_t levels_ld,
+                        int64_t row_lo, int64_t row_hi, int64_t spill_lo, int64_t spill_hi, int64_t* indptr,
+                        int32_t* nbr, double* d2, int32_t* counts, int64_t cap_entries, void* work, int32_t* status,
+                        void* stream) {
+    CHECK_ARG(B >= 1 && N >= 1 && N <= kMaxN, "invalid batch shape");
+    CHECK_ARG(L >= 1 && L <= levels_ld && L <= 32, "invalid level count %d (1..32)", L);
+    CHECK_ARG(cap_entries >= N && cap_entries < ((int64_t)1 << 31), "cap_entries must be in [N, 2^31)");
+    const int64_t stride = ps::ell_row_stride(cap_entries, N);
+    CHECK_ARG(stride <= 65535, "row stride too large");
+    CHECK_ARG(0 <= row_lo && row_lo < row_hi && row_hi <= N, "invalid row range [%lld, %lld)", (long long)row_lo,
+              (long long)row_hi);
+    CHECK_ARG(0 <= spill_lo && spill_lo < spill_hi && spill_hi <= cap_entries - N * stride,
+              "spill range must lie in [0, %lld)", (long long)(cap_entries - N * stride));
+    CHECK_ARG(work && status && indptr && nbr && d2 && counts, "null pointer");
+    unsigned char* w = static_cast<unsigned char*>(work);
+    ps::ExclWork ew = {};
+    ps::GridWork gw = {};
+    ew.cap_edges = 1;
+    const int64_t mc = grid_max_cells(N);
+    gw.max_cells = (int)mc;
+    gw.params = reinterpret_cast<ps::GridParams*>(w); w += align_up(sizeof(ps::GridParams) * B);
+    gw.cell_start = reinterpret_cast<int*>(w); w += align_up(sizeof(int) * B * (mc + 1));
+    gw.cursor = reinterpret_cast<int*>(w); w += align_up(sizeof(int) * B * mc);
+    gw.cell_of = reinterpret_cast<int32_t*>(w); w += align_up(sizeof(int32_t) * B * N);
+    gw.sorted_idx = reinterpret_cast<int32_t*>(w); w += align_up(sizeof(int32_t) * B * N);
+    gw.sorted_xyz = reinterpret_cast<float4*>(w); w += align_up(sizeof(float4) * B * N);
+    gw.evals = reinterpret_cast<unsigned long long*>(w); w += align_up(sizeof(unsigned long long) * B);
+    ew.spill = reinterpret_cast<unsigned long long*>(w); w += align_up(sizeof(unsigned long long) * B);
+    ew.deg = reinterpret_cast<int32_t*>(w); w += align_up(sizeof(int32_t) * B * N);
+    ew.long_rows = reinterpret_cast<int32_t*>(w); w += align_up(sizeof(int32_t) * B * N);
+    ew.long_count = reinterpret_cast<unsigned*>(w);
+    ew.status = status;
+    ps::CsrView csr = {indptr, nbr, d2, counts, cap_entries, N, L, row_lo, row_hi, spill_lo, spill_hi};
+    return cuda_status(ps::launch_excl_build(reinterpret_cast<const float4*>(xyz4), B, N, r2_levels, L, levels_ld,
+                                             csr, ew, gw, 2, S(stream)),
+                       "excl_build_shard", ps::excl_build_launches(N, 2));
+}
+
 int ps_ball_query_rf(const int64_t* indptr, const int32_t* nbr, const double* d2, int64_t cap_entries,
                      const int32_t* counts, int32_t L, int32_t level, const int64_t* centroids, int64_t cent_ld,
                      int64_t B, int64_t N, int64_t n, int32_t k, int32_t* idx_out, double* dist_out, int32_t* cnt_out,

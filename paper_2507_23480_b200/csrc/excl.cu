@@ -305,8 +305,8 @@ __global__ void grid_assign_kernel(const float4* __restrict__ xyz, int64_t B, in
         const int64_t b = t / N;
         if (write_indptr) {
             const int64_t i = t - b * N;
-            csr.indptr[b * (N + 1) + i] = i * stride;
-            if (i == N - 1) csr.indptr[b * (N + 1) + N] = N * stride;
+            if (i >= csr.row_lo && i < csr.row_hi) csr.indptr[b * (N + 1) + i] = i * stride;
+            if (i == N - 1 && csr.row_hi == N) csr.indptr[b * (N + 1) + N] = N * stride;
         }
         const GridParams gp = g.params[b];
         const float4 p = xyz[t];
@@ -509,7 +509,8 @@ __global__ void __launch_bounds__(1024) grid_build_kernel(const float4* __restri
     }
     // 5. method 2: fixed-stride row pointers
     if (write_indptr)
-        for (int64_t r = tid; r <= N; r += 1024) csr.indptr[b * (N + 1) + r] = r * stride;
+        for (int64_t r = csr.row_lo + tid; r <= csr.row_hi; r += 1024)
+            if (r < csr.row_hi || r == N) csr.indptr[b * (N + 1) + r] = r * stride;
 }
 
 // ---- row sort by (d2, index) + fused level counts -----------------------
@@ -911,6 +912,7 @@ __global__ void __launch_bounds__(kEllWarps * 32, 1024 / (kEllWarps * 32)) grid_
         __syncwarp();
         const float4 p = sx[s];
         const int32_t i = __float_as_int(p.w);  // original index (grid_scatter_kernel)
+        if (i < csr.row_lo || i >= csr.row_hi) continue;  // another rank's row (warp-uniform)
         const int cx = cell_coord(p.x, gp.ox, gp.inv_h, gp.nx);
         const int cy = cell_coord(p.y, gp.oy, gp.inv_h, gp.ny);
         const int cz = cell_coord(p.z, gp.oz, gp.inv_h, gp.nz);
@@ -999,8 +1001,8 @@ __global__ void __launch_bounds__(kEllWarps * 32, 1024 / (kEllWarps * 32)) grid_
             unsigned long long o = 0;
             if (lane == 0) o = atomicAdd(&w.spill[b], (unsigned long long)((cnt + 3) & ~3));
             o = __shfl_sync(kFull, o, 0);
-            const int64_t off = N * stride + (int64_t)o;
-            if (off + cnt > csr.cap_entries) {
+            const int64_t off = N * stride + csr.spill_lo + (int64_t)o;
+            if (off + cnt > N * stride + csr.spill_hi) {
                 if (lane == 0) atomicOr(&w.status[b], 2);
                 if (lane < L) csr.counts[(b * csr.L + lane) * N + i] = 0;
                 continue;
@@ -1109,6 +1111,11 @@ cudaError_t launch_excl_build(const float4* xyz, int64_t B, int64_t N, const dou
     // -- and loses 11 us at C3's 24000 points, where the multi-kernel build
     // spreads assignment and scatter over the whole GPU)
     const bool fused_grid = (method == 1 || method == 2) && N <= kGridFusedMaxN && !getenv("PS_GRID_MULTI");
+    if (csr.row_hi <= 0) { csr.row_lo = 0; csr.row_hi = N; }
+    if (method == 2 && csr.spill_hi <= 0) {
+        csr.spill_lo = 0;
+        csr.spill_hi = csr.cap_entries - N * ell_row_stride(csr.cap_entries, N);
+    }
     if (method != 2 && (e = cudaMemsetAsync(w.deg, 0, sizeof(int32_t) * B * N, s)) != cudaSuccess) return e;
     if (method == 0) {  // the grid kernels (methods 1, 2) zero these themselves
         if ((e = cudaMemsetAsync(w.long_count, 0, sizeof(unsigned), s)) != cudaSuccess) return e;

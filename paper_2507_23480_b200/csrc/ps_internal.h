@@ -73,6 +73,11 @@ struct CsrView {
     int64_t cap_entries;
     int64_t N;
     int L;
+    // method 2, row-sharded build (one rank of a point split): only rows
+    // [row_lo, row_hi) are written (indptr, entries, counts) and long rows take
+    // spill entries [spill_lo, spill_hi) of the arena.  row_hi == 0 / spill_hi
+    // == 0: every row / the whole arena (launch_excl_build normalises).
+    int64_t row_lo, row_hi, spill_lo, spill_hi;
 };
 
 struct ExclWork {

@@ -199,7 +199,8 @@ __global__ void et_prepare_kernel(EtArgs a) {
         const int64_t b = g / a.N;
         if (a.reached[b] >= a.n_total) continue;
         a.taken[g] = 0;
-        a.md[g] = __longlong_as_double(0x7ff0000000000000LL);
+        const int64_t i = g - b * a.N;
+        if (a.md_hi == 0 || (i >= a.md_lo && i < a.md_hi)) a.md[g] = __longlong_as_double(0x7ff0000000000000LL);
     }
 }
 
@@ -307,6 +308,26 @@ cudaError_t launch_et(const EtArgs& a, cudaStream_t s) {
     sa.taken = a.taken; sa.md = a.md; sa.reached = a.reached; sa.n_total = a.n_total;
     sa.B = a.B; sa.N = a.N; sa.lo = 0; sa.hi = a.N;
     const unsigned g3 = (unsigned)std::min<int64_t>(148 * 16, (a.B * a.N + 7) / 8 + 1);
+    et_scan_kernel<<<g3, 256, 0, s>>>(sa);
+    return cudaGetLastError();
+}
+
+// One rank of a point split: taken from the whole sample prefix, md reset
+// and pulled for the rank's points [lo, hi) only -- the rows it holds.
+cudaError_t launch_et_shard(const EtArgs& a_in, int64_t lo, int64_t hi, cudaStream_t s) {
+    EtArgs a = a_in;
+    a.md_lo = lo;  // md of the other ranks' points is theirs (virtual ranks share the buffer)
+    a.md_hi = hi;
+    const unsigned g1 = (unsigned)std::min<int64_t>(148 * 8, (a.B * a.N + 255) / 256 + 1);
+    et_prepare_kernel<<<g1, 256, 0, s>>>(a);
+    const unsigned g2 = (unsigned)std::min<int64_t>(148 * 8, (a.B * a.n_total + 255) / 256 + 1);
+    et_mark_kernel<<<g2, 256, 0, s>>>(a);
+    EtScanArgs sa;
+    sa.indptr = a.indptr; sa.nbr = a.nbr; sa.d2 = a.d2; sa.cap_entries = a.cap_entries;
+    sa.lvl1_counts = a.lvl1_counts; sa.counts_stride = a.counts_stride;
+    sa.taken = a.taken; sa.md = a.md; sa.reached = a.reached; sa.n_total = a.n_total;
+    sa.B = a.B; sa.N = a.N; sa.lo = lo; sa.hi = hi;
+    const unsigned g3 = (unsigned)std::min<int64_t>(148 * 16, (a.B * (hi - lo) + 7) / 8 + 1);
     et_scan_kernel<<<g3, 256, 0, s>>>(sa);
     return cudaGetLastError();
 }

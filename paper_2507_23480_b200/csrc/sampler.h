@@ -65,6 +65,7 @@ struct EtArgs {
     int64_t ld_out;
     const int64_t* reached;      // [B]
     int64_t n_total, B, N;
+    int64_t md_lo, md_hi;        // md reset range (md_hi == 0: all points)
 };
 
 struct EtScanArgs {
@@ -88,5 +89,6 @@ size_t sampler_v4_ws_bytes(int64_t B, int64_t N);
 cudaError_t launch_et(const EtArgs& a, cudaStream_t s);
 int et_launches();
 cudaError_t launch_et_scan(const EtScanArgs& a, cudaStream_t s);
+cudaError_t launch_et_shard(const EtArgs& a, int64_t lo, int64_t hi, cudaStream_t s);
 
 }  // namespace ps

@@ -467,6 +467,110 @@ class FastPoint:
         return [N * (self.k0 - 1) + excl[b] + N + N * (self.n - int(r)) for b, r in enumerate(reached)]
 
 
+def shard_ranges(N: int, G: int) -> list[tuple[int, int]]:
+    """Original-index range [lo, hi) of every rank of a point split (the
+    partition of ps_fps_split: ceil(N / G) points per rank)."""
+    Ns = -(-N // G)
+    return [(min(N, g * Ns), min(N, (g + 1) * Ns)) for g in range(G)]
+
+
+class FastPointSplit(FastPoint):
+    """FastPoint with every cloud point-split over G ranks (config C5's MDPS,
+    SURVEY.md 8e), here all G ranks on this GPU ("virtual ranks"); the same
+    per-rank calls make up pointsplit.PointSplitFastPoint over one process
+    per GPU:
+
+      prefix      point-split FPS (ps_fps_split, mailbox exchange), k0 samples
+      thresholds  every rank (identical prefix -> identical radii)
+      exclusion   row-sharded: rank g builds the rows of its points
+                  (ps_excl_build_shard, own spill sub-arena, own status)
+      sampler     one rank over all rows (the rows meet on it: here they
+                  share one buffer; across GPUs they are gathered)
+      early term  every rank seeds md of its points from its own rows
+                  (ps_early_termination_shard), then the point-split FPS
+                  tail (ps_fps_split_loop from the sampler's reached count)
+      grouping    rank g answers the sampled centroids it owns (its rows);
+                  the per-rank answers are disjoint and summed
+
+    Results are identical to FastPoint (and the oracle) for any G."""
+
+    def __init__(self, B, N, n, G, **kw):
+        super().__init__(B, N, n, **kw)
+        if self.excl_method != 2:
+            raise ValueError("the row-sharded build uses the method-2 layout (excl_method='grid')")
+        self.G = int(G)
+        if not (1 <= self.G <= 32):
+            raise ValueError("1 <= G <= 32 ranks")
+        self.ranges = shard_ranges(self.N, self.G)
+        self.mb = SplitMailboxes(self.B, self.G, self.device)
+        ws = int(_lib.raw("ps_excl_workspace_bytes", self.B, self.N, 1, 2))
+        self.shard_ws = [torch.empty(ws, dtype=torch.uint8, device=self.device) for _ in range(self.G)]
+        self.shard_status = torch.zeros(self.G, self.B, dtype=torch.int32, device=self.device)
+
+    def capture(self):
+        raise RuntimeError("FastPointSplit tags its mailbox exchanges from the host (ps_fps_split); run it eagerly "
+                           "-- ps_fps's internal split is the graph-capturable form")
+
+    def spill_ranges(self):
+        spill = self.csr.cap_entries - self.N * self.csr.stride
+        per = (spill // self.G) & ~3
+        return [(g * per, (g + 1) * per if g < self.G - 1 else spill) for g in range(self.G)]
+
+    def _prefix(self):
+        _lib.call("ps_fps_split", _p(self.xyz4), self.B, self.N, _p(self.md), _p(self.taken), _p(self.out),
+                  _p(self.curve), self.n, self.k0, self.seed_index, self.G, 0, self.G, _p(self.mb.ptrs),
+                  self.mb.next_seq(self.k0), 0, _stream())
+
+    def _exclusion(self):
+        c = self.csr
+        sp = self.spill_ranges()
+        for g, (lo, hi) in enumerate(self.ranges):
+            if hi <= lo:
+                continue
+            _lib.call("ps_excl_build_shard", _p(self.xyz4), self.B, self.N, _p(c.levels), self.L, c.levels.shape[1],
+                      lo, hi, sp[g][0], sp[g][1], _p(c.indptr), _p(c.nbr), _p(c.d2), _p(c.counts), c.cap_entries,
+                      _p(self.shard_ws[g]), _p(self.shard_status[g]), _stream())
+        torch.amax(self.shard_status, dim=0, out=c.status)  # a failed rank fails the cloud
+
+    def _early_termination(self):
+        c = self.csr
+        lvl1 = c.counts[:, int(self.seg_level_rows[0]), :]
+        for lo, hi in self.ranges:
+            if hi <= lo:
+                continue
+            _lib.call("ps_early_termination_shard", _p(c.indptr), _p(c.nbr), _p(c.d2), c.cap_entries, _p(lvl1),
+                      self.L * self.N, _p(self.taken), _p(self.md), _p(self.out), self.n, _p(self.reached), self.n,
+                      self.B, self.N, lo, hi, _stream())
+        _lib.call("ps_fps_split_loop", _p(self.xyz4), self.B, self.N, _p(self.md), _p(self.taken), _p(self.out),
+                  _p(self.curve), self.n, 1, _p(self.reached), self.n, self.G, 0, self.G, _p(self.mb.ptrs),
+                  self.mb.next_seq(self.n), 0, _stream())
+
+    def group_rf(self, radius, k, centroids=None, out=None):
+        """rf_ball_query, centroid-sharded: rank g answers the centroids in its
+        point range (the other positions come back as count -1); the disjoint
+        answers are summed (index + 1, count + 1, distance)."""
+        cent = self.out if centroids is None else centroids
+        B, n = cent.shape
+        acc_i = torch.zeros(B, n, k, dtype=torch.int32, device=self.device)
+        acc_d = torch.zeros(B, n, k, dtype=torch.float64, device=self.device)
+        acc_c = torch.zeros(B, n, dtype=torch.int32, device=self.device)
+        for lo, hi in self.ranges:
+            if hi <= lo:
+                continue
+            mine = torch.where((cent >= lo) & (cent < hi), cent, torch.full_like(cent, -1))
+            gi, gd, gc = FastPoint.group_rf(self, radius, k, centroids=mine)
+            own = gc >= 0
+            acc_i += torch.where(own[..., None], gi + 1, 0)
+            acc_d += torch.where(own[..., None], gd, 0.0)
+            acc_c += torch.where(own, gc + 1, 0)
+        res = (acc_i - 1, acc_d, acc_c - 1)
+        if out is not None:
+            for o, r in zip(out, res):
+                o.copy_(r)
+            return out
+        return res
+
+
 def ball_query_naive(xyz4, centroids, radius, k):
     B, N, _ = xyz4.shape
     n = centroids.shape[1]

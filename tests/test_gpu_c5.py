@@ -110,3 +110,55 @@ def test_fastpoint_c5_matches_oracle_digest(graph):
     cloud = generate_cloud(c["family"], c["N"], c["cloud_seed"])
     fp, gi, gc = run_fastpoint(cloud, c["n"], PRM["exponent"], graph=graph)
     check_digest(fp, gi, gc, DIG["fastpoint"])
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("case", ["room-24k-G3", "dup-spill-G5", "mid-2e18-G4"])
+def test_fastpoint_point_split_matches_single_rank_and_oracle(case):
+    """MDPS with every cloud point-split over G virtual ranks (split prefix,
+    row-sharded exclusion build with per-rank spill arenas, sampler over the
+    joined rows, per-rank early-termination seeding + split FPS tail,
+    centroid-sharded rf grouping): identical to the single-rank FastPoint
+    and to the oracle."""
+    if case == "mid-2e18-G4":
+        m = DIG["mid"]
+        cloud = generate_cloud(m["family"], m["N"], m["cloud_seed"])
+        n, e, G, r = m["n"], PRM["mid_exponent"], 4, PRM["radius"]
+    elif case == "room-24k-G3":
+        cloud = generate_cloud("room-surfaces", 24000, 77)
+        n, e, G, r = 6000, 0.2, 3, 0.1  # low exponent: long early-termination tail
+    else:
+        cloud = generate_cloud("uniform-box", 30000, 78)
+        cloud[:400] = cloud[0]  # dense duplicates: long rows spill
+        cloud = cloud[np.random.default_rng(0).permutation(30000)].copy()
+        n, e, G, r = 4000, 0.45, 5, 0.05
+    B, N = 1, cloud.shape[0]
+    seed = PRM["rng_seed"] if case == "mid-2e18-G4" else 3
+    fs = engine.FastPointSplit(B, N, n, G, exponent=e, extra_radii=(r,))
+    fs.set_points(torch.from_numpy(cloud[None]).cuda())
+    fs.set_rng([seed])
+    fs.sample()
+    fs.check()
+    si, sd, sc = fs.group_rf(r, 32)
+    fp = engine.FastPoint(B, N, n, exponent=e, extra_radii=(r,))
+    fp.set_points(torch.from_numpy(cloud[None]).cuda())
+    fp.set_rng([seed])
+    fp.sample()
+    fp.check()
+    gi, gd, gc = fp.group_rf(r, 32)
+    torch.cuda.synchronize()
+    assert torch.equal(fs.out, fp.out)
+    assert torch.equal(fs.reached, fp.reached) and torch.equal(fs.state, fp.state)
+    assert torch.equal(sc, gc) and torch.equal(si, gi)
+    assert torch.equal(torch.nan_to_num(sd, nan=-1.0), torch.nan_to_num(gd, nan=-1.0))
+    if case == "mid-2e18-G4":
+        check_digest(fs, si[0].cpu().numpy().astype(np.int64), sc[0].cpu().numpy().astype(np.int64),
+                     DIG["mid"]["fastpoint"])
+    else:
+        ref = O.mdps(cloud, n, exponent=e, rng_seed=3, extra_radii=(r,))
+        np.testing.assert_array_equal(fs.out[0].cpu().numpy(), ref.indices)
+        if case == "room-24k-G3":
+            assert ref.reached < n  # the split tail ran
+        else:
+            stride = fs.csr.stride
+            assert int(fs.csr.counts[0].amax(dim=0).max()) > stride  # spilled rows

@@ -917,3 +917,22 @@ def test_point_split_two_processes_cuda_ipc():
                          env=env, capture_output=True, text=True, timeout=200, cwd=root)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
     assert out.stdout.count("identical to single-rank: True") == 2
+
+
+@pytest.mark.timeout(300)
+def test_point_split_fastpoint_two_processes():
+    """pointsplit.PointSplitFastPoint over two processes (both on this GPU,
+    gloo for the row transfer / broadcast / all-reduce): identical indices
+    and groups to the single-process FastPoint on both ranks, with an
+    early-termination tail (low exponent) running through the split FPS."""
+    import subprocess
+    import sys as _sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    port = 29500 + os.getpid() % 400
+    out = subprocess.run([_sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port),
+                          os.path.join(root, "tools", "ipc_mdps_selftest.py")],
+                         capture_output=True, text=True, timeout=280, cwd=root)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert out.stdout.count("identical to single-process FastPoint: True") == 2
