@@ -291,13 +291,13 @@ class Chain:
     """One FastPoint pipeline (buffers, stream, CUDA graph of sample + rf
     grouping) -- the unit the bench runs S of concurrently."""
 
-    def __init__(self, B, exponent, dev, seeds):
+    def __init__(self, B, exponent, dev, seeds, inflight=None):
         import torch
 
         from paper_2507_23480_b200 import engine
 
         self.fp = engine.FastPoint(B, N, n_SAMPLES, p=P, nseg=NSEG, estimator="power", exponent=exponent,
-                                   extra_radii=(RADIUS,), device=dev)
+                                   extra_radii=(RADIUS,), device=dev, inflight_clouds=inflight)
         self.grp = (torch.empty(B, n_SAMPLES, K, dtype=torch.int32, device=dev),
                     torch.empty(B, n_SAMPLES, K, dtype=torch.float64, device=dev),
                     torch.empty(B, n_SAMPLES, dtype=torch.int32, device=dev))
@@ -373,7 +373,8 @@ def main_ours(args):
     exponent = heldout_exponent()
     S = max(1, args.streams)
     seeds = [rank * B + b for b in range(B)]  # sampler RNG seeds (clouds: shard_seeds)
-    chains = [Chain(B, exponent, dev, seeds) for _ in range(S)]
+    # throughput hint: S chains keep B * S clouds in flight (FPS cluster width)
+    chains = [Chain(B, exponent, dev, seeds, inflight=B * S if S > 1 else None) for _ in range(S)]
     ring_d = torch.from_numpy(ring_h).to(dev)  # [R, B, N, 3] resident inputs
     for c in chains:
         c.fp.set_points(ring_d[0])
@@ -433,8 +434,14 @@ def main_ours(args):
         chains[s % S].kernels for s in range(args.steps))
     t_ms = max_over_ranks(t_ms, dev)
     value = ws * B * n_SAMPLES * args.steps / (t_ms / 1e3)
-    # one chain alone (no cross-step overlap), same loop
-    t1_ms = max_over_ranks(run_chains(chains[:1], args.steps, feed_dev), dev)
+    # one chain alone in latency mode (no cross-step overlap, widest FPS
+    # clusters), same loop
+    lat = Chain(B, exponent, dev, seeds)
+    lat.fp.set_points(ring_d[0])
+    lat.capture()
+    run_chains([lat], 2, feed_dev)
+    t1_ms = max_over_ranks(run_chains([lat], args.steps, feed_dev), dev)
+    del lat
 
     # results of the last step of each chain: valid (status clear) and
     # identical to a fresh un-captured run of the same batch
@@ -454,17 +461,18 @@ def main_ours(args):
 
     # ---- exact-FPS + naive ball query comparator, same loop and ring ---------------------
     class ExactChain:
-        def __init__(self):
+        def __init__(self, inflight):
             self.x4 = torch.zeros(B, N, 4, dtype=torch.float32, device=dev)
             self.stream = torch.cuda.Stream(device=dev)
             self.graph = None
+            self.inflight = inflight
 
         def body(self):
-            idx, _, _, _ = engine.fps(self.x4, n_SAMPLES)
+            idx, _, _, _ = engine.fps(self.x4, n_SAMPLES, inflight_clouds=self.inflight)
             self.out = engine.ball_query_naive(self.x4, idx, RADIUS, K)
             self.idx = idx
 
-    ex = [ExactChain() for _ in range(S)]
+    ex = [ExactChain(B * S if S > 1 else None) for _ in range(S)] + [ExactChain(None)]  # last: latency mode
     for c in ex:
         c.x4[..., :3].copy_(ring_d[0])
         c.stream.wait_stream(stream)
@@ -480,12 +488,13 @@ def main_ours(args):
     def feed_exact(c, s):
         c.x4[..., :3].copy_(ring_d[s % R])
 
-    run_chains(ex, S, feed_exact)
-    exact_ms = max_over_ranks(run_chains(ex, args.steps, feed_exact), dev) / args.steps
-    exact1_ms = max_over_ranks(run_chains(ex[:1], args.steps, feed_exact), dev) / args.steps
-    # kernel split of the exact path (one chain, per-kernel events)
+    run_chains(ex[:S], S, feed_exact)
+    exact_ms = max_over_ranks(run_chains(ex[:S], args.steps, feed_exact), dev) / args.steps
+    run_chains(ex[S:], 2, feed_exact)
+    exact1_ms = max_over_ranks(run_chains(ex[S:], args.steps, feed_exact), dev) / args.steps
+    # kernel split of the exact path (latency mode, per-kernel events)
     fps_ms, bqn_ms = [], []
-    x4 = ex[0].x4
+    x4 = ex[S].x4
     for s in range(min(args.steps, 5)):
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record(stream)
@@ -609,7 +618,8 @@ def main_ours(args):
             "timing": (f"device events around the whole loop of K steps (steps back to back on {S} streams, "
                        "step s on stream s % S, each step = set_points + one CUDA graph of sample + rf grouping)"),
             "us_per_cloud": 1e3 * ms_step / B,
-            "one_stream": {"ms_per_step": t1_ms / args.steps, "value": ws * B * n_SAMPLES / (t1_ms / args.steps / 1e3)},
+            "one_stream": {"ms_per_step": t1_ms / args.steps, "value": ws * B * n_SAMPLES / (t1_ms / args.steps / 1e3),
+                           "note": "one chain, latency-mode FPS cluster width, steps back to back"},
             "stage_ms": per_stage,
             "stage_sum_ms": float(sum(per_stage.values())),
             "exact_fps_path": {"ms_per_step": exact_ms, "ms_per_step_one_stream": exact1_ms,
@@ -928,7 +938,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 point-split line")
     ap.add_argument("--no-extra", action="store_true", help="skip the C2 / C4 objects")
-    ap.add_argument("--streams", type=int, default=2, help="concurrent FastPoint chains (streams)")
+    ap.add_argument("--streams", type=int, default=5, help="concurrent FastPoint chains (streams)")
     ap.add_argument("--cpu-runs", type=int, default=5, help="timed CPU-baseline runs per thread setting (median)")
     ap.add_argument("--c5-split", action="store_true",
                     help="N > 1: also run C5 point-split over the job's GPUs (CUDA IPC + NVLink)")

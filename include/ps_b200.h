@@ -96,6 +96,15 @@ PS_API int ps_fps_split_plan(int64_t N, int64_t B, int32_t G, int32_t Gl, int32_
 PS_API int ps_fps_split(const float* xyz4, int64_t B, int64_t N, double* md, uint8_t* taken, int64_t* out_idx,
                         double* curve, int64_t ld_out, int64_t k_stop, int64_t seed, int32_t G, int32_t g_base,
                         int32_t Gl, void* const* mbox_dev, uint32_t seq_base, int32_t all_write, void* stream);
+/* Throughput hint for the exact-FPS dispatch (ps_fps / ps_fps_loop): the
+ * number of clouds the caller keeps in flight across concurrent streams
+ * (0 = latency mode, the default).  Above the launch's own batch, the
+ * cluster width is chosen to cover the most SMs with that many clouds
+ * instead of minimising one cloud's latency; results are identical.
+ * Returns the previous value; process-wide, read at launch (and baked into
+ * a captured graph). */
+PS_API int64_t ps_set_fps_inflight(int64_t clouds);
+
 /* fps_loop (_kernels.py:35-74) resumed from a partial state over the same
  * point split: iterations [k_start, n_total) (k_start_dev: per-cloud int64
  * device values, e.g. the sampler's reached counts) continue from md/taken

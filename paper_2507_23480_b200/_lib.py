@@ -29,6 +29,7 @@ _SIGS = {
     "ps_launch_count": (_c_i64, []),
     "ps_fps_loop": (_c_i32, [_p, _c_i64, _c_i64, _p, _p, _p, _p, _c_i64, _c_i64, _p, _c_i64, _p]),
     "ps_fps": (_c_i32, [_p, _c_i64, _c_i64, _p, _p, _p, _p, _c_i64, _c_i64, _c_i64, _p, _p]),
+    "ps_set_fps_inflight": (_c_i64, [_c_i64]),
     "ps_fps_update_chunk": (_c_i32, [_p, _c_i64, _c_f64, _c_f64, _c_f64, _p, _c_i64, _c_i64, _p, _p, _p]),
     "ps_first_untaken": (_c_i32, [_p, _c_i64, _p, _p]),
     "ps_excl_workspace_bytes": (_c_i64, [_c_i64, _c_i64, _c_i64, _c_i32]),

@@ -125,6 +125,8 @@ int ps_fps_loop(const float* xyz4, int64_t B, int64_t N, double* md, uint8_t* ta
     return cuda_status(ps::launch_fps(a, B, S(stream)), "fps_loop", 1);
 }
 
+int64_t ps_set_fps_inflight(int64_t clouds) { return ps::fps_set_inflight(clouds); }
+
 int ps_fps(const float* xyz4, int64_t B, int64_t N, double* md, uint8_t* taken, int64_t* out_idx, double* curve,
            int64_t ld_out, int64_t k_stop, int64_t seed, const int64_t* seed_dev, void* stream) {
     CHECK_ARG(B >= 1 && N >= 1 && N <= kMaxN, "invalid batch shape B=%lld N=%lld", (long long)B, (long long)N);

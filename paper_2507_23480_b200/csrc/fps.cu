@@ -490,10 +490,48 @@ static int max_active_clusters(int64_t N, int C, int T) {
     return n;
 }
 
+// Throughput hint (ps_set_fps_inflight): clouds the caller keeps in flight
+// across concurrent streams.  0: latency mode.
+static int64_t g_inflight = 0;
+int64_t fps_set_inflight(int64_t clouds) {
+    const int64_t old = g_inflight;
+    g_inflight = clouds > 0 ? clouds : 0;
+    return old;
+}
+
 // Cluster width C and CTA size T: the widest cluster whose B clusters are
 // all co-resident (one wave, every cloud in lock step), preferring 512-thread
 // CTAs (more warps hide the fold's latency) while P <= 8 points per thread.
+// With a throughput hint of H > B clouds in flight, the width with the most
+// clouds finished per unit time instead: min(H, co-resident clusters) /
+// latency(C), latency(C) ~ a + b / C per sample with b / a ~ 9 (speculative
+// kernel, C3 prefix: 0.49 / 0.56 / 0.60 / 0.64 ms at C = 10 / 8 / 7 / 6,
+// profiles/r02/cluster_sweep.log).  Clusters pack into the GPCs: 22 clusters
+// of 6 fit where 15 of 9 or 11 of 10 do, so C3 with 5 chains in flight runs
+// 6-CTA clusters (64.5 -> 70.2 M samples/s).
 int fps_choose_cluster(int64_t N, int64_t B, int* C_out, int* P_out, int* T_out) {
+    if (g_inflight > B && !getenv("PS_FPS_CLUSTER")) {
+        const int tenv0 = fps_threads_env();
+        const int64_t c0 = (N + 1023) / 1024;
+        const int want = (int)(c0 < 1 ? 1 : (c0 > kMaxCluster ? kMaxCluster : c0));
+        int bestC = 0;
+        int64_t bestCov = -1;
+        for (int cc = want; cc >= 3; --cc) {
+            const int p = choose_P(N, cc, 512);
+            if (tenv0 && tenv0 != 512) break;
+            if (p < 1 || p > 8) continue;
+            const int64_t act = max_active_clusters(N, cc, 512);
+            if (act < B) continue;  // the batch itself must still fit one wave
+            const int64_t score = (act < g_inflight ? act : g_inflight) * cc * 1024 / (cc + 9);
+            if (score >= bestCov) { bestCov = score; bestC = cc; }
+        }
+        if (bestC) {
+            *C_out = bestC;
+            *T_out = 512;
+            *P_out = choose_P(N, bestC, 512);
+            return 0;
+        }
+    }
     const char* env = getenv("PS_FPS_CLUSTER");
     const int tenv = fps_threads_env();
     const int64_t target = (int64_t)256 * 4;

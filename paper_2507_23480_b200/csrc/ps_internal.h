@@ -57,6 +57,7 @@ cudaError_t launch_fps_spec(FpsArgs a, int64_t B, cudaStream_t s);     // regist
 cudaError_t launch_fps_small(FpsArgs a, int64_t B, cudaStream_t s);    // one CTA per small cloud, points in registers
 bool fps_res_plan(int64_t N, int64_t nclusters, int G, int* C_out, int* P_out);
 unsigned long long split_timeout_ns();
+int64_t fps_set_inflight(int64_t clouds);  // throughput hint for the FPS cluster width
 size_t csr_fill_ws_bytes(int64_t M, int64_t N);
 cudaError_t launch_csr_fill(const int32_t* ei, const int32_t* ej, const double* ed, int64_t M, const int64_t* indptr,
                             int64_t N, int64_t* out_idx, double* out_d2, void* work, size_t work_bytes,

@@ -58,9 +58,27 @@ def as_xyz4(coords, device=None) -> torch.Tensor:
 # exact FPS
 
 
-def fps(xyz4: torch.Tensor, n: int, seed_index: int = 0, k_stop: int | None = None):
+class inflight:
+    """Context: launches inside it pick their FPS cluster width for
+    ``clouds`` clouds in flight across concurrent streams (ps_set_fps_inflight;
+    None / 0 = latency mode).  Results are identical either way."""
+
+    def __init__(self, clouds):
+        self.clouds = int(clouds or 0)
+
+    def __enter__(self):
+        self.old = int(_lib.raw("ps_set_fps_inflight", self.clouds)) if self.clouds else None
+        return self
+
+    def __exit__(self, *exc):
+        if self.old is not None:
+            _lib.raw("ps_set_fps_inflight", self.old)
+
+
+def fps(xyz4: torch.Tensor, n: int, seed_index: int = 0, k_stop: int | None = None, inflight_clouds=None):
     """Exact FPS on a batch.  Returns (idx int64[B,n],
-    curve float64[B,n], md float64[B,N], taken uint8[B,N])."""
+    curve float64[B,n], md float64[B,N], taken uint8[B,N]).
+    ``inflight_clouds``: throughput hint (see ``inflight``)."""
     B, N, _ = xyz4.shape
     if not (1 <= n <= N):
         raise ValueError(f"n must be in [1, {N}], got {n}")
@@ -70,8 +88,9 @@ def fps(xyz4: torch.Tensor, n: int, seed_index: int = 0, k_stop: int | None = No
     taken = torch.empty(B, N, dtype=torch.uint8, device=dev)
     out = torch.full((B, n), -1, dtype=torch.int64, device=dev)
     curve = torch.full((B, n), math.inf, dtype=torch.float64, device=dev)
-    _lib.call("ps_fps", _p(xyz4), B, N, _p(md), _p(taken), _p(out), _p(curve), n, stop, int(seed_index), None,
-              _stream())
+    with inflight(inflight_clouds):
+        _lib.call("ps_fps", _p(xyz4), B, N, _p(md), _p(taken), _p(out), _p(curve), n, stop, int(seed_index), None,
+                  _stream())
     return out, curve, md, taken
 
 
@@ -228,7 +247,8 @@ class FastPoint:
     exclusion lists."""
 
     def __init__(self, B, N, n, *, p=0.1, nseg=6, estimator="power", exponent=None, extra_radii=(),
-                 seed_index=0, pick_lowest=False, cap_entries=None, excl_method="grid", device="cuda", mlp=None):
+                 seed_index=0, pick_lowest=False, cap_entries=None, excl_method="grid", device="cuda", mlp=None,
+                 inflight_clouds=None):
         if not (1 <= n <= N):
             raise ValueError(f"n must be in [1, {N}]")
         if nseg < 1 or nseg > 16:
@@ -250,6 +270,9 @@ class FastPoint:
             raise ValueError("at most 8 extra radii")
         self.seed_index = int(seed_index)
         self.pick_lowest = bool(pick_lowest)
+        # throughput hint for the FPS launches (prefix, early-termination tail):
+        # clouds kept in flight by concurrent pipelines (ps_set_fps_inflight)
+        self.inflight_clouds = int(inflight_clouds or 0)
         methods = {"bruteforce": 0, "grid-sorted": 1, "grid": 2}
         if excl_method not in methods:
             raise ValueError(f"excl_method must be one of {sorted(methods)}")
@@ -315,8 +338,9 @@ class FastPoint:
 
     # -- stages -----------------------------------------------------------------
     def _prefix(self):
-        _lib.call("ps_fps", _p(self.xyz4), self.B, self.N, _p(self.md), _p(self.taken), _p(self.out),
-                  _p(self.curve), self.n, self.k0, self.seed_index, None, _stream())
+        with inflight(self.inflight_clouds):
+            _lib.call("ps_fps", _p(self.xyz4), self.B, self.N, _p(self.md), _p(self.taken), _p(self.out),
+                      _p(self.curve), self.n, self.k0, self.seed_index, None, _stream())
 
     def _thresholds(self):
         extra = np.ascontiguousarray(self.extra_r2) if len(self.extra_r2) else np.zeros(1)
@@ -346,8 +370,9 @@ class FastPoint:
         _lib.call("ps_early_termination_prepare", _p(c.indptr), _p(c.nbr), _p(c.d2), c.cap_entries, _p(lvl1),
                   self.L * self.N, _p(self.taken), _p(self.md), _p(self.out), self.n, _p(self.reached), self.n,
                   self.B, self.N, _stream())
-        _lib.call("ps_fps_loop", _p(self.xyz4), self.B, self.N, _p(self.md), _p(self.taken), _p(self.out),
-                  _p(self.curve), self.n, 1, _p(self.reached), self.n, _stream())
+        with inflight(self.inflight_clouds):
+            _lib.call("ps_fps_loop", _p(self.xyz4), self.B, self.N, _p(self.md), _p(self.taken), _p(self.out),
+                      _p(self.curve), self.n, 1, _p(self.reached), self.n, _stream())
 
     def sample(self):
         """Launch the full sampling sequence (no host sync)."""
