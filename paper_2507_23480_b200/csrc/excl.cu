@@ -224,7 +224,8 @@ __global__ void excl_fill_kernel(int64_t N, ExclWork w, CsrView csr) {
 
 __global__ void __launch_bounds__(1024) grid_setup_kernel(const float4* __restrict__ xyz, int64_t N,
                                                           const double* __restrict__ r2_levels, int L,
-                                                          int64_t levels_ld, GridWork g, ExclWork w, int zero) {
+                                                          int64_t levels_ld, GridWork g, ExclWork w, int zero,
+                                                          int reach) {
     __shared__ float red[6][32];
     __shared__ int nc_s;
     const int64_t b = blockIdx.x;
@@ -256,7 +257,7 @@ __global__ void __launch_bounds__(1024) grid_setup_kernel(const float4* __restri
         }
         double r2 = 0.0;
         for (int l = 0; l < L; ++l) r2 = fmax(r2, r2_levels[b * levels_ld + l]);
-        double h = sqrt(r2) * (1.0 + 1e-6);
+        double h = sqrt(r2) * (1.0 + 1e-6) / (double)reach;
         if (!(h > 1e-30)) h = 1e-30;
         int n[3];
         for (int it = 0; it < 64; ++it) {
@@ -274,6 +275,8 @@ __global__ void __launch_bounds__(1024) grid_setup_kernel(const float4* __restri
         gp.inv_h = 1.0 / h;
         gp.nx = n[0]; gp.ny = n[1]; gp.nz = n[2];
         gp.ncells = n[0] * n[1] * n[2];
+        gp.h = h;
+        gp.reach = reach;
         g.params[b] = gp;
         nc_s = gp.ncells;
         if (zero) {
@@ -388,7 +391,7 @@ constexpr int64_t kGridFusedMaxN = 4096;
 __global__ void __launch_bounds__(1024) grid_build_kernel(const float4* __restrict__ xyz, int64_t N,
                                                           const double* __restrict__ r2_levels, int L,
                                                           int64_t levels_ld, GridWork g, ExclWork w, CsrView csr,
-                                                          int64_t stride, int write_indptr) {
+                                                          int64_t stride, int write_indptr, int reach) {
     extern __shared__ int cnt_s[];
     __shared__ float red[6][32];
     __shared__ GridParams gps;
@@ -429,7 +432,7 @@ __global__ void __launch_bounds__(1024) grid_build_kernel(const float4* __restri
         }
         double r2 = 0.0;
         for (int l = 0; l < L; ++l) r2 = fmax(r2, r2_levels[b * levels_ld + l]);
-        double h = sqrt(r2) * (1.0 + 1e-6);
+        double h = sqrt(r2) * (1.0 + 1e-6) / (double)reach;
         if (!(h > 1e-30)) h = 1e-30;
         int n[3];
         for (int it = 0; it < 64; ++it) {
@@ -447,6 +450,8 @@ __global__ void __launch_bounds__(1024) grid_build_kernel(const float4* __restri
         gp.inv_h = 1.0 / h;
         gp.nx = n[0]; gp.ny = n[1]; gp.nz = n[2];
         gp.ncells = n[0] * n[1] * n[2];
+        gp.h = h;
+        gp.reach = reach;
         g.params[b] = gp;
         gps = gp;
         carry = 0;
@@ -863,7 +868,7 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) grid_rows_kernel(int64_t B,
 // instances: 8 warps x 256 entries for short rows (C1-C4), 4 warps x 512
 // for strides above 256 (C5-sized clouds, ~270 entries per row), so that
 // the rescan stays rare.
-template <int kEllWarps, int kEllCap>
+template <int kEllWarps, int kEllCap, bool kCull>
 __global__ void __launch_bounds__(kEllWarps * 32, 1024 / (kEllWarps * 32)) grid_ell_kernel(
     int64_t B, int64_t N, const double* __restrict__ r2_levels, int L, int64_t levels_ld, int64_t stride, GridWork g,
     ExclWork w, CsrView csr) {
@@ -875,7 +880,7 @@ __global__ void __launch_bounds__(kEllWarps * 32, 1024 / (kEllWarps * 32)) grid_
     __shared__ double lvs[kEllWarps][32];
     __shared__ unsigned long long lvb[kEllWarps][32];
     __shared__ unsigned long long lvsort[kEllWarps][16];  // levels ascending, padded (L <= 16)
-    __shared__ int tbase[kEllWarps][9];
+    __shared__ int tbase[kEllWarps][32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
     // one cloud per grid row: the cloud's level values and grid parameters
@@ -917,7 +922,48 @@ __global__ void __launch_bounds__(kEllWarps * 32, 1024 / (kEllWarps * 32)) grid_
         const int cy = cell_coord(p.y, gp.oy, gp.inv_h, gp.ny);
         const int cz = cell_coord(p.z, gp.oz, gp.inv_h, gp.nz);
         int r0 = 0, rlen = 0;
-        if (lane < 9) {
+        if constexpr (kCull) {
+            // cells of width >= R_max / 2: candidate cell rows (dz, dy) in
+            // [-2, 2]^2, one per lane; a row whose y/z slab is farther than
+            // R_max is dropped, the others keep only the x cells that can hold
+            // a point of the ball (|qx - px| <= sqrt(R_max^2 - gy^2 - gz^2)).
+            // Gaps shrink by tol (far above the rounding of the cell
+            // assignment) and the x half-width grows by 1e-5 relative (above
+            // the float sqrt's rounding): no point within R_max is lost.
+            const int reach = gp.reach, wdt = 2 * reach + 1;
+            if (lane < wdt * wdt) {
+                const int dz = lane / wdt - reach, dy = lane % wdt - reach;
+                const int z = cz + dz, y = cy + dy;
+                if (z >= 0 && z < gp.nz && y >= 0 && y < gp.ny) {
+                    const double tol = 1e-9 * (fabs(gp.ox) + fabs(gp.oy) + fabs(gp.oz) + fabs((double)p.x) +
+                                               fabs((double)p.y) + fabs((double)p.z) + gp.h * (gp.nx + gp.ny + gp.nz));
+                    double gy = 0.0, gz = 0.0;
+                    if (dy > 0) gy = (gp.oy + y * gp.h) - (double)p.y;
+                    else if (dy < 0) gy = (double)p.y - (gp.oy + (y + 1) * gp.h);
+                    if (dz > 0) gz = (gp.oz + z * gp.h) - (double)p.z;
+                    else if (dz < 0) gz = (double)p.z - (gp.oz + (z + 1) * gp.h);
+                    gy = fmax(0.0, gy - tol);
+                    gz = fmax(0.0, gz - tol);
+                    const double rem = r2 - gy * gy - gz * gz;
+                    if (rem >= 0.0) {
+                        int x0 = cx - reach, x1 = cx + reach;
+                        if (rem < 1e30) {
+                            const double w = (double)sqrtf((float)rem) * (1.0 + 1e-5) + tol;
+                            x0 = max(x0, cell_coord((double)p.x - w, gp.ox, gp.inv_h, gp.nx));
+                            x1 = min(x1, cell_coord((double)p.x + w, gp.ox, gp.inv_h, gp.nx));
+                        }
+                        x0 = max(x0, 0);
+                        x1 = min(x1, gp.nx - 1);
+                        if (x0 <= x1) {
+                            const int row = (z * gp.ny + y) * gp.nx;
+                            r0 = cs[row + x0];
+                            rlen = cs[row + x1 + 1] - r0;
+                        }
+                    }
+                }
+            }
+        } else if (lane < 9) {
+            // cells of width >= R_max: the 3 x 3 cell rows around the point
             const int z = cz + lane / 3 - 1, y = cy + lane % 3 - 1;
             if (z >= 0 && z < gp.nz && y >= 0 && y < gp.ny) {
                 const int x0 = cx > 0 ? cx - 1 : 0, x1 = cx + 1 < gp.nx ? cx + 1 : gp.nx - 1;
@@ -928,16 +974,16 @@ __global__ void __launch_bounds__(kEllWarps * 32, 1024 / (kEllWarps * 32)) grid_
         }
         int incl = rlen;
 #pragma unroll
-        for (int o = 1; o < 16; o <<= 1) {
+        for (int o = 1; o < (kCull ? 32 : 16); o <<= 1) {
             const int y = __shfl_up_sync(kFull, incl, o);
             if (lane >= o) incl += y;
         }
-        const int total = __shfl_sync(kFull, incl, 8);
-        const int excl0 = incl - rlen;
-        // range of flattened candidate f: #(later range starts <= f), from registers;
+        const int total = __shfl_sync(kFull, incl, kCull ? 31 : 8);
+        const int excl0 = incl - rlen;  // non-decreasing over the rows' lanes
+        // range of flattened candidate f: the last row lane whose start <= f;
         // sorted position = base[range] + f (per-warp table)
-        if (lane < 9) tbase[warp][lane] = r0 - excl0;
-        int e[8];
+        tbase[warp][lane] = r0 - excl0;
+        int e[8];  // !kCull: the 8 later range starts in registers
 #pragma unroll
         for (int q = 0; q < 8; ++q) e[q] = __shfl_sync(kFull, excl0, q + 1);
         __syncwarp();
@@ -945,14 +991,22 @@ __global__ void __launch_bounds__(kEllWarps * 32, 1024 / (kEllWarps * 32)) grid_
 #pragma unroll 4
         for (int tb = 0; tb < total; tb += 32) {
             const int f = tb + lane;
-            // rr = #(e[q] <= f) over the 8 sorted range starts: branch-free
-            // binary search by selects on registers
-            const bool c4 = f >= e[3];
-            int rr = c4 ? 4 : 0;
-            const bool c2 = f >= (c4 ? e[5] : e[1]);
-            rr += c2 ? 2 : 0;
-            rr += (f >= (c4 ? (c2 ? e[6] : e[4]) : (c2 ? e[2] : e[0]))) ? 1 : 0;
-            rr += (rr == 7 && f >= e[7]) ? 1 : 0;
+            int rr;
+            if constexpr (kCull) {
+                // five shuffle steps over the 32 non-decreasing starts
+                int rc = 0;
+#pragma unroll
+                for (int st = 16; st > 0; st >>= 1) rc += (__shfl_sync(kFull, excl0, rc + st - 1) <= f) ? st : 0;
+                rr = rc - 1;
+            } else {
+                // rr = #(e[q] <= f) over the 8 later starts: selects on registers
+                const bool c4 = f >= e[3];
+                rr = c4 ? 4 : 0;
+                const bool c2 = f >= (c4 ? e[5] : e[1]);
+                rr += c2 ? 2 : 0;
+                rr += (f >= (c4 ? (c2 ? e[6] : e[4]) : (c2 ? e[2] : e[0]))) ? 1 : 0;
+                rr += (rr == 7 && f >= e[7]) ? 1 : 0;
+            }
             const int t = tbase[warp][rr] + f;
             bool hit = false;
             double d = 0.0;
@@ -1021,10 +1075,11 @@ __global__ void __launch_bounds__(kEllWarps * 32, 1024 / (kEllWarps * 32)) grid_
                 int here = 0;
                 for (int tb = 0; tb < total; tb += 32) {
                     const int f = tb + lane;
-                    int rr = 0;
+                    int rc = 0;
 #pragma unroll
-                    for (int q = 1; q < 9; ++q) rr += (f >= __shfl_sync(kFull, excl0, q)) ? 1 : 0;
-                    const int t = __shfl_sync(kFull, r0, rr) - __shfl_sync(kFull, excl0, rr) + f;
+                    for (int st = 16; st > 0; st >>= 1)
+                        rc += (__shfl_sync(kFull, excl0, rc + st - 1) <= f) ? st : 0;
+                    const int t = tbase[warp][rc - 1] + f;
                     bool in = false;
                     double d = 0.0;
                     if (f < total) {
@@ -1124,10 +1179,18 @@ cudaError_t launch_excl_build(const float4* xyz, int64_t B, int64_t N, const dou
     const unsigned gpts = (unsigned)std::min<int64_t>(148 * 16, (B * N + 255) / 256 + 1);
     if (method == 1 || method == 2) {
         const int64_t stride = method == 2 ? ell_row_stride(csr.cap_entries, N) : 0;
+        // long rows (stride > 256, e.g. C5's ~270 entries per row in a volume):
+        // candidates from cells of width R_max / 2, +-2 cells per axis, rows
+        // culled and trimmed to the ball (C5 build 10.2 -> 6.3 ms); shorter rows
+        // (surface clouds, C1-C4) keep width R_max and the 3 x 3 cell rows,
+        // whose set-up is cheaper than the candidates trimming would save
+        // (C3: 267 vs 286 us).  PS_GRID_REACH=1|2 forces either.
+        const char* re = getenv("PS_GRID_REACH");
+        const int reach = method == 2 ? (re ? (atoi(re) == 1 ? 1 : 2) : (stride > 256 ? 2 : 1)) : 1;
         const bool multi = !fused_grid;
         if (multi) {
             // grid_setup_kernel zeroes the counters and bookkeeping it owns
-            grid_setup_kernel<<<(unsigned)B, 1024, 0, s>>>(xyz, N, r2_levels, L, levels_ld, g, w, 1);
+            grid_setup_kernel<<<(unsigned)B, 1024, 0, s>>>(xyz, N, r2_levels, L, levels_ld, g, w, 1, reach);
             grid_assign_kernel<<<gpts, 256, 0, s>>>(xyz, B, N, g, csr, stride, method == 2 ? 1 : 0);
             grid_scan_kernel<<<(unsigned)B, 1024, 0, s>>>(N, g);
             grid_scatter_kernel<<<gpts, 256, 0, s>>>(xyz, B, N, g);
@@ -1141,19 +1204,23 @@ cudaError_t launch_excl_build(const float4* xyz, int64_t B, int64_t N, const dou
                 attr = true;
             }
             grid_build_kernel<<<(unsigned)B, 1024, dsm, s>>>(xyz, N, r2_levels, L, levels_ld, g, w, csr, stride,
-                                                             method == 2 ? 1 : 0);
+                                                             method == 2 ? 1 : 0, reach);
         }
         if (method == 2) {
-            if (stride <= 256) {
+            if (reach == 1 && stride <= 256) {
                 constexpr int kW = 8;
                 const int64_t gx = std::max<int64_t>(1, std::min<int64_t>((148 * 16 + B - 1) / B, (N + kW - 1) / kW));
-                grid_ell_kernel<kW, 256><<<dim3((unsigned)gx, (unsigned)B), kW * 32, 0, s>>>(
+                grid_ell_kernel<kW, 256, false><<<dim3((unsigned)gx, (unsigned)B), kW * 32, 0, s>>>(
                     B, N, r2_levels, L, levels_ld, stride, g, w, csr);
             } else {
                 constexpr int kW = 4;
                 const int64_t gx = std::max<int64_t>(1, std::min<int64_t>((148 * 32 + B - 1) / B, (N + kW - 1) / kW));
-                grid_ell_kernel<kW, 512><<<dim3((unsigned)gx, (unsigned)B), kW * 32, 0, s>>>(
-                    B, N, r2_levels, L, levels_ld, stride, g, w, csr);
+                if (reach == 2)
+                    grid_ell_kernel<kW, 512, true><<<dim3((unsigned)gx, (unsigned)B), kW * 32, 0, s>>>(
+                        B, N, r2_levels, L, levels_ld, stride, g, w, csr);
+                else
+                    grid_ell_kernel<kW, 512, false><<<dim3((unsigned)gx, (unsigned)B), kW * 32, 0, s>>>(
+                        B, N, r2_levels, L, levels_ld, stride, g, w, csr);
             }
             return cudaGetLastError();
         }

@@ -106,6 +106,8 @@ inline int64_t ell_row_stride(int64_t cap_entries, int64_t N) {
 struct GridParams {
     double ox, oy, oz, inv_h;
     int nx, ny, nz, ncells;
+    double h;       // cell width (>= R_max / reach)
+    int reach;      // neighbour cells per axis and side that can hold a point within R_max
 };
 
 struct GridWork {

@@ -418,8 +418,14 @@ def test_excl_matches_oracle(family, N, R):
         np.testing.assert_array_equal(counts, e.counts)
 
 
+@pytest.mark.parametrize("reach", ["auto", "2"])
 @pytest.mark.parametrize("N", [5000, 4096, 1000])
-def test_excl_bucketed_rows_match_oracle_sets(N):
+def test_excl_bucketed_rows_match_oracle_sets(N, reach, monkeypatch):
+    """Method-2 rows against the oracle's sorted CSR as sets per level; reach
+    2 = cells of width R_max / 2 with culled / trimmed candidate rows (the
+    long-row path), forced here on ordinary clouds."""
+    if reach != "auto":
+        monkeypatch.setenv("PS_GRID_REACH", reach)
     # method 2 (hot path): fixed stride, rows bucketed by level -- every
     # level's entries are the row prefix; as sets they equal the reference's.
     # N <= 4096 takes the fused one-CTA grid build, 5000 the multi-kernel one.
@@ -534,12 +540,15 @@ def test_mdps_golden(golden, method):
             assert fp.pair_evals()[0] <= int(golden[f"{k}/evals"]), k
 
 
+@pytest.mark.parametrize("reach", ["auto", "2"])
 @pytest.mark.parametrize("B,N,n,family,nseg,pick", [
     (4, 4096, 1024, "uniform-box", 6, False), (3, 3000, 750, "room-surfaces", 6, True),
     (2, 24000, 6000, "room-surfaces", 6, False), (2, 5000, 1250, "lattice", 4, False),
     (1, 40000, 10000, "uniform-box", 6, False),  # global-memory sampler workspace
 ])
-def test_mdps_batched_matches_oracle(B, N, n, family, nseg, pick):
+def test_mdps_batched_matches_oracle(B, N, n, family, nseg, pick, reach, monkeypatch):
+    if reach != "auto":
+        monkeypatch.setenv("PS_GRID_REACH", reach)
     clouds = np.stack([generate_cloud(family, N, 1000 + b) for b in range(B)])
     e = 0.42
     fp = engine.FastPoint(B, N, n, nseg=nseg, exponent=e, extra_radii=(0.1,), pick_lowest=pick)
