@@ -1105,6 +1105,11 @@ __global__ void __launch_bounds__(kEllWarps * 32, 1024 / (kEllWarps * 32)) grid_
                 if (lane < L && bk == rank_lt) hist2 = base2;
             }
             if (lane < L) csr.counts[(b * csr.L + lane) * N + i] = hist2;
+            // pad the row to a whole 16-byte chunk (readers load int4 chunks, masked by the counts)
+            {
+                const int64_t row_cap = row_off == (int64_t)i * stride ? stride : ((base2 + 3) & ~3);
+                if (lane < min((int64_t)((base2 + 3) & ~3), row_cap) - base2) rn[base2 + lane] = -1;
+            }
             continue;
         }
         // scatter by bucket: bucket bases from the per-bucket counts (exclusive
@@ -1129,6 +1134,11 @@ __global__ void __launch_bounds__(kEllWarps * 32, 1024 / (kEllWarps * 32)) grid_
         // level l holds buckets 0 .. rank_lt(l)
         const int hist_mine = __shfl_sync(kFull, hincl, rank_lt < 31 ? rank_lt : 31);
         if (lane < L) csr.counts[(b * csr.L + lane) * N + i] = hist_mine;
+        // pad the row to a whole 16-byte chunk (readers load int4 chunks, masked by the counts)
+        {
+            const int64_t row_cap = row_off == (int64_t)i * stride ? stride : ((cnt + 3) & ~3);
+            if (lane < min((int64_t)((cnt + 3) & ~3), row_cap) - cnt) rn[cnt + lane] = -1;
+        }
         __syncwarp();
     }
     if (lane == 0 && evals) atomicAdd(g.evals + b, evals);

@@ -520,6 +520,9 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
                         }
                     }
                 }
+                // pad the lists to whole 16-byte chunks (the MIS pass reads them as int4)
+                for (int k = n1; k < ((n1 + 3) & ~3) && k < kAdj4; ++k) ao1[k] = 0;
+                for (int k = n2; k < ((n2 + 3) & ~3) && k < kAdj4; ++k) ao2[k] = 0;
                 if (a1) adjcnt[j] = n1 > kAdj4 ? kAdjOvf : (uint8_t)n1;
                 if (a2) adjcnt[j2] = n2 > kAdj4 ? kAdjOvf : (uint8_t)n2;
             }

@@ -22,10 +22,13 @@ from paper_2507_23480_b200 import engine  # noqa: E402
 
 def main():
     exact = "--exact" in sys.argv
+    # --inflight K: the FPS cluster width of K clouds in flight (the bench's
+    # concurrent chains; default 8 x 5)
+    infl = int(sys.argv[sys.argv.index("--inflight") + 1]) if "--inflight" in sys.argv else None
     B = bench.B_PER_GPU
     clouds = bench.clouds_for(0, B)
     fp = engine.FastPoint(B, bench.N, bench.n_SAMPLES, p=bench.P, nseg=bench.NSEG, estimator="power",
-                          exponent=bench.heldout_exponent(), extra_radii=(bench.RADIUS,))
+                          exponent=bench.heldout_exponent(), extra_radii=(bench.RADIUS,), inflight_clouds=infl)
     fp.set_points(torch.from_numpy(clouds).cuda())
     for _ in range(2):
         fp.set_rng(list(range(B)))
