@@ -71,15 +71,19 @@ def max_over_ranks(value: float, device=None) -> float:
     return float(t.item())
 
 
+HELDOUT = 5  # held-out clouds of the family for the exponent fit (A3)
+
+
 def heldout_exponent():
-    """Offline exponent fit on 2 held-out clouds of the
-    family, from exact GPU FPS curves -- outside every timed region."""
+    """Offline exponent fit on 5 held-out clouds of the
+    family (the A3 protocol), from exact GPU FPS curves --
+    outside every timed region."""
     import torch
 
     from paper_2507_23480_b200 import curve, engine
     from paper_2507_23480_b200.harness import generate_cloud
 
-    held = np.stack([generate_cloud(FAMILY, N, 99000 + i) for i in range(2)])
+    held = np.stack([generate_cloud(FAMILY, N, 99000 + i) for i in range(HELDOUT)])
     _, cv, _, _ = engine.fps(engine.as_xyz4(torch.from_numpy(held).cuda()), n_SAMPLES)
     return curve.fit_power_exponent(cv.cpu().numpy())
 
@@ -91,7 +95,7 @@ def heldout_exponent_cpu():
     from paper_2507_23480_b200 import curve
     from paper_2507_23480_b200.harness import generate_cloud
 
-    curves = [O.fps(generate_cloud(FAMILY, N, 99000 + i), n_SAMPLES)[1] for i in range(2)]
+    curves = [O.fps(generate_cloud(FAMILY, N, 99000 + i), n_SAMPLES)[1] for i in range(HELDOUT)]
     return curve.fit_power_exponent(curves)
 
 
@@ -680,7 +684,7 @@ def bench_c2_cascade(dev, steps):
     from paper_2507_23480_b200.harness import generate_cloud
 
     B, Nc = 32, 1024
-    held = np.stack([generate_cloud("unit-sphere", Nc, 77000 + i) for i in range(4)])
+    held = np.stack([generate_cloud("unit-sphere", Nc, 77000 + i) for i in range(HELDOUT)])
     _, cv, _, _ = engine.fps(engine.as_xyz4(torch.from_numpy(held).to(dev)), Nc // 2)
     e = curve.fit_power_exponent(cv.cpu().numpy())
     clouds = np.stack([generate_cloud("unit-sphere", Nc, 2000 + b) for b in range(B)])
@@ -710,7 +714,7 @@ def bench_c4(dev, steps):
     from paper_2507_23480_b200.harness import generate_cloud
 
     B, Nc, nc = 2, 65536, 16384
-    held = np.stack([generate_cloud(FAMILY, Nc, 88000 + i) for i in range(2)])
+    held = np.stack([generate_cloud(FAMILY, Nc, 88000 + i) for i in range(HELDOUT)])
     _, cv, _, _ = engine.fps(engine.as_xyz4(torch.from_numpy(held).to(dev)), nc)
     e = curve.fit_power_exponent(cv.cpu().numpy())
     clouds = np.stack([generate_cloud(FAMILY, Nc, 3000 + b) for b in range(B)])
