@@ -1144,6 +1144,310 @@ __global__ void __launch_bounds__(kEllWarps * 32, 1024 / (kEllWarps * 32)) grid_
     if (lane == 0 && evals) atomicAdd(g.evals + b, evals);
 }
 
+// A row with more f32 survivors than grid_ell_cell_kernel stages: exact
+// count, spill decision, then one pass per level bucket over the candidates
+// straight to the row (dense neighbourhoods only).  Out of line, so that its
+// registers do not weigh on the cell kernel's main path.  tb / ts: the cell
+// segment's flattened candidate ranges (start in f, sorted base).
+__device__ __noinline__ void ell_rescan_row(float4 p, int32_t i, int64_t b, int64_t N, int total, const int* tb,
+                                            const int* ts, const float4* sx, double r2, float thr, bool no_filter,
+                                            int L, const double* lvs, int rank_lt, int64_t stride, ExclWork w,
+                                            CsrView csr) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    auto at = [&](int f) -> float4 {
+        int rr = 0;
+#pragma unroll
+        for (int q = 1; q < 9; ++q) rr += (f >= ts[q]) ? 1 : 0;
+        return sx[tb[rr] + f];
+    };
+    int cnt = 0;
+    for (int tb0 = 0; tb0 < total; tb0 += 32) {
+        const int f = tb0 + lane;
+        bool in = false;
+        if (f < total) {
+            const float4 q = at(f);
+            in = (no_filter || sqdist_f32(p, q) < thr) && sqdist4(p, q) < r2;
+        }
+        cnt += __popc(__ballot_sync(kFull, in));
+    }
+    int64_t row_off = (int64_t)i * stride;
+    if (cnt > stride) {
+        unsigned long long o = 0;
+        if (lane == 0) o = atomicAdd(&w.spill[b], (unsigned long long)((cnt + 3) & ~3));
+        o = __shfl_sync(kFull, o, 0);
+        const int64_t off = N * stride + csr.spill_lo + (int64_t)o;
+        if (off + cnt > N * stride + csr.spill_hi) {
+            if (lane == 0) atomicOr(&w.status[b], 2);
+            if (lane < L) csr.counts[(b * csr.L + lane) * N + i] = 0;
+            __syncwarp();
+            return;
+        }
+        row_off = off;
+        if (lane == 0) csr.indptr[b * (N + 1) + i] = off;
+    }
+    int32_t* rn = csr.nbr + b * csr.cap_entries + row_off;
+    double* rd = csr.d2 + b * csr.cap_entries + row_off;
+    int base2 = 0, hist2 = 0;
+    for (int bk = 0; bk <= L; ++bk) {
+        int here = 0;
+        for (int tb0 = 0; tb0 < total; tb0 += 32) {
+            const int f = tb0 + lane;
+            bool in = false;
+            double d = 0.0;
+            int32_t qi = 0;
+            if (f < total) {
+                const float4 q = at(f);
+                if (no_filter || sqdist_f32(p, q) < thr) {
+                    d = sqdist4(p, q);
+                    if (d < r2) {
+                        int bb = 0;
+                        for (int l = 0; l < L; ++l) bb += (lvs[l] <= d) ? 1 : 0;
+                        in = bb == bk;
+                        qi = __float_as_int(q.w);
+                    }
+                }
+            }
+            const unsigned bm = __ballot_sync(kFull, in);
+            if (in) {
+                const int pos = base2 + here + __popc(bm & lt);
+                __stcs(rd + pos, d);
+                rn[pos] = qi;
+            }
+            here += __popc(bm);
+        }
+        base2 += here;
+        if (lane < L && bk == rank_lt) hist2 = base2;
+    }
+    if (lane < L) csr.counts[(b * csr.L + lane) * N + i] = hist2;
+    const int64_t row_cap = row_off == (int64_t)i * stride ? stride : ((base2 + 3) & ~3);
+    if (lane < min((int64_t)((base2 + 3) & ~3), row_cap) - base2) rn[base2 + lane] = -1;
+    __syncwarp();
+}
+
+// Method 2, short rows (cells of width >= R_max, 3 x 3 cell rows): a warp
+// takes kChunk consecutive sorted points (rows).  The points of one grid cell
+// are consecutive in sorted order and share one candidate set (the points of
+// the 3 x 3 x 3 neighbouring cells), so the warp enumerates the candidates
+// once per cell segment of its chunk, up to 32 * kSlots of them held in
+// registers (one per lane and slot; larger sets are reloaded per row in
+// windows), and runs each row of the segment against them:
+//   A. f32 screen, lanes = candidates; survivors compacted into shared memory;
+//   B. lanes = survivors (dense): exact f64 test, level bucket, rank within
+//      the bucket from ballots over the bucket bits (no atomics);
+//   C. scatter to the row at bucket base + rank.
+// Same row layout, buckets, spill and padding as grid_ell_kernel, whose
+// per-row candidate fetch and sparse per-hit lanes cost ~950 warp
+// instructions per C3 row.
+template <int kEllWarps, int kEllCap, int kSlots, int kChunk, int kMinBlocks>
+__global__ void __launch_bounds__(kEllWarps * 32, kMinBlocks) grid_ell_cell_kernel(
+    int64_t B, int64_t N, const double* __restrict__ r2_levels, int L, int64_t levels_ld, int64_t stride, GridWork g,
+    ExclWork w, CsrView csr) {
+    static_assert(kChunk <= 32, "one row per lane in the chunk prefetch");
+    __shared__ float4 sc[kEllWarps][32 * kSlots];  // the cell segment's candidates (window)
+    __shared__ float4 sq[kEllWarps][kEllCap];     // f32 survivors of the row (xyz, original index in w)
+    __shared__ double hd[kEllWarps][kEllCap];     // their exact d2
+    __shared__ uint16_t hb[kEllWarps][kEllCap];   // rank within the bucket
+    __shared__ uint8_t hk[kEllWarps][kEllCap];    // bucket; 0xff: not within R_max
+    __shared__ double lvs[kEllWarps][32];
+    __shared__ unsigned long long lvb[kEllWarps][8];
+    __shared__ int tbase[kEllWarps][32];
+    __shared__ int tstart[kEllWarps][32];
+    __shared__ float4 qs[kEllWarps][kChunk];  // the chunk's points
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const int64_t b = blockIdx.y;
+    const float kInfF = __int_as_float(0x7f800000);
+    const double my_r2 = lane < L ? r2_levels[b * levels_ld + lane] : 0.0;
+    if (lane < L) lvs[warp][lane] = my_r2;
+    int rank_lt = 0, rank_st = 0;
+    double r2 = 0.0;
+    for (int l = 0; l < L; ++l) {
+        const double v = __shfl_sync(kFull, my_r2, l);
+        rank_lt += (v < my_r2) ? 1 : 0;
+        rank_st += (v < my_r2 || (v == my_r2 && l < lane)) ? 1 : 0;  // stable sort position
+        r2 = fmax(r2, v);
+    }
+    // L <= 8 levels (launcher), ascending, padded above every d2: a hit is
+    // below the largest level, so its bucket #(levels <= d2) is 0 .. 7 --
+    // three bits, three steps of a binary search
+    if (lane < 8) lvb[warp][lane] = ~0ull;
+    __syncwarp();
+    if (lane < L) lvb[warp][rank_st] = (unsigned long long)__double_as_longlong(my_r2);
+    const float thr = prefilter_threshold(r2);
+    const bool no_filter = !(thr <= FLT_MAX);
+    const GridParams gp = g.params[b];
+    const float4* sx = g.sorted_xyz + b * N;
+    const int* cs = g.cell_start + b * (g.max_cells + 1);
+    __syncwarp();
+    unsigned long long evals = 0;
+    for (int64_t s0 = ((int64_t)blockIdx.x * kEllWarps + warp) * kChunk; s0 < N;
+         s0 += (int64_t)gridDim.x * kEllWarps * kChunk) {
+        const int nq = (int)(N - s0 < kChunk ? N - s0 : kChunk);
+        int qc = -1;
+        __syncwarp();
+        if (lane < nq) {
+            const float4 qp = sx[s0 + lane];
+            qs[warp][lane] = qp;
+            qc = (cell_coord(qp.z, gp.oz, gp.inv_h, gp.nz) * gp.ny + cell_coord(qp.y, gp.oy, gp.inv_h, gp.ny)) *
+                     gp.nx + cell_coord(qp.x, gp.ox, gp.inv_h, gp.nx);
+        }
+        __syncwarp();
+        for (int j = 0; j < nq;) {
+            // the cell segment [j, jend) of the chunk
+            const int c = __shfl_sync(kFull, qc, j);
+            const unsigned after = __ballot_sync(kFull, lane < nq && qc != c) & ~((2u << j) - 1u);
+            const int jend = after ? __ffs(after) - 1 : nq;
+            const int cx = c % gp.nx, cy = (c / gp.nx) % gp.ny, cz = c / (gp.nx * gp.ny);
+            int r0 = 0, rlen = 0;
+            if (lane < 9) {
+                const int z = cz + lane / 3 - 1, y = cy + lane % 3 - 1;
+                if (z >= 0 && z < gp.nz && y >= 0 && y < gp.ny) {
+                    const int x0 = cx > 0 ? cx - 1 : 0, x1 = cx + 1 < gp.nx ? cx + 1 : gp.nx - 1;
+                    const int row = (z * gp.ny + y) * gp.nx;
+                    r0 = cs[row + x0];
+                    rlen = cs[row + x1 + 1] - r0;
+                }
+            }
+            int incl = rlen;
+#pragma unroll
+            for (int o = 1; o < 16; o <<= 1) {
+                const int y = __shfl_up_sync(kFull, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int total = __shfl_sync(kFull, incl, 8);
+            const int excl0 = incl - rlen;
+            __syncwarp();
+            tbase[warp][lane] = r0 - excl0;
+            tstart[warp][lane] = lane < 9 ? excl0 : 0x7fffffff;
+            __syncwarp();
+            // flattened candidate f (< total) -> its point (the 9 ranges are consecutive in f)
+            auto cand_at = [&](int f) -> float4 {
+                if (f >= total) return make_float4(kInfF, kInfF, kInfF, 0.f);  // screened out (finite thr)
+                int rr = 0;
+#pragma unroll
+                for (int q = 1; q < 9; ++q) rr += (f >= tstart[warp][q]) ? 1 : 0;
+                return sx[tbase[warp][rr] + f];
+            };
+            const bool fits = total <= 32 * kSlots;
+            auto load_window = [&](int w0) {
+                __syncwarp();
+#pragma unroll
+                for (int k = 0; k < kSlots; ++k) sc[warp][k * 32 + lane] = cand_at(w0 + k * 32 + lane);
+                __syncwarp();
+            };
+            if (fits) load_window(0);
+            for (int sj = j; sj < jend; ++sj) {
+                const float4 p = qs[warp][sj];
+                const int32_t i = __float_as_int(p.w);  // original index (grid_scatter_kernel)
+                if (i < csr.row_lo || i >= csr.row_hi) continue;  // another rank's row (warp-uniform)
+                evals += (unsigned long long)total;
+                // A. f32 screen, survivors compacted
+                int nsv = 0;
+                for (int w0 = 0; w0 < total; w0 += 32 * kSlots) {
+                    if (!fits) load_window(w0);
+                    const int ns = min(kSlots, (total - w0 + 31) >> 5);
+#pragma unroll
+                    for (int k = 0; k < kSlots; ++k) {
+                        if (k < ns) {
+                            const float4 q = sc[warp][k * 32 + lane];
+                            const bool sv = sqdist_f32(p, q) < thr;
+                            const unsigned m = __ballot_sync(kFull, sv);
+                            const int pos = nsv + __popc(m & lt);
+                            if (sv && pos < kEllCap) sq[warp][pos] = q;
+                            nsv += __popc(m);
+                        }
+                    }
+                }
+                __syncwarp();
+                int64_t row_off = (int64_t)i * stride;
+                if (nsv > kEllCap || no_filter) {
+                    // more survivors than the staging holds (dense neighbourhoods only),
+                    // or levels beyond float range (no screen)
+                    ell_rescan_row(p, i, b, N, total, tbase[warp], tstart[warp], sx, r2, thr, no_filter, L, lvs[warp],
+                                   rank_lt, stride, w, csr);
+                    continue;
+                }
+                // B. dense pass over the survivors: exact test, bucket (#levels <= d2,
+                // binary search on the bit patterns of the sorted, padded levels),
+                // rank within the bucket from ballots over the three bucket bits
+                int runs = 0;  // lane t: entries of bucket t so far
+                for (int e0 = 0; e0 < nsv; e0 += 32) {
+                    const int ee = e0 + lane;
+                    const bool valid = ee < nsv;
+                    const double d = sqdist4(p, sq[warp][valid ? ee : 0]);
+                    const bool hit = valid && d < r2;
+                    const unsigned long long db = (unsigned long long)__double_as_longlong(d);
+                    const unsigned long long* lv = lvb[warp];
+                    int bk = (lv[3] <= db) ? 4 : 0;
+                    bk += (lv[bk + 1] <= db) ? 2 : 0;
+                    bk += (lv[bk] <= db) ? 1 : 0;
+                    const unsigned hm = __ballot_sync(kFull, hit);
+                    const unsigned m0 = __ballot_sync(kFull, hit && (bk & 1));
+                    const unsigned m1 = __ballot_sync(kFull, hit && (bk & 2));
+                    const unsigned m2 = __ballot_sync(kFull, hit && (bk & 4));
+                    const unsigned peers = hm & ((bk & 1) ? m0 : ~m0) & ((bk & 2) ? m1 : ~m1) & ((bk & 4) ? m2 : ~m2);
+                    const unsigned mine =
+                        hm & ((lane & 1) ? m0 : ~m0) & ((lane & 2) ? m1 : ~m1) & ((lane & 4) ? m2 : ~m2);
+                    const int rank = __shfl_sync(kFull, runs, bk & 7) + __popc(peers & lt);
+                    runs += __popc(mine);
+                    if (valid) {
+                        hk[warp][ee] = hit ? (uint8_t)bk : (uint8_t)0xff;
+                        hb[warp][ee] = (uint16_t)rank;
+                        hd[warp][ee] = d;
+                    }
+                }
+                // bucket bases: exclusive scan of the per-bucket totals
+                int hincl = lane <= L ? runs : 0;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(kFull, hincl, o);
+                    if (lane >= o) hincl += y;
+                }
+                const int cnt = __shfl_sync(kFull, hincl, L);
+                const int hbase = hincl - (lane <= L ? runs : 0);
+                if (cnt > stride) {  // spill arena (see grid_ell_kernel)
+                    unsigned long long o = 0;
+                    if (lane == 0) o = atomicAdd(&w.spill[b], (unsigned long long)((cnt + 3) & ~3));
+                    o = __shfl_sync(kFull, o, 0);
+                    const int64_t off = N * stride + csr.spill_lo + (int64_t)o;
+                    if (off + cnt > N * stride + csr.spill_hi) {
+                        if (lane == 0) atomicOr(&w.status[b], 2);
+                        if (lane < L) csr.counts[(b * csr.L + lane) * N + i] = 0;
+                        __syncwarp();
+                        continue;
+                    }
+                    row_off = off;
+                    if (lane == 0) csr.indptr[b * (N + 1) + i] = off;
+                }
+                __syncwarp();
+                // C. scatter
+                int32_t* rn = csr.nbr + b * csr.cap_entries + row_off;
+                double* rd = csr.d2 + b * csr.cap_entries + row_off;
+                for (int e0 = 0; e0 < nsv; e0 += 32) {
+                    const int ee = e0 + lane;
+                    const int bk = ee < nsv ? hk[warp][ee] : 0xff;
+                    const int pos = __shfl_sync(kFull, hbase, bk & 31) + (ee < nsv ? hb[warp][ee] : 0);
+                    if (bk != 0xff) {
+                        __stcs(rd + pos, hd[warp][ee]);  // d2 streams to HBM: keep L2 for the nbr rows
+                        rn[pos] = __float_as_int(sq[warp][ee].w);
+                    }
+                }
+                // level l holds buckets 0 .. rank_lt(l)
+                const int hist_mine = __shfl_sync(kFull, hincl, rank_lt < 31 ? rank_lt : 31);
+                if (lane < L) csr.counts[(b * csr.L + lane) * N + i] = hist_mine;
+                {
+                    const int64_t row_cap = row_off == (int64_t)i * stride ? stride : ((cnt + 3) & ~3);
+                    if (lane < min((int64_t)((cnt + 3) & ~3), row_cap) - cnt) rn[cnt + lane] = -1;
+                }
+                __syncwarp();
+            }
+            j = jend;
+        }
+    }
+    if (lane == 0 && evals) atomicAdd(g.evals + b, evals);
+}
+
 static cudaError_t launch_sort(CsrView csr, int64_t B, const double* r2_levels, int64_t levels_ld, ExclWork w,
                                cudaStream_t s) {
     excl_sort_small_kernel<<<148 * 8, kSortWarps * 32, 0, s>>>(csr, B, r2_levels, levels_ld, w);
@@ -1217,7 +1521,14 @@ cudaError_t launch_excl_build(const float4* xyz, int64_t B, int64_t N, const dou
                                                              method == 2 ? 1 : 0, reach);
         }
         if (method == 2) {
-            if (reach == 1 && stride <= 256) {
+            if (reach == 1 && L <= 8 && !getenv("PS_ELL_ROW")) {
+                // warp per chunk of sorted rows, candidates per cell segment in registers
+                // (C3: 260 vs 276 us for the stage with grid_ell_kernel, PS_ELL_ROW=1)
+                constexpr int kWc = 4, kChunk = 16;
+                const int64_t gxc = std::max<int64_t>(1, (N + kWc * kChunk - 1) / (kWc * kChunk));
+                grid_ell_cell_kernel<kWc, 128, 8, kChunk, 7><<<dim3((unsigned)gxc, (unsigned)B), kWc * 32, 0, s>>>(
+                    B, N, r2_levels, L, levels_ld, stride, g, w, csr);
+            } else if (reach == 1 && stride <= 256) {
                 constexpr int kW = 8;
                 const int64_t gx = std::max<int64_t>(1, std::min<int64_t>((148 * 16 + B - 1) / B, (N + kW - 1) / kW));
                 grid_ell_kernel<kW, 256, false><<<dim3((unsigned)gx, (unsigned)B), kW * 32, 0, s>>>(

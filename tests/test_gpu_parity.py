@@ -418,22 +418,44 @@ def test_excl_matches_oracle(family, N, R):
         np.testing.assert_array_equal(counts, e.counts)
 
 
-@pytest.mark.parametrize("reach", ["auto", "2"])
+def _set_excl_variant(variant, monkeypatch):
+    # "auto": the default choice; "2": cells of width R_max / 2 with culled /
+    # trimmed candidate rows (the long-row path) forced; "1": cells of width
+    # R_max (warp per cell, candidates in registers) forced; "row": the warp-
+    # per-point kernel over 3 x 3 cell rows (grid_ell_kernel)
+    if variant in ("1", "2"):
+        monkeypatch.setenv("PS_GRID_REACH", variant)
+    elif variant == "row":
+        monkeypatch.setenv("PS_GRID_REACH", "1")
+        monkeypatch.setenv("PS_ELL_ROW", "1")
+
+
+@pytest.mark.parametrize("reach", ["auto", "2", "row"])
 @pytest.mark.parametrize("N", [5000, 4096, 1000])
 def test_excl_bucketed_rows_match_oracle_sets(N, reach, monkeypatch):
-    """Method-2 rows against the oracle's sorted CSR as sets per level; reach
-    2 = cells of width R_max / 2 with culled / trimmed candidate rows (the
-    long-row path), forced here on ordinary clouds."""
-    if reach != "auto":
-        monkeypatch.setenv("PS_GRID_REACH", reach)
+    """Method-2 rows against the oracle's sorted CSR as sets per level, for
+    every row kernel (see _set_excl_variant)."""
+    _set_excl_variant(reach, monkeypatch)
     # method 2 (hot path): fixed stride, rows bucketed by level -- every
     # level's entries are the row prefix; as sets they equal the reference's.
     # N <= 4096 takes the fused one-CTA grid build, 5000 the multi-kernel one.
-    c = generate_cloud("room-surfaces", N, 5)
-    R = [0.3, 0.25, 0.2, 0.2, 0.15, 0.1]
-    e = O.build_exclusion_lists(c, R, (0.12,))
-    levels = np.array([O.radius_sq(r) for r in R] + [O.radius_sq(0.12)])
-    csr = engine.DeviceCsr.allocate(1, N, len(levels), N * 256, 1, torch.device("cuda"), 2)
+    _check_bucketed_rows(generate_cloud("room-surfaces", N, 5), [0.3, 0.25, 0.2, 0.2, 0.15, 0.1], 0.12, 256)
+
+
+@pytest.mark.parametrize("reach", ["1", "row"])
+def test_excl_bucketed_rows_dense(reach, monkeypatch):
+    """A dense volume: ~1300 candidates per cell (the cell kernel reloads its
+    register window per row), rows above 256 entries (the per-bucket rescan),
+    rows beyond the stride (spill arena)."""
+    _set_excl_variant(reach, monkeypatch)
+    _check_bucketed_rows(generate_cloud("uniform-box", 6000, 8), [0.21, 0.2, 0.17, 0.15, 0.12, 0.1], 0.05, 300)
+
+
+def _check_bucketed_rows(c, R, extra, cap_per_point):
+    N = c.shape[0]
+    e = O.build_exclusion_lists(c, R, (extra,))
+    levels = np.array([O.radius_sq(r) for r in R] + [O.radius_sq(extra)])
+    csr = engine.DeviceCsr.allocate(1, N, len(levels), N * cap_per_point, 1, torch.device("cuda"), 2)
     csr.levels.copy_(torch.from_numpy(levels.reshape(1, -1)))
     csr.build(engine.as_xyz4(c))
     assert not csr.overflowed()
@@ -540,15 +562,14 @@ def test_mdps_golden(golden, method):
             assert fp.pair_evals()[0] <= int(golden[f"{k}/evals"]), k
 
 
-@pytest.mark.parametrize("reach", ["auto", "2"])
+@pytest.mark.parametrize("reach", ["auto", "2", "row"])
 @pytest.mark.parametrize("B,N,n,family,nseg,pick", [
     (4, 4096, 1024, "uniform-box", 6, False), (3, 3000, 750, "room-surfaces", 6, True),
     (2, 24000, 6000, "room-surfaces", 6, False), (2, 5000, 1250, "lattice", 4, False),
     (1, 40000, 10000, "uniform-box", 6, False),  # global-memory sampler workspace
 ])
 def test_mdps_batched_matches_oracle(B, N, n, family, nseg, pick, reach, monkeypatch):
-    if reach != "auto":
-        monkeypatch.setenv("PS_GRID_REACH", reach)
+    _set_excl_variant(reach, monkeypatch)
     clouds = np.stack([generate_cloud(family, N, 1000 + b) for b in range(B)])
     e = 0.42
     fp = engine.FastPoint(B, N, n, nseg=nseg, exponent=e, extra_radii=(0.1,), pick_lowest=pick)
