@@ -387,37 +387,47 @@ def main_ours(args):
     stream = torch.cuda.current_stream()
 
     # ---- stage breakdown: one chain, per-stage events, L2 flushed between steps ----
+    # stage_ms: each stage alone at its latency-mode width (the FastPoint a
+    # single chain runs); stage_ms_inflight: the same with the chains'
+    # throughput-hint FPS width
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     stages = ["fps_prefix", "thresholds", "excl_build", "sampler", "early_term", "rf_ball_query"]
+    lat_chain = Chain(B, exponent, dev, seeds)
 
-    def staged(events):
-        fp.state.copy_(chains[0].seed_t)
+    def staged(ch, events):
+        f = ch.fp
+        f.state.copy_(ch.seed_t)
         events[0].record(stream)
-        fp._prefix()
+        f._prefix()
         events[1].record(stream)
-        fp._thresholds()
+        f._thresholds()
         events[2].record(stream)
-        fp._exclusion()
+        f._exclusion()
         events[3].record(stream)
-        fp._sampler()
+        f._sampler()
         events[4].record(stream)
-        fp._early_termination()
+        f._early_termination()
         events[5].record(stream)
-        fp.group_rf(RADIUS, K, out=chains[0].grp)
+        f.group_rf(RADIUS, K, out=ch.grp)
         events[6].record(stream)
 
+    def breakdown(ch):
+        ch.fp.set_points(ring_d[0])
+        for _ in range(max(args.warmup, 3)):
+            staged(ch, [torch.cuda.Event(enable_timing=True) for _ in range(7)])
+        torch.cuda.synchronize()
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in range(args.steps)]
+        for s in range(args.steps):
+            ch.fp.set_points(ring_d[s % R])
+            flush.zero_()  # L2 flush between steps, outside the events
+            staged(ch, ev[s])
+        torch.cuda.synchronize()
+        sm = np.array([[ev[s][i].elapsed_time(ev[s][i + 1]) for i in range(6)] for s in range(args.steps)])
+        return {nm: float(sm[:, i].mean()) for i, nm in enumerate(stages)}
+
+    per_stage = breakdown(lat_chain)
+    per_stage_inflight = breakdown(chains[0])
     fp.set_points(ring_d[0])
-    for _ in range(max(args.warmup, 3)):
-        staged([torch.cuda.Event(enable_timing=True) for _ in range(7)])
-    torch.cuda.synchronize()
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in range(args.steps)]
-    for s in range(args.steps):
-        fp.set_points(ring_d[s % R])
-        flush.zero_()  # L2 flush between steps, outside the events
-        staged(ev[s])
-    torch.cuda.synchronize()
-    stage_ms = np.array([[ev[s][i].elapsed_time(ev[s][i + 1]) for i in range(6)] for s in range(args.steps)])
-    per_stage = {nm: float(stage_ms[:, i].mean()) for i, nm in enumerate(stages)}
     del flush
 
     # ---- headline: S concurrent chains, steps back to back, inputs cold (ring > L2) ----
@@ -440,12 +450,12 @@ def main_ours(args):
     value = ws * B * n_SAMPLES * args.steps / (t_ms / 1e3)
     # one chain alone in latency mode (no cross-step overlap, widest FPS
     # clusters), same loop
-    lat = Chain(B, exponent, dev, seeds)
+    lat = lat_chain
     lat.fp.set_points(ring_d[0])
     lat.capture()
     run_chains([lat], 2, feed_dev)
     t1_ms = max_over_ranks(run_chains([lat], args.steps, feed_dev), dev)
-    del lat
+    del lat, lat_chain
 
     # results of the last step of each chain: valid (status clear) and
     # identical to a fresh un-captured run of the same batch
@@ -626,6 +636,10 @@ def main_ours(args):
                            "note": "one chain, latency-mode FPS cluster width, steps back to back"},
             "stage_ms": per_stage,
             "stage_sum_ms": float(sum(per_stage.values())),
+            "stage_ms_inflight": per_stage_inflight,
+            "stage_note": ("stage_ms: one chain, each stage alone at its latency-mode width (FPS: widest "
+                           "co-resident clusters); stage_ms_inflight: the same stages with the throughput-hint FPS "
+                           "width the concurrent chains use; timeline: profiles/r02/timeline_c3_5chains.txt"),
             "exact_fps_path": {"ms_per_step": exact_ms, "ms_per_step_one_stream": exact1_ms,
                                "fps_ms": float(np.mean(fps_ms)), "ball_query_naive_ms": float(np.mean(bqn_ms)),
                                "value": ws * B * n_SAMPLES / (exact_ms / 1e3), "us_per_cloud": 1e3 * exact_ms / B,

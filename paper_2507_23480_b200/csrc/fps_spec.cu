@@ -353,6 +353,7 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
         fold_one(lv.x, lv.y, lv.z, (uint32_t)last, true);
     }
 
+    const unsigned poll_ns = a.poll_ns > 0 ? (unsigned)a.poll_ns : 32u;
     uint32_t ex = 0;
     const bool tdbg = kTiming && a.dbg && b == 0 && r == 0 && warp == kLead && lane == 0;
     long long tacc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -667,7 +668,7 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
                 if (n <= k && !((pw & 0xffff0000u) == tag && (pw & 0x100u))) {
                     // nothing new: back off so the lead warp's shared-memory
                     // traffic is not queued behind the polls
-                    __nanosleep(32);
+                    __nanosleep(poll_ns);
                     continue;
                 }
                 for (; k < n; ++k) {
@@ -802,6 +803,7 @@ cudaError_t launch_fps_spec(FpsArgs a, int64_t B, cudaStream_t s) {
     a.points_per_cta = S;
     a.dbg = nullptr;
     a.spec_target = getenv("PS_SPEC_TARGET") ? atof(getenv("PS_SPEC_TARGET")) : 0.0;  // development override
+    a.poll_ns = getenv("PS_SPEC_POLL_NS") ? atoi(getenv("PS_SPEC_POLL_NS")) : 0;        // development override
     static long long* dbg = nullptr;
     const bool timing = kTiming && getenv("PS_FPS_TIMING");
     if (timing) {

@@ -21,6 +21,7 @@ struct FpsArgs {
     long long* dbg;             // development timing buffer (PS_FPS_TIMING)
     int64_t dbg_t0;             // first recorded iteration offset (PS_FPS_T0)
     double spec_target;         // fps_spec: candidates aimed for per exchange (0: default, < 0: no speculation)
+    int poll_ns;                // fps_spec: worker poll back-off in ns (0: default)
 };
 
 // Clouds split over G ranks (point-split FPS): rank g owns original indices
