@@ -1229,45 +1229,52 @@ __device__ __noinline__ void ell_rescan_row(float4 p, int32_t i, int64_t b, int6
 // takes kChunk consecutive sorted points (rows).  The points of one grid cell
 // are consecutive in sorted order and share one candidate set (the points of
 // the 3 x 3 x 3 neighbouring cells), so the warp enumerates the candidates
-// once per cell segment of its chunk, up to 32 * kSlots of them held in
-// registers (one per lane and slot; larger sets are reloaded per row in
-// windows), and runs each row of the segment against them:
+// once per cell segment of its chunk into a shared-memory window of
+// 32 * kSlots (larger sets are reloaded per row in windows) and runs the
+// segment's rows against them, kG rows at a time on 32 / kG lanes each:
 //   A. f32 screen, lanes = candidates; survivors compacted into shared memory;
 //   B. lanes = survivors (dense): exact f64 test, level bucket, rank within
-//      the bucket from ballots over the bucket bits (no atomics);
+//      the bucket from ballots over the three bucket bits (no atomics);
 //   C. scatter to the row at bucket base + rank.
-// Same row layout, buckets, spill and padding as grid_ell_kernel, whose
-// per-row candidate fetch and sparse per-hit lanes cost ~950 warp
-// instructions per C3 row.
-template <int kEllWarps, int kEllCap, int kSlots, int kChunk, int kMinBlocks>
+// Rows with more than kEllCap survivors (dense neighbourhoods) are rescanned
+// per bucket by the whole warp (ell_rescan_row).  Same row layout, buckets,
+// spill and padding as grid_ell_kernel, whose per-row candidate fetch and
+// sparse per-hit lanes cost ~950 warp instructions per C3 row (this kernel:
+// ~500 at kG = 2).
+template <int kEllWarps, int kEllCap, int kSlots, int kChunk, int kMinBlocks, int kG>
 __global__ void __launch_bounds__(kEllWarps * 32, kMinBlocks) grid_ell_cell_kernel(
     int64_t B, int64_t N, const double* __restrict__ r2_levels, int L, int64_t levels_ld, int64_t stride, GridWork g,
     ExclWork w, CsrView csr) {
     static_assert(kChunk <= 32, "one row per lane in the chunk prefetch");
-    __shared__ float4 sc[kEllWarps][32 * kSlots];  // the cell segment's candidates (window)
-    __shared__ float4 sq[kEllWarps][kEllCap];     // f32 survivors of the row (xyz, original index in w)
-    __shared__ double hd[kEllWarps][kEllCap];     // their exact d2
-    __shared__ uint16_t hb[kEllWarps][kEllCap];   // rank within the bucket
-    __shared__ uint8_t hk[kEllWarps][kEllCap];    // bucket; 0xff: not within R_max
+    static_assert(kG == 1 || kG == 2 || kG == 4, "rows per warp");
+    constexpr int kW = 32 / kG;  // lanes per row (>= 8: one lane per bucket)
+    __shared__ float4 sc[kEllWarps][32 * kSlots];    // the cell segment's candidates (window)
+    __shared__ float4 sq[kEllWarps][kG][kEllCap];    // f32 survivors of each row (xyz, original index in w)
+    __shared__ double hd[kEllWarps][kG][kEllCap];    // their exact d2
+    __shared__ uint16_t hb[kEllWarps][kG][kEllCap];  // rank within the bucket
+    __shared__ uint8_t hk[kEllWarps][kG][kEllCap];   // bucket; 0xff: not within R_max
     __shared__ double lvs[kEllWarps][32];
     __shared__ unsigned long long lvb[kEllWarps][8];
     __shared__ int tbase[kEllWarps][32];
     __shared__ int tstart[kEllWarps][32];
     __shared__ float4 qs[kEllWarps][kChunk];  // the chunk's points
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const unsigned lt = (1u << lane) - 1u;
+    const int h = lane / kW, hl = lane % kW;  // row slot, lane within the row's lanes
+    const unsigned hmask = kW == 32 ? kFull : (((1u << kW) - 1u) << (h * kW));
+    const unsigned ltw = ((1u << lane) - 1u) & hmask;
     const int64_t b = blockIdx.y;
     const float kInfF = __int_as_float(0x7f800000);
     const double my_r2 = lane < L ? r2_levels[b * levels_ld + lane] : 0.0;
     if (lane < L) lvs[warp][lane] = my_r2;
-    int rank_lt = 0, rank_st = 0;
+    int rank_lt_full = 0, rank_st = 0;
     double r2 = 0.0;
     for (int l = 0; l < L; ++l) {
         const double v = __shfl_sync(kFull, my_r2, l);
-        rank_lt += (v < my_r2) ? 1 : 0;
+        rank_lt_full += (v < my_r2) ? 1 : 0;  // lane l: #levels below level l
         rank_st += (v < my_r2 || (v == my_r2 && l < lane)) ? 1 : 0;  // stable sort position
         r2 = fmax(r2, v);
     }
+    const int rank_lt = __shfl_sync(kFull, rank_lt_full, hl);  // of level hl
     // L <= 8 levels (launcher), ascending, padded above every d2: a hit is
     // below the largest level, so its bucket #(levels <= d2) is 0 .. 7 --
     // three bits, three steps of a binary search
@@ -1337,114 +1344,126 @@ __global__ void __launch_bounds__(kEllWarps * 32, kMinBlocks) grid_ell_cell_kern
                 __syncwarp();
             };
             if (fits) load_window(0);
-            for (int sj = j; sj < jend; ++sj) {
-                const float4 p = qs[warp][sj];
+            // kG rows at a time, kW lanes per row (lane = h * kW + hl): row sj + h
+            for (int sj = j; sj < jend; sj += kG) {
+                const int myrow = sj + h;
+                const float4 p = qs[warp][myrow < jend ? myrow : j];
                 const int32_t i = __float_as_int(p.w);  // original index (grid_scatter_kernel)
-                if (i < csr.row_lo || i >= csr.row_hi) continue;  // another rank's row (warp-uniform)
-                evals += (unsigned long long)total;
-                // A. f32 screen, survivors compacted
+                // another rank's row, or past the segment: the lanes idle
+                const bool act = myrow < jend && i >= csr.row_lo && i < csr.row_hi;
+                if (act && hl == 0) evals += (unsigned long long)total;
+                // A. f32 screen of the candidates, survivors compacted per row
                 int nsv = 0;
                 for (int w0 = 0; w0 < total; w0 += 32 * kSlots) {
                     if (!fits) load_window(w0);
-                    const int ns = min(kSlots, (total - w0 + 31) >> 5);
-#pragma unroll
-                    for (int k = 0; k < kSlots; ++k) {
-                        if (k < ns) {
-                            const float4 q = sc[warp][k * 32 + lane];
-                            const bool sv = sqdist_f32(p, q) < thr;
-                            const unsigned m = __ballot_sync(kFull, sv);
-                            const int pos = nsv + __popc(m & lt);
-                            if (sv && pos < kEllCap) sq[warp][pos] = q;
+                    const int nsl = (min(32 * kSlots, total - w0) + kW - 1) / kW;
+#pragma unroll 4
+                    for (int k = 0; k < 32 * kSlots / kW; ++k) {
+                        if (k < nsl) {
+                            const float4 q = sc[warp][k * kW + hl];
+                            const bool sv = act && sqdist_f32(p, q) < thr;
+                            const unsigned m = __ballot_sync(kFull, sv) & hmask;
+                            const int pos = nsv + __popc(m & ltw);
+                            if (sv && pos < kEllCap) sq[warp][h][pos] = q;
                             nsv += __popc(m);
                         }
                     }
                 }
                 __syncwarp();
-                int64_t row_off = (int64_t)i * stride;
-                if (nsv > kEllCap || no_filter) {
-                    // more survivors than the staging holds (dense neighbourhoods only),
-                    // or levels beyond float range (no screen)
-                    ell_rescan_row(p, i, b, N, total, tbase[warp], tstart[warp], sx, r2, thr, no_filter, L, lvs[warp],
-                                   rank_lt, stride, w, csr);
-                    continue;
-                }
-                // B. dense pass over the survivors: exact test, bucket (#levels <= d2,
-                // binary search on the bit patterns of the sorted, padded levels),
-                // rank within the bucket from ballots over the three bucket bits
-                int runs = 0;  // lane t: entries of bucket t so far
-                for (int e0 = 0; e0 < nsv; e0 += 32) {
-                    const int ee = e0 + lane;
-                    const bool valid = ee < nsv;
-                    const double d = sqdist4(p, sq[warp][valid ? ee : 0]);
+                // more survivors than the staging holds (dense neighbourhoods) or
+                // levels beyond float range (no screen): the whole warp rescans
+                // that row afterwards
+                const bool ovf = act && (nsv > kEllCap || no_filter);
+                const bool dense = act && !ovf;
+                const int nmax = __reduce_max_sync(kFull, dense ? nsv : 0);
+                // B. dense pass over the survivors: exact test, bucket (#levels <=
+                // d2, binary search on the bit patterns of the sorted, padded
+                // levels), rank within the bucket from ballots over the three bits
+                int runs = 0;  // lane hl < 8 of row h: entries of bucket hl so far
+                for (int e0 = 0; e0 < nmax; e0 += kW) {
+                    const int ee = e0 + hl;
+                    const bool valid = dense && ee < nsv;
+                    const double d = sqdist4(p, sq[warp][h][valid ? ee : 0]);
                     const bool hit = valid && d < r2;
                     const unsigned long long db = (unsigned long long)__double_as_longlong(d);
                     const unsigned long long* lv = lvb[warp];
                     int bk = (lv[3] <= db) ? 4 : 0;
                     bk += (lv[bk + 1] <= db) ? 2 : 0;
                     bk += (lv[bk] <= db) ? 1 : 0;
-                    const unsigned hm = __ballot_sync(kFull, hit);
+                    const unsigned hm = __ballot_sync(kFull, hit) & hmask;
                     const unsigned m0 = __ballot_sync(kFull, hit && (bk & 1));
                     const unsigned m1 = __ballot_sync(kFull, hit && (bk & 2));
                     const unsigned m2 = __ballot_sync(kFull, hit && (bk & 4));
                     const unsigned peers = hm & ((bk & 1) ? m0 : ~m0) & ((bk & 2) ? m1 : ~m1) & ((bk & 4) ? m2 : ~m2);
-                    const unsigned mine =
-                        hm & ((lane & 1) ? m0 : ~m0) & ((lane & 2) ? m1 : ~m1) & ((lane & 4) ? m2 : ~m2);
-                    const int rank = __shfl_sync(kFull, runs, bk & 7) + __popc(peers & lt);
+                    const unsigned mine = hm & ((hl & 1) ? m0 : ~m0) & ((hl & 2) ? m1 : ~m1) & ((hl & 4) ? m2 : ~m2);
+                    const int rank = __shfl_sync(kFull, runs, h * kW + (bk & 7)) + __popc(peers & ltw);
                     runs += __popc(mine);
                     if (valid) {
-                        hk[warp][ee] = hit ? (uint8_t)bk : (uint8_t)0xff;
-                        hb[warp][ee] = (uint16_t)rank;
-                        hd[warp][ee] = d;
+                        hk[warp][h][ee] = hit ? (uint8_t)bk : (uint8_t)0xff;
+                        hb[warp][h][ee] = (uint16_t)rank;
+                        hd[warp][h][ee] = d;
                     }
                 }
-                // bucket bases: exclusive scan of the per-bucket totals
-                int hincl = lane <= L ? runs : 0;
+                // bucket bases: exclusive scan of the eight per-bucket totals of the row
+                const int v = (hl < 8 && hl <= L) ? runs : 0;
+                int hincl = v;
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int y = __shfl_up_sync(kFull, hincl, o);
-                    if (lane >= o) hincl += y;
+                for (int o = 1; o < 8; o <<= 1) {
+                    const int y = __shfl_up_sync(kFull, hincl, o, kW);
+                    if (hl >= o) hincl += y;
                 }
-                const int cnt = __shfl_sync(kFull, hincl, L);
-                const int hbase = hincl - (lane <= L ? runs : 0);
-                if (cnt > stride) {  // spill arena (see grid_ell_kernel)
-                    unsigned long long o = 0;
-                    if (lane == 0) o = atomicAdd(&w.spill[b], (unsigned long long)((cnt + 3) & ~3));
-                    o = __shfl_sync(kFull, o, 0);
-                    const int64_t off = N * stride + csr.spill_lo + (int64_t)o;
-                    if (off + cnt > N * stride + csr.spill_hi) {
-                        if (lane == 0) atomicOr(&w.status[b], 2);
-                        if (lane < L) csr.counts[(b * csr.L + lane) * N + i] = 0;
-                        __syncwarp();
-                        continue;
-                    }
+                const int cnt = __shfl_sync(kFull, hincl, h * kW + 7);
+                const int hbase = hincl - v;
+                // rows longer than the stride: a run of the spill arena (see grid_ell_kernel)
+                int64_t row_off = (int64_t)i * stride;
+                const bool spill = dense && cnt > stride;
+                unsigned long long o = 0;
+                if (spill && hl == 0) o = atomicAdd(&w.spill[b], (unsigned long long)((cnt + 3) & ~3));
+                o = __shfl_sync(kFull, o, h * kW);
+                const int64_t off = N * stride + csr.spill_lo + (int64_t)o;
+                const bool fail = spill && off + cnt > N * stride + csr.spill_hi;
+                if (fail && hl == 0) atomicOr(&w.status[b], 2);
+                if (fail && hl < L) csr.counts[(b * csr.L + hl) * N + i] = 0;
+                if (spill && !fail) {
                     row_off = off;
-                    if (lane == 0) csr.indptr[b * (N + 1) + i] = off;
+                    if (hl == 0) csr.indptr[b * (N + 1) + i] = off;
                 }
+                const bool emit = dense && !fail;
                 __syncwarp();
                 // C. scatter
                 int32_t* rn = csr.nbr + b * csr.cap_entries + row_off;
                 double* rd = csr.d2 + b * csr.cap_entries + row_off;
-                for (int e0 = 0; e0 < nsv; e0 += 32) {
-                    const int ee = e0 + lane;
-                    const int bk = ee < nsv ? hk[warp][ee] : 0xff;
-                    const int pos = __shfl_sync(kFull, hbase, bk & 31) + (ee < nsv ? hb[warp][ee] : 0);
+                for (int e0 = 0; e0 < nmax; e0 += kW) {
+                    const int ee = e0 + hl;
+                    const int bk = (emit && ee < nsv) ? hk[warp][h][ee] : 0xff;
+                    const int pos = __shfl_sync(kFull, hbase, h * kW + (bk & 7)) + (bk != 0xff ? hb[warp][h][ee] : 0);
                     if (bk != 0xff) {
-                        __stcs(rd + pos, hd[warp][ee]);  // d2 streams to HBM: keep L2 for the nbr rows
-                        rn[pos] = __float_as_int(sq[warp][ee].w);
+                        __stcs(rd + pos, hd[warp][h][ee]);  // d2 streams to HBM: keep L2 for the nbr rows
+                        rn[pos] = __float_as_int(sq[warp][h][ee].w);
                     }
                 }
-                // level l holds buckets 0 .. rank_lt(l)
-                const int hist_mine = __shfl_sync(kFull, hincl, rank_lt < 31 ? rank_lt : 31);
-                if (lane < L) csr.counts[(b * csr.L + lane) * N + i] = hist_mine;
+                // level l = hl holds buckets 0 .. rank_lt(l)
+                const int hist = __shfl_sync(kFull, hincl, h * kW + (rank_lt < 7 ? rank_lt : 7));
+                if (emit && hl < L) csr.counts[(b * csr.L + hl) * N + i] = hist;
                 {
+                    // pad the row to a whole 16-byte chunk (readers load int4 chunks, masked by the counts)
                     const int64_t row_cap = row_off == (int64_t)i * stride ? stride : ((cnt + 3) & ~3);
-                    if (lane < min((int64_t)((cnt + 3) & ~3), row_cap) - cnt) rn[cnt + lane] = -1;
+                    if (emit && hl < min((int64_t)((cnt + 3) & ~3), row_cap) - cnt) rn[cnt + hl] = -1;
                 }
                 __syncwarp();
+                // overflowing rows, one at a time by the whole warp
+                for (unsigned om = __ballot_sync(kFull, ovf && hl == 0); om; om &= om - 1) {
+                    const int r0w = sj + (__ffs(om) - 1) / kW;
+                    const float4 pr = qs[warp][r0w];
+                    ell_rescan_row(pr, __float_as_int(pr.w), b, N, total, tbase[warp], tstart[warp], sx, r2, thr,
+                                   no_filter, L, lvs[warp], rank_lt_full, stride, w, csr);
+                }
             }
             j = jend;
         }
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) evals += __shfl_xor_sync(kFull, evals, o);  // rows of every lane group
     if (lane == 0 && evals) atomicAdd(g.evals + b, evals);
 }
 
@@ -1523,11 +1542,18 @@ cudaError_t launch_excl_build(const float4* xyz, int64_t B, int64_t N, const dou
         if (method == 2) {
             if (reach == 1 && L <= 8 && !getenv("PS_ELL_ROW")) {
                 // warp per chunk of sorted rows, candidates per cell segment in registers
-                // (C3: 260 vs 276 us for the stage with grid_ell_kernel, PS_ELL_ROW=1)
+                // (C3: stage 204 vs 265 us with grid_ell_kernel, PS_ELL_ROW=1)
                 constexpr int kWc = 4, kChunk = 16;
                 const int64_t gxc = std::max<int64_t>(1, (N + kWc * kChunk - 1) / (kWc * kChunk));
-                grid_ell_cell_kernel<kWc, 128, 8, kChunk, 7><<<dim3((unsigned)gxc, (unsigned)B), kWc * 32, 0, s>>>(
-                    B, N, r2_levels, L, levels_ld, stride, g, w, csr);
+                // two rows per warp, 16 lanes each: the per-row bookkeeping (bucket
+                // scan, spill check, counts, padding) serves both rows at once (C3:
+                // 97 M vs 119 M instructions with one row per warp, PS_ELL_G=1)
+                if (getenv("PS_ELL_G") && atoi(getenv("PS_ELL_G")) == 1)
+                    grid_ell_cell_kernel<kWc, 128, 8, kChunk, 7, 1><<<dim3((unsigned)gxc, (unsigned)B), kWc * 32, 0, s>>>(
+                        B, N, r2_levels, L, levels_ld, stride, g, w, csr);
+                else
+                    grid_ell_cell_kernel<kWc, 96, 8, kChunk, 5, 2><<<dim3((unsigned)gxc, (unsigned)B), kWc * 32, 0, s>>>(
+                        B, N, r2_levels, L, levels_ld, stride, g, w, csr);
             } else if (reach == 1 && stride <= 256) {
                 constexpr int kW = 8;
                 const int64_t gx = std::max<int64_t>(1, std::min<int64_t>((148 * 16 + B - 1) / B, (N + kW - 1) / kW));
