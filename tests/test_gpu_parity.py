@@ -451,9 +451,42 @@ def test_excl_bucketed_rows_dense(reach, monkeypatch):
     _check_bucketed_rows(generate_cloud("uniform-box", 6000, 8), [0.21, 0.2, 0.17, 0.15, 0.12, 0.1], 0.05, 300)
 
 
+@pytest.mark.parametrize("variant", ["auto", "1", "row"])
+@pytest.mark.parametrize("family,N,R", [("uniform-box", 6000, 0.05), ("lattice", 4096, 0.1000001),
+                                        ("gaussian-clusters", 3000, 0.02), ("uniform-box", 700, 3.0),
+                                        ("lidar-rings", 5000, 1e-30), ("uniform-box", 1, 0.1),
+                                        ("room-surfaces", 7, 0.5)])
+def test_excl_bucketed_rows_families(family, N, R, variant, monkeypatch):
+    """Method-2 rows for every row kernel on the families of
+    test_excl_matches_oracle: lattice ties, dense clusters, a radius above the
+    cloud's diameter (every row the whole cloud: rescans), no neighbour at all,
+    one- and seven-point clouds."""
+    _set_excl_variant(variant, monkeypatch)
+    _check_bucketed_rows(generate_cloud(family, N, 77), [R, R * 0.8, R * 0.5], R * 0.6, None)
+
+
+def test_excl_bucketed_rows_many_levels():
+    """Ten levels (eight segments + two baked radii): beyond the cell
+    kernel's eight buckets, the build takes the per-row kernel."""
+    R = [0.3, 0.28, 0.25, 0.21, 0.18, 0.15, 0.12, 0.1]
+    c = generate_cloud("room-surfaces", 5000, 9)
+    e = O.build_exclusion_lists(c, R, (0.13, 0.07))
+    levels = np.array([O.radius_sq(r) for r in R] + [O.radius_sq(0.13), O.radius_sq(0.07)])
+    csr = engine.DeviceCsr.allocate(1, 5000, len(levels), 5000 * 256, 1, torch.device("cuda"), 2)
+    csr.levels.copy_(torch.from_numpy(levels.reshape(1, -1)))
+    csr.build(engine.as_xyz4(c))
+    assert not csr.overflowed()
+    counts = csr.counts[0].cpu().numpy()
+    pos = {float(v): k for k, v in enumerate(e.r2_levels)}
+    for l, lv in enumerate(levels):
+        np.testing.assert_array_equal(counts[l], e.counts[pos[float(lv)]])
+
+
 def _check_bucketed_rows(c, R, extra, cap_per_point):
     N = c.shape[0]
     e = O.build_exclusion_lists(c, R, (extra,))
+    if cap_per_point is None:  # room for the longest row in the strided part
+        cap_per_point = max(16, int(1.25 * int(e.counts[-1].max())) + 8)
     levels = np.array([O.radius_sq(r) for r in R] + [O.radius_sq(extra)])
     csr = engine.DeviceCsr.allocate(1, N, len(levels), N * cap_per_point, 1, torch.device("cuda"), 2)
     csr.levels.copy_(torch.from_numpy(levels.reshape(1, -1)))
