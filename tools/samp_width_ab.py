@@ -1,5 +1,6 @@
-"""Sampler stage time (C3 bench batch, latency mode) at the current
-PS_SAMPLER_CLUSTER width, median of 21 CUDA-event-timed runs."""
+"""Sampler stage time (C3 bench batch, latency mode; --c4: the C4 per-GPU
+share, B=2 room clouds N=65536 -> 16384) at the current PS_SAMPLER_* knobs,
+median of 21 CUDA-event-timed runs."""
 import os
 import sys
 
@@ -9,10 +10,20 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 from paper_2507_23480_b200 import engine  # noqa: E402
 
-B = bench.B_PER_GPU
-fp = engine.FastPoint(B, bench.N, bench.n_SAMPLES, p=bench.P, nseg=bench.NSEG, estimator="power",
-                      exponent=bench.heldout_exponent(), extra_radii=(bench.RADIUS,))
-fp.set_points(torch.from_numpy(bench.clouds_for(0, B)).cuda())
+if "--c4" in sys.argv:
+    import numpy as np
+
+    from paper_2507_23480_b200.harness import generate_cloud
+    B, N, n = 2, 65536, 16384
+    clouds = np.stack([generate_cloud(bench.FAMILY, N, 3000 + b) for b in range(B)])
+    fp = engine.FastPoint(B, N, n, p=bench.P, nseg=bench.NSEG, estimator="power", exponent=0.536,
+                          extra_radii=(bench.RADIUS,))
+    fp.set_points(torch.from_numpy(clouds).cuda())
+else:
+    B = bench.B_PER_GPU
+    fp = engine.FastPoint(B, bench.N, bench.n_SAMPLES, p=bench.P, nseg=bench.NSEG, estimator="power",
+                          exponent=bench.heldout_exponent(), extra_radii=(bench.RADIUS,))
+    fp.set_points(torch.from_numpy(bench.clouds_for(0, B)).cuda())
 fp.set_rng(list(range(B)))
 fp.sample()
 fp.check()
@@ -32,4 +43,5 @@ fp.sample()
 torch.cuda.synchronize()
 ok = torch.equal(fp.out, ref)
 ts.sort()
-print(f"C={os.environ.get('PS_SAMPLER_CLUSTER', 'default')}: sampler {1e3 * ts[len(ts) // 2]:.1f} us (min {1e3 * ts[0]:.1f}), same indices {ok}")
+knobs = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith("PS_SAMPLER")) or "default"
+print(f"{knobs}: sampler {1e3 * ts[len(ts) // 2]:.1f} us (min {1e3 * ts[0]:.1f}), same indices {ok}")
