@@ -1358,15 +1358,13 @@ __global__ void __launch_bounds__(kEllWarps * 32, kMinBlocks) grid_ell_cell_kern
                     if (!fits) load_window(w0);
                     const int nsl = (min(32 * kSlots, total - w0) + kW - 1) / kW;
 #pragma unroll 4
-                    for (int k = 0; k < 32 * kSlots / kW; ++k) {
-                        if (k < nsl) {
-                            const float4 q = sc[warp][k * kW + hl];
-                            const bool sv = act && sqdist_f32(p, q) < thr;
-                            const unsigned m = __ballot_sync(kFull, sv) & hmask;
-                            const int pos = nsv + __popc(m & ltw);
-                            if (sv && pos < kEllCap) sq[warp][h][pos] = q;
-                            nsv += __popc(m);
-                        }
+                    for (int k = 0; k < nsl; ++k) {
+                        const float4 q = sc[warp][k * kW + hl];
+                        const bool sv = act && sqdist_f32(p, q) < thr;
+                        const unsigned m = __ballot_sync(kFull, sv) & hmask;
+                        const int pos = nsv + __popc(m & ltw);
+                        if (sv && pos < kEllCap) sq[warp][h][pos] = q;
+                        nsv += __popc(m);
                     }
                 }
                 __syncwarp();
