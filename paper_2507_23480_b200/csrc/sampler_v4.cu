@@ -180,6 +180,15 @@ PS_DEV uint8_t ld_cluster_u8(uint32_t addr) {
     asm volatile("ld.shared::cluster.u8 %0, [%1];" : "=h"(v) : "r"(addr) : "memory");
     return (uint8_t)v;
 }
+// relaxed cluster-scope state accesses (the MIS dataflow polls them)
+PS_DEV uint8_t ld_cluster_u8_rlx(uint32_t addr) {
+    uint16_t v;
+    asm volatile("ld.relaxed.cluster.shared::cluster.u8 %0, [%1];" : "=h"(v) : "r"(addr) : "memory");
+    return (uint8_t)v;
+}
+PS_DEV void st_shared_u8_rlx(uint32_t addr, uint8_t v) {
+    asm volatile("st.relaxed.cluster.shared::cta.u8 [%0], %1;" ::"r"(addr), "h"((uint16_t)v) : "memory");
+}
 PS_DEV void red_cluster_max(uint32_t addr, uint32_t v) {
     asm volatile("red.shared::cluster.max.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
@@ -639,10 +648,10 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
             ow -= (ow * tspan32 > (uint32_t)q) ? 1u : 0u;
             ow += ((ow + 1u) * tspan32 <= (uint32_t)q) ? 1u : 0u;
             const uint32_t lq = (uint32_t)q - ow * tspan32;
-            return ld_cluster_u8(mapa(st_base + lq, ow));
+            return ld_cluster_u8_rlx(mapa(st_base + lq, ow));
         };
         auto st_set = [&](int t, uint8_t v) {
-            if (kSm) *reinterpret_cast<volatile uint8_t*>(st_s + (t - tlo)) = v;
+            if (kSm) st_shared_u8_rlx(st_base + (uint32_t)(t - tlo), v);
             else st_st(stt + t, v);
         };
         // decided count: every CTA's cumulative count pushed into every CTA's
@@ -750,69 +759,130 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
             }
         }
         VT4(19);
-        int total_dec = publish(decided);
-        VT4(6);
-        while (total_dec < L) {
-            if (tdbg) s_acc[12] += 1;
-            int dd = 0;
+        if (!a.rounds) {
+            // Dataflow: every thread settles its undecided draws in draw order,
+            // polling the states of their undecided earlier neighbours until
+            // one is IN (-> OUT) or all are OUT (-> IN) -- no barrier between
+            // "rounds".  Progress: the smallest undecided draw has only decided
+            // predecessors, and its owner thread is at it (each thread walks its
+            // draws in increasing order); the CTAs of a cloud are co-resident.
             for (int t = tlo + tid; t < thi; t += kT4) {
                 if (st_get(t) != kUnd4) continue;
-                bool outf = false, blocked = false;
-                const uint8_t np = npred[t];
-                if (np != kPredOvf) {
-                    for (int k0p = 0; k0p < np && !outf; k0p += 16) {
-                        int pr[16];
+                for (int spin = 0;; ++spin) {
+                    bool outf = false, blocked = false;
+                    const uint8_t np = npred[t];
+                    if (np != kPredOvf) {
+                        for (int k0p = 0; k0p < np && !outf; k0p += 16) {
+                            int pr[16];
 #pragma unroll
-                        for (int k = 0; k < 16; ++k) pr[k] = k0p + k < np ? preds[(int64_t)t * kPred4 + k0p + k] : -1;
-                        uint8_t sq[16];
+                            for (int k = 0; k < 16; ++k) pr[k] = k0p + k < np ? preds[(int64_t)t * kPred4 + k0p + k] : -1;
+                            uint8_t sq[16];
 #pragma unroll
-                        for (int k = 0; k < 16; ++k) sq[k] = pr[k] >= 0 ? st_get(pr[k]) : kOut4;
+                            for (int k = 0; k < 16; ++k) sq[k] = pr[k] >= 0 ? st_get(pr[k]) : kOut4;
 #pragma unroll
-                        for (int k = 0; k < 16; ++k) {
-                            outf = outf || sq[k] == kIn4;
-                            blocked = blocked || sq[k] == kUnd4;
+                            for (int k = 0; k < 16; ++k) {
+                                outf = outf || sq[k] == kIn4;
+                                blocked = blocked || sq[k] == kUnd4;
+                            }
+                        }
+                    } else {
+                        if (a.dbg && b == 0) atomicAdd((unsigned long long*)&a.dbg[15], 1ull);
+                        // more than kPred4 undecided predecessors: rescan the neighbours
+                        const int32_t c = cand[t];
+                        const uint8_t nc = kSm ? kAdjOvf : adjcnt[c];
+                        const int32_t m = nc != kAdjOvf ? (int32_t)nc : cnt_lvl[c];
+                        const int32_t* row = nc != kAdjOvf ? adj + (int64_t)c * kAdj4 : nbr + indptr[c];
+                        for (int32_t u0 = 0; u0 < m && !outf; u0 += kRB) {
+                            int32_t qq[kRB];
+#pragma unroll
+                            for (int k = 0; k < kRB; ++k) qq[k] = (u0 + k < m) ? row[u0 + k] : -1;
+                            uint8_t av[kRB];
+#pragma unroll
+                            for (int k = 0; k < kRB; ++k)
+                                av[k] = (qq[k] >= 0 && qq[k] != c) ? (nc != kAdjOvf ? 1 : avail[qq[k]]) : 0;
+                            int rq[kRB];
+#pragma unroll
+                            for (int k = 0; k < kRB; ++k) rq[k] = av[k] ? rank[qq[k]] : 0x7fffffff;
+                            uint8_t sq[kRB];
+#pragma unroll
+                            for (int k = 0; k < kRB; ++k) sq[k] = rq[k] < t ? st_get(rq[k]) : kOut4;
+#pragma unroll
+                            for (int k = 0; k < kRB; ++k) {
+                                outf = outf || sq[k] == kIn4;
+                                blocked = blocked || sq[k] == kUnd4;
+                            }
                         }
                     }
-                } else {
-                    if (a.dbg && b == 0) atomicAdd((unsigned long long*)&a.dbg[15], 1ull);
-                    // more than kPred4 undecided predecessors: rescan the neighbours
-                    const int32_t c = cand[t];
-                    const uint8_t nc = kSm ? kAdjOvf : adjcnt[c];
-                    const int32_t m = nc != kAdjOvf ? (int32_t)nc : cnt_lvl[c];
-                    const int32_t* row = nc != kAdjOvf ? adj + (int64_t)c * kAdj4 : nbr + indptr[c];
-                    for (int32_t u0 = 0; u0 < m && !outf; u0 += kRB) {
-                        int32_t qq[kRB];
-#pragma unroll
-                        for (int k = 0; k < kRB; ++k) qq[k] = (u0 + k < m) ? row[u0 + k] : -1;
-                        uint8_t av[kRB];
-#pragma unroll
-                        for (int k = 0; k < kRB; ++k)
-                            av[k] = (qq[k] >= 0 && qq[k] != c) ? (nc != kAdjOvf ? 1 : avail[qq[k]]) : 0;
-                        int rq[kRB];
-#pragma unroll
-                        for (int k = 0; k < kRB; ++k) rq[k] = av[k] ? rank[qq[k]] : 0x7fffffff;
-                        uint8_t sq[kRB];
-#pragma unroll
-                        for (int k = 0; k < kRB; ++k) sq[k] = rq[k] < t ? st_get(rq[k]) : kOut4;
-#pragma unroll
-                        for (int k = 0; k < kRB; ++k) {
-                            outf = outf || sq[k] == kIn4;
-                            blocked = blocked || sq[k] == kUnd4;
-                        }
-                    }
-                }
-                if (outf) {
-                    st_set(t, kOut4);
-                    ++dd;
-                } else if (!blocked) {
-                    st_set(t, kIn4);
-                    ++dd;
+                    if (outf) { st_set(t, kOut4); break; }
+                    if (!blocked) { st_set(t, kIn4); break; }
+                    __nanosleep(spin < 8 ? 32 : 128);
                 }
             }
-            VT4(20);
-            total_dec = publish(dd);
+            VT4(6);
+        } else {
+            int total_dec = publish(decided);
+            VT4(6);
+            while (total_dec < L) {
+                if (tdbg) s_acc[12] += 1;
+                int dd = 0;
+                for (int t = tlo + tid; t < thi; t += kT4) {
+                    if (st_get(t) != kUnd4) continue;
+                    bool outf = false, blocked = false;
+                    const uint8_t np = npred[t];
+                    if (np != kPredOvf) {
+                        for (int k0p = 0; k0p < np && !outf; k0p += 16) {
+                            int pr[16];
+#pragma unroll
+                            for (int k = 0; k < 16; ++k) pr[k] = k0p + k < np ? preds[(int64_t)t * kPred4 + k0p + k] : -1;
+                            uint8_t sq[16];
+#pragma unroll
+                            for (int k = 0; k < 16; ++k) sq[k] = pr[k] >= 0 ? st_get(pr[k]) : kOut4;
+#pragma unroll
+                            for (int k = 0; k < 16; ++k) {
+                                outf = outf || sq[k] == kIn4;
+                                blocked = blocked || sq[k] == kUnd4;
+                            }
+                        }
+                    } else {
+                        if (a.dbg && b == 0) atomicAdd((unsigned long long*)&a.dbg[15], 1ull);
+                        // more than kPred4 undecided predecessors: rescan the neighbours
+                        const int32_t c = cand[t];
+                        const uint8_t nc = kSm ? kAdjOvf : adjcnt[c];
+                        const int32_t m = nc != kAdjOvf ? (int32_t)nc : cnt_lvl[c];
+                        const int32_t* row = nc != kAdjOvf ? adj + (int64_t)c * kAdj4 : nbr + indptr[c];
+                        for (int32_t u0 = 0; u0 < m && !outf; u0 += kRB) {
+                            int32_t qq[kRB];
+#pragma unroll
+                            for (int k = 0; k < kRB; ++k) qq[k] = (u0 + k < m) ? row[u0 + k] : -1;
+                            uint8_t av[kRB];
+#pragma unroll
+                            for (int k = 0; k < kRB; ++k)
+                                av[k] = (qq[k] >= 0 && qq[k] != c) ? (nc != kAdjOvf ? 1 : avail[qq[k]]) : 0;
+                            int rq[kRB];
+#pragma unroll
+                            for (int k = 0; k < kRB; ++k) rq[k] = av[k] ? rank[qq[k]] : 0x7fffffff;
+                            uint8_t sq[kRB];
+#pragma unroll
+                            for (int k = 0; k < kRB; ++k) sq[k] = rq[k] < t ? st_get(rq[k]) : kOut4;
+#pragma unroll
+                            for (int k = 0; k < kRB; ++k) {
+                                outf = outf || sq[k] == kIn4;
+                                blocked = blocked || sq[k] == kUnd4;
+                            }
+                        }
+                    }
+                    if (outf) {
+                        st_set(t, kOut4);
+                        ++dd;
+                    } else if (!blocked) {
+                        st_set(t, kIn4);
+                        ++dd;
+                    }
+                }
+                VT4(20);
+                total_dec = publish(dd);
+            }
         }
-
         VT4(7);
         // ---- P5: truncation at the segment boundary --------------------------------------
         const int64_t need = a.boundaries[seg] - i;
@@ -944,6 +1014,7 @@ cudaError_t launch_sampler_v4(SampArgs a, int64_t B, cudaStream_t s) {
     // one CTA per cloud and room for 7 int32 arrays of N + the scratch: tiny layout
     const size_t dsm_tiny = ((dsm + 15) & ~(size_t)15) + 7 * 4 * (size_t)Npad + 4 * kScr;
     a.tiny = (sm && C == 1 && dsm_tiny <= 200 * 1024 && !getenv("PS_SAMPLER_NOTINY")) ? 1 : 0;
+    a.rounds = getenv("PS_SAMPLER_ROUNDS") ? 1 : 0;
     const size_t dsm_used = a.tiny ? dsm_tiny : dsm;
     if (!sm && !getenv("PS_SAMPLER_NOGRID")) {
         // grid mode: few clouds too large for shared memory -- spread each over
