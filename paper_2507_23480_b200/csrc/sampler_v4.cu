@@ -175,11 +175,6 @@ PS_DEV uint4 ld_cluster_v4(uint32_t addr) {
     return v;
 }
 
-PS_DEV uint8_t ld_cluster_u8(uint32_t addr) {
-    uint16_t v;
-    asm volatile("ld.shared::cluster.u8 %0, [%1];" : "=h"(v) : "r"(addr) : "memory");
-    return (uint8_t)v;
-}
 // relaxed cluster-scope state accesses (the MIS dataflow polls them)
 PS_DEV uint8_t ld_cluster_u8_rlx(uint32_t addr) {
     uint16_t v;
@@ -295,10 +290,15 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
     // position of the row; INT_MAX = none), persistent over the visits
     int32_t* wpos = reinterpret_cast<int32_t*>(tkb + ((Wtk + 3) & ~(int64_t)3));
     const int64_t span_sm = ((N + C - 1) / C + 15) & ~(int64_t)15;
-    int32_t* s_cnt = wpos + span_sm;  // kSm: this visit's level counts of my range
-    int32_t* s_list = s_cnt + span_sm;  // kSm: points of my range that need a row scan
-    int64_t* s_ip = reinterpret_cast<int64_t*>(s_list + span_sm);  // kSm: their row offsets
-    uint8_t* st_s = reinterpret_cast<uint8_t*>(s_ip + span_sm);      // kSm: MIS states of my draw range
+    // kSm, per draw of my range [tlo, thi) (written by the resolution pass, read
+    // by the MIS pass of the same thread): candidate, its level count, its row
+    // offset -- the MIS pass then starts with the row loads, not with three
+    // dependent global loads
+    int32_t* d_cand = wpos + span_sm;
+    int32_t* d_cnt = d_cand + span_sm;
+    int32_t* d_row = d_cnt + span_sm;  // (16 bytes per point reserved: d_row + one spare int32)
+    uint8_t* st_s = reinterpret_cast<uint8_t*>(d_row + 2 * span_sm);  // kSm: MIS states of my draw range
+    const bool stash = kSm && a.cap_entries < (int64_t(1) << 31);
     int64_t i_tk = 0;  // sampled points already pushed
     int prev_seg = 0;  // segment of the previous visit (its accepts are pushed next)
     if (kSm) {
@@ -377,11 +377,6 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
         if (gt == 0) scr[SL::decided] = 0;
         if (kSm) {
             VT4(16);
-            // this visit's level counts and row offsets of my range, staged once (P2)
-            for (int64_t x = tid; x < jhi - jlo; x += kT4) {
-                s_cnt[x] = cnt_lvl[jlo + x];
-                s_ip[x] = indptr[jlo + x];
-            }
             VT4(17);
             // push: every point sampled since the last visit (the FPS prefix at the
             // first visit, else the previous visit's accepts) walks its row prefix
@@ -469,8 +464,8 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
                 }
                 avail[q] = 0;
             }
+            sync_grp();
         }
-        sync_grp();
         if (kSm) {
             for (int64_t j = jlo + tid; j < jhi; j += kT4) avail[j] = (uint32_t)wpos[j - jlo] <= (uint32_t)seg ? 1 : 0;
             sync_grp();
@@ -573,12 +568,23 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
         VT4(2);
         if (tdbg) { s_acc[10] += 1; s_acc[11] += L; }
 
+        // MIS states / truncation / the draws' stash: CTA r owns the draws [tlo, thi)
+        const int tspan = (L + C - 1) / C;
+        const int tlo = min(L, r * tspan), thi = min(L, tlo + tspan);
+        auto stash_draw = [&](int t, int32_t c) {
+            if (stash) {
+                d_cand[t - tlo] = c;
+                d_cnt[t - tlo] = cnt_lvl[c];
+                d_row[t - tlo] = (int32_t)indptr[c];
+            }
+        };
         // ---- P3: candidate order of all L draws ----------------------------------------
         if (a.pick_lowest) {
-            for (int t = gt; t < L; t += GT) {
+            for (int t = tlo + tid; t < thi; t += kT4) {
                 const int32_t c = pool[t];
                 cand[t] = c;
                 if (!kSm) rank[c] = t;
+                stash_draw(t, c);
             }
         } else {
             for (int t = gt; t < L; t += GT) {
@@ -602,7 +608,7 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
             }
             sync_grp();
             VT4(4);
-            for (int t = gt; t < L; t += GT) {
+            for (int t = tlo + tid; t < thi; t += kT4) {
                 // value at pos[t] before draw t: untouched -> pool; else the value
                 // moved in by its latest writer x, i.e. the value of slot L-1-x at
                 // draw x, found by following the tail-slot writers back
@@ -617,11 +623,9 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
                 }
                 cand[t] = c;
                 if (!kSm) rank[c] = t;
+                stash_draw(t, c);
             }
         }
-        // MIS states: CTA r owns the draws [tlo, thi) (also the truncation ranges)
-        const int tspan = (L + C - 1) / C;
-        const int tlo = min(L, r * tspan), thi = min(L, tlo + tspan);
         for (int t = tlo + tid; t < thi; t += kT4) {
             if (kSm) st_s[t - tlo] = kUnd4;
             else stt[t] = kUnd4;
@@ -682,7 +686,7 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
         };
         int decided = 0;
         for (int t = tlo + tid; t < thi; t += kT4) {
-            const int32_t c = cand[t];
+            const int32_t c = stash ? d_cand[t - tlo] : cand[t];
             // kSm: no adjacency lists -- the candidate scans its own row prefix
             // (availability and ranks in shared memory, states through DSMEM)
             const uint8_t nc = kSm ? kAdjOvf : adjcnt[c];
@@ -717,8 +721,8 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
                 }
             } else {
                 if (!kSm && a.dbg && b == 0) atomicAdd((unsigned long long*)&a.dbg[14], 1ull);
-                const int32_t m = cnt_lvl[c];
-                const int32_t* row = nbr + indptr[c];
+                const int32_t m = stash ? d_cnt[t - tlo] : cnt_lvl[c];
+                const int32_t* row = nbr + (stash ? (int64_t)d_row[t - tlo] : indptr[c]);
                 const bool al = (reinterpret_cast<uintptr_t>(row) & 15u) == 0;
                 constexpr int kRow = 16;
                 for (int32_t u0 = 0; u0 < m && !outf; u0 += kRow) {
