@@ -819,7 +819,7 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
                     }
                     if (outf) { st_set(t, kOut4); break; }
                     if (!blocked) { st_set(t, kIn4); break; }
-                    __nanosleep(spin < 8 ? 32 : 128);
+                    if (a.poll_ns) __nanosleep(spin < 8 ? 32 : (unsigned)a.poll_ns);
                 }
             }
             VT4(6);
@@ -1019,6 +1019,7 @@ cudaError_t launch_sampler_v4(SampArgs a, int64_t B, cudaStream_t s) {
     const size_t dsm_tiny = ((dsm + 15) & ~(size_t)15) + 7 * 4 * (size_t)Npad + 4 * kScr;
     a.tiny = (sm && C == 1 && dsm_tiny <= 200 * 1024 && !getenv("PS_SAMPLER_NOTINY")) ? 1 : 0;
     a.rounds = getenv("PS_SAMPLER_ROUNDS") ? 1 : 0;
+    a.poll_ns = getenv("PS_SAMPLER_POLL") ? atoi(getenv("PS_SAMPLER_POLL")) : 128;
     const size_t dsm_used = a.tiny ? dsm_tiny : dsm;
     if (!sm && !getenv("PS_SAMPLER_NOGRID")) {
         // grid mode: few clouds too large for shared memory -- spread each over
