@@ -82,9 +82,23 @@ PS_DEV void bq_rf_one(const BqArgs& a, int64_t g, double* ld, int32_t* li, int l
         if (lane == 0) a.cnt_out[g] = -1;
         return;
     }
-    const int32_t cnt = a.counts[(b * a.L + a.level) * a.N + c];
+    const int32_t cnt0 = a.counts[(b * a.L + a.level) * a.N + c];
     const int64_t base = b * a.cap_entries + a.indptr[b * (a.N + 1) + c];
-    const int m = cnt < K ? cnt : K;
+    const int m = cnt0 < K ? cnt0 : K;
+    // Only the k nearest are reported, and every level is a row prefix: the
+    // shortest level prefix holding >= k of the query level's entries holds
+    // the k nearest (the k-th nearest lies below that level's radius) -- rank
+    // that prefix instead of the whole query level (C5: ~270 -> ~40 entries).
+    int32_t cnt = cnt0;
+    if (cnt0 > K) {
+        uint32_t cl = 0xffffffffu;
+        if (lane < a.L) {
+            const int32_t v = a.counts[(b * a.L + lane) * a.N + c];
+            if (v >= K && v <= cnt0) cl = (uint32_t)v;
+        }
+        cl = __reduce_min_sync(kFull, cl);
+        if (cl < (uint32_t)cnt0) cnt = (int32_t)cl;
+    }
     if (cnt <= 64) {
         double d0 = lane < cnt ? a.d2[base + lane] : kInf;
         int32_t i0 = lane < cnt ? a.nbr[base + lane] : 0x7fffffff;
