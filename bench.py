@@ -240,6 +240,13 @@ def cpu_baseline(clouds, exponent, gpu_idx, runs):
             "indices_bit_exact_vs_gpu": match}
 
 
+def workload_config(ws: int, exponent: float) -> dict:
+    """The workload both arms run (identical in their JSON lines)."""
+    return {"workload": WORKLOAD, "family": FAMILY, "B_per_gpu": B_PER_GPU, "B": B_PER_GPU,
+            "global_batch": B_PER_GPU * ws, "N": N, "n": n_SAMPLES, "p": P, "nseg": NSEG, "radius": RADIUS, "k": K,
+            "exponent": round(exponent, 6), "parallelism": f"batch-shard x{ws}"}
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -260,8 +267,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "family": FAMILY, "B": B_PER_GPU, "B_per_gpu": B_PER_GPU, "N": N,
-                       "n": n_SAMPLES},
+            "config": workload_config(ws, exponent),
             "us_per_cloud": 1e6 * t / (args.steps * B_PER_GPU),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
                              "cpu": cpu_model()},
@@ -622,10 +628,8 @@ def main_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "family": FAMILY, "B_per_gpu": B, "B": B, "global_batch": B * ws,
-                       "N": N, "n": n_SAMPLES, "p": P, "nseg": NSEG, "radius": RADIUS, "k": K,
-                       "exponent": round(exponent, 6), "parallelism": f"batch-shard x{ws}",
-                       "streams": S,
+            "config": workload_config(ws, exponent),
+            "method": {"streams": S,
                        "l2": (f"inputs larger than L2: a ring of {R} distinct batches "
                               f"({R * B * N * 12 / 2**20:.0f} MiB of float32 coordinates) cycled step by step; "
                               "stage breakdown: 512 MiB flush between steps")},
