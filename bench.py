@@ -960,7 +960,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 point-split line")
     ap.add_argument("--no-extra", action="store_true", help="skip the C2 / C4 objects")
-    ap.add_argument("--streams", type=int, default=5, help="concurrent FastPoint chains (streams)")
+    ap.add_argument("--streams", type=int, default=8, help="concurrent FastPoint chains (streams)")
     ap.add_argument("--cpu-runs", type=int, default=5, help="timed CPU-baseline runs per thread setting (median)")
     ap.add_argument("--c5-split", action="store_true",
                     help="N > 1: also run C5 point-split over the job's GPUs (CUDA IPC + NVLink)")
