@@ -176,10 +176,13 @@ PS_DEV uint4 ld_cluster_v4(uint32_t addr) {
 }
 
 // relaxed cluster-scope state accesses (the MIS dataflow polls them)
-PS_DEV uint8_t ld_cluster_u8_rlx(uint32_t addr) {
+PS_DEV uint8_t ld_shared_u8_rlx(uint32_t addr) {
     uint16_t v;
-    asm volatile("ld.relaxed.cluster.shared::cluster.u8 %0, [%1];" : "=h"(v) : "r"(addr) : "memory");
+    asm volatile("ld.relaxed.cluster.shared::cta.u8 %0, [%1];" : "=h"(v) : "r"(addr) : "memory");
     return (uint8_t)v;
+}
+PS_DEV void st_cluster_u8_rlx(uint32_t addr, uint8_t v) {
+    asm volatile("st.relaxed.cluster.shared::cluster.u8 [%0], %1;" ::"r"(addr), "h"((uint16_t)v) : "memory");
 }
 PS_DEV void st_shared_u8_rlx(uint32_t addr, uint8_t v) {
     asm volatile("st.relaxed.cluster.shared::cta.u8 [%0], %1;" ::"r"(addr), "h"((uint16_t)v) : "memory");
@@ -273,7 +276,7 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
         // shared-memory latency for the draw resolution and the pool)
         const int64_t Np = (N + 15) & ~(int64_t)15;
         const int64_t sp0 = ((N + 15) & ~(int64_t)15);
-        const int64_t base0 = Np + 4 * Np + 4 * (((N + 31) / 32 + 3) & ~(int64_t)3) + 21 * sp0;
+        const int64_t base0 = Np + 4 * Np + 4 * (((N + 31) / 32 + 3) & ~(int64_t)3) + 20 * sp0 + Np;
         int32_t* t0 = reinterpret_cast<int32_t*>(dsm4 + ((base0 + 15) & ~(int64_t)15));
         pool = t0;
         pos = reinterpret_cast<uint32_t*>(t0 + Np);
@@ -297,7 +300,10 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
     int32_t* d_cand = wpos + span_sm;
     int32_t* d_cnt = d_cand + span_sm;
     int32_t* d_row = d_cnt + span_sm;  // (16 bytes per point reserved: d_row + one spare int32)
-    uint8_t* st_s = reinterpret_cast<uint8_t*>(d_row + 2 * span_sm);  // kSm: MIS states of my draw range
+    // kSm: MIS states of ALL draws, replicated in every CTA of the cluster: the
+    // owner of a draw stores its decision into every copy, readers (first pass,
+    // dataflow polls) load their local copy
+    uint8_t* st_s = reinterpret_cast<uint8_t*>(d_row + 2 * span_sm);
     const bool stash = kSm && a.cap_entries < (int64_t(1) << 31);
     int64_t i_tk = 0;  // sampled points already pushed
     int prev_seg = 0;  // segment of the previous visit (its accepts are pushed next)
@@ -319,7 +325,7 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
     };
     if (kSm && a.tiny) {
         const int64_t Np = (N + 15) & ~(int64_t)15;
-        const int64_t base0 = Np + 4 * Np + 4 * (((N + 31) / 32 + 3) & ~(int64_t)3) + 21 * Np;
+        const int64_t base0 = Np + 4 * Np + 4 * (((N + 31) / 32 + 3) & ~(int64_t)3) + 20 * Np + Np;
         scr = reinterpret_cast<int32_t*>(dsm4 + ((base0 + 15) & ~(int64_t)15)) + 7 * Np;
     }
     int64_t* out = a.out_idx + b * a.ld_out;
@@ -626,9 +632,10 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
                 stash_draw(t, c);
             }
         }
-        for (int t = tlo + tid; t < thi; t += kT4) {
-            if (kSm) st_s[t - tlo] = kUnd4;
-            else stt[t] = kUnd4;
+        if (kSm) {
+            for (int t = tid; t < L; t += kT4) st_s[t] = kUnd4;
+        } else {
+            for (int t = tlo + tid; t < thi; t += kT4) stt[t] = kUnd4;
         }
         sync_grp();
         if (kSm) {
@@ -644,19 +651,19 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
         const uint32_t st_base = kSm ? smem_u32(st_s) : 0u;
         const uint32_t tspan32 = (uint32_t)max(tspan, 1);
         const uint32_t inv_tspan = 0xffffffffu / tspan32 + 1u;
+        (void)inv_tspan;
         auto st_get = [&](int q) -> uint8_t {
             if (!kSm) return ld_st(stt + q);
-            // owner = q / tspan by multiply-high (+-1 fix), read through the
-            // cluster window for every owner (no branch: independent loads pipeline)
-            uint32_t ow = __umulhi((uint32_t)q, inv_tspan);
-            ow -= (ow * tspan32 > (uint32_t)q) ? 1u : 0u;
-            ow += ((ow + 1u) * tspan32 <= (uint32_t)q) ? 1u : 0u;
-            const uint32_t lq = (uint32_t)q - ow * tspan32;
-            return ld_cluster_u8_rlx(mapa(st_base + lq, ow));
+            return ld_shared_u8_rlx(st_base + (uint32_t)q);  // the local copy
         };
         auto st_set = [&](int t, uint8_t v) {
-            if (kSm) st_shared_u8_rlx(st_base + (uint32_t)(t - tlo), v);
-            else st_st(stt + t, v);
+            if (!kSm) {
+                st_st(stt + t, v);
+            } else if (C == 1) {
+                st_shared_u8_rlx(st_base + (uint32_t)t, v);
+            } else {
+                for (int ow = 0; ow < C; ++ow) st_cluster_u8_rlx(mapa(st_base + (uint32_t)t, (uint32_t)ow), v);
+            }
         };
         // decided count: every CTA's cumulative count pushed into every CTA's
         // shared slot (double-buffered by round parity), summed after the barrier
@@ -1013,11 +1020,11 @@ cudaError_t launch_sampler_v4(SampArgs a, int64_t B, cudaStream_t s) {
     cudaError_t e = cudaSuccess;
     const int64_t Npad = (N + 15) & ~(int64_t)15;
     const int64_t span0 = ((N + C - 1) / C + 15) & ~(int64_t)15;
-    const size_t dsm = (size_t)(Npad + 4 * Npad + 4 * (((N + 31) / 32 + 3) & ~(int64_t)3) + 21 * span0);
-    const bool sm = dsm <= 200 * 1024 && !getenv("PS_SAMPLER_GLOBAL");
+    const size_t dsm = (size_t)(Npad + 4 * Npad + 4 * (((N + 31) / 32 + 3) & ~(int64_t)3) + 20 * span0 + Npad);
+    const bool sm = dsm <= 220 * 1024 && !getenv("PS_SAMPLER_GLOBAL");
     // one CTA per cloud and room for 7 int32 arrays of N + the scratch: tiny layout
     const size_t dsm_tiny = ((dsm + 15) & ~(size_t)15) + 7 * 4 * (size_t)Npad + 4 * kScr;
-    a.tiny = (sm && C == 1 && dsm_tiny <= 200 * 1024 && !getenv("PS_SAMPLER_NOTINY")) ? 1 : 0;
+    a.tiny = (sm && C == 1 && dsm_tiny <= 220 * 1024 && !getenv("PS_SAMPLER_NOTINY")) ? 1 : 0;
     a.rounds = getenv("PS_SAMPLER_ROUNDS") ? 1 : 0;
     a.poll_ns = getenv("PS_SAMPLER_POLL") ? atoi(getenv("PS_SAMPLER_POLL")) : 128;
     const size_t dsm_used = a.tiny ? dsm_tiny : dsm;
