@@ -868,7 +868,7 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) grid_rows_kernel(int64_t B,
 // instances: 8 warps x 256 entries for short rows (C1-C4), 4 warps x 512
 // for strides above 256 (C5-sized clouds, ~270 entries per row), so that
 // the rescan stays rare.
-template <int kEllWarps, int kEllCap, bool kCull>
+template <int kEllWarps, int kEllCap, bool kCull, bool kDense = false>
 __global__ void __launch_bounds__(kEllWarps * 32, 1024 / (kEllWarps * 32)) grid_ell_kernel(
     int64_t B, int64_t N, const double* __restrict__ r2_levels, int L, int64_t levels_ld, int64_t stride, GridWork g,
     ExclWork w, CsrView csr) {
@@ -987,6 +987,110 @@ __global__ void __launch_bounds__(kEllWarps * 32, 1024 / (kEllWarps * 32)) grid_
 #pragma unroll
         for (int q = 0; q < 8; ++q) e[q] = __shfl_sync(kFull, excl0, q + 1);
         __syncwarp();
+        if constexpr (kDense) {
+            // Long rows (kCull, L <= 15): A. f32 screen of the candidates, the
+            // survivors' sorted positions compacted; B. lanes = survivors:
+            // exact f64 test, bucket, rank within the bucket from ballots over
+            // the four bucket bits; C. scatter -- no divergent per-hit work in
+            // the candidate loop, no shared-memory atomics (the long-row form
+            // of grid_ell_cell_kernel's phases)
+            evals += (unsigned long long)total;
+            int nsv = 0;
+#pragma unroll 4
+            for (int tb = 0; tb < total; tb += 32) {
+                const int f = tb + lane;
+                int rc = 0;
+#pragma unroll
+                for (int st = 16; st > 0; st >>= 1) rc += (__shfl_sync(kFull, excl0, rc + st - 1) <= f) ? st : 0;
+                const int t = tbase[warp][rc - 1] + f;
+                bool sv = false;
+                if (f < total) sv = no_filter || sqdist_f32(p, sx[t]) < thr;
+                const unsigned m = __ballot_sync(kFull, sv);
+                const int pos = nsv + __popc(m & lt);
+                if (sv && pos < kEllCap) hj[warp][pos] = t;
+                nsv += __popc(m);
+            }
+            __syncwarp();
+            if (nsv <= kEllCap) {
+                int runs = 0;  // lane t < 16: entries of bucket t so far
+                for (int e0 = 0; e0 < nsv; e0 += 32) {
+                    const int ee = e0 + lane;
+                    const bool valid = ee < nsv;
+                    const float4 q = sx[valid ? hj[warp][ee] : s];
+                    const double d = sqdist4(p, q);
+                    const bool hit = valid && d < r2;
+                    const unsigned long long db = (unsigned long long)__double_as_longlong(d);
+                    const unsigned long long* ls = lvsort[warp];
+                    int bk = (ls[7] <= db) ? 8 : 0;
+                    bk += (ls[bk + 3] <= db) ? 4 : 0;
+                    bk += (ls[bk + 1] <= db) ? 2 : 0;
+                    bk += (ls[bk] <= db) ? 1 : 0;
+                    const unsigned hm = __ballot_sync(kFull, hit);
+                    unsigned peers = hm, mine = hm;
+#pragma unroll
+                    for (int bt = 0; bt < 4; ++bt) {
+                        const unsigned mb = __ballot_sync(kFull, hit && ((bk >> bt) & 1));
+                        peers &= ((bk >> bt) & 1) ? mb : ~mb;
+                        mine &= ((lane >> bt) & 1) ? mb : ~mb;
+                    }
+                    const int rank = __shfl_sync(kFull, runs, bk & 15) + __popc(peers & lt);
+                    runs += __popc(mine);
+                    if (valid) {
+                        hk[warp][ee] = hit ? (uint8_t)bk : (uint8_t)0xff;
+                        hb[warp][ee] = (uint16_t)rank;
+                        hd[warp][ee] = d;
+                        hj[warp][ee] = __float_as_int(q.w);  // now the original index
+                    }
+                }
+                const int v = (lane < 16 && lane <= L) ? runs : 0;
+                int hincl = v;
+#pragma unroll
+                for (int o = 1; o < 16; o <<= 1) {
+                    const int y = __shfl_up_sync(kFull, hincl, o);
+                    if (lane >= o) hincl += y;
+                }
+                const int cntd = __shfl_sync(kFull, hincl, 15);
+                const int hbase = hincl - v;
+                int64_t row_off = (int64_t)i * stride;
+                if (cntd > stride) {  // spill arena (see below)
+                    unsigned long long o = 0;
+                    if (lane == 0) o = atomicAdd(&w.spill[b], (unsigned long long)((cntd + 3) & ~3));
+                    o = __shfl_sync(kFull, o, 0);
+                    const int64_t off = N * stride + csr.spill_lo + (int64_t)o;
+                    if (off + cntd > N * stride + csr.spill_hi) {
+                        if (lane == 0) atomicOr(&w.status[b], 2);
+                        if (lane < L) csr.counts[(b * csr.L + lane) * N + i] = 0;
+                        __syncwarp();
+                        continue;
+                    }
+                    row_off = off;
+                    if (lane == 0) csr.indptr[b * (N + 1) + i] = off;
+                }
+                __syncwarp();
+                int32_t* rn = csr.nbr + b * csr.cap_entries + row_off;
+                double* rd = csr.d2 + b * csr.cap_entries + row_off;
+                for (int e0 = 0; e0 < nsv; e0 += 32) {
+                    const int ee = e0 + lane;
+                    const int bk = ee < nsv ? hk[warp][ee] : 0xff;
+                    const int pos = __shfl_sync(kFull, hbase, bk & 15) + (bk != 0xff ? hb[warp][ee] : 0);
+                    if (bk != 0xff) {
+                        __stcs(rd + pos, hd[warp][ee]);  // d2 streams to HBM: keep L2 for the nbr rows
+                        rn[pos] = hj[warp][ee];
+                    }
+                }
+                const int hist_mine = __shfl_sync(kFull, hincl, rank_lt < 15 ? rank_lt : 15);
+                if (lane < L) csr.counts[(b * csr.L + lane) * N + i] = hist_mine;
+                {
+                    const int64_t row_cap = row_off == (int64_t)i * stride ? stride : ((cntd + 3) & ~3);
+                    if (lane < min((int64_t)((cntd + 3) & ~3), row_cap) - cntd) rn[cntd + lane] = -1;
+                }
+                __syncwarp();
+                continue;
+            }
+            // more survivors than the staging holds: the general path below
+            // (its exact count, spill and per-bucket rescan); evals counted once
+            evals -= (unsigned long long)total;
+        }
         int cnt = 0;
 #pragma unroll 4
         for (int tb = 0; tb < total; tb += 32) {
@@ -1560,7 +1664,10 @@ cudaError_t launch_excl_build(const float4* xyz, int64_t B, int64_t N, const dou
             } else {
                 constexpr int kW = 4;
                 const int64_t gx = std::max<int64_t>(1, std::min<int64_t>((148 * 32 + B - 1) / B, (N + kW - 1) / kW));
-                if (reach == 2)
+                if (reach == 2 && L <= 15 && !getenv("PS_ELL_LONG_OLD"))
+                    grid_ell_kernel<kW, 512, true, true><<<dim3((unsigned)gx, (unsigned)B), kW * 32, 0, s>>>(
+                        B, N, r2_levels, L, levels_ld, stride, g, w, csr);
+                else if (reach == 2)
                     grid_ell_kernel<kW, 512, true><<<dim3((unsigned)gx, (unsigned)B), kW * 32, 0, s>>>(
                         B, N, r2_levels, L, levels_ld, stride, g, w, csr);
                 else
