@@ -236,10 +236,20 @@ __global__ void et_push_kernel(EtArgs a) {
         const int32_t* nbr = a.nbr + b * a.cap_entries + base;
         const double* d2 = a.d2 + b * a.cap_entries + base;
         unsigned long long* md = reinterpret_cast<unsigned long long*>(a.md + b * a.N);
-        for (int32_t u = gl; u < c; u += 8) {
-            const int32_t j = __ldg(nbr + u);
-            const double d = __ldg(d2 + u);
-            atomicMin(md + j, (unsigned long long)__double_as_longlong(d));
+        // four entries per lane in flight: the loads of a batch are issued
+        // before its reductions (the row reads are the latency)
+        for (int32_t u0 = gl; u0 < c; u0 += 32) {
+            int32_t j[4];
+            double d[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int32_t u = u0 + 8 * k;
+                j[k] = u < c ? __ldg(nbr + u) : -1;
+                d[k] = u < c ? __ldg(d2 + u) : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (j[k] >= 0) atomicMin(md + j[k], (unsigned long long)__double_as_longlong(d[k]));
         }
     }
 }
