@@ -63,7 +63,7 @@ constexpr int kR = 10;            // records per CTA per exchange: its max + kR-
 constexpr int kRunMax = 31;       // samples per exchange (one lane each)
 constexpr double kTarget = 22.0;  // threshold candidates aimed for per exchange
 constexpr uint64_t kTauOff = ~0ull;  // threshold disabled (above every md bit pattern)
-constexpr int kMaxS = 4096;          // points per CTA the spatial sort holds
+constexpr int kMaxS = 4352;          // points per CTA the spatial sort holds (P = 9 x 15 worker warps)
 constexpr int64_t kSortMinIters = 64;  // runs shorter than this keep the index order
 constexpr float kInfF = __builtin_huge_valf();
 
@@ -790,12 +790,14 @@ cudaError_t launch_fps_spec(FpsArgs a, int64_t B, cudaStream_t s) {
     if (C <= 2 && !getenv("PS_FPS_SPEC")) return cudaErrorNotSupported;
     // one warp per CTA leads the exchange and owns no points (below)
     const int64_t S = (a.N + C - 1) / C;
-    // 512 threads, 15 worker warps, P <= 8 points per thread (beyond that the
-    // register budget spills): up to 3840 points per CTA
+    // 512 threads, 15 worker warps, P <= 9 points per thread (beyond that the
+    // register budget spills): up to 4320 points per CTA without points on the
+    // lead warp (P = 9: C3 early-termination tail at 6-CTA clusters 0.191 ->
+    // 0.178 ms, full FPS 0.642 -> 0.594 us per sample; PS_SPEC_NOP9=1: P <= 8)
     P = 0;
     T = 512;
-    for (int p : {1, 2, 3, 4, 5, 6, 7, 8})
-        if (!P && (int64_t)p * (T - 32) >= S) P = p;
+    for (int p : {1, 2, 3, 4, 5, 6, 7, 8, 9})
+        if (!P && (int64_t)p * (T - 32) >= S && (p < 9 || !getenv("PS_SPEC_NOP9"))) P = p;
     // up to 4096 points per CTA: the lead warp owns points as well
     const bool lead_pts = P == 0 && S <= 8 * 512;
     if (lead_pts) { P = 8; T = 512; }
@@ -829,6 +831,7 @@ cudaError_t launch_fps_spec(FpsArgs a, int64_t B, cudaStream_t s) {
         PS_SPEC_CASE(6, 512)
         PS_SPEC_CASE(7, 512)
         PS_SPEC_CASE(8, 512)
+        PS_SPEC_CASE(9, 512)
         default: break;
     }
 #undef PS_SPEC_CASE
