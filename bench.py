@@ -606,6 +606,19 @@ def main_ours(args):
                          "DRAM traffic ~1000x lower) and certifies several samples per exchange, so frac compares "
                          "it with such a streaming kernel at HBM speed -- it is bound by its exchange/pick "
                          "latency chain, not by DRAM")}
+    if dom == "fps_prefix":
+        # the bound that actually applies: one cluster exchange (DSMEM send + wait, 400-600 SM cycles measured,
+        # profiles/r01 micro_sync.log) per group of certified picks; picks per exchange from the instrumented
+        # build (profiles/r02/fps_spec_phase_cycles.log)
+        picks_per_ex = 4.87
+        us_per_sample = per_stage[dom] * 1e3 / max(k0 - 1, 1)
+        cyc_ex = us_per_sample * picks_per_ex * pk.get("sm_max_mhz", 1965.0)
+        roofline["latency_model"] = {
+            "us_per_sample": us_per_sample, "picks_per_exchange": picks_per_ex,
+            "sm_cycles_per_exchange": cyc_ex, "exchange_floor_cycles": 500.0,
+            "frac": 500.0 / cyc_ex,
+            "note": "fraction of each exchange spent in the unavoidable cluster round trip; the rest is the lead "
+                    "warp's serial pick chain (~550-700 cycles per certified pick)"}
 
     # ---- other configs ------------------------------------------------------------------
     c5 = c5f = c2 = c4 = None
