@@ -50,6 +50,7 @@ struct SampArgs {
     int tiny;                    // v4, one CTA per cloud: the per-cloud arrays live in shared memory
     int rounds;                  // v4: 1 = MIS in barrier-separated rounds, 0 = dataflow (default)
     int poll_ns;                 // v4 dataflow: poll back-off after the first polls (0: spin)
+    int push_grouped;            // v4 P1 push: lane groups per row instead of flattened rows (A/B knob)
     const int32_t* excl_status;  // [B] nullable: nonzero -> the cloud's rows are incomplete (error outputs)
     int grid_c;                  // v4 grid mode: CTAs per cloud (0: cluster mode)
 };

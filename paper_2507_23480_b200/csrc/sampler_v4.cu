@@ -27,6 +27,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "ps_internal.h"
@@ -250,6 +251,11 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
     static_assert(!(kSm && kGrid), "grid mode keeps the per-cloud arrays in global memory");
     using SL = Scr<kGrid>;
     __shared__ int wt[32];
+    // P1 push, flattened rows (kSm, nseg <= 8): per warp, its 8 rows' entry
+    // offsets, nbr index deltas and coverage bounds
+    __shared__ int pr_off[kSm ? kW4 : 1][8];
+    __shared__ int64_t pr_delta[kSm ? kW4 : 1][8];
+    __shared__ __align__(16) int32_t pr_csm[kSm ? kW4 : 1][8][8];
     __shared__ int s_dec[2][kMaxC4];
     __shared__ int s_tmp;
     extern __shared__ __align__(16) uint8_t dsm4[];
@@ -403,51 +409,134 @@ __global__ void __launch_bounds__(kT4, 1) samp4_kernel(SampArgs a, V4Work w) {
                 return ow;
             };
             const int64_t nnew = i - i_tk;
-            for (int64_t kb = (int64_t)r * (kT4 / kG) + warp * (32 / kG); kb < nnew;
-                 kb += (int64_t)C * (kT4 / kG)) {
-                const int64_t k = kb + grp;
-                const bool valid = k < nnew;
-                int32_t q = 0, c = 0;
-                int32_t cs[kMaxSeg];
+            // kS >= nseg segment slots: csm[s2] = INT_MAX before s_from (past
+            // segments always count), the level count for s_from <= s2 < nseg,
+            // 0 beyond -- cov = #(s2 : u < csm[s2]) with no per-entry range tests
+            // (the slowest group's long rows bound this phase)
+            auto push = [&](auto kS_tag) {
+                constexpr int kS = decltype(kS_tag)::value;
+                for (int64_t kb = (int64_t)r * (kT4 / kG) + warp * (32 / kG); kb < nnew;
+                     kb += (int64_t)C * (kT4 / kG)) {
+                    const int64_t k = kb + grp;
+                    const bool valid = k < nnew;
+                    int32_t q = 0, c = 0;
+                    int32_t csm[kS];
 #pragma unroll
-                for (int s2 = 0; s2 < kMaxSeg; ++s2) cs[s2] = 0;
-                const int32_t* row = nbr;
-                if (valid) {
-                    q = (int32_t)out[i_tk + k];
-                    for (int s2 = s_from; s2 < nseg; ++s2)
-                        cs[s2] = a.counts[(b * a.L + a.seg_level_rows[s2]) * N + q];
-                    c = cs[s_from];
-                    row = nbr + indptr[q];
-                    if (gl == 0) {
+                    for (int s2 = 0; s2 < kS; ++s2) csm[s2] = s2 < s_from ? 0x7fffffff : 0;
+                    const int32_t* row = nbr;
+                    if (valid) {
+                        q = (int32_t)out[i_tk + k];
+#pragma unroll
+                        for (int s2 = 0; s2 < kS; ++s2)
+                            if (s2 >= s_from && s2 < nseg)
+                                csm[s2] = a.counts[(b * a.L + a.seg_level_rows[s2]) * N + q];
+                        c = a.counts[(b * a.L + a.seg_level_rows[s_from]) * N + q];
+                        row = nbr + indptr[q];
+                        if (gl == 0) {
+                            const uint32_t ow = owner_of((uint32_t)q);
+                            red_cluster_max(mapa(blv_base + 4u * ((uint32_t)q - ow * span32), ow), (uint32_t)nseg);
+                        }
+                    }
+                    const bool al = (reinterpret_cast<uintptr_t>(row) & 15u) == 0;
+                    constexpr int kPush = 4 * kGStep;
+                    for (int32_t u0 = 0;; u0 += kPush) {
+                        const bool act = valid && u0 < c;
+                        if (!__any_sync(kFull, act)) break;
+                        if (!act) continue;
+#pragma unroll
+                        for (int q4 = 0; q4 < 4; ++q4) {
+                            const int32_t u = u0 + q4 * kGStep + 4 * gl;
+                            const int4 v = grp_load4(row, u, c, al);
+                            const int32_t jv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const int32_t j = jv[e];
+                                if (j < 0) continue;
+                                uint32_t cov = 0;
+#pragma unroll
+                                for (int s2 = 0; s2 < kS; ++s2) cov += (u + e < csm[s2]) ? 1u : 0u;
+                                const uint32_t ow = owner_of((uint32_t)j);
+                                red_cluster_max(mapa(blv_base + 4u * ((uint32_t)j - ow * span32), ow), cov);
+                            }
+                        }
+                    }
+                }
+            };
+            // nseg <= 8: the warp's 8 rows are flattened -- entry f of their
+            // concatenation goes to lane f % 32 -- so a warp costs sum(c) / 32
+            // entries per lane instead of max(c) / 4 (the grouped walk above
+            // issues every slot while any row of the warp is still running)
+            auto push_flat = [&]() {
+                const int64_t step = (int64_t)C * (kT4 / kG);
+                for (int64_t kb = (int64_t)r * (kT4 / kG) + warp * 8; kb < nnew; kb += step) {
+                    const int64_t k = kb + lane;
+                    const bool valid = lane < 8 && k < nnew;
+                    int32_t c = 0;
+                    int64_t rowp = 0;
+                    if (valid) {
+                        const int32_t q = (int32_t)out[i_tk + k];
+                        int32_t cm[8];
+#pragma unroll
+                        for (int s2 = 0; s2 < 8; ++s2)
+                            cm[s2] = s2 < s_from ? 0x7fffffff
+                                                 : (s2 < nseg ? a.counts[(b * a.L + a.seg_level_rows[s2]) * N + q] : 0);
+#pragma unroll
+                        for (int s2 = 0; s2 < 8; ++s2)
+                            if (s2 == s_from) c = cm[s2];
+                        rowp = indptr[q];
+                        *reinterpret_cast<int4*>(&pr_csm[warp][lane][0]) = make_int4(cm[0], cm[1], cm[2], cm[3]);
+                        *reinterpret_cast<int4*>(&pr_csm[warp][lane][4]) = make_int4(cm[4], cm[5], cm[6], cm[7]);
                         const uint32_t ow = owner_of((uint32_t)q);
                         red_cluster_max(mapa(blv_base + 4u * ((uint32_t)q - ow * span32), ow), (uint32_t)nseg);
                     }
-                }
-                const bool al = (reinterpret_cast<uintptr_t>(row) & 15u) == 0;
-                constexpr int kPush = 4 * kGStep;
-                for (int32_t u0 = 0;; u0 += kPush) {
-                    const bool act = valid && u0 < c;
-                    if (!__any_sync(kFull, act)) break;
-                    if (!act) continue;
+                    int incl = c;
 #pragma unroll
-                    for (int q4 = 0; q4 < 4; ++q4) {
-                        const int32_t u = u0 + q4 * kGStep + 4 * gl;
-                        const int4 v = grp_load4(row, u, c, al);
-                        const int32_t jv[4] = {v.x, v.y, v.z, v.w};
+                    for (int o = 1; o < 8; o <<= 1) {
+                        const int y = __shfl_up_sync(kFull, incl, o);
+                        if (lane >= o) incl += y;
+                    }
+                    const int total = __shfl_sync(kFull, incl, 7);
+                    const int excl = incl - c;
+                    if (lane < 8) {
+                        pr_off[warp][lane] = excl;
+                        pr_delta[warp][lane] = rowp - excl;  // entry f of row kr: nbr[f + delta]
+                    }
+                    // row starts 1..7 in every lane: kr = #(starts <= f)
+                    int o7[7];
+#pragma unroll
+                    for (int x = 0; x < 7; ++x) o7[x] = __shfl_sync(kFull, excl, x + 1);
+                    __syncwarp();
+                    for (int f0 = 0; f0 < total; f0 += 128) {
+                        int32_t jv[4], uv[4], kv[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int f = f0 + 32 * e + lane;
+                            int kr = 0;
+#pragma unroll
+                            for (int x = 0; x < 7; ++x) kr += f >= o7[x] ? 1 : 0;
+                            kv[e] = kr;
+                            uv[e] = f - pr_off[warp][kr];
+                            jv[e] = f < total ? __ldg(nbr + (f + pr_delta[warp][kr])) : -1;
+                        }
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
                             const int32_t j = jv[e];
                             if (j < 0) continue;
-                            uint32_t cov = 0;
-#pragma unroll
-                            for (int s2 = 0; s2 < kMaxSeg; ++s2) cov += (s2 >= s_from && s2 < nseg && u + e < cs[s2]) ? 1u : 0u;
-                            cov += (uint32_t)s_from;  // segments before s_from are past
+                            const int4 m0 = *reinterpret_cast<const int4*>(&pr_csm[warp][kv[e]][0]);
+                            const int4 m1 = *reinterpret_cast<const int4*>(&pr_csm[warp][kv[e]][4]);
+                            const int32_t u = uv[e];
+                            const uint32_t cov = (u < m0.x) + (u < m0.y) + (u < m0.z) + (u < m0.w) + (u < m1.x) +
+                                                 (u < m1.y) + (u < m1.z) + (u < m1.w);
                             const uint32_t ow = owner_of((uint32_t)j);
                             red_cluster_max(mapa(blv_base + 4u * ((uint32_t)j - ow * span32), ow), cov);
                         }
                     }
+                    __syncwarp();
                 }
-            }
+            };
+            if (nseg <= 8 && !a.push_grouped) push_flat();
+            else if (nseg <= 8) push(std::integral_constant<int, 8>{});
+            else push(std::integral_constant<int, kMaxSeg>{});
             i_tk = i;
         }
         sync_grp();
@@ -1027,6 +1116,7 @@ cudaError_t launch_sampler_v4(SampArgs a, int64_t B, cudaStream_t s) {
     a.tiny = (sm && C == 1 && dsm_tiny <= 220 * 1024 && !getenv("PS_SAMPLER_NOTINY")) ? 1 : 0;
     a.rounds = getenv("PS_SAMPLER_ROUNDS") ? 1 : 0;
     a.poll_ns = getenv("PS_SAMPLER_POLL") ? atoi(getenv("PS_SAMPLER_POLL")) : 128;
+    a.push_grouped = getenv("PS_SAMPLER_PUSH_GROUPED") ? 1 : 0;  // A/B knob (flattened rows by default)
     const size_t dsm_used = a.tiny ? dsm_tiny : dsm;
     if (!sm && !getenv("PS_SAMPLER_NOGRID")) {
         // grid mode: few clouds too large for shared memory -- spread each over
