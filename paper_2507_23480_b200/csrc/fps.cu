@@ -514,15 +514,24 @@ int fps_choose_cluster(int64_t N, int64_t B, int* C_out, int* P_out, int* T_out)
         const int tenv0 = fps_threads_env();
         const int64_t c0 = (N + 1023) / 1024;
         const int want = (int)(c0 < 1 ? 1 : (c0 > kMaxCluster ? kMaxCluster : c0));
+        // deep concurrency (>= 2 batches in flight): the other stages share the
+        // SMs, so SM-time per cloud, C x latency(C), decides -- lowest at the
+        // narrowest width the speculative kernel holds without spills (<= 10
+        // points on each of its 480 point-owning threads; C3: 5-CTA clusters,
+        // 85.5 -> 89.4 M samples/s, profiles/r02/fps_pmax.log)
+        const bool deep = g_inflight >= 2 * B;
         int bestC = 0;
         int64_t bestCov = -1;
         for (int cc = want; cc >= 3; --cc) {
             const int p = choose_P(N, cc, 512);
             if (tenv0 && tenv0 != 512) break;
-            if (p < 1 || p > 8) continue;
+            const int64_t S = (N + cc - 1) / cc;
+            const int ps = (int)((S + 479) / 480);  // speculative kernel's points per thread
+            if (p < 1 || (p > 8 && ps > 10)) continue;
             const int64_t act = max_active_clusters(N, cc, 512);
             if (act < B) continue;  // the batch itself must still fit one wave
-            const int64_t score = (act < g_inflight ? act : g_inflight) * cc * 1024 / (cc + 9);
+            const int64_t score = deep ? (int64_t)(kMaxCluster + 1 - cc)
+                                       : (act < g_inflight ? act : g_inflight) * cc * 1024 / (cc + 9);
             if (score >= bestCov) { bestCov = score; bestC = cc; }
         }
         if (bestC) {

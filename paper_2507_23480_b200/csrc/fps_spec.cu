@@ -63,7 +63,8 @@ constexpr int kR = 10;            // records per CTA per exchange: its max + kR-
 constexpr int kRunMax = 31;       // samples per exchange (one lane each)
 constexpr double kTarget = 22.0;  // threshold candidates aimed for per exchange
 constexpr uint64_t kTauOff = ~0ull;  // threshold disabled (above every md bit pattern)
-constexpr int kMaxS = 4352;          // points per CTA the spatial sort holds (P = 9 x 15 worker warps)
+// point slots of a CTA (sort arrays): P per worker thread, rounded to 8
+constexpr int spec_slots(int P, int T, bool lead_pts) { return ((P * (lead_pts ? T : T - 32)) + 7) / 8 * 8; }
 constexpr int64_t kSortMinIters = 64;  // runs shorter than this keep the index order
 constexpr float kInfF = __builtin_huge_valf();
 
@@ -92,8 +93,12 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
     __shared__ int cnt_s;
     __shared__ uint32_t pub_s;
     __shared__ uint32_t bin_s[4096];    // spatial sort: cell counts / offsets
-    __shared__ uint16_t ord_s[kMaxS];   // sorted position -> local index
-    __shared__ uint16_t pos_s[kMaxS];   // local index -> sorted position
+    // sorted position -> local index / local index -> sorted position
+    // (dynamic shared memory: 4 bytes per point slot of the CTA)
+    extern __shared__ __align__(16) uint16_t dyn_s[];
+    constexpr int kS = spec_slots(P, T, kLeadPts);
+    uint16_t* const ord_s = dyn_s;
+    uint16_t* const pos_s = dyn_s + kS;
     __shared__ float red_s[kW][6], bb_s[6];
     __shared__ uint32_t wsum_s[kW];
     __shared__ __align__(8) uint64_t bars[2];
@@ -126,7 +131,7 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
     // (fold_one).  The order inside a cell follows shared-memory atomics and may
     // differ between runs; no result depends on it (every choice is by
     // (md, original index)).
-    static_assert(kMaxS >= P * TW, "sort capacity");
+    static_assert(kS >= P * TW, "sort capacity");
     const int ncta = hi > lo ? (int)(hi - lo) : 0;
     if (k_stop - k_start < kSortMinIters) {
         // short runs (early-termination tails) do not repay the sort
@@ -219,27 +224,41 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
 
     // ---- state into registers ---------------------------------------------
     float fx[P], fy[P], fz[P], thr[P];
-    double m[P];
+    // md: registers, or (P >= 10) shared memory after the sort arrays -- the
+    // float32 screen needs only thr, so md is touched on the exact path,
+    // once per exchange for the thread maximum / candidates, and at the ends
+    constexpr bool kMs = P >= 10;
+    double m_reg[kMs ? 1 : P] = {};
+    double* const m_sm = reinterpret_cast<double*>(dyn_s + 2 * kS) + (kMs ? tid : 0);
+    auto mget = [&](int q) -> double {
+        if constexpr (kMs) return m_sm[q * TW];
+        else return m_reg[q];
+    };
+    auto mset = [&](int q, double v) {
+        if constexpr (kMs) m_sm[q * TW] = v;
+        else m_reg[q] = v;
+    };
     uint32_t tk = 0, valid = 0;
 #pragma unroll
     for (int q = 0; q < P; ++q) {
         const int sp = warp * 32 * P + q * 32 + lane;
         fx[q] = fy[q] = fz[q] = 0.f;
-        m[q] = 0.0;
+        double mq = 0.0;
         if (worker && sp < ncta) {
             const int64_t j = lo + ord_s[sp];
             valid |= 1u << q;
             const float4 v = xyz[j];
             fx[q] = v.x; fy[q] = v.y; fz[q] = v.z;
             if (a.fresh) {
-                m[q] = kInf;
+                mq = kInf;
                 tk |= (j == seed ? 1u : 0u) << q;
             } else {
-                m[q] = md[j];
+                mq = md[j];
                 tk |= (taken[j] ? 1u : 0u) << q;
             }
         }
-        thr[q] = ((valid >> q) & 1u) ? skip_threshold(m[q]) : -1.0f;
+        if (!kMs || worker) mset(q, mq);  // (kMs: the lead owns no md slot)
+        thr[q] = ((valid >> q) & 1u) ? skip_threshold(mq) : -1.0f;
     }
     // the warp's bounding box and the largest skip threshold of its points
     float wb[6] = {kInfF, kInfF, kInfF, -kInfF, -kInfF, -kInfF};
@@ -323,12 +342,13 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
             if (dbox > wthr) return;
         }
         uint32_t need = 0;
-        float d32s[P];
+        constexpr int kD = P >= 10 ? 1 : P;  // P >= 10: recompute instead of keeping P distances live
+        float d32s[kD];
 #pragma unroll
         for (int q = 0; q < P; ++q) {
             const float dx = fx[q] - sx32, dy = fy[q] - sy32, dz = fz[q] - sz32;
             const float d32 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
-            d32s[q] = d32;
+            if constexpr (P < 10) d32s[q] = d32;
             need |= (!(d32 > thr[q]) ? 1u : 0u) << q;
         }
         if (__any_sync(kFull, need != 0)) {
@@ -337,9 +357,16 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
             for (int q = 0; q < P; ++q) {
                 if (__any_sync(kFull, (need >> q) & 1u)) {
                     const double d = sqdist(sx, sy, sz, (double)fx[q], (double)fy[q], (double)fz[q]);
-                    if (((need >> q) & 1u) && dbits(d) < dbits(m[q])) {
-                        m[q] = d;
-                        thr[q] = skip_threshold_d32(d, d32s[q]);
+                    if (((need >> q) & 1u) && dbits(d) < dbits(mget(q))) {
+                        float d32;
+                        if constexpr (P < 10) {
+                            d32 = d32s[q];
+                        } else {  // the screen's float32 distance, same operations
+                            const float dx = fx[q] - sx32, dy = fy[q] - sy32, dz = fz[q] - sz32;
+                            d32 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+                        }
+                        mset(q, d);
+                        thr[q] = skip_threshold_d32(d, d32);
                         dirty = dirty || (q == bq);
                     }
                 }
@@ -358,79 +385,12 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
     const bool tdbg = kTiming && a.dbg && b == 0 && r == 0 && warp == kLead && lane == 0;
     long long tacc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     long long tsp = 0;
-    while (it < k_stop) {
-        const uint32_t par = ex & 1u, phase = (ex >> 1) & 1u;
-        ++ex;
-        long long t0 = 0, t1 = 0;
-        if (tdbg) t0 = clock64();
-
-        // B. thread max (cached), threshold candidates, warp argmax; the
-        // warp's skip bound for the next exchange's folds (thr only falls)
-        wthr = warp_thr_max();
-        if (__any_sync(kFull, dirty)) {
-            double tv[P];
-            int ti[P];
-#pragma unroll
-            for (int q = 0; q < P; ++q) {
-                tv[q] = ((valid >> q) & 1u) ? m[q] : -1.0;
-                ti[q] = q;
-            }
-#pragma unroll
-            for (int st = 1; st < P; st <<= 1) {
-#pragma unroll
-                for (int q = 0; q + st < P; q += 2 * st) {
-                    bool take = tv[q + st] > tv[q];
-                    if (tv[q + st] == tv[q] && tv[q] >= 0.0) take = oid(ti[q + st]) < oid(ti[q]);  // lowest index
-                    if (take) { tv[q] = tv[q + st]; ti[q] = ti[q + st]; }
-                }
-            }
-            if (dirty) {
-                bv = tv[0];
-                bq = ti[0];
-#pragma unroll
-                for (int q = 0; q < P; ++q)
-                    if (q == bq) { bx = fx[q]; by = fy[q]; bz = fz[q]; }
-            }
-            dirty = false;
-        }
-        {
-            uint32_t cm = 0;
-#pragma unroll
-            for (int q = 0; q < P; ++q) cm |= ((((valid >> q) & 1u) && dbits(m[q]) >= tau) ? 1u : 0u) << q;
-            if (__any_sync(kFull, cm != 0)) {
-#pragma unroll
-                for (int q = 0; q < P; ++q) {
-                    if ((cm >> q) & 1u) {
-                        const int slot = atomicAdd(&cnt_s, 1);
-                        if (slot < kR - 1) {
-                            const uint64_t kq = dbits(m[q]);
-                            const uint32_t ca = a_cand + 32u * (uint32_t)slot;
-                            sts_v4(ca, make_uint4((uint32_t)kq, (uint32_t)(kq >> 32), oid(q), (tk >> q) & 1u));
-                            sts_v4(ca + 16u, make_uint4(__float_as_uint(fx[q]), __float_as_uint(fy[q]),
-                                                         __float_as_uint(fz[q]), 0u));
-                        }
-                    }
-                }
-            }
-            const uint64_t bkey = bv >= 0.0 ? dbits(bv) : 0ull;
-            const uint32_t bidx = bv >= 0.0 ? oid(bq) : kNone;
-            const int wl = warp_argmax_lane(bkey, bidx);
-            if (wl < 0) {
-                if (lane == 0) sts_v4(a_wrec + 32u * warp, make_uint4(0u, 0u, kNone, 0u));
-            } else if (lane == wl) {
-                sts_v4(a_wrec + 32u * warp, make_uint4((uint32_t)bkey, (uint32_t)(bkey >> 32), bidx, (tk >> bq) & 1u));
-                sts_v4(a_wrec + 32u * warp + 16u,
-                       make_uint4(__float_as_uint(bx), __float_as_uint(by), __float_as_uint(bz), 0u));
-            }
-        }
-        if (tdbg) { t1 = clock64(); tacc[1] += t1 - t0; t0 = t1; }
-        __syncthreads();
-        if (tdbg) { t1 = clock64(); tacc[2] += t1 - t0; t0 = t1; }
-
-        // published word: exchange tag << 16 | fallback << 9 | done << 8 | picks
-        const uint32_t tag = (ex & 0xffffu) << 16;
-        uint32_t pw;
-        if (warp == kLead) {
+    // The lead-only warp (!kLeadPts) runs its own copy of the loop: the
+    // workers' register-resident points are dead there, so the two roles
+    // share the register budget instead of adding up (room for more
+    // points per thread).  Both loops meet the same CTA barriers.
+    auto lead_step = [&](uint32_t tag, uint32_t par, uint32_t phase, long long& t0, long long& t1) -> uint32_t {
+        uint32_t pw = 0;
             // C. CTA record set: header (the CTA max, candidate count) and
             // up to kR-1 threshold candidates, pushed to every CTA; each
             // sender announces its byte count on the peer's mbarrier.
@@ -659,7 +619,10 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
                              it + k < k_stop - 1);
                 }
             }
-        } else {
+        return pw;
+    };
+    auto worker_step = [&](uint32_t tag) -> uint32_t {
+        uint32_t pw = 0;
             // fold each pick as soon as the lead warp publishes it
             int k = 0;
             while (true) {
@@ -678,56 +641,193 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
                 }
                 if ((pw & 0xffff0000u) == tag && (pw & 0x100u)) break;
             }
-        }
-        pw = __shfl_sync(kFull, pw, 0);
-        const int rn = (int)(pw & 0xffu);
-        it += rn;
-        tau = tau_s;
-
-        if (pw & 0x200u) {
-            // duplicate fallback (_kernels.py:65-70): lowest untaken index
-            uint32_t fidx = kNone;
-            Rec fr{};
-#pragma unroll
-            for (int q = 0; q < P; ++q) {
-                if (((valid >> q) & 1u) && !((tk >> q) & 1u) && oid(q) < fidx) {
-                    fidx = oid(q);
-                    const uint64_t kk = dbits(m[q]);
-                    fr.klo = (uint32_t)kk; fr.khi = (uint32_t)(kk >> 32);
-                    fr.x = fx[q]; fr.y = fy[q]; fr.z = fz[q];
-                }
-            }
-            fr.idx = fidx;
-            const uint32_t wmin = __reduce_min_sync(kFull, fidx);
-            __syncthreads();  // wrec reuse
-            if (fidx == wmin && fidx != kNone) wrec[warp] = fr;
-            else if (lane == 0 && wmin == kNone) { Rec z{}; z.idx = kNone; wrec[warp] = z; }
+        return pw;
+    };
+    if (!kLeadPts && warp == kLead) {
+        while (it < k_stop) {
+            const uint32_t par = ex & 1u, phase = (ex >> 1) & 1u;
+            ++ex;
+            long long t0 = 0, t1 = 0;
+            if (tdbg) t0 = clock64();
+            // B: no points -- an empty warp record
+            if (lane == 0) sts_v4(a_wrec + 32u * warp, make_uint4(0u, 0u, kNone, 0u));
+            if (tdbg) { t1 = clock64(); tacc[1] += t1 - t0; t0 = t1; }
             __syncthreads();
-            if (warp == 0) {
-                const Rec cr = warp_min_idx_recs(wrec, kW, lane);
-                if (lane < (int)C) {
-                    const uint32_t dst = mapa(smem_u32(&fb_slots[r]), lane);
-                    st_cluster_u64(dst, ((uint64_t)cr.khi << 32) | cr.klo);
-                    st_cluster_u64(dst + 8, ((uint64_t)cr.taken << 32) | cr.idx);
-                    st_cluster_u64(dst + 16, ((uint64_t)__float_as_uint(cr.y) << 32) | __float_as_uint(cr.x));
-                    st_cluster_u64(dst + 24, (uint64_t)__float_as_uint(cr.z));
+            if (tdbg) { t1 = clock64(); tacc[2] += t1 - t0; t0 = t1; }
+            const uint32_t tag = (ex & 0xffffu) << 16;
+            uint32_t pw = lead_step(tag, par, phase, t0, t1);
+            pw = __shfl_sync(kFull, pw, 0);
+            const int rn = (int)(pw & 0xffu);
+            it += rn;
+            tau = tau_s;
+
+            if (pw & 0x200u) {
+                // duplicate fallback, lead side (see the workers' loop)
+                __syncthreads();  // wrec reuse
+                if (lane == 0) { Rec z{}; z.idx = kNone; wrec[warp] = z; }
+                __syncthreads();
+                cluster_sync_all();
+                const Rec fw = warp_min_idx_recs(fb_slots, (int)C, lane);
+                Rec w = fbw_s;  // no untaken point left: the argmax stands
+                if (fw.idx != kNone) w = fw;
+                cluster_sync_all();  // fb_slots / wrec free again
+                if (writer) {
+                    out[it] = (int64_t)w.idx;
+                    curve[it] = bitsd(rec_key(w));
                 }
-            }
-            cluster_sync_all();
-            const Rec fw = warp_min_idx_recs(fb_slots, (int)C, lane);
-            Rec w = fbw_s;  // no untaken point left: the argmax stands
-            if (fw.idx != kNone) w = fw;
-            cluster_sync_all();  // fb_slots / wrec free again
-            if (writer) {
-                out[it] = (int64_t)w.idx;
-                curve[it] = bitsd(rec_key(w));
-            }
-            if (warp == kLead) {
                 if (lane == 0) hist_s[hc & 31] = bitsd(rec_key(w));
                 ++hc;
+                ++it;
             }
-            fold_one(w.x, w.y, w.z, w.idx, it < k_stop - 1);
-            ++it;
+        }
+    } else {
+        while (it < k_stop) {
+            const uint32_t par = ex & 1u, phase = (ex >> 1) & 1u;
+            ++ex;
+            long long t0 = 0, t1 = 0;
+            if (tdbg) t0 = clock64();
+
+            // B. thread max (cached), threshold candidates, warp argmax; the
+            // warp's skip bound for the next exchange's folds (thr only falls)
+            wthr = warp_thr_max();
+            if (__any_sync(kFull, dirty)) {
+                double tv0;
+                int ti0;
+                if constexpr (P >= 10) {
+                    // many points per thread: a running maximum (three live
+                    // registers instead of the tree's 3P)
+                    tv0 = -1.0;
+                    ti0 = 0;
+    #pragma unroll
+                    for (int q = 0; q < P; ++q) {
+                        const double v = ((valid >> q) & 1u) ? mget(q) : -1.0;
+                        bool take = v > tv0;
+                        if (v == tv0 && v >= 0.0) take = oid(q) < oid(ti0);  // lowest index
+                        if (take) { tv0 = v; ti0 = q; }
+                    }
+                } else {
+                    double tv[P];
+                    int ti[P];
+    #pragma unroll
+                    for (int q = 0; q < P; ++q) {
+                        tv[q] = ((valid >> q) & 1u) ? mget(q) : -1.0;
+                        ti[q] = q;
+                    }
+    #pragma unroll
+                    for (int st = 1; st < P; st <<= 1) {
+    #pragma unroll
+                        for (int q = 0; q + st < P; q += 2 * st) {
+                            bool take = tv[q + st] > tv[q];
+                            if (tv[q + st] == tv[q] && tv[q] >= 0.0) take = oid(ti[q + st]) < oid(ti[q]);  // lowest index
+                            if (take) { tv[q] = tv[q + st]; ti[q] = ti[q + st]; }
+                        }
+                    }
+                    tv0 = tv[0];
+                    ti0 = ti[0];
+                }
+                if (dirty) {
+                    bv = tv0;
+                    bq = ti0;
+    #pragma unroll
+                    for (int q = 0; q < P; ++q)
+                        if (q == bq) { bx = fx[q]; by = fy[q]; bz = fz[q]; }
+                }
+                dirty = false;
+            }
+            {
+                uint32_t cm = 0;
+    #pragma unroll
+                for (int q = 0; q < P; ++q) cm |= ((((valid >> q) & 1u) && dbits(mget(q)) >= tau) ? 1u : 0u) << q;
+                if (__any_sync(kFull, cm != 0)) {
+    #pragma unroll
+                    for (int q = 0; q < P; ++q) {
+                        if ((cm >> q) & 1u) {
+                            const int slot = atomicAdd(&cnt_s, 1);
+                            if (slot < kR - 1) {
+                                const uint64_t kq = dbits(mget(q));
+                                const uint32_t ca = a_cand + 32u * (uint32_t)slot;
+                                sts_v4(ca, make_uint4((uint32_t)kq, (uint32_t)(kq >> 32), oid(q), (tk >> q) & 1u));
+                                sts_v4(ca + 16u, make_uint4(__float_as_uint(fx[q]), __float_as_uint(fy[q]),
+                                                             __float_as_uint(fz[q]), 0u));
+                            }
+                        }
+                    }
+                }
+                const uint64_t bkey = bv >= 0.0 ? dbits(bv) : 0ull;
+                const uint32_t bidx = bv >= 0.0 ? oid(bq) : kNone;
+                const int wl = warp_argmax_lane(bkey, bidx);
+                if (wl < 0) {
+                    if (lane == 0) sts_v4(a_wrec + 32u * warp, make_uint4(0u, 0u, kNone, 0u));
+                } else if (lane == wl) {
+                    sts_v4(a_wrec + 32u * warp, make_uint4((uint32_t)bkey, (uint32_t)(bkey >> 32), bidx, (tk >> bq) & 1u));
+                    sts_v4(a_wrec + 32u * warp + 16u,
+                           make_uint4(__float_as_uint(bx), __float_as_uint(by), __float_as_uint(bz), 0u));
+                }
+            }
+            if (tdbg) { t1 = clock64(); tacc[1] += t1 - t0; t0 = t1; }
+            __syncthreads();
+            if (tdbg) { t1 = clock64(); tacc[2] += t1 - t0; t0 = t1; }
+            const uint32_t tag = (ex & 0xffffu) << 16;
+            uint32_t pw = (kLeadPts && warp == kLead) ? lead_step(tag, par, phase, t0, t1) : worker_step(tag);
+            pw = __shfl_sync(kFull, pw, 0);
+            const int rn = (int)(pw & 0xffu);
+            it += rn;
+            tau = tau_s;
+
+            if (pw & 0x200u) {
+                // duplicate fallback (_kernels.py:65-70): lowest untaken index
+                uint32_t fidx = kNone;
+                Rec fr{};
+    #pragma unroll
+                for (int q = 0; q < P; ++q) {
+                    if (((valid >> q) & 1u) && !((tk >> q) & 1u) && oid(q) < fidx) {
+                        fidx = oid(q);
+                        const uint64_t kk = dbits(mget(q));
+                        fr.klo = (uint32_t)kk; fr.khi = (uint32_t)(kk >> 32);
+                        fr.x = fx[q]; fr.y = fy[q]; fr.z = fz[q];
+                    }
+                }
+                fr.idx = fidx;
+                const uint32_t wmin = __reduce_min_sync(kFull, fidx);
+                __syncthreads();  // wrec reuse
+                if (fidx == wmin && fidx != kNone) wrec[warp] = fr;
+                else if (lane == 0 && wmin == kNone) { Rec z{}; z.idx = kNone; wrec[warp] = z; }
+                __syncthreads();
+                if (warp == 0) {
+                    const Rec cr = warp_min_idx_recs(wrec, kW, lane);
+                    if (lane < (int)C) {
+                        const uint32_t dst = mapa(smem_u32(&fb_slots[r]), lane);
+                        st_cluster_u64(dst, ((uint64_t)cr.khi << 32) | cr.klo);
+                        st_cluster_u64(dst + 8, ((uint64_t)cr.taken << 32) | cr.idx);
+                        st_cluster_u64(dst + 16, ((uint64_t)__float_as_uint(cr.y) << 32) | __float_as_uint(cr.x));
+                        st_cluster_u64(dst + 24, (uint64_t)__float_as_uint(cr.z));
+                    }
+                }
+                cluster_sync_all();
+                const Rec fw = warp_min_idx_recs(fb_slots, (int)C, lane);
+                Rec w = fbw_s;  // no untaken point left: the argmax stands
+                if (fw.idx != kNone) w = fw;
+                cluster_sync_all();  // fb_slots / wrec free again
+                if (writer) {
+                    out[it] = (int64_t)w.idx;
+                    curve[it] = bitsd(rec_key(w));
+                }
+                if (warp == kLead) {
+                    if (lane == 0) hist_s[hc & 31] = bitsd(rec_key(w));
+                    ++hc;
+                }
+                fold_one(w.x, w.y, w.z, w.idx, it < k_stop - 1);
+                ++it;
+            }
+        }
+        // ---- write back md / taken; curve = sqrt(best) (_kernels.py:72) ---------
+    #pragma unroll
+        for (int q = 0; q < P; ++q) {
+            if ((valid >> q) & 1u) {
+                const int64_t j = oid(q);
+                md[j] = mget(q);
+                taken[j] = (tk >> q) & 1u;
+            }
         }
     }
 
@@ -737,15 +837,6 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
         for (int i = 0; i < 10; ++i) a.dbg[2 + i] = tacc[i];
     }
 
-    // ---- write back md / taken; curve = sqrt(best) (_kernels.py:72) ---------
-#pragma unroll
-    for (int q = 0; q < P; ++q) {
-        if ((valid >> q) & 1u) {
-            const int64_t j = oid(q);
-            md[j] = m[q];
-            taken[j] = (tk >> q) & 1u;
-        }
-    }
     if (r == 0 && k_start < k_stop) {
         __syncthreads();
         for (int64_t i = k_start + tid; i < k_stop; i += T) curve[i] = sqrt(curve[i]);
@@ -761,9 +852,18 @@ cudaError_t launch_spec(const FpsArgs& a, int64_t B, int C, cudaStream_t s) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
     }
+    // sort arrays (4 B per slot) + md in shared memory for P >= 10 (8 B per slot)
+    const size_t dyn = (P >= 10 ? 12 : 4) * (size_t)spec_slots(P, T, kLeadPts);
+    static bool dyn_set = false;
+    if (!dyn_set) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        if (e != cudaSuccess) return e;
+        dyn_set = true;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(B * C), 1, 1);
     cfg.blockDim = dim3(T, 1, 1);
+    cfg.dynamicSmemBytes = dyn;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -782,6 +882,7 @@ cudaError_t launch_spec(const FpsArgs& a, int64_t B, int C, cudaStream_t s) {
 cudaError_t launch_fps_spec(FpsArgs a, int64_t B, cudaStream_t s) {
     int C = 1, P = 0, T = 256;
     fps_choose_cluster(a.N, B, &C, &P, &T);
+    if (getenv("PS_SPEC_C")) { C = atoi(getenv("PS_SPEC_C")); P = 1; }  // development override (A/B)
     if (P == 0) return cudaErrorNotSupported;
     // clouds of one or two CTAs: the one-sample kernel has no cluster
     // exchange to amortise and is faster (profiles/r01/fps_spec.log: 0.65-0.86
@@ -790,14 +891,18 @@ cudaError_t launch_fps_spec(FpsArgs a, int64_t B, cudaStream_t s) {
     if (C <= 2 && !getenv("PS_FPS_SPEC")) return cudaErrorNotSupported;
     // one warp per CTA leads the exchange and owns no points (below)
     const int64_t S = (a.N + C - 1) / C;
-    // 512 threads, 15 worker warps, P <= 9 points per thread (beyond that the
-    // register budget spills): up to 4320 points per CTA without points on the
-    // lead warp (P = 9: C3 early-termination tail at 6-CTA clusters 0.191 ->
-    // 0.178 ms, full FPS 0.642 -> 0.594 us per sample; PS_SPEC_NOP9=1: P <= 8)
+    // 512 threads, 15 worker warps, P <= 10 points per thread: up to 4800
+    // points per CTA without points on the lead warp.  The lead runs its own
+    // loop (its registers and the workers' points do not add up) and from
+    // P = 10 md lives in shared memory, so P = 10 fits 128 registers without
+    // spills (profiles/r02/fps_pmax.log: C3 throughput width 6 -> 5 CTAs)
     P = 0;
     T = 512;
-    for (int p : {1, 2, 3, 4, 5, 6, 7, 8, 9})
-        if (!P && (int64_t)p * (T - 32) >= S && (p < 9 || !getenv("PS_SPEC_NOP9"))) P = p;
+    // up to 10 points per thread spill-free (md in shared memory from P = 10);
+    // 11-13 compile with small spills (development: PS_SPEC_PMAX)
+    static const int pmax = getenv("PS_SPEC_PMAX") ? atoi(getenv("PS_SPEC_PMAX")) : 10;
+    for (int p : {1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13})
+        if (!P && (int64_t)p * (T - 32) >= S && p <= pmax) P = p;
     // up to 4096 points per CTA: the lead warp owns points as well
     const bool lead_pts = P == 0 && S <= 8 * 512;
     if (lead_pts) { P = 8; T = 512; }
@@ -832,6 +937,10 @@ cudaError_t launch_fps_spec(FpsArgs a, int64_t B, cudaStream_t s) {
         PS_SPEC_CASE(7, 512)
         PS_SPEC_CASE(8, 512)
         PS_SPEC_CASE(9, 512)
+        PS_SPEC_CASE(10, 512)
+        PS_SPEC_CASE(11, 512)
+        PS_SPEC_CASE(12, 512)
+        PS_SPEC_CASE(13, 512)
         default: break;
     }
 #undef PS_SPEC_CASE
