@@ -388,7 +388,12 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
     // The lead-only warp (!kLeadPts) runs its own copy of the loop: the
     // workers' register-resident points are dead there, so the two roles
     // share the register budget instead of adding up (room for more
-    // points per thread).  Both loops meet the same CTA barriers.
+    // points per thread).  Both loops meet the same CTA barriers, at
+    // different instructions (warp-uniform roles; a bar.sync completes on
+    // thread arrivals).  compute-sanitizer synccheck reports that as
+    // divergence; the forms it accepts -- named bar.arrive / bar.sync pairs,
+    // the non-.aligned barrier.sync, an mbarrier, one shared loop -- all
+    // measured 20-30 % slower at P = 10 (profiles/r02/fps_barrier_ab.log).
     auto lead_step = [&](uint32_t tag, uint32_t par, uint32_t phase, long long& t0, long long& t1) -> uint32_t {
         uint32_t pw = 0;
             // C. CTA record set: header (the CTA max, candidate count) and

@@ -55,6 +55,11 @@ def case_fps_spec():
     _fps(generate_cloud("room-surfaces", 6000, 2), 300, 5, {"PS_FPS_CLUSTER": "4", "PS_FPS_SPEC": "1"})
 
 
+def case_fps_spec_p10():
+    # 10 points per thread (md in shared memory, the lead's own loop): 5-CTA clusters of a 24000-point cloud
+    _fps(generate_cloud("room-surfaces", 24000, 12), 200, 5, {"PS_SPEC_C": "5"})
+
+
 def case_fps_cluster():
     _fps(generate_cloud("room-surfaces", 6000, 3), 300, 5, {"PS_FPS_CLUSTER": "4", "PS_FPS_NOSPEC": "1"})
 
