@@ -1650,8 +1650,15 @@ cudaError_t launch_excl_build(const float4* xyz, int64_t B, int64_t N, const dou
                 // two rows per warp, 16 lanes each: the per-row bookkeeping (bucket
                 // scan, spill check, counts, padding) serves both rows at once (C3:
                 // 97 M vs 119 M instructions with one row per warp, PS_ELL_G=1)
+                // 6 CTAs per SM (a 6 x 32-candidate window, 85 registers):
+                // C3 stage 201 -> 192 us vs 5 CTAs with an 8 x 32 window
+                // (profiles/r02/excl_kernels_ab.log; PS_ELL_V=0: the latter)
+                static const int ell_v = getenv("PS_ELL_V") ? atoi(getenv("PS_ELL_V")) : 2;
                 if (getenv("PS_ELL_G") && atoi(getenv("PS_ELL_G")) == 1)
                     grid_ell_cell_kernel<kWc, 128, 8, kChunk, 7, 1><<<dim3((unsigned)gxc, (unsigned)B), kWc * 32, 0, s>>>(
+                        B, N, r2_levels, L, levels_ld, stride, g, w, csr);
+                else if (ell_v == 2)
+                    grid_ell_cell_kernel<kWc, 96, 6, kChunk, 6, 2><<<dim3((unsigned)gxc, (unsigned)B), kWc * 32, 0, s>>>(
                         B, N, r2_levels, L, levels_ld, stride, g, w, csr);
                 else
                     grid_ell_cell_kernel<kWc, 96, 8, kChunk, 5, 2><<<dim3((unsigned)gxc, (unsigned)B), kWc * 32, 0, s>>>(
