@@ -152,6 +152,34 @@ def test_fps_speculative_lead_owns_points(family, monkeypatch):
 
 
 @pytest.mark.timeout(300)
+@pytest.mark.parametrize("family", ["room-surfaces", "half-duplicates"])
+def test_fps_throughput_width_ten_points_per_thread(family):
+    """The throughput-hint width (several batches in flight): C3 clouds at
+    5-CTA clusters, 10 points per thread with md in shared memory and the
+    lead warp on its own loop -- full run, early stop and a resumed tail,
+    bit-exact against the oracle (duplicates exercise the fallback)."""
+    N = 24000
+    if family == "half-duplicates":
+        base = generate_cloud("uniform-box", N // 2, 13)
+        c = np.concatenate([base, base])[np.random.default_rng(5).permutation(N)].copy()
+    else:
+        c = generate_cloud(family, N, 13)
+    B = 2
+    cl = np.stack([c, generate_cloud("room-surfaces", N, 14)])
+    xyz4 = engine.as_xyz4(torch.from_numpy(cl).cuda())
+    with engine.inflight(8 * B):
+        for n, k_stop in ((1500, 1500), (1500, 600)):
+            idx, curve, md, taken = engine.fps(xyz4, n, seed_index=N // 7, k_stop=k_stop)
+            for b in range(B):
+                ri, rc, rmd, rtk, _ = O.fps(cl[b], n, N // 7, k_stop=k_stop)
+                msg = f"{family} cloud {b} k_stop={k_stop}"
+                np.testing.assert_array_equal(idx[b].cpu().numpy()[:k_stop], ri[:k_stop], err_msg=msg)
+                np.testing.assert_array_equal(curve[b].cpu().numpy()[:k_stop], rc[:k_stop], err_msg=msg)
+                np.testing.assert_array_equal(md[b].cpu().numpy(), rmd, err_msg=msg)
+                np.testing.assert_array_equal(taken[b].cpu().numpy(), rtk, err_msg=msg)
+
+
+@pytest.mark.timeout(300)
 @pytest.mark.parametrize("W", [1, 2, 4, 8])
 def test_fps_small_cloud_kernel(W, monkeypatch):
     """The small-cloud kernel (fps_small.cu: one CTA of W warps per cloud,
