@@ -66,6 +66,15 @@ constexpr uint64_t kTauOff = ~0ull;  // threshold disabled (above every md bit p
 // point slots of a CTA (sort arrays): P per worker thread, rounded to 8
 constexpr int spec_slots(int P, int T, bool lead_pts) { return ((P * (lead_pts ? T : T - 32)) + 7) / 8 * 8; }
 constexpr int64_t kSortMinIters = 64;  // runs shorter than this keep the index order
+// Workers refresh their warp record while waiting for the next pick (instead
+// of after the run's end, on the lead's critical path) from P = 10 points per
+// thread: C3 5-CTA clusters prefix 688 -> 672 us, full run 3608 -> 3461 us;
+// at P = 5 the extra issue next to the lead costs more (517 -> 522 us).
+// Either way the record is rewritten only when a fold touched the warp.
+#ifndef PS_EAGER_REC
+#define PS_EAGER_REC 1
+#endif
+constexpr bool kEagerRec = PS_EAGER_REC;
 constexpr float kInfF = __builtin_huge_valf();
 
 template <int P, int T, bool kLeadPts>
@@ -324,11 +333,20 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
 
     // mark sample sidx taken if it is mine; fold it into md unless it is the
     // last sample of this call (the reference folds that one at the next call)
+    // TIMING build: worker warp 0 of cloud 0 / CTA 0 -- cycles from seeing a
+    // run's end to its barrier arrival, picks still unfolded at that point,
+    // cycles of phase B, folds run / skipped by the whole-warp test
+    const bool wdbg = kTiming && a.dbg && b == 0 && r == 0 && warp == 0 && lane == 0;
+    long long w_tdone = 0, wacc[5] = {0, 0, 0, 0, 0};
+    bool stale = true;  // the warp's record may not reflect its points (a fold ran since it was written)
     auto fold_one = [&](float sx32, float sy32, float sz32, uint32_t sidx, bool do_fold) {
         const int64_t li = (int64_t)sidx - lo;
         if (li >= 0 && li < ncta) {
             const int sp = (int)lds_u16(a_pos + 2u * (uint32_t)li);
-            if (worker && sp / (32 * P) == warp && (sp & 31) == lane) tk |= 1u << ((sp % (32 * P)) >> 5);
+            if (worker && sp / (32 * P) == warp) {  // warp-uniform: the taken bit may be in the record
+                if ((sp & 31) == lane) tk |= 1u << ((sp % (32 * P)) >> 5);
+                stale = true;
+            }
         }
         if (!do_fold) return;
         // whole-warp skip: a rounded-down lower bound of the squared distance
@@ -339,7 +357,10 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
             const float ey = fmaxf(fmaxf(__fsub_rd(wb[1], sy32), __fsub_rd(sy32, wb[4])), 0.f);
             const float ez = fmaxf(fmaxf(__fsub_rd(wb[2], sz32), __fsub_rd(sz32, wb[5])), 0.f);
             const float dbox = __fadd_rd(__fadd_rd(__fmul_rd(ex, ex), __fmul_rd(ey, ey)), __fmul_rd(ez, ez));
+            if (kTiming && wdbg) ++wacc[4];
             if (dbox > wthr) return;
+            if (kTiming && wdbg) ++wacc[3];
+            stale = true;
         }
         uint32_t need = 0;
         constexpr int kD = P >= 10 ? 1 : P;  // P >= 10: recompute instead of keeping P distances live
@@ -626,6 +647,67 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
             }
         return pw;
     };
+    // the warp's record (thread maxima -> warp argmax -> wrec) and its skip
+    // bound: in phase B, or earlier while a worker waits for the next pick
+    // (only after this exchange's first pick: the lead has read wrec by then)
+    auto refresh_record = [&]() {
+        wthr = warp_thr_max();
+        if (__any_sync(kFull, dirty)) {
+            double tv0;
+            int ti0;
+            if constexpr (P >= 10) {
+                // many points per thread: a running maximum (three live
+                // registers instead of the tree's 3P)
+                tv0 = -1.0;
+                ti0 = 0;
+#pragma unroll
+                for (int q = 0; q < P; ++q) {
+                    const double v = ((valid >> q) & 1u) ? mget(q) : -1.0;
+                    bool take = v > tv0;
+                    if (v == tv0 && v >= 0.0) take = oid(q) < oid(ti0);  // lowest index
+                    if (take) { tv0 = v; ti0 = q; }
+                }
+            } else {
+                double tv[P];
+                int ti[P];
+#pragma unroll
+                for (int q = 0; q < P; ++q) {
+                    tv[q] = ((valid >> q) & 1u) ? mget(q) : -1.0;
+                    ti[q] = q;
+                }
+#pragma unroll
+                for (int st = 1; st < P; st <<= 1) {
+#pragma unroll
+                    for (int q = 0; q + st < P; q += 2 * st) {
+                        bool take = tv[q + st] > tv[q];
+                        if (tv[q + st] == tv[q] && tv[q] >= 0.0) take = oid(ti[q + st]) < oid(ti[q]);  // lowest index
+                        if (take) { tv[q] = tv[q + st]; ti[q] = ti[q + st]; }
+                    }
+                }
+                tv0 = tv[0];
+                ti0 = ti[0];
+            }
+            if (dirty) {
+                bv = tv0;
+                bq = ti0;
+#pragma unroll
+                for (int q = 0; q < P; ++q)
+                    if (q == bq) { bx = fx[q]; by = fy[q]; bz = fz[q]; }
+            }
+            dirty = false;
+        }
+        const uint64_t bkey = bv >= 0.0 ? dbits(bv) : 0ull;
+        const uint32_t bidx = bv >= 0.0 ? oid(bq) : kNone;
+        const int wl = warp_argmax_lane(bkey, bidx);
+        if (wl < 0) {
+            if (lane == 0) sts_v4(a_wrec + 32u * warp, make_uint4(0u, 0u, kNone, 0u));
+        } else if (lane == wl) {
+            sts_v4(a_wrec + 32u * warp, make_uint4((uint32_t)bkey, (uint32_t)(bkey >> 32), bidx, (tk >> bq) & 1u));
+            sts_v4(a_wrec + 32u * warp + 16u,
+                   make_uint4(__float_as_uint(bx), __float_as_uint(by), __float_as_uint(bz), 0u));
+        }
+        stale = false;
+    };
     auto worker_step = [&](uint32_t tag) -> uint32_t {
         uint32_t pw = 0;
             // fold each pick as soon as the lead warp publishes it
@@ -633,9 +715,18 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
             while (true) {
                 pw = ld_acquire_cta(&pub_s);
                 const int n = (pw & 0xffff0000u) == tag ? (int)(pw & 0xffu) : 0;
+                if (kTiming && wdbg && (pw & 0xffff0000u) == tag && (pw & 0x100u) && w_tdone == 0) {
+                    w_tdone = clock64();
+                    wacc[1] += n - k;
+                }
                 if (n <= k && !((pw & 0xffff0000u) == tag && (pw & 0x100u))) {
-                    // nothing new: back off so the lead warp's shared-memory
-                    // traffic is not queued behind the polls
+                    // nothing new: refresh the warp's record if a fold changed
+                    // it (off the critical path), else back off so the lead
+                    // warp's shared-memory traffic is not queued behind the polls
+                    if (kEagerRec && P >= 10 && stale && k > 0) {
+                        refresh_record();
+                        continue;
+                    }
                     __nanosleep(poll_ns);
                     continue;
                 }
@@ -692,53 +783,11 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
             long long t0 = 0, t1 = 0;
             if (tdbg) t0 = clock64();
 
+            long long wb0 = 0;
+            if (kTiming && wdbg) wb0 = clock64();
             // B. thread max (cached), threshold candidates, warp argmax; the
             // warp's skip bound for the next exchange's folds (thr only falls)
-            wthr = warp_thr_max();
-            if (__any_sync(kFull, dirty)) {
-                double tv0;
-                int ti0;
-                if constexpr (P >= 10) {
-                    // many points per thread: a running maximum (three live
-                    // registers instead of the tree's 3P)
-                    tv0 = -1.0;
-                    ti0 = 0;
-    #pragma unroll
-                    for (int q = 0; q < P; ++q) {
-                        const double v = ((valid >> q) & 1u) ? mget(q) : -1.0;
-                        bool take = v > tv0;
-                        if (v == tv0 && v >= 0.0) take = oid(q) < oid(ti0);  // lowest index
-                        if (take) { tv0 = v; ti0 = q; }
-                    }
-                } else {
-                    double tv[P];
-                    int ti[P];
-    #pragma unroll
-                    for (int q = 0; q < P; ++q) {
-                        tv[q] = ((valid >> q) & 1u) ? mget(q) : -1.0;
-                        ti[q] = q;
-                    }
-    #pragma unroll
-                    for (int st = 1; st < P; st <<= 1) {
-    #pragma unroll
-                        for (int q = 0; q + st < P; q += 2 * st) {
-                            bool take = tv[q + st] > tv[q];
-                            if (tv[q + st] == tv[q] && tv[q] >= 0.0) take = oid(ti[q + st]) < oid(ti[q]);  // lowest index
-                            if (take) { tv[q] = tv[q + st]; ti[q] = ti[q + st]; }
-                        }
-                    }
-                    tv0 = tv[0];
-                    ti0 = ti[0];
-                }
-                if (dirty) {
-                    bv = tv0;
-                    bq = ti0;
-    #pragma unroll
-                    for (int q = 0; q < P; ++q)
-                        if (q == bq) { bx = fx[q]; by = fy[q]; bz = fz[q]; }
-                }
-                dirty = false;
-            }
+            if (stale) refresh_record();  // else the record written while polling stands
             {
                 uint32_t cm = 0;
     #pragma unroll
@@ -758,18 +807,14 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
                         }
                     }
                 }
-                const uint64_t bkey = bv >= 0.0 ? dbits(bv) : 0ull;
-                const uint32_t bidx = bv >= 0.0 ? oid(bq) : kNone;
-                const int wl = warp_argmax_lane(bkey, bidx);
-                if (wl < 0) {
-                    if (lane == 0) sts_v4(a_wrec + 32u * warp, make_uint4(0u, 0u, kNone, 0u));
-                } else if (lane == wl) {
-                    sts_v4(a_wrec + 32u * warp, make_uint4((uint32_t)bkey, (uint32_t)(bkey >> 32), bidx, (tk >> bq) & 1u));
-                    sts_v4(a_wrec + 32u * warp + 16u,
-                           make_uint4(__float_as_uint(bx), __float_as_uint(by), __float_as_uint(bz), 0u));
-                }
             }
             if (tdbg) { t1 = clock64(); tacc[1] += t1 - t0; t0 = t1; }
+            if (kTiming && wdbg) {
+                const long long wn = clock64();
+                wacc[2] += wn - wb0;
+                if (w_tdone) wacc[0] += wn - w_tdone;
+                w_tdone = 0;
+            }
             __syncthreads();
             if (tdbg) { t1 = clock64(); tacc[2] += t1 - t0; t0 = t1; }
             const uint32_t tag = (ex & 0xffffu) << 16;
@@ -822,9 +867,12 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
                     ++hc;
                 }
                 fold_one(w.x, w.y, w.z, w.idx, it < k_stop - 1);
+                stale = true;  // wrec now holds the fallback records
                 ++it;
             }
         }
+        if (kTiming && wdbg)
+            for (int i = 0; i < 5; ++i) a.dbg[12 + i] = wacc[i];
         // ---- write back md / taken; curve = sqrt(best) (_kernels.py:72) ---------
     #pragma unroll
         for (int q = 0; q < P; ++q) {
@@ -921,8 +969,8 @@ cudaError_t launch_fps_spec(FpsArgs a, int64_t B, cudaStream_t s) {
     if (timing) {
         // development aid (make TIMING=1): exchanges, samples taken by
         // speculation and per-phase SM cycles of cloud 0 / CTA 0 / lead lane 0
-        if (!dbg) cudaMalloc(&dbg, sizeof(long long) * 12);
-        cudaMemsetAsync(dbg, 0, sizeof(long long) * 12, s);
+        if (!dbg) cudaMalloc(&dbg, sizeof(long long) * 17);
+        cudaMemsetAsync(dbg, 0, sizeof(long long) * 17, s);
         a.dbg = dbg;
     }
     if (getenv("PS_FPS_VERBOSE"))
@@ -950,7 +998,7 @@ cudaError_t launch_fps_spec(FpsArgs a, int64_t B, cudaStream_t s) {
     }
 #undef PS_SPEC_CASE
     if (timing && e == cudaSuccess) {
-        long long h[12];
+        long long h[17];
         cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, s);
         cudaStreamSynchronize(s);
         const double nx = h[0] > 0 ? (double)h[0] : 1.0;
@@ -960,6 +1008,10 @@ cudaError_t launch_fps_spec(FpsArgs a, int64_t B, cudaStream_t s) {
                 C, P, T, (long long)a.N, (long long)(a.k_stop - a.k_start), h[0], (double)h[1] / nx,
                 h[2] / nx, h[3] / nx, h[4] / nx, h[5] / nx, h[6] / nx, h[7] / nx, h[8] / nx, h[9] / nx, h[10] / nx,
                 h[11] / nx);
+        fprintf(stderr, "[fps-spec timing] worker warp 0 per exchange: end-of-run -> barrier %.0f cycles, unfolded picks "
+                "at the end %.2f, phase B %.0f cycles; folds run %.1f of %.1f (whole-warp skip %.0f %%)\n",
+                h[12] / nx, h[13] / nx, h[14] / nx, h[15] / nx, h[16] / nx,
+                h[16] > 0 ? 100.0 * (1.0 - (double)h[15] / (double)h[16]) : 0.0);
     }
     return e;
 }
