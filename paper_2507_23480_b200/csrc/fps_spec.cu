@@ -710,33 +710,33 @@ __global__ void __launch_bounds__(T, 1) fps_spec_kernel(FpsArgs a) {
     };
     auto worker_step = [&](uint32_t tag) -> uint32_t {
         uint32_t pw = 0;
-            // fold each pick as soon as the lead warp publishes it
-            int k = 0;
-            while (true) {
-                pw = ld_acquire_cta(&pub_s);
-                const int n = (pw & 0xffff0000u) == tag ? (int)(pw & 0xffu) : 0;
-                if (kTiming && wdbg && (pw & 0xffff0000u) == tag && (pw & 0x100u) && w_tdone == 0) {
-                    w_tdone = clock64();
-                    wacc[1] += n - k;
-                }
-                if (n <= k && !((pw & 0xffff0000u) == tag && (pw & 0x100u))) {
-                    // nothing new: refresh the warp's record if a fold changed
-                    // it (off the critical path), else back off so the lead
-                    // warp's shared-memory traffic is not queued behind the polls
-                    if (kEagerRec && P >= 10 && stale && k > 0) {
-                        refresh_record();
-                        continue;
-                    }
-                    __nanosleep(poll_ns);
+        // fold each pick as soon as the lead warp publishes it
+        int k = 0;
+        while (true) {
+            pw = ld_acquire_cta(&pub_s);
+            const int n = (pw & 0xffff0000u) == tag ? (int)(pw & 0xffu) : 0;
+            if (kTiming && wdbg && (pw & 0xffff0000u) == tag && (pw & 0x100u) && w_tdone == 0) {
+                w_tdone = clock64();
+                wacc[1] += n - k;
+            }
+            if (n <= k && !((pw & 0xffff0000u) == tag && (pw & 0x100u))) {
+                // nothing new: refresh the warp's record if a fold changed
+                // it (off the critical path), else back off so the lead
+                // warp's shared-memory traffic is not queued behind the polls
+                if (kEagerRec && P >= 10 && stale && k > 0) {
+                    refresh_record();
                     continue;
                 }
-                for (; k < n; ++k) {
-                    const uint4 rv = lds_v4(a_run + 16u * k);
-                    fold_one(__uint_as_float(rv.x), __uint_as_float(rv.y), __uint_as_float(rv.z), rv.w,
-                             it + k < k_stop - 1);
-                }
-                if ((pw & 0xffff0000u) == tag && (pw & 0x100u)) break;
+                __nanosleep(poll_ns);
+                continue;
             }
+            for (; k < n; ++k) {
+                const uint4 rv = lds_v4(a_run + 16u * k);
+                fold_one(__uint_as_float(rv.x), __uint_as_float(rv.y), __uint_as_float(rv.z), rv.w,
+                         it + k < k_stop - 1);
+            }
+            if ((pw & 0xffff0000u) == tag && (pw & 0x100u)) break;
+        }
         return pw;
     };
     if (!kLeadPts && warp == kLead) {
